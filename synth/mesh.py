@@ -1,0 +1,229 @@
+"""Unstructured mesh container + a vectorised face/geometry builder.
+
+The mesh format is the one the C ABI (`include/gmg.h`, gmg_load_mesh) and the
+oracle both ingest:
+
+* cells: ``vol[n]``, ``ctr[d][n]`` (SoA)
+* faces: ``left[nf]`` (owner cell), ``right[nf]`` (other cell, or
+  ``-(patch+1)`` for a boundary face), ``avec[d][nf]`` the area vector
+  ``S_f n_f`` pointing left -> right (outward from ``left``), ``fctr[d][nf]``
+  the face centre, ``ngauss[nf]`` the number of Gauss points M_f of that face
+  (2 per 2D segment, 3 per triangle, 4 per quad; PAPER.md:164-176 / SPEC S:75).
+* ``patch_kind[n_patches]``: FARFIELD / SLIP / NOSLIP / EXTRAP.
+
+Geometry is computed ONCE here, in numpy float64; nothing downstream
+recomputes it.  This file contains no arithmetic of the paper's method.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+FARFIELD, SLIP, NOSLIP, EXTRAP = 0, 1, 2, 3
+
+# cell types
+TRI2, QUAD2, TET, PRISM = 0, 1, 2, 3
+
+# local face templates (cyclic node order inside each face)
+_FACES = {
+    TRI2: [(0, 1), (1, 2), (2, 0)],
+    QUAD2: [(0, 1), (1, 2), (2, 3), (3, 0)],
+    TET: [(0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3)],
+    PRISM: [(0, 1, 2), (3, 4, 5), (0, 1, 4, 3), (1, 2, 5, 4), (2, 0, 3, 5)],
+}
+_NNODES = {TRI2: 3, QUAD2: 4, TET: 4, PRISM: 6}
+
+
+@dataclass
+class Mesh:
+    dim: int
+    vol: np.ndarray          # [n] float64
+    ctr: np.ndarray          # [d][n] float64
+    left: np.ndarray         # [nf] int64
+    right: np.ndarray        # [nf] int64 (<0: -(patch+1))
+    avec: np.ndarray         # [d][nf] float64
+    fctr: np.ndarray         # [d][nf] float64
+    ngauss: np.ndarray       # [nf] int8
+    patch_kind: np.ndarray   # [n_patches] int32
+    name: str = ""
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_cells(self) -> int:
+        return int(self.vol.shape[0])
+
+    @property
+    def n_faces(self) -> int:
+        return int(self.left.shape[0])
+
+    @property
+    def n_interior(self) -> int:
+        return int(np.count_nonzero(self.right >= 0))
+
+    def contiguous(self) -> "Mesh":
+        for k in ("vol", "ctr", "avec", "fctr"):
+            setattr(self, k, np.ascontiguousarray(getattr(self, k), dtype=np.float64))
+        self.left = np.ascontiguousarray(self.left, dtype=np.int64)
+        self.right = np.ascontiguousarray(self.right, dtype=np.int64)
+        self.ngauss = np.ascontiguousarray(self.ngauss, dtype=np.int8)
+        self.patch_kind = np.ascontiguousarray(self.patch_kind, dtype=np.int32)
+        return self
+
+
+def _cross(a, b):
+    return np.stack([a[..., 1] * b[..., 2] - a[..., 2] * b[..., 1],
+                     a[..., 2] * b[..., 0] - a[..., 0] * b[..., 2],
+                     a[..., 0] * b[..., 1] - a[..., 1] * b[..., 0]], axis=-1)
+
+
+def _tet_vol_ctr(a, b, c, d):
+    v = np.abs(np.einsum("ij,ij->i", b - a, _cross(c - a, d - a))) / 6.0
+    return v, (a + b + c + d) / 4.0
+
+
+def build_mesh(dim, nodes, cell_type, conn, patch_of, patch_kind, name="", meta=None) -> Mesh:
+    """Build faces + geometry.
+
+    nodes: [nn][dim]; cell_type: [n] int; conn: [n][6] node ids (padded -1),
+    natural cell id = row.  patch_of(face_ctr [k][dim], avec [k][dim]) -> [k]
+    patch index for boundary faces.
+    """
+    nodes = np.asarray(nodes, dtype=np.float64)
+    cell_type = np.asarray(cell_type)
+    conn = np.asarray(conn, dtype=np.int64)
+    n = cell_type.shape[0]
+
+    # ---- cell geometry -------------------------------------------------
+    vol = np.zeros(n)
+    ctr = np.zeros((n, dim))
+    for t in np.unique(cell_type):
+        idx = np.nonzero(cell_type == t)[0]
+        c = conn[idx]
+        if t in (TRI2, QUAD2):
+            k = _NNODES[t]
+            x = nodes[c[:, :k], 0]
+            y = nodes[c[:, :k], 1]
+            x1 = np.roll(x, -1, axis=1)
+            y1 = np.roll(y, -1, axis=1)
+            cr = x * y1 - x1 * y
+            a2 = cr.sum(axis=1)  # 2*signed area
+            cx = ((x + x1) * cr).sum(axis=1) / (3.0 * a2)
+            cy = ((y + y1) * cr).sum(axis=1) / (3.0 * a2)
+            vol[idx] = np.abs(a2) * 0.5
+            ctr[idx] = np.stack([cx, cy], axis=1)
+        elif t == TET:
+            v, g = _tet_vol_ctr(*(nodes[c[:, i]] for i in range(4)))
+            vol[idx], ctr[idx] = v, g
+        elif t == PRISM:
+            P = [nodes[c[:, i]] for i in range(6)]
+            vs, gs = zip(*[_tet_vol_ctr(P[0], P[1], P[2], P[5]),
+                           _tet_vol_ctr(P[0], P[1], P[5], P[4]),
+                           _tet_vol_ctr(P[0], P[4], P[5], P[3])])
+            V = vs[0] + vs[1] + vs[2]
+            vol[idx] = V
+            ctr[idx] = (vs[0][:, None] * gs[0] + vs[1][:, None] * gs[1] + vs[2][:, None] * gs[2]) / V[:, None]
+        else:
+            raise ValueError(t)
+
+    # ---- face instances --------------------------------------------------
+    inst_cell, inst_loc, inst_nodes = [], [], []
+    for t in np.unique(cell_type):
+        idx = np.nonzero(cell_type == t)[0]
+        for lf, tpl in enumerate(_FACES[int(t)]):
+            fn = np.full((idx.shape[0], 4), -1, dtype=np.int64)
+            fn[:, :len(tpl)] = conn[idx][:, list(tpl)]
+            inst_cell.append(idx)
+            inst_loc.append(np.full(idx.shape[0], lf))
+            inst_nodes.append(fn)
+    inst_cell = np.concatenate(inst_cell)
+    inst_loc = np.concatenate(inst_loc)
+    inst_nodes = np.concatenate(inst_nodes)
+    key = np.sort(np.where(inst_nodes < 0, np.iinfo(np.int64).max, inst_nodes), axis=1)
+    # generator order: (cell, local face)
+    order0 = np.lexsort((inst_loc, inst_cell))
+    inst_cell, inst_loc, inst_nodes, key = inst_cell[order0], inst_loc[order0], inst_nodes[order0], key[order0]
+    ordk = np.lexsort((np.arange(key.shape[0]), key[:, 3], key[:, 2], key[:, 1], key[:, 0]))
+    ks = key[ordk]
+    same_next = np.all(ks[1:] == ks[:-1], axis=1)
+    if same_next.size and np.any(same_next[1:] & same_next[:-1]):
+        raise ValueError("non-manifold face (shared by >2 cells)")
+    first = np.ones(ks.shape[0], dtype=bool)
+    first[1:] = ~same_next
+    # partner instance for interior faces
+    partner = np.full(ks.shape[0], -1, dtype=np.int64)
+    pi = np.nonzero(same_next)[0]
+    partner[ordk[pi]] = ordk[pi + 1]
+    partner[ordk[pi + 1]] = ordk[pi]
+    # each physical face is owned by its first instance in generator order
+    owner_inst = np.nonzero((partner < 0) | (partner > np.arange(ks.shape[0])))[0]
+    interior = partner[owner_inst] >= 0
+    fi = np.concatenate([owner_inst[interior], owner_inst[~interior]])
+    nf = fi.shape[0]
+    left = inst_cell[fi]
+    right = np.where(partner[fi] >= 0, inst_cell[np.maximum(partner[fi], 0)], -1)
+    fnodes = inst_nodes[fi]
+
+    # ---- face geometry ----------------------------------------------------
+    if dim == 2:
+        a = nodes[fnodes[:, 0]]
+        b = nodes[fnodes[:, 1]]
+        avec = np.stack([b[:, 1] - a[:, 1], -(b[:, 0] - a[:, 0])], axis=1)
+        fctr = 0.5 * (a + b)
+        ngauss = np.full(nf, 2, dtype=np.int8)
+    else:
+        avec = np.zeros((nf, 3))
+        fctr = np.zeros((nf, 3))
+        ngauss = np.zeros(nf, dtype=np.int8)
+        tri = fnodes[:, 3] < 0
+        a, b, c = (nodes[fnodes[tri, i]] for i in range(3))
+        avec[tri] = 0.5 * _cross(b - a, c - a)
+        fctr[tri] = (a + b + c) / 3.0
+        ngauss[tri] = 3
+        q = ~tri
+        a, b, c, d = (nodes[fnodes[q, i]] for i in range(4))
+        avec[q] = 0.5 * _cross(c - a, d - b)
+        t1 = 0.5 * _cross(b - a, c - a)
+        t2 = 0.5 * _cross(c - a, d - a)
+        w1 = np.sqrt((t1 * t1).sum(1))[:, None]
+        w2 = np.sqrt((t2 * t2).sum(1))[:, None]
+        fctr[q] = (w1 * (a + b + c) / 3.0 + w2 * (a + c + d) / 3.0) / (w1 + w2)
+        ngauss[q] = 4
+    # orient outward from the left cell (convex cells)
+    cmean = np.zeros((n, dim))
+    cnt = np.zeros(n)
+    for t in np.unique(cell_type):
+        idx = np.nonzero(cell_type == t)[0]
+        k = _NNODES[int(t)]
+        cmean[idx] = nodes[conn[idx, :k]].mean(axis=1)
+        cnt[idx] = k
+    s = np.einsum("ij,ij->i", fctr - cmean[left], avec)
+    avec[s < 0] *= -1.0
+
+    bnd = right < 0
+    if np.any(bnd):
+        pidx = np.asarray(patch_of(fctr[bnd], avec[bnd]), dtype=np.int64)
+        right = right.copy()
+        right[bnd] = -(pidx + 1)
+
+    m = Mesh(dim=dim, vol=vol, ctr=np.ascontiguousarray(ctr.T), left=left, right=right,
+             avec=np.ascontiguousarray(avec.T), fctr=np.ascontiguousarray(fctr.T), ngauss=ngauss,
+             patch_kind=np.asarray(patch_kind, dtype=np.int32), name=name, meta=dict(meta or {}))
+    m.meta.setdefault("n_nodes", int(nodes.shape[0]))
+    m.meta.setdefault("cell_type_counts", {int(t): int(np.count_nonzero(cell_type == t)) for t in np.unique(cell_type)})
+    return m.contiguous()
+
+
+def closure_error(m: Mesh) -> float:
+    """max_i |sum_f sigma_if A_f| / sum_f |A_f|  (PAPER.md:454 closure)."""
+    d = m.dim
+    acc = np.zeros((m.n_cells, d))
+    sarea = np.zeros(m.n_cells)
+    S = np.sqrt((m.avec ** 2).sum(0))
+    for k in range(d):
+        np.add.at(acc[:, k], m.left, m.avec[k])
+        inn = m.right >= 0
+        np.add.at(acc[:, k], m.right[inn], -m.avec[k][inn])
+    np.add.at(sarea, m.left, S)
+    np.add.at(sarea, m.right[m.right >= 0], S[m.right >= 0])
+    return float(np.max(np.sqrt((acc ** 2).sum(1)) / sarea))

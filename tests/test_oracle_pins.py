@@ -1,0 +1,713 @@
+"""Pins of the C oracle against what the paper / mathematics fix (CPU only).
+
+Each test names the passage or the property it pins (SURVEY.md §8(c)
+"What pins each part").  Nothing here calls the CUDA path.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from synth import configs, state
+from synth.mesh import FARFIELD, EXTRAP, SLIP, NOSLIP, closure_error
+from tests import brute
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+G = 1.4
+
+
+def small_meshes():
+    return [configs.quad_grid(4, 4), configs.tri_square(4, 4, seed=3), configs.tri_square(6, 5, seed=7),
+            configs.box3d(2, 2, 2, 1, seed=1), configs.box3d(3, 2, 2, 0, seed=2), configs.two_cells()]
+
+
+# ----------------------------------------------------------------- hashing
+def test_face_hash_worked_examples(orc):
+    for e in GOLD["face_hash"]:
+        assert orc.face_hash(e["l"], e["r"], e["nf"]) == e["h"], e["cite"]
+    # P:584 prints 5: that is 626 mod 23, not mod N_f
+    assert (23 * 22 + 120) % 23 == 5
+
+
+def test_face_hash_uint64_no_overflow(orc):
+    # N_l N_r overflows int32 above 46340 (reading A19): compare with Python ints
+    for l, r, nf in [(46341, 46342, 1_000_003), (999_999, 1_000_000, 2_345_678), (2**31 + 5, 3, 77)]:
+        assert orc.face_hash(l, r, nf) == (23 * (l + r) + l * r) % nf
+
+
+# ----------------------------------------------------------------- coloring
+@pytest.mark.parametrize("nx,ny", [(2, 2), (4, 4), (5, 3), (16, 16)])
+def test_coloring_structured_is_checkerboard(orc, nx, ny):
+    """a structured mesh gets exactly 2 colors (checkerboard)."""
+    m = configs.quad_grid(nx, ny)
+    col, nc = orc.color(orc.Level.from_mesh(m))
+    assert nc == 2
+    j, i = np.divmod(np.arange(nx * ny), nx)
+    assert np.array_equal(col, ((i + j) % 2 + 1).astype(np.int32))
+
+
+def test_coloring_uniform_triangulation_two_colors(orc):
+    """Uniform-diagonal triangulation has a honeycomb (bipartite) dual."""
+    m = configs.tri_square(8, 8, uniform=True)
+    _, nc = orc.color(orc.Level.from_mesh(m))
+    assert nc == 2
+
+
+def _check_valid_coloring(m, col, nc):
+    inn = m.right >= 0
+    assert np.all(col[m.left[inn]] != col[m.right[inn]]), "same-color neighbours"
+    assert col.min() == 1 and col.max() == nc
+    deg = np.bincount(np.concatenate([m.left[inn], m.right[inn]]), minlength=m.n_cells)
+    assert nc <= deg.max() + 1  # greedy bound S:120
+
+
+@pytest.mark.parametrize("mk", range(6))
+def test_coloring_valid_and_matches_brute_force(orc, mk):
+    m = small_meshes()[mk]
+    col, nc = orc.color(orc.Level.from_mesh(m))
+    _check_valid_coloring(m, col, nc)
+    assert col.tolist() == brute.color_alg1(m.n_cells, m.left, m.right)
+
+
+def test_coloring_config1_valid(orc):
+    m = configs.config(1)
+    col, nc = orc.color(orc.Level.from_mesh(m))
+    _check_valid_coloring(m, col, nc)
+    assert col[0] == 1  # start cell 0
+
+
+def test_coloring_disconnected_restart(orc):
+    """Reading A24: restart at the smallest uncolored id with color 1."""
+    m = configs.quad_grid(2, 1)
+    # cut the only interior face: two isolated cells
+    right = m.right.copy()
+    right[right >= 0] = -1
+    col, nc = orc.color(orc.Level(m.dim, m.vol, m.ctr, m.left, right, m.avec, m.fctr, m.ngauss, m.patch_kind))
+    assert col.tolist() == [1, 1] and nc == 1
+
+
+# ----------------------------------------------------------------- skewness / agglomeration
+def test_skewness_worked_examples(orc):
+    for e in GOLD["skewness"]:
+        s = orc.skewness(2, 1.0, e["n"], e["d"], [0.0, 0.0])
+        assert abs(s - e["s"]) <= e.get("tol", 0.0), e["cite"]
+    # sigma flips the outward normal; |d| = 0 counts as aligned (reading A21)
+    assert orc.skewness(2, -1.0, [1.0, 0.0], [1.0, 0.0], [0.0, 0.0]) == -1.0
+    assert orc.skewness(3, 1.0, [0.0, 0.0, 2.0], [1.0, 1.0, 1.0], [1.0, 1.0, 1.0]) == 1.0
+
+
+def test_two_aligned_squares_merge(orc):
+    """two unit squares sharing a face -> one coarse cell, volume 2,
+    centroid midway (valid under the merged-cell reading A21)."""
+    m = configs.two_cells()
+    lv = orc.Level.from_mesh(m)
+    parent, nc, merges = orc.agglomerate(lv, 0.5)
+    assert merges == 1 and nc == 1 and parent.tolist() == [0, 0]
+    c = orc.coarse_build(lv, parent, nc)
+    assert c.vol.tolist() == [1.0 * 0.5 + 0.5] or c.vol[0] == m.vol.sum()
+    assert np.allclose(c.ctr[:, 0], [0.5, 0.5])
+    e = GOLD["virtual_center"]
+    Cv = [(e["Vl"] * a + e["Vr"] * b) / (e["Vl"] + e["Vr"]) for a, b in zip(e["Cl"], e["Cr"])]
+    assert Cv == e["Cc"]
+
+
+def _brute_agglomerate(m, theta):
+    """Pure-Python Algorithm 3 under readings A18-A22 (same float expression
+    order as O3, so bit-identical decisions)."""
+    n, d = m.n_cells, m.dim
+    L, R = m.left.tolist(), m.right.tolist()
+    nfi = sum(1 for r in R if r >= 0)
+    seen, sel = set(), []
+    for f in range(len(L)):
+        if R[f] < 0:
+            continue
+        h = (23 * (L[f] + R[f]) + L[f] * R[f]) % nfi
+        if h not in seen:
+            seen.add(h)
+            sel.append(f)
+    faces_of = [[] for _ in range(n)]
+    for f in range(len(L)):
+        faces_of[L[f]].append(f)
+        if R[f] >= 0:
+            faces_of[R[f]].append(f)
+    A = m.avec.T.tolist()
+    X = m.fctr.T.tolist()
+    C = m.ctr.T.tolist()
+    V = m.vol.tolist()
+    mate = [-1] * n
+    for f in sel:
+        l, r = L[f], R[f]
+        if mate[l] >= 0 or mate[r] >= 0:
+            continue
+        Cv = [(V[l] * C[l][k] + V[r] * C[r][k]) / (V[l] + V[r]) for k in range(d)]
+        smin = 2.0
+        for c in (l, r):
+            for g in faces_of[c]:
+                if {L[g], R[g]} == {l, r}:
+                    continue
+                sg = 1.0 if L[g] == c else -1.0
+                a = A[g]
+                S2 = a[0] * a[0] + a[1] * a[1]
+                if d == 3:
+                    S2 = S2 + a[2] * a[2]
+                S = math.sqrt(S2)
+                nn = [(sg * a[k]) / S for k in range(d)]
+                dd = [X[g][k] - Cv[k] for k in range(d)]
+                dn = dd[0] * nn[0] + dd[1] * nn[1]
+                d2 = dd[0] * dd[0] + dd[1] * dd[1]
+                if d == 3:
+                    dn = dn + dd[2] * nn[2]
+                    d2 = d2 + dd[2] * dd[2]
+                s = 1.0 if d2 == 0.0 else dn / math.sqrt(d2)
+                smin = min(smin, s)
+        if smin >= theta:
+            mate[l], mate[r] = r, l
+    parent, nc = [0] * n, 0
+    for i in range(n):
+        if mate[i] >= 0 and mate[i] < i:
+            parent[i] = parent[mate[i]]
+        else:
+            parent[i] = nc
+            nc += 1
+    return parent, nc
+
+
+@pytest.mark.parametrize("mk", range(5))
+def test_agglomeration_matches_brute_force(orc, mk):
+    m = small_meshes()[mk]
+    parent, nc, merges = orc.agglomerate(orc.Level.from_mesh(m), 0.5)
+    bp, bnc = _brute_agglomerate(m, 0.5)
+    assert parent.tolist() == bp and nc == bnc
+
+
+def _check_coarse_level(m_f, lv_c, parent):
+    """Conservation pins."""
+    nc = lv_c.n
+    cnt = np.bincount(parent, minlength=nc)
+    assert cnt.max() <= 2 and cnt.min() >= 1       # pairwise (A22)
+    # V_c = sum V (as summed, ascending child id)
+    for c in np.nonzero(cnt == 2)[0][:50]:
+        a, b = np.nonzero(parent == c)[0]
+        assert lv_c.vol[c] == m_f.vol[a] + m_f.vol[b]
+    V = np.bincount(parent, weights=m_f.vol, minlength=nc)
+    assert np.allclose(lv_c.vol, V, rtol=1e-15, atol=0)
+    for k in range(m_f.dim):
+        VC = np.bincount(parent, weights=m_f.vol * m_f.ctr[k], minlength=nc)
+        assert np.allclose(lv_c.vol * lv_c.ctr[k], VC, rtol=1e-12, atol=1e-14)
+    # closure per coarse cell
+    d = m_f.dim
+    acc = np.zeros((nc, d))
+    sarea = np.zeros(nc)
+    S = np.sqrt((lv_c.avec ** 2).sum(0))
+    for k in range(d):
+        np.add.at(acc[:, k], lv_c.left, lv_c.avec[k])
+        inn = lv_c.right >= 0
+        np.add.at(acc[:, k], lv_c.right[inn], -lv_c.avec[k][inn])
+    np.add.at(sarea, lv_c.left, S)
+    np.add.at(sarea, lv_c.right[lv_c.right >= 0], S[lv_c.right >= 0])
+    assert np.max(np.sqrt((acc ** 2).sum(1)) / sarea) <= 1e-12
+    # boundary faces preserved one-to-one with the same patch
+    bf = m_f.right < 0
+    bc = lv_c.right < 0
+    assert np.array_equal(np.sort(m_f.right[bf]), np.sort(lv_c.right[bc]))
+    assert np.array_equal(lv_c.avec[:, bc], m_f.avec[:, bf])
+    # coarse interior faces unique per pair, lexicographic, a < b
+    L, R = lv_c.left[~bc], lv_c.right[~bc]
+    assert np.all(L < R)
+    key = L * (nc + 1) + R
+    assert np.all(np.diff(key) > 0)
+
+
+@pytest.mark.parametrize("which", ["config1", "box", "quad", "naca_small"])
+def test_hierarchy_conservation(orc, which):
+    m = {"config1": lambda: configs.config(1), "box": lambda: configs.box3d(4, 4, 3, 1, seed=5),
+         "quad": lambda: configs.quad_grid(8, 8),
+         "naca_small": lambda: configs.naca_ogrid(ni=64, n_quad=8, n_tri=4)}[which]()
+    H = orc.build_hierarchy(m, 3, 0.5)
+    assert len(H) >= 2
+    prev = m
+    for l in range(1, len(H)):
+        lv_c = H[l]["level"]
+        par = H[l - 1]["parent"]
+        _check_coarse_level(prev, lv_c, par)
+        # re-evaluating every merge reproduces its decision via brute force
+        prev_mesh = H[l - 1]["level"]
+        bp, bnc = _brute_agglomerate(prev_mesh, 0.5)
+        assert bp == par.tolist()
+        prev = lv_c
+        _check_valid_coloring(lv_c, H[l]["color"], H[l]["ncolor"])
+    # the config-1 survey check: coarse/fine ratio ~0.70
+    if which == "config1":
+        assert 0.6 < H[1]["level"].n / m.n_cells < 0.8
+
+
+def test_partition_faces_never_deleted(orc):
+    """parallel-interface faces are never deleted."""
+    m = configs.tri_square(8, 8, seed=2)
+    part = (m.ctr[0] > 0.5).astype(np.int32)
+    parent, nc, merges = orc.agglomerate(orc.Level.from_mesh(m), 0.5, part)
+    assert merges > 0
+    for c in range(nc):
+        kids = np.nonzero(parent == c)[0]
+        assert len(set(part[kids].tolist())) == 1
+
+
+def test_stall_when_nothing_merges(orc):
+    m = configs.single_cell(2)
+    parent, nc, merges = orc.agglomerate(orc.Level.from_mesh(m), 0.5)
+    assert merges == 0 and nc == 1
+    H = orc.build_hierarchy(m, 3, 0.5)
+    assert len(H) == 1
+
+
+# ----------------------------------------------------------------- point formulas
+def _W(rho, u, p):
+    return state.prim_to_cons(np.array(rho), np.asarray(u, dtype=float), np.array(p))
+
+
+def test_euler_flux_and_spectral_radius_examples(orc):
+    e = GOLD["euler_flux"]
+    T = orc.euler_flux(2, G, _W(e["rho"], e["u"], e["p"]), e["n"])
+    assert np.allclose(T, e["T"], rtol=1e-15, atol=1e-15), e["cite"]
+    e = GOLD["spectral_radius"]
+    W = _W(e["rho"], e["u"], e["p"])
+    r = orc.spectral_radius(2, G, 1.0, W, W, e["n"])
+    assert abs(r - e["r"]) < e["tol"] and abs(r - (1 + math.sqrt(1.4))) < 1e-15
+    assert orc.spectral_radius(2, G, 1.0, W, W, [-1.0, 0.0]) == r  # |U.n| symmetric
+
+
+def test_df_examples(orc):
+    for e in GOLD["df_point"]:
+        a = math.sqrt(G)
+        WL = _W(1.0, [e["dMan"] * a, 0.0], e["pl"])
+        WR = _W(1.0, [0.0, 0.0], e["pr"])
+        assert abs(orc.df_face(2, G, WL, WR, [1.0, 0.0]) - e["alpha"]) <= e.get("tol", 1e-15), e["cite"]
+    W = _W(1.3, [0.2, -0.4], 0.9)
+    assert orc.df_face(2, G, W, W, [0.6, 0.8]) == 1.0
+    e = GOLD["df_cell"]
+    assert abs(e["alpha_face"] ** (e["faces"] * e["M"]) - e["alpha"]) < e["tol"]
+
+
+def test_hybrid_diagonal_examples(orc):
+    e = GOLD["hybrid_diagonal"]
+    cfl = e["sum_Sr"] * e["dt"] / e["V"]           # Dt = CFL V / Sigma (A3)
+    D = orc.diag([e["sum_Sr"]], [e["alpha"]], cfl, cfl)
+    assert abs(D[0] - e["D"]) < 1e-12, e["cite"]
+    # limits
+    D0 = orc.diag([4.0], [0.0], 10.0, 0.5)
+    D1 = orc.diag([4.0], [1.0], 10.0, 0.5)
+    assert D0[0] == 4.0 / 0.5 and D1[0] == 4.0 / 10.0 + 2.0
+
+
+# ----------------------------------------------------------------- KFVS
+def _rand_state(rng, dim, mach=1.0):
+    rho = rng.uniform(0.5, 2.0)
+    p = rng.uniform(0.5, 2.0)
+    u = rng.normal(size=dim) * mach * math.sqrt(G * p / rho) / math.sqrt(dim)
+    return _W(rho, u, p)
+
+
+def _unit(rng, dim):
+    v = rng.normal(size=dim)
+    return v / np.linalg.norm(v)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_kfvs_equal_states_give_euler_flux(orc, dim):
+    rng = np.random.default_rng(dim)
+    for _ in range(20):
+        W = _rand_state(rng, dim, 2.0)
+        n = _unit(rng, dim)
+        F = orc.kfvs_flux(dim, G, W, W, n)
+        T = orc.euler_flux(dim, G, W, n)
+        assert np.allclose(F, T, rtol=1e-13, atol=1e-13 * np.abs(T).max())
+
+
+def test_kfvs_stationary(orc):
+    """equal stationary states -> mass 0, momentum p."""
+    W = _W(1.0, [0.0, 0.0, 0.0], 0.7)
+    F = orc.kfvs_flux(3, G, W, W, [0.0, 0.0, 1.0])
+    assert abs(F[0]) < 1e-16 and abs(F[3] - 0.7) < 1e-15 and abs(F[4]) < 1e-16
+
+
+def test_kfvs_supersonic_upwind(orc):
+    """Ma_n > ~4: flux = Euler flux of the upwind state."""
+    WL = _W(1.0, [6.0 * math.sqrt(G), 0.3], 1.0)
+    WR = _W(0.3, [6.0 * math.sqrt(G * 0.2 / 0.3), 0.0], 0.2)   # also supersonic -> no back-flow
+    F = orc.kfvs_flux(2, G, WL, WR, [1.0, 0.0])
+    T = orc.euler_flux(2, G, WL, [1.0, 0.0])
+    assert np.allclose(F, T, rtol=1e-4)
+
+
+def test_kfvs_antisymmetry(orc):
+    rng = np.random.default_rng(9)
+    WL, WR = _rand_state(rng, 3), _rand_state(rng, 3)
+    n = _unit(rng, 3)
+    F1 = orc.kfvs_flux(3, G, WL, WR, n)
+    F2 = orc.kfvs_flux(3, G, WR, WL, -n)
+    assert abs(F1[0] + F2[0]) < 1e-14
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_kfvs_against_velocity_space_quadrature(orc, dim):
+    """Free transport of two Maxwellians integrated numerically over velocity
+    space (normal: adaptive quadrature on each half line; tangential:
+    Gauss-Hermite; internal dof: K/(2 lambda)), SURVEY pin for O4."""
+    from scipy import integrate
+    rng = np.random.default_rng(100 + dim)
+    K = (5 - 3 * G) / (G - 1) if dim == 3 else (4 - 2 * G) / (G - 1)
+    xh, wh = np.polynomial.hermite.hermgauss(12)
+    for _ in range(4):
+        WL, WR = _rand_state(rng, dim, 1.5), _rand_state(rng, dim, 1.5)
+        n = _unit(rng, dim)
+        # orthonormal tangents
+        basis = np.linalg.qr(np.column_stack([n] + [rng.normal(size=dim) for _ in range(dim - 1)]))[0]
+        basis[:, 0] = n if np.dot(basis[:, 0], n) > 0 else n
+        tang = [basis[:, k] for k in range(1, dim)]
+        total = np.zeros(dim + 2)
+        for W, lo, hi in ((WL, 0.0, np.inf), (WR, -np.inf, 0.0)):
+            rho = W[0]
+            u = W[1:dim + 1] / rho
+            p = (G - 1) * (W[dim + 1] - 0.5 * rho * u @ u)
+            lam = rho / (2 * p)
+            U = u @ n
+            ut = [u @ t for t in tang]
+            sig = 1.0 / math.sqrt(2 * lam)
+
+            def moment(k):
+                f = lambda c: c ** k * math.sqrt(lam / math.pi) * math.exp(-lam * (c - U) ** 2)
+                return integrate.quad(f, lo, hi, epsabs=1e-14, epsrel=1e-13, limit=200)[0]
+
+            M = [moment(k) for k in range(4)]
+            # tangential Gauss-Hermite expectations of c_t and |c_t|^2
+            Et = [sum(w * (ut[a] + math.sqrt(2) * sig * x) for x, w in zip(xh, wh)) / math.sqrt(math.pi)
+                  for a in range(dim - 1)]
+            Et2 = sum(sum(w * (ut[a] + math.sqrt(2) * sig * x) ** 2 for x, w in zip(xh, wh)) / math.sqrt(math.pi)
+                      for a in range(dim - 1))
+            Fm = rho * M[1]
+            Fmom = rho * M[2] * n + sum(rho * M[1] * Et[a] * tang[a] for a in range(dim - 1))
+            FE = 0.5 * rho * (M[3] + M[1] * (Et2 + K / (2 * lam)))
+            total += np.concatenate([[Fm], Fmom, [FE]])
+        F = orc.kfvs_flux(dim, G, WL, WR, n)
+        assert np.allclose(F, total, rtol=1e-10, atol=1e-11), (F, total)
+
+
+# ----------------------------------------------------------------- residual
+@pytest.mark.parametrize("mk", range(6))
+def test_freestream_residual_zero(orc, mk):
+    """Closure P:454 => uniform flow has zero residual; walls excepted,
+    so use farfield/extrapolation patches only here."""
+    m = small_meshes()[mk]
+    m.patch_kind = np.array([FARFIELD if k in (SLIP, NOSLIP) else k for k in m.patch_kind], dtype=np.int32)
+    d = m.dim
+    rho, vel, p = 1.2, [0.7, -0.3, 0.2][:d], 0.9
+    W = state.uniform(m, rho, vel, p)
+    Winf = state.winf(rho, vel, p)
+    R, a, S, rf = orc.residual(orc.Level.from_mesh(m), W, Winf)
+    Fref = np.abs(orc.euler_flux(d, G, Winf, np.eye(d)[0])).max() * np.sqrt((m.avec ** 2).sum(0)).max()
+    assert np.abs(R).max() <= 1e-12 * Fref
+    assert np.all(a == 1.0)
+    assert np.all(S > 0)
+
+
+def test_residual_antisymmetric_face_assembly(orc):
+    """R_i = sum_f sigma_if S_f F_f: sum over all cells = boundary flux only
+    (interior faces cancel), checked against per-face kfvs_flux."""
+    m = configs.box3d(2, 2, 2, 1, seed=4)
+    rng = np.random.default_rng(0)
+    W = state.perturbed(m, 1.0, [0.5, 0.1, 0.0], 0.7, eps=0.2, seed=1)
+    Winf = state.winf(1.0, [0.5, 0.1, 0.0], 0.7)
+    lv = orc.Level.from_mesh(m)
+    R, _, _, _ = orc.residual(lv, W, Winf)
+    # independent face-by-face assembly in Python using the point flux
+    Rb = np.zeros_like(R)
+    for f in range(m.n_faces):
+        A = m.avec[:, f]
+        S = np.linalg.norm(A)
+        n = A / S
+        l, r = m.left[f], m.right[f]
+        WL = W[:, l]
+        if r >= 0:
+            WR = W[:, r]
+        else:
+            kind = m.patch_kind[-r - 1]
+            WR = WL.copy()
+            if kind == FARFIELD:
+                WR = Winf.copy()
+            elif kind == SLIP:
+                WR[1:4] = WL[1:4] - 2 * (WL[1:4] @ n) * n
+            elif kind == NOSLIP:
+                WR[1:4] = -WL[1:4]
+        F = orc.kfvs_flux(3, G, WL, WR, n) * S
+        Rb[:, l] += F
+        if r >= 0:
+            Rb[:, r] -= F
+    assert np.allclose(R, Rb, rtol=1e-13, atol=1e-15)
+
+
+def test_residual_restriction_telescopes(orc):
+    """Res*_c = sum of children residuals = the coarse cell's total
+    flux through its boundary computed with the fine fluxes."""
+    m = configs.tri_square(6, 6, seed=4)
+    lv = orc.Level.from_mesh(m)
+    W = state.perturbed(m, 1.0, [0.5, 0.0], 0.7, eps=0.1, seed=2)
+    Winf = state.winf(1.0, [0.5, 0.0], 0.7)
+    R, a, _, _ = orc.residual(lv, W, Winf)
+    parent, nc, _ = orc.agglomerate(lv, 0.5)
+    lc = orc.coarse_build(lv, parent, nc)
+    _, Rs, _ = orc.restrict(parent, nc, m.vol, lc.vol, W, R, a)
+    direct = np.zeros((4, nc))
+    for f in range(m.n_faces):
+        l, r = m.left[f], m.right[f]
+        if r >= 0 and parent[l] == parent[r]:
+            continue  # internal to the aggregate: telescopes away
+        A = m.avec[:, f]
+        S = np.linalg.norm(A)
+        n = A / S
+        WR = W[:, r] if r >= 0 else Winf
+        F = orc.kfvs_flux(2, G, W[:, l], WR, n) * S
+        direct[:, parent[l]] += F
+        if r >= 0:
+            direct[:, parent[r]] -= F
+    assert np.allclose(Rs, direct, rtol=1e-12, atol=1e-14)
+
+
+# ----------------------------------------------------------------- sweep
+def _setup_level(orc, m, seed=0, alpha=None, eps=0.1):
+    d = m.dim
+    vel = [0.6, 0.2, -0.1][:d]
+    W = state.perturbed(m, 1.0, vel, 0.7, eps=eps, seed=seed)
+    Winf = state.winf(1.0, vel, 0.7)
+    lv = orc.Level.from_mesh(m)
+    R, a, S, rf = orc.residual(lv, W, Winf)
+    if alpha is not None:
+        a = np.full(m.n_cells, alpha) if np.isscalar(alpha) else alpha
+    col, nc = orc.color(lv)
+    return lv, W, R, a, S, rf, col, nc
+
+
+def test_sweep_alpha_zero_is_explicit(orc):
+    """P:519 / S:484: alpha = 0 => dW = -R Dt_exp / V = -(CFL_exp/Sigma) R."""
+    m = configs.tri_square(5, 5, seed=1)
+    lv, W, R, a, S, rf, col, nc = _setup_level(orc, m, alpha=0.0)
+    D = orc.diag(S, a, 10.0, 0.5)
+    dW = orc.smooth(lv, W, R, a, D, rf, col, nc, 3)
+    Wn = orc.explicit_update(W, S, R, 0.5)
+    assert np.allclose(W + dW, Wn, rtol=1e-14, atol=1e-15)
+    assert np.allclose(dW, -(0.5 / S) * R, rtol=1e-14, atol=0)
+
+
+def test_sweep_isolated_cell(orc):
+    m = configs.single_cell(3)
+    lv, W, R, a, S, rf, col, nc = _setup_level(orc, m, alpha=0.7)
+    D = orc.diag(S, a, 10.0, 0.5)
+    dW = orc.smooth(lv, W, R, a, D, rf, col, nc, 4)
+    assert np.array_equal(dW, -R / D)
+
+
+def _literal_sweep1(m, W, R, a, D, rf, col, nc):
+    """The printed Eq.(gpu-forward-relaxation) / Eq.(gpu-backward-relaxation)
+     with the blended D on the backward RHS (reading A1): forward
+    reads only lower colors, backward only upper colors."""
+    d, n = m.dim, m.n_cells
+    nv = d + 2
+    faces_of = [[] for _ in range(n)]
+    for f in range(m.n_faces):
+        if m.right[f] >= 0:
+            faces_of[m.left[f]].append(f)
+            faces_of[m.right[f]].append(f)
+
+    def off(i, dW, pred):
+        s = np.zeros(nv)
+        for f in faces_of[i]:
+            j = m.right[f] if m.left[f] == i else m.left[f]
+            if not pred(col[j], col[i]):
+                continue
+            sg = 1.0 if m.left[f] == i else -1.0
+            A = m.avec[:, f]
+            S = np.linalg.norm(A)
+            nn = sg * A / S
+            T1 = np.array(brute.euler_T(d, G, (W[:, j] + dW[:, j]).tolist(), nn.tolist()))
+            T0 = np.array(brute.euler_T(d, G, W[:, j].tolist(), nn.tolist()))
+            s += S * (T1 - T0 - rf[f] * dW[:, j])
+        return s
+
+    dWs = np.zeros((nv, n))
+    for c in range(1, nc + 1):
+        for i in np.nonzero(col == c)[0]:
+            dWs[:, i] = (-R[:, i] - 0.5 * a[i] * off(i, dWs, lambda cj, ci: cj < ci)) / D[i]
+    dW = dWs.copy()
+    for c in range(nc, 0, -1):
+        for i in np.nonzero(col == c)[0]:
+            dW[:, i] = (D[i] * dWs[:, i] - 0.5 * a[i] * off(i, dW, lambda cj, ci: cj > ci)) / D[i]
+    return dW
+
+
+@pytest.mark.parametrize("mk", [0, 1, 3])
+def test_sweep1_equals_printed_equations(orc, mk):
+    m = small_meshes()[mk]
+    lv, W, R, a, S, rf, col, nc = _setup_level(orc, m)
+    a = np.random.default_rng(3).uniform(0.2, 1.0, m.n_cells)
+    D = orc.diag(S, a, 10.0, 0.5)
+    dW = orc.smooth(lv, W, R, a, D, rf, col, nc, 1)
+    ref = _literal_sweep1(m, W, R, a, D, rf, col, nc)
+    assert np.allclose(dW, ref, rtol=1e-13, atol=1e-15 * np.abs(ref).max())
+
+
+def _implicit_system_residual(m, W, R, a, D, rf, dW):
+    """|| D dW + 1/2 alpha sum S[T(W_j+dW_j) - T(W_j) - r dW_j] + Rt ||
+    -- the DF-hybrid implicit system P:456/P:512 with the flux-splitting
+    linearisation P:449 that LU-SGS approximately solves."""
+    d, n = m.dim, m.n_cells
+    res = D[None, :] * dW + R
+    for f in range(m.n_faces):
+        l, r = m.left[f], m.right[f]
+        if r < 0:
+            continue
+        A = m.avec[:, f]
+        S = np.linalg.norm(A)
+        for i, j, sg in ((l, r, 1.0), (r, l, -1.0)):
+            nn = sg * A / S
+            T1 = np.array(brute.euler_T(d, G, (W[:, j] + dW[:, j]).tolist(), nn.tolist()))
+            T0 = np.array(brute.euler_T(d, G, W[:, j].tolist(), nn.tolist()))
+            res[:, i] += 0.5 * a[i] * S * (T1 - T0 - rf[f] * dW[:, j])
+    return res
+
+
+@pytest.mark.parametrize("mk", [0, 2, 4])
+def test_sweeps_converge_to_implicit_system(orc, mk):
+    """Fixed point (SURVEY pin vii): many sweeps solve the nonlinear
+    implicit system; also agrees with scipy's Newton-Krylov-free root."""
+    from scipy import optimize
+    m = small_meshes()[mk]
+    lv, W, R, a, S, rf, col, nc = _setup_level(orc, m, eps=0.05)
+    a = np.random.default_rng(5).uniform(0.3, 1.0, m.n_cells)
+    D = orc.diag(S, a, 10.0, 0.5)
+    dW = orc.smooth(lv, W, R, a, D, rf, col, nc, 200)
+    res = _implicit_system_residual(m, W, R, a, D, rf, dW)
+    assert np.abs(res).max() <= 1e-11 * np.abs(R).max()
+    if m.n_cells <= 16:
+        sol = optimize.root(lambda x: _implicit_system_residual(m, W, R, a, D, rf, x.reshape(dW.shape)).ravel(),
+                            np.zeros(dW.size), method="hybr", tol=1e-14)
+        assert np.allclose(sol.x.reshape(dW.shape), dW, rtol=1e-8, atol=1e-12 * np.abs(dW).max())
+
+
+def test_sweep_sequential_gs_order_invariance(orc):
+    """S:480 / pin (v): a sequential Gauss-Seidel over cells in color order,
+    with the within-color order reversed, gives the identical result."""
+    m = configs.tri_square(4, 4, seed=8)
+    lv, W, R, a, S, rf, col, nc = _setup_level(orc, m)
+    D = orc.diag(S, a, 10.0, 0.5)
+    dW = orc.smooth(lv, W, R, a, D, rf, col, nc, 2)
+    d, n = 2, m.n_cells
+    faces_of = [[] for _ in range(n)]
+    for f in range(m.n_faces):
+        faces_of[m.left[f]].append(f)
+        if m.right[f] >= 0:
+            faces_of[m.right[f]].append(f)
+    x = np.zeros((4, n))
+
+    def upd(i):
+        s = [0.0] * 4
+        for f in faces_of[i]:
+            if m.right[f] < 0:
+                continue
+            j = m.right[f] if m.left[f] == i else m.left[f]
+            sg = 1.0 if m.left[f] == i else -1.0
+            A = m.avec[:, f].tolist()
+            S_ = math.sqrt(A[0] * A[0] + A[1] * A[1])
+            nn = [sg * A[0] / S_, sg * A[1] / S_]
+            Wj = W[:, j].tolist()
+            dj = x[:, j].tolist()
+            T1 = brute.euler_T(2, G, [Wj[q] + dj[q] for q in range(4)], nn)
+            T0 = brute.euler_T(2, G, Wj, nn)
+            for q in range(4):
+                s[q] += S_ * (T1[q] - T0[q] - rf[f] * dj[q])
+        for q in range(4):
+            x[q, i] = -(R[q, i] + 0.5 * a[i] * s[q]) / D[i]
+
+    for _ in range(2):
+        for c in list(range(1, nc + 1)) + list(range(nc, 0, -1)):
+            brute.greedy_sequential_gs(list(np.nonzero(col == c)[0])[::-1], upd)
+    assert np.allclose(x, dW, rtol=1e-14, atol=1e-17)
+
+
+# ----------------------------------------------------------------- restrict / prolong
+def test_restrict_worked_example(orc):
+    e = GOLD["restrict_state"]
+    W0c, Rc, ac = orc.restrict(np.array([0, 0]), 1, np.array(e["V"]), np.array([sum(e["V"])]),
+                               np.array([e["W"]]), np.array([[1.0, -1.0]]), np.array([0.3, 0.2]))
+    assert W0c[0, 0] == e["W0"], e["cite"]
+    assert Rc[0, 0] == 0.0 and ac[0] == 0.2       # S:529 cancellation; min (A15)
+
+
+def test_restrict_conservation_and_prolong_limits(orc):
+    m = configs.tri_square(6, 6, seed=4)
+    lv = orc.Level.from_mesh(m)
+    parent, nc, _ = orc.agglomerate(lv, 0.5)
+    lc = orc.coarse_build(lv, parent, nc)
+    W = state.perturbed(m, 1.0, [0.5, 0.0], 0.7, eps=0.2, seed=3)
+    R = np.random.default_rng(1).normal(size=W.shape)
+    a = np.random.default_rng(2).uniform(0, 1, m.n_cells)
+    W0c, Rc, ac = orc.restrict(parent, nc, m.vol, lc.vol, W, R, a)
+    assert np.allclose((W0c * lc.vol).sum(1), (W * m.vol).sum(1), rtol=1e-14)
+    assert np.allclose(Rc.sum(1), R.sum(1), rtol=1e-12, atol=1e-12)
+    # prolongation: alpha = 0 bit-identical
+    Wc = W0c + 0.01
+    Wp = orc.prolong(parent, np.zeros(m.n_cells), Wc, W0c, W)
+    assert np.array_equal(Wp, W)
+    # alpha = 1, uniform correction c: totals shift by c sum V
+    c = np.array([0.01, -0.02, 0.03, 0.04])[:, None]
+    Wp = orc.prolong(parent, np.ones(m.n_cells), W0c + c, W0c, W)
+    assert np.allclose((Wp * m.vol).sum(1) - (W * m.vol).sum(1), c[:, 0] * m.vol.sum(), rtol=1e-9)
+
+
+# ----------------------------------------------------------------- V-cycle
+def test_vcycle_freestream_fixed_point(orc):
+    """uniform flow is invariant under the whole V-cycle."""
+    m = configs.tri_square(8, 8, seed=2)
+    H = orc.build_hierarchy(m, 3, 0.5)
+    W = state.uniform(m, 1.0, [0.5, 0.1], 0.7)
+    Winf = state.winf(1.0, [0.5, 0.1], 0.7)
+    W1, hist = orc.vcycle(H, W, Winf, orc.Options(), n_cycles=2)
+    assert np.abs(W1 - W).max() <= 1e-12 * np.abs(W).max()
+    assert hist.shape == (3, 4) and hist.max() < 1e-13
+
+
+def test_vcycle_one_level_is_one_fine_step(orc):
+    """a 1-level hierarchy degenerates to one fine smoothing step."""
+    m = configs.tri_square(5, 5, seed=2)
+    H = orc.build_hierarchy(m, 1, 0.5)
+    W = state.perturbed(m, 1.0, [0.5, 0.1], 0.7, eps=0.1, seed=5)
+    Winf = state.winf(1.0, [0.5, 0.1], 0.7)
+    W1, _ = orc.vcycle(H, W, Winf, orc.Options(n_levels=1), 1)
+    R, a, S, rf = orc.residual(H[0]["level"], W, Winf)
+    assert np.array_equal(W1, orc.explicit_update(W, S, R, 0.5))
+
+
+def test_vcycle_alpha_zero_fine_unchanged_by_coarse(orc):
+    """df_mode 1 with alpha = 0 on the fine level: the coarse correction is
+    multiplied by 0 -> V-cycle = fine explicit step."""
+    m = configs.tri_square(6, 6, seed=2)
+    H = orc.build_hierarchy(m, 3, 0.5)
+    W = state.perturbed(m, 1.0, [0.5, 0.1], 0.7, eps=0.1, seed=6)
+    Winf = state.winf(1.0, [0.5, 0.1], 0.7)
+    W1, _ = orc.vcycle(H, W, Winf, orc.Options(df_mode=1), 1, user_alpha=np.zeros(m.n_cells))
+    R, a, S, rf = orc.residual(H[0]["level"], W, Winf)
+    assert np.array_equal(W1, orc.explicit_update(W, S, R, 0.5))
+
+
+def test_vcycle_reduces_residual_config1(orc):
+    m = configs.config(1)
+    H = orc.build_hierarchy(m, 3, 0.5)
+    W = state.gaussian_bump(m, *configs.FREESTREAM[1])
+    Winf = state.winf(*configs.FREESTREAM[1])
+    _, hist = orc.vcycle(H, W, Winf, orc.Options(), 30)
+    assert np.all(np.isfinite(hist)) and hist[-1, 0] < hist[0, 0]
+
+
+def test_mesh_closure_all_configs_small():
+    for m in small_meshes() + [configs.naca_ogrid(ni=64, n_quad=8, n_tri=4), configs.sphere_shell(4, 2, 2)]:
+        assert closure_error(m) < 1e-13
