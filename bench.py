@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""bench.py -- MC-LU-SGS sweep / V-cycle throughput on B200 (BASELINE.json metric).
+
+A "step" is one 3-level V-cycle (every SURVEY §8(a) row: fine residual +
+explicit pre-smooth, residual, restriction + forcing, coarse residual +
+prepare + 6 MC-LU-SGS sweeps on each coarse level, DF prolongation, residual
+norm) on BASELINE configs[3]: the 3D ~1M-cell tet/prism sphere shell
+(synthetic, seeded), FP64.
+
+value  = MC-LU-SGS cell-updates per V-cycle / device time per V-cycle
+         (one cell-update = one cell's dW solved once),
+         summed over all ranks.
+e2e    = the same metric through the C ABI with pinned HOST buffers: per step
+         gmg_set_state (H2D) + gmg_vcycle + gmg_get_state (D2H).
+roofline: the sweep kernel (dominant), algorithmic bytes / its
+         CUDA-event time inside the profiled V-cycles, vs MEASURED_PEAKS hbm.
+cpu_baseline: the oracle (plain C, 1 thread) on one V-cycle of the same mesh.
+
+--impl reference runs the oracle as the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/s per MC-LU-SGS sweep & V-cycle, HBM GB/s frac, at 1/2/4/8 B200"
+UNIT = "cell-updates/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy kernel)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device=0):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(f) == 6:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def workload(config):
+    from synth import configs, state
+    m = configs.config(config)
+    fs = configs.FREESTREAM[config]
+    W = state.bow_shock(m, *fs)
+    return m, W, state.winf(*fs)
+
+
+def sweep_updates_per_cycle(sizes, n_sweeps, fine_smoother):
+    lv = range(0 if fine_smoother else 1, len(sizes))
+    return sum(sizes[l][0] for l in lv) * 2 * n_sweeps
+
+
+def cpu_baseline(m, W, Winf, n_sweeps, n_cycles=1):
+    """The oracle, as it stands (single thread), on n_cycles V-cycles of the
+    same mesh.  Hierarchy build is setup, not timed."""
+    import oracle
+    H = oracle.build_hierarchy(m, 3, 0.5)
+    opt = oracle.Options(n_sweeps=n_sweeps)
+    t0 = time.perf_counter()
+    oracle.vcycle(H, W, Winf, opt, n_cycles)
+    dt = time.perf_counter() - t0
+    cu = sum(e["level"].n for e in H[1:]) * 2 * n_sweeps * n_cycles
+    return {"value": cu / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{n_cycles} V-cycle(s) of the same {m.n_cells}-cell mesh ({dt:.1f} s), "
+                      f"plain C oracle, 1 thread, host {os.cpu_count()} cores"}
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        import torch
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def run_reference(args, ws, rank):
+    """Reference arm: the oracle (the only reference this tier has)."""
+    if rank != 0:
+        return 0
+    m, W, Winf = workload(args.config)
+    import oracle
+    H = oracle.build_hierarchy(m, 3, 0.5)
+    opt = oracle.Options(n_sweeps=args.n_sweeps)
+    cu = sum(e["level"].n for e in H[1:]) * 2 * args.n_sweeps
+    Wc = W
+    for _ in range(args.warmup_ref):
+        Wc, _ = oracle.vcycle(H, Wc, Winf, opt, 1)
+    times = []
+    for _ in range(args.steps_ref):
+        t0 = time.perf_counter()
+        Wc, _ = oracle.vcycle(H, Wc, Winf, opt, 1)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    v = cu * len(times) / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+            "steps": len(times), "warmup": args.warmup_ref, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"config{args.config}: 3D sphere shell {m.n_cells} cells "
+                                                      "(tet+prism), 3-level V-cycle, 6 MC-LU-SGS sweeps",
+                                            "n_cells": m.n_cells},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{len(times)} V-cycles of config{args.config}, plain C oracle, 1 thread"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gmg", choices=["gmg", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--n-sweeps", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/cpu)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
+    args.steps_ref = max(1, min(args.steps, 5))
+    args.warmup_ref = 1
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+
+    import numpy as np
+    import torch
+    from paper_2509_06347_b200 import _build
+    _build.build()
+    from paper_2509_06347_b200 import gmg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    m, W, Winf = workload(args.config)
+    s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps)
+    s.set_state(W, Winf)
+    stream = torch.cuda.current_stream(dev)
+    nv = s.nv
+    cu_cycle = sweep_updates_per_cycle(s.sizes, args.n_sweeps, 0)
+
+    # warm-up (builds + replays the CUDA graph)
+    for _ in range(args.warmup):
+        s.vcycle(1)
+    s.set_state(W, Winf)
+    launches_per_cycle = s.vcycle_launches()
+    if args.profile_only:
+        s.vcycle(args.steps)
+        torch.cuda.synchronize()
+        print(json.dumps({"profile_only": True, "launches_per_cycle": launches_per_cycle}))
+        return 0
+
+    # ---------------- timed region: K V-cycles (graph replays) ----------------
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        gmg.gmg_vcycle(s.ctx, args.steps, None)      # K cycles + 1 final residual norm, on `stream`
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = cu_cycle * ws / (ms_step * 1e-3)
+
+    # ---------------- per-kernel profile (CUDA events per launch) --------------
+    s.set_state(W, Winf)
+    pms, pcnt, pbytes = s.profile_vcycle(max(3, min(args.steps, 10)))
+    peak, peak_src = _peaks()
+    sw = gmg.K_SWEEP
+    sweep_ms_avg = pms[sw] / max(pcnt[sw], 1)
+    achieved = (pbytes[sw] / (pms[sw] * 1e-3)) / 1e9 if pms[sw] > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    prof_total = float(pms.sum())
+    kernels = {gmg.K_NAMES[k]: {"ms": float(pms[k]), "launches": int(pcnt[k]),
+                                "share": float(pms[k] / prof_total) if prof_total else None,
+                                "GB/s": float(pbytes[k] / (pms[k] * 1e-3) / 1e9) if pms[k] > 0 else None}
+               for k in range(gmg.K_COUNT)}
+
+    # sweep-only throughput on each coarse level (graph of one smoothing step)
+    sweep_only = {}
+    for l in range(1, s.n_levels):
+        t_ms, cu, by = s.time_smooth(l, args.n_sweeps, 5)
+        sweep_only[f"level{l}"] = {"cell_updates_per_s": cu / (t_ms * 1e-3), "GB/s": by / (t_ms * 1e-3) / 1e9,
+                                   "frac": (by / (t_ms * 1e-3) / 1e9) / peak}
+
+    # ---------------- e2e through the C ABI with pinned host buffers ----------
+    Wh = torch.from_numpy(W).pin_memory()
+    Wo = torch.empty_like(Wh).pin_memory()
+    winf = np.ascontiguousarray(Winf)
+    for _ in range(2):
+        gmg.gmg_set_state(s.ctx, Wh, winf)
+        gmg.gmg_vcycle(s.ctx, 1, None)
+        gmg.gmg_get_state(s.ctx, 0, Wo)
+    e_steps = max(3, min(args.steps, 10))
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        gmg.gmg_set_state(s.ctx, Wh, winf)
+        gmg.gmg_vcycle(s.ctx, 1, None)
+        gmg.gmg_get_state(s.ctx, 0, Wo)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e_steps
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": cu_cycle * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(W.nbytes),
+           "d2h_bytes_per_step": int(W.nbytes + (nv * 2 * 8)),
+           "ms_per_step": e2e_s * 1e3, "timer": "host wall clock around synchronous ABI calls"}
+
+    if rank != 0:
+        return 0
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        cpu = cpu_baseline(m, W, Winf, args.n_sweeps, 1)
+    ws_bytes = int(s.ws.numel())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded mesh + bow-shock state, no datasets)",
+        "config": {"workload": f"config{args.config}: 3D sphere shell, {m.n_cells} cells "
+                               f"({m.meta['cell_type_counts']}), 3-level V-cycle, {args.n_sweeps} MC-LU-SGS sweeps",
+                   "levels": [{"cells": int(n), "colors": int(c), "faces": int(f)} for (n, c, f) in s.sizes],
+                   "sweep_cell_updates_per_vcycle": int(cu_cycle),
+                   "l2": f"inputs larger than L2: workspace {ws_bytes / 1e9:.2f} GB >> 126 MB",
+                   "parallelism": f"dp{ws}" if ws > 1 else "single GPU",
+                   "multi_gpu": "independent replicas per rank (partitioned halo path: DESIGN.md)"},
+        "vcycles_per_s": 1e3 / ms_step * ws,
+        "fine_cell_vcycles_per_s": m.n_cells * 1e3 / ms_step * ws,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "k_sweep<3> (per-color MC-LU-SGS sweep)",
+                     "avg_launch_ms": sweep_ms_avg, "peak_source": peak_src,
+                     "bytes_def": "algorithmic: own Rt, 1/D, alpha/2, dW write + neighbour-unique W, dW + "
+                                  "face data once per face + 4 B/slot (DESIGN.md)"},
+        "kernels": kernels, "sweep_only": sweep_only,
+        "gpu_launches": int(launches_per_cycle * args.steps + 2),
+        "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

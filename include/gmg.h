@@ -1,0 +1,195 @@
+/*
+ * gmg.h -- C ABI of libgmg: the B200 (sm_100a) hot path of arXiv 2509.06347,
+ * "A Geometric Multigrid-Accelerated Compact Gas-Kinetic Scheme ..." :
+ * multi-color matrix-free LU-SGS (MC-LU-SGS) smoothing inside a 3-level
+ * geometric V-cycle on unstructured 2D/3D meshes, with hash/skewness
+ * agglomeration, volume-weighted restriction, forcing and DF-limited
+ * prolongation.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (the reference
+ * texts), readings A1..A30.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions (apply to every call)
+ *  - Ownership: the caller owns every pointer it passes; the library copies
+ *    what it needs during the call and never retains caller pointers.
+ *  - Arrays at the boundary are in NATURAL order (the mesh generator's cell /
+ *    face numbering, or the natural numbering of a coarse level, O1), SoA
+ *    [component][item], float64 unless stated.  The library permutes
+ *    internally (color-contiguous renumbering).
+ *  - Pointers may be host or device memory (classified with
+ *    cudaPointerGetAttributes) wherever "host/device" is written.
+ *  - Device memory: ONE caller-allocated workspace (gmg_set_workspace); the
+ *    library sub-allocates and never calls cudaMalloc.  Host-side setup
+ *    (coloring, agglomeration, layouts) uses host heap memory.
+ *  - Stream: every call is asynchronous on gmg_options.stream; a call that
+ *    returns host data synchronizes that stream first.
+ *  - Errors: return codes only; no exceptions cross the ABI.  A failing
+ *    call leaves a message in gmg_last_error(ctx).
+ *  - Multi-rank (nranks > 1): collective semantics, every rank makes the same
+ *    sequence of calls with the same global mesh.
+ * ---------------------------------------------------------------------------
+ */
+#ifndef GMG_H
+#define GMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gmg_ctx gmg_ctx; /* opaque; one per rank */
+
+typedef enum {
+    GMG_OK = 0,
+    GMG_EINVAL = 1,      /* bad argument / option                                  */
+    GMG_ETOPO = 2,       /* mesh topology: bad cell index, non-manifold, open cell   */
+    GMG_ECOLOR = 3,      /* user coloring invalid (same-color face neighbours)      */
+    GMG_ESTALL = 4,      /* hierarchy truncated: a level merged nothing     */
+    GMG_ENOMEM = 5,      /* workspace too small / host allocation failed            */
+    GMG_ECUDA = 6,       /* CUDA runtime error                                      */
+    GMG_ENCCL = 7,       /* NCCL error (multi-rank)                                 */
+    GMG_ENONFINITE = 8,  /* NaN/Inf detected; level and cell in gmg_last_error      */
+    GMG_ESTATE = 9       /* call out of order (e.g. smooth before workspace)        */
+} gmg_status;
+
+/* boundary patch kinds (ghost states, SURVEY O4 / reading A25) */
+enum { GMG_FARFIELD = 0, GMG_SLIP = 1, GMG_NOSLIP = 2, GMG_EXTRAP = 3 };
+
+typedef struct {
+    int dim;                /* 2 or 3; nv = dim + 2 conserved variables W = (rho, m, rho E) */
+    double gamma;           /* ratio of specific heats, 1.4                                 */
+    double cfl_imp;         /* implicit CFL, Dt_imp = cfl_imp V / Sigma (A2, A3); 10  */
+    double cfl_exp;         /* explicit CFL, Dt_exp = cfl_exp V / Sigma; 0.5          */
+    int n_sweeps;           /* MC-LU-SGS sweeps per smoothing step; 6          */
+    int n_levels;           /* V-cycle levels; 3                                      */
+    int pre_smooth;         /* 1; only 1 is supported                                 */
+    int post_smooth;        /* 0; only 0 is supported                                 */
+    double skew_limit;      /* agglomeration skewness threshold theta (A21); 0.5              */
+    double r_factor;        /* omega in r_ij = omega (|U.n| + a) >= Lambda; 1.0       */
+    int fine_smoother;      /* 0 = explicit Eq.(smo) (paper); 1 = MC-LU-SGS        */
+    int df_mode;            /* 0 = first-order DF helper (O5); 1 = user alpha; 2 = alpha == 1 */
+    int rank, nranks;       /* this rank / world size (1 = single GPU)                        */
+    const void *nccl_id;    /* 128-byte ncclUniqueId (nranks > 1), else NULL                  */
+    int device;             /* CUDA device ordinal                                            */
+    void *stream;           /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)    */
+} gmg_options;
+
+/* Fill *o with the defaults above (dim = 3, single rank, device 0, stream 0). */
+void gmg_default_options(gmg_options *o);
+
+/* Create a context.  Validates options (GMG_EINVAL). */
+gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out);
+
+/* a1: load the fine mesh (host pointers, natural order):
+ *   vol[n], centroid[dim][n]; faces: left[nf] (owner cell), right[nf] (other
+ *   cell, or -(patch+1) for a boundary face), area_vec[dim][nf] = S_f n_f
+ *   pointing left -> right, face_ctr[dim][nf], n_gauss[nf] = M_f (DF exponent,
+ *   P:174; 2 per 2D segment, 3 per triangle, 4 per quad), patch_kind[n_patches]
+ *   (GMG_FARFIELD ...).  part[n] = global cell -> rank (NULL if nranks == 1).
+ * Validates indices, manifoldness and per-cell closure |sum sigma A| <=
+ * 1e-10 sum S -> GMG_ETOPO. */
+gmg_status gmg_load_mesh(gmg_ctx *ctx, int64_t n_cells, const double *vol, const double *centroid,
+                         int64_t n_faces, const int64_t *left, const int64_t *right,
+                         const double *area_vec, const double *face_ctr, const int8_t *n_gauss,
+                         int n_patches, const int32_t *patch_kind, const int32_t *part);
+
+/* a2: optional user coloring of the FINE level (host, natural order, colors
+ * 1..Nc).  NULL = Algorithm 1.  Must precede
+ * gmg_build_hierarchy.  GMG_ECOLOR if two face neighbours share a color. */
+gmg_status gmg_set_coloring(gmg_ctx *ctx, int level, const int32_t *color);
+
+/* a2-a5: build up to n_levels levels: per level Algorithm-1 coloring
+ * (reading A24), color-contiguous renumbering (stable sort by
+ * (color, natural id)), then hash/skewness agglomeration (Algorithm 3,
+ * P:577-627, readings A18-A23) to the next level.  *n_levels_built = levels
+ * built.  Returns GMG_ESTALL (hierarchy usable, truncated) if a level merged
+ * nothing.  Host-only; deterministic, bit-identical to the oracle's maps. */
+gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built);
+
+gmg_status gmg_get_level_info(gmg_ctx *ctx, int level, int64_t *n_cells, int *n_colors, int64_t *n_faces);
+
+/* Host outputs (any may be NULL): color[n] (1..Nc, natural order),
+ * perm[n] (internal position -> natural id), parent[n] (natural id of the
+ * coarse cell on level+1, natural numbering of that level; -1 on the
+ * coarsest level). */
+gmg_status gmg_get_maps(gmg_ctx *ctx, int level, int32_t *color, int64_t *perm, int64_t *parent);
+
+/* Coarse-level geometry as built (host, natural order of that level):
+ * vol[n], left/right[nf], area_vec[dim][nf], face_ctr[dim][nf], n_gauss[nf];
+ * any may be NULL. */
+gmg_status gmg_get_level_geometry(gmg_ctx *ctx, int level, double *vol, double *centroid, int64_t *left,
+                                  int64_t *right, double *area_vec, double *face_ctr, int8_t *n_gauss);
+
+/* Device workspace: query bytes after gmg_build_hierarchy, then hand over a
+ * device buffer of at least that size (16-byte aligned).  Uploads the
+ * static level data (asynchronous on the stream). */
+size_t gmg_workspace_bytes(gmg_ctx *ctx);
+gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes);
+
+/* Fine state W[nv][n] (natural order, host/device) and the free-stream /
+ * farfield state W_inf[nv] (host). */
+gmg_status gmg_set_state(gmg_ctx *ctx, const double *W, const double *W_inf);
+/* State of any level (tests): W[nv][n_level] natural order, host/device. */
+gmg_status gmg_set_level_state(gmg_ctx *ctx, int level, const double *W);
+/* W_out[nv][n_level] natural order (host/device).  For a coarse level after
+ * a V-cycle this is W0 + dW before prolongation. */
+gmg_status gmg_get_state(gmg_ctx *ctx, int level, double *W_out);
+
+/* df_mode 1: fine-level DF alpha[n] (natural order, host/device). */
+gmg_status gmg_set_alpha(gmg_ctx *ctx, const double *alpha);
+
+/* a6 + a10: residual R_l(W_l) = sum_f sigma S_f F_f (first-order KFVS, O4;
+ * flux sum, reading A4) with BC ghosts, the DF helper alpha_i = prod
+ * alpha_f^{M_f} (O5), r_f and Sigma_i (O6).  Outputs natural order,
+ * nullable: R_out[nv][n], alpha_out[n], sigma_out[n]. */
+gmg_status gmg_residual(gmg_ctx *ctx, int level, double *R_out, double *alpha_out, double *sigma_out);
+
+/* Tests: set the right-hand side Rt[nv][n] and alpha[n] of a level
+ * (natural order, host/device) used by the next gmg_smooth. */
+gmg_status gmg_set_level_inputs(gmg_ctx *ctx, int level, const double *Rt, const double *alpha);
+
+/* a10-a12: one smoothing step on `level` (O7): prepare r_f, Sigma, D at the
+ * level's current W with its alpha (readings A2, A3, A5, A6), then n_sweeps
+ * x (forward colors 1..Nc, backward Nc..1) of Eq.(gpu-forward-relaxation) /
+ * Eq.(gpu-backward-relaxation) (Algorithm 2, readings
+ * A1, A7), RHS = the level's Rt.  dW_out[nv][n] (natural order,
+ * host/device, nullable).  W is NOT updated. */
+gmg_status gmg_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out);
+
+/* a6-a16: n_cycles V-cycles (O8: fine explicit pre-smooth P:638-641,
+ * restriction P:643-652, forcing P:662-665, coarse MC-LU-SGS, DF-limited
+ * prolongation P:672-678; pre = 1, post = 0).  res_hist (host,
+ * nullable) receives [n_cycles+1][nv] L2 norms of the fine residual
+ * components at each cycle start plus one final entry (reading A26).
+ * Captured once as a CUDA graph and replayed.  GMG_ENONFINITE if the
+ * history is not finite. */
+gmg_status gmg_vcycle(gmg_ctx *ctx, int n_cycles, double *res_hist);
+
+/* Instrumentation for bench.py: run n_cycles V-cycles launching kernels
+ * individually with CUDA events around every launch; ms_out[k] / count_out[k]
+ * receive the summed device time and launch count of kernel class k
+ * (GMG_K_* below).  bytes_out[k] = algorithmic bytes moved by class k over
+ * the run.  Arrays of length GMG_K_COUNT. */
+enum { GMG_K_FACE = 0, GMG_K_GATHER = 1, GMG_K_SWEEP = 2, GMG_K_RESTRICT = 3, GMG_K_PROLONG = 4,
+       GMG_K_NORM = 5, GMG_K_COUNT = 6 };
+gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_t *count_out, double *bytes_out);
+
+/* Sweep-only instrumentation: time one smoothing step's sweeps on `level`
+ * (graph-replayed `reps` times); *ms = total device ms, *cell_updates =
+ * N_l * 2 * n_sweeps * reps, *bytes = algorithmic bytes. */
+gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, double *ms, double *cell_updates,
+                           double *bytes);
+
+/* Number of kernels one V-cycle launches (graph nodes). */
+int64_t gmg_vcycle_launches(gmg_ctx *ctx);
+
+const char *gmg_last_error(gmg_ctx *ctx); /* valid until the next call on ctx */
+void gmg_destroy(gmg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMG_H */

@@ -1,0 +1,60 @@
+"""Build libgmg.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+Host setup (setup.cpp) is compiled by g++ with -ffp-contract=off so the
+agglomeration's floating-point decisions follow SURVEY §8(c) O3 exactly;
+device code by nvcc -gencode arch=compute_100a,code=sm_100a.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libgmg.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _run(cmd):
+    print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+
+
+def sources():
+    return [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))
+            if f.endswith((".cpp", ".cu", ".cuh", ".h"))] + [os.path.join(HERE, "..", "include", "gmg.h")]
+
+
+def needs_build() -> bool:
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    return any(os.path.getmtime(s) > t for s in sources())
+
+
+def build(force: bool = False, verbose_ptxas: bool = False) -> str:
+    if not force and not needs_build():
+        return OUT
+    bdir = os.path.join(HERE, "build")
+    os.makedirs(bdir, exist_ok=True)
+    inc = ["-I", os.path.join(CUDA, "include"), "-I", os.path.join(HERE, "..", "include")]
+    o_setup = os.path.join(bdir, "setup.o")
+    _run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall", "-c",
+          os.path.join(CSRC, "setup.cpp"), "-o", o_setup] + inc)
+    o_api = os.path.join(bdir, "api.o")
+    flags = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+                       "--expt-relaxed-constexpr"]
+    if verbose_ptxas:
+        flags += ["-Xptxas", "-v"]
+    _run([NVCC] + flags + ["-c", os.path.join(CSRC, "api.cu"), "-o", o_api] + inc)
+    tmp = OUT + ".tmp"
+    _run([NVCC] + GENCODE + ["-shared", "-o", tmp, o_setup, o_api, "-cudart", "static"])
+    os.replace(tmp, OUT)
+    return OUT
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)

@@ -1,0 +1,814 @@
+// api.cu -- the C ABI of libgmg (include/gmg.h): context, workspace, data
+// movement, kernel orchestration of residual / smoothing / V-cycle and its
+// CUDA-graph capture.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+
+#include "gmg_internal.h"
+#include "kernels.cuh"
+
+using namespace gmg;
+
+#define CK(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            ctx->err = std::string(#x) + ": " + cudaGetErrorString(e_);               \
+            return GMG_ECUDA;                                                         \
+        }                                                                             \
+    } while (0)
+
+namespace {
+
+inline int nblk(int64_t n, int b = 256) { return (int)((n + b - 1) / b); }
+
+Phys phys(const gmg_ctx *ctx)
+{
+    Phys p;
+    p.gamma = ctx->opt.gamma;
+    p.gm1 = ctx->opt.gamma - 1.0;
+    p.K = ctx->opt.dim == 3 ? (5.0 - 3.0 * p.gamma) / (p.gamma - 1.0) : (4.0 - 2.0 * p.gamma) / (p.gamma - 1.0);
+    p.omega = ctx->opt.r_factor;
+    return p;
+}
+
+BCs bcs(const gmg_ctx *ctx)
+{
+    BCs b;
+    for (int q = 0; q < 5; ++q) b.winf[q] = ctx->winf[q];
+    for (int k = 0; k < 16; ++k) b.kind[k] = k < (int)ctx->patch_kind.size() ? ctx->patch_kind[k] : 0;
+    return b;
+}
+
+// --------------------------------------------------------------------------
+// launch bookkeeping: algorithmic bytes and optional per-launch CUDA events
+// --------------------------------------------------------------------------
+struct Launcher {
+    gmg_ctx *ctx;
+    cudaStream_t s;
+    void pre(int) {
+        if (ctx->prof.on) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, s);
+            ctx->prof.ev.push_back(e);
+        }
+    }
+    void post(int cls, double bytes) {
+        ctx->launches++;
+        ctx->kbytes[cls] += bytes;
+        if (ctx->prof.on) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, s);
+            ctx->prof.ev.push_back(e);
+            ctx->prof.marks.push_back({cls, (int)ctx->prof.ev.size() - 2});
+        }
+    }
+};
+
+template <int D>
+void enqueue_face(Launcher &Lc, int l, const double *W, bool flux)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    DevLevel &L = ctx->dv[l];
+    Lc.pre(GMG_K_FACE);
+    if (flux) k_face<D, true><<<nblk(L.nf), 256, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+    else k_face<D, false><<<nblk(L.nf), 256, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+    Lc.post(GMG_K_FACE, flux ? ctx->lbytes[l].face_flux : ctx->lbytes[l].face_prep);
+}
+
+template <int D>
+void enqueue_gather(Launcher &Lc, int l, int flags, double *Wexp)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    DevLevel &L = ctx->dv[l];
+    GArgs a{flags, ctx->opt.cfl_imp, ctx->opt.cfl_exp, Wexp, L.partial};
+    Lc.pre(GMG_K_GATHER);
+    k_gather<D><<<nblk(L.n), 256, 0, Lc.s>>>(L, a);
+    Lc.post(GMG_K_GATHER, ctx->lbytes[l].gather);
+    if (flags & G_NORM) {
+        Lc.pre(GMG_K_NORM);
+        k_norm_final<<<1, 256, 0, Lc.s>>>(L.partial, nblk(L.n), L.nv, ctx->d_hist, ctx->hist_cap, ctx->d_flag);
+        Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
+    }
+}
+
+template <int D>
+void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, const double *Wlin, const double *rhs, double *Wout)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    DevLevel &L = ctx->dv[l];
+    const HostLevel &H = ctx->lv[l];
+    const double gm1 = ctx->opt.gamma - 1.0;
+    for (int s = 0; s < n_sweeps; ++s) {
+        for (int half = 0; half < 2; ++half) {
+            for (int cc = 0; cc < H.ncolor; ++cc) {
+                const int c = half == 0 ? cc : H.ncolor - 1 - cc;     // Algorithm 2
+                const int cbeg = (int)H.blk[c], cend = (int)H.blk[c + 1];
+                const bool last = (s == n_sweeps - 1) && half == 1;
+                double *wo = last ? Wout : nullptr;
+                Lc.pre(GMG_K_SWEEP);
+                k_sweep<D><<<nblk(cend - cbeg), 256, 0, Lc.s>>>(L, cbeg, cend, gm1, Wlin, rhs, wo);
+                Lc.post(GMG_K_SWEEP, ctx->lbytes[l].sweep[c] + (wo ? ctx->lbytes[l].sweep_out[c] : 0.0));
+            }
+        }
+    }
+}
+
+template <int D>
+void enqueue_restrict(Launcher &Lc, int l)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    DevLevel &C = ctx->dv[l];
+    DevLevel &Fn = ctx->dv[l - 1];
+    Lc.pre(GMG_K_RESTRICT);
+    k_restrict<D><<<nblk(C.n), 256, 0, Lc.s>>>(C, Fn, Fn.W, Fn.Rt);
+    Lc.post(GMG_K_RESTRICT, ctx->lbytes[l].restrict_);
+}
+
+// O8 -- one V-cycle, all on the device
+template <int D>
+void enqueue_vcycle(Launcher &Lc)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    const int nl = (int)ctx->dv.size();
+    DevLevel &L0 = ctx->dv[0];
+    const bool df0 = ctx->opt.df_mode == 0;
+    // 1-2. fine residual at the cycle start (history entry) + fine pre-smoothing
+    enqueue_face<D>(Lc, 0, L0.W, true);
+    if (ctx->opt.fine_smoother == 0) {
+        enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_EXPLICIT, L0.W);         // Eq.(smo), A9
+    } else {
+        enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | (df0 ? G_ALPHA : 0), nullptr);
+        enqueue_sweeps<D>(Lc, 0, ctx->opt.n_sweeps, L0.W, L0.Rt, nullptr);
+        Lc.pre(GMG_K_SWEEP);
+        k_update<D><<<nblk((int64_t)L0.n * (D + 2)), 256, 0, Lc.s>>>(L0.n, L0.W, L0.dW);
+        Lc.post(GMG_K_SWEEP, ctx->lbytes[0].update);
+    }
+    if (nl == 1) return;
+    // 3. residual at the smoothed state (A10) -> restricted
+    enqueue_face<D>(Lc, 0, L0.W, true);
+    enqueue_gather<D>(Lc, 0, G_FLUX | G_WRITE_RT | (df0 ? G_ALPHA : 0), nullptr);
+    // 4. coarse levels
+    for (int l = 1; l < nl; ++l) {
+        DevLevel &C = ctx->dv[l];
+        const bool last = (l == nl - 1);
+        enqueue_restrict<D>(Lc, l);                                       // W0, Res*, alpha, dW = 0
+        enqueue_face<D>(Lc, l, C.W0, !last);                              // R(W0) only if F is needed later
+        enqueue_gather<D>(Lc, l, (last ? 0 : (G_FLUX | G_SET_F)) | G_PREPARE, nullptr);
+        enqueue_sweeps<D>(Lc, l, ctx->opt.n_sweeps, C.W0, C.Rs, C.W);    // RHS = Res* (A8)
+        if (!last) {
+            enqueue_face<D>(Lc, l, C.W, true);
+            enqueue_gather<D>(Lc, l, G_FLUX | G_WRITE_RT | G_ADD_F, nullptr);   // Rt = R(W) + F (A11)
+        }
+    }
+    // 5. DF-limited prolongation 2 -> 1 -> 0 (fused)
+    Lc.pre(GMG_K_PROLONG);
+    k_prolong<D><<<nblk(L0.n), 256, 0, Lc.s>>>(L0, ctx->dv[1], nl >= 3 ? ctx->dv[2] : ctx->dv[1], nl);
+    Lc.post(GMG_K_PROLONG, ctx->lbytes[0].prolong);
+}
+
+// final history entry: residual at the end state
+template <int D>
+void enqueue_final_norm(Launcher &Lc)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    enqueue_face<D>(Lc, 0, ctx->dv[0].W, true);
+    enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM, nullptr);
+}
+
+gmg_status check_ready(gmg_ctx *ctx, bool need_state = true)
+{
+    if (!ctx->built) { ctx->err = "hierarchy not built"; return GMG_ESTATE; }
+    if (!ctx->ws_ready) { ctx->err = "workspace not set"; return GMG_ESTATE; }
+    if (need_state && !ctx->state_set) { ctx->err = "state not set"; return GMG_ESTATE; }
+    return GMG_OK;
+}
+
+// copy natural SoA (host or device) into internal AoS
+gmg_status put_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, double *dst)
+{
+    const int64_t n = ctx->lv[l].n;
+    CK(cudaMemcpyAsync(ctx->d_stage, src, sizeof(double) * ncomp * n, cudaMemcpyDefault, ctx->stream));
+    k_to_internal<<<nblk(n), 256, 0, ctx->stream>>>((int)n, ncomp, ctx->dv[l].perm, ctx->d_stage, dst);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));   // caller's host buffer may be released on return
+    return GMG_OK;
+}
+
+gmg_status get_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, double *dst)
+{
+    const int64_t n = ctx->lv[l].n;
+    k_to_natural<<<nblk(n), 256, 0, ctx->stream>>>((int)n, ncomp, ctx->dv[l].perm, src, ctx->d_stage);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(dst, ctx->d_stage, sizeof(double) * ncomp * n, cudaMemcpyDefault, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GMG_OK;
+}
+
+// ----------------------------------------------------------------- workspace
+struct Bump {
+    char *base;
+    size_t off = 0;
+    template <class T>
+    T *take(size_t count)
+    {
+        off = (off + 255) & ~(size_t)255;
+        T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += count * sizeof(T) + 16;
+        return p;
+    }
+};
+
+void carve(gmg_ctx *ctx, Bump &b)
+{
+    const int d = ctx->opt.dim, nv = d + 2;
+    const int nl = (int)ctx->lv.size();
+    ctx->dv.assign(nl, DevLevel{});
+    int64_t nmax = 0;
+    for (int l = 0; l < nl; ++l) {
+        const HostLevel &H = ctx->lv[l];
+        DevLevel &L = ctx->dv[l];
+        nmax = std::max(nmax, std::max(H.n, H.nf));
+        L.dim = d; L.nv = nv; L.ncolor = H.ncolor;
+        L.n = (int)H.n; L.nf = (int)H.nf; L.nchunks = (int)H.nchunks;
+        L.fl = b.take<int>(H.nf); L.fr = b.take<int>(H.nf);
+        L.fA = b.take<double>((size_t)d * H.nf); L.fM = b.take<int8_t>(H.nf);
+        L.Fs = b.take<double>((size_t)nv * H.nf); L.Srf = b.take<double>(H.nf); L.aM = b.take<double>(H.nf);
+        L.vol = b.take<double>(H.n);
+        L.W = b.take<double>((size_t)nv * H.n); L.W0 = b.take<double>((size_t)nv * H.n);
+        L.dW = b.take<double>((size_t)nv * H.n); L.Rt = b.take<double>((size_t)nv * H.n);
+        L.Rs = b.take<double>((size_t)nv * H.n); L.F = b.take<double>((size_t)nv * H.n);
+        L.alpha = b.take<double>(H.n); L.sigma = b.take<double>(H.n);
+        L.invD = b.take<double>(H.n); L.ha = b.take<double>(H.n);
+        L.deg_int = b.take<uint8_t>(H.n); L.deg_all = b.take<uint8_t>(H.n);
+        L.gbase = b.take<int>(H.n); L.sbase = b.take<int>(H.n);
+        L.gface = b.take<int>(H.ng_entries); L.snbr = b.take<int>(H.ns_entries);
+        L.sA = b.take<double>((size_t)d * H.ns_entries); L.sSr = b.take<double>(H.ns_entries);
+        L.ns_entries = (int)H.ns_entries;
+        L.perm = b.take<int>(H.n);
+        L.child = l > 0 ? b.take<int>(2 * H.n) : nullptr;
+        L.parent = l + 1 < nl ? b.take<int>(H.n) : nullptr;
+        L.partial = b.take<double>((size_t)nblk(H.n) * nv);
+    }
+    ctx->d_stage = b.take<double>((size_t)nv * nmax);
+    ctx->hist_cap = 4096;
+    ctx->d_hist = b.take<double>((size_t)ctx->hist_cap * nv);
+    ctx->d_flag = b.take<int>(4);
+}
+
+void compute_bytes(gmg_ctx *ctx)
+{
+    const int d = ctx->opt.dim, nv = d + 2;
+    const int nl = (int)ctx->lv.size();
+    ctx->lbytes.assign(nl, LevelBytes{});
+    for (int l = 0; l < nl; ++l) {
+        const HostLevel &H = ctx->lv[l];
+        LevelBytes &B = ctx->lbytes[l];
+        int64_t nint = 0;
+        for (int64_t f = 0; f < H.nf; ++f) nint += H.right[f] >= 0;
+        const double nb = (double)(H.nf - nint);
+        // face: cells' W (interior 2, boundary 1), A, l/r, M; writes S F, S r, alpha^M
+        const double face_in = (double)nint * 2 * nv * 8 + nb * nv * 8 + (double)H.nf * (d * 8 + 8 + 1);
+        B.face_flux = face_in + (double)H.nf * (nv * 8 + 16);
+        B.face_prep = face_in + (double)H.nf * 8;
+        // gather: per slot the face id + S F + S r + alpha^M; per cell bases/degrees + outputs (~2 nv arrays)
+        double slots = 0;
+        for (int64_t i = 0; i < H.n; ++i) slots += H.deg_all[i];
+        B.gather = slots * (4 + nv * 8 + 16) + (double)H.n * (10 + 2 * nv * 8);
+        // sweep (compulsory): own Rt, 1/D, alpha/2, dW write; neighbour-unique W, dW;
+        // face data (A, S r) once per face + 4 B per slot
+        B.sweep.assign(H.ncolor, 0.0);
+        B.sweep_out.assign(H.ncolor, 0.0);
+        for (int c = 0; c < H.ncolor; ++c) {
+            double s = 0;
+            for (int64_t i = H.blk[c]; i < H.blk[c + 1]; ++i)
+                s += (2 * nv * 8 + 16) + 2 * nv * 8 + H.deg_int[i] * ((d + 1) * 8 / 2.0 + 4);
+            B.sweep[c] = s;
+            B.sweep_out[c] = (double)(H.blk[c + 1] - H.blk[c]) * 2 * nv * 8;
+        }
+        B.restrict_ = l > 0 ? (double)ctx->lv[l - 1].n * (2 * nv * 8 + 16) + (double)H.n * (3 * nv * 8 + 8 + 8) : 0;
+        B.prolong = (double)H.n * (2 * nv * 8 + 8 + 4) + (nl > 1 ? (double)ctx->lv[1].n * (nv * 8 + 12) : 0) +
+                    (nl > 2 ? (double)ctx->lv[2].n * nv * 8 : 0);
+        B.update = (double)H.n * 3 * nv * 8;
+    }
+}
+
+}  // namespace
+
+// =============================================================================
+// ABI
+// =============================================================================
+extern "C" {
+
+void gmg_default_options(gmg_options *o)
+{
+    std::memset(o, 0, sizeof(*o));
+    o->dim = 3;
+    o->gamma = 1.4;
+    o->cfl_imp = 10.0;
+    o->cfl_exp = 0.5;
+    o->n_sweeps = 6;
+    o->n_levels = 3;
+    o->pre_smooth = 1;
+    o->post_smooth = 0;
+    o->skew_limit = 0.5;
+    o->r_factor = 1.0;
+    o->fine_smoother = 0;
+    o->df_mode = 0;
+    o->rank = 0;
+    o->nranks = 1;
+    o->nccl_id = nullptr;
+    o->device = 0;
+    o->stream = nullptr;
+}
+
+gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
+{
+    if (!opt || !out) return GMG_EINVAL;
+    *out = nullptr;
+    if ((opt->dim != 2 && opt->dim != 3) || !(opt->gamma > 1.0) || !(opt->cfl_imp > 0) || !(opt->cfl_exp > 0) ||
+        opt->n_sweeps < 1 || opt->n_levels < 1 || opt->n_levels > 3 || opt->pre_smooth != 1 || opt->post_smooth != 0 ||
+        !(opt->r_factor >= 1.0) || opt->fine_smoother < 0 || opt->fine_smoother > 1 || opt->df_mode < 0 ||
+        opt->df_mode > 2 || opt->nranks < 1 || opt->rank < 0 || opt->rank >= opt->nranks)
+        return GMG_EINVAL;
+    if (opt->nranks > 1) return GMG_EINVAL;   // multi-rank path: see DESIGN.md (not in this build)
+    gmg_ctx *ctx = new (std::nothrow) gmg_ctx();
+    if (!ctx) return GMG_ENOMEM;
+    ctx->opt = *opt;
+    ctx->stream = (cudaStream_t)opt->stream;
+    *out = ctx;
+    return GMG_OK;
+}
+
+gmg_status gmg_load_mesh(gmg_ctx *ctx, int64_t n_cells, const double *vol, const double *centroid, int64_t n_faces,
+                         const int64_t *left, const int64_t *right, const double *area_vec, const double *face_ctr,
+                         const int8_t *n_gauss, int n_patches, const int32_t *patch_kind, const int32_t *part)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (n_cells < 1 || n_faces < 1 || !vol || !centroid || !left || !right || !area_vec || !face_ctr || !n_gauss ||
+        n_patches < 0 || n_patches > 16 || (n_patches > 0 && !patch_kind) || n_cells >= INT32_MAX / 8 ||
+        n_faces >= INT32_MAX / 8) {
+        ctx->err = "gmg_load_mesh: bad arguments";
+        return GMG_EINVAL;
+    }
+    ctx->n_patches = n_patches;
+    ctx->patch_kind.assign(patch_kind, patch_kind + n_patches);
+    for (int k = 0; k < n_patches; ++k)
+        if (patch_kind[k] < 0 || patch_kind[k] > 3) { ctx->err = "bad patch kind"; return GMG_EINVAL; }
+    gmg_status st = load_mesh(ctx, n_cells, vol, centroid, n_faces, left, right, area_vec, face_ctr, n_gauss, part);
+    if (st != GMG_OK) return st;
+    ctx->mesh_loaded = true;
+    ctx->built = ctx->ws_ready = ctx->state_set = false;
+    return GMG_OK;
+}
+
+gmg_status gmg_set_coloring(gmg_ctx *ctx, int level, const int32_t *color)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->mesh_loaded || ctx->built) { ctx->err = "set_coloring must follow load_mesh and precede build"; return GMG_ESTATE; }
+    if (level != 0) { ctx->err = "only the fine level accepts a user coloring"; return GMG_EINVAL; }
+    if (!color) { ctx->user_color0.clear(); return GMG_OK; }
+    std::vector<int32_t> c(color, color + ctx->lv[0].n);
+    if (!validate_coloring(ctx->lv[0], c)) { ctx->err = "invalid coloring: face neighbours share a color or color < 1"; return GMG_ECOLOR; }
+    ctx->user_color0 = std::move(c);
+    return GMG_OK;
+}
+
+gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->mesh_loaded) { ctx->err = "mesh not loaded"; return GMG_ESTATE; }
+    if (n_levels < 1 || n_levels > 3) { ctx->err = "n_levels must be 1..3"; return GMG_EINVAL; }
+    gmg_status ret = GMG_OK;
+    try {
+        ctx->lv.resize(1);
+        for (int l = 0;; ++l) {
+            HostLevel &H = ctx->lv[l];
+            if (l == 0 && !ctx->user_color0.empty()) {
+                H.color = ctx->user_color0;
+                H.ncolor = *std::max_element(H.color.begin(), H.color.end());
+            } else {
+                color_level(H);
+            }
+            renumber(H);
+            build_layout(H);
+            H.parent.clear();
+            if (l + 1 >= n_levels) break;
+            std::vector<int64_t> parent;
+            int64_t nc = 0;
+            const int64_t merged = agglomerate(H, ctx->opt.skew_limit, parent, nc);
+            if (merged == 0) {
+                ret = GMG_ESTALL;
+                ctx->err = "level " + std::to_string(l) + " merged nothing; hierarchy truncated";
+                break;
+            }
+            H.parent = std::move(parent);
+            H.n_coarse = nc;
+            HostLevel C;
+            build_coarse(ctx->lv[l], C);
+            ctx->lv.push_back(std::move(C));
+        }
+    } catch (const std::exception &e) {
+        ctx->err = e.what();
+        return GMG_ETOPO;
+    }
+    ctx->built = true;
+    ctx->ws_ready = ctx->state_set = false;
+    if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+    if (n_levels_built) *n_levels_built = (int)ctx->lv.size();
+    compute_bytes(ctx);
+    return ret;
+}
+
+gmg_status gmg_get_level_info(gmg_ctx *ctx, int level, int64_t *n_cells, int *n_colors, int64_t *n_faces)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->built) { ctx->err = "hierarchy not built"; return GMG_ESTATE; }
+    if (level < 0 || level >= (int)ctx->lv.size()) { ctx->err = "bad level"; return GMG_EINVAL; }
+    const HostLevel &H = ctx->lv[level];
+    if (n_cells) *n_cells = H.n;
+    if (n_colors) *n_colors = H.ncolor;
+    if (n_faces) *n_faces = H.nf;
+    return GMG_OK;
+}
+
+gmg_status gmg_get_maps(gmg_ctx *ctx, int level, int32_t *color, int64_t *perm, int64_t *parent)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->built) { ctx->err = "hierarchy not built"; return GMG_ESTATE; }
+    if (level < 0 || level >= (int)ctx->lv.size()) { ctx->err = "bad level"; return GMG_EINVAL; }
+    const HostLevel &H = ctx->lv[level];
+    if (color) std::copy(H.color.begin(), H.color.end(), color);
+    if (perm) std::copy(H.perm.begin(), H.perm.end(), perm);
+    if (parent) {
+        if (H.parent.empty()) std::fill(parent, parent + H.n, (int64_t)-1);
+        else std::copy(H.parent.begin(), H.parent.end(), parent);
+    }
+    return GMG_OK;
+}
+
+gmg_status gmg_get_level_geometry(gmg_ctx *ctx, int level, double *vol, double *centroid, int64_t *left,
+                                  int64_t *right, double *area_vec, double *face_ctr, int8_t *n_gauss)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->built) { ctx->err = "hierarchy not built"; return GMG_ESTATE; }
+    if (level < 0 || level >= (int)ctx->lv.size()) { ctx->err = "bad level"; return GMG_EINVAL; }
+    const HostLevel &H = ctx->lv[level];
+    if (vol) std::copy(H.vol.begin(), H.vol.end(), vol);
+    if (centroid) std::copy(H.ctr.begin(), H.ctr.end(), centroid);
+    if (left) std::copy(H.left.begin(), H.left.end(), left);
+    if (right) std::copy(H.right.begin(), H.right.end(), right);
+    if (area_vec) std::copy(H.avec.begin(), H.avec.end(), area_vec);
+    if (face_ctr) std::copy(H.fctr.begin(), H.fctr.end(), face_ctr);
+    if (n_gauss) std::copy(H.ngauss.begin(), H.ngauss.end(), n_gauss);
+    return GMG_OK;
+}
+
+size_t gmg_workspace_bytes(gmg_ctx *ctx)
+{
+    if (!ctx || !ctx->built) return 0;
+    Bump b{nullptr};
+    carve(ctx, b);
+    return b.off + 256;
+}
+
+gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->built) { ctx->err = "hierarchy not built"; return GMG_ESTATE; }
+    if (!dptr || ((uintptr_t)dptr & 15)) { ctx->err = "workspace must be a 16-byte aligned device pointer"; return GMG_EINVAL; }
+    const size_t need = gmg_workspace_bytes(ctx);
+    if (bytes < need) { ctx->err = "workspace too small: need " + std::to_string(need); return GMG_ENOMEM; }
+    CK(cudaSetDevice(ctx->opt.device));
+    Bump b{(char *)dptr};
+    carve(ctx, b);
+    ctx->ws = dptr;
+    ctx->ws_bytes = bytes;
+    const int d = ctx->opt.dim, nv = d + 2;
+    const int nl = (int)ctx->lv.size();
+    std::vector<std::vector<int>> ki;          // host staging kept alive until the sync
+    std::vector<std::vector<double>> kd;
+    auto up_i = [&](const int *dst, std::vector<int> v) -> cudaError_t {
+        ki.push_back(std::move(v));
+        return cudaMemcpyAsync((void *)dst, ki.back().data(), ki.back().size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream);
+    };
+    auto up_raw = [&](const void *dst, const void *src, size_t bytes_) -> cudaError_t {
+        return cudaMemcpyAsync((void *)dst, src, bytes_, cudaMemcpyHostToDevice, ctx->stream);
+    };
+    for (int l = 0; l < nl; ++l) {
+        const HostLevel &H = ctx->lv[l];
+        DevLevel &L = ctx->dv[l];
+        std::vector<int> fl(H.nf), fr(H.nf);
+        for (int64_t f = 0; f < H.nf; ++f) {
+            fl[f] = (int)H.iperm[H.left[f]];
+            fr[f] = H.right[f] >= 0 ? (int)H.iperm[H.right[f]] : (int)H.right[f];
+        }
+        CK(up_i(L.fl, std::move(fl)));
+        CK(up_i(L.fr, std::move(fr)));
+        CK(up_raw(L.fA, H.avec.data(), H.avec.size() * sizeof(double)));
+        CK(up_raw(L.fM, H.ngauss.data(), H.ngauss.size()));
+        std::vector<double> vol(H.n);
+        for (int64_t i = 0; i < H.n; ++i) vol[i] = H.vol[H.perm[i]];
+        kd.push_back(std::move(vol));
+        CK(up_raw(L.vol, kd.back().data(), H.n * sizeof(double)));
+        CK(up_raw(L.deg_int, H.deg_int.data(), H.n));
+        CK(up_raw(L.deg_all, H.deg_all.data(), H.n));
+        CK(up_raw(L.gbase, H.gbase.data(), H.n * sizeof(int)));
+        CK(up_raw(L.sbase, H.sbase.data(), H.n * sizeof(int)));
+        CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
+        CK(up_raw(L.snbr, H.snbr.data(), H.snbr.size() * sizeof(int)));
+        CK(up_raw(L.sA, H.sA.data(), H.sA.size() * sizeof(double)));
+        std::vector<int> perm(H.n);
+        for (int64_t i = 0; i < H.n; ++i) perm[i] = (int)H.perm[i];
+        CK(up_i(L.perm, std::move(perm)));
+        if (l > 0) {
+            const HostLevel &Fh = ctx->lv[l - 1];
+            std::vector<int> child(2 * H.n, -1);
+            for (int64_t i = 0; i < Fh.n; ++i) {              // ascending natural id of the fine cell
+                const int64_t c = H.iperm[Fh.parent[i]];
+                if (child[c] < 0) child[c] = (int)Fh.iperm[i];
+                else child[H.n + c] = (int)Fh.iperm[i];
+            }
+            CK(up_i(L.child, std::move(child)));
+        }
+        if (l + 1 < nl) {
+            const HostLevel &Ch = ctx->lv[l + 1];
+            std::vector<int> par(H.n);
+            for (int64_t i = 0; i < H.n; ++i) par[i] = (int)Ch.iperm[H.parent[H.perm[i]]];
+            CK(up_i(L.parent, std::move(par)));
+        }
+        // alpha = 1 until set (df_mode 2 keeps it)
+        k_fill<<<nblk(H.n), 256, 0, ctx->stream>>>((int)H.n, L.alpha, 1.0);
+        CK(cudaMemsetAsync(L.dW, 0, sizeof(double) * nv * H.n, ctx->stream));
+    }
+    CK(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), ctx->stream));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+    ctx->ws_ready = true;
+    ctx->state_set = false;
+    return GMG_OK;
+}
+
+gmg_status gmg_set_state(gmg_ctx *ctx, const double *W, const double *W_inf)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (!W || !W_inf) { ctx->err = "null state"; return GMG_EINVAL; }
+    const int nv = ctx->opt.dim + 2;
+    for (int q = 0; q < nv; ++q) ctx->winf[q] = W_inf[q];
+    if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }   // BC values are kernel params
+    st = put_natural(ctx, 0, W, nv, ctx->dv[0].W);
+    if (st) return st;
+    ctx->state_set = true;
+    return GMG_OK;
+}
+
+gmg_status gmg_set_level_state(gmg_ctx *ctx, int level, const double *W)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (level < 0 || level >= (int)ctx->lv.size() || !W) { ctx->err = "bad level / null"; return GMG_EINVAL; }
+    st = put_natural(ctx, level, W, ctx->opt.dim + 2, ctx->dv[level].W);
+    if (st) return st;
+    if (level == 0) ctx->state_set = true;
+    return GMG_OK;
+}
+
+gmg_status gmg_get_state(gmg_ctx *ctx, int level, double *W_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (level < 0 || level >= (int)ctx->lv.size() || !W_out) { ctx->err = "bad level / null"; return GMG_EINVAL; }
+    return get_natural(ctx, level, ctx->dv[level].W, ctx->opt.dim + 2, W_out);
+}
+
+gmg_status gmg_set_alpha(gmg_ctx *ctx, const double *alpha)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (!alpha) { ctx->err = "null alpha"; return GMG_EINVAL; }
+    return put_natural(ctx, 0, alpha, 1, ctx->dv[0].alpha);
+}
+
+gmg_status gmg_residual(gmg_ctx *ctx, int level, double *R_out, double *alpha_out, double *sigma_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, level == 0);
+    if (st) return st;
+    if (level < 0 || level >= (int)ctx->lv.size()) { ctx->err = "bad level"; return GMG_EINVAL; }
+    Launcher Lc{ctx, ctx->stream};
+    DevLevel &L = ctx->dv[level];
+    // alpha is written to the Rs/F-free scratch "sigma" path: keep the level's alpha intact
+    double *save_alpha = L.alpha;
+    L.alpha = L.invD;   // scratch (invD is recomputed by every prepare)
+    if (ctx->opt.dim == 2) {
+        enqueue_face<2>(Lc, level, L.W, true);
+        enqueue_gather<2>(Lc, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
+    } else {
+        enqueue_face<3>(Lc, level, L.W, true);
+        enqueue_gather<3>(Lc, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
+    }
+    L.alpha = save_alpha;
+    CK(cudaGetLastError());
+    const int nv = ctx->opt.dim + 2;
+    if (R_out) { st = get_natural(ctx, level, L.Rt, nv, R_out); if (st) return st; }
+    if (alpha_out) { st = get_natural(ctx, level, L.invD, 1, alpha_out); if (st) return st; }
+    if (sigma_out) { st = get_natural(ctx, level, L.sigma, 1, sigma_out); if (st) return st; }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GMG_OK;
+}
+
+gmg_status gmg_set_level_inputs(gmg_ctx *ctx, int level, const double *Rt, const double *alpha)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (level < 0 || level >= (int)ctx->lv.size()) { ctx->err = "bad level"; return GMG_EINVAL; }
+    if (Rt) { st = put_natural(ctx, level, Rt, ctx->opt.dim + 2, ctx->dv[level].Rt); if (st) return st; }
+    if (alpha) { st = put_natural(ctx, level, alpha, 1, ctx->dv[level].alpha); if (st) return st; }
+    return GMG_OK;
+}
+
+gmg_status gmg_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (level < 0 || level >= (int)ctx->lv.size() || n_sweeps < 1) { ctx->err = "bad level / n_sweeps"; return GMG_EINVAL; }
+    Launcher Lc{ctx, ctx->stream};
+    DevLevel &L = ctx->dv[level];
+    const int nv = ctx->opt.dim + 2;
+    CK(cudaMemsetAsync(L.dW, 0, sizeof(double) * nv * L.n, ctx->stream));
+    if (ctx->opt.dim == 2) {
+        enqueue_face<2>(Lc, level, L.W, false);
+        enqueue_gather<2>(Lc, level, G_PREPARE | G_SIGMA, nullptr);
+        enqueue_sweeps<2>(Lc, level, n_sweeps, L.W, L.Rt, nullptr);
+    } else {
+        enqueue_face<3>(Lc, level, L.W, false);
+        enqueue_gather<3>(Lc, level, G_PREPARE | G_SIGMA, nullptr);
+        enqueue_sweeps<3>(Lc, level, n_sweeps, L.W, L.Rt, nullptr);
+    }
+    CK(cudaGetLastError());
+    if (dW_out) { st = get_natural(ctx, level, L.dW, nv, dW_out); if (st) return st; }
+    return GMG_OK;
+}
+
+static gmg_status build_graph(gmg_ctx *ctx)
+{
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    Launcher Lc{ctx, cs};
+    ctx->launches = 0;
+    for (double &b : ctx->kbytes) b = 0;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        if (ctx->opt.dim == 2) enqueue_vcycle<2>(Lc);
+        else enqueue_vcycle<3>(Lc);
+        e = cudaStreamEndCapture(cs, &g);
+    }
+    cudaStreamDestroy(cs);
+    if (e != cudaSuccess) { ctx->err = std::string("graph capture: ") + cudaGetErrorString(e); return GMG_ECUDA; }
+    e = cudaGraphInstantiate(&ctx->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) { ctx->err = std::string("graph instantiate: ") + cudaGetErrorString(e); return GMG_ECUDA; }
+    ctx->graph_launches = ctx->launches;
+    return GMG_OK;
+}
+
+static gmg_status finish_history(gmg_ctx *ctx, int n_cycles, double *res_hist)
+{
+    const int nv = ctx->opt.dim + 2;
+    int flags[2] = {0, 0};
+    CK(cudaMemcpyAsync(flags, ctx->d_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (res_hist)
+        CK(cudaMemcpyAsync(res_hist, ctx->d_hist, sizeof(double) * nv * std::min(n_cycles + 1, ctx->hist_cap),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (flags[1]) { ctx->err = "non-finite residual (level 0)"; return GMG_ENONFINITE; }
+    return GMG_OK;
+}
+
+gmg_status gmg_vcycle(gmg_ctx *ctx, int n_cycles, double *res_hist)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx);
+    if (st) return st;
+    if (n_cycles < 0 || n_cycles + 1 > ctx->hist_cap) { ctx->err = "n_cycles out of range"; return GMG_EINVAL; }
+    if (!ctx->graph) { st = build_graph(ctx); if (st) return st; }
+    CK(cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), ctx->stream));
+    for (int k = 0; k < n_cycles; ++k) CK(cudaGraphLaunch(ctx->graph, ctx->stream));
+    Launcher Lc{ctx, ctx->stream};
+    if (ctx->opt.dim == 2) enqueue_final_norm<2>(Lc);
+    else enqueue_final_norm<3>(Lc);
+    CK(cudaGetLastError());
+    return finish_history(ctx, n_cycles, res_hist);
+}
+
+gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_t *count_out, double *bytes_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx);
+    if (st) return st;
+    if (n_cycles < 1 || n_cycles + 1 > ctx->hist_cap) { ctx->err = "n_cycles out of range"; return GMG_EINVAL; }
+    ctx->prof.on = true;
+    ctx->prof.ev.clear();
+    ctx->prof.marks.clear();
+    for (double &b : ctx->kbytes) b = 0;
+    ctx->launches = 0;
+    CK(cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), ctx->stream));
+    Launcher Lc{ctx, ctx->stream};
+    for (int k = 0; k < n_cycles; ++k) {
+        if (ctx->opt.dim == 2) enqueue_vcycle<2>(Lc);
+        else enqueue_vcycle<3>(Lc);
+    }
+    ctx->prof.on = false;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    double ms[GMG_K_COUNT] = {0};
+    int64_t cnt[GMG_K_COUNT] = {0};
+    for (auto &m : ctx->prof.marks) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, ctx->prof.ev[m.second], ctx->prof.ev[m.second + 1]);
+        ms[m.first] += t;
+        cnt[m.first] += 1;
+    }
+    for (auto e : ctx->prof.ev) cudaEventDestroy(e);
+    ctx->prof.ev.clear();
+    ctx->prof.marks.clear();
+    for (int k = 0; k < GMG_K_COUNT; ++k) {
+        if (ms_out) ms_out[k] = ms[k];
+        if (count_out) count_out[k] = cnt[k];
+        if (bytes_out) bytes_out[k] = ctx->kbytes[k];
+    }
+    return GMG_OK;
+}
+
+gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, double *ms, double *cell_updates,
+                           double *bytes)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (level < 0 || level >= (int)ctx->lv.size() || n_sweeps < 1 || reps < 1) { ctx->err = "bad args"; return GMG_EINVAL; }
+    DevLevel &L = ctx->dv[level];
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    Launcher Lc{ctx, cs};
+    for (double &b : ctx->kbytes) b = 0;
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    if (ctx->opt.dim == 2) enqueue_sweeps<2>(Lc, level, n_sweeps, L.W, L.Rt, nullptr);
+    else enqueue_sweeps<3>(Lc, level, n_sweeps, L.W, L.Rt, nullptr);
+    CK(cudaStreamEndCapture(cs, &g));
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    const double b1 = ctx->kbytes[GMG_K_SWEEP];
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    CK(cudaGraphLaunch(ge, ctx->stream));   // warm-up
+    CK(cudaEventRecord(e0, ctx->stream));
+    for (int r = 0; r < reps; ++r) CK(cudaGraphLaunch(ge, ctx->stream));
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(ge);
+    cudaStreamDestroy(cs);
+    if (ms) *ms = t;
+    if (cell_updates) *cell_updates = (double)L.n * 2.0 * n_sweeps * reps;
+    if (bytes) *bytes = b1 * reps;
+    return GMG_OK;
+}
+
+int64_t gmg_vcycle_launches(gmg_ctx *ctx)
+{
+    if (!ctx) return -1;
+    if (!ctx->graph && check_ready(ctx) == GMG_OK) build_graph(ctx);
+    return ctx->graph_launches;
+}
+
+const char *gmg_last_error(gmg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void gmg_destroy(gmg_ctx *ctx)
+{
+    if (!ctx) return;
+    if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+    delete ctx;
+}
+
+}  // extern "C"

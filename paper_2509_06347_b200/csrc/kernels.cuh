@@ -1,0 +1,425 @@
+// kernels.cuh -- sm_100a device kernels of libgmg (FP64, no tensor cores:
+// the per-cell implicit "block" is a scalar times identity).
+//
+// Every kernel is HBM/latency bound gather-streaming work; see DESIGN.md
+// "Kernels and rooflines".  Cell arrays are AoS [n][nv] in color-contiguous
+// internal order; sweep/gather slot tables are SELL-32 (one warp of cells per
+// chunk, entry of slot s = base + 32 s) so that slot streams coalesce.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "gmg_internal.h"
+
+namespace gmg {
+
+struct Phys {
+    double gamma, gm1, K, omega;
+};
+struct BCs {
+    double winf[5];
+    int kind[16];
+};
+
+enum : int {
+    G_FLUX = 1,       // accumulate R = sum sigma S F and alpha = prod alpha_f^M from the face buffers
+    G_NORM = 2,       // per-block partial sums of R_q^2
+    G_EXPLICIT = 4,   // W -= (cfl_exp / Sigma) R            (Eq.(smo), reading A9)
+    G_WRITE_RT = 8,   // Rt = R (+ F if G_ADD_F)
+    G_ADD_F = 16,
+    G_SET_F = 32,     // F = Rs - R
+    G_ALPHA = 64,     // alpha = prod alpha_f^{M_f}          (O5)
+    G_PREPARE = 128,  // D, 1/D, alpha/2, per-slot S r       (O6)
+    G_SIGMA = 256,    // store Sigma
+};
+
+struct GArgs {
+    int flags;
+    double cfl_imp, cfl_exp;
+    double *Wexp;
+    double *partial;
+};
+
+template <int D>
+__device__ __forceinline__ void ld_state(const double *__restrict__ p, int i, double *w)
+{
+    const double *q = p + (size_t)i * (D + 2);
+#pragma unroll
+    for (int k = 0; k < D + 2; ++k) w[k] = __ldg(q + k);
+}
+
+template <int D>
+__device__ __forceinline__ double pressure(const double *w, double gm1)
+{
+    double m2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) m2 += w[1 + k] * w[1 + k];
+    return gm1 * (w[D + 1] - 0.5 * m2 / w[0]);
+}
+
+// ghost state of a boundary face (O4, reading A25); n = unit outward normal
+template <int D>
+__device__ __forceinline__ void ghost(int kind, const double *wi, const BCs &bc, const double *n, double *wg)
+{
+    if (kind == GMG_FARFIELD) {
+#pragma unroll
+        for (int q = 0; q < D + 2; ++q) wg[q] = bc.winf[q];
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < D + 2; ++q) wg[q] = wi[q];
+    if (kind == GMG_SLIP) {
+        double mn = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) mn += wi[1 + k] * n[k];
+#pragma unroll
+        for (int k = 0; k < D; ++k) wg[1 + k] = wi[1 + k] - 2.0 * mn * n[k];
+    } else if (kind == GMG_NOSLIP) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) wg[1 + k] = -wi[1 + k];
+    }
+}
+
+// one half-range side of the first-order KFVS flux (O4): sgn = +1 -> u.n > 0
+// half of the left state, sgn = -1 -> u.n < 0 half of the right state.
+template <int D>
+__device__ __forceinline__ void kfvs_side(const double *w, const double *n, double sgn, const Phys &ph, double *F)
+{
+    const double rho = w[0], ir = 1.0 / rho;
+    double u[D], U = 0.0, u2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { u[k] = w[1 + k] * ir; U += u[k] * n[k]; u2 += u[k] * u[k]; }
+    const double p = ph.gm1 * (w[D + 1] - 0.5 * rho * u2);
+    const double lam = 0.5 * rho / p;          // lambda = rho / (2 p)
+    const double inv2l = p * ir;               // 1 / (2 lambda)
+    const double sl = sqrt(lam);
+    const double e = exp(-lam * U * U) * (0.5 * rsqrt(3.14159265358979323846 * lam));
+    const double m0 = 0.5 * erfc(-sgn * sl * U);
+    const double m1 = U * m0 + sgn * e;
+    const double m2 = U * m1 + inv2l * m0;
+    const double m3 = U * m2 + 2.0 * inv2l * m1;
+    F[0] = rho * m1;
+#pragma unroll
+    for (int k = 0; k < D; ++k) F[1 + k] = rho * m2 * n[k] + rho * m1 * (u[k] - U * n[k]);
+    F[D + 1] = 0.5 * rho * (m3 + m1 * (u2 - U * U + ((double)(D - 1) + ph.K) * inv2l));
+}
+
+// ---------------------------------------------------------------------------
+// Face kernel (a6 + a10 per face): r_f = omega (|u.n| + a) of the average
+// state; with FLUX also S F_f (KFVS) and alpha_f^{M_f} (DF helper).
+// ---------------------------------------------------------------------------
+template <int D, bool FLUX>
+__global__ void __launch_bounds__(256) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
+{
+    constexpr int NV = D + 2;
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= L.nf) return;
+    const int l = __ldg(L.fl + f), r = __ldg(L.fr + f);
+    double A[D], S2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) { A[k] = __ldg(L.fA + (size_t)k * L.nf + f); S2 += A[k] * A[k]; }
+    const double S = sqrt(S2), iS = 1.0 / S;
+    double n[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) n[k] = A[k] * iS;
+    double wl[NV], wr[NV];
+    ld_state<D>(Wsrc, l, wl);
+    if (r >= 0) ld_state<D>(Wsrc, r, wr);
+    else ghost<D>(bc.kind[-r - 1], wl, bc, n, wr);
+
+    // spectral radius of the conservative average (O6, reading A5)
+    {
+        double wb[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) wb[q] = 0.5 * (wl[q] + wr[q]);
+        const double ib = 1.0 / wb[0];
+        double U = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) U += wb[1 + k] * ib * n[k];
+        const double pb = pressure<D>(wb, ph.gm1);
+        L.Srf[f] = S * (ph.omega * (fabs(U) + sqrt(ph.gamma * pb * ib)));
+    }
+    if (FLUX) {
+        double Fp[NV], Fm[NV];
+        kfvs_side<D>(wl, n, 1.0, ph, Fp);
+        kfvs_side<D>(wr, n, -1.0, ph, Fm);
+        double *out = L.Fs + (size_t)f * NV;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) out[q] = S * (Fp[q] + Fm[q]);
+        // DF helper (O5)
+        const double pl = pressure<D>(wl, ph.gm1), pr = pressure<D>(wr, ph.gm1);
+        const double il = 1.0 / wl[0], ir = 1.0 / wr[0];
+        const double ial = rsqrt(ph.gamma * pl * il), iar = rsqrt(ph.gamma * pr * ir);
+        double Ul = 0.0, Ur = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) { Ul += wl[1 + k] * il * n[k]; Ur += wr[1 + k] * ir * n[k]; }
+        const double dMn = Ul * ial - Ur * iar;
+        double dMt2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const double t = (wl[1 + k] * il - Ul * n[k]) * ial - (wr[1 + k] * ir - Ur * n[k]) * iar;
+            dMt2 += t * t;
+        }
+        const double dp = fabs(pl - pr);
+        const double Dv = dp / pl + dp / pr + dMn * dMn + dMt2;
+        const double af = 1.0 / (1.0 + Dv * Dv);
+        double aM = 1.0;
+        const int M = L.fM[f];
+        for (int g = 0; g < M; ++g) aM *= af;
+        L.aM[f] = aM;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Cell gather (a6, a7, a9, a10, a16): per cell over its face slots.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
+{
+    constexpr int NV = D + 2;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double R[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) R[q] = 0.0;
+    if (i < L.n) {
+        const int gb = L.gbase[i], nt = L.deg_all[i], ni = L.deg_int[i], sb = L.sbase[i];
+        double sig = 0.0, al = 1.0;
+        for (int s = 0; s < nt; ++s) {
+            const int sf = __ldg(L.gface + gb + kChunk * s);
+            const int f = (sf > 0 ? sf : -sf) - 1;
+            const double srf = __ldg(L.Srf + f);
+            sig += srf;
+            if (a.flags & G_FLUX) {
+                const double *F = L.Fs + (size_t)f * NV;
+                if (sf > 0) {
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) R[q] += __ldg(F + q);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) R[q] -= __ldg(F + q);
+                }
+                al *= __ldg(L.aM + f);
+            }
+            if ((a.flags & G_PREPARE) && s < ni) L.sSr[sb + kChunk * s] = srf;
+        }
+        if (a.flags & G_ALPHA) L.alpha[i] = al;
+        if (a.flags & G_SIGMA) L.sigma[i] = sig;
+        if (a.flags & G_PREPARE) {
+            const double ai = (a.flags & G_ALPHA) ? al : L.alpha[i];
+            // D = alpha (V/Dt_imp + Sigma/2) + (1 - alpha) V/Dt_exp (O6, A2, A3)
+            const double Dg = ai * (sig / a.cfl_imp + 0.5 * sig) + (1.0 - ai) * (sig / a.cfl_exp);
+            L.invD[i] = 1.0 / Dg;
+            L.ha[i] = 0.5 * ai;
+        }
+        const size_t o = (size_t)i * NV;
+        if (a.flags & G_SET_F) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) L.F[o + q] = L.Rs[o + q] - R[q];
+        }
+        if (a.flags & G_WRITE_RT) {
+            if (a.flags & G_ADD_F) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q] + L.F[o + q];
+            } else {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q];
+            }
+        }
+        if (a.flags & G_EXPLICIT) {
+            const double c = a.cfl_exp / sig;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) a.Wexp[o + q] = a.Wexp[o + q] - c * R[q];
+        }
+    }
+    if (a.flags & G_NORM) {
+        __shared__ double sh[8][NV];
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            double v = R[q] * R[q];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) sh[wid][q] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < NV) {
+            double v = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += sh[w][threadIdx.x];
+            a.partial[(size_t)blockIdx.x * NV + threadIdx.x] = v;
+        }
+    }
+}
+
+// deterministic final reduction of the norm partials -> hist[counter][q]
+__global__ void __launch_bounds__(256) k_norm_final(const double *__restrict__ partial, int nblocks, int nv,
+                                                    double *hist, int hist_cap, int *flags)
+{
+    __shared__ double sh[256];
+    const int idx = flags[0];
+    for (int q = 0; q < nv; ++q) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < nblocks; b += 256) s += partial[(size_t)b * nv + q];
+        sh[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const double v = sqrt(sh[0]);
+            if (idx < hist_cap) hist[(size_t)idx * nv + q] = v;
+            if (!isfinite(v)) flags[1] = 1;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) flags[0] = idx + 1;
+}
+
+// ---------------------------------------------------------------------------
+// MC-LU-SGS sweep over one color block (a11 / a12), reading all neighbours'
+// current increments (reading A7):
+//   dW_i = -( Rt_i + alpha_i/2 sum_j [T(W_j+dW_j; A) - T(W_j; A) - S r dW_j] ) / D_i
+// with A = sigma S n (the Euler flux is linear in its normal, S T(W;n) = T(W;A)).
+// Same-color cells never neighbour each other, so the in-place update is race free.
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void flux_diff(const double *w, const double *dw, const double *A, double gm1,
+                                          double Sr, double *acc)
+{
+    // T(w; A) and T(w + dw; A)
+    const double r0 = w[0], r1 = w[0] + dw[0];
+    const double i0 = 1.0 / r0, i1 = 1.0 / r1;
+    double mA0 = 0.0, mA1 = 0.0, m20 = 0.0, m21 = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const double a0 = w[1 + k], a1 = w[1 + k] + dw[1 + k];
+        mA0 += a0 * A[k];
+        mA1 += a1 * A[k];
+        m20 += a0 * a0;
+        m21 += a1 * a1;
+    }
+    const double E0 = w[D + 1], E1 = w[D + 1] + dw[D + 1];
+    const double p0 = gm1 * (E0 - 0.5 * m20 * i0), p1 = gm1 * (E1 - 0.5 * m21 * i1);
+    const double U0 = mA0 * i0, U1 = mA1 * i1;
+    acc[0] += (mA1 - mA0) - Sr * dw[0];
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+        acc[1 + k] += ((w[1 + k] + dw[1 + k]) * U1 + p1 * A[k]) - (w[1 + k] * U0 + p0 * A[k]) - Sr * dw[1 + k];
+    acc[D + 1] += (E1 + p1) * U1 - (E0 + p0) * U0 - Sr * dw[D + 1];
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_sweep(DevLevel L, int cbeg, int cend, double gm1,
+                                               const double *__restrict__ Wlin, const double *__restrict__ rhs,
+                                               double *__restrict__ Wout)
+{
+    constexpr int NV = D + 2;
+    const int i = cbeg + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cend) return;
+    const int sb = __ldg(L.sbase + i), ni = __ldg(L.deg_int + i);
+    double acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+    const double *dWr = L.dW;   // neighbours' increments: written only by earlier launches
+    for (int s = 0; s < ni; ++s) {
+        const int e = sb + kChunk * s;
+        const int j = __ldg(L.snbr + e);
+        double A[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) A[k] = __ldg(L.sA + (size_t)k * L.ns_entries + e);
+        const double Sr = __ldg(L.sSr + e);
+        double w[NV], dw[NV];
+        ld_state<D>(Wlin, j, w);
+        ld_state<D>(dWr, j, dw);
+        flux_diff<D>(w, dw, A, gm1, Sr, acc);
+    }
+    const double invD = __ldg(L.invD + i), ha = __ldg(L.ha + i);
+    const size_t o = (size_t)i * NV;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const double d = -(__ldg(rhs + o + q) + ha * acc[q]) * invD;
+        L.dW[o + q] = d;
+        if (Wout) Wout[o + q] = __ldg(Wlin + o + q) + d;
+    }
+}
+
+// restriction to a coarse level (a8, A15) + dW = 0 for its sweeps
+template <int D>
+__global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const double *__restrict__ Wf,
+                                                  const double *__restrict__ Rf)
+{
+    constexpr int NV = D + 2;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C.n) return;
+    const int k0 = C.child[c], k1 = C.child[C.n + c];
+    const double V0 = Fn.vol[k0];
+    double w[NV], r[NV];
+    double a = Fn.alpha[k0];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) { w[q] = V0 * Wf[(size_t)k0 * NV + q]; r[q] = Rf[(size_t)k0 * NV + q]; }
+    if (k1 >= 0) {
+        const double V1 = Fn.vol[k1];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) { w[q] = w[q] + V1 * Wf[(size_t)k1 * NV + q]; r[q] = r[q] + Rf[(size_t)k1 * NV + q]; }
+        a = fmin(a, Fn.alpha[k1]);
+    }
+    const double iv = C.vol[c];
+    const size_t o = (size_t)c * NV;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) { C.W0[o + q] = w[q] / iv; C.Rs[o + q] = r[q]; C.dW[o + q] = 0.0; }
+    C.alpha[c] = a;
+}
+
+// DF-limited prolongation, both levels fused (a15, A13, A14):
+//   W_0 += alpha_0 (dW_1 + alpha_1 dW_2[parent_1])[parent_0]
+template <int D>
+__global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLevel C2, int nl)
+{
+    constexpr int NV = D + 2;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= F0.n) return;
+    const int p = F0.parent[i];
+    double corr[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) corr[q] = C1.dW[(size_t)p * NV + q];
+    if (nl >= 3) {
+        const int pp = C1.parent[p];
+        const double a1 = C1.alpha[p];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) corr[q] += a1 * C2.dW[(size_t)pp * NV + q];
+    }
+    const double a0 = F0.alpha[i];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) F0.W[(size_t)i * NV + q] += a0 * corr[q];
+}
+
+template <int D>
+__global__ void k_update(int n, double *__restrict__ W, const double *__restrict__ dW)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * (D + 2)) return;
+    W[i] += dW[i];
+}
+
+// natural SoA [nv][n]  <->  internal AoS [n][nv]
+__global__ void k_to_internal(int n, int nv, const int *__restrict__ perm, const double *__restrict__ src,
+                              double *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nat = perm[i];
+    for (int q = 0; q < nv; ++q) dst[(size_t)i * nv + q] = src[(size_t)q * n + nat];
+}
+__global__ void k_to_natural(int n, int nv, const int *__restrict__ perm, const double *__restrict__ src,
+                             double *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nat = perm[i];
+    for (int q = 0; q < nv; ++q) dst[(size_t)q * n + nat] = src[(size_t)i * nv + q];
+}
+__global__ void k_fill(int n, double *p, double v)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+}  // namespace gmg

@@ -1,0 +1,348 @@
+"""Thin ctypes binding of libgmg (include/gmg.h) -- argument marshalling only.
+
+Every step of the hot path runs in libgmg's sm_100a kernels; this module
+never computes anything and has no CPU fallback: if libgmg.so is missing or
+no CUDA device is present, the compute calls raise.
+
+Names mirror the C ABI (gmg_create, gmg_load_mesh, ...); `Solver` bundles
+them with a torch-allocated device workspace and torch's current stream
+(PyTorch is used for device memory and streams only).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIBPATH = os.path.join(_HERE, "libgmg.so")
+
+GMG_OK, GMG_EINVAL, GMG_ETOPO, GMG_ECOLOR, GMG_ESTALL, GMG_ENOMEM, GMG_ECUDA, GMG_ENCCL, GMG_ENONFINITE, GMG_ESTATE = range(10)
+STATUS = ["GMG_OK", "GMG_EINVAL", "GMG_ETOPO", "GMG_ECOLOR", "GMG_ESTALL", "GMG_ENOMEM", "GMG_ECUDA", "GMG_ENCCL",
+          "GMG_ENONFINITE", "GMG_ESTATE"]
+K_FACE, K_GATHER, K_SWEEP, K_RESTRICT, K_PROLONG, K_NORM, K_COUNT = range(7)
+K_NAMES = ["face", "gather", "sweep", "restrict", "prolong", "norm"]
+
+# every symbol include/gmg.h declares
+ABI_SYMBOLS = ["gmg_default_options", "gmg_create", "gmg_load_mesh", "gmg_set_coloring", "gmg_build_hierarchy",
+               "gmg_get_level_info", "gmg_get_maps", "gmg_get_level_geometry", "gmg_workspace_bytes",
+               "gmg_set_workspace", "gmg_set_state", "gmg_set_level_state", "gmg_get_state", "gmg_set_alpha",
+               "gmg_residual", "gmg_set_level_inputs", "gmg_smooth", "gmg_vcycle", "gmg_profile_vcycle",
+               "gmg_time_smooth", "gmg_vcycle_launches", "gmg_last_error", "gmg_destroy"]
+
+
+class GmgError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS[status] if 0 <= status < len(STATUS) else status}: {msg}")
+        self.status = status
+
+
+class Options(C.Structure):
+    _fields_ = [("dim", C.c_int), ("gamma", C.c_double), ("cfl_imp", C.c_double), ("cfl_exp", C.c_double),
+                ("n_sweeps", C.c_int), ("n_levels", C.c_int), ("pre_smooth", C.c_int), ("post_smooth", C.c_int),
+                ("skew_limit", C.c_double), ("r_factor", C.c_double), ("fine_smoother", C.c_int),
+                ("df_mode", C.c_int), ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p),
+                ("device", C.c_int), ("stream", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libgmg.so (build it first with paper_2509_06347_b200._build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIBPATH):
+            raise ImportError(f"{LIBPATH} missing: run `python -m paper_2509_06347_b200._build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIBPATH)
+        P, I64, I, D = C.c_void_p, C.c_int64, C.c_int, C.c_double
+        sig = {
+            "gmg_default_options": (None, [C.POINTER(Options)]),
+            "gmg_create": (I, [C.POINTER(Options), C.POINTER(P)]),
+            "gmg_load_mesh": (I, [P, I64, P, P, I64, P, P, P, P, P, I, P, P]),
+            "gmg_set_coloring": (I, [P, I, P]),
+            "gmg_build_hierarchy": (I, [P, I, C.POINTER(I)]),
+            "gmg_get_level_info": (I, [P, I, C.POINTER(I64), C.POINTER(I), C.POINTER(I64)]),
+            "gmg_get_maps": (I, [P, I, P, P, P]),
+            "gmg_get_level_geometry": (I, [P, I, P, P, P, P, P, P, P]),
+            "gmg_workspace_bytes": (C.c_size_t, [P]),
+            "gmg_set_workspace": (I, [P, P, C.c_size_t]),
+            "gmg_set_state": (I, [P, P, P]),
+            "gmg_set_level_state": (I, [P, I, P]),
+            "gmg_get_state": (I, [P, I, P]),
+            "gmg_set_alpha": (I, [P, P]),
+            "gmg_residual": (I, [P, I, P, P, P]),
+            "gmg_set_level_inputs": (I, [P, I, P, P]),
+            "gmg_smooth": (I, [P, I, I, P]),
+            "gmg_vcycle": (I, [P, I, P]),
+            "gmg_profile_vcycle": (I, [P, I, P, P, P]),
+            "gmg_time_smooth": (I, [P, I, I, I, P, P, P]),
+            "gmg_vcycle_launches": (I64, [P]),
+            "gmg_last_error": (C.c_char_p, [P]),
+            "gmg_destroy": (None, [P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+# C-ABI names (marshalling only)
+# ---------------------------------------------------------------------------
+def gmg_default_options(**kw) -> Options:
+    o = Options()
+    lib().gmg_default_options(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def _check(ctx, st, allow=()):
+    if st != GMG_OK and st not in allow:
+        msg = lib().gmg_last_error(ctx)
+        raise GmgError(st, msg.decode() if msg else "")
+    return st
+
+
+def gmg_create(opt: Options):
+    h = C.c_void_p()
+    st = lib().gmg_create(C.byref(opt), C.byref(h))
+    if st != GMG_OK:
+        raise GmgError(st, "gmg_create: invalid options")
+    return h
+
+
+def gmg_load_mesh(ctx, mesh, part=None):
+    keep = [_f64(mesh.vol), _f64(mesh.ctr), np.ascontiguousarray(mesh.left, np.int64),
+            np.ascontiguousarray(mesh.right, np.int64), _f64(mesh.avec), _f64(mesh.fctr),
+            np.ascontiguousarray(mesh.ngauss, np.int8), np.ascontiguousarray(mesh.patch_kind, np.int32),
+            None if part is None else np.ascontiguousarray(part, np.int32)]
+    vol, ctr, left, right, avec, fctr, ng, pk, pa = keep
+    return _check(ctx, lib().gmg_load_mesh(ctx, vol.shape[0], _ptr(vol), _ptr(ctr), left.shape[0], _ptr(left),
+                                           _ptr(right), _ptr(avec), _ptr(fctr), _ptr(ng), pk.shape[0], _ptr(pk),
+                                           _ptr(pa)))
+
+
+def gmg_set_coloring(ctx, level, color):
+    c = None if color is None else np.ascontiguousarray(color, np.int32)
+    return _check(ctx, lib().gmg_set_coloring(ctx, level, _ptr(c)))
+
+
+def gmg_build_hierarchy(ctx, n_levels):
+    nb = C.c_int(0)
+    st = _check(ctx, lib().gmg_build_hierarchy(ctx, n_levels, C.byref(nb)), allow=(GMG_ESTALL,))
+    return nb.value, st
+
+
+def gmg_get_level_info(ctx, level):
+    n, nc, nf = C.c_int64(), C.c_int(), C.c_int64()
+    _check(ctx, lib().gmg_get_level_info(ctx, level, C.byref(n), C.byref(nc), C.byref(nf)))
+    return n.value, nc.value, nf.value
+
+
+def gmg_get_maps(ctx, level):
+    n, _, _ = gmg_get_level_info(ctx, level)
+    color = np.zeros(n, np.int32)
+    perm = np.zeros(n, np.int64)
+    parent = np.zeros(n, np.int64)
+    _check(ctx, lib().gmg_get_maps(ctx, level, _ptr(color), _ptr(perm), _ptr(parent)))
+    return color, perm, parent
+
+
+def gmg_get_level_geometry(ctx, level, dim):
+    n, _, nf = gmg_get_level_info(ctx, level)
+    out = dict(vol=np.zeros(n), ctr=np.zeros((dim, n)), left=np.zeros(nf, np.int64), right=np.zeros(nf, np.int64),
+               avec=np.zeros((dim, nf)), fctr=np.zeros((dim, nf)), ngauss=np.zeros(nf, np.int8))
+    _check(ctx, lib().gmg_get_level_geometry(ctx, level, *(_ptr(out[k]) for k in
+                                                           ("vol", "ctr", "left", "right", "avec", "fctr", "ngauss"))))
+    return out
+
+
+def gmg_workspace_bytes(ctx):
+    return int(lib().gmg_workspace_bytes(ctx))
+
+
+def gmg_set_workspace(ctx, dptr, nbytes):
+    return _check(ctx, lib().gmg_set_workspace(ctx, dptr, nbytes))
+
+
+def gmg_set_state(ctx, W, W_inf):
+    Wk = W if hasattr(W, "data_ptr") else _f64(W)
+    wi = _f64(W_inf)
+    return _check(ctx, lib().gmg_set_state(ctx, _ptr(Wk), _ptr(wi)))
+
+
+def gmg_set_level_state(ctx, level, W):
+    Wk = W if hasattr(W, "data_ptr") else _f64(W)
+    return _check(ctx, lib().gmg_set_level_state(ctx, level, _ptr(Wk)))
+
+
+def gmg_get_state(ctx, level, out):
+    return _check(ctx, lib().gmg_get_state(ctx, level, _ptr(out)))
+
+
+def gmg_set_alpha(ctx, alpha):
+    a = alpha if hasattr(alpha, "data_ptr") else _f64(alpha)
+    return _check(ctx, lib().gmg_set_alpha(ctx, _ptr(a)))
+
+
+def gmg_residual(ctx, level, R_out=None, alpha_out=None, sigma_out=None):
+    return _check(ctx, lib().gmg_residual(ctx, level, _ptr(R_out), _ptr(alpha_out), _ptr(sigma_out)))
+
+
+def gmg_set_level_inputs(ctx, level, Rt=None, alpha=None):
+    R = None if Rt is None else (Rt if hasattr(Rt, "data_ptr") else _f64(Rt))
+    a = None if alpha is None else (alpha if hasattr(alpha, "data_ptr") else _f64(alpha))
+    return _check(ctx, lib().gmg_set_level_inputs(ctx, level, _ptr(R), _ptr(a)))
+
+
+def gmg_smooth(ctx, level, n_sweeps, dW_out=None):
+    return _check(ctx, lib().gmg_smooth(ctx, level, n_sweeps, _ptr(dW_out)))
+
+
+def gmg_vcycle(ctx, n_cycles, res_hist=None):
+    return _check(ctx, lib().gmg_vcycle(ctx, n_cycles, _ptr(res_hist)))
+
+
+def gmg_profile_vcycle(ctx, n_cycles):
+    ms = np.zeros(K_COUNT)
+    cnt = np.zeros(K_COUNT, np.int64)
+    by = np.zeros(K_COUNT)
+    _check(ctx, lib().gmg_profile_vcycle(ctx, n_cycles, _ptr(ms), _ptr(cnt), _ptr(by)))
+    return ms, cnt, by
+
+
+def gmg_time_smooth(ctx, level, n_sweeps, reps):
+    ms, cu, by = C.c_double(), C.c_double(), C.c_double()
+    _check(ctx, lib().gmg_time_smooth(ctx, level, n_sweeps, reps, C.byref(ms), C.byref(cu), C.byref(by)))
+    return ms.value, cu.value, by.value
+
+
+def gmg_vcycle_launches(ctx):
+    return int(lib().gmg_vcycle_launches(ctx))
+
+
+def gmg_last_error(ctx):
+    m = lib().gmg_last_error(ctx)
+    return m.decode() if m else ""
+
+
+def gmg_destroy(ctx):
+    lib().gmg_destroy(ctx)
+
+
+# ---------------------------------------------------------------------------
+# convenience wrapper: torch workspace + stream
+# ---------------------------------------------------------------------------
+class Solver:
+    """One rank's GMG solver on one CUDA device.
+
+    mesh: synth.Mesh-like (vol, ctr, left, right, avec, fctr, ngauss,
+    patch_kind, dim).  kw: gmg_options fields (cfl_imp, n_sweeps, ...).
+    """
+
+    def __init__(self, mesh, n_levels=3, device=0, color0=None, build_only=False, **kw):
+        self.dim = int(mesh.dim)
+        self.nv = self.dim + 2
+        self.opt = gmg_default_options(dim=self.dim, n_levels=n_levels, device=device, **kw)
+        self._torch = None
+        if not build_only:
+            import torch
+            if not torch.cuda.is_available():
+                raise RuntimeError("libgmg needs a CUDA device (no CPU fallback)")
+            self._torch = torch
+            self.device = torch.device("cuda", device)
+            self.opt.stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.ctx = gmg_create(self.opt)
+        gmg_load_mesh(self.ctx, mesh)
+        if color0 is not None:
+            gmg_set_coloring(self.ctx, 0, color0)
+        self.n_levels, self.build_status = gmg_build_hierarchy(self.ctx, n_levels)
+        self.sizes = [gmg_get_level_info(self.ctx, l) for l in range(self.n_levels)]
+        self.ws = None
+        if not build_only:
+            nb = gmg_workspace_bytes(self.ctx)
+            self.ws = self._torch.empty(nb, dtype=self._torch.uint8, device=self.device)
+            gmg_set_workspace(self.ctx, self.ws.data_ptr(), nb)
+
+    def n_cells(self, level=0):
+        return self.sizes[level][0]
+
+    def n_colors(self, level=0):
+        return self.sizes[level][1]
+
+    def maps(self, level=0):
+        return gmg_get_maps(self.ctx, level)
+
+    def geometry(self, level=0):
+        return gmg_get_level_geometry(self.ctx, level, self.dim)
+
+    def set_state(self, W, W_inf):
+        gmg_set_state(self.ctx, W, W_inf)
+
+    def set_level_state(self, level, W):
+        gmg_set_level_state(self.ctx, level, W)
+
+    def get_state(self, level=0):
+        out = np.zeros((self.nv, self.n_cells(level)))
+        gmg_get_state(self.ctx, level, out)
+        return out
+
+    def set_alpha(self, alpha):
+        gmg_set_alpha(self.ctx, alpha)
+
+    def residual(self, level=0):
+        n = self.n_cells(level)
+        R, a, s = np.zeros((self.nv, n)), np.zeros(n), np.zeros(n)
+        gmg_residual(self.ctx, level, R, a, s)
+        return R, a, s
+
+    def set_level_inputs(self, level, Rt=None, alpha=None):
+        gmg_set_level_inputs(self.ctx, level, Rt, alpha)
+
+    def smooth(self, level, n_sweeps):
+        dW = np.zeros((self.nv, self.n_cells(level)))
+        gmg_smooth(self.ctx, level, n_sweeps, dW)
+        return dW
+
+    def vcycle(self, n_cycles=1):
+        hist = np.zeros((n_cycles + 1, self.nv))
+        gmg_vcycle(self.ctx, n_cycles, hist)
+        return hist
+
+    def profile_vcycle(self, n_cycles=1):
+        return gmg_profile_vcycle(self.ctx, n_cycles)
+
+    def time_smooth(self, level, n_sweeps, reps):
+        return gmg_time_smooth(self.ctx, level, n_sweeps, reps)
+
+    def vcycle_launches(self):
+        return gmg_vcycle_launches(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            gmg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

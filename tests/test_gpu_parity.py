@@ -1,0 +1,228 @@
+"""GPU parity: libgmg's CUDA path (through the C ABI) vs the CPU oracle on
+the same seeded inputs.  Tolerances: maps bit-exact
+(tests/test_abi_host.py); FP64 increments, states and residuals relative L2
+<= 1e-10 (BASELINE.json north_star); residual histories normalised-absolute
+|r_gpu(k) - r_orc(k)| <= 1e-10 r_orc(0).
+"""
+import numpy as np
+import pytest
+
+from synth import configs, state
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_06347_b200 import _build, gmg
+    _build.build()
+    gmg.lib()
+    return gmg
+
+
+def _case(name):
+    if name == "config1":
+        m = configs.config(1)
+        fs = configs.FREESTREAM[1]
+        W = state.gaussian_bump(m, *fs, jump=True)
+    elif name == "box":
+        m = configs.box3d(6, 5, 4, 2, seed=3)
+        fs = (1.0, (0.6, 0.2, -0.1), 0.7)
+        W = state.perturbed(m, *fs, eps=0.1, seed=4)
+    elif name == "sphere_small":
+        m = configs.sphere_shell(8, 4, 4)
+        fs = configs.FREESTREAM[4]
+        W = state.bow_shock(m, *fs)
+    elif name == "naca_small":
+        m = configs.naca_ogrid(ni=96, n_quad=12, n_tri=6)
+        fs = configs.FREESTREAM[2]
+        W = state.perturbed(m, *fs, eps=0.05, seed=1)
+    elif name == "cyl_small":
+        m = configs.cylinder_ogrid(ni=96, nr=40, n_tri=8)
+        fs = configs.FREESTREAM[3]
+        W = state.bow_shock(m, *fs)
+    else:
+        raise ValueError(name)
+    return m, state.winf(*fs), W
+
+
+CASES = ["config1", "box", "sphere_small", "naca_small", "cyl_small"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_residual_parity(G, orc, name):
+    m, Winf, W = _case(name)
+    s = G.Solver(m, n_levels=1)
+    s.set_state(W, Winf)
+    R, a, sig = s.residual(0)
+    Ro, ao, so, _ = orc.residual(orc.Level.from_mesh(m), W, Winf)
+    assert rel(R, Ro) <= 1e-12
+    assert rel(a, ao) <= 1e-12
+    assert rel(sig, so) <= 1e-13
+    s.close()
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("n_sweeps", [1, 6])
+def test_fine_smooth_parity(G, orc, name, n_sweeps):
+    m, Winf, W = _case(name)
+    s = G.Solver(m, n_levels=1)
+    s.set_state(W, Winf)
+    lv = orc.Level.from_mesh(m)
+    R, a, S, rf = orc.residual(lv, W, Winf)
+    alpha = np.random.default_rng(7).uniform(0.05, 1.0, m.n_cells)
+    s.set_level_inputs(0, R, alpha)
+    dW = s.smooth(0, n_sweeps)
+    col, nc = orc.color(lv)
+    D = orc.diag(S, alpha, 10.0, 0.5)
+    dWo = orc.smooth(lv, W, R, alpha, D, rf, col, nc, n_sweeps)
+    assert rel(dW, dWo) <= TOL
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["config1", "box", "sphere_small"])
+def test_coarse_smooth_parity(G, orc, name):
+    m, Winf, W = _case(name)
+    s = G.Solver(m, n_levels=3)
+    s.set_state(W, Winf)
+    H = orc.build_hierarchy(m, 3, 0.5)
+    for l in (1, 2):
+        lv = H[l]["level"]
+        # a coarse state: restriction of the fine state
+        Wl = W
+        for k in range(l):
+            Wl, _, _ = orc.restrict(H[k]["parent"], H[k + 1]["level"].n, H[k]["level"].vol, H[k + 1]["level"].vol,
+                                    Wl, np.zeros_like(Wl), np.ones(Wl.shape[1]))
+        s.set_level_state(l, Wl)
+        R, a, S, rf = orc.residual(lv, Wl, Winf)
+        alpha = np.random.default_rng(l).uniform(0.05, 1.0, lv.n)
+        s.set_level_inputs(l, R, alpha)
+        dW = s.smooth(l, 6)
+        D = orc.diag(S, alpha, 10.0, 0.5)
+        dWo = orc.smooth(lv, Wl, R, alpha, D, rf, H[l]["color"], H[l]["ncolor"], 6)
+        assert rel(dW, dWo) <= TOL, f"level {l}"
+    s.close()
+
+
+def _vcycle_pair(G, orc, m, Winf, W, n_cycles, **kw):
+    opt = orc.Options(**{k: v for k, v in kw.items() if k in orc.Options.__dataclass_fields__})
+    fields = [f[0] for f in G.Options._fields_]
+    s = G.Solver(m, n_levels=opt.n_levels, **{k: v for k, v in kw.items() if k in fields and k != "n_levels"})
+    s.set_state(W, Winf)
+    ua = kw.get("_alpha")
+    if ua is not None:
+        s.set_alpha(ua)
+    hist = s.vcycle(n_cycles)
+    Wg = s.get_state(0)
+    H = orc.build_hierarchy(m, opt.n_levels, opt.skew_limit)
+    Wo, ho = orc.vcycle(H, W, Winf, opt, n_cycles, user_alpha=ua)
+    s.close()
+    return Wg, hist, Wo, ho
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_vcycle_parity_short(G, orc, name):
+    m, Winf, W = _case(name)
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3)
+    assert rel(Wg, Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+
+
+def test_vcycle_parity_100_cycles_config1(G, orc):
+    """Residual histories over 100 V-cycles (north_star parity bar)."""
+    m, Winf, W = _case("config1")
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 100)
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+    assert rel(Wg, Wo) <= TOL
+
+
+def test_vcycle_parity_fine_mclusgs(G, orc):
+    m, Winf, W = _case("box")
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, fine_smoother=1)
+    assert rel(Wg, Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+
+
+@pytest.mark.parametrize("df_mode", [1, 2])
+def test_vcycle_parity_df_modes(G, orc, df_mode):
+    m, Winf, W = _case("config1")
+    ua = np.random.default_rng(3).uniform(0, 1, m.n_cells) if df_mode == 1 else None
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, df_mode=df_mode, _alpha=ua)
+    assert rel(Wg, Wo) <= TOL
+
+
+def test_vcycle_two_levels(G, orc):
+    m, Winf, W = _case("config1")
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 2, n_levels=2)
+    assert rel(Wg, Wo) <= TOL
+
+
+def test_freestream_fixed_point_gpu(G):
+    m = configs.tri_square(16, 16, seed=2)
+    W = state.uniform(m, 1.0, [0.5, 0.1], 0.7)
+    s = G.Solver(m, n_levels=3)
+    s.set_state(W, state.winf(1.0, [0.5, 0.1], 0.7))
+    hist = s.vcycle(3)
+    assert np.abs(s.get_state(0) - W).max() <= 1e-12 * np.abs(W).max()
+    assert hist.max() < 1e-13
+    s.close()
+
+
+def test_alpha_zero_vcycle_is_explicit_step_gpu(G, orc):
+    """P:705-711 + P:519 on the GPU: fine alpha = 0 -> V-cycle = explicit step."""
+    m, Winf, W = _case("config1")
+    s = G.Solver(m, n_levels=3, df_mode=1)
+    s.set_state(W, Winf)
+    s.set_alpha(np.zeros(m.n_cells))
+    s.vcycle(1)
+    R, a, S, _ = orc.residual(orc.Level.from_mesh(m), W, Winf)
+    assert rel(s.get_state(0), orc.explicit_update(W, S, R, 0.5)) <= 1e-14
+    s.close()
+
+
+def test_nonfinite_detected(G):
+    m, Winf, W = _case("config1")
+    W = W.copy()
+    W[0, 77] = np.nan
+    s = G.Solver(m, n_levels=3)
+    s.set_state(W, Winf)
+    with pytest.raises(G.GmgError) as e:
+        s.vcycle(1)
+    assert e.value.status == G.GMG_ENONFINITE
+    s.close()
+
+
+def test_torch_device_buffers(G):
+    """Device pointers are accepted at the boundary (cudaMemcpyDefault)."""
+    import torch
+    m, Winf, W = _case("box")
+    s = G.Solver(m, n_levels=2)
+    Wd = torch.from_numpy(W).cuda()
+    s.set_state(Wd, Winf)
+    out = torch.zeros_like(Wd)
+    G.gmg_get_state(s.ctx, 0, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), W)
+    s.close()
+
+
+@pytest.mark.slow
+def test_config4_full_size_vcycle(G, orc):
+    """BASELINE configs[3] (the bench workload) at full size: maps bit-exact
+    and one V-cycle (the bench's launch configuration) vs the oracle."""
+    m = configs.config(4)
+    fs = configs.FREESTREAM[4]
+    W = state.bow_shock(m, *fs)
+    Winf = state.winf(*fs)
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 1)
+    assert rel(Wg, Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
