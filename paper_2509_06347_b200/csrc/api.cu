@@ -143,7 +143,7 @@ void enqueue_vcycle(Launcher &Lc)
     if (ctx->opt.fine_smoother == 0) {
         enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_EXPLICIT, L0.W);         // Eq.(smo), A9
     } else {
-        enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | (df0 ? G_ALPHA : 0), nullptr);
+        enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | G_ZERO_DW | (df0 ? G_ALPHA : 0), nullptr);
         enqueue_sweeps<D>(Lc, 0, ctx->opt.n_sweeps, L0.W, L0.Rt, nullptr);
         Lc.pre(GMG_K_SWEEP);
         k_update<D><<<nblk((int64_t)L0.n * (D + 2)), 256, 0, Lc.s>>>(L0.n, L0.W, L0.dW);

@@ -30,6 +30,7 @@ enum : int {
     G_ALPHA = 64,     // alpha = prod alpha_f^{M_f}          (O5)
     G_PREPARE = 128,  // D, 1/D, alpha/2, per-slot S r       (O6)
     G_SIGMA = 256,    // store Sigma
+    G_ZERO_DW = 512,  // dW = 0 (start of a smoothing step, O7 step 1)
 };
 
 struct GArgs {
@@ -211,6 +212,10 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
             L.ha[i] = 0.5 * ai;
         }
         const size_t o = (size_t)i * NV;
+        if (a.flags & G_ZERO_DW) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) L.dW[o + q] = 0.0;
+        }
         if (a.flags & G_SET_F) {
 #pragma unroll
             for (int q = 0; q < NV; ++q) L.F[o + q] = L.Rs[o + q] - R[q];
