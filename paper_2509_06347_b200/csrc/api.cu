@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -71,13 +72,20 @@ struct Launcher {
 };
 
 template <int D>
-void enqueue_face(Launcher &Lc, int l, const double *W, bool flux)
+void enqueue_face(Launcher &Lc, int l, const double *W, bool flux, bool from_rec)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = ctx->dv[l];
+    constexpr int RS = Rec<D>::STRIDE, NV = D + 2;
     Lc.pre(GMG_K_FACE);
-    if (flux) k_face<D, true><<<nblk(L.nf), 256, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
-    else k_face<D, false><<<nblk(L.nf), 256, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+    const dim3 g(nblk(L.nf)), b(256);
+    if (flux) {
+        if (from_rec) k_face<D, true, RS><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+        else k_face<D, true, NV><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+    } else {
+        if (from_rec) k_face<D, false, RS><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+        else k_face<D, false, NV><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+    }
     Lc.post(GMG_K_FACE, flux ? ctx->lbytes[l].face_flux : ctx->lbytes[l].face_prep);
 }
 
@@ -97,23 +105,38 @@ void enqueue_gather(Launcher &Lc, int l, int flags, double *Wexp)
     }
 }
 
+template <int D, int LPC>
+void launch_sweep(const SweepArgs &a, cudaStream_t s)
+{
+    const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
+    k_sweep<D, LPC><<<nblk(nthreads), 256, 0, s>>>(a);
+}
+
+// n_sweeps x (forward colors 1..Nc, backward Nc..1), Algorithm 2;
+// the record's W_lin is the linearisation state, Wout (last backward pass)
+// receives W = W_lin + dW
 template <int D>
-void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, const double *Wlin, const double *rhs, double *Wout)
+void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, const double *rhs, double *Wout)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = ctx->dv[l];
     const HostLevel &H = ctx->lv[l];
-    const double gm1 = ctx->opt.gamma - 1.0;
+    const int lpc = ctx->lpc;
     for (int s = 0; s < n_sweeps; ++s) {
         for (int half = 0; half < 2; ++half) {
             for (int cc = 0; cc < H.ncolor; ++cc) {
-                const int c = half == 0 ? cc : H.ncolor - 1 - cc;     // Algorithm 2
-                const int cbeg = (int)H.blk[c], cend = (int)H.blk[c + 1];
+                const int c = half == 0 ? cc : H.ncolor - 1 - cc;
                 const bool last = (s == n_sweeps - 1) && half == 1;
-                double *wo = last ? Wout : nullptr;
+                SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.soff, L.sJ, L.sRec,
+                            rhs, last ? Wout : nullptr};
                 Lc.pre(GMG_K_SWEEP);
-                k_sweep<D><<<nblk(cend - cbeg), 256, 0, Lc.s>>>(L, cbeg, cend, gm1, Wlin, rhs, wo);
-                Lc.post(GMG_K_SWEEP, ctx->lbytes[l].sweep[c] + (wo ? ctx->lbytes[l].sweep_out[c] : 0.0));
+                switch (lpc) {
+                    case 1: launch_sweep<D, 1>(a, Lc.s); break;
+                    case 2: launch_sweep<D, 2>(a, Lc.s); break;
+                    case 8: launch_sweep<D, 8>(a, Lc.s); break;
+                    default: launch_sweep<D, 4>(a, Lc.s); break;
+                }
+                Lc.post(GMG_K_SWEEP, ctx->lbytes[l].sweep[c] + (a.Wout ? ctx->lbytes[l].sweep_out[c] : 0.0));
             }
         }
     }
@@ -139,30 +162,28 @@ void enqueue_vcycle(Launcher &Lc)
     DevLevel &L0 = ctx->dv[0];
     const bool df0 = ctx->opt.df_mode == 0;
     // 1-2. fine residual at the cycle start (history entry) + fine pre-smoothing
-    enqueue_face<D>(Lc, 0, L0.W, true);
+    enqueue_face<D>(Lc, 0, L0.W, true, false);
     if (ctx->opt.fine_smoother == 0) {
         enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_EXPLICIT, L0.W);         // Eq.(smo), A9
     } else {
-        enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | G_ZERO_DW | (df0 ? G_ALPHA : 0), nullptr);
-        enqueue_sweeps<D>(Lc, 0, ctx->opt.n_sweeps, L0.W, L0.Rt, nullptr);
-        Lc.pre(GMG_K_SWEEP);
-        k_update<D><<<nblk((int64_t)L0.n * (D + 2)), 256, 0, Lc.s>>>(L0.n, L0.W, L0.dW);
-        Lc.post(GMG_K_SWEEP, ctx->lbytes[0].update);
+        enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | G_ZERO_DW | G_COPY_W |
+                                     (df0 ? G_ALPHA : 0), nullptr);
+        enqueue_sweeps<D>(Lc, 0, ctx->opt.n_sweeps, L0.Rt, L0.W);
     }
     if (nl == 1) return;
     // 3. residual at the smoothed state (A10) -> restricted
-    enqueue_face<D>(Lc, 0, L0.W, true);
+    enqueue_face<D>(Lc, 0, L0.W, true, false);
     enqueue_gather<D>(Lc, 0, G_FLUX | G_WRITE_RT | (df0 ? G_ALPHA : 0), nullptr);
     // 4. coarse levels
     for (int l = 1; l < nl; ++l) {
         DevLevel &C = ctx->dv[l];
         const bool last = (l == nl - 1);
         enqueue_restrict<D>(Lc, l);                                       // W0, Res*, alpha, dW = 0
-        enqueue_face<D>(Lc, l, C.W0, !last);                              // R(W0) only if F is needed later
+        enqueue_face<D>(Lc, l, C.rec, !last, true);                       // R(W0) only if F is needed later
         enqueue_gather<D>(Lc, l, (last ? 0 : (G_FLUX | G_SET_F)) | G_PREPARE, nullptr);
-        enqueue_sweeps<D>(Lc, l, ctx->opt.n_sweeps, C.W0, C.Rs, C.W);    // RHS = Res* (A8)
+        enqueue_sweeps<D>(Lc, l, ctx->opt.n_sweeps, C.Rs, C.W);          // RHS = Res* (A8)
         if (!last) {
-            enqueue_face<D>(Lc, l, C.W, true);
+            enqueue_face<D>(Lc, l, C.W, true, false);
             enqueue_gather<D>(Lc, l, G_FLUX | G_WRITE_RT | G_ADD_F, nullptr);   // Rt = R(W) + F (A11)
         }
     }
@@ -177,7 +198,7 @@ template <int D>
 void enqueue_final_norm(Launcher &Lc)
 {
     gmg_ctx *ctx = Lc.ctx;
-    enqueue_face<D>(Lc, 0, ctx->dv[0].W, true);
+    enqueue_face<D>(Lc, 0, ctx->dv[0].W, true, false);
     enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM, nullptr);
 }
 
@@ -189,21 +210,23 @@ gmg_status check_ready(gmg_ctx *ctx, bool need_state = true)
     return GMG_OK;
 }
 
-// copy natural SoA (host or device) into internal AoS
-gmg_status put_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, double *dst)
+// copy natural SoA [ncomp][n] (host or device) into internal AoS (stride, offset)
+gmg_status put_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, double *dst, int stride = -1, int offset = 0)
 {
     const int64_t n = ctx->lv[l].n;
+    if (stride < 0) stride = ncomp;
     CK(cudaMemcpyAsync(ctx->d_stage, src, sizeof(double) * ncomp * n, cudaMemcpyDefault, ctx->stream));
-    k_to_internal<<<nblk(n), 256, 0, ctx->stream>>>((int)n, ncomp, ctx->dv[l].perm, ctx->d_stage, dst);
+    k_to_internal<<<nblk(n), 256, 0, ctx->stream>>>((int)n, ncomp, ctx->dv[l].perm, ctx->d_stage, dst, stride, offset);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));   // caller's host buffer may be released on return
     return GMG_OK;
 }
 
-gmg_status get_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, double *dst)
+gmg_status get_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, double *dst, int stride = -1, int offset = 0)
 {
     const int64_t n = ctx->lv[l].n;
-    k_to_natural<<<nblk(n), 256, 0, ctx->stream>>>((int)n, ncomp, ctx->dv[l].perm, src, ctx->d_stage);
+    if (stride < 0) stride = ncomp;
+    k_to_natural<<<nblk(n), 256, 0, ctx->stream>>>((int)n, ncomp, ctx->dv[l].perm, src, ctx->d_stage, stride, offset);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(dst, ctx->d_stage, sizeof(double) * ncomp * n, cudaMemcpyDefault, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -240,16 +263,16 @@ void carve(gmg_ctx *ctx, Bump &b)
         L.fA = b.take<double>((size_t)d * H.nf); L.fM = b.take<int8_t>(H.nf);
         L.Fs = b.take<double>((size_t)nv * H.nf); L.Srf = b.take<double>(H.nf); L.aM = b.take<double>(H.nf);
         L.vol = b.take<double>(H.n);
-        L.W = b.take<double>((size_t)nv * H.n); L.W0 = b.take<double>((size_t)nv * H.n);
-        L.dW = b.take<double>((size_t)nv * H.n); L.Rt = b.take<double>((size_t)nv * H.n);
+        L.W = b.take<double>((size_t)nv * H.n); L.Rt = b.take<double>((size_t)nv * H.n);
+        L.rec = b.take<double>((size_t)(d == 3 ? Rec<3>::STRIDE : Rec<2>::STRIDE) * H.n);
+        L.tmp = b.take<double>(H.n);
         L.Rs = b.take<double>((size_t)nv * H.n); L.F = b.take<double>((size_t)nv * H.n);
         L.alpha = b.take<double>(H.n); L.sigma = b.take<double>(H.n);
-        L.invD = b.take<double>(H.n); L.ha = b.take<double>(H.n);
         L.deg_int = b.take<uint8_t>(H.n); L.deg_all = b.take<uint8_t>(H.n);
-        L.gbase = b.take<int>(H.n); L.sbase = b.take<int>(H.n);
-        L.gface = b.take<int>(H.ng_entries); L.snbr = b.take<int>(H.ns_entries);
-        L.sA = b.take<double>((size_t)d * H.ns_entries); L.sSr = b.take<double>(H.ns_entries);
-        L.ns_entries = (int)H.ns_entries;
+        L.gbase = b.take<int>(H.n);
+        L.gface = b.take<int>(H.ng_entries);
+        L.soff = b.take<int>(H.n + 1); L.sJ = b.take<int>(H.ns_entries);
+        L.sRec = b.take<double>((size_t)kSlotRec * H.ns_entries);
         L.perm = b.take<int>(H.n);
         L.child = l > 0 ? b.take<int>(2 * H.n) : nullptr;
         L.parent = l + 1 < nl ? b.take<int>(H.n) : nullptr;
@@ -341,6 +364,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (!ctx) return GMG_ENOMEM;
     ctx->opt = *opt;
     ctx->stream = (cudaStream_t)opt->stream;
+    if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
     *out = ctx;
     return GMG_OK;
 }
@@ -519,10 +543,10 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         CK(up_raw(L.deg_int, H.deg_int.data(), H.n));
         CK(up_raw(L.deg_all, H.deg_all.data(), H.n));
         CK(up_raw(L.gbase, H.gbase.data(), H.n * sizeof(int)));
-        CK(up_raw(L.sbase, H.sbase.data(), H.n * sizeof(int)));
+        CK(up_raw(L.soff, H.soffc.data(), (H.n + 1) * sizeof(int)));
         CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
-        CK(up_raw(L.snbr, H.snbr.data(), H.snbr.size() * sizeof(int)));
-        CK(up_raw(L.sA, H.sA.data(), H.sA.size() * sizeof(double)));
+        CK(up_raw(L.sJ, H.sJ.data(), H.sJ.size() * sizeof(int)));
+        CK(up_raw(L.sRec, H.sRec.data(), H.sRec.size() * sizeof(double)));
         std::vector<int> perm(H.n);
         for (int64_t i = 0; i < H.n; ++i) perm[i] = (int)H.perm[i];
         CK(up_i(L.perm, std::move(perm)));
@@ -544,7 +568,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         }
         // alpha = 1 until set (df_mode 2 keeps it)
         k_fill<<<nblk(H.n), 256, 0, ctx->stream>>>((int)H.n, L.alpha, 1.0);
-        CK(cudaMemsetAsync(L.dW, 0, sizeof(double) * nv * H.n, ctx->stream));
+        CK(cudaMemsetAsync(L.rec, 0, sizeof(double) * (d == 3 ? Rec<3>::STRIDE : Rec<2>::STRIDE) * H.n, ctx->stream));
     }
     CK(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), ctx->stream));
     CK(cudaGetLastError());
@@ -610,19 +634,19 @@ gmg_status gmg_residual(gmg_ctx *ctx, int level, double *R_out, double *alpha_ou
     DevLevel &L = ctx->dv[level];
     // alpha is written to the Rs/F-free scratch "sigma" path: keep the level's alpha intact
     double *save_alpha = L.alpha;
-    L.alpha = L.invD;   // scratch (invD is recomputed by every prepare)
+    L.alpha = L.tmp;    // scratch: the level's own alpha stays intact
     if (ctx->opt.dim == 2) {
-        enqueue_face<2>(Lc, level, L.W, true);
+        enqueue_face<2>(Lc, level, L.W, true, false);
         enqueue_gather<2>(Lc, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
     } else {
-        enqueue_face<3>(Lc, level, L.W, true);
+        enqueue_face<3>(Lc, level, L.W, true, false);
         enqueue_gather<3>(Lc, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
     }
     L.alpha = save_alpha;
     CK(cudaGetLastError());
     const int nv = ctx->opt.dim + 2;
     if (R_out) { st = get_natural(ctx, level, L.Rt, nv, R_out); if (st) return st; }
-    if (alpha_out) { st = get_natural(ctx, level, L.invD, 1, alpha_out); if (st) return st; }
+    if (alpha_out) { st = get_natural(ctx, level, L.tmp, 1, alpha_out); if (st) return st; }
     if (sigma_out) { st = get_natural(ctx, level, L.sigma, 1, sigma_out); if (st) return st; }
     CK(cudaStreamSynchronize(ctx->stream));
     return GMG_OK;
@@ -648,18 +672,20 @@ gmg_status gmg_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out)
     Launcher Lc{ctx, ctx->stream};
     DevLevel &L = ctx->dv[level];
     const int nv = ctx->opt.dim + 2;
-    CK(cudaMemsetAsync(L.dW, 0, sizeof(double) * nv * L.n, ctx->stream));
+    const int gf = G_PREPARE | G_SIGMA | G_COPY_W | G_ZERO_DW;
     if (ctx->opt.dim == 2) {
-        enqueue_face<2>(Lc, level, L.W, false);
-        enqueue_gather<2>(Lc, level, G_PREPARE | G_SIGMA, nullptr);
-        enqueue_sweeps<2>(Lc, level, n_sweeps, L.W, L.Rt, nullptr);
+        enqueue_face<2>(Lc, level, L.W, false, false);
+        enqueue_gather<2>(Lc, level, gf, nullptr);
+        enqueue_sweeps<2>(Lc, level, n_sweeps, L.Rt, nullptr);
     } else {
-        enqueue_face<3>(Lc, level, L.W, false);
-        enqueue_gather<3>(Lc, level, G_PREPARE | G_SIGMA, nullptr);
-        enqueue_sweeps<3>(Lc, level, n_sweeps, L.W, L.Rt, nullptr);
+        enqueue_face<3>(Lc, level, L.W, false, false);
+        enqueue_gather<3>(Lc, level, gf, nullptr);
+        enqueue_sweeps<3>(Lc, level, n_sweeps, L.Rt, nullptr);
     }
     CK(cudaGetLastError());
-    if (dW_out) { st = get_natural(ctx, level, L.dW, nv, dW_out); if (st) return st; }
+    const int RS = ctx->opt.dim == 3 ? Rec<3>::STRIDE : Rec<2>::STRIDE;
+    const int RD = ctx->opt.dim == 3 ? Rec<3>::DW : Rec<2>::DW;
+    if (dW_out) { st = get_natural(ctx, level, L.rec, nv, dW_out, RS, RD); if (st) return st; }
     return GMG_OK;
 }
 
@@ -769,8 +795,8 @@ gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, doub
     cudaGraph_t g;
     cudaGraphExec_t ge;
     CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    if (ctx->opt.dim == 2) enqueue_sweeps<2>(Lc, level, n_sweeps, L.W, L.Rt, nullptr);
-    else enqueue_sweeps<3>(Lc, level, n_sweeps, L.W, L.Rt, nullptr);
+    if (ctx->opt.dim == 2) enqueue_sweeps<2>(Lc, level, n_sweeps, L.Rt, nullptr);
+    else enqueue_sweeps<3>(Lc, level, n_sweeps, L.Rt, nullptr);
     CK(cudaStreamEndCapture(cs, &g));
     CK(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);

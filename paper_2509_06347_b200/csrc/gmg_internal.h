@@ -36,16 +36,17 @@ struct HostLevel {
     std::vector<int64_t> parent;           // [n] natural -> natural coarse id (empty: coarsest)
     int64_t n_coarse = 0;
 
-    // SELL-32 layouts (internal order)
+    // layouts (internal order), see build_layout
     int64_t nchunks = 0;
-    std::vector<int32_t> chunk_base;       // [ncolor+1] first chunk of each color
-    std::vector<int32_t> goff, soff;       // [nchunks] entry offset of each chunk (gather / sweep)
+    std::vector<int32_t> chunk_base;       // [ncolor+1] first gather chunk of each color
+    std::vector<int32_t> goff;             // [nchunks] gather entry offset of each chunk
     int64_t ng_entries = 0, ns_entries = 0;
-    std::vector<int32_t> gbase, sbase;     // [n] entry of slot 0 of each internal cell (gather / sweep)
+    std::vector<int32_t> gbase;            // [n] gather entry of slot 0 (slot s at gbase + 32 s)
     std::vector<uint8_t> deg_int, deg_all; // [n] interior / all face slots
     std::vector<int32_t> gface;            // [ng_entries] signed face slot: +(f+1) left, -(f+1) right, 0 pad
-    std::vector<int32_t> snbr;             // [ns_entries] internal neighbour (-1 pad)
-    std::vector<double> sA;                // [dim][ns_entries] area vector outward from the cell
+    std::vector<int32_t> soffc;            // [n+1] sweep slots of cell i: [soffc[i], soffc[i+1])
+    std::vector<int32_t> sJ;               // [ns_entries] neighbour (internal)
+    std::vector<double> sRec;              // [ns_entries][4] (A_x, A_y, A_z | S r) 3D, (A_x, A_y, S r, 0) 2D
     std::vector<int32_t> sface;            // [ns_entries] face id of the slot (host bookkeeping)
 };
 
@@ -63,18 +64,18 @@ struct DevLevel {
     double *Fs;                  // [nf][nv]  S_f F_f (left -> right)
     double *Srf;                 // [nf]      S_f r_f
     double *aM;                  // [nf]      alpha_f^{M_f}
-    // cells
+    // cells (AoS [n][nv], internal order)
     const double *vol;           // [n]
-    double *W, *W0, *dW;         // [n][nv]
-    double *Rt, *Rs, *F;         // [n][nv]
-    double *alpha, *sigma, *invD, *ha;   // [n]
+    double *W;                   // [n][nv] state
+    double *Rt, *Rs, *F;         // [n][nv] RHS / restricted residual / forcing
+    double *alpha, *sigma, *tmp; // [n]
+    double *rec;                 // [n][REC] sweep record: W_lin | 1/D | dW | alpha/2 (kernels.cuh Rec<D>)
     const uint8_t *deg_int, *deg_all;    // [n]
-    const int *gbase, *sbase;    // [n] entry of slot 0; slot s at base + 32 s
+    const int *gbase;            // [n] gather entry of slot 0; slot s at gbase + 32 s
     const int *gface;            // gather entries
-    const int *snbr;             // sweep entries
-    const double *sA;            // [dim][ns_entries]
-    double *sSr;                 // [ns_entries]
-    int ns_entries;
+    const int *soff;             // [n+1] sweep slot range per cell
+    const int *sJ;               // [ns] neighbour
+    double *sRec;                // [ns][4] A (outward) + S r
     const int *perm;             // [n] internal -> natural
     // multigrid links
     const int *child;            // [2][n] fine children (internal idx in level-1), -1 = none (coarse levels)
@@ -120,6 +121,7 @@ struct gmg_ctx {
     std::vector<gmg::LevelBytes> lbytes;
     double kbytes[GMG_K_COUNT] = {0};   // algorithmic bytes accumulated by the recorded sequence
     int64_t launches = 0;          // kernels launched by the last recorded sequence
+    int lpc = 2;                   // sweep lanes per cell (1, 2, 4, 8)
     double *d_stage = nullptr;     // natural-order staging buffer [nv][nmax]
     std::vector<int> host_keep_alive;
 };

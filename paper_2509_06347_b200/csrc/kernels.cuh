@@ -3,14 +3,23 @@
 //
 // Every kernel is HBM/latency bound gather-streaming work; see DESIGN.md
 // "Kernels and rooflines".  Cell arrays are AoS [n][nv] in color-contiguous
-// internal order; sweep/gather slot tables are SELL-32 (one warp of cells per
-// chunk, entry of slot s = base + 32 s) so that slot streams coalesce.
+// internal order.  The sweep reads a per-cell 16-byte aligned record
+// Rec<D> = (W_lin | 1/D | dW | alpha/2) so that one neighbour gather touches
+// 3 (3D) / 2.5 (2D) sectors, and per-slot 32-byte records (A | S r).
 #pragma once
 #include <cuda_runtime.h>
 
 #include "gmg_internal.h"
 
 namespace gmg {
+
+// per-cell sweep record layout (doubles)
+template <int D> struct Rec;
+template <> struct Rec<3> { static constexpr int W = 0, INVD = 5, DW = 6, HA = 11, STRIDE = 12; };
+template <> struct Rec<2> { static constexpr int W = 0, DW = 4, INVD = 8, HA = 9, STRIDE = 12; };
+// (both 96 B: 32-byte aligned, so a neighbour record is three 256-bit loads)
+// per-slot record: A_0..A_{D-1}, S r at [D]
+constexpr int kSlotRec = 4;
 
 struct Phys {
     double gamma, gm1, K, omega;
@@ -28,9 +37,10 @@ enum : int {
     G_ADD_F = 16,
     G_SET_F = 32,     // F = Rs - R
     G_ALPHA = 64,     // alpha = prod alpha_f^{M_f}          (O5)
-    G_PREPARE = 128,  // D, 1/D, alpha/2, per-slot S r       (O6)
+    G_PREPARE = 128,  // 1/D, alpha/2 into the record, S r into the slot records (O6)
     G_SIGMA = 256,    // store Sigma
-    G_ZERO_DW = 512,  // dW = 0 (start of a smoothing step, O7 step 1)
+    G_ZERO_DW = 512,  // record dW = 0 (start of a smoothing step, O7 step 1)
+    G_COPY_W = 1024,  // record W_lin = W (fine-level smoothing)
 };
 
 struct GArgs {
@@ -40,12 +50,11 @@ struct GArgs {
     double *partial;
 };
 
-template <int D>
-__device__ __forceinline__ void ld_state(const double *__restrict__ p, int i, double *w)
+template <int NV>
+__device__ __forceinline__ void ld_vec(const double *__restrict__ q, double *w)
 {
-    const double *q = p + (size_t)i * (D + 2);
 #pragma unroll
-    for (int k = 0; k < D + 2; ++k) w[k] = __ldg(q + k);
+    for (int k = 0; k < NV; ++k) w[k] = __ldg(q + k);
 }
 
 template <int D>
@@ -106,9 +115,10 @@ __device__ __forceinline__ void kfvs_side(const double *w, const double *n, doub
 
 // ---------------------------------------------------------------------------
 // Face kernel (a6 + a10 per face): r_f = omega (|u.n| + a) of the average
-// state; with FLUX also S F_f (KFVS) and alpha_f^{M_f} (DF helper).
+// state; with FLUX also S F_f (KFVS) and alpha_f^{M_f} (DF helper).  The
+// state is read with a stride (NV for W, Rec<D>::STRIDE for the record).
 // ---------------------------------------------------------------------------
-template <int D, bool FLUX>
+template <int D, bool FLUX, int STRIDE>
 __global__ void __launch_bounds__(256) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
 {
     constexpr int NV = D + 2;
@@ -123,8 +133,8 @@ __global__ void __launch_bounds__(256) k_face(DevLevel L, const double *__restri
 #pragma unroll
     for (int k = 0; k < D; ++k) n[k] = A[k] * iS;
     double wl[NV], wr[NV];
-    ld_state<D>(Wsrc, l, wl);
-    if (r >= 0) ld_state<D>(Wsrc, r, wr);
+    ld_vec<NV>(Wsrc + (size_t)l * STRIDE, wl);
+    if (r >= 0) ld_vec<NV>(Wsrc + (size_t)r * STRIDE, wr);
     else ghost<D>(bc.kind[-r - 1], wl, bc, n, wr);
 
     // spectral radius of the conservative average (O6, reading A5)
@@ -177,12 +187,14 @@ template <int D>
 __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 {
     constexpr int NV = D + 2;
+    using RC = Rec<D>;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double R[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) R[q] = 0.0;
     if (i < L.n) {
-        const int gb = L.gbase[i], nt = L.deg_all[i], ni = L.deg_int[i], sb = L.sbase[i];
+        const int gb = L.gbase[i], nt = L.deg_all[i], ni = L.deg_int[i];
+        const int s0 = (a.flags & G_PREPARE) ? L.soff[i] : 0;
         double sig = 0.0, al = 1.0;
         for (int s = 0; s < nt; ++s) {
             const int sf = __ldg(L.gface + gb + kChunk * s);
@@ -200,21 +212,26 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
                 }
                 al *= __ldg(L.aM + f);
             }
-            if ((a.flags & G_PREPARE) && s < ni) L.sSr[sb + kChunk * s] = srf;
+            if ((a.flags & G_PREPARE) && s < ni) L.sRec[(size_t)(s0 + s) * kSlotRec + D] = srf;
         }
         if (a.flags & G_ALPHA) L.alpha[i] = al;
         if (a.flags & G_SIGMA) L.sigma[i] = sig;
+        double *rc = L.rec + (size_t)i * RC::STRIDE;
         if (a.flags & G_PREPARE) {
             const double ai = (a.flags & G_ALPHA) ? al : L.alpha[i];
             // D = alpha (V/Dt_imp + Sigma/2) + (1 - alpha) V/Dt_exp (O6, A2, A3)
             const double Dg = ai * (sig / a.cfl_imp + 0.5 * sig) + (1.0 - ai) * (sig / a.cfl_exp);
-            L.invD[i] = 1.0 / Dg;
-            L.ha[i] = 0.5 * ai;
+            rc[RC::INVD] = 1.0 / Dg;
+            rc[RC::HA] = 0.5 * ai;
         }
-        const size_t o = (size_t)i * NV;
         if (a.flags & G_ZERO_DW) {
 #pragma unroll
-            for (int q = 0; q < NV; ++q) L.dW[o + q] = 0.0;
+            for (int q = 0; q < NV; ++q) rc[RC::DW + q] = 0.0;
+        }
+        const size_t o = (size_t)i * NV;
+        if (a.flags & G_COPY_W) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) rc[RC::W + q] = L.W[o + q];
         }
         if (a.flags & G_SET_F) {
 #pragma unroll
@@ -283,13 +300,15 @@ __global__ void __launch_bounds__(256) k_norm_final(const double *__restrict__ p
 // current increments (reading A7):
 //   dW_i = -( Rt_i + alpha_i/2 sum_j [T(W_j+dW_j; A) - T(W_j; A) - S r dW_j] ) / D_i
 // with A = sigma S n (the Euler flux is linear in its normal, S T(W;n) = T(W;A)).
-// Same-color cells never neighbour each other, so the in-place update is race free.
+// LPC lanes per cell: each lane gathers its slots' neighbours (one dependent
+// index->record round trip), partial sums are combined with warp shuffles.
+// Same-color cells never neighbour each other, so the in-place dW update is
+// race free and neighbours' dW may be read through the non-coherent path.
 // ---------------------------------------------------------------------------
 template <int D>
 __device__ __forceinline__ void flux_diff(const double *w, const double *dw, const double *A, double gm1,
                                           double Sr, double *acc)
 {
-    // T(w; A) and T(w + dw; A)
     const double r0 = w[0], r1 = w[0] + dw[0];
     const double i0 = 1.0 / r0, i1 = 1.0 / r1;
     double mA0 = 0.0, mA1 = 0.0, m20 = 0.0, m21 = 0.0;
@@ -311,47 +330,132 @@ __device__ __forceinline__ void flux_diff(const double *w, const double *dw, con
     acc[D + 1] += (E1 + p1) * U1 - (E0 + p0) * U0 - Sr * dw[D + 1];
 }
 
-template <int D>
-__global__ void __launch_bounds__(256) k_sweep(DevLevel L, int cbeg, int cend, double gm1,
-                                               const double *__restrict__ Wlin, const double *__restrict__ rhs,
-                                               double *__restrict__ Wout)
+struct SweepArgs {
+    int cbeg, cend;
+    double gm1;
+    double *rec;               // [n][Rec::STRIDE]
+    const int *soff;           // [n+1]
+    const int *sJ;             // [ns]
+    const double *sRec;        // [ns][4]
+    const double *rhs;         // [n][nv]
+    double *Wout;              // [n][nv] or null: W = W_lin + dW (last backward half-sweep)
+};
+
+// 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256)
+__device__ __forceinline__ void ld4nc(const double *p, double *v)
 {
-    constexpr int NV = D + 2;
-    const int i = cbeg + blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cend) return;
-    const int sb = __ldg(L.sbase + i), ni = __ldg(L.deg_int + i);
-    double acc[NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-    const double *dWr = L.dW;   // neighbours' increments: written only by earlier launches
-    for (int s = 0; s < ni; ++s) {
-        const int e = sb + kChunk * s;
-        const int j = __ldg(L.snbr + e);
-        double A[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) A[k] = __ldg(L.sA + (size_t)k * L.ns_entries + e);
-        const double Sr = __ldg(L.sSr + e);
-        double w[NV], dw[NV];
-        ld_state<D>(Wlin, j, w);
-        ld_state<D>(dWr, j, dw);
-        flux_diff<D>(w, dw, A, gm1, Sr, acc);
-    }
-    const double invD = __ldg(L.invD + i), ha = __ldg(L.ha + i);
-    const size_t o = (size_t)i * NV;
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-        const double d = -(__ldg(rhs + o + q) + ha * acc[q]) * invD;
-        L.dW[o + q] = d;
-        if (Wout) Wout[o + q] = __ldg(Wlin + o + q) + d;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld4cs(const double *p, double *v)
+{
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void st4(double *p, const double *v)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+
+// neighbour record -> (W_lin, dW)
+template <int D>
+__device__ __forceinline__ void ld_neighbour(const double *rj, double *w, double *dw)
+{
+    if constexpr (D == 3) {
+        double c0[4], c1[4], c2[4];
+        ld4nc(rj, c0);
+        ld4nc(rj + 4, c1);
+        ld4nc(rj + 8, c2);
+        w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
+        dw[0] = c1[2]; dw[1] = c1[3]; dw[2] = c2[0]; dw[3] = c2[1]; dw[4] = c2[2];
+    } else {
+        ld4nc(rj, w);
+        ld4nc(rj + 4, dw);
     }
 }
 
-// restriction to a coarse level (a8, A15) + dW = 0 for its sweeps
+template <int D, int LPC>
+__global__ void __launch_bounds__(256) k_sweep(SweepArgs a)
+{
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = a.cbeg + g / LPC;
+    const int sub = g % LPC;
+    const bool valid = i < a.cend;
+    double acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+    if (valid) {
+        const int e0 = __ldg(a.soff + i), e1 = __ldg(a.soff + i + 1);
+        for (int e = e0 + sub; e < e1; e += LPC) {
+            const int j = __ldcs(a.sJ + e);
+            double sr[4];
+            ld4cs(a.sRec + (size_t)e * kSlotRec, sr);
+            double w[NV], dw[NV];
+            ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
+            flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+        }
+    }
+    if (LPC > 1) {
+#pragma unroll
+        for (int o = LPC / 2; o > 0; o >>= 1) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+        }
+    }
+    if (valid && sub == 0) {
+        double *ri = a.rec + (size_t)i * RC::STRIDE;
+        const size_t o = (size_t)i * NV;
+        double r[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
+        if constexpr (D == 3) {
+            double c0[4], c1[4], c2[4];
+            ld4nc(ri + 4, c1);                          // W[4], 1/D, dW0, dW1
+            ld4nc(ri + 8, c2);                          // dW2, dW3, dW4, alpha/2
+            const double invD = c1[1], ha = c2[3];
+            double d[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+            c1[2] = d[0]; c1[3] = d[1]; c2[0] = d[2]; c2[1] = d[3]; c2[2] = d[4];
+            st4(ri + 4, c1);
+            st4(ri + 8, c2);
+            if (a.Wout) {
+                ld4nc(ri, c0);
+                a.Wout[o + 0] = c0[0] + d[0];
+                a.Wout[o + 1] = c0[1] + d[1];
+                a.Wout[o + 2] = c0[2] + d[2];
+                a.Wout[o + 3] = c0[3] + d[3];
+                a.Wout[o + 4] = c1[0] + d[4];
+            }
+        } else {
+            double c2[4];
+            ld4nc(ri + 8, c2);                          // 1/D, alpha/2, -, -
+            const double invD = c2[0], ha = c2[1];
+            double d[4];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+            st4(ri + 4, d);
+            if (a.Wout) {
+                double c0[4];
+                ld4nc(ri, c0);
+#pragma unroll
+                for (int q = 0; q < NV; ++q) a.Wout[o + q] = c0[q] + d[q];
+            }
+        }
+    }
+}
+
+// restriction to a coarse level (a8, A15) into the coarse record's
+// W_lin, plus dW = 0 for its sweeps
 template <int D>
 __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const double *__restrict__ Wf,
                                                   const double *__restrict__ Rf)
 {
     constexpr int NV = D + 2;
+    using RC = Rec<D>;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C.n) return;
     const int k0 = C.child[c], k1 = C.child[C.n + c];
@@ -366,10 +470,11 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
         for (int q = 0; q < NV; ++q) { w[q] = w[q] + V1 * Wf[(size_t)k1 * NV + q]; r[q] = r[q] + Rf[(size_t)k1 * NV + q]; }
         a = fmin(a, Fn.alpha[k1]);
     }
-    const double iv = C.vol[c];
+    const double vc = C.vol[c];
+    double *rc = C.rec + (size_t)c * RC::STRIDE;
     const size_t o = (size_t)c * NV;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) { C.W0[o + q] = w[q] / iv; C.Rs[o + q] = r[q]; C.dW[o + q] = 0.0; }
+    for (int q = 0; q < NV; ++q) { rc[RC::W + q] = w[q] / vc; C.Rs[o + q] = r[q]; rc[RC::DW + q] = 0.0; }
     C.alpha[c] = a;
 }
 
@@ -379,47 +484,42 @@ template <int D>
 __global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLevel C2, int nl)
 {
     constexpr int NV = D + 2;
+    using RC = Rec<D>;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= F0.n) return;
     const int p = F0.parent[i];
     double corr[NV];
+    const double *r1 = C1.rec + (size_t)p * RC::STRIDE + RC::DW;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) corr[q] = C1.dW[(size_t)p * NV + q];
+    for (int q = 0; q < NV; ++q) corr[q] = r1[q];
     if (nl >= 3) {
         const int pp = C1.parent[p];
         const double a1 = C1.alpha[p];
+        const double *r2 = C2.rec + (size_t)pp * RC::STRIDE + RC::DW;
 #pragma unroll
-        for (int q = 0; q < NV; ++q) corr[q] += a1 * C2.dW[(size_t)pp * NV + q];
+        for (int q = 0; q < NV; ++q) corr[q] += a1 * r2[q];
     }
     const double a0 = F0.alpha[i];
 #pragma unroll
     for (int q = 0; q < NV; ++q) F0.W[(size_t)i * NV + q] += a0 * corr[q];
 }
 
-template <int D>
-__global__ void k_update(int n, double *__restrict__ W, const double *__restrict__ dW)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n * (D + 2)) return;
-    W[i] += dW[i];
-}
-
-// natural SoA [nv][n]  <->  internal AoS [n][nv]
-__global__ void k_to_internal(int n, int nv, const int *__restrict__ perm, const double *__restrict__ src,
-                              double *__restrict__ dst)
+// natural SoA [ncomp][n]  <->  internal AoS (stride, offset)
+__global__ void k_to_internal(int n, int ncomp, const int *__restrict__ perm, const double *__restrict__ src,
+                              double *__restrict__ dst, int stride, int offset)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int nat = perm[i];
-    for (int q = 0; q < nv; ++q) dst[(size_t)i * nv + q] = src[(size_t)q * n + nat];
+    for (int q = 0; q < ncomp; ++q) dst[(size_t)i * stride + offset + q] = src[(size_t)q * n + nat];
 }
-__global__ void k_to_natural(int n, int nv, const int *__restrict__ perm, const double *__restrict__ src,
-                             double *__restrict__ dst)
+__global__ void k_to_natural(int n, int ncomp, const int *__restrict__ perm, const double *__restrict__ src,
+                             double *__restrict__ dst, int stride, int offset)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int nat = perm[i];
-    for (int q = 0; q < nv; ++q) dst[(size_t)q * n + nat] = src[(size_t)i * nv + q];
+    for (int q = 0; q < ncomp; ++q) dst[(size_t)q * n + nat] = src[(size_t)i * stride + offset + q];
 }
 __global__ void k_fill(int n, double *p, double v)
 {

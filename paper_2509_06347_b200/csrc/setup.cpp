@@ -350,10 +350,14 @@ void build_coarse(const HostLevel &fine, HostLevel &C)
     }
 }
 
-// SELL-32 layouts: per color, chunks of 32 consecutive internal cells; a
-// chunk's entries are [slot][lane] with the chunk padded to its max degree.
-// Gather slots: interior faces (ascending id) then boundary faces; sweep
-// slots: the interior ones, same order.
+// Layouts (internal order).
+//  * gather slots (residual/prepare, thread per cell): SELL-32 -- per color,
+//    chunks of 32 consecutive cells, entries [slot][lane], chunk padded to its
+//    max degree.  Slots: interior faces (ascending id) then boundary faces.
+//  * sweep slots (lanes per cell): CSR -- cell i's interior slots are
+//    contiguous at [soffc[i], soffc[i+1]), same order as its gather slots;
+//    per slot the neighbour sJ and a 32-byte record (A_x, A_y, [A_z,] S r)
+//    with A = sigma S n oriented outward from the cell.
 void build_layout(HostLevel &L)
 {
     const int d = L.dim;
@@ -365,10 +369,9 @@ void build_layout(HostLevel &L)
     }
     L.nchunks = L.chunk_base[L.ncolor];
     L.gbase.assign(L.n, 0);
-    L.sbase.assign(L.n, 0);
-    std::vector<int32_t> cchunk(L.n, 0);
     L.deg_int.assign(L.n, 0);
     L.deg_all.assign(L.n, 0);
+    std::vector<int32_t> cchunk(L.n, 0);
     std::vector<std::vector<int64_t>> slots(L.n);
     for (int c = 0; c < L.ncolor; ++c) {
         for (int64_t i = L.blk[c]; i < L.blk[c + 1]; ++i) {
@@ -387,45 +390,44 @@ void build_layout(HostLevel &L)
         }
     }
     L.goff.assign(L.nchunks, 0);
-    L.soff.assign(L.nchunks, 0);
-    int64_t go = 0, so = 0;
+    int64_t go = 0;
     for (int c = 0; c < L.ncolor; ++c) {
         for (int32_t k = L.chunk_base[c]; k < L.chunk_base[c + 1]; ++k) {
             const int64_t i0 = L.blk[c] + (int64_t)(k - L.chunk_base[c]) * kChunk;
             const int64_t i1 = std::min<int64_t>(i0 + kChunk, L.blk[c + 1]);
-            int mg = 0, ms = 0;
-            for (int64_t i = i0; i < i1; ++i) { mg = std::max<int>(mg, L.deg_all[i]); ms = std::max<int>(ms, L.deg_int[i]); }
+            int mg = 0;
+            for (int64_t i = i0; i < i1; ++i) mg = std::max<int>(mg, L.deg_all[i]);
             L.goff[k] = (int32_t)go;
-            L.soff[k] = (int32_t)so;
             go += (int64_t)mg * kChunk;
-            so += (int64_t)ms * kChunk;
         }
     }
-    if (go >= INT32_MAX || so >= INT32_MAX) throw std::runtime_error("slot table exceeds int32");
+    L.soffc.assign(L.n + 1, 0);
+    for (int64_t i = 0; i < L.n; ++i) L.soffc[i + 1] = L.soffc[i] + L.deg_int[i];
+    const int64_t so = L.soffc[L.n];
+    if (go >= INT32_MAX || so >= INT32_MAX / 4) throw std::runtime_error("slot table exceeds int32");
     L.ng_entries = go;
     L.ns_entries = so;
     L.gface.assign(go, 0);
-    L.snbr.assign(so, -1);
+    L.sJ.assign(so, -1);
     L.sface.assign(so, -1);
-    L.sA.assign((size_t)d * so, 0.0);
+    L.sRec.assign((size_t)4 * so, 0.0);
     for (int c = 0; c < L.ncolor; ++c)
     for (int64_t i = L.blk[c]; i < L.blk[c + 1]; ++i) {
         const int32_t k = cchunk[i];
         const int64_t lane = (i - L.blk[c]) % kChunk;
         L.gbase[i] = (int32_t)(L.goff[k] + lane);
-        L.sbase[i] = (int32_t)(L.soff[k] + lane);
         const int64_t nat = L.perm[i];
         for (size_t s = 0; s < slots[i].size(); ++s) {
             const int64_t f = slots[i][s];
             const bool is_left = (L.left[f] == nat);
             L.gface[L.goff[k] + s * kChunk + lane] = is_left ? (int32_t)(f + 1) : -(int32_t)(f + 1);
             if (s < L.deg_int[i]) {
-                const int64_t e = L.soff[k] + s * kChunk + lane;
+                const int64_t e = L.soffc[i] + (int64_t)s;
                 const int64_t other = is_left ? L.right[f] : L.left[f];
-                L.snbr[e] = (int32_t)L.iperm[other];
+                L.sJ[e] = (int32_t)L.iperm[other];
                 L.sface[e] = (int32_t)f;
                 const double sg = is_left ? 1.0 : -1.0;
-                for (int q = 0; q < d; ++q) L.sA[(size_t)q * so + e] = sg * L.avec[(size_t)q * L.nf + f];
+                for (int q = 0; q < d; ++q) L.sRec[(size_t)4 * e + q] = sg * L.avec[(size_t)q * L.nf + f];
             }
         }
     }
