@@ -105,11 +105,39 @@ void enqueue_gather(Launcher &Lc, int l, int flags, double *Wexp)
     }
 }
 
+// optional L2 access-policy window over the level's cell records (the
+// gathered data), attached per launch so that graph capture keeps it
+template <class K>
+void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArgs &a, const void *win, size_t win_bytes)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    if (win && win_bytes) {
+        at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[0].val.accessPolicyWindow.base_ptr = const_cast<void *>(win);
+        at[0].val.accessPolicyWindow.num_bytes = win_bytes;
+        at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 template <int D, int LPC>
-void launch_sweep(const SweepArgs &a, cudaStream_t s)
+void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win = nullptr, size_t win_bytes = 0)
 {
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
-    k_sweep<D, LPC><<<nblk(nthreads), 256, 0, s>>>(a);
+    const dim3 g(nblk(nthreads)), b(256);
+    switch (minb) {
+        case 6: launch_with_window(k_sweep<D, LPC, 6>, g, b, s, a, win, win_bytes); break;
+        case 8: launch_with_window(k_sweep<D, LPC, 8>, g, b, s, a, win, win_bytes); break;
+        default: launch_with_window(k_sweep<D, LPC, 4>, g, b, s, a, win, win_bytes); break;
+    }
 }
 
 // n_sweeps x (forward colors 1..Nc, backward Nc..1), Algorithm 2;
@@ -128,13 +156,25 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, const double *rhs, double
                 const int c = half == 0 ? cc : H.ncolor - 1 - cc;
                 const bool last = (s == n_sweeps - 1) && half == 1;
                 SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.soff, L.sJ, L.sRec,
-                            rhs, last ? Wout : nullptr};
+                            rhs, last ? Wout : nullptr, ctx->prefetch, 0};
                 Lc.pre(GMG_K_SWEEP);
-                switch (lpc) {
-                    case 1: launch_sweep<D, 1>(a, Lc.s); break;
-                    case 2: launch_sweep<D, 2>(a, Lc.s); break;
-                    case 8: launch_sweep<D, 8>(a, Lc.s); break;
-                    default: launch_sweep<D, 4>(a, Lc.s); break;
+                const int ncell = a.cend - a.cbeg;
+                if (ctx->sweep_mode == 1 || ctx->sweep_mode == 2) {
+                    const int C = ctx->sweep_mode == 1 ? 64 : 128;
+                    a.max_slots = C == 64 ? ctx->lbytes[l].max_slots64 : ctx->lbytes[l].max_slots128;
+                    const size_t smem = (size_t)a.max_slots * (Rec<D>::STRIDE + kSlotRec) * sizeof(double);
+                    if (C == 64) k_sweep_sm<D, 64><<<(ncell + 63) / 64, 64, smem, Lc.s>>>(a);
+                    else k_sweep_sm<D, 128><<<(ncell + 127) / 128, 128, smem, Lc.s>>>(a);
+                } else {
+                    const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
+                    const size_t wb = ctx->l2_window
+                                          ? std::min<size_t>(ctx->l2_window, (size_t)L.n * Rec<D>::STRIDE * sizeof(double))
+                                          : 0;
+                    switch (lpc) {
+                        case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb); break;
+                        case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb); break;
+                        default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb); break;
+                    }
                 }
                 Lc.post(GMG_K_SWEEP, ctx->lbytes[l].sweep[c] + (a.Wout ? ctx->lbytes[l].sweep_out[c] : 0.0));
             }
@@ -318,6 +358,16 @@ void compute_bytes(gmg_ctx *ctx)
         B.prolong = (double)H.n * (2 * nv * 8 + 8 + 4) + (nl > 1 ? (double)ctx->lv[1].n * (nv * 8 + 12) : 0) +
                     (nl > 2 ? (double)ctx->lv[2].n * nv * 8 : 0);
         B.update = (double)H.n * 3 * nv * 8;
+        // smem staging: max slots of any C-cell chunk within a color block
+        for (int C : {64, 128}) {
+            int mx = 0;
+            for (int c = 0; c < H.ncolor; ++c)
+                for (int64_t i0 = H.blk[c]; i0 < H.blk[c + 1]; i0 += C) {
+                    const int64_t i1 = std::min<int64_t>(i0 + C, H.blk[c + 1]);
+                    mx = std::max<int>(mx, H.soffc[i1] - H.soffc[i0]);
+                }
+            (C == 64 ? B.max_slots64 : B.max_slots128) = std::max(mx, 1);
+        }
     }
 }
 
@@ -365,6 +415,9 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     ctx->opt = *opt;
     ctx->stream = (cudaStream_t)opt->stream;
     if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
+    if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
+    if (const char *e = std::getenv("GMG_PREFETCH")) ctx->prefetch = std::atoi(e);
+    if (const char *e = std::getenv("GMG_SWEEP")) ctx->sweep_mode = std::atoi(e);
     *out = ctx;
     return GMG_OK;
 }
@@ -574,6 +627,25 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+    if (const char *e = std::getenv("GMG_L2PERSIST")) {   // experimental: persisting-L2 window over records
+        if (std::atoi(e) > 0) {
+            int maxp = 0, maxw = 0;
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->opt.device);
+            cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, ctx->opt.device);
+            CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
+            ctx->l2_window = std::min<size_t>((size_t)maxw, (size_t)maxp);
+            std::fprintf(stderr, "gmg: persisting L2 %d B, max window %d B\n", maxp, maxw);
+        }
+    }
+    {   // dynamic shared memory of the staged sweep (may exceed the 48 KB default)
+        int mx = 1;
+        for (auto &B : ctx->lbytes) mx = std::max(mx, std::max(B.max_slots64, B.max_slots128));
+        const int bytes_sm = mx * (Rec<3>::STRIDE + kSlotRec) * (int)sizeof(double);
+        CK(cudaFuncSetAttribute(k_sweep_sm<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
+        CK(cudaFuncSetAttribute(k_sweep_sm<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
+        CK(cudaFuncSetAttribute(k_sweep_sm<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
+        CK(cudaFuncSetAttribute(k_sweep_sm<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
+    }
     ctx->ws_ready = true;
     ctx->state_set = false;
     return GMG_OK;

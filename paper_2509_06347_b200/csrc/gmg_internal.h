@@ -92,6 +92,7 @@ struct Profile {
 // algorithmic bytes bookkeeping
 struct LevelBytes {
     double face_flux = 0, face_prep = 0, gather = 0, restrict_ = 0, prolong = 0, update = 0;
+    int max_slots64 = 1, max_slots128 = 1;   // staged sweep: max slots per 64 / 128-cell chunk
     std::vector<double> sweep;     // per color
     std::vector<double> sweep_out; // per color, extra bytes when the launch also writes W = W0 + dW
 };
@@ -121,7 +122,11 @@ struct gmg_ctx {
     std::vector<gmg::LevelBytes> lbytes;
     double kbytes[GMG_K_COUNT] = {0};   // algorithmic bytes accumulated by the recorded sequence
     int64_t launches = 0;          // kernels launched by the last recorded sequence
-    int lpc = 2;                   // sweep lanes per cell (1, 2, 4, 8)
+    int lpc = 2;                   // sweep lanes per cell (1, 2, 4)
+    int minb = 4;                  // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
+    int prefetch = 0;              // sweep: L2-prefetch neighbour records before gathering (slower; kept for experiments)
+    int sweep_mode = 0;            // 0 = register gather (lpc lanes/cell), 1/2 = smem-staged 64/128-cell chunks
+    size_t l2_window = 0;          // bytes of the persisting-L2 window over a level's records (0 = off)
     double *d_stage = nullptr;     // natural-order staging buffer [nv][nmax]
     std::vector<int> host_keep_alive;
 };

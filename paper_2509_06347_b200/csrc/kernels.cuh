@@ -339,6 +339,8 @@ struct SweepArgs {
     const double *sRec;        // [ns][4]
     const double *rhs;         // [n][nv]
     double *Wout;              // [n][nv] or null: W = W_lin + dW (last backward half-sweep)
+    int prefetch;              // issue L2 prefetches of neighbour records first
+    int max_slots;             // k_sweep_sm: max slots of any chunk of this level (smem sizing)
 };
 
 // 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256)
@@ -375,8 +377,56 @@ __device__ __forceinline__ void ld_neighbour(const double *rj, double *w, double
     }
 }
 
-template <int D, int LPC>
-__global__ void __launch_bounds__(256) k_sweep(SweepArgs a)
+// own-cell epilogue: dW_i = -(rhs_i + alpha_i/2 acc) / D_i into the record,
+// and W = W_lin + dW on the last backward half-sweep
+template <int D>
+__device__ __forceinline__ void sweep_finish(const SweepArgs &a, int i, const double *acc)
+{
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    double *ri = a.rec + (size_t)i * RC::STRIDE;
+    const size_t o = (size_t)i * NV;
+    double r[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
+    if constexpr (D == 3) {
+        double c0[4], c1[4], c2[4];
+        ld4nc(ri + 4, c1);                          // W[4], 1/D, dW0, dW1
+        ld4nc(ri + 8, c2);                          // dW2, dW3, dW4, alpha/2
+        const double invD = c1[1], ha = c2[3];
+        double d[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+        c1[2] = d[0]; c1[3] = d[1]; c2[0] = d[2]; c2[1] = d[3]; c2[2] = d[4];
+        st4(ri + 4, c1);
+        st4(ri + 8, c2);
+        if (a.Wout) {
+            ld4nc(ri, c0);
+            a.Wout[o + 0] = c0[0] + d[0];
+            a.Wout[o + 1] = c0[1] + d[1];
+            a.Wout[o + 2] = c0[2] + d[2];
+            a.Wout[o + 3] = c0[3] + d[3];
+            a.Wout[o + 4] = c1[0] + d[4];
+        }
+    } else {
+        double c2[4];
+        ld4nc(ri + 8, c2);                          // 1/D, alpha/2, -, -
+        const double invD = c2[0], ha = c2[1];
+        double d[4];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+        st4(ri + 4, d);
+        if (a.Wout) {
+            double c0[4];
+            ld4nc(ri, c0);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) a.Wout[o + q] = c0[q] + d[q];
+        }
+    }
+}
+
+template <int D, int LPC, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 {
     constexpr int NV = D + 2;
     using RC = Rec<D>;
@@ -389,8 +439,29 @@ __global__ void __launch_bounds__(256) k_sweep(SweepArgs a)
     for (int q = 0; q < NV; ++q) acc[q] = 0.0;
     if (valid) {
         const int e0 = __ldg(a.soff + i), e1 = __ldg(a.soff + i + 1);
+        if (a.prefetch) {
+            // phase A: all of this lane's neighbour indices at once, then L2
+            // prefetches of their records and of the cell's own data, so the
+            // real loads below wait on L2, not on a chain of DRAM latencies
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rhs + (size_t)i * NV));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + (size_t)i * RC::STRIDE + 4));
+            int jj[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int e = e0 + sub + k * LPC;
+                jj[k] = e < e1 ? __ldg(a.sJ + e) : -1;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (jj[k] >= 0) {
+                    const double *rj = a.rec + (size_t)jj[k] * RC::STRIDE;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rj));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rj + RC::STRIDE - 1));
+                }
+            }
+        }
         for (int e = e0 + sub; e < e1; e += LPC) {
-            const int j = __ldcs(a.sJ + e);
+            const int j = __ldg(a.sJ + e);
             double sr[4];
             ld4cs(a.sRec + (size_t)e * kSlotRec, sr);
             double w[NV], dw[NV];
@@ -405,47 +476,65 @@ __global__ void __launch_bounds__(256) k_sweep(SweepArgs a)
             for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
         }
     }
-    if (valid && sub == 0) {
-        double *ri = a.rec + (size_t)i * RC::STRIDE;
-        const size_t o = (size_t)i * NV;
-        double r[NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
-        if constexpr (D == 3) {
-            double c0[4], c1[4], c2[4];
-            ld4nc(ri + 4, c1);                          // W[4], 1/D, dW0, dW1
-            ld4nc(ri + 8, c2);                          // dW2, dW3, dW4, alpha/2
-            const double invD = c1[1], ha = c2[3];
-            double d[NV];
-#pragma unroll
-            for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-            c1[2] = d[0]; c1[3] = d[1]; c2[0] = d[2]; c2[1] = d[3]; c2[2] = d[4];
-            st4(ri + 4, c1);
-            st4(ri + 8, c2);
-            if (a.Wout) {
-                ld4nc(ri, c0);
-                a.Wout[o + 0] = c0[0] + d[0];
-                a.Wout[o + 1] = c0[1] + d[1];
-                a.Wout[o + 2] = c0[2] + d[2];
-                a.Wout[o + 3] = c0[3] + d[3];
-                a.Wout[o + 4] = c1[0] + d[4];
-            }
-        } else {
-            double c2[4];
-            ld4nc(ri + 8, c2);                          // 1/D, alpha/2, -, -
-            const double invD = c2[0], ha = c2[1];
-            double d[4];
-#pragma unroll
-            for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-            st4(ri + 4, d);
-            if (a.Wout) {
-                double c0[4];
-                ld4nc(ri, c0);
-#pragma unroll
-                for (int q = 0; q < NV; ++q) a.Wout[o + q] = c0[q] + d[q];
-            }
-        }
+    if (valid && sub == 0) sweep_finish<D>(a, i, acc);
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory staged variant: one CTA per chunk of C consecutive cells of
+// the color.  Phase 1 issues cp.async (LDGSTS, no registers held) for every
+// slot's neighbour record (6 x 16 B) and slot record (2 x 16 B) of the chunk;
+// phase 2 computes thread-per-cell from shared memory.  Memory-level
+// parallelism is set by the chunk's bytes in flight, not by registers.
+// Dynamic smem: max_slots * (96 + 32) bytes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+template <int D, int C>
+__global__ void __launch_bounds__(C) k_sweep_sm(SweepArgs a)
+{
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    extern __shared__ __align__(16) double sm[];
+    const int c0 = a.cbeg + blockIdx.x * C;
+    const int c1 = min(c0 + C, a.cend);
+    const int e0 = __ldg(a.soff + c0), e1 = __ldg(a.soff + c1);
+    const int ns = e1 - e0;
+    double *recS = sm;                                    // [ns][12]
+    double *slotS = sm + (size_t)a.max_slots * RC::STRIDE; // [ns][4]
+    for (int it = threadIdx.x; it < ns * 6; it += C) {
+        const int s = it / 6, p = it - 6 * (it / 6);
+        const int j = __ldg(a.sJ + e0 + s);
+        cp_async16(recS + (size_t)s * RC::STRIDE + 2 * p, a.rec + (size_t)j * RC::STRIDE + 2 * p);
     }
+    for (int it = threadIdx.x; it < ns * 2; it += C)
+        cp_async16(slotS + 2 * it, a.sRec + (size_t)e0 * kSlotRec + 2 * it);
+    cp_async_wait_all();
+    __syncthreads();
+    const int i = c0 + threadIdx.x;
+    if (i >= c1) return;
+    double acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+    const int s0 = __ldg(a.soff + i) - e0, s1 = __ldg(a.soff + i + 1) - e0;
+    for (int s = s0; s < s1; ++s) {
+        const double *r = recS + (size_t)s * RC::STRIDE;
+        const double *sr = slotS + (size_t)s * kSlotRec;
+        double w[NV], dw[NV], A[D];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) { w[q] = r[RC::W + q]; dw[q] = r[RC::DW + q]; }
+#pragma unroll
+        for (int k = 0; k < D; ++k) A[k] = sr[k];
+        flux_diff<D>(w, dw, A, a.gm1, sr[D], acc);
+    }
+    sweep_finish<D>(a, i, acc);
 }
 
 // restriction to a coarse level (a8, A15) into the coarse record's
