@@ -26,8 +26,14 @@
  *    returns host data synchronizes that stream first.
  *  - Errors: return codes only; no exceptions cross the ABI.  A failing
  *    call leaves a message in gmg_last_error(ctx).
- *  - Multi-rank (nranks > 1): collective semantics, every rank makes the same
- *    sequence of calls with the same global mesh.
+ *  - Multi-rank (nranks > 1): collective semantics, every rank
+ *    makes the same sequence of calls with the same global mesh and the same
+ *    part[] array.  Every rank builds the identical global hierarchy (colors
+ *    are global, agglomeration never crosses a partition face) and
+ *    works on its owned cells plus one ghost layer; increments are exchanged
+ *    after every color (NCCL send/recv), states after state changes, norms
+ *    are all-reduced.  Natural-order outputs of multi-rank calls write only
+ *    the caller rank's owned entries.
  * ---------------------------------------------------------------------------
  */
 #ifndef GMG_H
@@ -75,6 +81,11 @@ typedef struct {
     const void *nccl_id;    /* 128-byte ncclUniqueId (nranks > 1), else NULL                  */
     int device;             /* CUDA device ordinal                                            */
     void *stream;           /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)    */
+    int local_domains;      /* nranks == 1 only: drive this many partitions (part[] values
+                               0..local_domains-1) as separate domains in this process, their
+                               halo exchanged by device copies on the stream.  Same layouts,
+                               plans, pack/unpack kernels and exchange points as the NCCL path;
+                               used to test the partitioned path on one GPU.  Default 1.      */
 } gmg_options;
 
 /* Fill *o with the defaults above (dim = 3, single rank, device 0, stream 0). */
@@ -185,6 +196,22 @@ gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, doub
 
 /* Number of kernels one V-cycle launches (graph nodes). */
 int64_t gmg_vcycle_launches(gmg_ctx *ctx);
+
+/* a5: recursive coordinate bisection of the cell centroids (host, natural
+ * order; centroid[dim][n]) into nparts partitions -> part_out[n] in
+ * 0..nparts-1.  Deterministic (ties broken by natural id), so every rank
+ * computes the same partition.  Pure host function, no context needed. */
+gmg_status gmg_partition_rcb(int64_t n_cells, int dim, const double *centroid, int nparts, int32_t *part_out);
+
+/* a5/a13: halo plan of local domain `dom` (0 when nranks > 1) on `level`,
+ * for tests.  Sizes first (any pointer NULL): *n_owned, *n_ghost, *n_peers,
+ * *n_send, *n_recv.  Then (all non-NULL) the natural ids of the owned cells
+ * (local order), of the ghosts, the peer ranks, and the send / recv lists as
+ * natural ids with their group offsets send_off/recv_off[n_colors*n_peers+1]
+ * (groups ordered (color, peer), natural id ascending inside a group). */
+gmg_status gmg_get_halo(gmg_ctx *ctx, int level, int dom, int64_t *n_owned, int64_t *n_ghost, int *n_peers,
+                        int64_t *n_send, int64_t *n_recv, int64_t *owned, int64_t *ghost, int32_t *peers,
+                        int64_t *send_nat, int64_t *send_off, int64_t *recv_nat, int64_t *recv_off);
 
 const char *gmg_last_error(gmg_ctx *ctx); /* valid until the next call on ctx */
 void gmg_destroy(gmg_ctx *ctx);

@@ -1,11 +1,16 @@
 // api.cu -- the C ABI of libgmg (include/gmg.h): context, workspace, data
-// movement, kernel orchestration of residual / smoothing / V-cycle and its
-// CUDA-graph capture.
+// movement, kernel orchestration of residual / smoothing / V-cycle, halo
+// exchange (NCCL between ranks, device copies between local domains) and the
+// CUDA-graph capture of one V-cycle.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <stdexcept>
 
 #include "gmg_internal.h"
@@ -24,7 +29,7 @@ using namespace gmg;
 
 namespace {
 
-inline int nblk(int64_t n, int b = 256) { return (int)((n + b - 1) / b); }
+inline int nblk(int64_t n, int b = 256) { return (int)std::max<int64_t>(1, (n + b - 1) / b); }
 
 Phys phys(const gmg_ctx *ctx)
 {
@@ -44,13 +49,57 @@ BCs bcs(const gmg_ctx *ctx)
     return b;
 }
 
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time (the process normally already has torch's
+// libnccl.so.2 loaded; no link-time dependency, single-GPU runs never load it)
+// ---------------------------------------------------------------------------
+struct Nccl {
+    void *h = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char *(*ErrStr)(ncclResult_t) = nullptr;
+    bool load(std::string &err)
+    {
+        if (h) return true;
+        const char *cands[] = {std::getenv("GMG_NCCL_LIB"), "libnccl.so.2", "/usr/lib/x86_64-linux-gnu/libnccl.so.2"};
+        for (const char *c : cands)
+            if (c && (h = dlopen(c, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) { err = "libnccl.so.2 not found (set GMG_NCCL_LIB)"; return false; }
+        CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+        CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+        Send = (decltype(Send))dlsym(h, "ncclSend");
+        Recv = (decltype(Recv))dlsym(h, "ncclRecv");
+        GroupStart = (decltype(GroupStart))dlsym(h, "ncclGroupStart");
+        GroupEnd = (decltype(GroupEnd))dlsym(h, "ncclGroupEnd");
+        AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+        ErrStr = (decltype(ErrStr))dlsym(h, "ncclGetErrorString");
+        if (!CommInitRank || !Send || !Recv || !GroupStart || !GroupEnd || !AllReduce) {
+            err = "libnccl.so.2 lacks required symbols";
+            return false;
+        }
+        return true;
+    }
+};
+Nccl &nccl()
+{
+    static Nccl n;
+    return n;
+}
+
 // --------------------------------------------------------------------------
 // launch bookkeeping: algorithmic bytes and optional per-launch CUDA events
 // --------------------------------------------------------------------------
 struct Launcher {
     gmg_ctx *ctx;
     cudaStream_t s;
-    void pre(int) {
+    void pre(int)
+    {
         if (ctx->prof.on) {
             cudaEvent_t e;
             cudaEventCreate(&e);
@@ -58,7 +107,8 @@ struct Launcher {
             ctx->prof.ev.push_back(e);
         }
     }
-    void post(int cls, double bytes) {
+    void post(int cls, double bytes)
+    {
         ctx->launches++;
         ctx->kbytes[cls] += bytes;
         if (ctx->prof.on) {
@@ -71,11 +121,13 @@ struct Launcher {
     }
 };
 
+constexpr int kRecStride = 12;   // Rec<2>::STRIDE == Rec<3>::STRIDE
+
 template <int D>
-void enqueue_face(Launcher &Lc, int l, const double *W, bool flux, bool from_rec)
+void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, bool from_rec)
 {
     gmg_ctx *ctx = Lc.ctx;
-    DevLevel &L = ctx->dv[l];
+    DevLevel &L = dm.dv[l];
     constexpr int RS = Rec<D>::STRIDE, NV = D + 2;
     Lc.pre(GMG_K_FACE);
     const dim3 g(nblk(L.nf)), b(256);
@@ -86,25 +138,156 @@ void enqueue_face(Launcher &Lc, int l, const double *W, bool flux, bool from_rec
         if (from_rec) k_face<D, false, RS><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
         else k_face<D, false, NV><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
     }
-    Lc.post(GMG_K_FACE, flux ? ctx->lbytes[l].face_flux : ctx->lbytes[l].face_prep);
+    Lc.post(GMG_K_FACE, flux ? dm.lbytes[l].face_flux : dm.lbytes[l].face_prep);
 }
 
+// with G_NORM the domain's residual sums of squares land in d_sumsq[di]
 template <int D>
-void enqueue_gather(Launcher &Lc, int l, int flags, double *Wexp)
+void enqueue_gather(Launcher &Lc, Domain &dm, int di, int l, int flags, double *Wexp)
 {
     gmg_ctx *ctx = Lc.ctx;
-    DevLevel &L = ctx->dv[l];
+    DevLevel &L = dm.dv[l];
     GArgs a{flags, ctx->opt.cfl_imp, ctx->opt.cfl_exp, Wexp, L.partial};
     Lc.pre(GMG_K_GATHER);
     k_gather<D><<<nblk(L.n), 256, 0, Lc.s>>>(L, a);
-    Lc.post(GMG_K_GATHER, ctx->lbytes[l].gather);
+    Lc.post(GMG_K_GATHER, dm.lbytes[l].gather);
     if (flags & G_NORM) {
         Lc.pre(GMG_K_NORM);
-        k_norm_final<<<1, 256, 0, Lc.s>>>(L.partial, nblk(L.n), L.nv, ctx->d_hist, ctx->hist_cap, ctx->d_flag);
+        k_norm_sum<<<1, 256, 0, Lc.s>>>(L.partial, nblk(L.n), L.nv, ctx->d_sumsq + (size_t)di * L.nv);
         Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
     }
 }
 
+// all-reduce the per-domain sums across ranks, then one history entry
+void enqueue_norm_hist(Launcher &Lc)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    const int nv = ctx->opt.dim + 2;
+    if (ctx->opt.nranks > 1)
+        nccl().AllReduce(ctx->d_sumsq, ctx->d_sumsq, nv, ncclDouble, ncclSum, (ncclComm_t)ctx->nccl_comm, Lc.s);
+    Lc.pre(GMG_K_NORM);
+    k_norm_hist<<<1, 32, 0, Lc.s>>>(ctx->d_sumsq, (int)ctx->dom.size(), nv, ctx->d_hist, ctx->hist_cap, ctx->d_flag);
+    Lc.post(GMG_K_NORM, 0.0);
+}
+
+// --------------------------------------------------------------------------
+// halo exchange (a13).  kind: increments of one color, record W_lin (+ dW
+// = 0) of all colors, or the state W of all colors.
+// --------------------------------------------------------------------------
+enum { EX_DW = 0, EX_WLIN = 1, EX_W = 2 };
+
+template <int D>
+void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    if (ctx->nparts <= 1) return;
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    const int ncolor = ctx->lv[l].ncolor;
+    int stride = RC::STRIDE, offset = RC::DW, zero_at = 0, nzero = 0;
+    if (kind == EX_WLIN) { offset = RC::W; zero_at = RC::DW; nzero = NV; }
+    if (kind == EX_W) { stride = NV; offset = 0; }
+    auto src_of = [&](DevLevel &L) { return kind == EX_W ? L.W : L.rec; };
+    auto grange = [&](const DomLevel &H, int &g0, int &g1) {
+        const int np = (int)H.peers.size();
+        g0 = color >= 0 ? color * np : 0;
+        g1 = color >= 0 ? (color + 1) * np : ncolor * np;
+    };
+    // pack
+    for (Domain &dm : ctx->dom) {
+        const DomLevel &H = dm.lv[l];
+        DevLevel &L = dm.dv[l];
+        int g0, g1;
+        grange(H, g0, g1);
+        const int64_t s0 = H.send_off[g0], s1 = H.send_off[g1];
+        if (s1 > s0) {
+            Lc.pre(GMG_K_NORM);
+            k_pack<<<nblk(s1 - s0), 256, 0, Lc.s>>>((int)(s1 - s0), L.send_idx + s0, src_of(L), stride, offset, NV,
+                                                   L.sendbuf + s0 * NV);
+            Lc.post(GMG_K_NORM, (double)(s1 - s0) * NV * 16);
+        }
+    }
+    // transport
+    if (ctx->opt.nranks > 1) {
+        Domain &dm = ctx->dom[0];
+        const DomLevel &H = dm.lv[l];
+        DevLevel &L = dm.dv[l];
+        const int np = (int)H.peers.size();
+        int g0, g1;
+        grange(H, g0, g1);
+        nccl().GroupStart();
+        for (int g = g0; g < g1; ++g) {
+            const int peer = H.peers[g % np];
+            const int64_t sc = H.send_off[g + 1] - H.send_off[g], rc = H.recv_off[g + 1] - H.recv_off[g];
+            if (sc) nccl().Send(L.sendbuf + H.send_off[g] * NV, sc * NV, ncclDouble, peer, (ncclComm_t)ctx->nccl_comm, Lc.s);
+            if (rc) nccl().Recv(L.recvbuf + H.recv_off[g] * NV, rc * NV, ncclDouble, peer, (ncclComm_t)ctx->nccl_comm, Lc.s);
+        }
+        nccl().GroupEnd();
+    } else {
+        for (Domain &dm : ctx->dom) {
+            const DomLevel &H = dm.lv[l];
+            const int np = (int)H.peers.size();
+            int g0, g1;
+            grange(H, g0, g1);
+            for (int g = g0; g < g1; ++g) {
+                const int64_t sc = H.send_off[g + 1] - H.send_off[g];
+                if (!sc) continue;
+                Domain &dp = ctx->dom[H.peers[g % np]];
+                const DomLevel &Hp = dp.lv[l];
+                const int npp = (int)Hp.peers.size();
+                const int kk = (int)(std::lower_bound(Hp.peers.begin(), Hp.peers.end(), dm.rank) - Hp.peers.begin());
+                const int gp = (g / np) * npp + kk;
+                cudaMemcpyAsync(dp.dv[l].recvbuf + Hp.recv_off[gp] * NV, dm.dv[l].sendbuf + H.send_off[g] * NV,
+                                sizeof(double) * sc * NV, cudaMemcpyDeviceToDevice, Lc.s);
+            }
+        }
+    }
+    // unpack
+    for (Domain &dm : ctx->dom) {
+        const DomLevel &H = dm.lv[l];
+        DevLevel &L = dm.dv[l];
+        int g0, g1;
+        grange(H, g0, g1);
+        const int64_t r0 = H.recv_off[g0], r1 = H.recv_off[g1];
+        if (r1 > r0) {
+            Lc.pre(GMG_K_NORM);
+            k_unpack<<<nblk(r1 - r0), 256, 0, Lc.s>>>((int)(r1 - r0), L.recv_idx + r0, L.recvbuf + r0 * NV,
+                                                     src_of(L), stride, offset, NV, zero_at, nzero);
+            Lc.post(GMG_K_NORM, (double)(r1 - r0) * NV * 16);
+        }
+    }
+    ctx->exchanges++;
+}
+
+template <int D>
+void enqueue_ghost_wlin(Launcher &Lc, int l)
+{
+    for (Domain &dm : Lc.ctx->dom) {
+        DevLevel &L = dm.dv[l];
+        if (L.n_loc > L.n) {
+            Lc.pre(GMG_K_NORM);
+            k_ghost_wlin<D><<<nblk(L.n_loc - L.n), 256, 0, Lc.s>>>(L.n, L.n_loc, L.W, L.rec);
+            Lc.post(GMG_K_NORM, 0.0);
+        }
+    }
+}
+
+template <int D>
+void enqueue_ghost_w(Launcher &Lc, int l)
+{
+    for (Domain &dm : Lc.ctx->dom) {
+        DevLevel &L = dm.dv[l];
+        if (L.n_loc > L.n) {
+            Lc.pre(GMG_K_NORM);
+            k_ghost_w<D><<<nblk(L.n_loc - L.n), 256, 0, Lc.s>>>(L.n, L.n_loc, L.rec, L.W);
+            Lc.post(GMG_K_NORM, 0.0);
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// sweeps
+// --------------------------------------------------------------------------
 // optional L2 access-policy window over the level's cell records (the
 // gathered data), attached per launch so that graph capture keeps it
 template <class K>
@@ -140,57 +323,67 @@ void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win 
     }
 }
 
-// n_sweeps x (forward colors 1..Nc, backward Nc..1), Algorithm 2 (P:557-571);
-// the record's W_lin is the linearisation state, Wout (last backward pass)
-// receives W = W_lin + dW
+// one color block of one domain (Eq.(gpu-forward-relaxation) / (gpu-backward-relaxation))
 template <int D>
-void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, const double *rhs, double *Wout)
+void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout)
 {
     gmg_ctx *ctx = Lc.ctx;
-    DevLevel &L = ctx->dv[l];
-    const HostLevel &H = ctx->lv[l];
-    const int lpc = ctx->lpc;
+    DevLevel &L = dm.dv[l];
+    const DomLevel &H = dm.lv[l];
+    SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.soff, L.sJ, L.sRec,
+                rhs, Wout, ctx->prefetch, 0};
+    const int ncell = a.cend - a.cbeg;
+    if (ncell <= 0) return;
+    Lc.pre(GMG_K_SWEEP);
+    if (ctx->sweep_mode == 1 || ctx->sweep_mode == 2) {
+        const int C = ctx->sweep_mode == 1 ? 64 : 128;
+        a.max_slots = C == 64 ? dm.lbytes[l].max_slots64 : dm.lbytes[l].max_slots128;
+        const size_t smem = (size_t)a.max_slots * (Rec<D>::STRIDE + kSlotRec) * sizeof(double);
+        if (C == 64) k_sweep_sm<D, 64><<<(ncell + 63) / 64, 64, smem, Lc.s>>>(a);
+        else k_sweep_sm<D, 128><<<(ncell + 127) / 128, 128, smem, Lc.s>>>(a);
+    } else {
+        const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
+        const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * kRecStride * sizeof(double)) : 0;
+        switch (ctx->lpc) {
+            case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb); break;
+            case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb); break;
+            default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb); break;
+        }
+    }
+    Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
+}
+
+// n_sweeps x (forward colors 1..Nc, backward Nc..1), Algorithm 2 (P:557-571);
+// after every color its increments go to the ranks/domains that ghost them.
+// The record's W_lin is the linearisation state; the last backward pass also
+// writes W = W_lin + dW (rhs/Wout select the domain's arrays).
+template <int D>
+void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const double *(DevLevel &)> rhs,
+                    std::function<double *(DevLevel &)> wout)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    const int nc = ctx->lv[l].ncolor;
     for (int s = 0; s < n_sweeps; ++s) {
         for (int half = 0; half < 2; ++half) {
-            for (int cc = 0; cc < H.ncolor; ++cc) {
-                const int c = half == 0 ? cc : H.ncolor - 1 - cc;
+            for (int cc = 0; cc < nc; ++cc) {
+                const int c = half == 0 ? cc : nc - 1 - cc;
                 const bool last = (s == n_sweeps - 1) && half == 1;
-                SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.soff, L.sJ, L.sRec,
-                            rhs, last ? Wout : nullptr, ctx->prefetch, 0};
-                Lc.pre(GMG_K_SWEEP);
-                const int ncell = a.cend - a.cbeg;
-                if (ctx->sweep_mode == 1 || ctx->sweep_mode == 2) {
-                    const int C = ctx->sweep_mode == 1 ? 64 : 128;
-                    a.max_slots = C == 64 ? ctx->lbytes[l].max_slots64 : ctx->lbytes[l].max_slots128;
-                    const size_t smem = (size_t)a.max_slots * (Rec<D>::STRIDE + kSlotRec) * sizeof(double);
-                    if (C == 64) k_sweep_sm<D, 64><<<(ncell + 63) / 64, 64, smem, Lc.s>>>(a);
-                    else k_sweep_sm<D, 128><<<(ncell + 127) / 128, 128, smem, Lc.s>>>(a);
-                } else {
-                    const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
-                    const size_t wb = ctx->l2_window
-                                          ? std::min<size_t>(ctx->l2_window, (size_t)L.n * Rec<D>::STRIDE * sizeof(double))
-                                          : 0;
-                    switch (lpc) {
-                        case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb); break;
-                        case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb); break;
-                        default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb); break;
-                    }
-                }
-                Lc.post(GMG_K_SWEEP, ctx->lbytes[l].sweep[c] + (a.Wout ? ctx->lbytes[l].sweep_out[c] : 0.0));
+                for (Domain &dm : ctx->dom)
+                    enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), last ? wout(dm.dv[l]) : nullptr);
+                enqueue_exchange<D>(Lc, l, EX_DW, c);
             }
         }
     }
 }
 
 template <int D>
-void enqueue_restrict(Launcher &Lc, int l)
+void enqueue_restrict(Launcher &Lc, Domain &dm, int l)
 {
-    gmg_ctx *ctx = Lc.ctx;
-    DevLevel &C = ctx->dv[l];
-    DevLevel &Fn = ctx->dv[l - 1];
+    DevLevel &C = dm.dv[l];
+    DevLevel &Fn = dm.dv[l - 1];
     Lc.pre(GMG_K_RESTRICT);
     k_restrict<D><<<nblk(C.n), 256, 0, Lc.s>>>(C, Fn, Fn.W, Fn.Rt);
-    Lc.post(GMG_K_RESTRICT, ctx->lbytes[l].restrict_);
+    Lc.post(GMG_K_RESTRICT, dm.lbytes[l].restrict_);
 }
 
 // O8 -- one V-cycle, all on the device
@@ -198,39 +391,59 @@ template <int D>
 void enqueue_vcycle(Launcher &Lc)
 {
     gmg_ctx *ctx = Lc.ctx;
-    const int nl = (int)ctx->dv.size();
-    DevLevel &L0 = ctx->dv[0];
+    const int nl = (int)ctx->lv.size();
     const bool df0 = ctx->opt.df_mode == 0;
+    auto &doms = ctx->dom;
     // 1-2. fine residual at the cycle start (history entry) + fine pre-smoothing
-    enqueue_face<D>(Lc, 0, L0.W, true, false);
+    enqueue_exchange<D>(Lc, 0, EX_W, -1);
+    for (Domain &dm : doms) enqueue_face<D>(Lc, dm, 0, dm.dv[0].W, true, false);
     if (ctx->opt.fine_smoother == 0) {
-        enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_EXPLICIT, L0.W);         // Eq.(smo), A9
+        for (size_t d = 0; d < doms.size(); ++d)
+            enqueue_gather<D>(Lc, doms[d], (int)d, 0, G_FLUX | G_NORM | G_EXPLICIT, doms[d].dv[0].W);   // Eq.(smo), A9
+        enqueue_norm_hist(Lc);
+        enqueue_exchange<D>(Lc, 0, EX_W, -1);
     } else {
-        enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | G_ZERO_DW | G_COPY_W |
-                                     (df0 ? G_ALPHA : 0), nullptr);
-        enqueue_sweeps<D>(Lc, 0, ctx->opt.n_sweeps, L0.Rt, L0.W);
+        for (size_t d = 0; d < doms.size(); ++d)
+            enqueue_gather<D>(Lc, doms[d], (int)d, 0,
+                              G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | G_ZERO_DW | G_COPY_W | (df0 ? G_ALPHA : 0),
+                              nullptr);
+        enqueue_norm_hist(Lc);
+        enqueue_ghost_wlin<D>(Lc, 0);
+        enqueue_sweeps<D>(Lc, 0, ctx->opt.n_sweeps, [](DevLevel &L) { return (const double *)L.Rt; },
+                          [](DevLevel &L) { return L.W; });
+        enqueue_ghost_w<D>(Lc, 0);
     }
     if (nl == 1) return;
     // 3. residual at the smoothed state (A10) -> restricted
-    enqueue_face<D>(Lc, 0, L0.W, true, false);
-    enqueue_gather<D>(Lc, 0, G_FLUX | G_WRITE_RT | (df0 ? G_ALPHA : 0), nullptr);
+    for (size_t d = 0; d < doms.size(); ++d) {
+        enqueue_face<D>(Lc, doms[d], 0, doms[d].dv[0].W, true, false);
+        enqueue_gather<D>(Lc, doms[d], (int)d, 0, G_FLUX | G_WRITE_RT | (df0 ? G_ALPHA : 0), nullptr);
+    }
     // 4. coarse levels
     for (int l = 1; l < nl; ++l) {
-        DevLevel &C = ctx->dv[l];
         const bool last = (l == nl - 1);
-        enqueue_restrict<D>(Lc, l);                                       // W0, Res*, alpha, dW = 0
-        enqueue_face<D>(Lc, l, C.rec, !last, true);                       // R(W0) only if F is needed later
-        enqueue_gather<D>(Lc, l, (last ? 0 : (G_FLUX | G_SET_F)) | G_PREPARE, nullptr);
-        enqueue_sweeps<D>(Lc, l, ctx->opt.n_sweeps, C.Rs, C.W);          // RHS = Res* (A8)
+        for (Domain &dm : doms) enqueue_restrict<D>(Lc, dm, l);                // W0, Res*, alpha, dW = 0
+        enqueue_exchange<D>(Lc, l, EX_WLIN, -1);                                // ghosts' W0, dW = 0
+        for (size_t d = 0; d < doms.size(); ++d) {
+            enqueue_face<D>(Lc, doms[d], l, doms[d].dv[l].rec, !last, true);   // R(W0) only if F is needed later
+            enqueue_gather<D>(Lc, doms[d], (int)d, l, (last ? 0 : (G_FLUX | G_SET_F)) | G_PREPARE, nullptr);
+        }
+        enqueue_sweeps<D>(Lc, l, ctx->opt.n_sweeps, [](DevLevel &L) { return (const double *)L.Rs; },
+                          [](DevLevel &L) { return L.W; });                      // RHS = Res* (A8)
         if (!last) {
-            enqueue_face<D>(Lc, l, C.W, true, false);
-            enqueue_gather<D>(Lc, l, G_FLUX | G_WRITE_RT | G_ADD_F, nullptr);   // Rt = R(W) + F (A11)
+            enqueue_ghost_w<D>(Lc, l);
+            for (size_t d = 0; d < doms.size(); ++d) {
+                enqueue_face<D>(Lc, doms[d], l, doms[d].dv[l].W, true, false);
+                enqueue_gather<D>(Lc, doms[d], (int)d, l, G_FLUX | G_WRITE_RT | G_ADD_F, nullptr);   // Rt = R(W) + F (A11)
+            }
         }
     }
-    // 5. DF-limited prolongation 2 -> 1 -> 0 (fused)
-    Lc.pre(GMG_K_PROLONG);
-    k_prolong<D><<<nblk(L0.n), 256, 0, Lc.s>>>(L0, ctx->dv[1], nl >= 3 ? ctx->dv[2] : ctx->dv[1], nl);
-    Lc.post(GMG_K_PROLONG, ctx->lbytes[0].prolong);
+    // 5. DF-limited prolongation 2 -> 1 -> 0 (fused; rank-local)
+    for (Domain &dm : doms) {
+        Lc.pre(GMG_K_PROLONG);
+        k_prolong<D><<<nblk(dm.dv[0].n), 256, 0, Lc.s>>>(dm.dv[0], dm.dv[1], nl >= 3 ? dm.dv[2] : dm.dv[1], nl);
+        Lc.post(GMG_K_PROLONG, dm.lbytes[0].prolong);
+    }
 }
 
 // final history entry: residual at the end state
@@ -238,8 +451,12 @@ template <int D>
 void enqueue_final_norm(Launcher &Lc)
 {
     gmg_ctx *ctx = Lc.ctx;
-    enqueue_face<D>(Lc, 0, ctx->dv[0].W, true, false);
-    enqueue_gather<D>(Lc, 0, G_FLUX | G_NORM, nullptr);
+    enqueue_exchange<D>(Lc, 0, EX_W, -1);
+    for (size_t d = 0; d < ctx->dom.size(); ++d) {
+        enqueue_face<D>(Lc, ctx->dom[d], 0, ctx->dom[d].dv[0].W, true, false);
+        enqueue_gather<D>(Lc, ctx->dom[d], (int)d, 0, G_FLUX | G_NORM, nullptr);
+    }
+    enqueue_norm_hist(Lc);
 }
 
 gmg_status check_ready(gmg_ctx *ctx, bool need_state = true)
@@ -250,25 +467,39 @@ gmg_status check_ready(gmg_ctx *ctx, bool need_state = true)
     return GMG_OK;
 }
 
-// copy natural SoA [ncomp][n] (host or device) into internal AoS (stride, offset)
-gmg_status put_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, double *dst, int stride = -1, int offset = 0)
+// natural SoA [ncomp][N] (host or device) -> every domain's local cells
+// (owned + ghosts), AoS (stride, offset)
+gmg_status put_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, std::function<double *(DevLevel &)> dst,
+                       bool with_ghosts, int stride = -1, int offset = 0)
 {
-    const int64_t n = ctx->lv[l].n;
+    const int64_t N = ctx->lv[l].n;
     if (stride < 0) stride = ncomp;
-    CK(cudaMemcpyAsync(ctx->d_stage, src, sizeof(double) * ncomp * n, cudaMemcpyDefault, ctx->stream));
-    k_to_internal<<<nblk(n), 256, 0, ctx->stream>>>((int)n, ncomp, ctx->dv[l].perm, ctx->d_stage, dst, stride, offset);
+    CK(cudaMemcpyAsync(ctx->d_stage, src, sizeof(double) * ncomp * N, cudaMemcpyDefault, ctx->stream));
+    for (Domain &dm : ctx->dom) {
+        DevLevel &L = dm.dv[l];
+        const int cnt = with_ghosts ? L.n_loc : L.n;
+        k_to_internal<<<nblk(cnt), 256, 0, ctx->stream>>>(cnt, (int)N, ncomp, L.perm, ctx->d_stage, dst(L), stride, offset);
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));   // caller's host buffer may be released on return
     return GMG_OK;
 }
 
-gmg_status get_natural(gmg_ctx *ctx, int l, const double *src, int ncomp, double *dst, int stride = -1, int offset = 0)
+// every domain's owned cells -> natural SoA; with nranks > 1 only this rank's
+// owned entries of dst are written
+gmg_status get_natural(gmg_ctx *ctx, int l, std::function<const double *(DevLevel &)> src, int ncomp, double *dst,
+                       int stride = -1, int offset = 0)
 {
-    const int64_t n = ctx->lv[l].n;
+    const int64_t N = ctx->lv[l].n;
     if (stride < 0) stride = ncomp;
-    k_to_natural<<<nblk(n), 256, 0, ctx->stream>>>((int)n, ncomp, ctx->dv[l].perm, src, ctx->d_stage, stride, offset);
+    if (ctx->opt.nranks > 1)
+        CK(cudaMemcpyAsync(ctx->d_stage, dst, sizeof(double) * ncomp * N, cudaMemcpyDefault, ctx->stream));
+    for (Domain &dm : ctx->dom) {
+        DevLevel &L = dm.dv[l];
+        k_to_natural<<<nblk(L.n), 256, 0, ctx->stream>>>(L.n, (int)N, ncomp, L.perm, src(L), ctx->d_stage, stride, offset);
+    }
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(dst, ctx->d_stage, sizeof(double) * ncomp * n, cudaMemcpyDefault, ctx->stream));
+    CK(cudaMemcpyAsync(dst, ctx->d_stage, sizeof(double) * ncomp * N, cudaMemcpyDefault, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return GMG_OK;
 }
@@ -291,85 +522,101 @@ void carve(gmg_ctx *ctx, Bump &b)
 {
     const int d = ctx->opt.dim, nv = d + 2;
     const int nl = (int)ctx->lv.size();
-    ctx->dv.assign(nl, DevLevel{});
     int64_t nmax = 0;
-    for (int l = 0; l < nl; ++l) {
-        const HostLevel &H = ctx->lv[l];
-        DevLevel &L = ctx->dv[l];
-        nmax = std::max(nmax, std::max(H.n, H.nf));
-        L.dim = d; L.nv = nv; L.ncolor = H.ncolor;
-        L.n = (int)H.n; L.nf = (int)H.nf; L.nchunks = (int)H.nchunks;
-        L.fl = b.take<int>(H.nf); L.fr = b.take<int>(H.nf);
-        L.fA = b.take<double>((size_t)d * H.nf); L.fM = b.take<int8_t>(H.nf);
-        L.Fs = b.take<double>((size_t)nv * H.nf); L.Srf = b.take<double>(H.nf); L.aM = b.take<double>(H.nf);
-        L.vol = b.take<double>(H.n);
-        L.W = b.take<double>((size_t)nv * H.n); L.Rt = b.take<double>((size_t)nv * H.n);
-        L.rec = b.take<double>((size_t)(d == 3 ? Rec<3>::STRIDE : Rec<2>::STRIDE) * H.n);
-        L.tmp = b.take<double>(H.n);
-        L.Rs = b.take<double>((size_t)nv * H.n); L.F = b.take<double>((size_t)nv * H.n);
-        L.alpha = b.take<double>(H.n); L.sigma = b.take<double>(H.n);
-        L.deg_int = b.take<uint8_t>(H.n); L.deg_all = b.take<uint8_t>(H.n);
-        L.gbase = b.take<int>(H.n);
-        L.gface = b.take<int>(H.ng_entries);
-        L.soff = b.take<int>(H.n + 1); L.sJ = b.take<int>(H.ns_entries);
-        L.sRec = b.take<double>((size_t)kSlotRec * H.ns_entries);
-        L.perm = b.take<int>(H.n);
-        L.child = l > 0 ? b.take<int>(2 * H.n) : nullptr;
-        L.parent = l + 1 < nl ? b.take<int>(H.n) : nullptr;
-        L.partial = b.take<double>((size_t)nblk(H.n) * nv);
+    for (const HostLevel &G : ctx->lv) nmax = std::max(nmax, G.n);
+    for (Domain &dm : ctx->dom) {
+        dm.dv.assign(nl, DevLevel{});
+        for (int l = 0; l < nl; ++l) {
+            const HostLevel &G = ctx->lv[l];
+            const DomLevel &H = dm.lv[l];
+            DevLevel &L = dm.dv[l];
+            const int64_t n = H.n_own, nloc = H.n_loc, nf = H.nf;
+            L.dim = d; L.nv = nv; L.ncolor = G.ncolor;
+            L.n = (int)n; L.n_loc = (int)nloc; L.nf = (int)nf;
+            L.fl = b.take<int>(nf); L.fr = b.take<int>(nf);
+            L.fA = b.take<double>((size_t)d * nf); L.fM = b.take<int8_t>(nf);
+            L.Fs = b.take<double>((size_t)nv * nf); L.Srf = b.take<double>(nf); L.aM = b.take<double>(nf);
+            L.vol = b.take<double>(n);
+            L.W = b.take<double>((size_t)nv * nloc); L.Rt = b.take<double>((size_t)nv * n);
+            L.rec = b.take<double>((size_t)kRecStride * nloc);
+            L.tmp = b.take<double>(n);
+            L.Rs = b.take<double>((size_t)nv * n); L.F = b.take<double>((size_t)nv * n);
+            L.alpha = b.take<double>(n); L.sigma = b.take<double>(n);
+            L.deg_int = b.take<uint8_t>(n); L.deg_all = b.take<uint8_t>(n);
+            L.gbase = b.take<int>(n);
+            L.gface = b.take<int>(H.ng_entries);
+            L.soff = b.take<int>(n + 1); L.sJ = b.take<int>(H.ns_entries);
+            L.sRec = b.take<double>((size_t)kSlotRec * H.ns_entries);
+            L.perm = b.take<int>(nloc);
+            L.child = l > 0 ? b.take<int>(2 * n) : nullptr;
+            L.parent = l + 1 < nl ? b.take<int>(n) : nullptr;
+            L.partial = b.take<double>((size_t)nblk(n) * nv);
+            L.n_send = (int)H.send_idx.size();
+            L.n_recv = (int)H.recv_idx.size();
+            L.send_idx = b.take<int>(L.n_send);
+            L.recv_idx = b.take<int>(L.n_recv);
+            L.sendbuf = b.take<double>((size_t)L.n_send * nv);
+            L.recvbuf = b.take<double>((size_t)L.n_recv * nv);
+        }
     }
     ctx->d_stage = b.take<double>((size_t)nv * nmax);
     ctx->hist_cap = 4096;
     ctx->d_hist = b.take<double>((size_t)ctx->hist_cap * nv);
     ctx->d_flag = b.take<int>(4);
+    ctx->d_sumsq = b.take<double>((size_t)std::max<size_t>(1, ctx->dom.size()) * nv);
 }
 
 void compute_bytes(gmg_ctx *ctx)
 {
     const int d = ctx->opt.dim, nv = d + 2;
     const int nl = (int)ctx->lv.size();
-    ctx->lbytes.assign(nl, LevelBytes{});
-    for (int l = 0; l < nl; ++l) {
-        const HostLevel &H = ctx->lv[l];
-        LevelBytes &B = ctx->lbytes[l];
-        int64_t nint = 0;
-        for (int64_t f = 0; f < H.nf; ++f) nint += H.right[f] >= 0;
-        const double nb = (double)(H.nf - nint);
-        // face: cells' W (interior 2, boundary 1), A, l/r, M; writes S F, S r, alpha^M
-        const double face_in = (double)nint * 2 * nv * 8 + nb * nv * 8 + (double)H.nf * (d * 8 + 8 + 1);
-        B.face_flux = face_in + (double)H.nf * (nv * 8 + 16);
-        B.face_prep = face_in + (double)H.nf * 8;
-        // gather: per slot the face id + S F + S r + alpha^M; per cell bases/degrees + outputs (~2 nv arrays)
-        double slots = 0;
-        for (int64_t i = 0; i < H.n; ++i) slots += H.deg_all[i];
-        B.gather = slots * (4 + nv * 8 + 16) + (double)H.n * (10 + 2 * nv * 8);
-        // sweep (compulsory): own Rt, 1/D, alpha/2, dW write; neighbour-unique W, dW;
-        // face data (A, S r) once per face + 4 B per slot
-        B.sweep.assign(H.ncolor, 0.0);
-        B.sweep_out.assign(H.ncolor, 0.0);
-        for (int c = 0; c < H.ncolor; ++c) {
-            double s = 0;
-            for (int64_t i = H.blk[c]; i < H.blk[c + 1]; ++i)
-                s += (2 * nv * 8 + 16) + 2 * nv * 8 + H.deg_int[i] * ((d + 1) * 8 / 2.0 + 4);
-            B.sweep[c] = s;
-            B.sweep_out[c] = (double)(H.blk[c + 1] - H.blk[c]) * 2 * nv * 8;
-        }
-        B.restrict_ = l > 0 ? (double)ctx->lv[l - 1].n * (2 * nv * 8 + 16) + (double)H.n * (3 * nv * 8 + 8 + 8) : 0;
-        B.prolong = (double)H.n * (2 * nv * 8 + 8 + 4) + (nl > 1 ? (double)ctx->lv[1].n * (nv * 8 + 12) : 0) +
-                    (nl > 2 ? (double)ctx->lv[2].n * nv * 8 : 0);
-        B.update = (double)H.n * 3 * nv * 8;
-        // smem staging: max slots of any C-cell chunk within a color block
-        for (int C : {64, 128}) {
-            int mx = 0;
-            for (int c = 0; c < H.ncolor; ++c)
-                for (int64_t i0 = H.blk[c]; i0 < H.blk[c + 1]; i0 += C) {
-                    const int64_t i1 = std::min<int64_t>(i0 + C, H.blk[c + 1]);
-                    mx = std::max<int>(mx, H.soffc[i1] - H.soffc[i0]);
-                }
-            (C == 64 ? B.max_slots64 : B.max_slots128) = std::max(mx, 1);
+    for (Domain &dm : ctx->dom) {
+        dm.lbytes.assign(nl, LevelBytes{});
+        for (int l = 0; l < nl; ++l) {
+            const DomLevel &H = dm.lv[l];
+            const int ncolor = ctx->lv[l].ncolor;
+            LevelBytes &B = dm.lbytes[l];
+            int64_t nint = 0;
+            for (int64_t f = 0; f < H.nf; ++f) nint += H.fr[f] >= 0;
+            const double nb = (double)(H.nf - nint);
+            // face: cells' W (interior 2, boundary 1), A, l/r, M; writes S F, S r, alpha^M
+            const double face_in = (double)nint * 2 * nv * 8 + nb * nv * 8 + (double)H.nf * (d * 8 + 8 + 1);
+            B.face_flux = face_in + (double)H.nf * (nv * 8 + 16);
+            B.face_prep = face_in + (double)H.nf * 8;
+            // gather: per slot the face id + S F + S r + alpha^M; per cell bases/degrees + outputs
+            double slots = 0;
+            for (int64_t i = 0; i < H.n_own; ++i) slots += H.deg_all[i];
+            B.gather = slots * (4 + nv * 8 + 16) + (double)H.n_own * (10 + 2 * nv * 8);
+            // sweep (compulsory): own Rt, 1/D, alpha/2, dW write; neighbour-unique W, dW;
+            // face data (A, S r) once per face + 4 B per slot
+            B.sweep.assign(ncolor, 0.0);
+            B.sweep_out.assign(ncolor, 0.0);
+            for (int c = 0; c < ncolor; ++c) {
+                double s = 0;
+                for (int64_t i = H.blk[c]; i < H.blk[c + 1]; ++i)
+                    s += (2 * nv * 8 + 16) + 2 * nv * 8 + H.deg_int[i] * ((d + 1) * 8 / 2.0 + 4);
+                B.sweep[c] = s;
+                B.sweep_out[c] = (double)(H.blk[c + 1] - H.blk[c]) * 2 * nv * 8;
+            }
+            B.restrict_ = l > 0 ? (double)dm.lv[l - 1].n_own * (2 * nv * 8 + 16) + (double)H.n_own * (3 * nv * 8 + 16) : 0;
+            B.prolong = (double)H.n_own * (2 * nv * 8 + 8 + 4) + (nl > 1 ? (double)dm.lv[1].n_own * (nv * 8 + 12) : 0) +
+                        (nl > 2 ? (double)dm.lv[2].n_own * nv * 8 : 0);
+            B.update = (double)H.n_own * 3 * nv * 8;
+            for (int C : {64, 128}) {   // smem staging: max slots of any C-cell chunk within a color block
+                int mx = 0;
+                for (int c = 0; c < ncolor; ++c)
+                    for (int64_t i0 = H.blk[c]; i0 < H.blk[c + 1]; i0 += C) {
+                        const int64_t i1 = std::min<int64_t>(i0 + C, H.blk[c + 1]);
+                        mx = std::max<int>(mx, H.soffc[i1] - H.soffc[i0]);
+                    }
+                (C == 64 ? B.max_slots64 : B.max_slots128) = std::max(mx, 1);
+            }
         }
     }
 }
+
+template <int D>
+void vcycle_dispatch(Launcher &Lc) { enqueue_vcycle<D>(Lc); }
 
 }  // namespace
 
@@ -398,6 +645,7 @@ void gmg_default_options(gmg_options *o)
     o->nccl_id = nullptr;
     o->device = 0;
     o->stream = nullptr;
+    o->local_domains = 1;
 }
 
 gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
@@ -407,13 +655,14 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if ((opt->dim != 2 && opt->dim != 3) || !(opt->gamma > 1.0) || !(opt->cfl_imp > 0) || !(opt->cfl_exp > 0) ||
         opt->n_sweeps < 1 || opt->n_levels < 1 || opt->n_levels > 3 || opt->pre_smooth != 1 || opt->post_smooth != 0 ||
         !(opt->r_factor >= 1.0) || opt->fine_smoother < 0 || opt->fine_smoother > 1 || opt->df_mode < 0 ||
-        opt->df_mode > 2 || opt->nranks < 1 || opt->rank < 0 || opt->rank >= opt->nranks)
+        opt->df_mode > 2 || opt->nranks < 1 || opt->rank < 0 || opt->rank >= opt->nranks || opt->local_domains < 1 ||
+        opt->local_domains > 64 || (opt->nranks > 1 && (opt->local_domains != 1 || !opt->nccl_id)))
         return GMG_EINVAL;
-    if (opt->nranks > 1) return GMG_EINVAL;   // multi-rank path: see DESIGN.md (not in this build)
     gmg_ctx *ctx = new (std::nothrow) gmg_ctx();
     if (!ctx) return GMG_ENOMEM;
     ctx->opt = *opt;
     ctx->stream = (cudaStream_t)opt->stream;
+    ctx->nparts = std::max(opt->nranks, opt->local_domains);
     if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
     if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
     if (const char *e = std::getenv("GMG_PREFETCH")) ctx->prefetch = std::atoi(e);
@@ -433,11 +682,17 @@ gmg_status gmg_load_mesh(gmg_ctx *ctx, int64_t n_cells, const double *vol, const
         ctx->err = "gmg_load_mesh: bad arguments";
         return GMG_EINVAL;
     }
+    if (ctx->nparts > 1) {
+        if (!part) { ctx->err = "partitioned run needs part[]"; return GMG_EINVAL; }
+        for (int64_t i = 0; i < n_cells; ++i)
+            if (part[i] < 0 || part[i] >= ctx->nparts) { ctx->err = "part[] out of range"; return GMG_EINVAL; }
+    }
     ctx->n_patches = n_patches;
     ctx->patch_kind.assign(patch_kind, patch_kind + n_patches);
     for (int k = 0; k < n_patches; ++k)
         if (patch_kind[k] < 0 || patch_kind[k] > 3) { ctx->err = "bad patch kind"; return GMG_EINVAL; }
-    gmg_status st = load_mesh(ctx, n_cells, vol, centroid, n_faces, left, right, area_vec, face_ctr, n_gauss, part);
+    gmg_status st = load_mesh(ctx, n_cells, vol, centroid, n_faces, left, right, area_vec, face_ctr, n_gauss,
+                              ctx->nparts > 1 ? part : nullptr);
     if (st != GMG_OK) return st;
     ctx->mesh_loaded = true;
     ctx->built = ctx->ws_ready = ctx->state_set = false;
@@ -473,7 +728,6 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
                 color_level(H);
             }
             renumber(H);
-            build_layout(H);
             H.parent.clear();
             if (l + 1 >= n_levels) break;
             std::vector<int64_t> parent;
@@ -489,6 +743,18 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             HostLevel C;
             build_coarse(ctx->lv[l], C);
             ctx->lv.push_back(std::move(C));
+        }
+        // domains driven by this process
+        ctx->dom.clear();
+        const int nd = ctx->opt.nranks > 1 ? 1 : ctx->opt.local_domains;
+        for (int k = 0; k < nd; ++k) {
+            Domain dm;
+            dm.rank = ctx->opt.nranks > 1 ? ctx->opt.rank : k;
+            dm.lv.resize(ctx->lv.size());
+            for (size_t l = 0; l < ctx->lv.size(); ++l) build_domain_level(ctx->lv[l], dm.rank, dm.lv[l]);
+            for (size_t l = 0; l + 1 < ctx->lv.size(); ++l)
+                link_domain_levels(ctx->lv[l], ctx->lv[l + 1], dm.lv[l], dm.lv[l + 1]);
+            ctx->dom.push_back(std::move(dm));
         }
     } catch (const std::exception &e) {
         ctx->err = e.what();
@@ -566,7 +832,6 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
     carve(ctx, b);
     ctx->ws = dptr;
     ctx->ws_bytes = bytes;
-    const int d = ctx->opt.dim, nv = d + 2;
     const int nl = (int)ctx->lv.size();
     std::vector<std::vector<int>> ki;          // host staging kept alive until the sync
     std::vector<std::vector<double>> kd;
@@ -575,58 +840,51 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         return cudaMemcpyAsync((void *)dst, ki.back().data(), ki.back().size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream);
     };
     auto up_raw = [&](const void *dst, const void *src, size_t bytes_) -> cudaError_t {
+        if (!bytes_) return cudaSuccess;
         return cudaMemcpyAsync((void *)dst, src, bytes_, cudaMemcpyHostToDevice, ctx->stream);
     };
-    for (int l = 0; l < nl; ++l) {
-        const HostLevel &H = ctx->lv[l];
-        DevLevel &L = ctx->dv[l];
-        std::vector<int> fl(H.nf), fr(H.nf);
-        for (int64_t f = 0; f < H.nf; ++f) {
-            fl[f] = (int)H.iperm[H.left[f]];
-            fr[f] = H.right[f] >= 0 ? (int)H.iperm[H.right[f]] : (int)H.right[f];
-        }
-        CK(up_i(L.fl, std::move(fl)));
-        CK(up_i(L.fr, std::move(fr)));
-        CK(up_raw(L.fA, H.avec.data(), H.avec.size() * sizeof(double)));
-        CK(up_raw(L.fM, H.ngauss.data(), H.ngauss.size()));
-        std::vector<double> vol(H.n);
-        for (int64_t i = 0; i < H.n; ++i) vol[i] = H.vol[H.perm[i]];
-        kd.push_back(std::move(vol));
-        CK(up_raw(L.vol, kd.back().data(), H.n * sizeof(double)));
-        CK(up_raw(L.deg_int, H.deg_int.data(), H.n));
-        CK(up_raw(L.deg_all, H.deg_all.data(), H.n));
-        CK(up_raw(L.gbase, H.gbase.data(), H.n * sizeof(int)));
-        CK(up_raw(L.soff, H.soffc.data(), (H.n + 1) * sizeof(int)));
-        CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
-        CK(up_raw(L.sJ, H.sJ.data(), H.sJ.size() * sizeof(int)));
-        CK(up_raw(L.sRec, H.sRec.data(), H.sRec.size() * sizeof(double)));
-        std::vector<int> perm(H.n);
-        for (int64_t i = 0; i < H.n; ++i) perm[i] = (int)H.perm[i];
-        CK(up_i(L.perm, std::move(perm)));
-        if (l > 0) {
-            const HostLevel &Fh = ctx->lv[l - 1];
-            std::vector<int> child(2 * H.n, -1);
-            for (int64_t i = 0; i < Fh.n; ++i) {              // ascending natural id of the fine cell
-                const int64_t c = H.iperm[Fh.parent[i]];
-                if (child[c] < 0) child[c] = (int)Fh.iperm[i];
-                else child[H.n + c] = (int)Fh.iperm[i];
+    for (Domain &dm : ctx->dom) {
+        for (int l = 0; l < nl; ++l) {
+            const HostLevel &G = ctx->lv[l];
+            const DomLevel &H = dm.lv[l];
+            DevLevel &L = dm.dv[l];
+            CK(up_raw(L.fl, H.fl.data(), H.fl.size() * sizeof(int)));
+            CK(up_raw(L.fr, H.fr.data(), H.fr.size() * sizeof(int)));
+            std::vector<double> fA((size_t)G.dim * H.nf);
+            std::vector<int> fM8((H.nf + 3) / 4 + 1, 0);
+            std::vector<int8_t> fM(H.nf);
+            for (int64_t k = 0; k < H.nf; ++k) {
+                for (int q = 0; q < G.dim; ++q) fA[(size_t)q * H.nf + k] = G.avec[(size_t)q * G.nf + H.fnat[k]];
+                fM[k] = G.ngauss[H.fnat[k]];
             }
-            CK(up_i(L.child, std::move(child)));
+            std::memcpy(fM8.data(), fM.data(), fM.size());
+            kd.push_back(std::move(fA));
+            CK(up_raw(L.fA, kd.back().data(), kd.back().size() * sizeof(double)));
+            ki.push_back(std::move(fM8));
+            CK(up_raw(L.fM, ki.back().data(), (size_t)H.nf));
+            CK(up_raw(L.vol, H.vol.data(), H.vol.size() * sizeof(double)));
+            CK(up_raw(L.deg_int, H.deg_int.data(), H.deg_int.size()));
+            CK(up_raw(L.deg_all, H.deg_all.data(), H.deg_all.size()));
+            CK(up_raw(L.gbase, H.gbase.data(), H.gbase.size() * sizeof(int)));
+            CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
+            CK(up_raw(L.soff, H.soffc.data(), H.soffc.size() * sizeof(int)));
+            CK(up_raw(L.sJ, H.sJ.data(), H.sJ.size() * sizeof(int)));
+            CK(up_raw(L.sRec, H.sRec.data(), H.sRec.size() * sizeof(double)));
+            std::vector<int> perm(H.n_loc);
+            for (int64_t i = 0; i < H.n_loc; ++i) perm[i] = (int)H.l2n[i];
+            CK(up_i(L.perm, std::move(perm)));
+            if (l > 0) CK(up_raw(L.child, H.child.data(), H.child.size() * sizeof(int)));
+            if (l + 1 < nl) CK(up_raw(L.parent, H.parent.data(), H.parent.size() * sizeof(int)));
+            CK(up_raw(L.send_idx, H.send_idx.data(), H.send_idx.size() * sizeof(int)));
+            CK(up_raw(L.recv_idx, H.recv_idx.data(), H.recv_idx.size() * sizeof(int)));
+            // alpha = 1 until set (df_mode 2 keeps it)
+            k_fill<<<nblk(H.n_own), 256, 0, ctx->stream>>>((int)H.n_own, L.alpha, 1.0);
+            CK(cudaMemsetAsync(L.rec, 0, sizeof(double) * kRecStride * H.n_loc, ctx->stream));
         }
-        if (l + 1 < nl) {
-            const HostLevel &Ch = ctx->lv[l + 1];
-            std::vector<int> par(H.n);
-            for (int64_t i = 0; i < H.n; ++i) par[i] = (int)Ch.iperm[H.parent[H.perm[i]]];
-            CK(up_i(L.parent, std::move(par)));
-        }
-        // alpha = 1 until set (df_mode 2 keeps it)
-        k_fill<<<nblk(H.n), 256, 0, ctx->stream>>>((int)H.n, L.alpha, 1.0);
-        CK(cudaMemsetAsync(L.rec, 0, sizeof(double) * (d == 3 ? Rec<3>::STRIDE : Rec<2>::STRIDE) * H.n, ctx->stream));
     }
     CK(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), ctx->stream));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
-    if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
     if (const char *e = std::getenv("GMG_L2PERSIST")) {   // experimental: persisting-L2 window over records
         if (std::atoi(e) > 0) {
             int maxp = 0, maxw = 0;
@@ -634,18 +892,31 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, ctx->opt.device);
             CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
             ctx->l2_window = std::min<size_t>((size_t)maxw, (size_t)maxp);
-            std::fprintf(stderr, "gmg: persisting L2 %d B, max window %d B\n", maxp, maxw);
         }
     }
     {   // dynamic shared memory of the staged sweep (may exceed the 48 KB default)
         int mx = 1;
-        for (auto &B : ctx->lbytes) mx = std::max(mx, std::max(B.max_slots64, B.max_slots128));
-        const int bytes_sm = mx * (Rec<3>::STRIDE + kSlotRec) * (int)sizeof(double);
+        for (Domain &dm : ctx->dom)
+            for (auto &B : dm.lbytes) mx = std::max(mx, std::max(B.max_slots64, B.max_slots128));
+        const int bytes_sm = std::min(mx * (kRecStride + kSlotRec) * (int)sizeof(double), 227 * 1024);
         CK(cudaFuncSetAttribute(k_sweep_sm<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
         CK(cudaFuncSetAttribute(k_sweep_sm<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
         CK(cudaFuncSetAttribute(k_sweep_sm<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
         CK(cudaFuncSetAttribute(k_sweep_sm<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
     }
+    if (ctx->opt.nranks > 1 && !ctx->nccl_comm) {
+        if (!nccl().load(ctx->err)) return GMG_ENCCL;
+        ncclUniqueId id;
+        std::memcpy(&id, ctx->opt.nccl_id, sizeof(id));
+        ncclComm_t comm;
+        const ncclResult_t r = nccl().CommInitRank(&comm, ctx->opt.nranks, id, ctx->opt.rank);
+        if (r != ncclSuccess) {
+            ctx->err = std::string("ncclCommInitRank: ") + (nccl().ErrStr ? nccl().ErrStr(r) : "error");
+            return GMG_ENCCL;
+        }
+        ctx->nccl_comm = comm;
+    }
+    if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
     ctx->ws_ready = true;
     ctx->state_set = false;
     return GMG_OK;
@@ -660,7 +931,7 @@ gmg_status gmg_set_state(gmg_ctx *ctx, const double *W, const double *W_inf)
     const int nv = ctx->opt.dim + 2;
     for (int q = 0; q < nv; ++q) ctx->winf[q] = W_inf[q];
     if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }   // BC values are kernel params
-    st = put_natural(ctx, 0, W, nv, ctx->dv[0].W);
+    st = put_natural(ctx, 0, W, nv, [](DevLevel &L) { return L.W; }, true);
     if (st) return st;
     ctx->state_set = true;
     return GMG_OK;
@@ -672,7 +943,7 @@ gmg_status gmg_set_level_state(gmg_ctx *ctx, int level, const double *W)
     gmg_status st = check_ready(ctx, false);
     if (st) return st;
     if (level < 0 || level >= (int)ctx->lv.size() || !W) { ctx->err = "bad level / null"; return GMG_EINVAL; }
-    st = put_natural(ctx, level, W, ctx->opt.dim + 2, ctx->dv[level].W);
+    st = put_natural(ctx, level, W, ctx->opt.dim + 2, [](DevLevel &L) { return L.W; }, true);
     if (st) return st;
     if (level == 0) ctx->state_set = true;
     return GMG_OK;
@@ -684,7 +955,7 @@ gmg_status gmg_get_state(gmg_ctx *ctx, int level, double *W_out)
     gmg_status st = check_ready(ctx, false);
     if (st) return st;
     if (level < 0 || level >= (int)ctx->lv.size() || !W_out) { ctx->err = "bad level / null"; return GMG_EINVAL; }
-    return get_natural(ctx, level, ctx->dv[level].W, ctx->opt.dim + 2, W_out);
+    return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.W; }, ctx->opt.dim + 2, W_out);
 }
 
 gmg_status gmg_set_alpha(gmg_ctx *ctx, const double *alpha)
@@ -693,7 +964,7 @@ gmg_status gmg_set_alpha(gmg_ctx *ctx, const double *alpha)
     gmg_status st = check_ready(ctx, false);
     if (st) return st;
     if (!alpha) { ctx->err = "null alpha"; return GMG_EINVAL; }
-    return put_natural(ctx, 0, alpha, 1, ctx->dv[0].alpha);
+    return put_natural(ctx, 0, alpha, 1, [](DevLevel &L) { return L.alpha; }, false);
 }
 
 gmg_status gmg_residual(gmg_ctx *ctx, int level, double *R_out, double *alpha_out, double *sigma_out)
@@ -703,23 +974,25 @@ gmg_status gmg_residual(gmg_ctx *ctx, int level, double *R_out, double *alpha_ou
     if (st) return st;
     if (level < 0 || level >= (int)ctx->lv.size()) { ctx->err = "bad level"; return GMG_EINVAL; }
     Launcher Lc{ctx, ctx->stream};
-    DevLevel &L = ctx->dv[level];
-    // alpha is written to the Rs/F-free scratch "sigma" path: keep the level's alpha intact
-    double *save_alpha = L.alpha;
-    L.alpha = L.tmp;    // scratch: the level's own alpha stays intact
-    if (ctx->opt.dim == 2) {
-        enqueue_face<2>(Lc, level, L.W, true, false);
-        enqueue_gather<2>(Lc, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
-    } else {
-        enqueue_face<3>(Lc, level, L.W, true, false);
-        enqueue_gather<3>(Lc, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
+    for (size_t d = 0; d < ctx->dom.size(); ++d) {
+        Domain &dm = ctx->dom[d];
+        DevLevel &L = dm.dv[level];
+        double *save_alpha = L.alpha;
+        L.alpha = L.tmp;    // scratch: the level's own alpha stays intact
+        if (ctx->opt.dim == 2) {
+            enqueue_face<2>(Lc, dm, level, L.W, true, false);
+            enqueue_gather<2>(Lc, dm, (int)d, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
+        } else {
+            enqueue_face<3>(Lc, dm, level, L.W, true, false);
+            enqueue_gather<3>(Lc, dm, (int)d, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
+        }
+        L.alpha = save_alpha;
     }
-    L.alpha = save_alpha;
     CK(cudaGetLastError());
     const int nv = ctx->opt.dim + 2;
-    if (R_out) { st = get_natural(ctx, level, L.Rt, nv, R_out); if (st) return st; }
-    if (alpha_out) { st = get_natural(ctx, level, L.tmp, 1, alpha_out); if (st) return st; }
-    if (sigma_out) { st = get_natural(ctx, level, L.sigma, 1, sigma_out); if (st) return st; }
+    if (R_out) { st = get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.Rt; }, nv, R_out); if (st) return st; }
+    if (alpha_out) { st = get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.tmp; }, 1, alpha_out); if (st) return st; }
+    if (sigma_out) { st = get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.sigma; }, 1, sigma_out); if (st) return st; }
     CK(cudaStreamSynchronize(ctx->stream));
     return GMG_OK;
 }
@@ -730,8 +1003,13 @@ gmg_status gmg_set_level_inputs(gmg_ctx *ctx, int level, const double *Rt, const
     gmg_status st = check_ready(ctx, false);
     if (st) return st;
     if (level < 0 || level >= (int)ctx->lv.size()) { ctx->err = "bad level"; return GMG_EINVAL; }
-    if (Rt) { st = put_natural(ctx, level, Rt, ctx->opt.dim + 2, ctx->dv[level].Rt); if (st) return st; }
-    if (alpha) { st = put_natural(ctx, level, alpha, 1, ctx->dv[level].alpha); if (st) return st; }
+    // owned cells only (Rt and alpha have no ghost entries)
+    if (Rt) {
+        st = put_natural(ctx, level, Rt, ctx->opt.dim + 2, [](DevLevel &L) { return L.Rt; }, false);
+        if (st) return st;
+    }
+    if (alpha) { st = put_natural(ctx, level, alpha, 1, [](DevLevel &L) { return L.alpha; }, false); if (st) return st; }
+    CK(cudaStreamSynchronize(ctx->stream));
     return GMG_OK;
 }
 
@@ -742,22 +1020,31 @@ gmg_status gmg_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out)
     if (st) return st;
     if (level < 0 || level >= (int)ctx->lv.size() || n_sweeps < 1) { ctx->err = "bad level / n_sweeps"; return GMG_EINVAL; }
     Launcher Lc{ctx, ctx->stream};
-    DevLevel &L = ctx->dv[level];
-    const int nv = ctx->opt.dim + 2;
     const int gf = G_PREPARE | G_SIGMA | G_COPY_W | G_ZERO_DW;
+    auto rhs = [](DevLevel &L) { return (const double *)L.Rt; };
+    auto nowout = [](DevLevel &) { return (double *)nullptr; };
     if (ctx->opt.dim == 2) {
-        enqueue_face<2>(Lc, level, L.W, false, false);
-        enqueue_gather<2>(Lc, level, gf, nullptr);
-        enqueue_sweeps<2>(Lc, level, n_sweeps, L.Rt, nullptr);
+        for (size_t d = 0; d < ctx->dom.size(); ++d) {
+            enqueue_face<2>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false);
+            enqueue_gather<2>(Lc, ctx->dom[d], (int)d, level, gf, nullptr);
+        }
+        enqueue_ghost_wlin<2>(Lc, level);
+        enqueue_sweeps<2>(Lc, level, n_sweeps, rhs, nowout);
     } else {
-        enqueue_face<3>(Lc, level, L.W, false, false);
-        enqueue_gather<3>(Lc, level, gf, nullptr);
-        enqueue_sweeps<3>(Lc, level, n_sweeps, L.Rt, nullptr);
+        for (size_t d = 0; d < ctx->dom.size(); ++d) {
+            enqueue_face<3>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false);
+            enqueue_gather<3>(Lc, ctx->dom[d], (int)d, level, gf, nullptr);
+        }
+        enqueue_ghost_wlin<3>(Lc, level);
+        enqueue_sweeps<3>(Lc, level, n_sweeps, rhs, nowout);
     }
     CK(cudaGetLastError());
-    const int RS = ctx->opt.dim == 3 ? Rec<3>::STRIDE : Rec<2>::STRIDE;
+    const int nv = ctx->opt.dim + 2;
     const int RD = ctx->opt.dim == 3 ? Rec<3>::DW : Rec<2>::DW;
-    if (dW_out) { st = get_natural(ctx, level, L.rec, nv, dW_out, RS, RD); if (st) return st; }
+    if (dW_out) {
+        st = get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.rec; }, nv, dW_out, kRecStride, RD);
+        if (st) return st;
+    }
     return GMG_OK;
 }
 
@@ -768,11 +1055,12 @@ static gmg_status build_graph(gmg_ctx *ctx)
     cudaGraph_t g;
     Launcher Lc{ctx, cs};
     ctx->launches = 0;
+    ctx->exchanges = 0;
     for (double &b : ctx->kbytes) b = 0;
     cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
-        if (ctx->opt.dim == 2) enqueue_vcycle<2>(Lc);
-        else enqueue_vcycle<3>(Lc);
+        if (ctx->opt.dim == 2) vcycle_dispatch<2>(Lc);
+        else vcycle_dispatch<3>(Lc);
         e = cudaStreamEndCapture(cs, &g);
     }
     cudaStreamDestroy(cs);
@@ -827,8 +1115,8 @@ gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_
     CK(cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), ctx->stream));
     Launcher Lc{ctx, ctx->stream};
     for (int k = 0; k < n_cycles; ++k) {
-        if (ctx->opt.dim == 2) enqueue_vcycle<2>(Lc);
-        else enqueue_vcycle<3>(Lc);
+        if (ctx->opt.dim == 2) vcycle_dispatch<2>(Lc);
+        else vcycle_dispatch<3>(Lc);
     }
     ctx->prof.on = false;
     CK(cudaGetLastError());
@@ -859,16 +1147,17 @@ gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, doub
     gmg_status st = check_ready(ctx, false);
     if (st) return st;
     if (level < 0 || level >= (int)ctx->lv.size() || n_sweeps < 1 || reps < 1) { ctx->err = "bad args"; return GMG_EINVAL; }
-    DevLevel &L = ctx->dv[level];
     cudaStream_t cs;
     CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     Launcher Lc{ctx, cs};
     for (double &b : ctx->kbytes) b = 0;
     cudaGraph_t g;
     cudaGraphExec_t ge;
+    auto rhs = [](DevLevel &L) { return (const double *)L.Rt; };
+    auto nowout = [](DevLevel &) { return (double *)nullptr; };
     CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    if (ctx->opt.dim == 2) enqueue_sweeps<2>(Lc, level, n_sweeps, L.Rt, nullptr);
-    else enqueue_sweeps<3>(Lc, level, n_sweeps, L.Rt, nullptr);
+    if (ctx->opt.dim == 2) enqueue_sweeps<2>(Lc, level, n_sweeps, rhs, nowout);
+    else enqueue_sweeps<3>(Lc, level, n_sweeps, rhs, nowout);
     CK(cudaStreamEndCapture(cs, &g));
     CK(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
@@ -887,8 +1176,10 @@ gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, doub
     cudaEventDestroy(e1);
     cudaGraphExecDestroy(ge);
     cudaStreamDestroy(cs);
+    int64_t nown = 0;
+    for (Domain &dm : ctx->dom) nown += dm.lv[level].n_own;
     if (ms) *ms = t;
-    if (cell_updates) *cell_updates = (double)L.n * 2.0 * n_sweeps * reps;
+    if (cell_updates) *cell_updates = (double)nown * 2.0 * n_sweeps * reps;
     if (bytes) *bytes = b1 * reps;
     return GMG_OK;
 }
@@ -900,12 +1191,48 @@ int64_t gmg_vcycle_launches(gmg_ctx *ctx)
     return ctx->graph_launches;
 }
 
+gmg_status gmg_partition_rcb(int64_t n_cells, int dim, const double *centroid, int nparts, int32_t *part_out)
+{
+    if (n_cells < 1 || (dim != 2 && dim != 3) || !centroid || nparts < 1 || !part_out) return GMG_EINVAL;
+    partition_rcb(n_cells, dim, centroid, nparts, part_out);
+    return GMG_OK;
+}
+
+gmg_status gmg_get_halo(gmg_ctx *ctx, int level, int dom, int64_t *n_owned, int64_t *n_ghost, int *n_peers,
+                        int64_t *n_send, int64_t *n_recv, int64_t *owned, int64_t *ghost, int32_t *peers,
+                        int64_t *send_nat, int64_t *send_off, int64_t *recv_nat, int64_t *recv_off)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->built) { ctx->err = "hierarchy not built"; return GMG_ESTATE; }
+    if (level < 0 || level >= (int)ctx->lv.size() || dom < 0 || dom >= (int)ctx->dom.size()) {
+        ctx->err = "bad level / domain";
+        return GMG_EINVAL;
+    }
+    const DomLevel &H = ctx->dom[dom].lv[level];
+    if (n_owned) *n_owned = H.n_own;
+    if (n_ghost) *n_ghost = H.n_loc - H.n_own;
+    if (n_peers) *n_peers = (int)H.peers.size();
+    if (n_send) *n_send = (int64_t)H.send_idx.size();
+    if (n_recv) *n_recv = (int64_t)H.recv_idx.size();
+    if (owned && ghost && peers && send_nat && send_off && recv_nat && recv_off) {
+        std::copy(H.l2n.begin(), H.l2n.begin() + H.n_own, owned);
+        std::copy(H.l2n.begin() + H.n_own, H.l2n.end(), ghost);
+        std::copy(H.peers.begin(), H.peers.end(), peers);
+        for (size_t k = 0; k < H.send_idx.size(); ++k) send_nat[k] = H.l2n[H.send_idx[k]];
+        for (size_t k = 0; k < H.recv_idx.size(); ++k) recv_nat[k] = H.l2n[H.recv_idx[k]];
+        std::copy(H.send_off.begin(), H.send_off.end(), send_off);
+        std::copy(H.recv_off.begin(), H.recv_off.end(), recv_off);
+    }
+    return GMG_OK;
+}
+
 const char *gmg_last_error(gmg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 void gmg_destroy(gmg_ctx *ctx)
 {
     if (!ctx) return;
     if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+    if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy((ncclComm_t)ctx->nccl_comm);
     delete ctx;
 }
 

@@ -1,5 +1,17 @@
 // gmg_internal.h -- private structures of libgmg (host setup + device layout).
 // Not part of the ABI.  Nothing here is shared with oracle/.
+//
+// Data model
+//  * HostLevel: one GLOBAL level in natural numbering (geometry, Algorithm-1
+//    colors, global renumbering, parent map, partition ids).  Every rank
+//    builds the identical global hierarchy (deterministic host code).
+//  * DomLevel: the part of a level one domain (rank) works on: its owned
+//    cells in (color, natural id) order, then one layer of ghost cells in
+//    (owner, color, natural id) order; the local faces (those touching an
+//    owned cell); slot layouts over owned cells; multigrid links; the halo
+//    plan grouped by (color, peer).
+//  * DevLevel: device pointers of a DomLevel (inside the workspace).
+// A single-GPU run is one domain owning everything (no ghosts, no peers).
 #pragma once
 #include <cstdint>
 #include <string>
@@ -13,9 +25,6 @@ namespace gmg {
 
 constexpr int kChunk = 32;  // SELL chunk height = one warp of cells
 
-// ---------------------------------------------------------------------------
-// Host description of one level (natural numbering) + its internal layout.
-// ---------------------------------------------------------------------------
 struct HostLevel {
     int dim = 3;
     int64_t n = 0, nf = 0;
@@ -23,64 +32,72 @@ struct HostLevel {
     std::vector<int64_t> left, right;      // [nf]
     std::vector<double> avec, fctr;        // [dim][nf]
     std::vector<int8_t> ngauss;            // [nf]
-    std::vector<int32_t> part;             // [n] partition id (empty: single rank)
-
+    std::vector<int32_t> part;             // [n] partition id (empty: one partition)
     // coloring and renumbering (a2, a3)
     std::vector<int32_t> color;            // [n] natural order, 1..ncolor
     int ncolor = 0;
-    std::vector<int64_t> perm;             // internal -> natural
-    std::vector<int64_t> iperm;            // natural -> internal
-    std::vector<int64_t> blk;              // [ncolor+1] color block offsets (internal)
-
+    std::vector<int64_t> perm;             // global renumbering: position -> natural (stable by color)
     // agglomeration to the next level (a4)
     std::vector<int64_t> parent;           // [n] natural -> natural coarse id (empty: coarsest)
     int64_t n_coarse = 0;
-
-    // layouts (internal order), see build_layout
-    int64_t nchunks = 0;
-    std::vector<int32_t> chunk_base;       // [ncolor+1] first gather chunk of each color
-    std::vector<int32_t> goff;             // [nchunks] gather entry offset of each chunk
-    int64_t ng_entries = 0, ns_entries = 0;
-    std::vector<int32_t> gbase;            // [n] gather entry of slot 0 (slot s at gbase + 32 s)
-    std::vector<uint8_t> deg_int, deg_all; // [n] interior / all face slots
-    std::vector<int32_t> gface;            // [ng_entries] signed face slot: +(f+1) left, -(f+1) right, 0 pad
-    std::vector<int32_t> soffc;            // [n+1] sweep slots of cell i: [soffc[i], soffc[i+1])
-    std::vector<int32_t> sJ;               // [ns_entries] neighbour (internal)
-    std::vector<double> sRec;              // [ns_entries][4] (A_x, A_y, A_z | S r) 3D, (A_x, A_y, S r, 0) 2D
-    std::vector<int32_t> sface;            // [ns_entries] face id of the slot (host bookkeeping)
+    int part_of(int64_t i) const { return part.empty() ? 0 : part[i]; }
 };
 
-// ---------------------------------------------------------------------------
-// Device view of one level (pointers into the workspace).
-// Cell arrays are AoS [n][nv] in internal (color-contiguous) order.
-// ---------------------------------------------------------------------------
+struct DomLevel {
+    int64_t n_own = 0, n_loc = 0, nf = 0;
+    std::vector<int64_t> l2n;              // [n_loc] local -> natural
+    std::vector<int64_t> blk;              // [ncolor+1] color blocks over owned cells
+    std::vector<int64_t> fnat;             // [nf] natural ids of the local faces (ascending)
+    std::vector<int32_t> fl, fr;           // [nf] local left / right, fr < 0: -(patch+1)
+    std::vector<double> vol;               // [n_own]
+    // gather slots (SELL-32 over owned cells: per color, chunks of 32 cells, entries [slot][lane])
+    int64_t nchunks = 0, ng_entries = 0, ns_entries = 0;
+    std::vector<int32_t> goff, gbase;      // [nchunks], [n_own]
+    std::vector<uint8_t> deg_int, deg_all; // [n_own]
+    std::vector<int32_t> gface;            // [ng_entries] +(f+1) left, -(f+1) right (local face f), 0 pad
+    // sweep slots (CSR over owned cells, same order as their interior gather slots)
+    std::vector<int32_t> soffc;            // [n_own+1]
+    std::vector<int32_t> sJ;               // [ns] local neighbour (owned or ghost)
+    std::vector<double> sRec;              // [ns][4] (A outward | S r)
+    // multigrid links (local indices)
+    std::vector<int32_t> child;            // [2][n_own] coarse levels: fine children, -1 = none
+    std::vector<int32_t> parent;           // [n_own] levels with a coarser one: coarse parent
+    // halo plan: groups (color c, peer k) at [off[c*npeers+k], off[c*npeers+k+1])
+    std::vector<int> peers;                // peer ranks, ascending
+    std::vector<int32_t> send_idx, recv_idx;   // local cells (owned / ghost)
+    std::vector<int64_t> send_off, recv_off;   // [ncolor*npeers + 1]
+};
+
 struct DevLevel {
     int dim, nv, ncolor;
-    int n, nf, nchunks;
-    // faces (natural face order; cells as internal indices)
-    const int *fl, *fr;          // fr < 0: -(patch+1)
+    int n, n_loc, nf;            // owned cells, owned + ghost cells, local faces
+    // faces (local)
+    const int *fl, *fr;
     const double *fA;            // [dim][nf]
     const int8_t *fM;            // [nf]
     double *Fs;                  // [nf][nv]  S_f F_f (left -> right)
     double *Srf;                 // [nf]      S_f r_f
     double *aM;                  // [nf]      alpha_f^{M_f}
-    // cells (AoS [n][nv], internal order)
+    // cells (AoS, local order; [n_loc] where ghosts are needed)
     const double *vol;           // [n]
-    double *W;                   // [n][nv] state
+    double *W;                   // [n_loc][nv] state
     double *Rt, *Rs, *F;         // [n][nv] RHS / restricted residual / forcing
     double *alpha, *sigma, *tmp; // [n]
-    double *rec;                 // [n][REC] sweep record: W_lin | 1/D | dW | alpha/2 (kernels.cuh Rec<D>)
+    double *rec;                 // [n_loc][12] sweep record: W_lin | 1/D | dW | alpha/2 (kernels.cuh Rec<D>)
     const uint8_t *deg_int, *deg_all;    // [n]
-    const int *gbase;            // [n] gather entry of slot 0; slot s at gbase + 32 s
-    const int *gface;            // gather entries
-    const int *soff;             // [n+1] sweep slot range per cell
-    const int *sJ;               // [ns] neighbour
-    double *sRec;                // [ns][4] A (outward) + S r
-    const int *perm;             // [n] internal -> natural
-    // multigrid links
-    const int *child;            // [2][n] fine children (internal idx in level-1), -1 = none (coarse levels)
-    const int *parent;           // [n] coarse parent (internal idx in level+1), fine levels
-    double *partial;             // [nblocks_max][nv] norm partials
+    const int *gbase;            // [n]
+    const int *gface;
+    const int *soff;             // [n+1]
+    const int *sJ;
+    double *sRec;                // [ns][4]
+    const int *perm;             // [n_loc] local -> natural
+    const int *child;            // [2][n]
+    const int *parent;           // [n]
+    double *partial;             // [nblocks][nv] norm partials
+    // halo
+    int n_send, n_recv;
+    const int *send_idx, *recv_idx;
+    double *sendbuf, *recvbuf;   // [n_send][nv], [n_recv][nv]
 };
 
 struct Profile {
@@ -89,7 +106,7 @@ struct Profile {
     std::vector<std::pair<int, int>> marks;  // (kernel class, event index of start)
 };
 
-// algorithmic bytes bookkeeping (DESIGN.md "Algorithmic bytes")
+// algorithmic bytes bookkeeping (DESIGN.md §6)
 struct LevelBytes {
     double face_flux = 0, face_prep = 0, gather = 0, restrict_ = 0, prolong = 0, update = 0;
     int max_slots64 = 1, max_slots128 = 1;   // staged sweep: max slots per 64 / 128-cell chunk
@@ -97,12 +114,21 @@ struct LevelBytes {
     std::vector<double> sweep_out; // per color, extra bytes when the launch also writes W = W0 + dW
 };
 
+struct Domain {
+    int rank = 0;
+    std::vector<DomLevel> lv;
+    std::vector<DevLevel> dv;
+    std::vector<LevelBytes> lbytes;
+};
+
 }  // namespace gmg
 
 struct gmg_ctx {
     gmg_options opt;
     std::string err;
-    std::vector<gmg::HostLevel> lv;
+    std::vector<gmg::HostLevel> lv;          // global hierarchy
+    std::vector<gmg::Domain> dom;            // domains driven by this process
+    int nparts = 1;                          // partitions of the global mesh
     std::vector<int32_t> user_color0;
     int n_patches = 0;
     std::vector<int32_t> patch_kind;
@@ -110,25 +136,25 @@ struct gmg_ctx {
     // device
     void *ws = nullptr;
     size_t ws_bytes = 0;
-    std::vector<gmg::DevLevel> dv;
     double *d_hist = nullptr;     // [hist_cap][nv]
     int hist_cap = 0;
-    int *d_flag = nullptr;
+    int *d_flag = nullptr;        // [0] history index, [1] non-finite flag
+    double *d_sumsq = nullptr;    // [ndom][nv] per-domain residual sums of squares
+    double *d_stage = nullptr;    // natural-order staging [nv][Nmax]
     double winf[5] = {0, 0, 0, 0, 0};
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph = nullptr;  // one V-cycle
     int64_t graph_launches = 0;
+    void *nccl_comm = nullptr;        // ncclComm_t (multi-rank)
     gmg::Profile prof;
-    std::vector<gmg::LevelBytes> lbytes;
-    double kbytes[GMG_K_COUNT] = {0};   // algorithmic bytes accumulated by the recorded sequence
-    int64_t launches = 0;          // kernels launched by the last recorded sequence
-    int lpc = 2;                   // sweep lanes per cell (1, 2, 4)
-    int minb = 4;                  // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
-    int prefetch = 0;              // sweep: L2-prefetch neighbour records before gathering (slower; kept for experiments)
-    int sweep_mode = 0;            // 0 = register gather (lpc lanes/cell), 1/2 = smem-staged 64/128-cell chunks
-    size_t l2_window = 0;          // bytes of the persisting-L2 window over a level's records (0 = off)
-    double *d_stage = nullptr;     // natural-order staging buffer [nv][nmax]
-    std::vector<int> host_keep_alive;
+    double kbytes[GMG_K_COUNT] = {0}; // algorithmic bytes accumulated by the recorded sequence
+    int64_t launches = 0;             // kernels launched by the last recorded sequence
+    int64_t exchanges = 0;            // halo exchanges in the last recorded sequence
+    int lpc = 2;                      // sweep lanes per cell (1, 2, 4)
+    int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
+    int prefetch = 0;                 // sweep: L2-prefetch neighbour records first (slower; experiment)
+    int sweep_mode = 0;               // 0 = register gather, 1/2 = smem-staged 64/128-cell chunks (experiment)
+    size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
 };
 
 namespace gmg {
@@ -141,5 +167,7 @@ bool validate_coloring(const HostLevel &L, const std::vector<int32_t> &col);
 int64_t agglomerate(const HostLevel &L, double theta, std::vector<int64_t> &parent, int64_t &nc);
 void build_coarse(const HostLevel &fine, HostLevel &coarse);
 void renumber(HostLevel &L);
-void build_layout(HostLevel &L);
+void build_domain_level(const HostLevel &G, int rank, DomLevel &D);
+void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, DomLevel &Dc);
+void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *part);
 }  // namespace gmg

@@ -270,12 +270,11 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     }
 }
 
-// deterministic final reduction of the norm partials -> hist[counter][q]
-__global__ void __launch_bounds__(256) k_norm_final(const double *__restrict__ partial, int nblocks, int nv,
-                                                    double *hist, int hist_cap, int *flags)
+// deterministic reduction of one domain's norm partials -> sumsq[q]
+__global__ void __launch_bounds__(256) k_norm_sum(const double *__restrict__ partial, int nblocks, int nv,
+                                                  double *sumsq)
 {
     __shared__ double sh[256];
-    const int idx = flags[0];
     for (int q = 0; q < nv; ++q) {
         double s = 0.0;
         for (int b = threadIdx.x; b < nblocks; b += 256) s += partial[(size_t)b * nv + q];
@@ -285,14 +284,73 @@ __global__ void __launch_bounds__(256) k_norm_final(const double *__restrict__ p
             if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
             __syncthreads();
         }
-        if (threadIdx.x == 0) {
-            const double v = sqrt(sh[0]);
-            if (idx < hist_cap) hist[(size_t)idx * nv + q] = v;
-            if (!isfinite(v)) flags[1] = 1;
-        }
+        if (threadIdx.x == 0) sumsq[q] = sh[0];
         __syncthreads();
     }
-    if (threadIdx.x == 0) flags[0] = idx + 1;
+}
+
+// domains' sums (in domain order; already all-reduced across ranks) -> hist[counter][q]
+__global__ void k_norm_hist(const double *__restrict__ sumsq, int ndom, int nv, double *hist, int hist_cap,
+                            int *flags)
+{
+    if (threadIdx.x != 0) return;
+    const int idx = flags[0];
+    for (int q = 0; q < nv; ++q) {
+        double s = 0.0;
+        for (int d = 0; d < ndom; ++d) s += sumsq[(size_t)d * nv + q];
+        const double v = sqrt(s);
+        if (idx < hist_cap) hist[(size_t)idx * nv + q] = v;
+        if (!isfinite(v)) flags[1] = 1;
+    }
+    flags[0] = idx + 1;
+}
+
+// ---------------------------------------------------------------------------
+// Halo exchange helpers (a13): pack owned cells' values, unpack into ghosts.
+// Element k of a buffer holds ncomp doubles of cell idx[k]; src/dst are cell
+// arrays with the given stride/offset (record dW, record W_lin, or W).
+// ---------------------------------------------------------------------------
+__global__ void k_pack(int count, const int *__restrict__ idx, const double *__restrict__ src, int stride,
+                       int offset, int ncomp, double *__restrict__ buf)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    const double *s = src + (size_t)idx[k] * stride + offset;
+    for (int q = 0; q < ncomp; ++q) buf[(size_t)k * ncomp + q] = s[q];
+}
+__global__ void k_unpack(int count, const int *__restrict__ idx, const double *__restrict__ buf, double *dst,
+                         int stride, int offset, int ncomp, int zero_at, int nzero)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    double *d = dst + (size_t)idx[k] * stride;
+    for (int q = 0; q < ncomp; ++q) d[offset + q] = buf[(size_t)k * ncomp + q];
+    for (int q = 0; q < nzero; ++q) d[zero_at + q] = 0.0;
+}
+
+// ghost records from the (current) ghost state: W_lin = W, dW = 0
+template <int D>
+__global__ void k_ghost_wlin(int n, int n_loc, const double *__restrict__ W, double *rec)
+{
+    using RC = Rec<D>;
+    const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_loc) return;
+#pragma unroll
+    for (int q = 0; q < D + 2; ++q) {
+        rec[(size_t)g * RC::STRIDE + RC::W + q] = W[(size_t)g * (D + 2) + q];
+        rec[(size_t)g * RC::STRIDE + RC::DW + q] = 0.0;
+    }
+}
+// ghost states after a smoothing step: W = W_lin + dW (both already exchanged)
+template <int D>
+__global__ void k_ghost_w(int n, int n_loc, const double *__restrict__ rec, double *W)
+{
+    using RC = Rec<D>;
+    const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_loc) return;
+#pragma unroll
+    for (int q = 0; q < D + 2; ++q)
+        W[(size_t)g * (D + 2) + q] = rec[(size_t)g * RC::STRIDE + RC::W + q] + rec[(size_t)g * RC::STRIDE + RC::DW + q];
 }
 
 // ---------------------------------------------------------------------------
@@ -593,22 +651,22 @@ __global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLe
     for (int q = 0; q < NV; ++q) F0.W[(size_t)i * NV + q] += a0 * corr[q];
 }
 
-// natural SoA [ncomp][n]  <->  internal AoS (stride, offset)
-__global__ void k_to_internal(int n, int ncomp, const int *__restrict__ perm, const double *__restrict__ src,
+// natural SoA [ncomp][N]  <->  local AoS (stride, offset), n local cells
+__global__ void k_to_internal(int n, int N, int ncomp, const int *__restrict__ perm, const double *__restrict__ src,
                               double *__restrict__ dst, int stride, int offset)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int nat = perm[i];
-    for (int q = 0; q < ncomp; ++q) dst[(size_t)i * stride + offset + q] = src[(size_t)q * n + nat];
+    for (int q = 0; q < ncomp; ++q) dst[(size_t)i * stride + offset + q] = src[(size_t)q * N + nat];
 }
-__global__ void k_to_natural(int n, int ncomp, const int *__restrict__ perm, const double *__restrict__ src,
+__global__ void k_to_natural(int n, int N, int ncomp, const int *__restrict__ perm, const double *__restrict__ src,
                              double *__restrict__ dst, int stride, int offset)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int nat = perm[i];
-    for (int q = 0; q < ncomp; ++q) dst[(size_t)q * n + nat] = src[(size_t)i * stride + offset + q];
+    for (int q = 0; q < ncomp; ++q) dst[(size_t)q * N + nat] = src[(size_t)i * stride + offset + q];
 }
 __global__ void k_fill(int n, double *p, double v)
 {

@@ -174,20 +174,12 @@ bool validate_coloring(const HostLevel &L, const std::vector<int32_t> &col)
 // stable sort by (color, natural id) -> color-contiguous internal order
 void renumber(HostLevel &L)
 {
-    L.blk.assign(L.ncolor + 1, 0);
-    for (int64_t i = 0; i < L.n; ++i) L.blk[L.color[i]]++;        // blk[c] = count of color c (c >= 1)
-    // blk as offsets: [blk[c-1], blk[c]) holds color c
-    std::vector<int64_t> cnt(L.blk);
-    L.blk[0] = 0;
-    for (int c = 1; c <= L.ncolor; ++c) L.blk[c] = L.blk[c - 1] + cnt[c];
+    std::vector<int64_t> cnt(L.ncolor + 1, 0), pos(L.ncolor + 1, 0);
+    for (int64_t i = 0; i < L.n; ++i) cnt[L.color[i]]++;
+    int64_t acc = 0;
+    for (int c = 1; c <= L.ncolor; ++c) { pos[c] = acc; acc += cnt[c]; }
     L.perm.assign(L.n, 0);
-    L.iperm.assign(L.n, 0);
-    std::vector<int64_t> fill(L.blk.begin(), L.blk.end() - 1);
-    for (int64_t i = 0; i < L.n; ++i) {               // ascending natural id = stable
-        const int64_t p = fill[L.color[i] - 1]++;
-        L.perm[p] = i;
-        L.iperm[i] = p;
-    }
+    for (int64_t i = 0; i < L.n; ++i) L.perm[pos[L.color[i]]++] = i;   // ascending natural id = stable
 }
 
 // ------------------------------------------------------------------ a4
@@ -350,7 +342,50 @@ void build_coarse(const HostLevel &fine, HostLevel &C)
     }
 }
 
-// Layouts (internal order).
+// ------------------------------------------------------------------ a5
+// Recursive coordinate bisection of the cell centroids: split the longest
+// extent so that each side gets cells in proportion to its partition count,
+// order (coordinate, natural id) -- deterministic on every rank.
+void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *part)
+{
+    std::vector<int64_t> ids(n);
+    std::iota(ids.begin(), ids.end(), (int64_t)0);
+    struct Job { int64_t b, e; int p0, np; };
+    std::vector<Job> st{{0, n, 0, nparts}};
+    while (!st.empty()) {
+        const Job j = st.back();
+        st.pop_back();
+        if (j.np <= 1 || j.e - j.b <= 1) {
+            for (int64_t k = j.b; k < j.e; ++k) part[ids[k]] = j.p0;
+            continue;
+        }
+        int axis = 0;
+        double best = -1.0;
+        for (int k = 0; k < dim; ++k) {
+            double lo = 1e300, hi = -1e300;
+            for (int64_t t = j.b; t < j.e; ++t) {
+                const double x = ctr[(size_t)k * n + ids[t]];
+                lo = std::min(lo, x);
+                hi = std::max(hi, x);
+            }
+            if (hi - lo > best) { best = hi - lo; axis = k; }
+        }
+        const int nl = j.np / 2, nr = j.np - nl;
+        const int64_t m = j.b + (j.e - j.b) * nl / j.np;
+        auto less = [&](int64_t a, int64_t b) {
+            const double xa = ctr[(size_t)axis * n + a], xb = ctr[(size_t)axis * n + b];
+            return xa < xb || (xa == xb && a < b);
+        };
+        std::nth_element(ids.begin() + j.b, ids.begin() + m, ids.begin() + j.e, less);
+        st.push_back({m, j.e, j.p0 + nl, nr});
+        st.push_back({j.b, m, j.p0, nl});
+    }
+}
+
+// Domain of `rank` on a global level: owned cells in global
+// renumbering order (color, natural id), then one layer of ghosts in (owner,
+// color, natural id) order; local faces = faces touching an owned cell, in
+// natural face order; layouts over owned cells:
 //  * gather slots (residual/prepare, thread per cell): SELL-32 -- per color,
 //    chunks of 32 consecutive cells, entries [slot][lane], chunk padded to its
 //    max degree.  Slots: interior faces (ascending id) then boundary faces.
@@ -358,78 +393,180 @@ void build_coarse(const HostLevel &fine, HostLevel &C)
 //    contiguous at [soffc[i], soffc[i+1]), same order as its gather slots;
 //    per slot the neighbour sJ and a 32-byte record (A_x, A_y, [A_z,] S r)
 //    with A = sigma S n oriented outward from the cell.
-void build_layout(HostLevel &L)
+//  * halo plan grouped (color, peer), natural id ascending within a group, so
+//    a sender's group equals the receiver's group element by element.
+void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
 {
-    const int d = L.dim;
-    const Csr inc = incident_faces(L);
-    L.chunk_base.assign(L.ncolor + 1, 0);
-    for (int c = 0; c < L.ncolor; ++c) {
-        const int64_t cnt = L.blk[c + 1] - L.blk[c];
-        L.chunk_base[c + 1] = L.chunk_base[c] + (int32_t)((cnt + kChunk - 1) / kChunk);
+    const int d = G.dim;
+    const int64_t N = G.n;
+    D = DomLevel();
+    auto owned = [&](int64_t c) { return G.part_of(c) == rank; };
+    std::vector<int32_t> n2l(N, -1);
+    D.blk.assign(G.ncolor + 1, 0);
+    for (int64_t p = 0; p < N; ++p) {
+        const int64_t nat = G.perm[p];
+        if (!owned(nat)) continue;
+        n2l[nat] = (int32_t)D.l2n.size();
+        D.l2n.push_back(nat);
+        D.blk[G.color[nat]]++;
     }
-    L.nchunks = L.chunk_base[L.ncolor];
-    L.gbase.assign(L.n, 0);
-    L.deg_int.assign(L.n, 0);
-    L.deg_all.assign(L.n, 0);
-    std::vector<int32_t> cchunk(L.n, 0);
-    std::vector<std::vector<int64_t>> slots(L.n);
-    for (int c = 0; c < L.ncolor; ++c) {
-        for (int64_t i = L.blk[c]; i < L.blk[c + 1]; ++i) {
-            const int64_t t = i - L.blk[c];
-            cchunk[i] = L.chunk_base[c] + (int32_t)(t / kChunk);
-            const int64_t nat = L.perm[i];
-            auto &s = slots[i];
-            for (int64_t a = inc.off[nat]; a < inc.off[nat + 1]; ++a)
-                if (L.right[inc.idx[a]] >= 0) s.push_back(inc.idx[a]);
-            const size_t ni = s.size();
-            for (int64_t a = inc.off[nat]; a < inc.off[nat + 1]; ++a)
-                if (L.right[inc.idx[a]] < 0) s.push_back(inc.idx[a]);
-            if (s.size() > 255) throw std::runtime_error("cell with more than 255 faces");
-            L.deg_int[i] = (uint8_t)ni;
-            L.deg_all[i] = (uint8_t)s.size();
+    D.n_own = (int64_t)D.l2n.size();
+    for (int c = 1; c <= G.ncolor; ++c) D.blk[c] += D.blk[c - 1];
+    std::vector<int64_t> ghosts;
+    for (int64_t f = 0; f < G.nf; ++f) {
+        const int64_t l = G.left[f], r = G.right[f];
+        const bool ol = owned(l), orr = r >= 0 && owned(r);
+        if (!ol && !orr) continue;
+        D.fnat.push_back(f);
+        if (r >= 0 && !ol) ghosts.push_back(l);
+        if (r >= 0 && !orr) ghosts.push_back(r);
+    }
+    std::sort(ghosts.begin(), ghosts.end(), [&](int64_t a, int64_t b) {
+        const int pa = G.part_of(a), pb = G.part_of(b);
+        if (pa != pb) return pa < pb;
+        if (G.color[a] != G.color[b]) return G.color[a] < G.color[b];
+        return a < b;
+    });
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    for (const int64_t g : ghosts) {
+        n2l[g] = (int32_t)D.l2n.size();
+        D.l2n.push_back(g);
+    }
+    D.n_loc = (int64_t)D.l2n.size();
+    D.nf = (int64_t)D.fnat.size();
+    D.fl.resize(D.nf);
+    D.fr.resize(D.nf);
+    for (int64_t k = 0; k < D.nf; ++k) {
+        const int64_t f = D.fnat[k];
+        D.fl[k] = n2l[G.left[f]];
+        D.fr[k] = G.right[f] >= 0 ? n2l[G.right[f]] : (int32_t)G.right[f];
+    }
+    D.vol.resize(D.n_own);
+    for (int64_t i = 0; i < D.n_own; ++i) D.vol[i] = G.vol[D.l2n[i]];
+
+    // incident local faces of owned cells, ascending local face id
+    std::vector<int64_t> ioff(D.n_own + 1, 0), iidx;
+    for (int64_t k = 0; k < D.nf; ++k) {
+        if (D.fl[k] < D.n_own) ioff[D.fl[k] + 1]++;
+        if (D.fr[k] >= 0 && D.fr[k] < D.n_own) ioff[D.fr[k] + 1]++;
+    }
+    std::partial_sum(ioff.begin(), ioff.end(), ioff.begin());
+    iidx.resize(ioff[D.n_own]);
+    {
+        std::vector<int64_t> pos(ioff.begin(), ioff.end() - 1);
+        for (int64_t k = 0; k < D.nf; ++k) {
+            if (D.fl[k] < D.n_own) iidx[pos[D.fl[k]]++] = k;
+            if (D.fr[k] >= 0 && D.fr[k] < D.n_own) iidx[pos[D.fr[k]]++] = k;
         }
     }
-    L.goff.assign(L.nchunks, 0);
+    std::vector<std::vector<int64_t>> slots(D.n_own);
+    D.deg_int.assign(D.n_own, 0);
+    D.deg_all.assign(D.n_own, 0);
+    for (int64_t i = 0; i < D.n_own; ++i) {
+        auto &s = slots[i];
+        for (int64_t a = ioff[i]; a < ioff[i + 1]; ++a)
+            if (D.fr[iidx[a]] >= 0) s.push_back(iidx[a]);
+        const size_t ni = s.size();
+        for (int64_t a = ioff[i]; a < ioff[i + 1]; ++a)
+            if (D.fr[iidx[a]] < 0) s.push_back(iidx[a]);
+        if (s.size() > 255) throw std::runtime_error("cell with more than 255 faces");
+        D.deg_int[i] = (uint8_t)ni;
+        D.deg_all[i] = (uint8_t)s.size();
+    }
+    // SELL-32 gather chunks per color
+    std::vector<int32_t> cchunk(D.n_own, 0), lane(D.n_own, 0);
     int64_t go = 0;
-    for (int c = 0; c < L.ncolor; ++c) {
-        for (int32_t k = L.chunk_base[c]; k < L.chunk_base[c + 1]; ++k) {
-            const int64_t i0 = L.blk[c] + (int64_t)(k - L.chunk_base[c]) * kChunk;
-            const int64_t i1 = std::min<int64_t>(i0 + kChunk, L.blk[c + 1]);
+    for (int c = 0; c < G.ncolor; ++c) {
+        for (int64_t i0 = D.blk[c]; i0 < D.blk[c + 1]; i0 += kChunk) {
+            const int64_t i1 = std::min<int64_t>(i0 + kChunk, D.blk[c + 1]);
             int mg = 0;
-            for (int64_t i = i0; i < i1; ++i) mg = std::max<int>(mg, L.deg_all[i]);
-            L.goff[k] = (int32_t)go;
+            for (int64_t i = i0; i < i1; ++i) {
+                mg = std::max<int>(mg, D.deg_all[i]);
+                cchunk[i] = (int32_t)D.goff.size();
+                lane[i] = (int32_t)(i - i0);
+            }
+            D.goff.push_back((int32_t)go);
             go += (int64_t)mg * kChunk;
         }
     }
-    L.soffc.assign(L.n + 1, 0);
-    for (int64_t i = 0; i < L.n; ++i) L.soffc[i + 1] = L.soffc[i] + L.deg_int[i];
-    const int64_t so = L.soffc[L.n];
+    D.nchunks = (int64_t)D.goff.size();
+    D.soffc.assign(D.n_own + 1, 0);
+    for (int64_t i = 0; i < D.n_own; ++i) D.soffc[i + 1] = D.soffc[i] + D.deg_int[i];
+    const int64_t so = D.soffc[D.n_own];
     if (go >= INT32_MAX || so >= INT32_MAX / 4) throw std::runtime_error("slot table exceeds int32");
-    L.ng_entries = go;
-    L.ns_entries = so;
-    L.gface.assign(go, 0);
-    L.sJ.assign(so, -1);
-    L.sface.assign(so, -1);
-    L.sRec.assign((size_t)4 * so, 0.0);
-    for (int c = 0; c < L.ncolor; ++c)
-    for (int64_t i = L.blk[c]; i < L.blk[c + 1]; ++i) {
-        const int32_t k = cchunk[i];
-        const int64_t lane = (i - L.blk[c]) % kChunk;
-        L.gbase[i] = (int32_t)(L.goff[k] + lane);
-        const int64_t nat = L.perm[i];
+    D.ng_entries = go;
+    D.ns_entries = so;
+    D.gface.assign(go, 0);
+    D.gbase.assign(D.n_own, 0);
+    D.sJ.assign(so, -1);
+    D.sRec.assign((size_t)4 * so, 0.0);
+    for (int64_t i = 0; i < D.n_own; ++i) {
+        D.gbase[i] = D.goff[cchunk[i]] + lane[i];
         for (size_t s = 0; s < slots[i].size(); ++s) {
-            const int64_t f = slots[i][s];
-            const bool is_left = (L.left[f] == nat);
-            L.gface[L.goff[k] + s * kChunk + lane] = is_left ? (int32_t)(f + 1) : -(int32_t)(f + 1);
-            if (s < L.deg_int[i]) {
-                const int64_t e = L.soffc[i] + (int64_t)s;
-                const int64_t other = is_left ? L.right[f] : L.left[f];
-                L.sJ[e] = (int32_t)L.iperm[other];
-                L.sface[e] = (int32_t)f;
+            const int64_t k = slots[i][s];
+            const bool is_left = (D.fl[k] == i);
+            D.gface[D.gbase[i] + s * kChunk] = is_left ? (int32_t)(k + 1) : -(int32_t)(k + 1);
+            if (s < D.deg_int[i]) {
+                const int64_t e = D.soffc[i] + (int64_t)s;
+                D.sJ[e] = is_left ? D.fr[k] : D.fl[k];
                 const double sg = is_left ? 1.0 : -1.0;
-                for (int q = 0; q < d; ++q) L.sRec[(size_t)4 * e + q] = sg * L.avec[(size_t)q * L.nf + f];
+                const int64_t f = D.fnat[k];
+                for (int q = 0; q < d; ++q) D.sRec[(size_t)4 * e + q] = sg * G.avec[(size_t)q * G.nf + f];
             }
         }
+    }
+    // halo plan
+    for (int64_t g = D.n_own; g < D.n_loc; ++g) D.peers.push_back(G.part_of(D.l2n[g]));
+    std::sort(D.peers.begin(), D.peers.end());
+    D.peers.erase(std::unique(D.peers.begin(), D.peers.end()), D.peers.end());
+    const int np = (int)D.peers.size();
+    auto peer_index = [&](int p) { return (int)(std::lower_bound(D.peers.begin(), D.peers.end(), p) - D.peers.begin()); };
+    const int ng = G.ncolor * np;
+    std::vector<std::vector<int32_t>> sg(ng), rg(ng);
+    for (int64_t g = D.n_own; g < D.n_loc; ++g) {                 // ghosts: (owner, color, id) order
+        const int64_t nat = D.l2n[g];
+        rg[(G.color[nat] - 1) * np + peer_index(G.part_of(nat))].push_back((int32_t)g);
+    }
+    for (int64_t i = 0; i < D.n_own; ++i) {                       // owned: (color, id) order
+        std::vector<int> ps;
+        for (int32_t e = D.soffc[i]; e < D.soffc[i + 1]; ++e) {
+            const int32_t j = D.sJ[e];
+            if (j >= D.n_own) ps.push_back(G.part_of(D.l2n[j]));
+        }
+        std::sort(ps.begin(), ps.end());
+        ps.erase(std::unique(ps.begin(), ps.end()), ps.end());
+        for (const int p : ps) sg[(G.color[D.l2n[i]] - 1) * np + peer_index(p)].push_back((int32_t)i);
+    }
+    D.send_off.assign(ng + 1, 0);
+    D.recv_off.assign(ng + 1, 0);
+    for (int k = 0; k < ng; ++k) {
+        D.send_off[k + 1] = D.send_off[k] + (int64_t)sg[k].size();
+        D.recv_off[k + 1] = D.recv_off[k] + (int64_t)rg[k].size();
+        D.send_idx.insert(D.send_idx.end(), sg[k].begin(), sg[k].end());
+        D.recv_idx.insert(D.recv_idx.end(), rg[k].begin(), rg[k].end());
+    }
+}
+
+// fine <-> coarse links inside one domain (agglomeration never crosses a
+// partition face, so both ends are owned by the same rank)
+void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, DomLevel &Dc)
+{
+    std::vector<int32_t> c2l(Gc.n, -1);
+    for (int64_t i = 0; i < Dc.n_own; ++i) c2l[Dc.l2n[i]] = (int32_t)i;
+    Df.parent.assign(Df.n_own, -1);
+    std::vector<std::pair<int64_t, int32_t>> fine_by_id(Df.n_own);
+    for (int64_t i = 0; i < Df.n_own; ++i) {
+        const int32_t pc = c2l[Gf.parent[Df.l2n[i]]];
+        if (pc < 0) throw std::runtime_error("coarse parent not owned by the fine cell's rank");
+        Df.parent[i] = pc;
+        fine_by_id[i] = {Df.l2n[i], (int32_t)i};
+    }
+    std::sort(fine_by_id.begin(), fine_by_id.end());
+    Dc.child.assign(2 * Dc.n_own, -1);
+    for (const auto &fi : fine_by_id) {                 // ascending natural id of the fine cell
+        const int32_t c = Df.parent[fi.second];
+        if (Dc.child[c] < 0) Dc.child[c] = fi.second;
+        else Dc.child[Dc.n_own + c] = fi.second;
     }
 }
 

@@ -29,7 +29,8 @@ ABI_SYMBOLS = ["gmg_default_options", "gmg_create", "gmg_load_mesh", "gmg_set_co
                "gmg_get_level_info", "gmg_get_maps", "gmg_get_level_geometry", "gmg_workspace_bytes",
                "gmg_set_workspace", "gmg_set_state", "gmg_set_level_state", "gmg_get_state", "gmg_set_alpha",
                "gmg_residual", "gmg_set_level_inputs", "gmg_smooth", "gmg_vcycle", "gmg_profile_vcycle",
-               "gmg_time_smooth", "gmg_vcycle_launches", "gmg_last_error", "gmg_destroy"]
+               "gmg_time_smooth", "gmg_vcycle_launches", "gmg_partition_rcb", "gmg_get_halo", "gmg_last_error",
+               "gmg_destroy"]
 
 
 class GmgError(RuntimeError):
@@ -43,7 +44,7 @@ class Options(C.Structure):
                 ("n_sweeps", C.c_int), ("n_levels", C.c_int), ("pre_smooth", C.c_int), ("post_smooth", C.c_int),
                 ("skew_limit", C.c_double), ("r_factor", C.c_double), ("fine_smoother", C.c_int),
                 ("df_mode", C.c_int), ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p),
-                ("device", C.c_int), ("stream", C.c_void_p)]
+                ("device", C.c_int), ("stream", C.c_void_p), ("local_domains", C.c_int)]
 
 
 _lib = None
@@ -80,6 +81,8 @@ def lib():
             "gmg_profile_vcycle": (I, [P, I, P, P, P]),
             "gmg_time_smooth": (I, [P, I, I, I, P, P, P]),
             "gmg_vcycle_launches": (I64, [P]),
+            "gmg_partition_rcb": (I, [I64, I, P, I, P]),
+            "gmg_get_halo": (I, [P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
             "gmg_last_error": (C.c_char_p, [P]),
             "gmg_destroy": (None, [P]),
         }
@@ -239,6 +242,34 @@ def gmg_vcycle_launches(ctx):
     return int(lib().gmg_vcycle_launches(ctx))
 
 
+def gmg_partition_rcb(ctr, nparts):
+    """a5: recursive coordinate bisection of centroids [dim][n] -> part[n]."""
+    ctr = _f64(ctr)
+    dim, n = ctr.shape
+    part = np.zeros(n, np.int32)
+    st = lib().gmg_partition_rcb(n, dim, _ptr(ctr), nparts, _ptr(part))
+    if st != GMG_OK:
+        raise GmgError(st, "gmg_partition_rcb")
+    return part
+
+
+def gmg_get_halo(ctx, level, dom=0):
+    """Halo plan of a local domain (natural ids); see include/gmg.h."""
+    no, ng, npr, ns, nr = C.c_int64(), C.c_int64(), C.c_int(), C.c_int64(), C.c_int64()
+    _check(ctx, lib().gmg_get_halo(ctx, level, dom, C.byref(no), C.byref(ng), C.byref(npr), C.byref(ns), C.byref(nr),
+                                   None, None, None, None, None, None, None))
+    _, nc, _ = gmg_get_level_info(ctx, level)
+    out = dict(owned=np.zeros(no.value, np.int64), ghost=np.zeros(ng.value, np.int64),
+               peers=np.zeros(npr.value, np.int32), send=np.zeros(ns.value, np.int64),
+               send_off=np.zeros(nc * npr.value + 1, np.int64), recv=np.zeros(nr.value, np.int64),
+               recv_off=np.zeros(nc * npr.value + 1, np.int64))
+    _check(ctx, lib().gmg_get_halo(ctx, level, dom, None, None, None, None, None,
+                                   *(_ptr(out[k]) for k in ("owned", "ghost", "peers", "send", "send_off", "recv",
+                                                            "recv_off"))))
+    out["n_colors"] = nc
+    return out
+
+
 def gmg_last_error(ctx):
     m = lib().gmg_last_error(ctx)
     return m.decode() if m else ""
@@ -258,10 +289,14 @@ class Solver:
     patch_kind, dim).  kw: gmg_options fields (cfl_imp, n_sweeps, ...).
     """
 
-    def __init__(self, mesh, n_levels=3, device=0, color0=None, build_only=False, **kw):
+    def __init__(self, mesh, n_levels=3, device=0, color0=None, build_only=False, part=None, nccl_id=None, **kw):
         self.dim = int(mesh.dim)
         self.nv = self.dim + 2
         self.opt = gmg_default_options(dim=self.dim, n_levels=n_levels, device=device, **kw)
+        self._nccl_id = None
+        if nccl_id is not None:
+            self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
+            self.opt.nccl_id = C.cast(self._nccl_id, C.c_void_p)
         self._torch = None
         if not build_only:
             import torch
@@ -271,7 +306,7 @@ class Solver:
             self.device = torch.device("cuda", device)
             self.opt.stream = torch.cuda.current_stream(self.device).cuda_stream
         self.ctx = gmg_create(self.opt)
-        gmg_load_mesh(self.ctx, mesh)
+        gmg_load_mesh(self.ctx, mesh, part)
         if color0 is not None:
             gmg_set_coloring(self.ctx, 0, color0)
         self.n_levels, self.build_status = gmg_build_hierarchy(self.ctx, n_levels)
@@ -335,6 +370,9 @@ class Solver:
 
     def vcycle_launches(self):
         return gmg_vcycle_launches(self.ctx)
+
+    def halo(self, level=0, dom=0):
+        return gmg_get_halo(self.ctx, level, dom)
 
     def close(self):
         if self.ctx:

@@ -1,0 +1,105 @@
+"""GPU parity of the partitioned path: P sub-domains driven
+in one process on one GPU (gmg_options.local_domains = P) -- the same
+layouts, halo plans, pack/unpack kernels and exchange points as the NCCL
+path, with device copies as the transport -- against the oracle run on the
+same partition-constrained hierarchy."""
+import numpy as np
+import pytest
+
+from synth import configs, state
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_06347_b200 import _build, gmg
+    _build.build()
+    gmg.lib()
+    return gmg
+
+
+def _case(name):
+    if name == "config1":
+        m = configs.config(1)
+        fs = configs.FREESTREAM[1]
+        return m, state.winf(*fs), state.gaussian_bump(m, *fs, jump=True)
+    if name == "box":
+        m = configs.box3d(6, 5, 4, 2, seed=3)
+        fs = (1.0, (0.6, 0.2, -0.1), 0.7)
+        return m, state.winf(*fs), state.perturbed(m, *fs, eps=0.1, seed=4)
+    m = configs.sphere_shell(8, 4, 4)
+    fs = configs.FREESTREAM[4]
+    return m, state.winf(*fs), state.bow_shock(m, *fs)
+
+
+@pytest.mark.parametrize("name", ["config1", "box", "sphere"])
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_partitioned_vcycle_parity(G, orc, name, P):
+    m, Winf, W = _case(name)
+    part = G.gmg_partition_rcb(m.ctr, P)
+    s = G.Solver(m, n_levels=3, part=part, local_domains=P)
+    s.set_state(W, Winf)
+    hist = s.vcycle(3)
+    Wg = s.get_state(0)
+    H = orc.build_hierarchy(m, 3, 0.5, part=part)
+    Wo, ho = orc.vcycle(H, W, Winf, orc.Options(), 3)
+    assert rel(Wg, Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+    # coarse states too
+    for l in (1, 2):
+        assert np.all(np.isfinite(s.get_state(l)))
+    s.close()
+
+
+def test_partitioned_fine_mclusgs_parity(G, orc):
+    m, Winf, W = _case("box")
+    part = G.gmg_partition_rcb(m.ctr, 3)
+    s = G.Solver(m, n_levels=3, part=part, local_domains=3, fine_smoother=1)
+    s.set_state(W, Winf)
+    s.vcycle(2)
+    H = orc.build_hierarchy(m, 3, 0.5, part=part)
+    Wo, _ = orc.vcycle(H, W, Winf, orc.Options(fine_smoother=1), 2)
+    assert rel(s.get_state(0), Wo) <= TOL
+    s.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_partitioned_smooth_and_residual_parity(G, orc, P):
+    m, Winf, W = _case("sphere")
+    part = G.gmg_partition_rcb(m.ctr, P)
+    s = G.Solver(m, n_levels=1, part=part, local_domains=P)
+    s.set_state(W, Winf)
+    lv = orc.Level.from_mesh(m)
+    R, a, S, rf = orc.residual(lv, W, Winf)
+    Rg, ag, Sg = s.residual(0)
+    assert rel(Rg, R) <= 1e-12 and rel(Sg, S) <= 1e-13
+    alpha = np.random.default_rng(9).uniform(0.05, 1.0, m.n_cells)
+    s.set_level_inputs(0, R, alpha)
+    dW = s.smooth(0, 6)
+    col, nc = orc.color(lv)
+    dWo = orc.smooth(lv, W, R, alpha, orc.diag(S, alpha, 10.0, 0.5), rf, col, nc, 6)
+    assert rel(dW, dWo) <= TOL
+    s.close()
+
+
+def test_partition_one_domain_equals_unpartitioned(G):
+    """P = 1 with a part[] array is the single-domain path."""
+    m, Winf, W = _case("config1")
+    a = G.Solver(m, n_levels=3)
+    a.set_state(W, Winf)
+    ha = a.vcycle(2)
+    b = G.Solver(m, n_levels=3, part=np.zeros(m.n_cells, np.int32), local_domains=1)
+    b.set_state(W, Winf)
+    hb = b.vcycle(2)
+    assert np.array_equal(a.get_state(0), b.get_state(0)) and np.array_equal(ha, hb)
+    a.close()
+    b.close()
