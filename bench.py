@@ -131,9 +131,22 @@ def run_reference(args, ws, rank):
     """Reference arm: the oracle (the only reference this tier has)."""
     if rank != 0:
         return 0
-    m, W, Winf = workload(args.config)
+    part = None
+    if ws > 1 and os.environ.get("GMG_BENCH_REPLICAS", "0") != "1":
+        # the GPU arm's partitioned workload: config 5 at P = ws, same partition constraint;
+        # bounded sample: at most 2 timed V-cycles of the oracle
+        from synth import configs, state
+        args.config = 5
+        m = configs.config(5, ws)
+        fs = configs.FREESTREAM[5]
+        W, Winf = state.bow_shock(m, *fs), state.winf(*fs)
+        from synth.partition import rcb               # same RCB rule as the GPU arm, no product code
+        part = rcb(m.ctr, ws)
+        args.steps_ref = min(args.steps_ref, 2)
+    else:
+        m, W, Winf = workload(args.config)
     import oracle
-    H = oracle.build_hierarchy(m, 3, 0.5)
+    H = oracle.build_hierarchy(m, 3, 0.5, part=part)
     opt = oracle.Options(n_sweeps=args.n_sweeps)
     cu = sum(e["level"].n for e in H[1:]) * 2 * args.n_sweeps
     Wc = W
@@ -185,12 +198,30 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    m, W, Winf = workload(args.config)
-    s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps)
+    replicas = ws > 1 and os.environ.get("GMG_BENCH_REPLICAS", "0") == "1"
+    if ws > 1 and not replicas:
+        # weak scaling: config 5, n = round(40 sqrt(P)) columns per cube-face edge
+        # (~1M cells per GPU), RCB partition, NCCL halo exchange after every color
+        args.config = 5
+        from synth import configs, state
+        m = configs.config(5, ws)
+        fs = configs.FREESTREAM[5]
+        W, Winf = state.bow_shock(m, *fs), state.winf(*fs)
+        part = gmg.gmg_partition_rcb(m.ctr, ws)
+        uid = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, part=part, nranks=ws, rank=rank,
+                       nccl_id=uid[0])
+        parallelism = f"mesh partitioned over {ws} GPUs (RCB), NCCL halo exchange per color"
+    else:
+        m, W, Winf = workload(args.config)
+        s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps)
+        parallelism = f"{ws} independent replicas" if ws > 1 else "single GPU"
     s.set_state(W, Winf)
     stream = torch.cuda.current_stream(dev)
     nv = s.nv
-    cu_cycle = sweep_updates_per_cycle(s.sizes, args.n_sweeps, 0)
+    # global sweep cell-updates per V-cycle (all ranks' owned cells when partitioned)
+    cu_cycle = sweep_updates_per_cycle(s.sizes, args.n_sweeps, 0) * (ws if replicas else 1)
 
     # warm-up (builds + replays the CUDA graph)
     for _ in range(args.warmup):
@@ -222,7 +253,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = cu_cycle * ws / (ms_step * 1e-3)
+    value = cu_cycle / (ms_step * 1e-3)
 
     # ---------------- per-kernel profile (CUDA events per launch) --------------
     s.set_state(W, Winf)
@@ -274,7 +305,7 @@ def main():
         t = torch.tensor([e2e_s], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": cu_cycle * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(W.nbytes),
+    e2e = {"value": cu_cycle / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(W.nbytes),
            "d2h_bytes_per_step": int(W.nbytes + (nv * 2 * 8)),
            "ms_per_step": e2e_s * 1e3, "timer": "host wall clock around synchronous ABI calls"}
 
@@ -293,10 +324,10 @@ def main():
                    "levels": [{"cells": int(n), "colors": int(c), "faces": int(f)} for (n, c, f) in s.sizes],
                    "sweep_cell_updates_per_vcycle": int(cu_cycle),
                    "l2": f"inputs larger than L2: workspace {ws_bytes / 1e9:.2f} GB >> 126 MB",
-                   "parallelism": f"dp{ws}" if ws > 1 else "single GPU",
-                   "multi_gpu": "independent replicas per rank (partitioned halo path: DESIGN.md)"},
-        "vcycles_per_s": 1e3 / ms_step * ws,
-        "fine_cell_vcycles_per_s": m.n_cells * 1e3 / ms_step * ws,
+                   "parallelism": parallelism,
+                   "n_gpus_partitions": 1 if replicas else ws},
+        "vcycles_per_s": 1e3 / ms_step * (ws if replicas else 1),
+        "fine_cell_vcycles_per_s": m.n_cells * 1e3 / ms_step * (ws if replicas else 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "k_sweep<3> (per-color MC-LU-SGS sweep)",

@@ -34,6 +34,8 @@ def test_rcb_partition(G):
         cnt = np.bincount(part, minlength=P)
         assert cnt.max() - cnt.min() <= 1                    # balanced to one cell
         assert np.array_equal(part, G.gmg_partition_rcb(m.ctr, P))   # deterministic
+        from synth.partition import rcb
+        assert np.array_equal(part, rcb(m.ctr, P))                   # the reference arm's restatement
 
 
 @pytest.mark.parametrize("name", list(MESHES))
