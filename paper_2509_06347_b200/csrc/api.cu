@@ -535,7 +535,7 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.n = (int)n; L.n_loc = (int)nloc; L.nf = (int)nf;
             L.fl = b.take<int>(nf); L.fr = b.take<int>(nf);
             L.fA = b.take<double>((size_t)d * nf); L.fM = b.take<int8_t>(nf);
-            L.Fs = b.take<double>((size_t)nv * nf); L.Srf = b.take<double>(nf); L.aM = b.take<double>(nf);
+            L.Frec = b.take<double>((size_t)kFaceRec * nf);
             L.vol = b.take<double>(n);
             L.W = b.take<double>((size_t)nv * nloc); L.Rt = b.take<double>((size_t)nv * n);
             L.rec = b.take<double>((size_t)kRecStride * nloc);

@@ -75,9 +75,7 @@ struct DevLevel {
     const int *fl, *fr;
     const double *fA;            // [dim][nf]
     const int8_t *fM;            // [nf]
-    double *Fs;                  // [nf][nv]  S_f F_f (left -> right)
-    double *Srf;                 // [nf]      S_f r_f
-    double *aM;                  // [nf]      alpha_f^{M_f}
+    double *Frec;                // [nf][8] (S_f F_f (left -> right) | S_f r_f | alpha_f^{M_f} | 0)
     // cells (AoS, local order; [n_loc] where ghosts are needed)
     const double *vol;           // [n]
     double *W;                   // [n_loc][nv] state

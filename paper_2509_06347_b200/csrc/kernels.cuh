@@ -57,6 +57,23 @@ __device__ __forceinline__ void ld_vec(const double *__restrict__ q, double *w)
     for (int k = 0; k < NV; ++k) w[k] = __ldg(q + k);
 }
 
+// 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256); p 32-byte aligned
+__device__ __forceinline__ void ld4nc(const double *p, double *v)
+{
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld4cs(const double *p, double *v)
+{
+    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void st4(double *p, const double *v)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+
 template <int D>
 __device__ __forceinline__ double pressure(const double *w, double gm1)
 {
@@ -89,37 +106,62 @@ __device__ __forceinline__ void ghost(int kind, const double *wi, const BCs &bc,
     }
 }
 
-// one half-range side of the first-order KFVS flux (O4): sgn = +1 -> u.n > 0
-// half of the left state, sgn = -1 -> u.n < 0 half of the right state.
+// primitive view of one face side, shared by the KFVS flux, the DF helper
+// and nothing else recomputes it (one 1/rho, one 1/p, one rsqrt per side)
 template <int D>
-__device__ __forceinline__ void kfvs_side(const double *w, const double *n, double sgn, const Phys &ph, double *F)
+struct Side {
+    double rho, ir, u[D], U, u2, p, ip;
+};
+template <int D>
+__device__ __forceinline__ Side<D> side_of(const double *w, const double *n, double gm1)
 {
-    const double rho = w[0], ir = 1.0 / rho;
-    double u[D], U = 0.0, u2 = 0.0;
+    Side<D> s;
+    s.rho = w[0];
+    s.ir = 1.0 / s.rho;
+    s.U = 0.0;
+    s.u2 = 0.0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) { u[k] = w[1 + k] * ir; U += u[k] * n[k]; u2 += u[k] * u[k]; }
-    const double p = ph.gm1 * (w[D + 1] - 0.5 * rho * u2);
-    const double lam = 0.5 * rho / p;          // lambda = rho / (2 p)
-    const double inv2l = p * ir;               // 1 / (2 lambda)
-    const double sl = sqrt(lam);
-    const double e = exp(-lam * U * U) * (0.5 * rsqrt(3.14159265358979323846 * lam));
-    const double m0 = 0.5 * erfc(-sgn * sl * U);
-    const double m1 = U * m0 + sgn * e;
-    const double m2 = U * m1 + inv2l * m0;
-    const double m3 = U * m2 + 2.0 * inv2l * m1;
-    F[0] = rho * m1;
+    for (int k = 0; k < D; ++k) { s.u[k] = w[1 + k] * s.ir; s.U += s.u[k] * n[k]; s.u2 += s.u[k] * s.u[k]; }
+    s.p = gm1 * (w[D + 1] - 0.5 * s.rho * s.u2);
+    s.ip = 1.0 / s.p;
+    return s;
+}
+
+// one half-range side of the first-order KFVS flux (O4), accumulated into F:
+// sgn = +1 -> u.n > 0 half of the left state, sgn = -1 -> u.n < 0 half of the
+// right state.  lambda = rho/(2p), <u^0> = erfc(-sgn sqrt(lambda) U)/2,
+// <u^1> = U<u^0> + sgn e^{-lambda U^2}/(2 sqrt(pi lambda)), recurrence for k+2.
+template <int D>
+__device__ __forceinline__ void kfvs_side(const Side<D> &s, const double *n, double sgn, const Phys &ph, double *F)
+{
+    const double lam = 0.5 * s.rho * s.ip;
+    const double inv2l = s.p * s.ir;                     // 1 / (2 lambda)
+    const double rl = rsqrt(lam);
+    const double sl = lam * rl;                          // sqrt(lambda)
+    const double e = exp(-lam * s.U * s.U) * (0.28209479177387814 * rl);   // 1/(2 sqrt(pi lambda))
+    const double m0 = 0.5 * erfc(-sgn * sl * s.U);
+    const double m1 = s.U * m0 + sgn * e;
+    const double m2 = s.U * m1 + inv2l * m0;
+    const double m3 = s.U * m2 + 2.0 * inv2l * m1;
+    const double rm1 = s.rho * m1, rm2 = s.rho * m2;
+    F[0] += rm1;
 #pragma unroll
-    for (int k = 0; k < D; ++k) F[1 + k] = rho * m2 * n[k] + rho * m1 * (u[k] - U * n[k]);
-    F[D + 1] = 0.5 * rho * (m3 + m1 * (u2 - U * U + ((double)(D - 1) + ph.K) * inv2l));
+    for (int k = 0; k < D; ++k) F[1 + k] += rm2 * n[k] + rm1 * (s.u[k] - s.U * n[k]);
+    F[D + 1] += 0.5 * s.rho * (m3 + m1 * (s.u2 - s.U * s.U + ((double)(D - 1) + ph.K) * inv2l));
 }
 
 // ---------------------------------------------------------------------------
 // Face kernel (a6 + a10 per face): r_f = omega (|u.n| + a) of the average
 // state; with FLUX also S F_f (KFVS) and alpha_f^{M_f} (DF helper).  The
 // state is read with a stride (NV for W, Rec<D>::STRIDE for the record).
+// Output: one 64-byte record per face, Frec = (S F[nv] | S r | alpha^M | 0..),
+// written with two 256-bit stores.
 // ---------------------------------------------------------------------------
+constexpr int kFaceRec = 8;
+template <int D> struct FR { static constexpr int SR = D + 2, AM = D + 3; };
+
 template <int D, bool FLUX, int STRIDE>
-__global__ void __launch_bounds__(256) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
+__global__ void __launch_bounds__(256, 3) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
 {
     constexpr int NV = D + 2;
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -128,7 +170,7 @@ __global__ void __launch_bounds__(256) k_face(DevLevel L, const double *__restri
     double A[D], S2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) { A[k] = __ldg(L.fA + (size_t)k * L.nf + f); S2 += A[k] * A[k]; }
-    const double S = sqrt(S2), iS = 1.0 / S;
+    const double iS = rsqrt(S2), S = S2 * iS;
     double n[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) n[k] = A[k] * iS;
@@ -137,47 +179,50 @@ __global__ void __launch_bounds__(256) k_face(DevLevel L, const double *__restri
     if (r >= 0) ld_vec<NV>(Wsrc + (size_t)r * STRIDE, wr);
     else ghost<D>(bc.kind[-r - 1], wl, bc, n, wr);
 
+    double out[kFaceRec];
+#pragma unroll
+    for (int q = 0; q < kFaceRec; ++q) out[q] = 0.0;
     // spectral radius of the conservative average (O6, reading A5)
     {
         double wb[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) wb[q] = 0.5 * (wl[q] + wr[q]);
         const double ib = 1.0 / wb[0];
-        double U = 0.0;
+        double mb = 0.0, m2 = 0.0;
 #pragma unroll
-        for (int k = 0; k < D; ++k) U += wb[1 + k] * ib * n[k];
-        const double pb = pressure<D>(wb, ph.gm1);
-        L.Srf[f] = S * (ph.omega * (fabs(U) + sqrt(ph.gamma * pb * ib)));
+        for (int k = 0; k < D; ++k) { mb += wb[1 + k] * n[k]; m2 += wb[1 + k] * wb[1 + k]; }
+        const double pb = ph.gm1 * (wb[D + 1] - 0.5 * m2 * ib);
+        out[FR<D>::SR] = S * (ph.omega * (fabs(mb * ib) + sqrt(ph.gamma * pb * ib)));
     }
     if (FLUX) {
-        double Fp[NV], Fm[NV];
-        kfvs_side<D>(wl, n, 1.0, ph, Fp);
-        kfvs_side<D>(wr, n, -1.0, ph, Fm);
-        double *out = L.Fs + (size_t)f * NV;
+        const Side<D> sl = side_of<D>(wl, n, ph.gm1), sr = side_of<D>(wr, n, ph.gm1);
+        kfvs_side<D>(sl, n, 1.0, ph, out);
+        kfvs_side<D>(sr, n, -1.0, ph, out);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) out[q] = S * (Fp[q] + Fm[q]);
-        // DF helper (O5)
-        const double pl = pressure<D>(wl, ph.gm1), pr = pressure<D>(wr, ph.gm1);
-        const double il = 1.0 / wl[0], ir = 1.0 / wr[0];
-        const double ial = rsqrt(ph.gamma * pl * il), iar = rsqrt(ph.gamma * pr * ir);
-        double Ul = 0.0, Ur = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) { Ul += wl[1 + k] * il * n[k]; Ur += wr[1 + k] * ir * n[k]; }
-        const double dMn = Ul * ial - Ur * iar;
+        for (int q = 0; q < NV; ++q) out[q] *= S;
+        // DF helper (O5): D = |dp|/p_l + |dp|/p_r + (dMa_n)^2 + |dMa_t|^2, alpha = 1/(1+D^2)
+        const double ial = rsqrt(ph.gamma * sl.p * sl.ir), iar = rsqrt(ph.gamma * sr.p * sr.ir);
+        const double dMn = sl.U * ial - sr.U * iar;
         double dMt2 = 0.0;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            const double t = (wl[1 + k] * il - Ul * n[k]) * ial - (wr[1 + k] * ir - Ur * n[k]) * iar;
+            const double t = (sl.u[k] - sl.U * n[k]) * ial - (sr.u[k] - sr.U * n[k]) * iar;
             dMt2 += t * t;
         }
-        const double dp = fabs(pl - pr);
-        const double Dv = dp / pl + dp / pr + dMn * dMn + dMt2;
+        const double dp = fabs(sl.p - sr.p);
+        const double Dv = dp * sl.ip + dp * sr.ip + dMn * dMn + dMt2;
         const double af = 1.0 / (1.0 + Dv * Dv);
         double aM = 1.0;
         const int M = L.fM[f];
         for (int g = 0; g < M; ++g) aM *= af;
-        L.aM[f] = aM;
+        out[FR<D>::AM] = aM;
     }
+    double *o = L.Frec + (size_t)f * kFaceRec;
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o), "d"(out[0]), "d"(out[1]), "d"(out[2]), "d"(out[3])
+                 : "memory");
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o + 4), "d"(out[4]), "d"(out[5]), "d"(out[6]),
+                 "d"(out[7])
+                 : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -199,18 +244,19 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         for (int s = 0; s < nt; ++s) {
             const int sf = __ldg(L.gface + gb + kChunk * s);
             const int f = (sf > 0 ? sf : -sf) - 1;
-            const double srf = __ldg(L.Srf + f);
+            const double *fr = L.Frec + (size_t)f * kFaceRec;
+            double c1[4];
+            ld4nc(fr + 4, c1);                 // 3D: SF4, Sr, alpha^M, 0   2D: Sr, alpha^M, 0, 0
+            const double srf = c1[FR<D>::SR - 4];
             sig += srf;
             if (a.flags & G_FLUX) {
-                const double *F = L.Fs + (size_t)f * NV;
-                if (sf > 0) {
+                double c0[4];
+                ld4nc(fr, c0);
+                const double sg = sf > 0 ? 1.0 : -1.0;
 #pragma unroll
-                    for (int q = 0; q < NV; ++q) R[q] += __ldg(F + q);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < NV; ++q) R[q] -= __ldg(F + q);
-                }
-                al *= __ldg(L.aM + f);
+                for (int q = 0; q < 4; ++q) R[q] += sg * c0[q];
+                if (D == 3) R[NV - 1] += sg * c1[0];
+                al *= c1[FR<D>::AM - 4];
             }
             if ((a.flags & G_PREPARE) && s < ni) L.sRec[(size_t)(s0 + s) * kSlotRec + D] = srf;
         }
@@ -400,23 +446,6 @@ struct SweepArgs {
     int prefetch;              // issue L2 prefetches of neighbour records first
     int max_slots;             // k_sweep_sm: max slots of any chunk of this level (smem sizing)
 };
-
-// 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256)
-__device__ __forceinline__ void ld4nc(const double *p, double *v)
-{
-    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
-}
-__device__ __forceinline__ void ld4cs(const double *p, double *v)
-{
-    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
-}
-__device__ __forceinline__ void st4(double *p, const double *v)
-{
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
-                 : "memory");
-}
 
 // neighbour record -> (W_lin, dW)
 template <int D>

@@ -433,6 +433,20 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
         D.l2n.push_back(g);
     }
     D.n_loc = (int64_t)D.l2n.size();
+    // local face order: by the first local cell of the face, then natural id --
+    // the face kernel's state gathers and the gather kernel's face reads then
+    // walk memory roughly in cell order
+    {
+        auto key = [&](int64_t f) {
+            int32_t k = n2l[G.left[f]];
+            if (G.right[f] >= 0) k = std::min(k, n2l[G.right[f]]);
+            return k;
+        };
+        std::vector<std::pair<int32_t, int64_t>> kf(D.fnat.size());
+        for (size_t t = 0; t < D.fnat.size(); ++t) kf[t] = {key(D.fnat[t]), D.fnat[t]};
+        std::sort(kf.begin(), kf.end());
+        for (size_t t = 0; t < kf.size(); ++t) D.fnat[t] = kf[t].second;
+    }
     D.nf = (int64_t)D.fnat.size();
     D.fl.resize(D.nf);
     D.fr.resize(D.nf);
