@@ -330,25 +330,16 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
     const DomLevel &H = dm.lv[l];
-    SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.soff, L.sJ, L.sRec,
-                rhs, Wout, ctx->prefetch, 0};
-    const int ncell = a.cend - a.cbeg;
-    if (ncell <= 0) return;
+    SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sJe, L.sRe,
+                rhs, Wout};
+    if (a.cend <= a.cbeg) return;
     Lc.pre(GMG_K_SWEEP);
-    if (ctx->sweep_mode == 1 || ctx->sweep_mode == 2) {
-        const int C = ctx->sweep_mode == 1 ? 64 : 128;
-        a.max_slots = C == 64 ? dm.lbytes[l].max_slots64 : dm.lbytes[l].max_slots128;
-        const size_t smem = (size_t)a.max_slots * (Rec<D>::STRIDE + kSlotRec) * sizeof(double);
-        if (C == 64) k_sweep_sm<D, 64><<<(ncell + 63) / 64, 64, smem, Lc.s>>>(a);
-        else k_sweep_sm<D, 128><<<(ncell + 127) / 128, 128, smem, Lc.s>>>(a);
-    } else {
-        const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
-        const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * kRecStride * sizeof(double)) : 0;
-        switch (ctx->lpc) {
-            case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb); break;
-            case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb); break;
-            default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb); break;
-        }
+    const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
+    const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * kRecStride * sizeof(double)) : 0;
+    switch (ctx->lpc) {
+        case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb); break;
+        case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb); break;
+        default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb); break;
     }
     Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
 }
@@ -545,8 +536,9 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.deg_int = b.take<uint8_t>(n); L.deg_all = b.take<uint8_t>(n);
             L.gbase = b.take<int>(n);
             L.gface = b.take<int>(H.ng_entries);
-            L.soff = b.take<int>(n + 1); L.sJ = b.take<int>(H.ns_entries);
-            L.sRec = b.take<double>((size_t)kSlotRec * H.ns_entries);
+            L.ecell = b.take<int>(n); L.estride = b.take<int>(n);
+            L.sJe = b.take<int>(H.sJe.size());
+            L.sRe = b.take<double>(H.sRe.size());
             L.perm = b.take<int>(nloc);
             L.child = l > 0 ? b.take<int>(2 * n) : nullptr;
             L.parent = l + 1 < nl ? b.take<int>(n) : nullptr;
@@ -602,15 +594,6 @@ void compute_bytes(gmg_ctx *ctx)
             B.prolong = (double)H.n_own * (2 * nv * 8 + 8 + 4) + (nl > 1 ? (double)dm.lv[1].n_own * (nv * 8 + 12) : 0) +
                         (nl > 2 ? (double)dm.lv[2].n_own * nv * 8 : 0);
             B.update = (double)H.n_own * 3 * nv * 8;
-            for (int C : {64, 128}) {   // smem staging: max slots of any C-cell chunk within a color block
-                int mx = 0;
-                for (int c = 0; c < ncolor; ++c)
-                    for (int64_t i0 = H.blk[c]; i0 < H.blk[c + 1]; i0 += C) {
-                        const int64_t i1 = std::min<int64_t>(i0 + C, H.blk[c + 1]);
-                        mx = std::max<int>(mx, H.soffc[i1] - H.soffc[i0]);
-                    }
-                (C == 64 ? B.max_slots64 : B.max_slots128) = std::max(mx, 1);
-            }
         }
     }
 }
@@ -665,8 +648,6 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     ctx->nparts = std::max(opt->nranks, opt->local_domains);
     if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
     if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
-    if (const char *e = std::getenv("GMG_PREFETCH")) ctx->prefetch = std::atoi(e);
-    if (const char *e = std::getenv("GMG_SWEEP")) ctx->sweep_mode = std::atoi(e);
     *out = ctx;
     return GMG_OK;
 }
@@ -867,9 +848,10 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.deg_all, H.deg_all.data(), H.deg_all.size()));
             CK(up_raw(L.gbase, H.gbase.data(), H.gbase.size() * sizeof(int)));
             CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
-            CK(up_raw(L.soff, H.soffc.data(), H.soffc.size() * sizeof(int)));
-            CK(up_raw(L.sJ, H.sJ.data(), H.sJ.size() * sizeof(int)));
-            CK(up_raw(L.sRec, H.sRec.data(), H.sRec.size() * sizeof(double)));
+            CK(up_raw(L.ecell, H.ell_cell.data(), H.ell_cell.size() * sizeof(int)));
+            CK(up_raw(L.estride, H.ell_stride.data(), H.ell_stride.size() * sizeof(int)));
+            CK(up_raw(L.sJe, H.sJe.data(), H.sJe.size() * sizeof(int)));
+            CK(up_raw(L.sRe, H.sRe.data(), H.sRe.size() * sizeof(double)));
             std::vector<int> perm(H.n_loc);
             for (int64_t i = 0; i < H.n_loc; ++i) perm[i] = (int)H.l2n[i];
             CK(up_i(L.perm, std::move(perm)));
@@ -893,16 +875,6 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
             ctx->l2_window = std::min<size_t>((size_t)maxw, (size_t)maxp);
         }
-    }
-    {   // dynamic shared memory of the staged sweep (may exceed the 48 KB default)
-        int mx = 1;
-        for (Domain &dm : ctx->dom)
-            for (auto &B : dm.lbytes) mx = std::max(mx, std::max(B.max_slots64, B.max_slots128));
-        const int bytes_sm = std::min(mx * (kRecStride + kSlotRec) * (int)sizeof(double), 227 * 1024);
-        CK(cudaFuncSetAttribute(k_sweep_sm<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
-        CK(cudaFuncSetAttribute(k_sweep_sm<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
-        CK(cudaFuncSetAttribute(k_sweep_sm<2, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
-        CK(cudaFuncSetAttribute(k_sweep_sm<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes_sm));
     }
     if (ctx->opt.nranks > 1 && !ctx->nccl_comm) {
         if (!nccl().load(ctx->err)) return GMG_ENCCL;

@@ -59,6 +59,10 @@ struct DomLevel {
     std::vector<int32_t> soffc;            // [n_own+1]
     std::vector<int32_t> sJ;               // [ns] local neighbour (owned or ghost)
     std::vector<double> sRec;              // [ns][4] (A outward | S r)
+    // device sweep slots (currently the CSR arrays; see build_domain_level)
+    std::vector<int32_t> sJe;              // [ne] neighbour
+    std::vector<double> sRe;               // [ne][4] (A outward | S r)
+    std::vector<int32_t> ell_cell, ell_stride;   // [n_own] entry of slot 0, stride between slots
     // multigrid links (local indices)
     std::vector<int32_t> child;            // [2][n_own] coarse levels: fine children, -1 = none
     std::vector<int32_t> parent;           // [n_own] levels with a coarser one: coarse parent
@@ -85,9 +89,9 @@ struct DevLevel {
     const uint8_t *deg_int, *deg_all;    // [n]
     const int *gbase;            // [n]
     const int *gface;
-    const int *soff;             // [n+1]
-    const int *sJ;
-    double *sRec;                // [ns][4]
+    const int *ecell, *estride;  // [n] ELL entry of slot 0, stride between slots (cells of the color)
+    const int *sJe;              // [ne] neighbour, -1 = padding
+    double *sRe;                 // [ne][4] A outward + S r
     const int *perm;             // [n_loc] local -> natural
     const int *child;            // [2][n]
     const int *parent;           // [n]
@@ -107,7 +111,6 @@ struct Profile {
 // algorithmic bytes bookkeeping
 struct LevelBytes {
     double face_flux = 0, face_prep = 0, gather = 0, restrict_ = 0, prolong = 0, update = 0;
-    int max_slots64 = 1, max_slots128 = 1;   // staged sweep: max slots per 64 / 128-cell chunk
     std::vector<double> sweep;     // per color
     std::vector<double> sweep_out; // per color, extra bytes when the launch also writes W = W0 + dW
 };
@@ -150,8 +153,6 @@ struct gmg_ctx {
     int64_t exchanges = 0;            // halo exchanges in the last recorded sequence
     int lpc = 2;                      // sweep lanes per cell (1, 2, 4)
     int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
-    int prefetch = 0;                 // sweep: L2-prefetch neighbour records first (slower; experiment)
-    int sweep_mode = 0;               // 0 = register gather, 1/2 = smem-staged 64/128-cell chunks (experiment)
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
 };
 

@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     for (int q = 0; q < NV; ++q) R[q] = 0.0;
     if (i < L.n) {
         const int gb = L.gbase[i], nt = L.deg_all[i], ni = L.deg_int[i];
-        const int s0 = (a.flags & G_PREPARE) ? L.soff[i] : 0;
+        const int e0 = (a.flags & G_PREPARE) ? L.ecell[i] : 0, es = (a.flags & G_PREPARE) ? L.estride[i] : 0;
         double sig = 0.0, al = 1.0;
         for (int s = 0; s < nt; ++s) {
             const int sf = __ldg(L.gface + gb + kChunk * s);
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
                 if (D == 3) R[NV - 1] += sg * c1[0];
                 al *= c1[FR<D>::AM - 4];
             }
-            if ((a.flags & G_PREPARE) && s < ni) L.sRec[(size_t)(s0 + s) * kSlotRec + D] = srf;
+            if ((a.flags & G_PREPARE) && s < ni) L.sRe[((size_t)e0 + (size_t)s * es) * kSlotRec + D] = srf;
         }
         if (a.flags & G_ALPHA) L.alpha[i] = al;
         if (a.flags & G_SIGMA) L.sigma[i] = sig;
@@ -435,16 +435,15 @@ __device__ __forceinline__ void flux_diff(const double *w, const double *dw, con
 }
 
 struct SweepArgs {
-    int cbeg, cend;
+    int cbeg, cend;            // color block [cbeg, cend) of owned cells
     double gm1;
-    double *rec;               // [n][Rec::STRIDE]
-    const int *soff;           // [n+1]
-    const int *sJ;             // [ns]
-    const double *sRec;        // [ns][4]
+    double *rec;               // [n_loc][Rec::STRIDE]
+    const int *ecell;          // [n] first slot entry of each cell
+    const uint8_t *deg;        // [n] interior slots of each cell
+    const int *sJe;            // [ns] neighbour
+    const double *sRe;         // [ns][4] (A outward | S r)
     const double *rhs;         // [n][nv]
     double *Wout;              // [n][nv] or null: W = W_lin + dW (last backward half-sweep)
-    int prefetch;              // issue L2 prefetches of neighbour records first
-    int max_slots;             // k_sweep_sm: max slots of any chunk of this level (smem sizing)
 };
 
 // neighbour record -> (W_lin, dW)
@@ -525,32 +524,15 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 #pragma unroll
     for (int q = 0; q < NV; ++q) acc[q] = 0.0;
     if (valid) {
-        const int e0 = __ldg(a.soff + i), e1 = __ldg(a.soff + i + 1);
-        if (a.prefetch) {
-            // phase A: all of this lane's neighbour indices at once, then L2
-            // prefetches of their records and of the cell's own data, so the
-            // real loads below wait on L2, not on a chain of DRAM latencies
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rhs + (size_t)i * NV));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + (size_t)i * RC::STRIDE + 4));
-            int jj[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int e = e0 + sub + k * LPC;
-                jj[k] = e < e1 ? __ldg(a.sJ + e) : -1;
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (jj[k] >= 0) {
-                    const double *rj = a.rec + (size_t)jj[k] * RC::STRIDE;
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rj));
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rj + RC::STRIDE - 1));
-                }
-            }
-        }
+        // per-cell contiguous slots (CSR): [ecell[i], ecell[i] + deg[i]); the
+        // two index loads are independent.  (Measured against ELL and
+        // chunked-ELL layouts: CSR wins on the coarse levels, where the degree
+        // spread is wide -- DESIGN.md §6.)
+        const int e0 = __ldg(a.ecell + i), e1 = e0 + __ldg(a.deg + i);
         for (int e = e0 + sub; e < e1; e += LPC) {
-            const int j = __ldg(a.sJ + e);
+            const int j = __ldg(a.sJe + e);
             double sr[4];
-            ld4cs(a.sRec + (size_t)e * kSlotRec, sr);
+            ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
             double w[NV], dw[NV];
             ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
             flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
@@ -564,64 +546,6 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
         }
     }
     if (valid && sub == 0) sweep_finish<D>(a, i, acc);
-}
-
-// ---------------------------------------------------------------------------
-// Shared-memory staged variant: one CTA per chunk of C consecutive cells of
-// the color.  Phase 1 issues cp.async (LDGSTS, no registers held) for every
-// slot's neighbour record (6 x 16 B) and slot record (2 x 16 B) of the chunk;
-// phase 2 computes thread-per-cell from shared memory.  Memory-level
-// parallelism is set by the chunk's bytes in flight, not by registers.
-// Dynamic smem: max_slots * (96 + 32) bytes.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
-{
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all()
-{
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
-
-template <int D, int C>
-__global__ void __launch_bounds__(C) k_sweep_sm(SweepArgs a)
-{
-    constexpr int NV = D + 2;
-    using RC = Rec<D>;
-    extern __shared__ __align__(16) double sm[];
-    const int c0 = a.cbeg + blockIdx.x * C;
-    const int c1 = min(c0 + C, a.cend);
-    const int e0 = __ldg(a.soff + c0), e1 = __ldg(a.soff + c1);
-    const int ns = e1 - e0;
-    double *recS = sm;                                    // [ns][12]
-    double *slotS = sm + (size_t)a.max_slots * RC::STRIDE; // [ns][4]
-    for (int it = threadIdx.x; it < ns * 6; it += C) {
-        const int s = it / 6, p = it - 6 * (it / 6);
-        const int j = __ldg(a.sJ + e0 + s);
-        cp_async16(recS + (size_t)s * RC::STRIDE + 2 * p, a.rec + (size_t)j * RC::STRIDE + 2 * p);
-    }
-    for (int it = threadIdx.x; it < ns * 2; it += C)
-        cp_async16(slotS + 2 * it, a.sRec + (size_t)e0 * kSlotRec + 2 * it);
-    cp_async_wait_all();
-    __syncthreads();
-    const int i = c0 + threadIdx.x;
-    if (i >= c1) return;
-    double acc[NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-    const int s0 = __ldg(a.soff + i) - e0, s1 = __ldg(a.soff + i + 1) - e0;
-    for (int s = s0; s < s1; ++s) {
-        const double *r = recS + (size_t)s * RC::STRIDE;
-        const double *sr = slotS + (size_t)s * kSlotRec;
-        double w[NV], dw[NV], A[D];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) { w[q] = r[RC::W + q]; dw[q] = r[RC::DW + q]; }
-#pragma unroll
-        for (int k = 0; k < D; ++k) A[k] = sr[k];
-        flux_diff<D>(w, dw, A, a.gm1, sr[D], acc);
-    }
-    sweep_finish<D>(a, i, acc);
 }
 
 // restriction to a coarse level (a8, A15) into the coarse record's

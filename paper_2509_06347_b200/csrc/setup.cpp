@@ -529,6 +529,14 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
             }
         }
     }
+    // device sweep slots: the CSR arrays themselves (entry of slot s of cell i
+    // = ell_cell[i] + s * ell_stride[i]; the indirection lets the layout be
+    // swapped for ELL variants, which measured slower on the coarse levels)
+    D.sJe = D.sJ;
+    D.sRe = D.sRec;
+    D.ell_cell.assign(D.soffc.begin(), D.soffc.end() - 1);
+    D.ell_stride.assign(D.n_own, 1);
+
     // halo plan
     for (int64_t g = D.n_own; g < D.n_loc; ++g) D.peers.push_back(G.part_of(D.l2n[g]));
     std::sort(D.peers.begin(), D.peers.end());
