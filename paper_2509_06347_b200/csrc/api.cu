@@ -121,6 +121,26 @@ struct Launcher {
     }
 };
 
+// every V-cycle kernel goes through here: optional programmatic dependent
+// launch (PDL) so a kernel's launch overlaps its predecessor's drain; the
+// kernels call pdl_enter() (griddepcontrol.wait) before touching its outputs
+template <typename... KP, typename... A>
+void klaunch(gmg_ctx *ctx, void (*k)(KP...), dim3 g, dim3 b, cudaStream_t s, A... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    if (ctx->pdl) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 constexpr int kRecStride = 12;   // Rec<2>::STRIDE == Rec<3>::STRIDE
 
 template <int D>
@@ -132,11 +152,11 @@ void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, b
     Lc.pre(GMG_K_FACE);
     const dim3 g(nblk(L.nf)), b(256);
     if (flux) {
-        if (from_rec) k_face<D, true, RS><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
-        else k_face<D, true, NV><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+        if (from_rec) klaunch(Lc.ctx, k_face<D, true, RS>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+        else klaunch(Lc.ctx, k_face<D, true, NV>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
     } else {
-        if (from_rec) k_face<D, false, RS><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
-        else k_face<D, false, NV><<<g, b, 0, Lc.s>>>(L, W, phys(ctx), bcs(ctx));
+        if (from_rec) klaunch(Lc.ctx, k_face<D, false, RS>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+        else klaunch(Lc.ctx, k_face<D, false, NV>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
     }
     Lc.post(GMG_K_FACE, flux ? dm.lbytes[l].face_flux : dm.lbytes[l].face_prep);
 }
@@ -149,11 +169,11 @@ void enqueue_gather(Launcher &Lc, Domain &dm, int di, int l, int flags, double *
     DevLevel &L = dm.dv[l];
     GArgs a{flags, ctx->opt.cfl_imp, ctx->opt.cfl_exp, Wexp, L.partial};
     Lc.pre(GMG_K_GATHER);
-    k_gather<D><<<nblk(L.n), 256, 0, Lc.s>>>(L, a);
+    klaunch(Lc.ctx, k_gather<D>, dim3(nblk(L.n)), dim3(256), Lc.s, L, a);
     Lc.post(GMG_K_GATHER, dm.lbytes[l].gather);
     if (flags & G_NORM) {
         Lc.pre(GMG_K_NORM);
-        k_norm_sum<<<1, 256, 0, Lc.s>>>(L.partial, nblk(L.n), L.nv, ctx->d_sumsq + (size_t)di * L.nv);
+        klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(256), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + (size_t)di * L.nv);
         Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
     }
 }
@@ -166,7 +186,7 @@ void enqueue_norm_hist(Launcher &Lc)
     if (ctx->opt.nranks > 1)
         nccl().AllReduce(ctx->d_sumsq, ctx->d_sumsq, nv, ncclDouble, ncclSum, (ncclComm_t)ctx->nccl_comm, Lc.s);
     Lc.pre(GMG_K_NORM);
-    k_norm_hist<<<1, 32, 0, Lc.s>>>(ctx->d_sumsq, (int)ctx->dom.size(), nv, ctx->d_hist, ctx->hist_cap, ctx->d_flag);
+    klaunch(Lc.ctx, k_norm_hist, dim3(1), dim3(32), Lc.s, ctx->d_sumsq, (int)ctx->dom.size(), nv, ctx->d_hist, ctx->hist_cap, ctx->d_flag);
     Lc.post(GMG_K_NORM, 0.0);
 }
 
@@ -202,7 +222,7 @@ void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
         const int64_t s0 = H.send_off[g0], s1 = H.send_off[g1];
         if (s1 > s0) {
             Lc.pre(GMG_K_NORM);
-            k_pack<<<nblk(s1 - s0), 256, 0, Lc.s>>>((int)(s1 - s0), L.send_idx + s0, src_of(L), stride, offset, NV,
+            klaunch(Lc.ctx, k_pack, dim3(nblk(s1 - s0)), dim3(256), Lc.s, (int)(s1 - s0), L.send_idx + s0, src_of(L), stride, offset, NV,
                                                    L.sendbuf + s0 * NV);
             Lc.post(GMG_K_NORM, (double)(s1 - s0) * NV * 16);
         }
@@ -251,7 +271,7 @@ void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
         const int64_t r0 = H.recv_off[g0], r1 = H.recv_off[g1];
         if (r1 > r0) {
             Lc.pre(GMG_K_NORM);
-            k_unpack<<<nblk(r1 - r0), 256, 0, Lc.s>>>((int)(r1 - r0), L.recv_idx + r0, L.recvbuf + r0 * NV,
+            klaunch(Lc.ctx, k_unpack, dim3(nblk(r1 - r0)), dim3(256), Lc.s, (int)(r1 - r0), L.recv_idx + r0, L.recvbuf + r0 * NV,
                                                      src_of(L), stride, offset, NV, zero_at, nzero);
             Lc.post(GMG_K_NORM, (double)(r1 - r0) * NV * 16);
         }
@@ -266,7 +286,7 @@ void enqueue_ghost_wlin(Launcher &Lc, int l)
         DevLevel &L = dm.dv[l];
         if (L.n_loc > L.n) {
             Lc.pre(GMG_K_NORM);
-            k_ghost_wlin<D><<<nblk(L.n_loc - L.n), 256, 0, Lc.s>>>(L.n, L.n_loc, L.W, L.rec);
+            klaunch(Lc.ctx, k_ghost_wlin<D>, dim3(nblk(L.n_loc - L.n)), dim3(256), Lc.s, L.n, L.n_loc, L.W, L.rec);
             Lc.post(GMG_K_NORM, 0.0);
         }
     }
@@ -279,7 +299,7 @@ void enqueue_ghost_w(Launcher &Lc, int l)
         DevLevel &L = dm.dv[l];
         if (L.n_loc > L.n) {
             Lc.pre(GMG_K_NORM);
-            k_ghost_w<D><<<nblk(L.n_loc - L.n), 256, 0, Lc.s>>>(L.n, L.n_loc, L.rec, L.W);
+            klaunch(Lc.ctx, k_ghost_w<D>, dim3(nblk(L.n_loc - L.n)), dim3(256), Lc.s, L.n, L.n_loc, L.rec, L.W);
             Lc.post(GMG_K_NORM, 0.0);
         }
     }
@@ -291,35 +311,43 @@ void enqueue_ghost_w(Launcher &Lc, int l)
 // optional L2 access-policy window over the level's cell records (the
 // gathered data), attached per launch so that graph capture keeps it
 template <class K>
-void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArgs &a, const void *win, size_t win_bytes)
+void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArgs &a, const void *win, size_t win_bytes,
+                        bool pdl)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = g;
     cfg.blockDim = b;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
+    int na = 0;
     if (win && win_bytes) {
-        at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        at[0].val.accessPolicyWindow.base_ptr = const_cast<void *>(win);
-        at[0].val.accessPolicyWindow.num_bytes = win_bytes;
-        at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-        at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
+        at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[na].val.accessPolicyWindow.base_ptr = const_cast<void *>(win);
+        at[na].val.accessPolicyWindow.num_bytes = win_bytes;
+        at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+        at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
     }
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = na ? at : nullptr;
+    cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
 template <int D, int LPC>
-void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win = nullptr, size_t win_bytes = 0)
+void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win, size_t win_bytes, bool pdl)
 {
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
     const dim3 g(nblk(nthreads)), b(256);
     switch (minb) {
-        case 6: launch_with_window(k_sweep<D, LPC, 6>, g, b, s, a, win, win_bytes); break;
-        case 8: launch_with_window(k_sweep<D, LPC, 8>, g, b, s, a, win, win_bytes); break;
-        default: launch_with_window(k_sweep<D, LPC, 4>, g, b, s, a, win, win_bytes); break;
+        case 6: launch_with_window(k_sweep<D, LPC, 6>, g, b, s, a, win, win_bytes, pdl); break;
+        case 8: launch_with_window(k_sweep<D, LPC, 8>, g, b, s, a, win, win_bytes, pdl); break;
+        default: launch_with_window(k_sweep<D, LPC, 4>, g, b, s, a, win, win_bytes, pdl); break;
     }
 }
 
@@ -337,9 +365,9 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
     const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
     const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * kRecStride * sizeof(double)) : 0;
     switch (ctx->lpc) {
-        case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb); break;
-        case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb); break;
-        default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb); break;
+        case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
+        case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
+        default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
     }
     Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
 }
@@ -373,7 +401,7 @@ void enqueue_restrict(Launcher &Lc, Domain &dm, int l)
     DevLevel &C = dm.dv[l];
     DevLevel &Fn = dm.dv[l - 1];
     Lc.pre(GMG_K_RESTRICT);
-    k_restrict<D><<<nblk(C.n), 256, 0, Lc.s>>>(C, Fn, Fn.W, Fn.Rt);
+    klaunch(Lc.ctx, k_restrict<D>, dim3(nblk(C.n)), dim3(256), Lc.s, C, Fn, Fn.W, Fn.Rt);
     Lc.post(GMG_K_RESTRICT, dm.lbytes[l].restrict_);
 }
 
@@ -432,7 +460,7 @@ void enqueue_vcycle(Launcher &Lc)
     // 5. DF-limited prolongation 2 -> 1 -> 0 (fused; rank-local)
     for (Domain &dm : doms) {
         Lc.pre(GMG_K_PROLONG);
-        k_prolong<D><<<nblk(dm.dv[0].n), 256, 0, Lc.s>>>(dm.dv[0], dm.dv[1], nl >= 3 ? dm.dv[2] : dm.dv[1], nl);
+        klaunch(Lc.ctx, k_prolong<D>, dim3(nblk(dm.dv[0].n)), dim3(256), Lc.s, dm.dv[0], dm.dv[1], nl >= 3 ? dm.dv[2] : dm.dv[1], nl);
         Lc.post(GMG_K_PROLONG, dm.lbytes[0].prolong);
     }
 }
@@ -648,6 +676,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     ctx->nparts = std::max(opt->nranks, opt->local_domains);
     if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
     if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
+    if (const char *e = std::getenv("GMG_PDL")) ctx->pdl = std::atoi(e);   // programmatic dependent launch
     *out = ctx;
     return GMG_OK;
 }

@@ -154,6 +154,7 @@ struct gmg_ctx {
     int lpc = 2;                      // sweep lanes per cell (1, 2, 4)
     int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
+    int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (no measured gain)
 };
 
 namespace gmg {

@@ -50,6 +50,16 @@ struct GArgs {
     double *partial;
 };
 
+// Programmatic dependent launch (sm_90+): every V-cycle kernel may be
+// launched while its predecessor drains; it waits here until the predecessor
+// grid has completed and its writes are visible, and immediately lets its
+// own successor be scheduled.  No-ops when launched without the attribute.
+__device__ __forceinline__ void pdl_enter()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <int NV>
 __device__ __forceinline__ void ld_vec(const double *__restrict__ q, double *w)
 {
@@ -163,6 +173,7 @@ template <int D> struct FR { static constexpr int SR = D + 2, AM = D + 3; };
 template <int D, bool FLUX, int STRIDE>
 __global__ void __launch_bounds__(256, 3) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
 {
+    pdl_enter();
     constexpr int NV = D + 2;
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= L.nf) return;
@@ -231,6 +242,7 @@ __global__ void __launch_bounds__(256, 3) k_face(DevLevel L, const double *__res
 template <int D>
 __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 {
+    pdl_enter();
     constexpr int NV = D + 2;
     using RC = Rec<D>;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -320,6 +332,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 __global__ void __launch_bounds__(256) k_norm_sum(const double *__restrict__ partial, int nblocks, int nv,
                                                   double *sumsq)
 {
+    pdl_enter();
     __shared__ double sh[256];
     for (int q = 0; q < nv; ++q) {
         double s = 0.0;
@@ -339,6 +352,7 @@ __global__ void __launch_bounds__(256) k_norm_sum(const double *__restrict__ par
 __global__ void k_norm_hist(const double *__restrict__ sumsq, int ndom, int nv, double *hist, int hist_cap,
                             int *flags)
 {
+    pdl_enter();
     if (threadIdx.x != 0) return;
     const int idx = flags[0];
     for (int q = 0; q < nv; ++q) {
@@ -359,6 +373,7 @@ __global__ void k_norm_hist(const double *__restrict__ sumsq, int ndom, int nv, 
 __global__ void k_pack(int count, const int *__restrict__ idx, const double *__restrict__ src, int stride,
                        int offset, int ncomp, double *__restrict__ buf)
 {
+    pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= count) return;
     const double *s = src + (size_t)idx[k] * stride + offset;
@@ -367,6 +382,7 @@ __global__ void k_pack(int count, const int *__restrict__ idx, const double *__r
 __global__ void k_unpack(int count, const int *__restrict__ idx, const double *__restrict__ buf, double *dst,
                          int stride, int offset, int ncomp, int zero_at, int nzero)
 {
+    pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= count) return;
     double *d = dst + (size_t)idx[k] * stride;
@@ -378,6 +394,7 @@ __global__ void k_unpack(int count, const int *__restrict__ idx, const double *_
 template <int D>
 __global__ void k_ghost_wlin(int n, int n_loc, const double *__restrict__ W, double *rec)
 {
+    pdl_enter();
     using RC = Rec<D>;
     const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_loc) return;
@@ -391,6 +408,7 @@ __global__ void k_ghost_wlin(int n, int n_loc, const double *__restrict__ W, dou
 template <int D>
 __global__ void k_ghost_w(int n, int n_loc, const double *__restrict__ rec, double *W)
 {
+    pdl_enter();
     using RC = Rec<D>;
     const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_loc) return;
@@ -514,6 +532,7 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, int i, const do
 template <int D, int LPC, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 {
+    pdl_enter();
     constexpr int NV = D + 2;
     using RC = Rec<D>;
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -554,6 +573,7 @@ template <int D>
 __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const double *__restrict__ Wf,
                                                   const double *__restrict__ Rf)
 {
+    pdl_enter();
     constexpr int NV = D + 2;
     using RC = Rec<D>;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -583,6 +603,7 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
 template <int D>
 __global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLevel C2, int nl)
 {
+    pdl_enter();
     constexpr int NV = D + 2;
     using RC = Rec<D>;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
