@@ -362,6 +362,17 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
                 rhs, Wout};
     if (a.cend <= a.cbeg) return;
     Lc.pre(GMG_K_SWEEP);
+    if (ctx->wsweep) {
+        const int W = ctx->wsweep, ms = dm.lbytes[l].max_ws;
+        const size_t smem = (size_t)W * ms * (kRecS + kSlotRec) * sizeof(double);
+        const int groups = (a.cend - a.cbeg + 31) / 32;
+        const dim3 g((groups + W - 1) / W), b(W * 32);
+        if (W == 1) k_sweep_ws<D, 1><<<g, b, smem, Lc.s>>>(a, ms);
+        else if (W == 4) k_sweep_ws<D, 4><<<g, b, smem, Lc.s>>>(a, ms);
+        else k_sweep_ws<D, 2><<<g, b, smem, Lc.s>>>(a, ms);
+        Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
+        return;
+    }
     const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
     const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * kRecStride * sizeof(double)) : 0;
     switch (ctx->lpc) {
@@ -622,6 +633,15 @@ void compute_bytes(gmg_ctx *ctx)
             B.prolong = (double)H.n_own * (2 * nv * 8 + 8 + 4) + (nl > 1 ? (double)dm.lv[1].n_own * (nv * 8 + 12) : 0) +
                         (nl > 2 ? (double)dm.lv[2].n_own * nv * 8 : 0);
             B.update = (double)H.n_own * 3 * nv * 8;
+            int mws = 1;
+            for (int c = 0; c < ncolor; ++c)
+                for (int64_t i0 = H.blk[c]; i0 < H.blk[c + 1]; i0 += kChunk) {
+                    const int64_t i1 = std::min<int64_t>(i0 + kChunk, H.blk[c + 1]);
+                    int s = 0;
+                    for (int64_t i = i0; i < i1; ++i) s += H.deg_int[i];
+                    mws = std::max(mws, s);
+                }
+            B.max_ws = mws;
         }
     }
 }
@@ -677,6 +697,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
     if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
     if (const char *e = std::getenv("GMG_PDL")) ctx->pdl = std::atoi(e);   // programmatic dependent launch
+    if (const char *e = std::getenv("GMG_WSWEEP")) ctx->wsweep = std::atoi(e);   // warp-staged sweep
     *out = ctx;
     return GMG_OK;
 }
@@ -904,6 +925,19 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
             ctx->l2_window = std::min<size_t>((size_t)maxw, (size_t)maxp);
         }
+    }
+    {   // dynamic shared memory of the warp-staged sweep (may exceed the 48 KB default)
+        int mx = 1;
+        for (Domain &dm : ctx->dom)
+            for (auto &B : dm.lbytes) mx = std::max(mx, B.max_ws);
+        const int per_warp = mx * (kRecS + kSlotRec) * (int)sizeof(double);
+        CK(cudaFuncSetAttribute(k_sweep_ws<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(per_warp, 227 * 1024)));
+        CK(cudaFuncSetAttribute(k_sweep_ws<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(2 * per_warp, 227 * 1024)));
+        CK(cudaFuncSetAttribute(k_sweep_ws<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(4 * per_warp, 227 * 1024)));
+        CK(cudaFuncSetAttribute(k_sweep_ws<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(per_warp, 227 * 1024)));
+        CK(cudaFuncSetAttribute(k_sweep_ws<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(2 * per_warp, 227 * 1024)));
+        CK(cudaFuncSetAttribute(k_sweep_ws<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(4 * per_warp, 227 * 1024)));
+        if (ctx->wsweep && ctx->wsweep * per_warp > 227 * 1024) ctx->wsweep = 1;
     }
     if (ctx->opt.nranks > 1 && !ctx->nccl_comm) {
         if (!nccl().load(ctx->err)) return GMG_ENCCL;

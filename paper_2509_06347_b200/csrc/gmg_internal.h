@@ -111,6 +111,7 @@ struct Profile {
 // algorithmic bytes bookkeeping
 struct LevelBytes {
     double face_flux = 0, face_prep = 0, gather = 0, restrict_ = 0, prolong = 0, update = 0;
+    int max_ws = 1;                // warp-staged sweep: max slots of any 32-cell group
     std::vector<double> sweep;     // per color
     std::vector<double> sweep_out; // per color, extra bytes when the launch also writes W = W0 + dW
 };
@@ -155,6 +156,7 @@ struct gmg_ctx {
     int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
     int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (no measured gain)
+    int wsweep = 0;                   // warp-staged sweep: warps per block (0 = register-gather sweep)
 };
 
 namespace gmg {

@@ -567,6 +567,66 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
     if (valid && sub == 0) sweep_finish<D>(a, i, acc);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-staged sweep: a warp owns 32 consecutive cells of the color; it
+// cp.async's (LDGSTS, no registers held) every neighbour record (6 x 16 B)
+// and slot record (2 x 16 B) of its cells' slots into its own smem slice,
+// waits (no block barrier), then computes thread-per-cell from smem.  Memory
+// parallelism = bytes staged per warp, independent of the register budget.
+// smem slice per warp: max_slots x (kRecS + 4) doubles; records padded to
+// 112 B so that 16-byte smem accesses of neighbouring slots spread over banks.
+// ---------------------------------------------------------------------------
+constexpr int kRecS = 14;   // staged record stride (doubles)
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+
+template <int D, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_sweep_ws(SweepArgs a, int max_slots)
+{
+    pdl_enter();
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    extern __shared__ __align__(16) double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = a.cbeg + (blockIdx.x * WARPS + warp) * 32;
+    if (i0 >= a.cend) return;                         // whole warp: no block-level sync below
+    const int i = i0 + lane;
+    const bool valid = i < a.cend;
+    const int last = min(i0 + 31, a.cend - 1);
+    const int g0 = __ldg(a.ecell + i0);
+    const int ns = __ldg(a.ecell + last) + __ldg(a.deg + last) - g0;
+    double *recS = sm + (size_t)warp * max_slots * (kRecS + kSlotRec);
+    double *slotS = recS + (size_t)max_slots * kRecS;
+    for (int t = lane; t < ns * 2; t += 32) cp_async16(slotS + 2 * t, a.sRe + (size_t)g0 * kSlotRec + 2 * t);
+    for (int t = lane; t < ns * 6; t += 32) {
+        const int s = t / 6, p = t - 6 * s;
+        const int j = __ldg(a.sJe + g0 + s);
+        cp_async16(recS + (size_t)s * kRecS + 2 * p, a.rec + (size_t)j * RC::STRIDE + 2 * p);
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    if (!valid) return;
+    double acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+    const int e0 = __ldg(a.ecell + i) - g0, e1 = e0 + __ldg(a.deg + i);
+    for (int s = e0; s < e1; ++s) {
+        const double *r = recS + (size_t)s * kRecS;
+        const double *sr = slotS + (size_t)s * kSlotRec;
+        double w[NV], dw[NV], A[D];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) { w[q] = r[RC::W + q]; dw[q] = r[RC::DW + q]; }
+#pragma unroll
+        for (int k = 0; k < D; ++k) A[k] = sr[k];
+        flux_diff<D>(w, dw, A, a.gm1, sr[D], acc);
+    }
+    sweep_finish<D>(a, i, acc);
+}
+
 // restriction to a coarse level (a8, A15) into the coarse record's
 // W_lin, plus dW = 0 for its sweeps
 template <int D>
