@@ -215,6 +215,19 @@ def test_torch_device_buffers(G):
     s.close()
 
 
+@pytest.mark.parametrize("k", [2, 3])
+def test_configs_2_3_full_size_vcycles(G, orc, k):
+    """BASELINE configs[1] (NACA0012 O-grid, ~20k mixed cells, no-slip wall)
+    and configs[2] (Mach-8 cylinder, 100k cells, bow-shock state, DF-adaptive
+    relaxation) at full size: 5 V-cycles, state and history vs the oracle."""
+    m = configs.config(k)
+    fs = configs.FREESTREAM[k]
+    W = state.bow_shock(m, *fs) if k == 3 else state.perturbed(m, *fs, eps=0.05, seed=2)
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, state.winf(*fs), W, 5)
+    assert rel(Wg, Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+
+
 @pytest.mark.slow
 def test_config4_full_size_vcycle(G, orc):
     """BASELINE configs[3] (the bench workload) at full size: maps bit-exact

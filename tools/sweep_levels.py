@@ -1,6 +1,6 @@
 """Quick sweep-kernel experiment (dev tool): time_smooth per level for a given GMG_LPC."""
 import json, os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_06347_b200 import gmg
 from synth import configs, state
 m = configs.config(4)
