@@ -310,6 +310,9 @@ void enqueue_ghost_w(Launcher &Lc, int l)
 // --------------------------------------------------------------------------
 // optional L2 access-policy window over the level's cell records (the
 // gathered data), attached per launch so that graph capture keeps it
+// sweep grid cap = resident waves x SMs x blocks/SM (set in gmg_set_workspace; 0 = one thread per cell)
+int g_sweep_grid_cap = 0;
+
 template <class K>
 void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArgs &a, const void *win, size_t win_bytes,
                         bool pdl)
@@ -343,7 +346,9 @@ template <int D, int LPC>
 void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win, size_t win_bytes, bool pdl)
 {
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
-    const dim3 g(nblk(nthreads)), b(256);
+    int nb = nblk(nthreads);
+    if (g_sweep_grid_cap > 0) nb = std::min(nb, g_sweep_grid_cap);
+    const dim3 g(nb), b(256);
     switch (minb) {
         case 6: launch_with_window(k_sweep<D, LPC, 6>, g, b, s, a, win, win_bytes, pdl); break;
         case 8: launch_with_window(k_sweep<D, LPC, 8>, g, b, s, a, win, win_bytes, pdl); break;
@@ -362,6 +367,12 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
                 rhs, Wout};
     if (a.cend <= a.cbeg) return;
     Lc.pre(GMG_K_SWEEP);
+    if (ctx->spsweep) {
+        const int64_t g0 = H.sp_off[c], ng = H.sp_off[c + 1] - g0 - 1;
+        klaunch(ctx, k_sweep_sp<D>, dim3((unsigned)ng), dim3(kSpT), Lc.s, a, L.spcell + g0);
+        Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
+        return;
+    }
     if (ctx->wsweep) {
         const int W = ctx->wsweep, ms = dm.lbytes[l].max_ws;
         const size_t smem = (size_t)W * ms * (kRecS + kSlotRec) * sizeof(double);
@@ -576,6 +587,7 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.gbase = b.take<int>(n);
             L.gface = b.take<int>(H.ng_entries);
             L.ecell = b.take<int>(n); L.estride = b.take<int>(n);
+            L.spcell = b.take<int>(H.sp_cell.size());
             L.sJe = b.take<int>(H.sJe.size());
             L.sRe = b.take<double>(H.sRe.size());
             L.perm = b.take<int>(nloc);
@@ -698,6 +710,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
     if (const char *e = std::getenv("GMG_PDL")) ctx->pdl = std::atoi(e);   // programmatic dependent launch
     if (const char *e = std::getenv("GMG_WSWEEP")) ctx->wsweep = std::atoi(e);   // warp-staged sweep
+    if (const char *e = std::getenv("GMG_SPSWEEP")) ctx->spsweep = std::atoi(e); // slot-parallel sweep
     *out = ctx;
     return GMG_OK;
 }
@@ -899,6 +912,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.gbase, H.gbase.data(), H.gbase.size() * sizeof(int)));
             CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
             CK(up_raw(L.ecell, H.ell_cell.data(), H.ell_cell.size() * sizeof(int)));
+            CK(up_raw(L.spcell, H.sp_cell.data(), H.sp_cell.size() * sizeof(int)));
             CK(up_raw(L.estride, H.ell_stride.data(), H.ell_stride.size() * sizeof(int)));
             CK(up_raw(L.sJe, H.sJe.data(), H.sJe.size() * sizeof(int)));
             CK(up_raw(L.sRe, H.sRe.data(), H.sRe.size() * sizeof(double)));
@@ -925,6 +939,16 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp));
             ctx->l2_window = std::min<size_t>((size_t)maxw, (size_t)maxp);
         }
+    }
+    {   // sweep grid: whole resident waves only (grid-stride kernel), GMG_SWEEP_WAVES (0 = uncapped)
+        int waves = 1, nsm = 0, per_sm = 0;
+        if (const char *e = std::getenv("GMG_SWEEP_WAVES")) waves = std::atoi(e);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
+        if (ctx->opt.dim == 3)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, 4>, 256, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, 4>, 256, 0);
+        g_sweep_grid_cap = waves > 0 ? waves * nsm * std::max(per_sm, 1) : 0;
     }
     {   // dynamic shared memory of the warp-staged sweep (may exceed the 48 KB default)
         int mx = 1;

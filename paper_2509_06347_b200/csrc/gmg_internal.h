@@ -63,6 +63,8 @@ struct DomLevel {
     std::vector<int32_t> sJe;              // [ne] neighbour
     std::vector<double> sRe;               // [ne][4] (A outward | S r)
     std::vector<int32_t> ell_cell, ell_stride;   // [n_own] entry of slot 0, stride between slots
+    std::vector<int32_t> sp_cell;          // slot-parallel sweep: group cell boundaries, per color
+    std::vector<int64_t> sp_off;           // [ncolor+1] first boundary of each color in sp_cell
     // multigrid links (local indices)
     std::vector<int32_t> child;            // [2][n_own] coarse levels: fine children, -1 = none
     std::vector<int32_t> parent;           // [n_own] levels with a coarser one: coarse parent
@@ -90,6 +92,7 @@ struct DevLevel {
     const int *gbase;            // [n]
     const int *gface;
     const int *ecell, *estride;  // [n] ELL entry of slot 0, stride between slots (cells of the color)
+    const int *spcell;           // slot-parallel sweep group boundaries
     const int *sJe;              // [ne] neighbour, -1 = padding
     double *sRe;                 // [ne][4] A outward + S r
     const int *perm;             // [n_loc] local -> natural
@@ -157,6 +160,7 @@ struct gmg_ctx {
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
     int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (no measured gain)
     int wsweep = 0;                   // warp-staged sweep: warps per block (0 = register-gather sweep)
+    int spsweep = 0;                  // slot-parallel sweep (thread per slot + block segmented reduction)
 };
 
 namespace gmg {

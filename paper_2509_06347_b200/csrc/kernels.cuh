@@ -535,7 +535,14 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
     pdl_enter();
     constexpr int NV = D + 2;
     using RC = Rec<D>;
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    // grid-stride over the color's cells: a launch sized to exactly the
+    // resident waves has no partial last wave (the block count of a color is
+    // rarely a multiple of SMs x resident blocks)
+    const int total = (a.cend - a.cbeg) * LPC;
+    const int stride = gridDim.x * blockDim.x;
+    const int rounds = (total + stride - 1) / stride;
+    for (int r = 0; r < rounds; ++r) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x + r * stride;
     const int i = a.cbeg + g / LPC;
     const int sub = g % LPC;
     const bool valid = i < a.cend;
@@ -565,6 +572,55 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
         }
     }
     if (valid && sub == 0) sweep_finish<D>(a, i, acc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Slot-parallel sweep: a block owns a run of whole cells of the color whose
+// CSR slots fit in SP_T lanes; lane t gathers slot e_begin + t (one dependent
+// index -> record round trip per lane, no per-cell serial slot loop), writes
+// its flux-difference contribution to smem, then one thread per cell sums its
+// contiguous slots and finishes the cell.  Groups: gcell[g] .. gcell[g+1].
+// ---------------------------------------------------------------------------
+constexpr int kSpT = 256;
+
+template <int D>
+__global__ void __launch_bounds__(kSpT) k_sweep_sp(SweepArgs a, const int *__restrict__ gcell)
+{
+    pdl_enter();
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    __shared__ double part[kSpT][NV];
+    const int c0 = __ldg(gcell + blockIdx.x), c1 = __ldg(gcell + blockIdx.x + 1);
+    const int eb = __ldg(a.ecell + c0);
+    const int ee = __ldg(a.ecell + c1 - 1) + __ldg(a.deg + c1 - 1);
+    const int t = threadIdx.x;
+    const int e = eb + t;
+    if (e < ee) {
+        double acc[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+        const int j = __ldg(a.sJe + e);
+        double sr[4];
+        ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+        double w[NV], dw[NV];
+        ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
+        flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) part[t][q] = acc[q];
+    }
+    __syncthreads();
+    const int i = c0 + t;
+    if (i >= c1) return;
+    double acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+    const int s0 = __ldg(a.ecell + i) - eb, s1 = s0 + __ldg(a.deg + i);
+    for (int s = s0; s < s1; ++s) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] += part[s][q];
+    }
+    sweep_finish<D>(a, i, acc);
 }
 
 // ---------------------------------------------------------------------------

@@ -536,6 +536,21 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
     D.sRe = D.sRec;
     D.ell_cell.assign(D.soffc.begin(), D.soffc.end() - 1);
     D.ell_stride.assign(D.n_own, 1);
+    // slot-parallel sweep groups: per color, runs of whole cells whose slots fit in 256 lanes
+    D.sp_off.assign(G.ncolor + 1, 0);
+    D.sp_cell.clear();
+    for (int c = 0; c < G.ncolor; ++c) {
+        D.sp_off[c] = (int64_t)D.sp_cell.size();
+        int64_t i = D.blk[c];
+        D.sp_cell.push_back((int32_t)i);
+        while (i < D.blk[c + 1]) {
+            int slots = 0, cells = 0;
+            while (i < D.blk[c + 1] && cells < 256 && slots + D.deg_int[i] <= 256) { slots += D.deg_int[i]; ++i; ++cells; }
+            if (cells == 0) throw std::runtime_error("cell with more than 256 interior faces");
+            D.sp_cell.push_back((int32_t)i);
+        }
+    }
+    D.sp_off[G.ncolor] = (int64_t)D.sp_cell.size();
 
     // halo plan
     for (int64_t g = D.n_own; g < D.n_loc; ++g) D.peers.push_back(G.part_of(D.l2n[g]));
