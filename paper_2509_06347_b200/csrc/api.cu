@@ -404,16 +404,47 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
 {
     gmg_ctx *ctx = Lc.ctx;
     const int nc = ctx->lv[l].ncolor;
-    for (int s = 0; s < n_sweeps; ++s) {
-        for (int half = 0; half < 2; ++half) {
-            for (int cc = 0; cc < nc; ++cc) {
-                const int c = half == 0 ? cc : nc - 1 - cc;
-                const bool last = (s == n_sweeps - 1) && half == 1;
-                for (Domain &dm : ctx->dom)
-                    enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), last ? wout(dm.dv[l]) : nullptr);
-                enqueue_exchange<D>(Lc, l, EX_DW, c);
+    struct Ph { int c; bool last; };
+    std::vector<Ph> seq;
+    for (int s = 0; s < n_sweeps; ++s)
+        for (int half = 0; half < 2; ++half)
+            for (int cc = 0; cc < nc; ++cc)
+                seq.push_back({half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1});
+    const bool fuse = ctx->tail_cells > 0 && ctx->nparts == 1 && ctx->dom.size() == 1;
+    for (size_t k = 0; k < seq.size();) {
+        if (fuse) {
+            // a run of >= 2 consecutive tiny color phases -> one single-CTA launch
+            Domain &dm = ctx->dom[0];
+            const DomLevel &H = dm.lv[l];
+            auto tiny = [&](size_t t) {
+                return t < seq.size() && H.blk[seq[t].c + 1] - H.blk[seq[t].c] <= ctx->tail_cells;
+            };
+            size_t r = k;
+            while (tiny(r) && r - k < (size_t)kTailMaxPh) ++r;
+            if (r - k >= 2) {
+                DevLevel &L = dm.dv[l];
+                TailArgs t{};
+                t.nph = (int)(r - k);
+                for (size_t p = k; p < r; ++p) {
+                    t.cbeg[p - k] = (int)H.blk[seq[p].c];
+                    t.cend[p - k] = (int)H.blk[seq[p].c + 1];
+                    t.wout[p - k] = seq[p].last ? 1 : 0;
+                }
+                t.a = SweepArgs{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sJe, L.sRe, rhs(L), wout(L)};
+                double bytes = 0;
+                for (size_t p = k; p < r; ++p)
+                    bytes += dm.lbytes[l].sweep[seq[p].c] + (seq[p].last ? dm.lbytes[l].sweep_out[seq[p].c] : 0.0);
+                Lc.pre(GMG_K_SWEEP);
+                klaunch(ctx, k_sweep_tail<D>, dim3(1), dim3(kTailT), Lc.s, t);
+                Lc.post(GMG_K_SWEEP, bytes);
+                k = r;
+                continue;
             }
         }
+        for (Domain &dm : ctx->dom)
+            enqueue_sweep_color<D>(Lc, dm, l, seq[k].c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr);
+        enqueue_exchange<D>(Lc, l, EX_DW, seq[k].c);
+        ++k;
     }
 }
 
@@ -711,6 +742,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_PDL")) ctx->pdl = std::atoi(e);   // programmatic dependent launch
     if (const char *e = std::getenv("GMG_WSWEEP")) ctx->wsweep = std::atoi(e);   // warp-staged sweep
     if (const char *e = std::getenv("GMG_SPSWEEP")) ctx->spsweep = std::atoi(e); // slot-parallel sweep
+    if (const char *e = std::getenv("GMG_TAIL")) ctx->tail_cells = std::atoi(e);  // tiny-color fusion threshold
     *out = ctx;
     return GMG_OK;
 }

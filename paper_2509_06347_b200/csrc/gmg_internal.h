@@ -161,6 +161,7 @@ struct gmg_ctx {
     int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (no measured gain)
     int wsweep = 0;                   // warp-staged sweep: warps per block (0 = register-gather sweep)
     int spsweep = 0;                  // slot-parallel sweep (thread per slot + block segmented reduction)
+    int tail_cells = 0;               // fuse runs of consecutive color phases with <= this many cells (0 = off; neutral)
 };
 
 namespace gmg {

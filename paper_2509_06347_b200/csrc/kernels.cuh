@@ -15,7 +15,9 @@ namespace gmg {
 
 // per-cell sweep record layout (doubles)
 template <int D> struct Rec;
-template <> struct Rec<3> { static constexpr int W = 0, INVD = 5, DW = 6, HA = 11, STRIDE = 12; };
+// 3D: [W0..W3 | W4 dW0 dW1 dW2 | dW3 dW4 1/D a/2]: the own-cell epilogue reads
+// only the last 32-B chunk (1/D, alpha/2) and rewrites dW without reading the rest
+template <> struct Rec<3> { static constexpr int W = 0, DW = 5, INVD = 10, HA = 11, STRIDE = 12; };
 template <> struct Rec<2> { static constexpr int W = 0, DW = 4, INVD = 8, HA = 9, STRIDE = 12; };
 // (both 96 B: 32-byte aligned, so a neighbour record is three 256-bit loads)
 // per-slot record: A_0..A_{D-1}, S r at [D]
@@ -474,7 +476,7 @@ __device__ __forceinline__ void ld_neighbour(const double *rj, double *w, double
         ld4nc(rj + 4, c1);
         ld4nc(rj + 8, c2);
         w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-        dw[0] = c1[2]; dw[1] = c1[3]; dw[2] = c2[0]; dw[3] = c2[1]; dw[4] = c2[2];
+        dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
     } else {
         ld4nc(rj, w);
         ld4nc(rj + 4, dw);
@@ -494,23 +496,26 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, int i, const do
 #pragma unroll
     for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
     if constexpr (D == 3) {
-        double c0[4], c1[4], c2[4];
-        ld4nc(ri + 4, c1);                          // W[4], 1/D, dW0, dW1
-        ld4nc(ri + 8, c2);                          // dW2, dW3, dW4, alpha/2
-        const double invD = c1[1], ha = c2[3];
+        double c2[4];
+        ld4nc(ri + 8, c2);                          // dW3, dW4, 1/D, alpha/2
+        const double invD = c2[2], ha = c2[3];
         double d[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-        c1[2] = d[0]; c1[3] = d[1]; c2[0] = d[2]; c2[1] = d[3]; c2[2] = d[4];
-        st4(ri + 4, c1);
+        ri[5] = d[0];                               // dW0 (W4 at ri[4] untouched)
+        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(ri + 6), "d"(d[1]), "d"(d[2]) : "memory");
+        c2[0] = d[3];
+        c2[1] = d[4];
         st4(ri + 8, c2);
         if (a.Wout) {
+            double c0[4];
             ld4nc(ri, c0);
+            const double w4 = __ldg(ri + 4);
             a.Wout[o + 0] = c0[0] + d[0];
             a.Wout[o + 1] = c0[1] + d[1];
             a.Wout[o + 2] = c0[2] + d[2];
             a.Wout[o + 3] = c0[3] + d[3];
-            a.Wout[o + 4] = c1[0] + d[4];
+            a.Wout[o + 4] = w4 + d[4];
         }
     } else {
         double c2[4];
@@ -572,6 +577,79 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
         }
     }
     if (valid && sub == 0) sweep_finish<D>(a, i, acc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Tail sweep: consecutive TINY color phases of a smoothing step (e.g. the last
+// colors of a forward pass and the first ones of the next backward pass) run
+// in ONE single-CTA launch, one phase after the other with a block barrier in
+// between -- the color order of Algorithm 2 is kept, only the launches are
+// merged.  Neighbour increments written by an earlier phase of the same launch
+// are read with coherent loads.  Single-domain runs only (a partitioned run
+// exchanges increments after every color).
+// ---------------------------------------------------------------------------
+constexpr int kTailMaxPh = 12;
+constexpr int kTailT = 1024;
+struct TailArgs {
+    int nph;
+    int cbeg[kTailMaxPh], cend[kTailMaxPh], wout[kTailMaxPh];
+    SweepArgs a;                // rec, ecell, deg, sJe, sRe, rhs, Wout, gm1 (cbeg/cend unused)
+};
+
+__device__ __forceinline__ void ld4(const double *p, double *v)
+{
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTailT) k_sweep_tail(TailArgs t)
+{
+    pdl_enter();
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    SweepArgs a = t.a;
+    for (int p = 0; p < t.nph; ++p) {
+        a.cbeg = t.cbeg[p];
+        a.cend = t.cend[p];
+        double *wout = t.wout[p] ? t.a.Wout : nullptr;
+        a.Wout = wout;
+        const int total = (a.cend - a.cbeg) * 2;
+        for (int base = 0; base < total; base += kTailT) {
+            const int g = base + threadIdx.x;
+            const int i = a.cbeg + g / 2, sub = g & 1;
+            const bool valid = g < total;
+            double acc[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+            if (valid) {
+                const int e0 = __ldg(a.ecell + i), e1 = e0 + __ldg(a.deg + i);
+                for (int e = e0 + sub; e < e1; e += 2) {
+                    const int j = __ldg(a.sJe + e);
+                    double sr[4];
+                    ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                    const double *rj = a.rec + (size_t)j * RC::STRIDE;
+                    double w[NV], dw[NV];
+                    if constexpr (D == 3) {
+                        double c0[4], c1[4], c2[4];
+                        ld4(rj, c0);
+                        ld4(rj + 4, c1);
+                        ld4(rj + 8, c2);
+                        w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
+                        dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                    } else {
+                        ld4(rj, w);
+                        ld4(rj + 4, dw);
+                    }
+                    flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 1);
+            if (valid && sub == 0) sweep_finish<D>(a, i, acc);
+        }
+        __syncthreads();
     }
 }
 
