@@ -76,11 +76,16 @@ typedef struct {
     double skew_limit;      /* agglomeration skewness threshold theta (A21); 0.5              */
     double r_factor;        /* omega in r_ij = omega (|U.n| + a) >= Lambda; 1.0       */
     int fine_smoother;      /* 0 = explicit Eq.(smo) (paper); 1 = MC-LU-SGS        */
-    int df_mode;            /* 0 = first-order DF helper (O5); 1 = user alpha; 2 = alpha == 1 */
+    int df_mode;            /* 0 = first-order DF helper (O5); 1 = user alpha; 2 = alpha == 1
+                               (DF off); 3 = fixed relaxation factor beta in the smoother      */
     int rank, nranks;       /* this rank / world size (1 = single GPU)                        */
     const void *nccl_id;    /* 128-byte ncclUniqueId (nranks > 1), else NULL                  */
     int device;             /* CUDA device ordinal                                            */
     void *stream;           /* cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)    */
+    double beta;            /* df_mode 3 only: the fixed relaxation factor of the "traditional
+                               relaxation" used in place of the per-cell DF alpha in
+                               the smoother's diagonal and off-diagonal; prolongation keeps the
+                               DF limiter (reading B3).  Default 0.5.                         */
     int local_domains;      /* nranks == 1 only: drive this many partitions (part[] values
                                0..local_domains-1) as separate domains in this process, their
                                halo exchanged by device copies on the stream.  Same layouts,

@@ -28,7 +28,8 @@ class Options:
     skew_limit: float = 0.5
     r_factor: float = 1.0
     fine_smoother: int = 0      # 0 explicit (paper), 1 MC-LU-SGS
-    df_mode: int = 0            # 0 first-order helper, 1 user alpha, 2 alpha == 1
+    df_mode: int = 0            # 0 first-order helper, 1 user alpha, 2 alpha == 1, 3 fixed beta relaxation
+    beta: float = 0.5           # df_mode 3: "traditional" fixed relaxation factor (reading B3)
 
 
 def perm_from_color(col):
@@ -83,6 +84,12 @@ def vcycle(levels, W0, Winf, opt: Options, n_cycles=1, user_alpha=None, trace=No
             return np.ones_like(a)
         return a
 
+    def relax(a):
+        # the factor that blends the implicit and explicit operators in the
+        # smoother: the DF alpha (Eq.(DF-relaxation-hybrid)), or a fixed
+        # beta for the traditional relaxation of P:526-532 (reading B3)
+        return np.full_like(a, opt.beta) if opt.df_mode == 3 else a
+
     for cyc in range(n_cycles):
         R0, a0, S0, rf0 = residual(L[0], W, Winf, g, om)
         a0 = fine_alpha(a0)
@@ -91,8 +98,8 @@ def vcycle(levels, W0, Winf, opt: Options, n_cycles=1, user_alpha=None, trace=No
         if opt.fine_smoother == 0:
             W = explicit_update(W, S0, R0, opt.cfl_exp)
         else:
-            D0 = diag(S0, a0, opt.cfl_imp, opt.cfl_exp)
-            dW = smooth(L[0], W, R0, a0, D0, rf0, levels[0]["color"], levels[0]["ncolor"], opt.n_sweeps, g)
+            D0 = diag(S0, relax(a0), opt.cfl_imp, opt.cfl_exp)
+            dW = smooth(L[0], W, R0, relax(a0), D0, rf0, levels[0]["color"], levels[0]["ncolor"], opt.n_sweeps, g)
             W = W + dW
         if nl == 1:
             continue
@@ -107,8 +114,8 @@ def vcycle(levels, W0, Winf, opt: Options, n_cycles=1, user_alpha=None, trace=No
             W0c, Rs, ac = restrict(par, L[l].n, L[l - 1].vol, L[l].vol, Wl[l - 1], Rt_prev, al[l - 1])
             Rc, _, Sc, rfc = residual(L[l], W0c, Winf, g, om)
             F = Rs - Rc
-            Dl = diag(Sc, ac, opt.cfl_imp, opt.cfl_exp)
-            dW = smooth(L[l], W0c, Rs, ac, Dl, rfc, levels[l]["color"], levels[l]["ncolor"], opt.n_sweeps, g)
+            Dl = diag(Sc, relax(ac), opt.cfl_imp, opt.cfl_exp)
+            dW = smooth(L[l], W0c, Rs, relax(ac), Dl, rfc, levels[l]["color"], levels[l]["ncolor"], opt.n_sweeps, g)
             Wc = W0c + dW
             if trace is not None:
                 trace.append({"level": l, "W0": W0c, "Rs": Rs, "alpha": ac, "dW": dW, "F": F})

@@ -167,7 +167,8 @@ void enqueue_gather(Launcher &Lc, Domain &dm, int di, int l, int flags, double *
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
-    GArgs a{flags, ctx->opt.cfl_imp, ctx->opt.cfl_exp, Wexp, L.partial};
+    if ((flags & G_PREPARE) && ctx->opt.df_mode == 3) flags |= G_BETA;   // fixed-beta relaxation
+    GArgs a{flags, ctx->opt.cfl_imp, ctx->opt.cfl_exp, Wexp, L.partial, ctx->opt.beta};
     Lc.pre(GMG_K_GATHER);
     klaunch(Lc.ctx, k_gather<D>, dim3(nblk(L.n)), dim3(256), Lc.s, L, a);
     Lc.post(GMG_K_GATHER, dm.lbytes[l].gather);
@@ -464,7 +465,7 @@ void enqueue_vcycle(Launcher &Lc)
 {
     gmg_ctx *ctx = Lc.ctx;
     const int nl = (int)ctx->lv.size();
-    const bool df0 = ctx->opt.df_mode == 0;
+    const bool df0 = ctx->opt.df_mode == 0 || ctx->opt.df_mode == 3;   // DF helper alpha (prolongation)
     auto &doms = ctx->dom;
     // 1-2. fine residual at the cycle start (history entry) + fine pre-smoothing
     enqueue_exchange<D>(Lc, 0, EX_W, -1);
@@ -720,6 +721,7 @@ void gmg_default_options(gmg_options *o)
     o->device = 0;
     o->stream = nullptr;
     o->local_domains = 1;
+    o->beta = 0.5;
 }
 
 gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
@@ -729,7 +731,8 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if ((opt->dim != 2 && opt->dim != 3) || !(opt->gamma > 1.0) || !(opt->cfl_imp > 0) || !(opt->cfl_exp > 0) ||
         opt->n_sweeps < 1 || opt->n_levels < 1 || opt->n_levels > 3 || opt->pre_smooth != 1 || opt->post_smooth != 0 ||
         !(opt->r_factor >= 1.0) || opt->fine_smoother < 0 || opt->fine_smoother > 1 || opt->df_mode < 0 ||
-        opt->df_mode > 2 || opt->nranks < 1 || opt->rank < 0 || opt->rank >= opt->nranks || opt->local_domains < 1 ||
+        opt->df_mode > 3 || (opt->df_mode == 3 && !(opt->beta >= 0.0 && opt->beta <= 1.0)) || opt->nranks < 1 ||
+        opt->rank < 0 || opt->rank >= opt->nranks || opt->local_domains < 1 ||
         opt->local_domains > 64 || (opt->nranks > 1 && (opt->local_domains != 1 || !opt->nccl_id)))
         return GMG_EINVAL;
     gmg_ctx *ctx = new (std::nothrow) gmg_ctx();

@@ -43,6 +43,7 @@ enum : int {
     G_SIGMA = 256,    // store Sigma
     G_ZERO_DW = 512,  // record dW = 0 (start of a smoothing step, O7 step 1)
     G_COPY_W = 1024,  // record W_lin = W (fine-level smoothing)
+    G_BETA = 2048,    // prepare with the fixed relaxation factor beta instead of alpha (df_mode 3)
 };
 
 struct GArgs {
@@ -50,6 +51,7 @@ struct GArgs {
     double cfl_imp, cfl_exp;
     double *Wexp;
     double *partial;
+    double beta;
 };
 
 // Programmatic dependent launch (sm_90+): every V-cycle kernel may be
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         if (a.flags & G_SIGMA) L.sigma[i] = sig;
         double *rc = L.rec + (size_t)i * RC::STRIDE;
         if (a.flags & G_PREPARE) {
-            const double ai = (a.flags & G_ALPHA) ? al : L.alpha[i];
+            const double ai = (a.flags & G_BETA) ? a.beta : ((a.flags & G_ALPHA) ? al : L.alpha[i]);
             // D = alpha (V/Dt_imp + Sigma/2) + (1 - alpha) V/Dt_exp (O6, A2, A3)
             const double Dg = ai * (sig / a.cfl_imp + 0.5 * sig) + (1.0 - ai) * (sig / a.cfl_exp);
             rc[RC::INVD] = 1.0 / Dg;

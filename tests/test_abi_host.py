@@ -38,8 +38,8 @@ def test_default_options(G):
 
 
 def test_invalid_options_rejected(G):
-    for kw in [dict(dim=4), dict(n_sweeps=0), dict(pre_smooth=2), dict(post_smooth=1), dict(df_mode=3),
-               dict(r_factor=0.5), dict(n_levels=4)]:
+    for kw in [dict(dim=4), dict(n_sweeps=0), dict(pre_smooth=2), dict(post_smooth=1), dict(df_mode=4),
+               dict(df_mode=3, beta=1.5), dict(r_factor=0.5), dict(n_levels=4), dict(nranks=2)]:
         with pytest.raises(G.GmgError) as e:
             G.gmg_create(G.gmg_default_options(**kw))
         assert e.value.status == G.GMG_EINVAL

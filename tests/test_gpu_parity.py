@@ -152,12 +152,19 @@ def test_vcycle_parity_fine_mclusgs(G, orc):
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
 
 
-@pytest.mark.parametrize("df_mode", [1, 2])
+@pytest.mark.parametrize("df_mode", [1, 2, 3])
 def test_vcycle_parity_df_modes(G, orc, df_mode):
     m, Winf, W = _case("config1")
     ua = np.random.default_rng(3).uniform(0, 1, m.n_cells) if df_mode == 1 else None
-    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, df_mode=df_mode, _alpha=ua)
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, df_mode=df_mode, _alpha=ua, beta=0.7)
     assert rel(Wg, Wo) <= TOL
+
+
+def test_vcycle_parity_fixed_beta_3d(G, orc):
+    m, Winf, W = _case("sphere_small")
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, df_mode=3, beta=0.3)
+    assert rel(Wg, Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
 
 
 def test_vcycle_two_levels(G, orc):

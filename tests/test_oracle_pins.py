@@ -699,6 +699,41 @@ def test_vcycle_alpha_zero_fine_unchanged_by_coarse(orc):
     assert np.array_equal(W1, orc.explicit_update(W, S, R, 0.5))
 
 
+def test_fixed_beta_zero_is_explicit_coarse_smoothing(orc):
+    """Fixed-relaxation variant (reading B3) at beta = 0: the
+    relaxation drops the implicit part entirely, so every coarse smoothing
+    step is the explicit update dW = -(CFL_exp / Sigma) Res* (P:519)."""
+    m = configs.tri_square(8, 8, seed=3)
+    H = orc.build_hierarchy(m, 3, 0.5)
+    W = state.perturbed(m, 1.0, [0.5, 0.1], 0.7, eps=0.1, seed=8)
+    Winf = state.winf(1.0, [0.5, 0.1], 0.7)
+    trace = []
+    orc.vcycle(H, W, Winf, orc.Options(df_mode=3, beta=0.0), 1, trace=trace)
+    assert len(trace) == 2
+    for t in trace:
+        lv = H[t["level"]]["level"]
+        _, _, S, _ = orc.residual(lv, t["W0"], Winf)
+        assert np.allclose(t["dW"], -(0.5 / S) * t["Rs"], rtol=1e-13, atol=1e-16)
+
+
+def test_fixed_beta_one_matches_alpha_one_smoothing(orc):
+    """beta = 1 relaxation equals the fully implicit smoother (alpha == 1,
+    P:521) on the coarse levels; the DF-limited prolongation is unchanged."""
+    m = configs.tri_square(8, 8, seed=3)
+    H = orc.build_hierarchy(m, 3, 0.5)
+    W = state.perturbed(m, 1.0, [0.5, 0.1], 0.7, eps=0.1, seed=8)
+    Winf = state.winf(1.0, [0.5, 0.1], 0.7)
+    ta, tb = [], []
+    orc.vcycle(H, W, Winf, orc.Options(df_mode=3, beta=1.0), 1, trace=ta)
+    for t in ta:
+        lv = H[t["level"]]["level"]
+        R, _, S, rf = orc.residual(lv, t["W0"], Winf)
+        one = np.ones(lv.n)
+        dW = orc.smooth(lv, t["W0"], t["Rs"], one, orc.diag(S, one, 10.0, 0.5), rf, H[t["level"]]["color"],
+                        H[t["level"]]["ncolor"], 6)
+        assert np.array_equal(dW, t["dW"])
+
+
 def test_vcycle_reduces_residual_config1(orc):
     m = configs.config(1)
     H = orc.build_hierarchy(m, 3, 0.5)
