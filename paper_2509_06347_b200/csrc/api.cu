@@ -368,6 +368,18 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
                 rhs, Wout};
     if (a.cend <= a.cbeg) return;
     Lc.pre(GMG_K_SWEEP);
+    if (ctx->pipe) {
+        PipeLayout pl{dm.lbytes[l].max_pipe};
+        const size_t smem = (size_t)kPW * pl.warp() * sizeof(double);
+        const int nb = (a.cend - a.cbeg + kPB - 1) / kPB;
+        int per_sm = 0, nsm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_pipe<D>, kPW * 32, smem);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
+        const int grid = std::max(1, std::min((nb + kPW - 1) / kPW, nsm * std::max(per_sm, 1)));
+        k_sweep_pipe<D><<<grid, kPW * 32, smem, Lc.s>>>(a, pl);
+        Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
+        return;
+    }
     if (ctx->spsweep) {
         const int64_t g0 = H.sp_off[c], ng = H.sp_off[c + 1] - g0 - 1;
         klaunch(ctx, k_sweep_sp<D>, dim3((unsigned)ng), dim3(kSpT), Lc.s, a, L.spcell + g0);
@@ -686,6 +698,15 @@ void compute_bytes(gmg_ctx *ctx)
                     mws = std::max(mws, s);
                 }
             B.max_ws = mws;
+            int mp = 1;
+            for (int c = 0; c < ncolor; ++c)
+                for (int64_t i0 = H.blk[c]; i0 < H.blk[c + 1]; i0 += kPB) {
+                    const int64_t i1 = std::min<int64_t>(i0 + kPB, H.blk[c + 1]);
+                    int s = 0;
+                    for (int64_t i = i0; i < i1; ++i) s += H.deg_int[i];
+                    mp = std::max(mp, s);
+                }
+            B.max_pipe = std::min(mp, 128);   // batch slots live in 4 registers per lane
         }
     }
 }
@@ -746,6 +767,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_WSWEEP")) ctx->wsweep = std::atoi(e);   // warp-staged sweep
     if (const char *e = std::getenv("GMG_SPSWEEP")) ctx->spsweep = std::atoi(e); // slot-parallel sweep
     if (const char *e = std::getenv("GMG_TAIL")) ctx->tail_cells = std::atoi(e);  // tiny-color fusion threshold
+    if (const char *e = std::getenv("GMG_PIPE")) ctx->pipe = std::atoi(e);        // pipelined warp sweep
     *out = ctx;
     return GMG_OK;
 }
@@ -997,6 +1019,12 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         CK(cudaFuncSetAttribute(k_sweep_ws<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(2 * per_warp, 227 * 1024)));
         CK(cudaFuncSetAttribute(k_sweep_ws<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(4 * per_warp, 227 * 1024)));
         if (ctx->wsweep && ctx->wsweep * per_warp > 227 * 1024) ctx->wsweep = 1;
+        int mp = 1;
+        for (Domain &dm : ctx->dom)
+            for (auto &B : dm.lbytes) mp = std::max(mp, B.max_pipe);
+        const int pipe_bytes = std::min(kPW * PipeLayout{mp}.warp() * (int)sizeof(double), 227 * 1024);
+        CK(cudaFuncSetAttribute(k_sweep_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe_bytes));
+        CK(cudaFuncSetAttribute(k_sweep_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe_bytes));
     }
     if (ctx->opt.nranks > 1 && !ctx->nccl_comm) {
         if (!nccl().load(ctx->err)) return GMG_ENCCL;

@@ -115,6 +115,7 @@ struct Profile {
 struct LevelBytes {
     double face_flux = 0, face_prep = 0, gather = 0, restrict_ = 0, prolong = 0, update = 0;
     int max_ws = 1;                // warp-staged sweep: max slots of any 32-cell group
+    int max_pipe = 1;              // pipelined sweep: max slots of any 8-cell batch
     std::vector<double> sweep;     // per color
     std::vector<double> sweep_out; // per color, extra bytes when the launch also writes W = W0 + dW
 };
@@ -162,6 +163,7 @@ struct gmg_ctx {
     int wsweep = 0;                   // warp-staged sweep: warps per block (0 = register-gather sweep)
     int spsweep = 0;                  // slot-parallel sweep (thread per slot + block segmented reduction)
     int tail_cells = 0;               // fuse runs of consecutive color phases with <= this many cells (0 = off; neutral)
+    int pipe = 0;                     // pipelined persistent warp sweep (2-stage cp.async ring)
 };
 
 namespace gmg {

@@ -763,6 +763,150 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep_ws(SweepArgs a, int max_sl
     sweep_finish<D>(a, i, acc);
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined persistent warp sweep: each warp walks 8-cell batches of the color
+// (b = warp id, + total warps, ...) with a 2-stage smem ring: while it computes
+// batch b from smem, the cp.async's of batch b+1 (neighbour records, slot
+// records, the cells' rhs and own 1/D-alpha chunk) are in flight, and the
+// slot indices of batch b+2 are being loaded into registers.  Compute is
+// thread-per-slot, then one lane per cell sums its contiguous slot partials.
+// ---------------------------------------------------------------------------
+constexpr int kPB = 8;            // cells per batch
+constexpr int kPW = 4;            // warps per block
+
+struct PipeLayout {               // per-warp smem (doubles)
+    int maxS;                     // max slots of a batch on this level
+    __device__ __host__ int stage() const { return maxS * (kRecS + kSlotRec) + kPB * 5 + kPB * 4; }
+    __device__ __host__ int warp() const { return 2 * stage() + ((maxS * 5 + 1) & ~1) + ((maxS + 1) / 2 + 1) / 2 * 2; }
+};
+
+template <int D>
+__device__ __forceinline__ void pipe_issue(const SweepArgs &a, int c0, int c1, int s0, int ns, const int *jr,
+                                           double *st, const PipeLayout &pl, int lane, int *jS)
+{
+    double *recS = st, *slotS = st + (size_t)pl.maxS * kRecS, *rhsS = slotS + (size_t)pl.maxS * kSlotRec;
+    double *ownS = rhsS + kPB * 5;
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    for (int t = lane; t < ns * 2; t += 32) cp_async16(slotS + 2 * t, a.sRe + (size_t)s0 * kSlotRec + 2 * t);
+    // neighbour records: indices via smem, then consecutive lanes copy consecutive
+    // 16-B pieces of the same record (5-6 records per warp instruction)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int s = lane + 32 * k;
+        if (s < ns) jS[s] = jr[k];
+    }
+    __syncwarp();
+    for (int t = lane; t < ns * 6; t += 32) {
+        const int s = t / 6, p = t - 6 * s;
+        cp_async16(recS + (size_t)s * kRecS + 2 * p, a.rec + (size_t)jS[s] * RC::STRIDE + 2 * p);
+    }
+    __syncwarp();
+    // rhs (nv doubles per cell, 8-byte aligned only -> 8-byte copies) and the own 1/D, alpha/2 chunk
+    const int nc = c1 - c0;
+    for (int t = lane; t < nc * NV; t += 32) {
+        const unsigned s = (unsigned)__cvta_generic_to_shared(rhsS + t);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(a.rhs + (size_t)c0 * NV + t) : "memory");
+    }
+    for (int t = lane; t < nc * 2; t += 32)
+        cp_async16(ownS + 2 * t, a.rec + (size_t)(c0 + t / 2) * RC::STRIDE + 8 + 2 * (t & 1));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kPW * 32) k_sweep_pipe(SweepArgs a, PipeLayout pl)
+{
+    pdl_enter();
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    extern __shared__ __align__(16) double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *wbase = sm + (size_t)warp * pl.warp();
+    double *part = wbase + 2 * (size_t)pl.stage();
+    int *jS = reinterpret_cast<int *>(part + ((pl.maxS * 5 + 1) & ~1));
+    const int ncell = a.cend - a.cbeg;
+    const int nb = (ncell + kPB - 1) / kPB;
+    const int W = gridDim.x * kPW;
+    int b = blockIdx.x * kPW + warp;
+    if (b >= nb) return;
+    auto range = [&](int bb, int &c0, int &c1, int &s0, int &ns) {
+        c0 = a.cbeg + bb * kPB;
+        c1 = min(c0 + kPB, a.cend);
+        s0 = __ldg(a.ecell + c0);
+        ns = __ldg(a.ecell + c1 - 1) + __ldg(a.deg + c1 - 1) - s0;
+    };
+    auto load_idx = [&](int s0, int ns, int *jr) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int s = lane + 32 * k;
+            jr[k] = s < ns ? __ldg(a.sJe + s0 + s) : 0;
+        }
+    };
+    int c0, c1, s0, ns, jr[4];
+    range(b, c0, c1, s0, ns);
+    load_idx(s0, ns, jr);
+    pipe_issue<D>(a, c0, c1, s0, ns, jr, wbase, pl, lane, jS);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    int stage = 0;
+    while (true) {
+        const int bn = b + W;
+        int d0 = 0, d1 = 0, t0 = 0, tn = 0, jn[4] = {0, 0, 0, 0};
+        if (bn < nb) { range(bn, d0, d1, t0, tn); load_idx(t0, tn, jn); }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        double *st = wbase + (size_t)stage * pl.stage();
+        if (bn < nb) {
+            pipe_issue<D>(a, d0, d1, t0, tn, jn, wbase + (size_t)(stage ^ 1) * pl.stage(), pl, lane, jS);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        // compute batch b from stage: thread per slot
+        const double *recS = st, *slotS = st + (size_t)pl.maxS * kRecS, *rhsS = slotS + (size_t)pl.maxS * kSlotRec;
+        const double *ownS = rhsS + kPB * 5;
+        for (int s = lane; s < ns; s += 32) {
+            double acc[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+            const double *r = recS + (size_t)s * kRecS;
+            const double *sr = slotS + (size_t)s * kSlotRec;
+            double w[NV], dw[NV], A[D];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) { w[q] = r[RC::W + q]; dw[q] = r[RC::DW + q]; }
+#pragma unroll
+            for (int k = 0; k < D; ++k) A[k] = sr[k];
+            flux_diff<D>(w, dw, A, a.gm1, sr[D], acc);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) part[s * 5 + q] = acc[q];
+        }
+        __syncwarp();
+        if (lane < c1 - c0) {
+            const int i = c0 + lane;
+            const int e0 = __ldg(a.ecell + i) - s0, e1 = e0 + __ldg(a.deg + i);
+            double acc[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+            for (int s = e0; s < e1; ++s) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) acc[q] += part[s * 5 + q];
+            }
+            const double *own = ownS + lane * 4;     // 3D: dW3, dW4, 1/D, a/2   2D: 1/D, a/2, -, -
+            const double invD = own[D == 3 ? 2 : 0], ha = own[D == 3 ? 3 : 1];
+            double d[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) d[q] = -(rhsS[lane * NV + q] + ha * acc[q]) * invD;
+            double *ri = a.rec + (size_t)i * RC::STRIDE;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) ri[RC::DW + q] = d[q];
+            if (a.Wout) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) a.Wout[(size_t)i * NV + q] = ri[RC::W + q] + d[q];
+            }
+        }
+        __syncwarp();
+        if (bn >= nb) break;
+        b = bn; c0 = d0; c1 = d1; s0 = t0; ns = tn;
+        stage ^= 1;
+    }
+}
+
 // restriction to a coarse level (a8, A15) into the coarse record's
 // W_lin, plus dW = 0 for its sweeps
 template <int D>
