@@ -364,7 +364,7 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
     const DomLevel &H = dm.lv[l];
-    SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sJe, L.sRe,
+    SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe,
                 rhs, Wout};
     if (a.cend <= a.cbeg) return;
     Lc.pre(GMG_K_SWEEP);
@@ -443,7 +443,7 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
                     t.cend[p - k] = (int)H.blk[seq[p].c + 1];
                     t.wout[p - k] = seq[p].last ? 1 : 0;
                 }
-                t.a = SweepArgs{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sJe, L.sRe, rhs(L), wout(L)};
+                t.a = SweepArgs{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs(L), wout(L)};
                 double bytes = 0;
                 for (size_t p = k; p < r; ++p)
                     bytes += dm.lbytes[l].sweep[seq[p].c] + (seq[p].last ? dm.lbytes[l].sweep_out[seq[p].c] : 0.0);
@@ -632,6 +632,8 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.gface = b.take<int>(H.ng_entries);
             L.ecell = b.take<int>(n); L.estride = b.take<int>(n);
             L.spcell = b.take<int>(H.sp_cell.size());
+            L.sinfo = b.take<int2>(n);
+            L.ginfo = b.take<int4>(n);
             L.sJe = b.take<int>(H.sJe.size());
             L.sRe = b.take<double>(H.sRe.size());
             L.perm = b.take<int>(nloc);
@@ -970,6 +972,19 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
             CK(up_raw(L.ecell, H.ell_cell.data(), H.ell_cell.size() * sizeof(int)));
             CK(up_raw(L.spcell, H.sp_cell.data(), H.sp_cell.size() * sizeof(int)));
+            {
+                std::vector<int> si(2 * H.n_own);
+                for (int64_t i = 0; i < H.n_own; ++i) { si[2 * i] = H.ell_cell[i]; si[2 * i + 1] = H.deg_int[i]; }
+                CK(up_i((const int *)L.sinfo, std::move(si)));
+                std::vector<int> gi(4 * H.n_own);
+                for (int64_t i = 0; i < H.n_own; ++i) {
+                    gi[4 * i] = H.gbase[i];
+                    gi[4 * i + 1] = (int)H.deg_all[i] | ((int)H.deg_int[i] << 16);
+                    gi[4 * i + 2] = H.ell_cell[i];
+                    gi[4 * i + 3] = H.ell_stride[i];
+                }
+                CK(up_i((const int *)L.ginfo, std::move(gi)));
+            }
             CK(up_raw(L.estride, H.ell_stride.data(), H.ell_stride.size() * sizeof(int)));
             CK(up_raw(L.sJe, H.sJe.data(), H.sJe.size() * sizeof(int)));
             CK(up_raw(L.sRe, H.sRe.data(), H.sRe.size() * sizeof(double)));

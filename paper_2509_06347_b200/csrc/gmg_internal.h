@@ -93,6 +93,8 @@ struct DevLevel {
     const int *gface;
     const int *ecell, *estride;  // [n] ELL entry of slot 0, stride between slots (cells of the color)
     const int *spcell;           // slot-parallel sweep group boundaries
+    const int2 *sinfo;           // [n] (first sweep slot, interior slots) packed for one 8-byte load
+    const int4 *ginfo;           // [n] (gbase, deg_all | deg_int << 16, ecell, estride) for the gather
     const int *sJe;              // [ne] neighbour, -1 = padding
     double *sRe;                 // [ne][4] A outward + S r
     const int *perm;             // [n_loc] local -> natural

@@ -254,8 +254,10 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 #pragma unroll
     for (int q = 0; q < NV; ++q) R[q] = 0.0;
     if (i < L.n) {
-        const int gb = L.gbase[i], nt = L.deg_all[i], ni = L.deg_int[i];
-        const int e0 = (a.flags & G_PREPARE) ? L.ecell[i] : 0, es = (a.flags & G_PREPARE) ? L.estride[i] : 0;
+        // (gather base, all slots | interior slots << 16, sweep slot 0, sweep stride): one 16-byte load
+        const int4 gi = __ldg(L.ginfo + i);
+        const int gb = gi.x, nt = gi.y & 0xffff, ni = gi.y >> 16;
+        const int e0 = gi.z, es = gi.w;
         double sig = 0.0, al = 1.0;
         for (int s = 0; s < nt; ++s) {
             const int sf = __ldg(L.gface + gb + kChunk * s);
@@ -462,6 +464,7 @@ struct SweepArgs {
     double *rec;               // [n_loc][Rec::STRIDE]
     const int *ecell;          // [n] first slot entry of each cell
     const uint8_t *deg;        // [n] interior slots of each cell
+    const int2 *sinfo;         // [n] (first slot entry, interior slots) packed
     const int *sJe;            // [ns] neighbour
     const double *sRe;         // [ns][4] (A outward | S r)
     const double *rhs;         // [n][nv]
@@ -561,7 +564,10 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
         // two index loads are independent.  (Measured against ELL and
         // chunked-ELL layouts: CSR wins on the coarse levels, where the degree
         // spread is wide -- DESIGN.md §6.)
-        const int e0 = __ldg(a.ecell + i), e1 = e0 + __ldg(a.deg + i);
+        // (first slot, degree) in ONE 8-byte load: separate loads were
+        // serialised by the compiler (degree test before the offset load)
+        const int2 sd = __ldg(a.sinfo + i);
+        const int e0 = sd.x, e1 = sd.x + sd.y;
         for (int e = e0 + sub; e < e1; e += LPC) {
             const int j = __ldg(a.sJe + e);
             double sr[4];
