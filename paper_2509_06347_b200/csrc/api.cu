@@ -144,19 +144,22 @@ void klaunch(gmg_ctx *ctx, void (*k)(KP...), dim3 g, dim3 b, cudaStream_t s, A..
 constexpr int kRecStride = 12;   // Rec<2>::STRIDE == Rec<3>::STRIDE
 
 template <int D>
-void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, bool from_rec)
+void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, bool from_rec, bool df = false)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
     constexpr int RS = Rec<D>::STRIDE, NV = D + 2;
     Lc.pre(GMG_K_FACE);
     const dim3 g(nblk(L.nf)), b(256);
-    if (flux) {
-        if (from_rec) klaunch(Lc.ctx, k_face<D, true, RS>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
-        else klaunch(Lc.ctx, k_face<D, true, NV>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+    if (flux && df) {
+        if (from_rec) klaunch(Lc.ctx, k_face<D, true, RS, true>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+        else klaunch(Lc.ctx, k_face<D, true, NV, true>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+    } else if (flux) {
+        if (from_rec) klaunch(Lc.ctx, k_face<D, true, RS, false>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+        else klaunch(Lc.ctx, k_face<D, true, NV, false>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
     } else {
-        if (from_rec) klaunch(Lc.ctx, k_face<D, false, RS>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
-        else klaunch(Lc.ctx, k_face<D, false, NV>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+        if (from_rec) klaunch(Lc.ctx, k_face<D, false, RS, false>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+        else klaunch(Lc.ctx, k_face<D, false, NV, false>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
     }
     Lc.post(GMG_K_FACE, flux ? dm.lbytes[l].face_flux : dm.lbytes[l].face_prep);
 }
@@ -481,7 +484,7 @@ void enqueue_vcycle(Launcher &Lc)
     auto &doms = ctx->dom;
     // 1-2. fine residual at the cycle start (history entry) + fine pre-smoothing
     enqueue_exchange<D>(Lc, 0, EX_W, -1);
-    for (Domain &dm : doms) enqueue_face<D>(Lc, dm, 0, dm.dv[0].W, true, false);
+    for (Domain &dm : doms) enqueue_face<D>(Lc, dm, 0, dm.dv[0].W, true, false, ctx->opt.fine_smoother == 1 && df0);
     if (ctx->opt.fine_smoother == 0) {
         for (size_t d = 0; d < doms.size(); ++d)
             enqueue_gather<D>(Lc, doms[d], (int)d, 0, G_FLUX | G_NORM | G_EXPLICIT, doms[d].dv[0].W);   // Eq.(smo), A9
@@ -501,7 +504,7 @@ void enqueue_vcycle(Launcher &Lc)
     if (nl == 1) return;
     // 3. residual at the smoothed state (A10) -> restricted
     for (size_t d = 0; d < doms.size(); ++d) {
-        enqueue_face<D>(Lc, doms[d], 0, doms[d].dv[0].W, true, false);
+        enqueue_face<D>(Lc, doms[d], 0, doms[d].dv[0].W, true, false, df0);
         enqueue_gather<D>(Lc, doms[d], (int)d, 0, G_FLUX | G_WRITE_RT | (df0 ? G_ALPHA : 0), nullptr);
     }
     // 4. coarse levels
@@ -1117,10 +1120,10 @@ gmg_status gmg_residual(gmg_ctx *ctx, int level, double *R_out, double *alpha_ou
         double *save_alpha = L.alpha;
         L.alpha = L.tmp;    // scratch: the level's own alpha stays intact
         if (ctx->opt.dim == 2) {
-            enqueue_face<2>(Lc, dm, level, L.W, true, false);
+            enqueue_face<2>(Lc, dm, level, L.W, true, false, true);
             enqueue_gather<2>(Lc, dm, (int)d, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
         } else {
-            enqueue_face<3>(Lc, dm, level, L.W, true, false);
+            enqueue_face<3>(Lc, dm, level, L.W, true, false, true);
             enqueue_gather<3>(Lc, dm, (int)d, level, G_FLUX | G_WRITE_RT | G_ALPHA | G_SIGMA, nullptr);
         }
         L.alpha = save_alpha;

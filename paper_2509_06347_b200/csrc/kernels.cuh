@@ -174,7 +174,7 @@ __device__ __forceinline__ void kfvs_side(const Side<D> &s, const double *n, dou
 constexpr int kFaceRec = 8;
 template <int D> struct FR { static constexpr int SR = D + 2, AM = D + 3; };
 
-template <int D, bool FLUX, int STRIDE>
+template <int D, bool FLUX, int STRIDE, bool DF>
 __global__ void __launch_bounds__(256, 3) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
 {
     pdl_enter();
@@ -215,6 +215,9 @@ __global__ void __launch_bounds__(256, 3) k_face(DevLevel L, const double *__res
         kfvs_side<D>(sr, n, -1.0, ph, out);
 #pragma unroll
         for (int q = 0; q < NV; ++q) out[q] *= S;
+    }
+    if (FLUX && DF) {   // only the fine residual whose alpha is consumed evaluates the DF helper
+        const Side<D> sl = side_of<D>(wl, n, ph.gm1), sr = side_of<D>(wr, n, ph.gm1);
         // DF helper (O5): D = |dp|/p_l + |dp|/p_r + (dMa_n)^2 + |dMa_t|^2, alpha = 1/(1+D^2)
         const double ial = rsqrt(ph.gamma * sl.p * sl.ir), iar = rsqrt(ph.gamma * sr.p * sr.ir);
         const double dMn = sl.U * ial - sr.U * iar;
