@@ -943,7 +943,19 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
     double *rc = C.rec + (size_t)c * RC::STRIDE;
     const size_t o = (size_t)c * NV;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) { rc[RC::W + q] = w[q] / vc; C.Rs[o + q] = r[q]; rc[RC::DW + q] = 0.0; }
+    for (int q = 0; q < NV; ++q) { w[q] = w[q] / vc; C.Rs[o + q] = r[q]; }
+    // whole 32-byte chunks (no partial-sector writes): W_lin, dW = 0; the 3D
+    // record's 1/D and alpha/2 slots are zeroed too -- the next prepare sets them
+    if constexpr (D == 3) {
+        const double c0[4] = {w[0], w[1], w[2], w[3]}, c1[4] = {w[4], 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
+        st4(rc, c0);
+        st4(rc + 4, c1);
+        st4(rc + 8, c2);
+    } else {
+        const double c1[4] = {0.0, 0.0, 0.0, 0.0};
+        st4(rc, w);
+        st4(rc + 4, c1);
+    }
     C.alpha[c] = a;
 }
 
