@@ -361,14 +361,31 @@ void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win,
 }
 
 // one color block of one domain (Eq.(gpu-forward-relaxation) / (gpu-backward-relaxation))
+// part: 0 = whole block, 1 = its boundary cells (ghost neighbours), 2 = its interior cells
 template <int D>
-void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout)
+void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout, int part = 0)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
     const DomLevel &H = dm.lv[l];
-    SweepArgs a{(int)H.blk[c], (int)H.blk[c + 1], ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe,
-                rhs, Wout};
+    int b0 = (int)H.blk[c], b1 = (int)H.blk[c + 1];
+    if (part) {
+        const int mid = b0 + (int)H.nbnd[c];
+        const double frac = b1 > b0 ? (double)(part == 1 ? mid - b0 : b1 - mid) / (b1 - b0) : 0.0;
+        if (part == 1) b1 = mid;
+        else b0 = mid;
+        SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs, Wout};
+        if (b1 <= b0) return;
+        Lc.pre(GMG_K_SWEEP);
+        switch (ctx->lpc) {
+            case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, nullptr, 0, ctx->pdl); break;
+            case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, nullptr, 0, ctx->pdl); break;
+            default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, nullptr, 0, ctx->pdl); break;
+        }
+        Lc.post(GMG_K_SWEEP, frac * (dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0)));
+        return;
+    }
+    SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs, Wout};
     if (a.cend <= a.cbeg) return;
     Lc.pre(GMG_K_SWEEP);
     if (ctx->pipe) {
@@ -427,6 +444,7 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
             for (int cc = 0; cc < nc; ++cc)
                 seq.push_back({half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1});
     const bool fuse = ctx->tail_cells > 0 && ctx->nparts == 1 && ctx->dom.size() == 1;
+    const bool overlap = (ctx->overlap < 0 ? ctx->opt.nranks > 1 : ctx->overlap != 0) && ctx->nparts > 1 && ctx->side && !ctx->pipe && !ctx->spsweep && !ctx->wsweep;
     for (size_t k = 0; k < seq.size();) {
         if (fuse) {
             // a run of >= 2 consecutive tiny color phases -> one single-CTA launch
@@ -457,9 +475,26 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
                 continue;
             }
         }
-        for (Domain &dm : ctx->dom)
-            enqueue_sweep_color<D>(Lc, dm, l, seq[k].c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr);
-        enqueue_exchange<D>(Lc, l, EX_DW, seq[k].c);
+        const int c = seq[k].c;
+        if (overlap) {
+            // boundary cells of color c first; their increments travel on the
+            // side stream while the interior cells of c (no ghost neighbours)
+            // are swept; the next color waits for the ghosts (fork / join)
+            for (Domain &dm : ctx->dom)
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 1);
+            cudaEventRecord(ctx->ev_fork, Lc.s);
+            cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+            Launcher Ls{ctx, ctx->side};
+            enqueue_exchange<D>(Ls, l, EX_DW, c);
+            cudaEventRecord(ctx->ev_join, ctx->side);
+            for (Domain &dm : ctx->dom)
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 2);
+            cudaStreamWaitEvent(Lc.s, ctx->ev_join, 0);
+        } else {
+            for (Domain &dm : ctx->dom)
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr);
+            enqueue_exchange<D>(Lc, l, EX_DW, c);
+        }
         ++k;
     }
 }
@@ -773,6 +808,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_SPSWEEP")) ctx->spsweep = std::atoi(e); // slot-parallel sweep
     if (const char *e = std::getenv("GMG_TAIL")) ctx->tail_cells = std::atoi(e);  // tiny-color fusion threshold
     if (const char *e = std::getenv("GMG_PIPE")) ctx->pipe = std::atoi(e);        // pipelined warp sweep
+    if (const char *e = std::getenv("GMG_OVERLAP")) ctx->overlap = std::atoi(e);  // boundary-first exchange overlap
     *out = ctx;
     return GMG_OK;
 }
@@ -1004,6 +1040,11 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         }
     }
     CK(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), ctx->stream));
+    if (ctx->nparts > 1 && !ctx->side) {   // side stream + events of the exchange overlap
+        CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     if (const char *e = std::getenv("GMG_L2PERSIST")) {   // experimental: persisting-L2 window over records
@@ -1372,6 +1413,9 @@ void gmg_destroy(gmg_ctx *ctx)
 {
     if (!ctx) return;
     if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy((ncclComm_t)ctx->nccl_comm);
     delete ctx;
 }

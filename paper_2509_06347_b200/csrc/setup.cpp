@@ -403,15 +403,31 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
     auto owned = [&](int64_t c) { return G.part_of(c) == rank; };
     std::vector<int32_t> n2l(N, -1);
     D.blk.assign(G.ncolor + 1, 0);
+    // owned cells with a face neighbour on another rank ("boundary" cells) go
+    // first inside their color block, so their increments can be sent while
+    // the interior cells of the same color are swept (exchange overlap)
+    std::vector<uint8_t> bnd(N, 0);
+    for (int64_t f = 0; f < G.nf; ++f) {
+        const int64_t l = G.left[f], r = G.right[f];
+        if (r < 0) continue;
+        if (owned(l) && !owned(r)) bnd[l] = 1;
+        if (owned(r) && !owned(l)) bnd[r] = 1;
+    }
     for (int64_t p = 0; p < N; ++p) {
         const int64_t nat = G.perm[p];
         if (!owned(nat)) continue;
-        n2l[nat] = (int32_t)D.l2n.size();
         D.l2n.push_back(nat);
         D.blk[G.color[nat]]++;
     }
     D.n_own = (int64_t)D.l2n.size();
     for (int c = 1; c <= G.ncolor; ++c) D.blk[c] += D.blk[c - 1];
+    D.nbnd.assign(G.ncolor, 0);
+    for (int c = 0; c < G.ncolor; ++c) {
+        auto b0 = D.l2n.begin() + D.blk[c], b1 = D.l2n.begin() + D.blk[c + 1];
+        auto mid = std::stable_partition(b0, b1, [&](int64_t nat) { return bnd[nat] != 0; });
+        D.nbnd[c] = (int64_t)(mid - b0);
+    }
+    for (int64_t i = 0; i < D.n_own; ++i) n2l[D.l2n[i]] = (int32_t)i;
     std::vector<int64_t> ghosts;
     for (int64_t f = 0; f < G.nf; ++f) {
         const int64_t l = G.left[f], r = G.right[f];

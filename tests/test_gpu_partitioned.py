@@ -41,9 +41,13 @@ def _case(name):
     return m, state.winf(*fs), state.bow_shock(m, *fs)
 
 
+@pytest.mark.parametrize("overlap", ["0", "1"])
 @pytest.mark.parametrize("name", ["config1", "box", "sphere"])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_partitioned_vcycle_parity(G, orc, name, P):
+def test_partitioned_vcycle_parity(G, orc, name, P, overlap, monkeypatch):
+    # overlap=1 forces the boundary-first sweep with the exchange on a side
+    # stream (the NCCL default) onto the local-domain transport
+    monkeypatch.setenv("GMG_OVERLAP", overlap)
     m, Winf, W = _case(name)
     part = G.gmg_partition_rcb(m.ctr, P)
     s = G.Solver(m, n_levels=3, part=part, local_domains=P)
