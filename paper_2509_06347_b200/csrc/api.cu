@@ -117,6 +117,7 @@ struct Launcher {
             cudaEventRecord(e, s);
             ctx->prof.ev.push_back(e);
             ctx->prof.marks.push_back({cls, (int)ctx->prof.ev.size() - 2});
+            ctx->prof.bytes.push_back(bytes);
         }
     }
 };
@@ -316,6 +317,7 @@ void enqueue_ghost_w(Launcher &Lc, int l)
 // gathered data), attached per launch so that graph capture keeps it
 // sweep grid cap = resident waves x SMs x blocks/SM (set in gmg_set_workspace; 0 = one thread per cell)
 int g_sweep_grid_cap = 0;
+int g_sweep_var = 3;   // k_sweep variant bits (kernels.cuh), GMG_SWEEPV
 
 template <class K>
 void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArgs &a, const void *win, size_t win_bytes,
@@ -353,6 +355,11 @@ void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win,
     int nb = nblk(nthreads);
     if (g_sweep_grid_cap > 0) nb = std::min(nb, g_sweep_grid_cap);
     const dim3 g(nb), b(256);
+    // variants kept for the record; 3 is the default
+    if (g_sweep_var == 0) { launch_with_window(k_sweep<D, LPC, 4, 0>, g, b, s, a, win, win_bytes, pdl); return; }
+    if (g_sweep_var == 1) { launch_with_window(k_sweep<D, LPC, 4, 1>, g, b, s, a, win, win_bytes, pdl); return; }
+    if (g_sweep_var == 2) { launch_with_window(k_sweep<D, LPC, 4, 2>, g, b, s, a, win, win_bytes, pdl); return; }
+    if (g_sweep_var == 7) { launch_with_window(k_sweep<D, LPC, 4, 7>, g, b, s, a, win, win_bytes, pdl); return; }
     switch (minb) {
         case 6: launch_with_window(k_sweep<D, LPC, 6>, g, b, s, a, win, win_bytes, pdl); break;
         case 8: launch_with_window(k_sweep<D, LPC, 8>, g, b, s, a, win, win_bytes, pdl); break;
@@ -419,9 +426,19 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
     }
     const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
     const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * kRecStride * sizeof(double)) : 0;
-    switch (ctx->lpc) {
+    // small color blocks are latency bound (one partial wave, each lane walks
+    // its slots one dependent gather after the other): spread the slots over
+    // more lanes while the whole block still fits in one resident wave
+    int lpc = ctx->lpc;
+    if (ctx->adapt_lpc && g_sweep_grid_cap > 0) {
+        const int64_t wave = (int64_t)g_sweep_grid_cap * 256, cells = a.cend - a.cbeg;
+        while (lpc < 16 && cells * lpc * 2 <= wave) lpc *= 2;
+    }
+    switch (lpc) {
         case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
         case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
+        case 8: launch_sweep<D, 8>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
+        case 16: launch_sweep<D, 16>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
         default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
     }
     Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
@@ -809,6 +826,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_TAIL")) ctx->tail_cells = std::atoi(e);  // tiny-color fusion threshold
     if (const char *e = std::getenv("GMG_PIPE")) ctx->pipe = std::atoi(e);        // pipelined warp sweep
     if (const char *e = std::getenv("GMG_OVERLAP")) ctx->overlap = std::atoi(e);  // boundary-first exchange overlap
+    if (const char *e = std::getenv("GMG_ALPC")) ctx->adapt_lpc = std::atoi(e);   // wider lanes for small colors
     *out = ctx;
     return GMG_OK;
 }
@@ -1059,11 +1077,12 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
     {   // sweep grid: whole resident waves only (grid-stride kernel), GMG_SWEEP_WAVES (0 = uncapped)
         int waves = 1, nsm = 0, per_sm = 0;
         if (const char *e = std::getenv("GMG_SWEEP_WAVES")) waves = std::atoi(e);
+        if (const char *e = std::getenv("GMG_SWEEPV")) g_sweep_var = std::atoi(e);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
         if (ctx->opt.dim == 3)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, 4>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, 4, 3>, 256, 0);
         else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, 4>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, 4, 3>, 256, 0);
         g_sweep_grid_cap = waves > 0 ? waves * nsm * std::max(per_sm, 1) : 0;
     }
     {   // dynamic shared memory of the warp-staged sweep (may exceed the 48 KB default)
@@ -1291,6 +1310,7 @@ gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_
     ctx->prof.on = true;
     ctx->prof.ev.clear();
     ctx->prof.marks.clear();
+    ctx->prof.bytes.clear();
     for (double &b : ctx->kbytes) b = 0;
     ctx->launches = 0;
     CK(cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), ctx->stream));
@@ -1304,12 +1324,18 @@ gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_
     CK(cudaStreamSynchronize(ctx->stream));
     double ms[GMG_K_COUNT] = {0};
     int64_t cnt[GMG_K_COUNT] = {0};
-    for (auto &m : ctx->prof.marks) {
+    FILE *dump = nullptr;   // dev aid: per-launch (class, ms, algorithmic bytes)
+    if (const char *e = std::getenv("GMG_PROF_DUMP")) dump = std::fopen(e, "w");
+    for (size_t q = 0; q < ctx->prof.marks.size(); ++q) {
+        const auto &m = ctx->prof.marks[q];
         float t = 0.f;
         cudaEventElapsedTime(&t, ctx->prof.ev[m.second], ctx->prof.ev[m.second + 1]);
         ms[m.first] += t;
         cnt[m.first] += 1;
+        if (dump) std::fprintf(dump, "%d %.6f %.0f\n", m.first, t, ctx->prof.bytes[q]);
     }
+    if (dump) std::fclose(dump);
+    ctx->prof.bytes.clear();
     for (auto e : ctx->prof.ev) cudaEventDestroy(e);
     ctx->prof.ev.clear();
     ctx->prof.marks.clear();

@@ -112,6 +112,7 @@ struct Profile {
     bool on = false;
     std::vector<cudaEvent_t> ev;
     std::vector<std::pair<int, int>> marks;  // (kernel class, event index of start)
+    std::vector<double> bytes;               // algorithmic bytes of each mark
 };
 
 // algorithmic bytes bookkeeping
@@ -159,7 +160,8 @@ struct gmg_ctx {
     double kbytes[GMG_K_COUNT] = {0}; // algorithmic bytes accumulated by the recorded sequence
     int64_t launches = 0;             // kernels launched by the last recorded sequence
     int64_t exchanges = 0;            // halo exchanges in the last recorded sequence
-    int lpc = 2;                      // sweep lanes per cell (1, 2, 4)
+    int lpc = 2;                      // sweep lanes per cell (1, 2, 4) of the large color blocks
+    int adapt_lpc = 1;                // blocks that fit one wave at 2x lanes get up to 16 lanes per cell
     int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
     int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (no measured gain)

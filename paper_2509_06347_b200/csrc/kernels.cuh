@@ -542,7 +542,56 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, int i, const do
     }
 }
 
-template <int D, int LPC, int MINB>
+// sweep variants (template bits, GMG_SWEEPV; default 3, measured DESIGN.md §6):
+//  1 = dW0..2 written as the whole 32-B chunk (W4 | dW0..2), no partial sector
+//  2 = neighbour index of the next slot loaded one iteration ahead
+//  4 = own record tail + rhs prefetched to L1 before the slot loop
+template <int D>
+__device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, const double *acc)
+{
+    constexpr int NV = D + 2;
+    double *ri = a.rec + (size_t)i * Rec<D>::STRIDE;
+    const size_t o = (size_t)i * NV;
+    double r[NV], c1[4], c2[4];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
+    if constexpr (D == 3) ld4nc(ri + 4, c1);
+    ld4nc(ri + 8, c2);
+    if constexpr (D == 3) {
+        const double invD = c2[2], ha = c2[3];
+        double d[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+        double w1[4] = {c1[0], d[0], d[1], d[2]};
+        st4(ri + 4, w1);
+        c2[0] = d[3];
+        c2[1] = d[4];
+        st4(ri + 8, c2);
+        if (a.Wout) {
+            double c0[4];
+            ld4nc(ri, c0);
+            a.Wout[o + 0] = c0[0] + d[0];
+            a.Wout[o + 1] = c0[1] + d[1];
+            a.Wout[o + 2] = c0[2] + d[2];
+            a.Wout[o + 3] = c0[3] + d[3];
+            a.Wout[o + 4] = c1[0] + d[4];
+        }
+    } else {
+        const double invD = c2[0], ha = c2[1];
+        double d[4];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+        st4(ri + 4, d);
+        if (a.Wout) {
+            double c0[4];
+            ld4nc(ri, c0);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) a.Wout[o + q] = c0[q] + d[q];
+        }
+    }
+}
+
+template <int D, int LPC, int MINB, int VAR = 3>
 __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 {
     pdl_enter();
@@ -570,14 +619,36 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
         // (first slot, degree) in ONE 8-byte load: separate loads were
         // serialised by the compiler (degree test before the offset load)
         const int2 sd = __ldg(a.sinfo + i);
+        if constexpr ((VAR & 4) != 0) {
+            if (sub == 0) {   // own record tail + rhs towards L1 while the gathers run
+                const double *ri = a.rec + (size_t)i * RC::STRIDE;
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(ri + 4));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rhs + (size_t)i * NV));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rhs + (size_t)i * NV + NV - 1));
+            }
+        }
         const int e0 = sd.x, e1 = sd.x + sd.y;
-        for (int e = e0 + sub; e < e1; e += LPC) {
-            const int j = __ldg(a.sJe + e);
-            double sr[4];
-            ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
-            double w[NV], dw[NV];
-            ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
-            flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+        if constexpr ((VAR & 2) != 0) {
+            int e = e0 + sub;
+            int j = e < e1 ? __ldg(a.sJe + e) : 0;
+            for (; e < e1; e += LPC) {
+                const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
+                double sr[4];
+                ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                double w[NV], dw[NV];
+                ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
+                flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                j = jn;
+            }
+        } else {
+            for (int e = e0 + sub; e < e1; e += LPC) {
+                const int j = __ldg(a.sJe + e);
+                double sr[4];
+                ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                double w[NV], dw[NV];
+                ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
+                flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+            }
         }
     }
     if (LPC > 1) {
@@ -587,7 +658,10 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
             for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
         }
     }
-    if (valid && sub == 0) sweep_finish<D>(a, i, acc);
+    if (valid && sub == 0) {
+        if constexpr ((VAR & 1) != 0) sweep_finish_full<D>(a, i, acc);
+        else sweep_finish<D>(a, i, acc);
+    }
     }
 }
 
