@@ -144,25 +144,37 @@ void klaunch(gmg_ctx *ctx, void (*k)(KP...), dim3 g, dim3 b, cudaStream_t s, A..
 
 constexpr int kRecStride = 12;   // Rec<2>::STRIDE == Rec<3>::STRIDE
 
+// prep: the launch also writes the sweep slot records (A outward | S r) of
+// both cells of every interior face (whole 32-byte records)
 template <int D>
-void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, bool from_rec, bool df = false)
+void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, bool from_rec, bool df = false,
+                  bool prep = false)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
     constexpr int RS = Rec<D>::STRIDE, NV = D + 2;
     Lc.pre(GMG_K_FACE);
     const dim3 g(nblk(L.nf)), b(256);
-    if (flux && df) {
-        if (from_rec) klaunch(Lc.ctx, k_face<D, true, RS, true>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
-        else klaunch(Lc.ctx, k_face<D, true, NV, true>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+    const Phys ph = phys(ctx);
+    const BCs bc = bcs(ctx);
+    if (prep) {
+        if (flux && df && !from_rec) klaunch(ctx, k_face<D, true, NV, true, true>, g, b, Lc.s, L, W, ph, bc);
+        else if (flux && !df && from_rec) klaunch(ctx, k_face<D, true, RS, false, true>, g, b, Lc.s, L, W, ph, bc);
+        else if (flux && !df && !from_rec) klaunch(ctx, k_face<D, true, NV, false, true>, g, b, Lc.s, L, W, ph, bc);
+        else if (!flux && from_rec) klaunch(ctx, k_face<D, false, RS, false, true>, g, b, Lc.s, L, W, ph, bc);
+        else if (!flux && !from_rec) klaunch(ctx, k_face<D, false, NV, false, true>, g, b, Lc.s, L, W, ph, bc);
+        else { ctx->err = "enqueue_face: unsupported prep variant"; return; }
+    } else if (flux && df) {
+        if (from_rec) klaunch(ctx, k_face<D, true, RS, true, false>, g, b, Lc.s, L, W, ph, bc);
+        else klaunch(ctx, k_face<D, true, NV, true, false>, g, b, Lc.s, L, W, ph, bc);
     } else if (flux) {
-        if (from_rec) klaunch(Lc.ctx, k_face<D, true, RS, false>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
-        else klaunch(Lc.ctx, k_face<D, true, NV, false>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+        if (from_rec) klaunch(ctx, k_face<D, true, RS, false, false>, g, b, Lc.s, L, W, ph, bc);
+        else klaunch(ctx, k_face<D, true, NV, false, false>, g, b, Lc.s, L, W, ph, bc);
     } else {
-        if (from_rec) klaunch(Lc.ctx, k_face<D, false, RS, false>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
-        else klaunch(Lc.ctx, k_face<D, false, NV, false>, dim3(g), dim3(b), Lc.s, L, W, phys(ctx), bcs(ctx));
+        if (from_rec) klaunch(ctx, k_face<D, false, RS, false, false>, g, b, Lc.s, L, W, ph, bc);
+        else klaunch(ctx, k_face<D, false, NV, false, false>, g, b, Lc.s, L, W, ph, bc);
     }
-    Lc.post(GMG_K_FACE, flux ? dm.lbytes[l].face_flux : dm.lbytes[l].face_prep);
+    Lc.post(GMG_K_FACE, (flux ? dm.lbytes[l].face_flux : dm.lbytes[l].face_prep) + (prep ? dm.lbytes[l].face_slots : 0.0));
 }
 
 // with G_NORM the domain's residual sums of squares land in d_sumsq[di]
@@ -536,7 +548,8 @@ void enqueue_vcycle(Launcher &Lc)
     auto &doms = ctx->dom;
     // 1-2. fine residual at the cycle start (history entry) + fine pre-smoothing
     enqueue_exchange<D>(Lc, 0, EX_W, -1);
-    for (Domain &dm : doms) enqueue_face<D>(Lc, dm, 0, dm.dv[0].W, true, false, ctx->opt.fine_smoother == 1 && df0);
+    for (Domain &dm : doms)
+        enqueue_face<D>(Lc, dm, 0, dm.dv[0].W, true, false, ctx->opt.fine_smoother == 1 && df0, ctx->opt.fine_smoother == 1);
     if (ctx->opt.fine_smoother == 0) {
         for (size_t d = 0; d < doms.size(); ++d)
             enqueue_gather<D>(Lc, doms[d], (int)d, 0, G_FLUX | G_NORM | G_EXPLICIT, doms[d].dv[0].W);   // Eq.(smo), A9
@@ -565,7 +578,7 @@ void enqueue_vcycle(Launcher &Lc)
         for (Domain &dm : doms) enqueue_restrict<D>(Lc, dm, l);                // W0, Res*, alpha, dW = 0
         enqueue_exchange<D>(Lc, l, EX_WLIN, -1);                                // ghosts' W0, dW = 0
         for (size_t d = 0; d < doms.size(); ++d) {
-            enqueue_face<D>(Lc, doms[d], l, doms[d].dv[l].rec, !last, true);   // R(W0) only if F is needed later
+            enqueue_face<D>(Lc, doms[d], l, doms[d].dv[l].rec, !last, true, false, true);   // R(W0) only if F is needed later
             enqueue_gather<D>(Lc, doms[d], (int)d, l, (last ? 0 : (G_FLUX | G_SET_F)) | G_PREPARE, nullptr);
         }
         enqueue_sweeps<D>(Lc, l, ctx->opt.n_sweeps, [](DevLevel &L) { return (const double *)L.Rs; },
@@ -688,6 +701,7 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.ecell = b.take<int>(n); L.estride = b.take<int>(n);
             L.spcell = b.take<int>(H.sp_cell.size());
             L.sinfo = b.take<int2>(n);
+            L.fslot = b.take<int2>(nf);
             L.ginfo = b.take<int4>(n);
             L.sJe = b.take<int>(H.sJe.size());
             L.sRe = b.take<double>(H.sRe.size());
@@ -727,6 +741,10 @@ void compute_bytes(gmg_ctx *ctx)
             const double face_in = (double)nint * 2 * nv * 8 + nb * nv * 8 + (double)H.nf * (d * 8 + 8 + 1);
             B.face_flux = face_in + (double)H.nf * (nv * 8 + 16);
             B.face_prep = face_in + (double)H.nf * 8;
+            // prep launches: fslot read + the (A outward | S r) slot record of each side that has one
+            double nslot = 0;
+            for (int32_t e : H.fslot) nslot += e >= 0;
+            B.face_slots = (double)H.nf * 8 + nslot * kSlotRec * 8;
             // gather: per slot the face id + S F + S r + alpha^M; per cell bases/degrees + outputs
             double slots = 0;
             for (int64_t i = 0; i < H.n_own; ++i) slots += H.deg_all[i];
@@ -1029,6 +1047,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
             CK(up_raw(L.ecell, H.ell_cell.data(), H.ell_cell.size() * sizeof(int)));
             CK(up_raw(L.spcell, H.sp_cell.data(), H.sp_cell.size() * sizeof(int)));
+            CK(up_raw(L.fslot, H.fslot.data(), H.fslot.size() * sizeof(int)));
             {
                 std::vector<int> si(2 * H.n_own);
                 for (int64_t i = 0; i < H.n_own; ++i) { si[2 * i] = H.ell_cell[i]; si[2 * i + 1] = H.deg_int[i]; }
@@ -1225,14 +1244,14 @@ gmg_status gmg_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out)
     auto nowout = [](DevLevel &) { return (double *)nullptr; };
     if (ctx->opt.dim == 2) {
         for (size_t d = 0; d < ctx->dom.size(); ++d) {
-            enqueue_face<2>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false);
+            enqueue_face<2>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false, false, true);
             enqueue_gather<2>(Lc, ctx->dom[d], (int)d, level, gf, nullptr);
         }
         enqueue_ghost_wlin<2>(Lc, level);
         enqueue_sweeps<2>(Lc, level, n_sweeps, rhs, nowout);
     } else {
         for (size_t d = 0; d < ctx->dom.size(); ++d) {
-            enqueue_face<3>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false);
+            enqueue_face<3>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false, false, true);
             enqueue_gather<3>(Lc, ctx->dom[d], (int)d, level, gf, nullptr);
         }
         enqueue_ghost_wlin<3>(Lc, level);

@@ -64,6 +64,7 @@ struct DomLevel {
     std::vector<int32_t> sJe;              // [ne] neighbour
     std::vector<double> sRe;               // [ne][4] (A outward | S r)
     std::vector<int32_t> ell_cell, ell_stride;   // [n_own] entry of slot 0, stride between slots
+    std::vector<int32_t> fslot;            // [nf][2] sweep entry of the face in its left / right cell's slots (-1: none)
     std::vector<int32_t> sp_cell;          // slot-parallel sweep: group cell boundaries, per color
     std::vector<int64_t> sp_off;           // [ncolor+1] first boundary of each color in sp_cell
     // multigrid links (local indices)
@@ -95,6 +96,7 @@ struct DevLevel {
     const int *ecell, *estride;  // [n] ELL entry of slot 0, stride between slots (cells of the color)
     const int *spcell;           // slot-parallel sweep group boundaries
     const int2 *sinfo;           // [n] (first sweep slot, interior slots) packed for one 8-byte load
+    const int2 *fslot;           // [nf] sweep entries of the face (left cell, right cell), -1 = none
     const int4 *ginfo;           // [n] (gbase, deg_all | deg_int << 16, ecell, estride) for the gather
     const int *sJe;              // [ne] neighbour, -1 = padding
     double *sRe;                 // [ne][4] A outward + S r
@@ -117,7 +119,7 @@ struct Profile {
 
 // algorithmic bytes bookkeeping
 struct LevelBytes {
-    double face_flux = 0, face_prep = 0, gather = 0, restrict_ = 0, prolong = 0, update = 0;
+    double face_flux = 0, face_prep = 0, face_slots = 0, gather = 0, restrict_ = 0, prolong = 0, update = 0;
     int max_ws = 1;                // warp-staged sweep: max slots of any 32-cell group
     int max_pipe = 1;              // pipelined sweep: max slots of any 8-cell batch
     std::vector<double> sweep;     // per color

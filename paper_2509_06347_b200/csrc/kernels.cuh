@@ -174,7 +174,10 @@ __device__ __forceinline__ void kfvs_side(const Side<D> &s, const double *n, dou
 constexpr int kFaceRec = 8;
 template <int D> struct FR { static constexpr int SR = D + 2, AM = D + 3; };
 
-template <int D, bool FLUX, int STRIDE, bool DF>
+// PREP: also write the sweep slot records (A outward | S r) of the face's
+// cells -- whole 32-byte records, so no partial-sector update (the gather
+// used to patch S r into each slot)
+template <int D, bool FLUX, int STRIDE, bool DF, bool PREP>
 __global__ void __launch_bounds__(256, 3) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
 {
     pdl_enter();
@@ -235,6 +238,18 @@ __global__ void __launch_bounds__(256, 3) k_face(DevLevel L, const double *__res
         for (int g = 0; g < M; ++g) aM *= af;
         out[FR<D>::AM] = aM;
     }
+    if (PREP) {
+        const int2 es = __ldg(L.fslot + f);
+        const double sr = out[FR<D>::SR];
+        if (es.x >= 0) {
+            const double v[4] = {A[0], A[1], D == 3 ? A[D - 1] : sr, D == 3 ? sr : 0.0};
+            st4(L.sRe + (size_t)es.x * kSlotRec, v);
+        }
+        if (es.y >= 0) {
+            const double v[4] = {-A[0], -A[1], D == 3 ? -A[D - 1] : sr, D == 3 ? sr : 0.0};
+            st4(L.sRe + (size_t)es.y * kSlotRec, v);
+        }
+    }
     double *o = L.Frec + (size_t)f * kFaceRec;
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o), "d"(out[0]), "d"(out[1]), "d"(out[2]), "d"(out[3])
                  : "memory");
@@ -259,8 +274,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     if (i < L.n) {
         // (gather base, all slots | interior slots << 16, sweep slot 0, sweep stride): one 16-byte load
         const int4 gi = __ldg(L.ginfo + i);
-        const int gb = gi.x, nt = gi.y & 0xffff, ni = gi.y >> 16;
-        const int e0 = gi.z, es = gi.w;
+        const int gb = gi.x, nt = gi.y & 0xffff;
         double sig = 0.0, al = 1.0;
         for (int s = 0; s < nt; ++s) {
             const int sf = __ldg(L.gface + gb + kChunk * s);
@@ -279,7 +293,6 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
                 if (D == 3) R[NV - 1] += sg * c1[0];
                 al *= c1[FR<D>::AM - 4];
             }
-            if ((a.flags & G_PREPARE) && s < ni) L.sRe[((size_t)e0 + (size_t)s * es) * kSlotRec + D] = srf;
         }
         if (a.flags & G_ALPHA) L.alpha[i] = al;
         if (a.flags & G_SIGMA) L.sigma[i] = sig;

@@ -530,6 +530,7 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
     D.gbase.assign(D.n_own, 0);
     D.sJ.assign(so, -1);
     D.sRec.assign((size_t)4 * so, 0.0);
+    D.fslot.assign((size_t)2 * D.nf, -1);
     for (int64_t i = 0; i < D.n_own; ++i) {
         D.gbase[i] = D.goff[cchunk[i]] + lane[i];
         for (size_t s = 0; s < slots[i].size(); ++s) {
@@ -539,6 +540,7 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
             if (s < D.deg_int[i]) {
                 const int64_t e = D.soffc[i] + (int64_t)s;
                 D.sJ[e] = is_left ? D.fr[k] : D.fl[k];
+                D.fslot[(size_t)2 * k + (is_left ? 0 : 1)] = (int32_t)e;
                 const double sg = is_left ? 1.0 : -1.0;
                 const int64_t f = D.fnat[k];
                 for (int q = 0; q < d; ++q) D.sRec[(size_t)4 * e + q] = sg * G.avec[(size_t)q * G.nf + f];
