@@ -332,6 +332,9 @@ def main():
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "k_sweep<3> (per-color MC-LU-SGS sweep)",
                      "avg_launch_ms": sweep_ms_avg, "peak_source": peak_src,
+                     # the DRAM view of the same launches: ncu bytes per launch / live launch time
+                     "traffic_GBs": (traffic / (sweep_ms_avg * 1e-3) / 1e9) if traffic and sweep_ms_avg else None,
+                     "traffic_frac": (traffic / (sweep_ms_avg * 1e-3) / 1e9 / peak) if traffic and sweep_ms_avg else None,
                      "bytes_def": "algorithmic: own Rt, 1/D, alpha/2, dW write + neighbour-unique W, dW + "
                                   "face data once per face + 4 B/slot (DESIGN.md)"},
         "kernels": kernels, "sweep_only": sweep_only,

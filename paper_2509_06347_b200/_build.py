@@ -42,7 +42,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     os.makedirs(bdir, exist_ok=True)
     inc = ["-I", os.path.join(CUDA, "include"), "-I", os.path.join(HERE, "..", "include")]
     o_setup = os.path.join(bdir, "setup.o")
-    _run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall", "-c",
+    _run(["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-Wall", "-c",
           os.path.join(CSRC, "setup.cpp"), "-o", o_setup] + inc)
     o_api = os.path.join(bdir, "api.o")
     flags = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
@@ -51,7 +51,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
         flags += ["-Xptxas", "-v"]
     _run([NVCC] + flags + ["-c", os.path.join(CSRC, "api.cu"), "-o", o_api] + inc)
     tmp = OUT + ".tmp"
-    _run([NVCC] + GENCODE + ["-shared", "-o", tmp, o_setup, o_api, "-cudart", "static"])
+    _run([NVCC] + GENCODE + ["-shared", "-o", tmp, o_setup, o_api, "-cudart", "static", "-lgomp"])
     os.replace(tmp, OUT)
     return OUT
 

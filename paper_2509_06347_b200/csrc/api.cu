@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -895,6 +896,15 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
     if (!ctx->mesh_loaded) { ctx->err = "mesh not loaded"; return GMG_ESTATE; }
     if (n_levels < 1 || n_levels > 3) { ctx->err = "n_levels must be 1..3"; return GMG_EINVAL; }
     gmg_status ret = GMG_OK;
+    // GMG_SETUP_TIMES=1: per-phase host setup times on stderr (dev aid)
+    const bool tm = std::getenv("GMG_SETUP_TIMES") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what, int l) {
+        if (!tm) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[setup] L%d %-14s %8.3f s\n", l, what, std::chrono::duration<double>(t - t_last).count());
+        t_last = t;
+    };
     try {
         ctx->lv.resize(1);
         for (int l = 0;; ++l) {
@@ -905,12 +915,15 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             } else {
                 color_level(H);
             }
+            lap("color", l);
             renumber(H);
+            lap("renumber", l);
             H.parent.clear();
             if (l + 1 >= n_levels) break;
             std::vector<int64_t> parent;
             int64_t nc = 0;
             const int64_t merged = agglomerate(H, ctx->opt.skew_limit, parent, nc);
+            lap("agglomerate", l);
             if (merged == 0) {
                 ret = GMG_ESTALL;
                 ctx->err = "level " + std::to_string(l) + " merged nothing; hierarchy truncated";
@@ -920,6 +933,7 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             H.n_coarse = nc;
             HostLevel C;
             build_coarse(ctx->lv[l], C);
+            lap("build_coarse", l);
             ctx->lv.push_back(std::move(C));
         }
         // domains driven by this process
@@ -929,9 +943,13 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             Domain dm;
             dm.rank = ctx->opt.nranks > 1 ? ctx->opt.rank : k;
             dm.lv.resize(ctx->lv.size());
-            for (size_t l = 0; l < ctx->lv.size(); ++l) build_domain_level(ctx->lv[l], dm.rank, dm.lv[l]);
+            for (size_t l = 0; l < ctx->lv.size(); ++l) {
+                build_domain_level(ctx->lv[l], dm.rank, dm.lv[l]);
+                lap("domain_level", (int)l);
+            }
             for (size_t l = 0; l + 1 < ctx->lv.size(); ++l)
                 link_domain_levels(ctx->lv[l], ctx->lv[l + 1], dm.lv[l], dm.lv[l + 1]);
+            lap("link", 0);
             ctx->dom.push_back(std::move(dm));
         }
     } catch (const std::exception &e) {

@@ -58,11 +58,8 @@ struct DomLevel {
     std::vector<int32_t> gface;            // [ng_entries] +(f+1) left, -(f+1) right (local face f), 0 pad
     // sweep slots (CSR over owned cells, same order as their interior gather slots)
     std::vector<int32_t> soffc;            // [n_own+1]
-    std::vector<int32_t> sJ;               // [ns] local neighbour (owned or ghost)
-    std::vector<double> sRec;              // [ns][4] (A outward | S r)
-    // device sweep slots (currently the CSR arrays; see build_domain_level)
-    std::vector<int32_t> sJe;              // [ne] neighbour
-    std::vector<double> sRe;               // [ne][4] (A outward | S r)
+    std::vector<int32_t> sJe;              // [ns] local neighbour (owned or ghost)
+    std::vector<double> sRe;               // [ns][4] (A outward | S r)
     std::vector<int32_t> ell_cell, ell_stride;   // [n_own] entry of slot 0, stride between slots
     std::vector<int32_t> fslot;            // [nf][2] sweep entry of the face in its left / right cell's slots (-1: none)
     std::vector<int32_t> sp_cell;          // slot-parallel sweep: group cell boundaries, per color

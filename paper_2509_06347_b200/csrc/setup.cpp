@@ -291,7 +291,17 @@ void build_coarse(const HostLevel &fine, HostLevel &C)
         if (a == b) continue;
         pairs.emplace_back(std::min(a, b), std::max(a, b), f);
     }
-    std::sort(pairs.begin(), pairs.end());
+    {   // (a, b, f) order: counting sort by a (stable, f ascending), then each small bucket by (b, f)
+        std::vector<int64_t> cnt(nc + 1, 0);
+        for (const auto &t : pairs) cnt[std::get<0>(t) + 1]++;
+        std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
+        std::vector<std::tuple<int64_t, int64_t, int64_t>> out(pairs.size());
+        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+        for (const auto &t : pairs) out[pos[std::get<0>(t)]++] = t;
+        for (int64_t a = 0; a < nc; ++a)
+            if (cnt[a + 1] - cnt[a] > 1) std::sort(out.begin() + cnt[a], out.begin() + cnt[a + 1]);
+        pairs.swap(out);
+    }
     int64_t ni = 0;
     for (size_t k = 0; k < pairs.size(); ++k)
         if (k == 0 || std::get<0>(pairs[k]) != std::get<0>(pairs[k - 1]) || std::get<1>(pairs[k]) != std::get<1>(pairs[k - 1])) ++ni;
@@ -391,7 +401,7 @@ void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *p
 //    max degree.  Slots: interior faces (ascending id) then boundary faces.
 //  * sweep slots (lanes per cell): CSR -- cell i's interior slots are
 //    contiguous at [soffc[i], soffc[i+1]), same order as its gather slots;
-//    per slot the neighbour sJ and a 32-byte record (A_x, A_y, [A_z,] S r)
+//    per slot the neighbour sJe and a 32-byte record (A_x, A_y, [A_z,] S r)
 //    with A = sigma S n oriented outward from the cell.
 //  * halo plan grouped (color, peer), natural id ascending within a group, so
 //    a sender's group equals the receiver's group element by element.
@@ -453,15 +463,19 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
     // the face kernel's state gathers and the gather kernel's face reads then
     // walk memory roughly in cell order
     {
+        // counting sort by key (stable: fnat is in ascending natural order), the
+        // same order as sorting (key, natural id) pairs
         auto key = [&](int64_t f) {
             int32_t k = n2l[G.left[f]];
             if (G.right[f] >= 0) k = std::min(k, n2l[G.right[f]]);
             return k;
         };
-        std::vector<std::pair<int32_t, int64_t>> kf(D.fnat.size());
-        for (size_t t = 0; t < D.fnat.size(); ++t) kf[t] = {key(D.fnat[t]), D.fnat[t]};
-        std::sort(kf.begin(), kf.end());
-        for (size_t t = 0; t < kf.size(); ++t) D.fnat[t] = kf[t].second;
+        std::vector<int64_t> cnt(D.n_loc + 1, 0), out(D.fnat.size());
+        std::vector<int32_t> kk(D.fnat.size());
+        for (size_t t = 0; t < D.fnat.size(); ++t) { kk[t] = key(D.fnat[t]); cnt[kk[t] + 1]++; }
+        std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
+        for (size_t t = 0; t < D.fnat.size(); ++t) out[cnt[kk[t]]++] = D.fnat[t];
+        D.fnat.swap(out);
     }
     D.nf = (int64_t)D.fnat.size();
     D.fl.resize(D.nf);
@@ -489,19 +503,27 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
             if (D.fr[k] >= 0 && D.fr[k] < D.n_own) iidx[pos[D.fr[k]]++] = k;
         }
     }
-    std::vector<std::vector<int64_t>> slots(D.n_own);
+    // slots of cell i = its incident faces, interior ones first (stable), in place in iidx
     D.deg_int.assign(D.n_own, 0);
     D.deg_all.assign(D.n_own, 0);
-    for (int64_t i = 0; i < D.n_own; ++i) {
-        auto &s = slots[i];
-        for (int64_t a = ioff[i]; a < ioff[i + 1]; ++a)
-            if (D.fr[iidx[a]] >= 0) s.push_back(iidx[a]);
-        const size_t ni = s.size();
-        for (int64_t a = ioff[i]; a < ioff[i + 1]; ++a)
-            if (D.fr[iidx[a]] < 0) s.push_back(iidx[a]);
-        if (s.size() > 255) throw std::runtime_error("cell with more than 255 faces");
-        D.deg_int[i] = (uint8_t)ni;
-        D.deg_all[i] = (uint8_t)s.size();
+    for (int64_t i = 0; i < D.n_own; ++i)
+        if (ioff[i + 1] - ioff[i] > 255) throw std::runtime_error("cell with more than 255 faces");
+#pragma omp parallel
+    {
+        std::vector<int64_t> tmp;
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < D.n_own; ++i) {
+            const int64_t a0 = ioff[i], a1 = ioff[i + 1];
+            tmp.clear();
+            for (int64_t a = a0; a < a1; ++a)
+                if (D.fr[iidx[a]] >= 0) tmp.push_back(iidx[a]);
+            const size_t ni = tmp.size();
+            for (int64_t a = a0; a < a1; ++a)
+                if (D.fr[iidx[a]] < 0) tmp.push_back(iidx[a]);
+            std::copy(tmp.begin(), tmp.end(), iidx.begin() + a0);
+            D.deg_int[i] = (uint8_t)ni;
+            D.deg_all[i] = (uint8_t)(a1 - a0);
+        }
     }
     // SELL-32 gather chunks per color
     std::vector<int32_t> cchunk(D.n_own, 0), lane(D.n_own, 0);
@@ -528,30 +550,30 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
     D.ns_entries = so;
     D.gface.assign(go, 0);
     D.gbase.assign(D.n_own, 0);
-    D.sJ.assign(so, -1);
-    D.sRec.assign((size_t)4 * so, 0.0);
+    D.sJe.assign(so, -1);
+    D.sRe.assign((size_t)4 * so, 0.0);
     D.fslot.assign((size_t)2 * D.nf, -1);
+    // every cell writes only its own gather / sweep slots and its (face, side) fslot entries
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < D.n_own; ++i) {
         D.gbase[i] = D.goff[cchunk[i]] + lane[i];
-        for (size_t s = 0; s < slots[i].size(); ++s) {
-            const int64_t k = slots[i][s];
+        for (int64_t s = 0; s < ioff[i + 1] - ioff[i]; ++s) {
+            const int64_t k = iidx[ioff[i] + s];
             const bool is_left = (D.fl[k] == i);
             D.gface[D.gbase[i] + s * kChunk] = is_left ? (int32_t)(k + 1) : -(int32_t)(k + 1);
             if (s < D.deg_int[i]) {
                 const int64_t e = D.soffc[i] + (int64_t)s;
-                D.sJ[e] = is_left ? D.fr[k] : D.fl[k];
+                D.sJe[e] = is_left ? D.fr[k] : D.fl[k];
                 D.fslot[(size_t)2 * k + (is_left ? 0 : 1)] = (int32_t)e;
                 const double sg = is_left ? 1.0 : -1.0;
                 const int64_t f = D.fnat[k];
-                for (int q = 0; q < d; ++q) D.sRec[(size_t)4 * e + q] = sg * G.avec[(size_t)q * G.nf + f];
+                for (int q = 0; q < d; ++q) D.sRe[(size_t)4 * e + q] = sg * G.avec[(size_t)q * G.nf + f];
             }
         }
     }
-    // device sweep slots: the CSR arrays themselves (entry of slot s of cell i
+    // device sweep slots: CSR (entry of slot s of cell i
     // = ell_cell[i] + s * ell_stride[i]; the indirection lets the layout be
     // swapped for ELL variants, which measured slower on the coarse levels)
-    D.sJe = D.sJ;
-    D.sRe = D.sRec;
     D.ell_cell.assign(D.soffc.begin(), D.soffc.end() - 1);
     D.ell_stride.assign(D.n_own, 1);
     // slot-parallel sweep groups: per color, runs of whole cells whose slots fit in 256 lanes
@@ -582,10 +604,12 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
         const int64_t nat = D.l2n[g];
         rg[(G.color[nat] - 1) * np + peer_index(G.part_of(nat))].push_back((int32_t)g);
     }
-    for (int64_t i = 0; i < D.n_own; ++i) {                       // owned: (color, id) order
-        std::vector<int> ps;
+    std::vector<int> ps;
+    for (int64_t i = 0; i < D.n_own; ++i) {                       // owned: (color, boundary first, id) order
+        if (!bnd[D.l2n[i]]) continue;                             // no ghost neighbour
+        ps.clear();
         for (int32_t e = D.soffc[i]; e < D.soffc[i + 1]; ++e) {
-            const int32_t j = D.sJ[e];
+            const int32_t j = D.sJe[e];
             if (j >= D.n_own) ps.push_back(G.part_of(D.l2n[j]));
         }
         std::sort(ps.begin(), ps.end());
@@ -609,19 +633,20 @@ void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, 
     std::vector<int32_t> c2l(Gc.n, -1);
     for (int64_t i = 0; i < Dc.n_own; ++i) c2l[Dc.l2n[i]] = (int32_t)i;
     Df.parent.assign(Df.n_own, -1);
-    std::vector<std::pair<int64_t, int32_t>> fine_by_id(Df.n_own);
+    std::vector<int32_t> f2l(Gf.n, -1);                 // natural -> local (owned) fine index
     for (int64_t i = 0; i < Df.n_own; ++i) {
         const int32_t pc = c2l[Gf.parent[Df.l2n[i]]];
         if (pc < 0) throw std::runtime_error("coarse parent not owned by the fine cell's rank");
         Df.parent[i] = pc;
-        fine_by_id[i] = {Df.l2n[i], (int32_t)i};
+        f2l[Df.l2n[i]] = (int32_t)i;
     }
-    std::sort(fine_by_id.begin(), fine_by_id.end());
     Dc.child.assign(2 * Dc.n_own, -1);
-    for (const auto &fi : fine_by_id) {                 // ascending natural id of the fine cell
-        const int32_t c = Df.parent[fi.second];
-        if (Dc.child[c] < 0) Dc.child[c] = fi.second;
-        else Dc.child[Dc.n_own + c] = fi.second;
+    for (int64_t nat = 0; nat < Gf.n; ++nat) {          // ascending natural id of the fine cell
+        const int32_t i = f2l[nat];
+        if (i < 0) continue;
+        const int32_t c = Df.parent[i];
+        if (Dc.child[c] < 0) Dc.child[c] = i;
+        else Dc.child[Dc.n_own + c] = i;
     }
 }
 
