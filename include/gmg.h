@@ -91,6 +91,10 @@ typedef struct {
                                halo exchanged by device copies on the stream.  Same layouts,
                                plans, pack/unpack kernels and exchange points as the NCCL path;
                                used to test the partitioned path on one GPU.  Default 1.      */
+    int setup_device;       /* 1: gmg_build_hierarchy runs Algorithm 1 (coloring) and
+                               Algorithm 3 (agglomeration) on `device`.
+                               The results are identical to the host setup (0, default):
+                               same colors, renumbering and parent maps, bit for bit.         */
 } gmg_options;
 
 /* Fill *o with the defaults above (dim = 3, single rank, device 0, stream 0). */

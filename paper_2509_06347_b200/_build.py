@@ -50,8 +50,11 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     if verbose_ptxas:
         flags += ["-Xptxas", "-v"]
     _run([NVCC] + flags + ["-c", os.path.join(CSRC, "api.cu"), "-o", o_api] + inc)
+    # device-side setup: no FMA contraction anywhere (bit-identical decisions to the host setup)
+    o_sdev = os.path.join(bdir, "setup_dev.o")
+    _run([NVCC] + flags + ["--fmad=false", "-c", os.path.join(CSRC, "setup_dev.cu"), "-o", o_sdev] + inc)
     tmp = OUT + ".tmp"
-    _run([NVCC] + GENCODE + ["-shared", "-o", tmp, o_setup, o_api, "-cudart", "static", "-lgomp"])
+    _run([NVCC] + GENCODE + ["-shared", "-o", tmp, o_setup, o_api, o_sdev, "-cudart", "static", "-lgomp"])
     os.replace(tmp, OUT)
     return OUT
 

@@ -818,6 +818,7 @@ void gmg_default_options(gmg_options *o)
     o->device = 0;
     o->stream = nullptr;
     o->local_domains = 1;
+    o->setup_device = 0;
     o->beta = 0.5;
 }
 
@@ -830,7 +831,8 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
         !(opt->r_factor >= 1.0) || opt->fine_smoother < 0 || opt->fine_smoother > 1 || opt->df_mode < 0 ||
         opt->df_mode > 3 || (opt->df_mode == 3 && !(opt->beta >= 0.0 && opt->beta <= 1.0)) || opt->nranks < 1 ||
         opt->rank < 0 || opt->rank >= opt->nranks || opt->local_domains < 1 ||
-        opt->local_domains > 64 || (opt->nranks > 1 && (opt->local_domains != 1 || !opt->nccl_id)))
+        opt->local_domains > 64 || (opt->nranks > 1 && (opt->local_domains != 1 || !opt->nccl_id)) ||
+        opt->setup_device < 0 || opt->setup_device > 1)
         return GMG_EINVAL;
     gmg_ctx *ctx = new (std::nothrow) gmg_ctx();
     if (!ctx) return GMG_ENOMEM;
@@ -905,6 +907,17 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
         std::fprintf(stderr, "[setup] L%d %-14s %8.3f s\n", l, what, std::chrono::duration<double>(t - t_last).count());
         t_last = t;
     };
+    const bool dev = ctx->opt.setup_device == 1;
+    cudaStream_t ss = nullptr;
+    SetupStats sst;
+    if (dev) {
+        CK(cudaSetDevice(ctx->opt.device));
+        CK(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+    }
+    struct StreamGuard {
+        cudaStream_t s;
+        ~StreamGuard() { if (s) cudaStreamDestroy(s); }
+    } sguard{ss};
     try {
         ctx->lv.resize(1);
         for (int l = 0;; ++l) {
@@ -912,6 +925,8 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             if (l == 0 && !ctx->user_color0.empty()) {
                 H.color = ctx->user_color0;
                 H.ncolor = *std::max_element(H.color.begin(), H.color.end());
+            } else if (dev) {
+                color_level_dev(H, ss, &sst);
             } else {
                 color_level(H);
             }
@@ -922,7 +937,8 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             if (l + 1 >= n_levels) break;
             std::vector<int64_t> parent;
             int64_t nc = 0;
-            const int64_t merged = agglomerate(H, ctx->opt.skew_limit, parent, nc);
+            const int64_t merged = dev ? agglomerate_dev(H, ctx->opt.skew_limit, parent, nc, ss, &sst)
+                                       : agglomerate(H, ctx->opt.skew_limit, parent, nc);
             lap("agglomerate", l);
             if (merged == 0) {
                 ret = GMG_ESTALL;
@@ -950,6 +966,9 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             for (size_t l = 0; l + 1 < ctx->lv.size(); ++l)
                 link_domain_levels(ctx->lv[l], ctx->lv[l + 1], dm.lv[l], dm.lv[l + 1]);
             lap("link", 0);
+            if (tm && dev)
+                std::fprintf(stderr, "[setup] device: %lld BFS levels, %lld color rounds, %lld matching rounds\n",
+                             (long long)sst.color_levels, (long long)sst.color_rounds, (long long)sst.match_rounds);
             ctx->dom.push_back(std::move(dm));
         }
     } catch (const std::exception &e) {

@@ -175,6 +175,13 @@ struct gmg_ctx {
 };
 
 namespace gmg {
+struct SetupStats {                 // device setup diagnostics
+    int64_t color_levels = 0, color_rounds = 0, match_rounds = 0;
+};
+// setup_dev.cu (device-side Algorithm 1 / Algorithm 3, results identical to the host versions)
+int color_level_dev(HostLevel &L, cudaStream_t s, SetupStats *st);
+int64_t agglomerate_dev(const HostLevel &L, double theta, std::vector<int64_t> &parent, int64_t &nc, cudaStream_t s,
+                        SetupStats *st);
 // setup.cpp
 gmg_status load_mesh(gmg_ctx *ctx, int64_t n, const double *vol, const double *ctr, int64_t nf,
                      const int64_t *left, const int64_t *right, const double *avec, const double *fctr,

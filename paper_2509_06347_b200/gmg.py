@@ -44,7 +44,8 @@ class Options(C.Structure):
                 ("n_sweeps", C.c_int), ("n_levels", C.c_int), ("pre_smooth", C.c_int), ("post_smooth", C.c_int),
                 ("skew_limit", C.c_double), ("r_factor", C.c_double), ("fine_smoother", C.c_int),
                 ("df_mode", C.c_int), ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p),
-                ("device", C.c_int), ("stream", C.c_void_p), ("beta", C.c_double), ("local_domains", C.c_int)]
+                ("device", C.c_int), ("stream", C.c_void_p), ("beta", C.c_double), ("local_domains", C.c_int),
+                ("setup_device", C.c_int)]
 
 
 _lib = None

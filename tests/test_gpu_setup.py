@@ -1,0 +1,94 @@
+"""Device-side setup: Algorithm 1 coloring and
+Algorithm 3 agglomeration run on the GPU (gmg_options.setup_device = 1) must
+give the host setup's hierarchy bit for bit -- colors, renumbering, parent
+maps and the coarse geometry built from them -- on every mesh family, with
+and without the partition constraint, and on a disconnected mesh (the
+Algorithm-1 restart at the least uncolored id)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from synth import configs
+from synth.mesh import Mesh
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_06347_b200 import _build, gmg
+    _build.build()
+    gmg.lib()
+    return gmg
+
+
+def _concat(a: Mesh, b: Mesh) -> Mesh:
+    """two meshes side by side, no shared face (a disconnected mesh)"""
+    na = a.vol.size
+    shift = lambda r: np.where(r >= 0, r + na, r)
+    return dataclasses.replace(
+        a, vol=np.concatenate([a.vol, b.vol]), ctr=np.concatenate([a.ctr, b.ctr + 10.0], axis=1),
+        left=np.concatenate([a.left, b.left + na]), right=np.concatenate([a.right, shift(b.right)]),
+        avec=np.concatenate([a.avec, b.avec], axis=1), fctr=np.concatenate([a.fctr, b.fctr + 10.0], axis=1),
+        ngauss=np.concatenate([a.ngauss, b.ngauss]), name="disconnected")
+
+
+MESHES = {
+    "config1": lambda: configs.config(1),
+    "config2": lambda: configs.config(2),
+    "cylinder": lambda: configs.cylinder_ogrid(64, 24),
+    "box": lambda: configs.box3d(9, 7, 6, 2, seed=5),
+    "sphere": lambda: configs.sphere_shell(10, 4, 4),
+    "disconnected": lambda: _concat(configs.box3d(5, 4, 3, 1, seed=1), configs.box3d(4, 4, 4, 2, seed=2)),
+}
+
+
+def _hier(G, m, dev, part=None, P=1):
+    kw = dict(setup_device=dev)
+    if part is not None:
+        kw.update(part=part, local_domains=P)
+    s = G.Solver(m, n_levels=3, build_only=True, **kw)
+    out = []
+    for l in range(s.n_levels):
+        col, perm, par = s.maps(l)
+        geo = s.geometry(l)
+        out.append((col, perm, par, geo))
+    s.close()
+    return out
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_device_setup_equals_host(G, name):
+    m = MESHES[name]()
+    h = _hier(G, m, 0)
+    d = _hier(G, m, 1)
+    assert len(h) == len(d)
+    for (c0, p0, q0, g0), (c1, p1, q1, g1) in zip(h, d):
+        assert np.array_equal(c0, c1)
+        assert np.array_equal(p0, p1)
+        assert np.array_equal(q0, q1)
+        for k in g0:
+            assert np.array_equal(g0[k], g1[k]), k
+
+
+@pytest.mark.parametrize("P", [2, 5])
+def test_device_setup_partitioned(G, P):
+    m = configs.sphere_shell(10, 4, 4)
+    part = G.gmg_partition_rcb(m.ctr, P)
+    h = _hier(G, m, 0, part, P)
+    d = _hier(G, m, 1, part, P)
+    for (c0, p0, q0, _), (c1, p1, q1, _) in zip(h, d):
+        assert np.array_equal(c0, c1) and np.array_equal(p0, p1) and np.array_equal(q0, q1)
+
+
+def test_device_setup_full_size(G):
+    """config 4 (998,400 cells), the benchmark's mesh"""
+    m = configs.config(4)
+    h = _hier(G, m, 0)
+    d = _hier(G, m, 1)
+    for (c0, p0, q0, _), (c1, p1, q1, _) in zip(h, d):
+        assert np.array_equal(c0, c1) and np.array_equal(p0, p1) and np.array_equal(q0, q1)
