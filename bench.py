@@ -100,6 +100,23 @@ def sweep_updates_per_cycle(sizes, n_sweeps, fine_smoother):
     return sum(sizes[l][0] for l in lv) * 2 * n_sweeps
 
 
+def sweep_cells_executed_per_cycle(solver, n_sweeps, fine_smoother):
+    """cell visits the library actually runs: the same-color phase at every
+    sweep turn (c_N then c_N, c_1 then c_1) is idempotent and skipped (exact,
+    DESIGN.md §6); the metric counts Algorithm 2's nominal N * 2 * n_sweeps
+    updates, whose result is delivered bit for bit
+    (tests/test_gpu_parity.py::test_repeated_phase_skip_is_bit_exact)"""
+    import numpy as np
+    tot = 0
+    for l in range(0 if fine_smoother else 1, solver.n_levels):
+        cnt = np.bincount(solver.maps(l)[0])[1:]
+        if len(cnt) == 1:
+            tot += int(cnt[0])
+        else:
+            tot += int(cnt.sum()) * 2 * n_sweeps - n_sweeps * int(cnt[-1]) - (n_sweeps - 1) * int(cnt[0])
+    return tot
+
+
 def cpu_baseline(m, W, Winf, n_sweeps, n_cycles=1):
     """The oracle, as it stands (single thread), on n_cycles V-cycles of the
     same mesh.  Hierarchy build is setup, not timed."""
@@ -323,6 +340,8 @@ def main():
                                f"({m.meta['cell_type_counts']}), 3-level V-cycle, {args.n_sweeps} MC-LU-SGS sweeps",
                    "levels": [{"cells": int(n), "colors": int(c), "faces": int(f)} for (n, c, f) in s.sizes],
                    "sweep_cell_updates_per_vcycle": int(cu_cycle),
+                   "sweep_cell_visits_executed_per_vcycle": int(sweep_cells_executed_per_cycle(s, args.n_sweeps, 0))
+                   * (ws if replicas else 1),
                    "l2": f"inputs larger than L2: workspace {ws_bytes / 1e9:.2f} GB >> 126 MB",
                    "parallelism": parallelism,
                    "n_gpus_partitions": 1 if replicas else ws},

@@ -469,10 +469,20 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
     const int nc = ctx->lv[l].ncolor;
     struct Ph { int c; bool last; };
     std::vector<Ph> seq;
+    // Algorithm 2's phase list.  A color phase that directly follows a phase
+    // of the SAME color (the turn of every forward -> backward and backward ->
+    // forward pass: c_N then c_N, c_1 then c_1) is idempotent: a cell's update
+    // reads only other-colored neighbours, none of which changed in between,
+    // and never its own dW -- so it recomputes bit-identical values and is
+    // dropped (its W = W_lin + dW write, if any, moves to the kept phase).
+    // Exact, not an approximation: the oracle runs every phase.
     for (int s = 0; s < n_sweeps; ++s)
         for (int half = 0; half < 2; ++half)
-            for (int cc = 0; cc < nc; ++cc)
-                seq.push_back({half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1});
+            for (int cc = 0; cc < nc; ++cc) {
+                const Ph ph{half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1};
+                if (ctx->skip_repeat && !seq.empty() && seq.back().c == ph.c) seq.back().last |= ph.last;
+                else seq.push_back(ph);
+            }
     const bool fuse = ctx->tail_cells > 0 && ctx->nparts == 1 && ctx->dom.size() == 1;
     const bool overlap = (ctx->overlap < 0 ? ctx->opt.nranks > 1 : ctx->overlap != 0) && ctx->nparts > 1 && ctx->side && !ctx->pipe && !ctx->spsweep && !ctx->wsweep;
     for (size_t k = 0; k < seq.size();) {
@@ -848,6 +858,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_PIPE")) ctx->pipe = std::atoi(e);        // pipelined warp sweep
     if (const char *e = std::getenv("GMG_OVERLAP")) ctx->overlap = std::atoi(e);  // boundary-first exchange overlap
     if (const char *e = std::getenv("GMG_ALPC")) ctx->adapt_lpc = std::atoi(e);   // wider lanes for small colors
+    if (const char *e = std::getenv("GMG_SKIP_REPEAT")) ctx->skip_repeat = std::atoi(e);   // drop idempotent phases
     *out = ctx;
     return GMG_OK;
 }

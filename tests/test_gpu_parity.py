@@ -246,3 +246,28 @@ def test_config4_full_size_vcycle(G, orc):
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 1)
     assert rel(Wg, Wo) <= TOL
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+
+
+@pytest.mark.parametrize("name", ["config1", "sphere_small", "cyl_small"])
+def test_repeated_phase_skip_is_bit_exact(G, name, monkeypatch):
+    """The same-color phase at each sweep turn (c_N then c_N, c_1 then c_1) is
+    dropped by default; running every phase of Algorithm 2 must give the SAME
+    bits (a cell's update never reads its own dW, and its other-colored
+    neighbours do not change in between)."""
+    m, Winf, W = _case(name)
+    out = {}
+    for skip in ("0", "1"):
+        monkeypatch.setenv("GMG_SKIP_REPEAT", skip)
+        s = G.Solver(m, n_levels=3)
+        s.set_state(W, Winf)
+        h = s.vcycle(3)
+        Wv = s.get_state(0)
+        s.set_level_state(1, s.get_state(1))
+        dW = s.smooth(1, 4)
+        out[skip] = (h, Wv, [s.get_state(l) for l in (1, 2)], dW)
+        s.close()
+    a, b = out["0"], out["1"]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for x, y in zip(a[2], b[2]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a[3], b[3])
