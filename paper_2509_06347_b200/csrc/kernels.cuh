@@ -152,8 +152,14 @@ __device__ __forceinline__ void kfvs_side(const Side<D> &s, const double *n, dou
     const double inv2l = s.p * s.ir;                     // 1 / (2 lambda)
     const double rl = rsqrt(lam);
     const double sl = lam * rl;                          // sqrt(lambda)
-    const double e = exp(-lam * s.U * s.U) * (0.28209479177387814 * rl);   // 1/(2 sqrt(pi lambda))
-    const double m0 = 0.5 * erfc(-sgn * sl * s.U);
+    // erfc(x) = e^{-x^2} erfcx(x) (x >= 0), 2 - e^{-x^2} erfcx(-x) (x < 0) with
+    // x = -sgn sqrt(lambda) U: the Gaussian e^{-lambda U^2} is shared with <u^1>
+    // instead of being recomputed inside erfc
+    const double g = exp(-lam * s.U * s.U);
+    const double e = g * (0.28209479177387814 * rl);   // e^{-lambda U^2} / (2 sqrt(pi lambda))
+    const double x = -sgn * sl * s.U;
+    const double gx = g * erfcx(fabs(x));
+    const double m0 = 0.5 * (x >= 0.0 ? gx : 2.0 - gx);
     const double m1 = s.U * m0 + sgn * e;
     const double m2 = s.U * m1 + inv2l * m0;
     const double m3 = s.U * m2 + 2.0 * inv2l * m1;
@@ -178,7 +184,7 @@ template <int D> struct FR { static constexpr int SR = D + 2, AM = D + 3; };
 // cells -- whole 32-byte records, so no partial-sector update (the gather
 // used to patch S r into each slot)
 template <int D, bool FLUX, int STRIDE, bool DF, bool PREP>
-__global__ void __launch_bounds__(256, 3) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
+__global__ void __launch_bounds__(256, DF ? 3 : 4) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
 {
     pdl_enter();
     constexpr int NV = D + 2;
