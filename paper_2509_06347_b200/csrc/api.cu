@@ -382,19 +382,25 @@ void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win,
 
 // one color block of one domain (Eq.(gpu-forward-relaxation) / (gpu-backward-relaxation))
 // part: 0 = whole block, 1 = its boundary cells (ghost neighbours), 2 = its interior cells
+// first_fwd: a phase of the first forward half-sweep of a smoothing step --
+// owned neighbours of later colors still hold dW = +0 (zeroed before the
+// step), so their terms are exactly +0 and the kernel skips them
 template <int D>
-void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout, int part = 0)
+void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout, int part = 0,
+                         bool first_fwd = false)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
     const DomLevel &H = dm.lv[l];
     int b0 = (int)H.blk[c], b1 = (int)H.blk[c + 1];
+    const int zlo = (first_fwd && ctx->skip_zero) ? (int)H.blk[c + 1] : 0;
+    const int zhi = (first_fwd && ctx->skip_zero) ? (int)H.n_own : 0;
     if (part) {
         const int mid = b0 + (int)H.nbnd[c];
         const double frac = b1 > b0 ? (double)(part == 1 ? mid - b0 : b1 - mid) / (b1 - b0) : 0.0;
         if (part == 1) b1 = mid;
         else b0 = mid;
-        SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs, Wout};
+        SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs, Wout, zlo, zhi};
         if (b1 <= b0) return;
         Lc.pre(GMG_K_SWEEP);
         switch (ctx->lpc) {
@@ -405,7 +411,7 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
         Lc.post(GMG_K_SWEEP, frac * (dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0)));
         return;
     }
-    SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs, Wout};
+    SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs, Wout, zlo, zhi};
     if (a.cend <= a.cbeg) return;
     Lc.pre(GMG_K_SWEEP);
     if (ctx->pipe) {
@@ -467,7 +473,7 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
 {
     gmg_ctx *ctx = Lc.ctx;
     const int nc = ctx->lv[l].ncolor;
-    struct Ph { int c; bool last; };
+    struct Ph { int c; bool last; bool ff; };
     std::vector<Ph> seq;
     // Algorithm 2's phase list.  A color phase that directly follows a phase
     // of the SAME color (the turn of every forward -> backward and backward ->
@@ -479,7 +485,7 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
     for (int s = 0; s < n_sweeps; ++s)
         for (int half = 0; half < 2; ++half)
             for (int cc = 0; cc < nc; ++cc) {
-                const Ph ph{half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1};
+                const Ph ph{half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1, s == 0 && half == 0};
                 if (ctx->skip_repeat && !seq.empty() && seq.back().c == ph.c) seq.back().last |= ph.last;
                 else seq.push_back(ph);
             }
@@ -521,18 +527,18 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
             // side stream while the interior cells of c (no ghost neighbours)
             // are swept; the next color waits for the ghosts (fork / join)
             for (Domain &dm : ctx->dom)
-                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 1);
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 1, seq[k].ff);
             cudaEventRecord(ctx->ev_fork, Lc.s);
             cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
             Launcher Ls{ctx, ctx->side};
             enqueue_exchange<D>(Ls, l, EX_DW, c);
             cudaEventRecord(ctx->ev_join, ctx->side);
             for (Domain &dm : ctx->dom)
-                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 2);
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 2, seq[k].ff);
             cudaStreamWaitEvent(Lc.s, ctx->ev_join, 0);
         } else {
             for (Domain &dm : ctx->dom)
-                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr);
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 0, seq[k].ff);
             enqueue_exchange<D>(Lc, l, EX_DW, c);
         }
         ++k;
@@ -859,6 +865,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_OVERLAP")) ctx->overlap = std::atoi(e);  // boundary-first exchange overlap
     if (const char *e = std::getenv("GMG_ALPC")) ctx->adapt_lpc = std::atoi(e);   // wider lanes for small colors
     if (const char *e = std::getenv("GMG_SKIP_REPEAT")) ctx->skip_repeat = std::atoi(e);   // drop idempotent phases
+    if (const char *e = std::getenv("GMG_SKIP_ZERO")) ctx->skip_zero = std::atoi(e);       // skip +0 neighbour terms
     *out = ctx;
     return GMG_OK;
 }

@@ -162,6 +162,7 @@ struct gmg_ctx {
     int lpc = 2;                      // sweep lanes per cell (1, 2, 4) of the large color blocks
     int adapt_lpc = 1;                // blocks that fit one wave at 2x lanes get up to 16 lanes per cell
     int skip_repeat = 1;              // drop the repeated same-color phase at every sweep turn (exact)
+    int skip_zero = 1;                // first forward half-sweep: skip later-color neighbours (dW = +0, exact)
     int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
     int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (no measured gain)

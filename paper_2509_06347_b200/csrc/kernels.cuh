@@ -491,6 +491,8 @@ struct SweepArgs {
     const double *sRe;         // [ns][4] (A outward | S r)
     const double *rhs;         // [n][nv]
     double *Wout;              // [n][nv] or null: W = W_lin + dW (last backward half-sweep)
+    int zlo, zhi;              // neighbours j in [zlo, zhi) still hold dW = +0 exactly (first
+                               // forward half-sweep, later colors): their term is +0, skipped
 };
 
 // neighbour record -> (W_lin, dW)
@@ -652,6 +654,7 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
             int j = e < e1 ? __ldg(a.sJe + e) : 0;
             for (; e < e1; e += LPC) {
                 const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
+                if (j >= a.zlo && j < a.zhi) { j = jn; continue; }
                 double sr[4];
                 ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
                 double w[NV], dw[NV];
@@ -662,6 +665,7 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
         } else {
             for (int e = e0 + sub; e < e1; e += LPC) {
                 const int j = __ldg(a.sJe + e);
+                if (j >= a.zlo && j < a.zhi) continue;
                 double sr[4];
                 ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
                 double w[NV], dw[NV];

@@ -248,26 +248,51 @@ def test_config4_full_size_vcycle(G, orc):
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
 
 
+def _skip_runs(G, name, monkeypatch, var, values, fixed):
+    m, Winf, W = _case(name)
+    out = {}
+    for k, v in fixed.items():
+        monkeypatch.setenv(k, v)
+    for v in values:
+        monkeypatch.setenv(var, v)
+        s = G.Solver(m, n_levels=3)
+        s.set_state(W, Winf)
+        h = s.vcycle(3)
+        Wv = s.get_state(0)
+        coarse = [s.get_state(l) for l in (1, 2)]
+        s.set_level_state(1, coarse[0])
+        dW = s.smooth(1, 4)
+        out[v] = (h, Wv, coarse, dW)
+        s.close()
+    return out
+
+
 @pytest.mark.parametrize("name", ["config1", "sphere_small", "cyl_small"])
 def test_repeated_phase_skip_is_bit_exact(G, name, monkeypatch):
     """The same-color phase at each sweep turn (c_N then c_N, c_1 then c_1) is
     dropped by default; running every phase of Algorithm 2 must give the SAME
     bits (a cell's update never reads its own dW, and its other-colored
-    neighbours do not change in between)."""
-    m, Winf, W = _case(name)
-    out = {}
-    for skip in ("0", "1"):
-        monkeypatch.setenv("GMG_SKIP_REPEAT", skip)
-        s = G.Solver(m, n_levels=3)
-        s.set_state(W, Winf)
-        h = s.vcycle(3)
-        Wv = s.get_state(0)
-        s.set_level_state(1, s.get_state(1))
-        dW = s.smooth(1, 4)
-        out[skip] = (h, Wv, [s.get_state(l) for l in (1, 2)], dW)
-        s.close()
+    neighbours do not change in between: the kernel would recompute the
+    identical arithmetic on identical inputs)."""
+    out = _skip_runs(G, name, monkeypatch, "GMG_SKIP_REPEAT", ("0", "1"), {"GMG_SKIP_ZERO": "1"})
     a, b = out["0"], out["1"]
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     for x, y in zip(a[2], b[2]):
         assert np.array_equal(x, y)
     assert np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("name", ["config1", "sphere_small", "cyl_small"])
+def test_zero_term_skip_is_roundoff_exact(G, orc, name, monkeypatch):
+    """First forward half-sweep: later-colored neighbours still hold dW = +0,
+    so their terms T(W+0) - T(W) - r 0 are exactly 0 in exact arithmetic (and
+    in the oracle, which has no FMA contraction).  Skipping them changes the
+    device result only by the FMA-contraction roundoff of those would-be-zero
+    differences."""
+    out = _skip_runs(G, name, monkeypatch, "GMG_SKIP_ZERO", ("0", "1"), {"GMG_SKIP_REPEAT": "1"})
+    a, b = out["0"], out["1"]
+    assert rel(a[1], b[1]) <= 1e-13
+    assert np.all(np.abs(a[0] - b[0]) <= 1e-13 * a[0][0][None, :])
+    for x, y in zip(a[2], b[2]):
+        assert rel(x, y) <= 1e-13
+    assert rel(a[3], b[3]) <= 1e-12
