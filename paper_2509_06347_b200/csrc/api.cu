@@ -1203,8 +1203,13 @@ gmg_status gmg_set_state(gmg_ctx *ctx, const double *W, const double *W_inf)
     if (st) return st;
     if (!W || !W_inf) { ctx->err = "null state"; return GMG_EINVAL; }
     const int nv = ctx->opt.dim + 2;
-    for (int q = 0; q < nv; ++q) ctx->winf[q] = W_inf[q];
-    if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }   // BC values are kernel params
+    bool same = true;
+    for (int q = 0; q < nv; ++q) {
+        same = same && std::memcmp(&ctx->winf[q], &W_inf[q], sizeof(double)) == 0;
+        ctx->winf[q] = W_inf[q];
+    }
+    // the far-field state is a kernel parameter of the captured V-cycle: re-capture only if it changed
+    if (ctx->graph && !same) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
     st = put_natural(ctx, 0, W, nv, [](DevLevel &L) { return L.W; }, true);
     if (st) return st;
     ctx->state_set = true;
