@@ -489,6 +489,43 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
                 if (ctx->skip_repeat && !seq.empty() && seq.back().c == ph.c) seq.back().last |= ph.last;
                 else seq.push_back(ph);
             }
+    // dependency-driven persistent sweep: one launch for the whole smoothing step
+    if (ctx->flow && ctx->flow_grid > 0 && ctx->nparts == 1 && ctx->dom.size() == 1 && ctx->dom[0].dv[l].nchunk > 0 &&
+        (int)seq.size() <= kFlowMaxPh && !ctx->pipe && !ctx->spsweep && !ctx->wsweep) {
+        Domain &dm = ctx->dom[0];
+        DevLevel &L = dm.dv[l];
+        FlowArgs f{};
+        f.nph = (int)seq.size();
+        f.K = L.nchunk;
+        f.n_own = L.n;
+        f.seg = L.seg;
+        f.cnoff = L.cnoff;
+        f.cnidx = L.cnidx;
+        f.prog = L.prog;
+        f.err = ctx->d_flag + 2;
+        double bytes = 0;
+        for (size_t k = 0; k < seq.size(); ++k) {
+            f.ph[k] = (unsigned short)(seq[k].c | (seq[k].last ? 1 << 8 : 0) | (seq[k].ff && ctx->skip_zero ? 1 << 9 : 0));
+            bytes += dm.lbytes[l].sweep[seq[k].c] + (seq[k].last ? dm.lbytes[l].sweep_out[seq[k].c] : 0.0);
+        }
+        SweepArgs a{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs(L), wout(L), 0, 0};
+        cudaMemsetAsync(L.prog, 0, sizeof(int) * L.nchunk, Lc.s);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(std::min(ctx->flow_grid, L.nchunk));
+        cfg.blockDim = dim3(256);
+        cfg.stream = Lc.s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (ctx->flow == 2) cfg.gridDim = dim3(std::min(ctx->flow_grid, (L.nchunk + 7) / 8));
+        Lc.pre(GMG_K_SWEEP);
+        if (ctx->flow == 2) cudaLaunchKernelEx(&cfg, k_sweep_flow_w<D>, a, f);
+        else cudaLaunchKernelEx(&cfg, k_sweep_flow<D>, a, f);
+        Lc.post(GMG_K_SWEEP, bytes);
+        return;
+    }
     const bool fuse = ctx->tail_cells > 0 && ctx->nparts == 1 && ctx->dom.size() == 1;
     const bool overlap = (ctx->overlap < 0 ? ctx->opt.nranks > 1 : ctx->overlap != 0) && ctx->nparts > 1 && ctx->side && !ctx->pipe && !ctx->spsweep && !ctx->wsweep;
     for (size_t k = 0; k < seq.size();) {
@@ -719,6 +756,11 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.spcell = b.take<int>(H.sp_cell.size());
             L.sinfo = b.take<int2>(n);
             L.fslot = b.take<int2>(nf);
+            L.nchunk = H.nchunk;
+            L.seg = b.take<int>(H.seg.size());
+            L.cnoff = b.take<int>(H.cnoff.size());
+            L.cnidx = b.take<int>(H.cnidx.size());
+            L.prog = b.take<int>(H.nchunk);
             L.ginfo = b.take<int4>(n);
             L.sJe = b.take<int>(H.sJe.size());
             L.sRe = b.take<double>(H.sRe.size());
@@ -866,6 +908,8 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_ALPC")) ctx->adapt_lpc = std::atoi(e);   // wider lanes for small colors
     if (const char *e = std::getenv("GMG_SKIP_REPEAT")) ctx->skip_repeat = std::atoi(e);   // drop idempotent phases
     if (const char *e = std::getenv("GMG_SKIP_ZERO")) ctx->skip_zero = std::atoi(e);       // skip +0 neighbour terms
+    if (const char *e = std::getenv("GMG_FLOW")) ctx->flow = std::atoi(e);                 // dependency-driven sweep
+    if (const char *e = std::getenv("GMG_FLOW_CHUNK")) ctx->flow_chunk = std::max(32, std::atoi(e));
     *out = ctx;
     return GMG_OK;
 }
@@ -978,7 +1022,8 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             dm.rank = ctx->opt.nranks > 1 ? ctx->opt.rank : k;
             dm.lv.resize(ctx->lv.size());
             for (size_t l = 0; l < ctx->lv.size(); ++l) {
-                build_domain_level(ctx->lv[l], dm.rank, dm.lv[l]);
+                build_domain_level(ctx->lv[l], dm.rank, dm.lv[l],
+                                   (ctx->flow && ctx->nparts == 1) ? ctx->flow_chunk : 0);
                 lap("domain_level", (int)l);
             }
             for (size_t l = 0; l + 1 < ctx->lv.size(); ++l)
@@ -1103,6 +1148,12 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.ecell, H.ell_cell.data(), H.ell_cell.size() * sizeof(int)));
             CK(up_raw(L.spcell, H.sp_cell.data(), H.sp_cell.size() * sizeof(int)));
             CK(up_raw(L.fslot, H.fslot.data(), H.fslot.size() * sizeof(int)));
+            if (H.nchunk) {
+                std::vector<int> sg(H.seg.begin(), H.seg.end());
+                CK(up_i(L.seg, std::move(sg)));
+                CK(up_raw(L.cnoff, H.cnoff.data(), H.cnoff.size() * sizeof(int)));
+                CK(up_raw(L.cnidx, H.cnidx.data(), H.cnidx.size() * sizeof(int)));
+            }
             {
                 std::vector<int> si(2 * H.n_own);
                 for (int64_t i = 0; i < H.n_own; ++i) { si[2 * i] = H.ell_cell[i]; si[2 * i + 1] = H.deg_int[i]; }
@@ -1158,6 +1209,10 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         else
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, 4, 3>, 256, 0);
         g_sweep_grid_cap = waves > 0 ? waves * nsm * std::max(per_sm, 1) : 0;
+        int per_flow = 0;
+        if (ctx->opt.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_flow, k_sweep_flow<3>, 256, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_flow, k_sweep_flow<2>, 256, 0);
+        ctx->flow_grid = per_flow * nsm;
     }
     {   // dynamic shared memory of the warp-staged sweep (may exceed the 48 KB default)
         int mx = 1;
@@ -1318,6 +1373,12 @@ gmg_status gmg_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out)
         enqueue_sweeps<3>(Lc, level, n_sweeps, rhs, nowout);
     }
     CK(cudaGetLastError());
+    {
+        int fe = 0;
+        CK(cudaMemcpyAsync(&fe, ctx->d_flag + 2, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (fe) { ctx->err = "dependency-driven sweep: progress wait timed out"; return GMG_ECUDA; }
+    }
     const int nv = ctx->opt.dim + 2;
     const int RD = ctx->opt.dim == 3 ? Rec<3>::DW : Rec<2>::DW;
     if (dW_out) {
@@ -1354,12 +1415,13 @@ static gmg_status build_graph(gmg_ctx *ctx)
 static gmg_status finish_history(gmg_ctx *ctx, int n_cycles, double *res_hist)
 {
     const int nv = ctx->opt.dim + 2;
-    int flags[2] = {0, 0};
-    CK(cudaMemcpyAsync(flags, ctx->d_flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int flags[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(flags, ctx->d_flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     if (res_hist)
         CK(cudaMemcpyAsync(res_hist, ctx->d_hist, sizeof(double) * nv * std::min(n_cycles + 1, ctx->hist_cap),
                            cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (flags[2]) { ctx->err = "dependency-driven sweep: progress wait timed out"; return GMG_ECUDA; }
     if (flags[1]) { ctx->err = "non-finite residual (level 0)"; return GMG_ENONFINITE; }
     return GMG_OK;
 }
@@ -1371,7 +1433,7 @@ gmg_status gmg_vcycle(gmg_ctx *ctx, int n_cycles, double *res_hist)
     if (st) return st;
     if (n_cycles < 0 || n_cycles + 1 > ctx->hist_cap) { ctx->err = "n_cycles out of range"; return GMG_EINVAL; }
     if (!ctx->graph) { st = build_graph(ctx); if (st) return st; }
-    CK(cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_flag, 0, 3 * sizeof(int), ctx->stream));
     for (int k = 0; k < n_cycles; ++k) CK(cudaGraphLaunch(ctx->graph, ctx->stream));
     Launcher Lc{ctx, ctx->stream};
     if (ctx->opt.dim == 2) enqueue_final_norm<2>(Lc);
@@ -1392,7 +1454,7 @@ gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_
     ctx->prof.bytes.clear();
     for (double &b : ctx->kbytes) b = 0;
     ctx->launches = 0;
-    CK(cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_flag, 0, 3 * sizeof(int), ctx->stream));
     Launcher Lc{ctx, ctx->stream};
     for (int k = 0; k < n_cycles; ++k) {
         if (ctx->opt.dim == 2) vcycle_dispatch<2>(Lc);

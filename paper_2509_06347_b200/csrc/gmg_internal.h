@@ -48,6 +48,10 @@ struct DomLevel {
     std::vector<int64_t> l2n;              // [n_loc] local -> natural
     std::vector<int64_t> blk;              // [ncolor+1] color blocks over owned cells
     std::vector<int64_t> nbnd;             // [ncolor] boundary cells (ghost neighbour) at the start of each block
+    // dependency-driven sweep (single domain): spatial chunks, (color, chunk) segments, chunk adjacency
+    int nchunk = 0;
+    std::vector<int64_t> seg;              // [ncolor][nchunk+1] first local cell of (color c, chunk x)
+    std::vector<int32_t> cnoff, cnidx;     // chunk -> neighbouring chunks (CSR, ascending, no self)
     std::vector<int64_t> fnat;             // [nf] natural ids of the local faces (ascending)
     std::vector<int32_t> fl, fr;           // [nf] local left / right, fr < 0: -(patch+1)
     std::vector<double> vol;               // [n_own]
@@ -101,6 +105,10 @@ struct DevLevel {
     const int *child;            // [2][n]
     const int *parent;           // [n]
     double *partial;             // [nblocks][nv] norm partials
+    // dependency-driven sweep
+    int nchunk;
+    const int *seg, *cnoff, *cnidx;   // [ncolor][nchunk+1], [nchunk+1], chunk neighbours
+    int *prog;                        // [nchunk] phases completed (zeroed before every smoothing step)
     // halo
     int n_send, n_recv;
     const int *send_idx, *recv_idx;
@@ -163,6 +171,9 @@ struct gmg_ctx {
     int adapt_lpc = 1;                // blocks that fit one wave at 2x lanes get up to 16 lanes per cell
     int skip_repeat = 1;              // drop the repeated same-color phase at every sweep turn (exact)
     int skip_zero = 1;                // first forward half-sweep: skip later-color neighbours (dW = +0, exact)
+    int flow = 0;                     // dependency-driven persistent sweep (single domain), GMG_FLOW
+    int flow_chunk = 512;             // cells per chunk, GMG_FLOW_CHUNK
+    int flow_grid = 0;                // resident CTAs of k_sweep_flow (set with the workspace)
     int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
     int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (no measured gain)
@@ -193,7 +204,7 @@ bool validate_coloring(const HostLevel &L, const std::vector<int32_t> &col);
 int64_t agglomerate(const HostLevel &L, double theta, std::vector<int64_t> &parent, int64_t &nc);
 void build_coarse(const HostLevel &fine, HostLevel &coarse);
 void renumber(HostLevel &L);
-void build_domain_level(const HostLevel &G, int rank, DomLevel &D);
+void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells = 0);
 void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, DomLevel &Dc);
 void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *part);
 }  // namespace gmg

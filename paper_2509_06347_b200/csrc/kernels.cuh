@@ -689,6 +689,281 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 }
 
 // ---------------------------------------------------------------------------
+// Dependency-driven sweep (single domain, GMG_FLOW): ONE persistent launch runs
+// every color phase of a smoothing step.  The cells are grouped into spatial
+// chunks; chunk x may run phase p once every neighbouring chunk has finished
+// phase p-1 (prog[y] >= p).  A chunk's cells of color(p) read only cells of
+// other colors, which by then hold exactly the increments of phases < p (a
+// neighbour cannot start phase p+1 before x has published p+1), so the result
+// is Algorithm 2's, without a grid-wide barrier (kernel boundary) between
+// phases.  Requires all CTAs resident (cooperative launch).  Records written
+// inside the launch are read with L2-coherent loads (.cg); progress is
+// published with st.release.gpu after a CTA barrier and observed with
+// ld.acquire.gpu.  A bounded wait reports a timeout in *err instead of hanging.
+// ---------------------------------------------------------------------------
+constexpr int kFlowMaxPh = 320;
+struct FlowArgs {
+    int nph, K, n_own;
+    const int *seg, *cnoff, *cnidx;
+    int *prog, *err;
+    unsigned short ph[kFlowMaxPh];   // color | last << 8 (write W) | first-forward << 9 (skip +0 terms)
+};
+
+__device__ __forceinline__ void ld4cg(const double *p, double *v)
+{
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ int ld_acquire(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v)
+{
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 4) k_sweep_flow(SweepArgs a, FlowArgs f)
+{
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    for (int p = 0; p < f.nph; ++p) {
+        const int code = f.ph[p];
+        const int c = code & 255;
+        double *Wout = (code >> 8 & 1) ? a.Wout : nullptr;
+        const int *sg = f.seg + (size_t)c * (f.K + 1);
+        const int zlo = (code >> 9 & 1) ? sg[f.K] : 0, zhi = (code >> 9 & 1) ? f.n_own : 0;
+        for (int x = blockIdx.x; x < f.K; x += gridDim.x) {
+            const int s0 = sg[x], s1 = sg[x + 1];
+            if (s1 > s0) {
+                if (p > 0) {
+                    for (int t = f.cnoff[x] + threadIdx.x; t < f.cnoff[x + 1]; t += blockDim.x) {
+                        const int y = f.cnidx[t];
+                        for (int spin = 0; ld_acquire(f.prog + y) < p; ++spin) {
+                            if (spin > (1 << 22) || *(volatile int *)f.err) {
+                                atomicExch(f.err, 1);
+                                s_bad = 1;
+                                break;
+                            }
+                            __nanosleep(64);
+                        }
+                    }
+                    __syncthreads();
+                    if (s_bad) return;
+                }
+                // lanes per cell: fill the CTA with the segment's cells
+                const int ncell = s1 - s0;
+                int L = 2;
+                while (L < 16 && ncell * L * 2 <= (int)blockDim.x) L *= 2;
+                const int cpi = blockDim.x / L;
+                for (int base = s0; base < s1; base += cpi) {
+                    const int i = base + threadIdx.x / L, sub = threadIdx.x % L;
+                    const bool valid = i < s1;
+                    double acc[NV];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+                    if (valid) {
+                        const int2 sd = __ldg(a.sinfo + i);
+                        const int e1 = sd.x + sd.y;
+                        for (int e = sd.x + sub; e < e1; e += L) {
+                            const int j = __ldg(a.sJe + e);
+                            if (j >= zlo && j < zhi) continue;
+                            double sr[4];
+                            ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                            const double *rj = a.rec + (size_t)j * RC::STRIDE;
+                            double w[NV], dw[NV];
+                            if constexpr (D == 3) {
+                                double c0[4], c1[4], c2[4];
+                                ld4cg(rj, c0);
+                                ld4cg(rj + 4, c1);
+                                ld4cg(rj + 8, c2);
+                                w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
+                                dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                            } else {
+                                ld4cg(rj, w);
+                                ld4cg(rj + 4, dw);
+                            }
+                            flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                        }
+                    }
+                    for (int o = L / 2; o > 0; o >>= 1) {
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                    }
+                    if (valid && sub == 0) {
+                        double *ri = a.rec + (size_t)i * RC::STRIDE;
+                        const size_t o = (size_t)i * NV;
+                        double r[NV], c1[4], c2[4];
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
+                        ld4cg(ri + 4, c1);
+                        ld4cg(ri + 8, c2);
+                        if constexpr (D == 3) {
+                            const double invD = c2[2], ha = c2[3];
+                            double d[NV];
+#pragma unroll
+                            for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+                            const double w1[4] = {c1[0], d[0], d[1], d[2]};
+                            st4(ri + 4, w1);
+                            c2[0] = d[3];
+                            c2[1] = d[4];
+                            st4(ri + 8, c2);
+                            if (Wout) {
+                                double c0[4];
+                                ld4cg(ri, c0);
+                                Wout[o + 0] = c0[0] + d[0];
+                                Wout[o + 1] = c0[1] + d[1];
+                                Wout[o + 2] = c0[2] + d[2];
+                                Wout[o + 3] = c0[3] + d[3];
+                                Wout[o + 4] = c1[0] + d[4];
+                            }
+                        } else {
+                            const double invD = c2[0], ha = c2[1];
+                            double d[4];
+#pragma unroll
+                            for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+                            st4(ri + 4, d);
+                            if (Wout) {
+                                double c0[4];
+                                ld4cg(ri, c0);
+#pragma unroll
+                                for (int q = 0; q < NV; ++q) Wout[o + q] = c0[q] + d[q];
+                            }
+                        }
+                    }
+                }
+                __syncthreads();   // every write of the segment before the release below
+            }
+            if (threadIdx.x == 0) st_release(f.prog + x, p + 1);
+        }
+    }
+}
+
+// warp-granular variant (GMG_FLOW=2): every WARP owns chunks and runs their
+// phases; no CTA barrier -- lanes wait with a warp vote, __syncwarp orders the
+// warp's record writes before lane 0's release
+template <int D>
+__global__ void __launch_bounds__(256, 4) k_sweep_flow_w(SweepArgs a, FlowArgs f)
+{
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    const int lane = threadIdx.x & 31;
+    const int worker = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nworker = gridDim.x * (blockDim.x >> 5);
+    for (int p = 0; p < f.nph; ++p) {
+        const int code = f.ph[p];
+        const int c = code & 255;
+        double *Wout = (code >> 8 & 1) ? a.Wout : nullptr;
+        const int *sg = f.seg + (size_t)c * (f.K + 1);
+        const int zlo = (code >> 9 & 1) ? sg[f.K] : 0, zhi = (code >> 9 & 1) ? f.n_own : 0;
+        for (int x = worker; x < f.K; x += nworker) {
+            const int s0 = sg[x], s1 = sg[x + 1];
+            if (s1 > s0) {
+                if (p > 0) {
+                    bool bad = false;
+                    for (int t = f.cnoff[x] + lane; t < f.cnoff[x + 1]; t += 32) {
+                        const int y = f.cnidx[t];
+                        for (int spin = 0; ld_acquire(f.prog + y) < p; ++spin) {
+                            if (spin > (1 << 22) || *(volatile int *)f.err) { atomicExch(f.err, 1); bad = true; break; }
+                            __nanosleep(32);
+                        }
+                    }
+                    if (__any_sync(0xffffffffu, bad)) return;
+                }
+                const int ncell = s1 - s0;
+                int L = 2;
+                while (L < 16 && ncell * L * 2 <= 32) L *= 2;
+                const int cpi = 32 / L;
+                for (int base = s0; base < s1; base += cpi) {
+                    const int i = base + lane / L, sub = lane % L;
+                    const bool valid = i < s1;
+                    double acc[NV];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+                    if (valid) {
+                        const int2 sd = __ldg(a.sinfo + i);
+                        const int e1 = sd.x + sd.y;
+                        for (int e = sd.x + sub; e < e1; e += L) {
+                            const int j = __ldg(a.sJe + e);
+                            if (j >= zlo && j < zhi) continue;
+                            double sr[4];
+                            ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                            const double *rj = a.rec + (size_t)j * RC::STRIDE;
+                            double w[NV], dw[NV];
+                            if constexpr (D == 3) {
+                                double c0[4], c1[4], c2[4];
+                                ld4cg(rj, c0);
+                                ld4cg(rj + 4, c1);
+                                ld4cg(rj + 8, c2);
+                                w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
+                                dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                            } else {
+                                ld4cg(rj, w);
+                                ld4cg(rj + 4, dw);
+                            }
+                            flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                        }
+                    }
+                    for (int o = L / 2; o > 0; o >>= 1) {
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                    }
+                    if (valid && sub == 0) {
+                        double *ri = a.rec + (size_t)i * RC::STRIDE;
+                        const size_t o = (size_t)i * NV;
+                        double r[NV], c1[4], c2[4];
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
+                        ld4cg(ri + 4, c1);
+                        ld4cg(ri + 8, c2);
+                        if constexpr (D == 3) {
+                            const double invD = c2[2], ha = c2[3];
+                            double d[NV];
+#pragma unroll
+                            for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+                            const double w1[4] = {c1[0], d[0], d[1], d[2]};
+                            st4(ri + 4, w1);
+                            c2[0] = d[3];
+                            c2[1] = d[4];
+                            st4(ri + 8, c2);
+                            if (Wout) {
+                                double c0[4];
+                                ld4cg(ri, c0);
+                                Wout[o + 0] = c0[0] + d[0];
+                                Wout[o + 1] = c0[1] + d[1];
+                                Wout[o + 2] = c0[2] + d[2];
+                                Wout[o + 3] = c0[3] + d[3];
+                                Wout[o + 4] = c1[0] + d[4];
+                            }
+                        } else {
+                            const double invD = c2[0], ha = c2[1];
+                            double d[4];
+#pragma unroll
+                            for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
+                            st4(ri + 4, d);
+                            if (Wout) {
+                                double c0[4];
+                                ld4cg(ri, c0);
+#pragma unroll
+                                for (int q = 0; q < NV; ++q) Wout[o + q] = c0[q] + d[q];
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) st_release(f.prog + x, p + 1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Tail sweep: consecutive TINY color phases of a smoothing step (e.g. the last
 // colors of a forward pass and the first ones of the next backward pass) run
 // in ONE single-CTA launch, one phase after the other with a block barrier in

@@ -405,7 +405,7 @@ void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *p
 //    with A = sigma S n oriented outward from the cell.
 //  * halo plan grouped (color, peer), natural id ascending within a group, so
 //    a sender's group equals the receiver's group element by element.
-void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
+void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells)
 {
     const int d = G.dim;
     const int64_t N = G.n;
@@ -436,6 +436,43 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D)
         auto b0 = D.l2n.begin() + D.blk[c], b1 = D.l2n.begin() + D.blk[c + 1];
         auto mid = std::stable_partition(b0, b1, [&](int64_t nat) { return bnd[nat] != 0; });
         D.nbnd[c] = (int64_t)(mid - b0);
+    }
+    // dependency-driven sweep (single domain): spatial chunks of ~chunk_cells
+    // cells (RCB of the centroids); inside each color block the cells are
+    // ordered (chunk, natural id), so (color c, chunk x) is a contiguous segment
+    D.nchunk = 0;
+    if (chunk_cells > 0 && N == D.n_own) {
+        const int K = (int)std::max<int64_t>(1, (N + chunk_cells - 1) / chunk_cells);
+        std::vector<int32_t> ch(N, 0);
+        partition_rcb(N, d, G.ctr.data(), K, ch.data());
+        for (int c = 0; c < G.ncolor; ++c)
+            std::stable_sort(D.l2n.begin() + D.blk[c], D.l2n.begin() + D.blk[c + 1],
+                             [&](int64_t a, int64_t b) { return ch[a] < ch[b]; });
+        D.nchunk = K;
+        D.seg.assign((size_t)G.ncolor * (K + 1), 0);
+        for (int c = 0; c < G.ncolor; ++c) {
+            int64_t *sg = D.seg.data() + (size_t)c * (K + 1);
+            std::vector<int64_t> cnt(K + 1, 0);
+            for (int64_t i = D.blk[c]; i < D.blk[c + 1]; ++i) cnt[ch[D.l2n[i]] + 1]++;
+            sg[0] = D.blk[c];
+            for (int x = 0; x < K; ++x) sg[x + 1] = sg[x] + cnt[x + 1];
+        }
+        std::vector<std::vector<int32_t>> adj(K);
+        for (int64_t f = 0; f < G.nf; ++f) {
+            const int64_t l = G.left[f], r = G.right[f];
+            if (r < 0 || ch[l] == ch[r]) continue;
+            adj[ch[l]].push_back(ch[r]);
+            adj[ch[r]].push_back(ch[l]);
+        }
+        D.cnoff.assign(K + 1, 0);
+        D.cnidx.clear();
+        for (int x = 0; x < K; ++x) {
+            auto &a = adj[x];
+            std::sort(a.begin(), a.end());
+            a.erase(std::unique(a.begin(), a.end()), a.end());
+            D.cnidx.insert(D.cnidx.end(), a.begin(), a.end());
+            D.cnoff[x + 1] = (int32_t)D.cnidx.size();
+        }
     }
     for (int64_t i = 0; i < D.n_own; ++i) n2l[D.l2n[i]] = (int32_t)i;
     std::vector<int64_t> ghosts;
