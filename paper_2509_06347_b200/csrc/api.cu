@@ -909,6 +909,8 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_SKIP_REPEAT")) ctx->skip_repeat = std::atoi(e);   // drop idempotent phases
     if (const char *e = std::getenv("GMG_SKIP_ZERO")) ctx->skip_zero = std::atoi(e);       // skip +0 neighbour terms
     if (const char *e = std::getenv("GMG_FLOW")) ctx->flow = std::atoi(e);                 // dependency-driven sweep
+    if (const char *e = std::getenv("GMG_CHUNK_ORDER")) ctx->chunk_order = std::atoi(e);   // (color, chunk, id) order
+    if (const char *e = std::getenv("GMG_ORDER_CHUNK")) ctx->order_chunk = std::max(8, std::atoi(e));
     if (const char *e = std::getenv("GMG_FLOW_CHUNK")) ctx->flow_chunk = std::max(32, std::atoi(e));
     *out = ctx;
     return GMG_OK;
@@ -1023,7 +1025,8 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             dm.lv.resize(ctx->lv.size());
             for (size_t l = 0; l < ctx->lv.size(); ++l) {
                 build_domain_level(ctx->lv[l], dm.rank, dm.lv[l],
-                                   (ctx->flow && ctx->nparts == 1) ? ctx->flow_chunk : 0);
+                                   ctx->nparts != 1 ? 0 : ctx->flow ? ctx->flow_chunk : ctx->chunk_order ? ctx->order_chunk : 0,
+                                   ctx->flow != 0);
                 lap("domain_level", (int)l);
             }
             for (size_t l = 0; l + 1 < ctx->lv.size(); ++l)

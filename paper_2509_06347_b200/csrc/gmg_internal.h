@@ -173,6 +173,8 @@ struct gmg_ctx {
     int skip_zero = 1;                // first forward half-sweep: skip later-color neighbours (dW = +0, exact)
     int flow = 0;                     // dependency-driven persistent sweep (single domain), GMG_FLOW
     int flow_chunk = 512;             // cells per chunk, GMG_FLOW_CHUNK
+    int chunk_order = 1;              // order cells inside color blocks by spatial RCB chunk (GMG_CHUNK_ORDER)
+    int order_chunk = 128;            // cells per ordering chunk without GMG_FLOW (GMG_ORDER_CHUNK)
     int flow_grid = 0;                // resident CTAs of k_sweep_flow (set with the workspace)
     int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
@@ -204,7 +206,7 @@ bool validate_coloring(const HostLevel &L, const std::vector<int32_t> &col);
 int64_t agglomerate(const HostLevel &L, double theta, std::vector<int64_t> &parent, int64_t &nc);
 void build_coarse(const HostLevel &fine, HostLevel &coarse);
 void renumber(HostLevel &L);
-void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells = 0);
+void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells = 0, bool flow = false);
 void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, DomLevel &Dc);
 void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *part);
 }  // namespace gmg

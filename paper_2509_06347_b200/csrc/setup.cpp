@@ -405,7 +405,7 @@ void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *p
 //    with A = sigma S n oriented outward from the cell.
 //  * halo plan grouped (color, peer), natural id ascending within a group, so
 //    a sender's group equals the receiver's group element by element.
-void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells)
+void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells, bool flow)
 {
     const int d = G.dim;
     const int64_t N = G.n;
@@ -437,17 +437,58 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
         auto mid = std::stable_partition(b0, b1, [&](int64_t nat) { return bnd[nat] != 0; });
         D.nbnd[c] = (int64_t)(mid - b0);
     }
-    // dependency-driven sweep (single domain): spatial chunks of ~chunk_cells
-    // cells (RCB of the centroids); inside each color block the cells are
-    // ordered (chunk, natural id), so (color c, chunk x) is a contiguous segment
+    // single domain: spatial chunks of ~chunk_cells cells (RCB of the
+    // centroids); inside each color block the cells are ordered (chunk,
+    // natural id) -- neighbours of consecutive cells are then close in memory
+    // (better L2 reuse of the gathered records, DESIGN.md §6 v13) -- and for
+    // the dependency-driven sweep (color c, chunk x) is a contiguous segment
     D.nchunk = 0;
-    if (chunk_cells > 0 && N == D.n_own) {
+    if (chunk_cells > 0 && N == D.n_own && !flow) {
+        // Morton (Z-order) key of the centroid: the same spatial grouping as
+        // fine RCB chunks at a fraction of the setup cost
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        for (int k = 0; k < d; ++k)
+            for (int64_t i = 0; i < N; ++i) {
+                lo[k] = std::min(lo[k], G.ctr[(size_t)k * N + i]);
+                hi[k] = std::max(hi[k], G.ctr[(size_t)k * N + i]);
+            }
+        const int bits = d == 3 ? 21 : 31;
+        const double scale = (double)((1u << bits) - 1);
+        auto spread = [&](uint64_t v) {
+            uint64_t r = 0;
+            for (int b = 0; b < bits; ++b) r |= ((v >> b) & 1ull) << (b * d);
+            return r;
+        };
+        std::vector<uint64_t> key(N);
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < N; ++i) {
+            uint64_t code = 0;
+            for (int k = 0; k < d; ++k) {
+                const double ext = hi[k] > lo[k] ? hi[k] - lo[k] : 1.0;
+                const uint64_t q = (uint64_t)((G.ctr[(size_t)k * N + i] - lo[k]) / ext * scale);
+                code |= spread(q) << k;
+            }
+            key[i] = code;
+        }
+        for (int c = 0; c < G.ncolor; ++c)
+            std::sort(D.l2n.begin() + D.blk[c], D.l2n.begin() + D.blk[c + 1],
+                      [&](int64_t a, int64_t b) { return key[a] < key[b] || (key[a] == key[b] && a < b); });
+    }
+    if (chunk_cells > 0 && N == D.n_own && flow) {
         const int K = (int)std::max<int64_t>(1, (N + chunk_cells - 1) / chunk_cells);
         std::vector<int32_t> ch(N, 0);
         partition_rcb(N, d, G.ctr.data(), K, ch.data());
-        for (int c = 0; c < G.ncolor; ++c)
-            std::stable_sort(D.l2n.begin() + D.blk[c], D.l2n.begin() + D.blk[c + 1],
-                             [&](int64_t a, int64_t b) { return ch[a] < ch[b]; });
+        {   // stable counting sort of every color block by chunk
+            std::vector<int64_t> cnt(K + 1), out;
+            for (int c = 0; c < G.ncolor; ++c) {
+                std::fill(cnt.begin(), cnt.end(), 0);
+                for (int64_t i = D.blk[c]; i < D.blk[c + 1]; ++i) cnt[ch[D.l2n[i]] + 1]++;
+                std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
+                out.resize(D.blk[c + 1] - D.blk[c]);
+                for (int64_t i = D.blk[c]; i < D.blk[c + 1]; ++i) out[cnt[ch[D.l2n[i]]]++] = D.l2n[i];
+                std::copy(out.begin(), out.end(), D.l2n.begin() + D.blk[c]);
+            }
+        }
         D.nchunk = K;
         D.seg.assign((size_t)G.ncolor * (K + 1), 0);
         for (int c = 0; c < G.ncolor; ++c) {
