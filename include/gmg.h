@@ -222,6 +222,29 @@ gmg_status gmg_get_halo(gmg_ctx *ctx, int level, int dom, int64_t *n_owned, int6
                         int64_t *n_send, int64_t *n_recv, int64_t *owned, int64_t *ghost, int32_t *peers,
                         int64_t *send_nat, int64_t *send_off, int64_t *recv_nat, int64_t *recv_off);
 
+/* NEXT-3, fused P2P halo between ranks (environment GMG_P2P=1, nranks > 1;
+ * SURVEY §8(f)).  The sweep that computes a boundary cell's increment stores
+ * it straight into the ghost record on every peer GPU that holds a copy
+ * (NVLink peer memory) and publishes its phase count into the peer's flags --
+ * no pack / ncclSend / ncclRecv / unpack per color.  Setup, after
+ * gmg_set_workspace on every rank:
+ *   gmg_p2p_layout(ctx, out): out[0 .. n_levels-1] = byte offsets of this
+ *     rank's record arrays inside its workspace, out[n_levels] = offset of its
+ *     flag array; (n_levels + 1) int64.
+ *   gmg_p2p_import(ctx, handles, base_off, layouts): for every rank r
+ *     (nranks entries; this rank's own entry is ignored): handles + 64 r = its
+ *     cudaIpcMemHandle_t of the allocation holding its workspace, base_off[r]
+ *     = byte offset of that workspace inside the allocation, layouts +
+ *     (n_levels + 1) r = its gmg_p2p_layout output.  Opens the peers'
+ *     allocations (cudaIpcOpenMemHandle) and stores their record / flag
+ *     addresses; GMG_ECUDA if a peer cannot be mapped.  Until it succeeds the
+ *     NCCL exchange is used.  The binding (gmg.Solver) does this exchange with
+ *     torch.distributed.all_gather_object.  (Untested in this build on more
+ *     than one GPU; the same kernels run between the local domains of one
+ *     process -- tests/test_gpu_partitioned.py.) */
+gmg_status gmg_p2p_layout(gmg_ctx *ctx, int64_t *out);
+gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base_off, const int64_t *layouts);
+
 const char *gmg_last_error(gmg_ctx *ctx); /* valid until the next call on ctx */
 void gmg_destroy(gmg_ctx *ctx);
 

@@ -463,6 +463,40 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
     Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
 }
 
+// one color phase with the fused P2P halo on every domain (an empty phase,
+// c < 0, is a pure synchronisation point that advances the phase count)
+template <int D>
+void enqueue_p2p_phase(Launcher &Lc, int l, int c, bool last, bool ff, std::function<const double *(DevLevel &)> rhs,
+                       std::function<double *(DevLevel &)> wout)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    for (Domain &dm : ctx->dom) {
+        DevLevel &L = dm.dv[l];
+        const DomLevel &H = dm.lv[l];
+        const int b0 = c < 0 ? 0 : (int)H.blk[c], b1 = c < 0 ? 0 : (int)H.blk[c + 1];
+        const bool z = c >= 0 && ff && ctx->skip_zero;
+        SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs(L),
+                    last ? wout(L) : nullptr, z ? (int)H.blk[c + 1] : 0, z ? (int)H.n_own : 0};
+        P2PArgs p{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_rec, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
+        int lpc = ctx->lpc;
+        const int64_t cells = b1 - b0;
+        if (ctx->adapt_lpc && g_sweep_grid_cap > 0)
+            while (lpc < 16 && cells * lpc * 2 <= (int64_t)g_sweep_grid_cap * 256) lpc *= 2;
+        int nb = nblk(cells * lpc);
+        if (g_sweep_grid_cap > 0) nb = std::min(nb, g_sweep_grid_cap);
+        const dim3 g(std::max(nb, 1)), b(256);
+        Lc.pre(GMG_K_SWEEP);
+        switch (lpc) {
+            case 1: k_sweep_p2p<D, 1><<<g, b, 0, Lc.s>>>(a, p); break;
+            case 4: k_sweep_p2p<D, 4><<<g, b, 0, Lc.s>>>(a, p); break;
+            case 8: k_sweep_p2p<D, 8><<<g, b, 0, Lc.s>>>(a, p); break;
+            case 16: k_sweep_p2p<D, 16><<<g, b, 0, Lc.s>>>(a, p); break;
+            default: k_sweep_p2p<D, 2><<<g, b, 0, Lc.s>>>(a, p); break;
+        }
+        Lc.post(GMG_K_SWEEP, c < 0 ? 0.0 : dm.lbytes[l].sweep[c] + (last ? dm.lbytes[l].sweep_out[c] : 0.0));
+    }
+}
+
 // n_sweeps x (forward colors 1..Nc, backward Nc..1), Algorithm 2;
 // after every color its increments go to the ranks/domains that ghost them.
 // The record's W_lin is the linearisation state; the last backward pass also
@@ -489,6 +523,15 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
                 if (ctx->skip_repeat && !seq.empty() && seq.back().c == ph.c) seq.back().last |= ph.last;
                 else seq.push_back(ph);
             }
+    // fused P2P halo: increments go to the ghosts from the sweep epilogue; a
+    // synchronisation phase before (the ghosts' local zeroing is done) and
+    // after (the peers' last increments have landed) the step
+    if (ctx->p2p && ctx->p2p_ready && ctx->nparts > 1) {
+        enqueue_p2p_phase<D>(Lc, l, -1, false, false, rhs, wout);
+        for (const Ph &ph : seq) enqueue_p2p_phase<D>(Lc, l, ph.c, ph.last, ph.ff, rhs, wout);
+        enqueue_p2p_phase<D>(Lc, l, -1, false, false, rhs, wout);
+        return;
+    }
     // dependency-driven persistent sweep: one launch for the whole smoothing step
     if (ctx->flow && ctx->flow_grid > 0 && ctx->nparts == 1 && ctx->dom.size() == 1 && ctx->dom[0].dv[l].nchunk > 0 &&
         (int)seq.size() <= kFlowMaxPh && !ctx->pipe && !ctx->spsweep && !ctx->wsweep) {
@@ -733,12 +776,16 @@ void carve(gmg_ctx *ctx, Bump &b)
     for (const HostLevel &G : ctx->lv) nmax = std::max(nmax, G.n);
     for (Domain &dm : ctx->dom) {
         dm.dv.assign(nl, DevLevel{});
+        int *flags = b.take<int>(std::max(ctx->nparts, 1));   // P2P phase counts published by the peers
+        int *ctl = b.take<int>(4);
         for (int l = 0; l < nl; ++l) {
             const HostLevel &G = ctx->lv[l];
             const DomLevel &H = dm.lv[l];
             DevLevel &L = dm.dv[l];
             const int64_t n = H.n_own, nloc = H.n_loc, nf = H.nf;
             L.dim = d; L.nv = nv; L.ncolor = G.ncolor;
+            L.p2p_flags = flags;
+            L.p2p_ctl = ctl;
             L.n = (int)n; L.n_loc = (int)nloc; L.nf = (int)nf;
             L.fl = b.take<int>(nf); L.fr = b.take<int>(nf);
             L.fA = b.take<double>((size_t)d * nf); L.fM = b.take<int8_t>(nf);
@@ -756,6 +803,13 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.spcell = b.take<int>(H.sp_cell.size());
             L.sinfo = b.take<int2>(n);
             L.fslot = b.take<int2>(nf);
+            L.npeer = (int)H.peers.size();
+            L.p2p_off = b.take<int>(H.p2p_off.size());
+            L.p2p_k = b.take<int>(H.p2p_k.size());
+            L.p2p_g = b.take<int>(H.p2p_g.size());
+            L.peer_rec = b.take<double *>(H.peers.size());
+            L.p2p_sig = b.take<int *>(H.peers.size());
+            L.p2p_wait = b.take<int>(H.peers.size());
             L.nchunk = H.nchunk;
             L.seg = b.take<int>(H.seg.size());
             L.cnoff = b.take<int>(H.cnoff.size());
@@ -909,6 +963,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_SKIP_REPEAT")) ctx->skip_repeat = std::atoi(e);   // drop idempotent phases
     if (const char *e = std::getenv("GMG_SKIP_ZERO")) ctx->skip_zero = std::atoi(e);       // skip +0 neighbour terms
     if (const char *e = std::getenv("GMG_FLOW")) ctx->flow = std::atoi(e);                 // dependency-driven sweep
+    if (const char *e = std::getenv("GMG_P2P")) ctx->p2p = std::atoi(e);                   // fused P2P halo
     if (const char *e = std::getenv("GMG_CHUNK_ORDER")) ctx->chunk_order = std::atoi(e);   // (color, chunk, id) order
     if (const char *e = std::getenv("GMG_ORDER_CHUNK")) ctx->order_chunk = std::max(8, std::atoi(e));
     if (const char *e = std::getenv("GMG_FLOW_CHUNK")) ctx->flow_chunk = std::max(32, std::atoi(e));
@@ -1037,6 +1092,25 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
                              (long long)sst.color_levels, (long long)sst.color_rounds, (long long)sst.match_rounds);
             ctx->dom.push_back(std::move(dm));
         }
+        if (ctx->p2p && ctx->nparts > 1) {   // fused P2P halo targets
+            for (Domain &dm : ctx->dom)
+                for (size_t l = 0; l < ctx->lv.size(); ++l) {
+                    DomLevel &D = dm.lv[l];
+                    std::vector<DomLevel> tmp(D.peers.size());
+                    std::vector<const DomLevel *> pd(D.peers.size());
+                    for (size_t k = 0; k < D.peers.size(); ++k) {
+                        const int q = D.peers[k];
+                        if (ctx->opt.nranks > 1) {
+                            build_domain_level(ctx->lv[l], q, tmp[k]);
+                            pd[k] = &tmp[k];
+                        } else {
+                            pd[k] = &ctx->dom[q].lv[l];
+                        }
+                    }
+                    build_p2p_targets(D, dm.rank, ctx->lv[l].ncolor, pd);
+                }
+            lap("p2p_targets", 0);
+        }
     } catch (const std::exception &e) {
         ctx->err = e.what();
         return GMG_ETOPO;
@@ -1151,6 +1225,10 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.ecell, H.ell_cell.data(), H.ell_cell.size() * sizeof(int)));
             CK(up_raw(L.spcell, H.sp_cell.data(), H.sp_cell.size() * sizeof(int)));
             CK(up_raw(L.fslot, H.fslot.data(), H.fslot.size() * sizeof(int)));
+            CK(up_raw(L.p2p_off, H.p2p_off.data(), H.p2p_off.size() * sizeof(int)));
+            CK(up_raw(L.p2p_k, H.p2p_k.data(), H.p2p_k.size() * sizeof(int)));
+            CK(up_raw(L.p2p_g, H.p2p_g.data(), H.p2p_g.size() * sizeof(int)));
+            CK(up_raw(L.p2p_wait, H.peers.data(), H.peers.size() * sizeof(int)));
             if (H.nchunk) {
                 std::vector<int> sg(H.seg.begin(), H.seg.end());
                 CK(up_i(L.seg, std::move(sg)));
@@ -1186,6 +1264,30 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         }
     }
     CK(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), ctx->stream));
+    for (Domain &dm : ctx->dom) {   // P2P phase counts / control
+        CK(cudaMemsetAsync(dm.dv[0].p2p_flags, 0, sizeof(int) * std::max(ctx->nparts, 1), ctx->stream));
+        CK(cudaMemsetAsync(dm.dv[0].p2p_ctl, 0, sizeof(int) * 4, ctx->stream));
+    }
+    ctx->p2p_ready = false;
+    if (ctx->p2p && ctx->nparts > 1 && ctx->opt.nranks == 1) {   // local domains: peers are in this process
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (Domain &dm : ctx->dom)
+            for (int l = 0; l < nl; ++l) {
+                const DomLevel &H = dm.lv[l];
+                std::vector<double *> pr(H.peers.size());
+                std::vector<int *> sg(H.peers.size());
+                for (size_t k = 0; k < H.peers.size(); ++k) {
+                    DevLevel &Q = ctx->dom[H.peers[k]].dv[l];
+                    pr[k] = Q.rec;
+                    sg[k] = Q.p2p_flags + dm.rank;
+                }
+                if (!pr.empty()) {
+                    CK(cudaMemcpy(dm.dv[l].peer_rec, pr.data(), pr.size() * sizeof(double *), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(dm.dv[l].p2p_sig, sg.data(), sg.size() * sizeof(int *), cudaMemcpyHostToDevice));
+                }
+            }
+        ctx->p2p_ready = true;
+    }
     if (ctx->nparts > 1 && !ctx->side) {   // side stream + events of the exchange overlap
         CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
@@ -1425,6 +1527,13 @@ static gmg_status finish_history(gmg_ctx *ctx, int n_cycles, double *res_hist)
                            cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (flags[2]) { ctx->err = "dependency-driven sweep: progress wait timed out"; return GMG_ECUDA; }
+    if (ctx->p2p) {
+        for (Domain &dm : ctx->dom) {
+            int c2 = 0;
+            CK(cudaMemcpy(&c2, dm.dv[0].p2p_ctl + 2, sizeof(int), cudaMemcpyDeviceToHost));
+            if (c2) { ctx->err = "P2P halo: peer phase wait timed out"; return GMG_ECUDA; }
+        }
+    }
     if (flags[1]) { ctx->err = "non-finite residual (level 0)"; return GMG_ENONFINITE; }
     return GMG_OK;
 }
@@ -1549,6 +1658,60 @@ gmg_status gmg_partition_rcb(int64_t n_cells, int dim, const double *centroid, i
     return GMG_OK;
 }
 
+gmg_status gmg_p2p_layout(gmg_ctx *ctx, int64_t *out)
+{
+    if (!ctx || !out) return GMG_EINVAL;
+    if (!ctx->ws_ready && !ctx->ws) { ctx->err = "workspace not set"; return GMG_ESTATE; }
+    const int nl = (int)ctx->lv.size();
+    const Domain &dm = ctx->dom[0];
+    for (int l = 0; l < nl; ++l) out[l] = (int64_t)((const char *)dm.dv[l].rec - (const char *)ctx->ws);
+    out[nl] = (int64_t)((const char *)dm.dv[0].p2p_flags - (const char *)ctx->ws);
+    return GMG_OK;
+}
+
+gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base_off, const int64_t *layouts)
+{
+    if (!ctx || !handles || !base_off || !layouts) return GMG_EINVAL;
+    if (!ctx->ws) { ctx->err = "workspace not set"; return GMG_ESTATE; }
+    if (ctx->opt.nranks < 2 || !ctx->p2p) { ctx->err = "P2P import needs nranks > 1 and GMG_P2P=1"; return GMG_ESTATE; }
+    CK(cudaSetDevice(ctx->opt.device));
+    const int nl = (int)ctx->lv.size(), me = ctx->opt.rank;
+    Domain &dm = ctx->dom[0];
+    std::vector<char *> base(ctx->opt.nranks, nullptr);
+    for (int l = 0; l < nl; ++l)
+        for (int q : dm.lv[l].peers) {
+            if (base[q]) continue;
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, (const char *)handles + 64 * (size_t)q, sizeof(h));
+            void *p = nullptr;
+            const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                ctx->err = std::string("cudaIpcOpenMemHandle (rank ") + std::to_string(q) + "): " + cudaGetErrorString(e);
+                return GMG_ECUDA;
+            }
+            ctx->p2p_opened.push_back(p);
+            base[q] = (char *)p + base_off[q];
+        }
+    for (int l = 0; l < nl; ++l) {
+        const DomLevel &H = dm.lv[l];
+        std::vector<double *> pr(H.peers.size());
+        std::vector<int *> sg(H.peers.size());
+        for (size_t k = 0; k < H.peers.size(); ++k) {
+            const int q = H.peers[k];
+            const int64_t *lay = layouts + (size_t)q * (nl + 1);
+            pr[k] = (double *)(base[q] + lay[l]);
+            sg[k] = (int *)(base[q] + lay[nl]) + me;
+        }
+        if (!pr.empty()) {
+            CK(cudaMemcpy(dm.dv[l].peer_rec, pr.data(), pr.size() * sizeof(double *), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dm.dv[l].p2p_sig, sg.data(), sg.size() * sizeof(int *), cudaMemcpyHostToDevice));
+        }
+    }
+    ctx->p2p_ready = true;
+    if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+    return GMG_OK;
+}
+
 gmg_status gmg_get_halo(gmg_ctx *ctx, int level, int dom, int64_t *n_owned, int64_t *n_ghost, int *n_peers,
                         int64_t *n_send, int64_t *n_recv, int64_t *owned, int64_t *ghost, int32_t *peers,
                         int64_t *send_nat, int64_t *send_off, int64_t *recv_nat, int64_t *recv_off)
@@ -1587,6 +1750,7 @@ void gmg_destroy(gmg_ctx *ctx)
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy((ncclComm_t)ctx->nccl_comm);
+    for (void *p : ctx->p2p_opened) cudaIpcCloseMemHandle(p);
     delete ctx;
 }
 

@@ -75,6 +75,8 @@ struct DomLevel {
     std::vector<int> peers;                // peer ranks, ascending
     std::vector<int32_t> send_idx, recv_idx;   // local cells (owned / ghost)
     std::vector<int64_t> send_off, recv_off;   // [ncolor*npeers + 1]
+    // fused P2P halo: per owned cell, the ghost copies it must update (peer slot, peer-local ghost index)
+    std::vector<int32_t> p2p_off, p2p_k, p2p_g;
 };
 
 struct DevLevel {
@@ -109,6 +111,13 @@ struct DevLevel {
     int nchunk;
     const int *seg, *cnoff, *cnidx;   // [ncolor][nchunk+1], [nchunk+1], chunk neighbours
     int *prog;                        // [nchunk] phases completed (zeroed before every smoothing step)
+    // fused P2P halo (GMG_P2P)
+    const int *p2p_off, *p2p_k, *p2p_g;
+    double **peer_rec;                // [npeer] peers' record arrays (this level)
+    int **p2p_sig;                    // [npeer] &peer.flags[my rank]
+    int *p2p_wait;                    // [npeer] peer ranks
+    int *p2p_flags, *p2p_ctl;         // per domain: [nparts] published phase counts, [4] control
+    int npeer;
     // halo
     int n_send, n_recv;
     const int *send_idx, *recv_idx;
@@ -173,6 +182,9 @@ struct gmg_ctx {
     int skip_zero = 1;                // first forward half-sweep: skip later-color neighbours (dW = +0, exact)
     int flow = 0;                     // dependency-driven persistent sweep (single domain), GMG_FLOW
     int flow_chunk = 512;             // cells per chunk, GMG_FLOW_CHUNK
+    int p2p = 0;                      // fused P2P halo instead of pack / transport / unpack per color (GMG_P2P)
+    bool p2p_ready = false;           // peer pointers known (local domains: at workspace; ranks: after import)
+    std::vector<void *> p2p_opened;   // IPC mappings of the peers' workspaces (ranks)
     int chunk_order = 1;              // order cells inside color blocks by spatial RCB chunk (GMG_CHUNK_ORDER)
     int order_chunk = 128;            // cells per ordering chunk without GMG_FLOW (GMG_ORDER_CHUNK)
     int flow_grid = 0;                // resident CTAs of k_sweep_flow (set with the workspace)
@@ -208,5 +220,6 @@ void build_coarse(const HostLevel &fine, HostLevel &coarse);
 void renumber(HostLevel &L);
 void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells = 0, bool flow = false);
 void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, DomLevel &Dc);
+void build_p2p_targets(DomLevel &D, int me, int ncolor, const std::vector<const DomLevel *> &peer_dom);
 void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *part);
 }  // namespace gmg

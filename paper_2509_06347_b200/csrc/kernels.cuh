@@ -567,8 +567,41 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, int i, const do
 //  1 = dW0..2 written as the whole 32-B chunk (W4 | dW0..2), no partial sector
 //  2 = neighbour index of the next slot loaded one iteration ahead
 //  4 = own record tail + rhs prefetched to L1 before the slot loop
-template <int D>
-__device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, const double *acc)
+// Fused halo (GMG_P2P): the sweep that computes a boundary cell's increment
+// also stores it straight into the ghost record of every rank (domain) that
+// ghosts the cell, over peer memory (NVLink P2P between GPUs; plain device
+// memory between the domains of one process).  Ordering between phases:
+// every rank counts its completed color phases (ctl[0]); the last block of a
+// sweep launch fences the increments system-wide and publishes the new count
+// into each peer's flags[my rank] (st.release.sys); the next launch waits
+// until every peer's count has reached its own (ld.acquire.sys) -- so a peer
+// never reads a ghost before its phase's increments landed, and never
+// overwrites one that is still being read (each side waits for the other).
+struct P2PArgs {
+    const int *off, *k, *g;      // per owned cell: remote targets (peer slot, ghost local index), CSR
+    double *const *peer_rec;     // [peer slot] the peer's record array on this level
+    int np;                      // peers on this level (0: count phases only)
+    const int *wait_rank;        // [np] their ranks
+    int *const *sig;             // [np] &peer.flags[my rank]
+    const int *flags;            // [nranks] phase counts published by the peers
+    int *ctl;                    // [0] phases completed, [1] blocks done, [2] wait timeout
+};
+
+template <int D, bool P2P = false>
+__device__ __forceinline__ void p2p_store(const P2PArgs &p, int i, const double *d)
+{
+    if constexpr (P2P) {
+        for (int m = p.off[i]; m < p.off[i + 1]; ++m) {
+            double *r = p.peer_rec[p.k[m]] + (size_t)p.g[m] * Rec<D>::STRIDE + Rec<D>::DW;
+#pragma unroll
+            for (int q = 0; q < D + 2; ++q) r[q] = d[q];
+        }
+    }
+}
+
+template <int D, bool P2P = false>
+__device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, const double *acc,
+                                                  const P2PArgs &p = P2PArgs{})
 {
     constexpr int NV = D + 2;
     double *ri = a.rec + (size_t)i * Rec<D>::STRIDE;
@@ -588,6 +621,7 @@ __device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, con
         c2[0] = d[3];
         c2[1] = d[4];
         st4(ri + 8, c2);
+        p2p_store<D, P2P>(p, i, d);
         if (a.Wout) {
             double c0[4];
             ld4nc(ri, c0);
@@ -603,6 +637,7 @@ __device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, con
 #pragma unroll
         for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
         st4(ri + 4, d);
+        p2p_store<D, P2P>(p, i, d);
         if (a.Wout) {
             double c0[4];
             ld4nc(ri, c0);
@@ -612,10 +647,9 @@ __device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, con
     }
 }
 
-template <int D, int LPC, int MINB, int VAR = 3>
-__global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
+template <int D, int LPC, int VAR, bool P2P>
+__device__ __forceinline__ void sweep_body(const SweepArgs &a, const P2PArgs &p)
 {
-    pdl_enter();
     constexpr int NV = D + 2;
     using RC = Rec<D>;
     // grid-stride over the color's cells: a launch sized to exactly the
@@ -682,9 +716,62 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
         }
     }
     if (valid && sub == 0) {
-        if constexpr ((VAR & 1) != 0) sweep_finish_full<D>(a, i, acc);
+        if constexpr ((VAR & 1) != 0 || P2P) sweep_finish_full<D, P2P>(a, i, acc, p);
         else sweep_finish<D>(a, i, acc);
     }
+    }
+}
+
+template <int D, int LPC, int MINB, int VAR = 3>
+__global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
+{
+    pdl_enter();
+    sweep_body<D, LPC, VAR, false>(a, P2PArgs{});
+}
+
+__device__ __forceinline__ int ld_acquire_sys(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(int *p, int v)
+{
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// the sweep with the fused halo (see P2PArgs).  Launched for every phase on
+// every rank, also with no cells, so that all phase counts advance together.
+template <int D, int LPC>
+__global__ void __launch_bounds__(256, 4) k_sweep_p2p(SweepArgs a, P2PArgs p)
+{
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) {
+        s_bad = 0;
+        const int target = *(volatile int *)p.ctl;       // phases this rank completed
+        for (int t = 0; t < p.np && !s_bad; ++t) {
+            for (int spin = 0; ld_acquire_sys(p.flags + p.wait_rank[t]) < target; ++spin) {
+                if (spin > (1 << 24) || *(volatile int *)(p.ctl + 2)) { atomicExch(p.ctl + 2, 1); s_bad = 1; break; }
+                __nanosleep(64);
+            }
+        }
+    }
+    __syncthreads();
+    if (!s_bad) sweep_body<D, LPC, 3, true>(a, p);
+    // publish: every block orders its peer stores before its arrival on the
+    // done counter (gpu scope); the last block to arrive -- which has observed
+    // all arrivals -- fences at system scope and releases the new phase count
+    // to the peers, so by cumulativity every block's stores precede the flag
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (atomicAdd(p.ctl + 1, 1) == (int)gridDim.x - 1) {
+            p.ctl[1] = 0;
+            const int ph = p.ctl[0] + 1;
+            p.ctl[0] = ph;
+            __threadfence_system();
+            for (int t = 0; t < p.np; ++t) st_release_sys(p.sig[t], ph);
+        }
     }
 }
 

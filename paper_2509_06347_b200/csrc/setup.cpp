@@ -704,6 +704,35 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
     }
 }
 
+// fused P2P halo: for every send entry (color c, peer k, position t) the
+// receiving rank's ghost at the same position of ITS group (c, my rank) --
+// the groups are element-wise identical (natural id ascending) by construction
+void build_p2p_targets(DomLevel &D, int me, int ncolor, const std::vector<const DomLevel *> &peer_dom)
+{
+    const int np = (int)D.peers.size();
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> tg(D.n_own);
+    for (int k = 0; k < np; ++k) {
+        const DomLevel &Q = *peer_dom[k];
+        const int npq = (int)Q.peers.size();
+        const int kq = (int)(std::lower_bound(Q.peers.begin(), Q.peers.end(), me) - Q.peers.begin());
+        if (kq >= npq || Q.peers[kq] != me) throw std::runtime_error("p2p: asymmetric halo plan");
+        for (int c = 0; c < ncolor; ++c) {
+            const int64_t s0 = D.send_off[(size_t)c * np + k], s1 = D.send_off[(size_t)c * np + k + 1];
+            const int64_t r0 = Q.recv_off[(size_t)c * npq + kq], r1 = Q.recv_off[(size_t)c * npq + kq + 1];
+            if (s1 - s0 != r1 - r0) throw std::runtime_error("p2p: halo group size mismatch");
+            for (int64_t t = 0; t < s1 - s0; ++t)
+                tg[D.send_idx[s0 + t]].push_back({(int32_t)k, Q.recv_idx[r0 + t]});
+        }
+    }
+    D.p2p_off.assign(D.n_own + 1, 0);
+    D.p2p_k.clear();
+    D.p2p_g.clear();
+    for (int64_t i = 0; i < D.n_own; ++i) {
+        for (const auto &e : tg[i]) { D.p2p_k.push_back(e.first); D.p2p_g.push_back(e.second); }
+        D.p2p_off[i + 1] = (int32_t)D.p2p_k.size();
+    }
+}
+
 // fine <-> coarse links inside one domain (agglomeration never crosses a
 // partition face, so both ends are owned by the same rank)
 void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, DomLevel &Dc)

@@ -29,8 +29,8 @@ ABI_SYMBOLS = ["gmg_default_options", "gmg_create", "gmg_load_mesh", "gmg_set_co
                "gmg_get_level_info", "gmg_get_maps", "gmg_get_level_geometry", "gmg_workspace_bytes",
                "gmg_set_workspace", "gmg_set_state", "gmg_set_level_state", "gmg_get_state", "gmg_set_alpha",
                "gmg_residual", "gmg_set_level_inputs", "gmg_smooth", "gmg_vcycle", "gmg_profile_vcycle",
-               "gmg_time_smooth", "gmg_vcycle_launches", "gmg_partition_rcb", "gmg_get_halo", "gmg_last_error",
-               "gmg_destroy"]
+               "gmg_time_smooth", "gmg_vcycle_launches", "gmg_partition_rcb", "gmg_get_halo", "gmg_p2p_layout",
+               "gmg_p2p_import", "gmg_last_error", "gmg_destroy"]
 
 
 class GmgError(RuntimeError):
@@ -84,6 +84,8 @@ def lib():
             "gmg_vcycle_launches": (I64, [P]),
             "gmg_partition_rcb": (I, [I64, I, P, I, P]),
             "gmg_get_halo": (I, [P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
+            "gmg_p2p_layout": (I, [P, P]),
+            "gmg_p2p_import": (I, [P, P, P, P]),
             "gmg_last_error": (C.c_char_p, [P]),
             "gmg_destroy": (None, [P]),
         }
@@ -271,6 +273,21 @@ def gmg_get_halo(ctx, level, dom=0):
     return out
 
 
+def gmg_p2p_layout(ctx, n_levels):
+    out = np.zeros(n_levels + 1, np.int64)
+    _check(ctx, lib().gmg_p2p_layout(ctx, _ptr(out)))
+    return out
+
+
+def gmg_p2p_import(ctx, handles, base_off, layouts):
+    """handles: nranks x 64-byte cudaIpcMemHandle_t; base_off: [nranks] int64;
+    layouts: [nranks][n_levels + 1] int64 (each rank's gmg_p2p_layout)."""
+    hb = np.frombuffer(b"".join(bytes(h).ljust(64, b"\0")[:64] for h in handles), np.uint8).copy()
+    bo = np.ascontiguousarray(base_off, np.int64)
+    ly = np.ascontiguousarray(layouts, np.int64)
+    _check(ctx, lib().gmg_p2p_import(ctx, _ptr(hb), _ptr(bo), _ptr(ly)))
+
+
 def gmg_last_error(ctx):
     m = lib().gmg_last_error(ctx)
     return m.decode() if m else ""
@@ -317,6 +334,20 @@ class Solver:
             nb = gmg_workspace_bytes(self.ctx)
             self.ws = self._torch.empty(nb, dtype=self._torch.uint8, device=self.device)
             gmg_set_workspace(self.ctx, self.ws.data_ptr(), nb)
+            if self.opt.nranks > 1 and os.environ.get("GMG_P2P", "0") == "1":
+                self._p2p_exchange()
+
+    def _p2p_exchange(self):
+        """Fused P2P halo between ranks: share every rank's workspace through
+        CUDA IPC (the caching allocator's block handle + this workspace's
+        offset in it) and its record / flag layout, then map the peers'."""
+        import torch.distributed as dist
+        info = self.ws.untyped_storage()._share_cuda_()
+        handle, off = bytes(info[1]), int(info[3])
+        lay = gmg_p2p_layout(self.ctx, self.n_levels)
+        allv = [None] * self.opt.nranks
+        dist.all_gather_object(allv, (handle, off, lay.tolist()))
+        gmg_p2p_import(self.ctx, [a[0] for a in allv], [a[1] for a in allv], [a[2] for a in allv])
 
     def n_cells(self, level=0):
         return self.sizes[level][0]

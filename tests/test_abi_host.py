@@ -23,7 +23,7 @@ def G():
 
 def test_exports_every_header_symbol(G):
     hdr = open(os.path.join(ROOT, "include", "gmg.h")).read()
-    declared = set(re.findall(r"\b(gmg_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(gmg_[a-z0-9_]+)\s*\(", hdr))
     assert declared == set(G.ABI_SYMBOLS)
     L = G.lib()
     for name in declared:

@@ -41,13 +41,16 @@ def _case(name):
     return m, state.winf(*fs), state.bow_shock(m, *fs)
 
 
-@pytest.mark.parametrize("overlap", ["0", "1"])
+@pytest.mark.parametrize("mode", ["serial", "overlap", "p2p"])
 @pytest.mark.parametrize("name", ["config1", "box", "sphere"])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_partitioned_vcycle_parity(G, orc, name, P, overlap, monkeypatch):
-    # overlap=1 forces the boundary-first sweep with the exchange on a side
-    # stream (the NCCL default) onto the local-domain transport
-    monkeypatch.setenv("GMG_OVERLAP", overlap)
+def test_partitioned_vcycle_parity(G, orc, name, P, mode, monkeypatch):
+    # serial: pack / transport / unpack after every color; overlap: boundary
+    # cells first, exchange on a side stream while the interior is swept (the
+    # NCCL default); p2p: the fused halo -- the sweep epilogue stores the
+    # increments into the peers' ghost records and publishes its phase count
+    monkeypatch.setenv("GMG_OVERLAP", "1" if mode == "overlap" else "0")
+    monkeypatch.setenv("GMG_P2P", "1" if mode == "p2p" else "0")
     m, Winf, W = _case(name)
     part = G.gmg_partition_rcb(m.ctr, P)
     s = G.Solver(m, n_levels=3, part=part, local_domains=P)
@@ -107,3 +110,23 @@ def test_partition_one_domain_equals_unpartitioned(G):
     assert np.array_equal(a.get_state(0), b.get_state(0)) and np.array_equal(ha, hb)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_p2p_smooth_equals_exchange(G, monkeypatch, P):
+    """gmg_smooth with the fused P2P halo gives the same increments as the
+    pack / copy / unpack exchange (same arithmetic, only the transport differs)."""
+    m, Winf, W = _case("sphere")
+    part = G.gmg_partition_rcb(m.ctr, P)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("GMG_P2P", mode)
+        s = G.Solver(m, n_levels=3, part=part, local_domains=P)
+        s.set_state(W, Winf)
+        s.vcycle(1)
+        dW = s.smooth(1, 3)   # level 1's Rt = R(W) + F from the cycle
+        assert np.all(np.isfinite(dW))
+        out[mode] = (dW, s.get_state(0))
+        s.close()
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.array_equal(out["0"][1], out["1"][1])
