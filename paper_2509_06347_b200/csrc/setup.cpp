@@ -443,7 +443,7 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
     // (better L2 reuse of the gathered records, DESIGN.md §6 v13) -- and for
     // the dependency-driven sweep (color c, chunk x) is a contiguous segment
     D.nchunk = 0;
-    if (chunk_cells > 0 && N == D.n_own && !flow) {
+    if (chunk_cells > 0 && !flow) {
         // Morton (Z-order) key of the centroid: the same spatial grouping as
         // fine RCB chunks at a fraction of the setup cost
         double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -470,9 +470,12 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
             }
             key[i] = code;
         }
-        for (int c = 0; c < G.ncolor; ++c)
-            std::sort(D.l2n.begin() + D.blk[c], D.l2n.begin() + D.blk[c + 1],
-                      [&](int64_t a, int64_t b) { return key[a] < key[b] || (key[a] == key[b] && a < b); });
+        // boundary cells stay first inside their block (exchange overlap): sort each part
+        auto cmp = [&](int64_t a, int64_t b) { return key[a] < key[b] || (key[a] == key[b] && a < b); };
+        for (int c = 0; c < G.ncolor; ++c) {
+            std::sort(D.l2n.begin() + D.blk[c], D.l2n.begin() + D.blk[c] + D.nbnd[c], cmp);
+            std::sort(D.l2n.begin() + D.blk[c] + D.nbnd[c], D.l2n.begin() + D.blk[c + 1], cmp);
+        }
     }
     if (chunk_cells > 0 && N == D.n_own && flow) {
         const int K = (int)std::max<int64_t>(1, (N + chunk_cells - 1) / chunk_cells);
@@ -694,6 +697,8 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
         ps.erase(std::unique(ps.begin(), ps.end()), ps.end());
         for (const int p : ps) sg[(G.color[D.l2n[i]] - 1) * np + peer_index(p)].push_back((int32_t)i);
     }
+    for (auto &g : sg)   // natural id ascending: element-wise equal to the receiver's ghost group
+        std::sort(g.begin(), g.end(), [&](int32_t a, int32_t b) { return D.l2n[a] < D.l2n[b]; });
     D.send_off.assign(ng + 1, 0);
     D.recv_off.assign(ng + 1, 0);
     for (int k = 0; k < ng; ++k) {
