@@ -6,8 +6,9 @@
 //    colors, global renumbering, parent map, partition ids).  Every rank
 //    builds the identical global hierarchy (deterministic host code).
 //  * DomLevel: the part of a level one domain (rank) works on: its owned
-//    cells in (color, natural id) order, then one layer of ghost cells in
-//    (owner, color, natural id) order; the local faces (those touching an
+//    cells in color blocks (boundary cells first when partitioned; Morton key
+//    of the centroid inside), then one layer of ghost cells in (owner, color,
+//    natural id) order; the local faces (those touching an
 //    owned cell); slot layouts over owned cells; multigrid links; the halo
 //    plan grouped by (color, peer).
 //  * DevLevel: device pointers of a DomLevel (inside the workspace).
