@@ -130,3 +130,21 @@ def test_p2p_smooth_equals_exchange(G, monkeypatch, P):
         s.close()
     assert np.array_equal(out["0"][0], out["1"][0])
     assert np.array_equal(out["0"][1], out["1"][1])
+
+
+@pytest.mark.parametrize("mode", ["serial", "p2p"])
+@pytest.mark.parametrize("kw", [dict(fine_smoother=1), dict(df_mode=2), dict(df_mode=3, beta=0.5)])
+def test_partitioned_variants_parity(G, orc, mode, kw, monkeypatch):
+    """MC-LU-SGS on the fine level, DF off and fixed-beta relaxation on the
+    partitioned path (copy exchange and fused P2P halo) vs the oracle."""
+    monkeypatch.setenv("GMG_P2P", "1" if mode == "p2p" else "0")
+    m, Winf, W = _case("box")
+    part = G.gmg_partition_rcb(m.ctr, 3)
+    s = G.Solver(m, n_levels=3, part=part, local_domains=3, **kw)
+    s.set_state(W, Winf)
+    hist = s.vcycle(2)
+    H = orc.build_hierarchy(m, 3, 0.5, part=part)
+    Wo, ho = orc.vcycle(H, W, Winf, orc.Options(**kw), 2)
+    assert rel(s.get_state(0), Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+    s.close()

@@ -92,3 +92,20 @@ def test_device_setup_full_size(G):
     d = _hier(G, m, 1)
     for (c0, p0, q0, _), (c1, p1, q1, _) in zip(h, d):
         assert np.array_equal(c0, c1) and np.array_equal(p0, p1) and np.array_equal(q0, q1)
+
+
+def test_device_built_hierarchy_runs_identically(G):
+    """V-cycles on the device-built hierarchy give the same bits as on the
+    host-built one (same colors, order and parents -> same arithmetic)."""
+    from synth import state
+    m = configs.sphere_shell(10, 4, 4)
+    fs = configs.FREESTREAM[4]
+    W, Winf = state.bow_shock(m, *fs), state.winf(*fs)
+    out = []
+    for dev in (0, 1):
+        s = G.Solver(m, n_levels=3, setup_device=dev)
+        s.set_state(W, Winf)
+        h = s.vcycle(3)
+        out.append((h, s.get_state(0)))
+        s.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
