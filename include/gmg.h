@@ -243,6 +243,13 @@ gmg_status gmg_get_halo(gmg_ctx *ctx, int level, int dom, int64_t *n_owned, int6
  *     than one GPU; the same kernels run between the local domains of one
  *     process -- tests/test_gpu_partitioned.py.) */
 gmg_status gmg_p2p_layout(gmg_ctx *ctx, int64_t *out);
+/* Host view of the fused-halo targets of domain `dom` on `level` (tests):
+ * *n_targets first (other pointers NULL), then off[n_owned+1] (CSR over the
+ * owned cells in local order), peer_slot[n_targets] (index into the domain's
+ * ascending peer list), ghost_local[n_targets] (the peer's local index of its
+ * ghost copy).  GMG_ESTATE unless built with GMG_P2P=1 and > 1 partition. */
+gmg_status gmg_get_p2p_targets(gmg_ctx *ctx, int level, int dom, int64_t *n_targets, int32_t *off,
+                               int32_t *peer_slot, int32_t *ghost_local);
 gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base_off, const int64_t *layouts);
 
 const char *gmg_last_error(gmg_ctx *ctx); /* valid until the next call on ctx */

@@ -1669,6 +1669,26 @@ gmg_status gmg_p2p_layout(gmg_ctx *ctx, int64_t *out)
     return GMG_OK;
 }
 
+gmg_status gmg_get_p2p_targets(gmg_ctx *ctx, int level, int dom, int64_t *n_targets, int32_t *off,
+                               int32_t *peer_slot, int32_t *ghost_local)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->built) { ctx->err = "hierarchy not built"; return GMG_ESTATE; }
+    if (level < 0 || level >= (int)ctx->lv.size() || dom < 0 || dom >= (int)ctx->dom.size()) {
+        ctx->err = "bad level / domain";
+        return GMG_EINVAL;
+    }
+    const DomLevel &H = ctx->dom[dom].lv[level];
+    if (!ctx->p2p || ctx->nparts < 2 || H.p2p_off.empty()) { ctx->err = "no P2P targets (GMG_P2P=1, > 1 partition)"; return GMG_ESTATE; }
+    if (n_targets) *n_targets = (int64_t)H.p2p_k.size();
+    if (off && peer_slot && ghost_local) {
+        std::copy(H.p2p_off.begin(), H.p2p_off.end(), off);
+        std::copy(H.p2p_k.begin(), H.p2p_k.end(), peer_slot);
+        std::copy(H.p2p_g.begin(), H.p2p_g.end(), ghost_local);
+    }
+    return GMG_OK;
+}
+
 gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base_off, const int64_t *layouts)
 {
     if (!ctx || !handles || !base_off || !layouts) return GMG_EINVAL;

@@ -30,7 +30,7 @@ ABI_SYMBOLS = ["gmg_default_options", "gmg_create", "gmg_load_mesh", "gmg_set_co
                "gmg_set_workspace", "gmg_set_state", "gmg_set_level_state", "gmg_get_state", "gmg_set_alpha",
                "gmg_residual", "gmg_set_level_inputs", "gmg_smooth", "gmg_vcycle", "gmg_profile_vcycle",
                "gmg_time_smooth", "gmg_vcycle_launches", "gmg_partition_rcb", "gmg_get_halo", "gmg_p2p_layout",
-               "gmg_p2p_import", "gmg_last_error", "gmg_destroy"]
+               "gmg_p2p_import", "gmg_get_p2p_targets", "gmg_last_error", "gmg_destroy"]
 
 
 class GmgError(RuntimeError):
@@ -86,6 +86,7 @@ def lib():
             "gmg_get_halo": (I, [P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
             "gmg_p2p_layout": (I, [P, P]),
             "gmg_p2p_import": (I, [P, P, P, P]),
+            "gmg_get_p2p_targets": (I, [P, I, I, P, P, P, P]),
             "gmg_last_error": (C.c_char_p, [P]),
             "gmg_destroy": (None, [P]),
         }
@@ -286,6 +287,18 @@ def gmg_p2p_import(ctx, handles, base_off, layouts):
     bo = np.ascontiguousarray(base_off, np.int64)
     ly = np.ascontiguousarray(layouts, np.int64)
     _check(ctx, lib().gmg_p2p_import(ctx, _ptr(hb), _ptr(bo), _ptr(ly)))
+
+
+def gmg_get_p2p_targets(ctx, level, dom=0):
+    """Fused-halo targets of a domain (see include/gmg.h): (off, peer_slot, ghost_local)."""
+    nt = C.c_int64()
+    _check(ctx, lib().gmg_get_p2p_targets(ctx, level, dom, C.byref(nt), None, None, None))
+    h = gmg_get_halo(ctx, level, dom)
+    off = np.zeros(len(h["owned"]) + 1, np.int32)
+    k = np.zeros(nt.value, np.int32)
+    g = np.zeros(nt.value, np.int32)
+    _check(ctx, lib().gmg_get_p2p_targets(ctx, level, dom, None, _ptr(off), _ptr(k), _ptr(g)))
+    return off, k, g
 
 
 def gmg_last_error(ctx):

@@ -114,10 +114,47 @@ def test_halo_plans_consistent(G, orc, name, P):
     s.close()
 
 
+def _check_targets(owned, off, k, g, peers, ghost_of_peer, n_own_of_peer):
+    """every fused-halo target must be the peer's ghost copy of the same natural cell"""
+    for i in range(len(owned)):
+        for m in range(off[i], off[i + 1]):
+            q = peers[k[m]]
+            gl = g[m] - n_own_of_peer[q]
+            if not (0 <= gl < len(ghost_of_peer[q]) and ghost_of_peer[q][gl] == owned[i]):
+                return False
+    return True
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+@pytest.mark.parametrize("P", [2, 3])
+def test_p2p_targets_local_domains(G, name, P, monkeypatch):
+    """Fused P2P halo addressing (host side): each owned boundary cell's
+    targets are exactly the peers' ghost copies of that cell, and every ghost
+    of every domain is targeted by its owner exactly once."""
+    monkeypatch.setenv("GMG_P2P", "1")
+    m = MESHES[name]()
+    part = G.gmg_partition_rcb(m.ctr, P)
+    s = G.Solver(m, n_levels=3, build_only=True, part=part, local_domains=P)
+    for l in range(s.n_levels):
+        plans = _plans(s, P, l)
+        ghost_of = {r: p["ghost"] for r, p in enumerate(plans)}
+        n_own = {r: len(p["owned"]) for r, p in enumerate(plans)}
+        hit = {r: np.zeros(len(p["ghost"]), int) for r, p in enumerate(plans)}
+        for r, p in enumerate(plans):
+            off, k, g = G.gmg_get_p2p_targets(s.ctx, l, r)
+            assert _check_targets(p["owned"], off, k, g, p["peers"], ghost_of, n_own)
+            for m_ in range(len(k)):
+                hit[p["peers"][k[m_]]][g[m_] - n_own[p["peers"][k[m_]]]] += 1
+        for r in hit:
+            assert np.all(hit[r] == 1)
+    s.close()
+
+
 def _worker(rank, world, port, name, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["GMG_P2P"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2509_06347_b200 import gmg
@@ -142,6 +179,11 @@ def _worker(rank, world, port, name, q):
             dist.all_gather_object(owned, mine["owned"].tolist())
             n = s.n_cells(l)
             ok &= sorted(sum(owned, [])) == list(range(n))
+            # fused P2P halo targets built from each rank's own view of its peers
+            off, k, g = gmg.gmg_get_p2p_targets(s.ctx, l, 0)
+            ghost_of = {r: allp[r]["ghost"] for r in range(world)}
+            n_own = {r: len(allp[r]["owned"]) for r in range(world)}
+            ok &= _check_targets(mine["owned"], off, k, g, mine["peers"], ghost_of, n_own)
         s.close()
         q.put((rank, ok))
     finally:
