@@ -329,8 +329,6 @@ void enqueue_ghost_w(Launcher &Lc, int l)
 // optional L2 access-policy window over the level's cell records (the
 // gathered data), attached per launch so that graph capture keeps it
 // sweep grid cap = resident waves x SMs x blocks/SM (set in gmg_set_workspace; 0 = one thread per cell)
-int g_sweep_grid_cap = 0;
-int g_sweep_var = 3;   // k_sweep variant bits (kernels.cuh), GMG_SWEEPV
 
 template <class K>
 void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArgs &a, const void *win, size_t win_bytes,
@@ -362,17 +360,19 @@ void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArg
 }
 
 template <int D, int LPC>
-void launch_sweep(const SweepArgs &a, cudaStream_t s, int minb, const void *win, size_t win_bytes, bool pdl)
+void launch_sweep(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, const void *win, size_t win_bytes)
 {
+    const int minb = ctx->minb, sweep_var = ctx->sweep_var;
+    const bool pdl = ctx->pdl != 0;
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
     int nb = nblk(nthreads);
-    if (g_sweep_grid_cap > 0) nb = std::min(nb, g_sweep_grid_cap);
+    if (ctx->sweep_grid_cap > 0) nb = std::min(nb, ctx->sweep_grid_cap);
     const dim3 g(nb), b(256);
     // variants kept for the record; 3 is the default
-    if (g_sweep_var == 0) { launch_with_window(k_sweep<D, LPC, 4, 0>, g, b, s, a, win, win_bytes, pdl); return; }
-    if (g_sweep_var == 1) { launch_with_window(k_sweep<D, LPC, 4, 1>, g, b, s, a, win, win_bytes, pdl); return; }
-    if (g_sweep_var == 2) { launch_with_window(k_sweep<D, LPC, 4, 2>, g, b, s, a, win, win_bytes, pdl); return; }
-    if (g_sweep_var == 7) { launch_with_window(k_sweep<D, LPC, 4, 7>, g, b, s, a, win, win_bytes, pdl); return; }
+    if (sweep_var == 0) { launch_with_window(k_sweep<D, LPC, 4, 0>, g, b, s, a, win, win_bytes, pdl); return; }
+    if (sweep_var == 1) { launch_with_window(k_sweep<D, LPC, 4, 1>, g, b, s, a, win, win_bytes, pdl); return; }
+    if (sweep_var == 2) { launch_with_window(k_sweep<D, LPC, 4, 2>, g, b, s, a, win, win_bytes, pdl); return; }
+    if (sweep_var == 7) { launch_with_window(k_sweep<D, LPC, 4, 7>, g, b, s, a, win, win_bytes, pdl); return; }
     switch (minb) {
         case 6: launch_with_window(k_sweep<D, LPC, 6>, g, b, s, a, win, win_bytes, pdl); break;
         case 8: launch_with_window(k_sweep<D, LPC, 8>, g, b, s, a, win, win_bytes, pdl); break;
@@ -404,9 +404,9 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
         if (b1 <= b0) return;
         Lc.pre(GMG_K_SWEEP);
         switch (ctx->lpc) {
-            case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, nullptr, 0, ctx->pdl); break;
-            case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, nullptr, 0, ctx->pdl); break;
-            default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, nullptr, 0, ctx->pdl); break;
+            case 1: launch_sweep<D, 1>(ctx, a, Lc.s, nullptr, 0); break;
+            case 4: launch_sweep<D, 4>(ctx, a, Lc.s, nullptr, 0); break;
+            default: launch_sweep<D, 2>(ctx, a, Lc.s, nullptr, 0); break;
         }
         Lc.post(GMG_K_SWEEP, frac * (dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0)));
         return;
@@ -449,16 +449,16 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
     // its slots one dependent gather after the other): spread the slots over
     // more lanes while the whole block still fits in one resident wave
     int lpc = ctx->lpc;
-    if (ctx->adapt_lpc && g_sweep_grid_cap > 0) {
-        const int64_t wave = (int64_t)g_sweep_grid_cap * 256, cells = a.cend - a.cbeg;
+    if (ctx->adapt_lpc && ctx->sweep_grid_cap > 0) {
+        const int64_t wave = (int64_t)ctx->sweep_grid_cap * 256, cells = a.cend - a.cbeg;
         while (lpc < 16 && cells * lpc * 2 <= wave) lpc *= 2;
     }
     switch (lpc) {
-        case 1: launch_sweep<D, 1>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
-        case 4: launch_sweep<D, 4>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
-        case 8: launch_sweep<D, 8>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
-        case 16: launch_sweep<D, 16>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
-        default: launch_sweep<D, 2>(a, Lc.s, ctx->minb, win, wb, ctx->pdl); break;
+        case 1: launch_sweep<D, 1>(ctx, a, Lc.s, win, wb); break;
+        case 4: launch_sweep<D, 4>(ctx, a, Lc.s, win, wb); break;
+        case 8: launch_sweep<D, 8>(ctx, a, Lc.s, win, wb); break;
+        case 16: launch_sweep<D, 16>(ctx, a, Lc.s, win, wb); break;
+        default: launch_sweep<D, 2>(ctx, a, Lc.s, win, wb); break;
     }
     Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
 }
@@ -480,10 +480,10 @@ void enqueue_p2p_phase(Launcher &Lc, int l, int c, bool last, bool ff, std::func
         P2PArgs p{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_rec, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
         int lpc = ctx->lpc;
         const int64_t cells = b1 - b0;
-        if (ctx->adapt_lpc && g_sweep_grid_cap > 0)
-            while (lpc < 16 && cells * lpc * 2 <= (int64_t)g_sweep_grid_cap * 256) lpc *= 2;
+        if (ctx->adapt_lpc && ctx->sweep_grid_cap > 0)
+            while (lpc < 16 && cells * lpc * 2 <= (int64_t)ctx->sweep_grid_cap * 256) lpc *= 2;
         int nb = nblk(cells * lpc);
-        if (g_sweep_grid_cap > 0) nb = std::min(nb, g_sweep_grid_cap);
+        if (ctx->sweep_grid_cap > 0) nb = std::min(nb, ctx->sweep_grid_cap);
         const dim3 g(std::max(nb, 1)), b(256);
         Lc.pre(GMG_K_SWEEP);
         switch (lpc) {
@@ -1307,13 +1307,13 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
     {   // sweep grid: whole resident waves only (grid-stride kernel), GMG_SWEEP_WAVES (0 = uncapped)
         int waves = 1, nsm = 0, per_sm = 0;
         if (const char *e = std::getenv("GMG_SWEEP_WAVES")) waves = std::atoi(e);
-        if (const char *e = std::getenv("GMG_SWEEPV")) g_sweep_var = std::atoi(e);
+        if (const char *e = std::getenv("GMG_SWEEPV")) ctx->sweep_var = std::atoi(e);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
         if (ctx->opt.dim == 3)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, 4, 3>, 256, 0);
         else
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, 4, 3>, 256, 0);
-        g_sweep_grid_cap = waves > 0 ? waves * nsm * std::max(per_sm, 1) : 0;
+        ctx->sweep_grid_cap = waves > 0 ? waves * nsm * std::max(per_sm, 1) : 0;
         int per_flow = 0;
         if (ctx->opt.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_flow, k_sweep_flow<3>, 256, 0);
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_flow, k_sweep_flow<2>, 256, 0);

@@ -177,6 +177,8 @@ struct gmg_ctx {
     double kbytes[GMG_K_COUNT] = {0}; // algorithmic bytes accumulated by the recorded sequence
     int64_t launches = 0;             // kernels launched by the last recorded sequence
     int64_t exchanges = 0;            // halo exchanges in the last recorded sequence
+    int sweep_grid_cap = 0;           // sweep grid = resident waves x SMs x blocks/SM (set with the workspace)
+    int sweep_var = 3;                // k_sweep variant bits (kernels.cuh), GMG_SWEEPV
     int lpc = 2;                      // sweep lanes per cell (1, 2, 4) of the large color blocks
     int adapt_lpc = 1;                // blocks that fit one wave at 2x lanes get up to 16 lanes per cell
     int skip_repeat = 1;              // drop the repeated same-color phase at every sweep turn (exact)

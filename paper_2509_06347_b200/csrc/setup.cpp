@@ -392,10 +392,12 @@ void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *p
     }
 }
 
-// Domain of `rank` on a global level: owned cells in global
-// renumbering order (color, natural id), then one layer of ghosts in (owner,
-// color, natural id) order; local faces = faces touching an owned cell, in
-// natural face order; layouts over owned cells:
+// Domain of `rank` on a global level: owned cells in color
+// blocks (boundary cells -- a face neighbour on another rank -- first), inside
+// a block by the Morton key of the centroid when chunk_cells > 0 (natural id
+// otherwise; RCB chunks for the dependency-driven sweep), then one layer of
+// ghosts in (owner, color, natural id) order; local faces = faces touching an
+// owned cell, ordered by their first local cell; layouts over owned cells:
 //  * gather slots (residual/prepare, thread per cell): SELL-32 -- per color,
 //    chunks of 32 consecutive cells, entries [slot][lane], chunk padded to its
 //    max degree.  Slots: interior faces (ascending id) then boundary faces.
