@@ -227,12 +227,18 @@ def main():
         part = gmg.gmg_partition_rcb(m.ctr, ws)
         uid = [torch.cuda.nccl.unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(uid, src=0)
+        t_setup = time.perf_counter()
         s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, part=part, nranks=ws, rank=rank,
-                       nccl_id=uid[0])
-        parallelism = f"mesh partitioned over {ws} GPUs (RCB), NCCL halo exchange per color"
+                       nccl_id=uid[0], setup_device=1)
+        t_setup = time.perf_counter() - t_setup
+        parallelism = (f"mesh partitioned over {ws} GPUs (RCB), "
+                       + ("fused P2P halo (CUDA IPC)" if os.environ.get("GMG_P2P", "0") == "1"
+                          else "NCCL halo exchange per color, overlapped with the interior sweep"))
     else:
         m, W, Winf = workload(args.config)
-        s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps)
+        t_setup = time.perf_counter()
+        s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, setup_device=1)
+        t_setup = time.perf_counter() - t_setup
         parallelism = f"{ws} independent replicas" if ws > 1 else "single GPU"
     s.set_state(W, Winf)
     stream = torch.cuda.current_stream(dev)
@@ -344,6 +350,9 @@ def main():
                    * (ws if replicas else 1),
                    "l2": f"inputs larger than L2: workspace {ws_bytes / 1e9:.2f} GB >> 126 MB",
                    "parallelism": parallelism,
+                   "setup_s": round(t_setup, 3),
+                   "setup": "hierarchy with device-side Algorithms 1 and 3 (bit-identical to the host setup), "
+                            "not timed",
                    "n_gpus_partitions": 1 if replicas else ws},
         "vcycles_per_s": 1e3 / ms_step * (ws if replicas else 1),
         "fine_cell_vcycles_per_s": m.n_cells * 1e3 / ms_step * (ws if replicas else 1),
