@@ -20,8 +20,12 @@
  *  - Pointers may be host or device memory (classified with
  *    cudaPointerGetAttributes) wherever "host/device" is written.
  *  - Device memory: ONE caller-allocated workspace (gmg_set_workspace); the
- *    library sub-allocates and never calls cudaMalloc.  Host-side setup
- *    (coloring, agglomeration, layouts) uses host heap memory.
+ *    library sub-allocates it.  The only other device allocations are the
+ *    temporaries of the optional device-side setup (setup_device = 1:
+ *    stream-ordered cudaMallocAsync, freed before gmg_build_hierarchy
+ *    returns).  Host-side setup (coloring, agglomeration, layouts) uses host
+ *    heap memory.
+ *  - Threads: a context is not thread-safe; use it from one thread at a time.
  *  - Stream: every call is asynchronous on gmg_options.stream; a call that
  *    returns host data synchronizes that stream first.
  *  - Errors: return codes only; no exceptions cross the ABI.  A failing
