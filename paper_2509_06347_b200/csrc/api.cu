@@ -570,6 +570,8 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
         return;
     }
     const bool fuse = ctx->tail_cells > 0 && ctx->nparts == 1 && ctx->dom.size() == 1;
+    const bool tailc = ctx->tailc && !fuse && ctx->tailc_grid > 0 && ctx->nparts == 1 && ctx->dom.size() == 1 &&
+                       ctx->sweep_grid_cap > 0 && !ctx->pipe && !ctx->spsweep && !ctx->wsweep;
     const bool overlap = (ctx->overlap < 0 ? ctx->opt.nranks > 1 : ctx->overlap != 0) && ctx->nparts > 1 && ctx->side && !ctx->pipe && !ctx->spsweep && !ctx->wsweep;
     for (size_t k = 0; k < seq.size();) {
         if (fuse) {
@@ -596,6 +598,46 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
                     bytes += dm.lbytes[l].sweep[seq[p].c] + (seq[p].last ? dm.lbytes[l].sweep_out[seq[p].c] : 0.0);
                 Lc.pre(GMG_K_SWEEP);
                 klaunch(ctx, k_sweep_tail<D>, dim3(1), dim3(kTailT), Lc.s, t);
+                Lc.post(GMG_K_SWEEP, bytes);
+                k = r;
+                continue;
+            }
+        }
+        if (tailc) {
+            // a run of >= 2 consecutive small phases (each fits one resident wave at 2 lanes per
+            // cell) -> one cooperative launch, grid barriers between the phases
+            Domain &dm = ctx->dom[0];
+            const DomLevel &H = dm.lv[l];
+            const int64_t small = ctx->tailc_cells > 0 ? ctx->tailc_cells : (int64_t)ctx->sweep_grid_cap * 256 / 2;
+            auto is_small = [&](size_t t) { return t < seq.size() && H.blk[seq[t].c + 1] - H.blk[seq[t].c] <= small; };
+            size_t r = k;
+            int64_t mx = 0;
+            while (is_small(r) && r - k < (size_t)kTailMaxPh) { mx = std::max<int64_t>(mx, H.blk[seq[r].c + 1] - H.blk[seq[r].c]); ++r; }
+            if (r - k >= 2) {
+                DevLevel &L = dm.dv[l];
+                TailArgs t{};
+                t.nph = (int)(r - k);
+                double bytes = 0;
+                for (size_t p = k; p < r; ++p) {
+                    t.cbeg[p - k] = (int)H.blk[seq[p].c];
+                    t.cend[p - k] = (int)H.blk[seq[p].c + 1];
+                    t.wout[p - k] = seq[p].last ? 1 : 0;
+                    bytes += dm.lbytes[l].sweep[seq[p].c] + (seq[p].last ? dm.lbytes[l].sweep_out[seq[p].c] : 0.0);
+                }
+                t.a = SweepArgs{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs(L), wout(L)};
+                const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->tailc_grid, (mx * 16 + 255) / 256));
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(grid);
+                cfg.blockDim = dim3(256);
+                cfg.stream = Lc.s;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int *bar = ctx->d_bar;
+                Lc.pre(GMG_K_SWEEP);
+                cudaLaunchKernelEx(&cfg, k_sweep_tailc<D>, t, bar);
                 Lc.post(GMG_K_SWEEP, bytes);
                 k = r;
                 continue;
@@ -834,6 +876,7 @@ void carve(gmg_ctx *ctx, Bump &b)
     ctx->hist_cap = 4096;
     ctx->d_hist = b.take<double>((size_t)ctx->hist_cap * nv);
     ctx->d_flag = b.take<int>(4);
+    ctx->d_bar = b.take<int>(2);
     ctx->d_sumsq = b.take<double>((size_t)std::max<size_t>(1, ctx->dom.size()) * nv);
 }
 
@@ -964,6 +1007,8 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if (const char *e = std::getenv("GMG_SKIP_ZERO")) ctx->skip_zero = std::atoi(e);       // skip +0 neighbour terms
     if (const char *e = std::getenv("GMG_FLOW")) ctx->flow = std::atoi(e);                 // dependency-driven sweep
     if (const char *e = std::getenv("GMG_P2P")) ctx->p2p = std::atoi(e);                   // fused P2P halo
+    if (const char *e = std::getenv("GMG_TAILC")) ctx->tailc = std::atoi(e);               // cooperative small-phase runs
+    if (const char *e = std::getenv("GMG_TAILC_CELLS")) ctx->tailc_cells = std::atoi(e);
     if (const char *e = std::getenv("GMG_CHUNK_ORDER")) ctx->chunk_order = std::atoi(e);   // (color, chunk, id) order
     if (const char *e = std::getenv("GMG_ORDER_CHUNK")) ctx->order_chunk = std::max(8, std::atoi(e));
     if (const char *e = std::getenv("GMG_FLOW_CHUNK")) ctx->flow_chunk = std::max(32, std::atoi(e));
@@ -1264,6 +1309,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         }
     }
     CK(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_bar, 0, 2 * sizeof(int), ctx->stream));
     for (Domain &dm : ctx->dom) {   // P2P phase counts / control
         CK(cudaMemsetAsync(dm.dv[0].p2p_flags, 0, sizeof(int) * std::max(ctx->nparts, 1), ctx->stream));
         CK(cudaMemsetAsync(dm.dv[0].p2p_ctl, 0, sizeof(int) * 4, ctx->stream));
@@ -1318,6 +1364,10 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         if (ctx->opt.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_flow, k_sweep_flow<3>, 256, 0);
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_flow, k_sweep_flow<2>, 256, 0);
         ctx->flow_grid = per_flow * nsm;
+        int per_tail = 0;
+        if (ctx->opt.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_tail, k_sweep_tailc<3>, 256, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_tail, k_sweep_tailc<2>, 256, 0);
+        ctx->tailc_grid = per_tail * nsm;
     }
     {   // dynamic shared memory of the warp-staged sweep (may exceed the 48 KB default)
         int mx = 1;

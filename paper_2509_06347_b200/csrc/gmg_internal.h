@@ -183,6 +183,10 @@ struct gmg_ctx {
     int adapt_lpc = 1;                // blocks that fit one wave at 2x lanes get up to 16 lanes per cell
     int skip_repeat = 1;              // drop the repeated same-color phase at every sweep turn (exact)
     int skip_zero = 1;                // first forward half-sweep: skip later-color neighbours (dW = +0, exact)
+    int tailc = 0;                    // runs of small color phases in one cooperative launch (GMG_TAILC; measured slower)
+    int tailc_grid = 0;               // resident CTAs of k_sweep_tailc
+    int tailc_cells = 0;              // largest phase fused (0: one wave at 2 lanes per cell)
+    int *d_bar = nullptr;             // grid barrier (count, generation) of k_sweep_tailc
     int flow = 0;                     // dependency-driven persistent sweep (single domain), GMG_FLOW
     int flow_chunk = 512;             // cells per chunk, GMG_FLOW_CHUNK
     int p2p = 0;                      // fused P2P halo instead of pack / transport / unpack per color (GMG_P2P)

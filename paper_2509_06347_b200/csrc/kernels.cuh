@@ -1067,6 +1067,120 @@ struct TailArgs {
     SweepArgs a;                // rec, ecell, deg, sJe, sRe, rhs, Wout, gm1 (cbeg/cend unused)
 };
 
+// Cooperative tail (opt-in, GMG_TAILC=1; measured slower): a run of
+// consecutive SMALL color phases (each fits one resident wave at >= 2 lanes
+// per cell) runs in ONE launch over the whole resident grid, phases separated
+// by a grid barrier instead of kernel boundaries.  Records written by an
+// earlier phase of the launch are read L2-coherent (.cg).
+__device__ __forceinline__ void grid_barrier(int *bar)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int g = ld_acquire(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1) == (int)gridDim.x - 1) {
+            bar[0] = 0;
+            st_release(bar + 1, g + 1);
+        } else {
+            while (ld_acquire(bar + 1) == g) __nanosleep(32);
+        }
+    }
+    __syncthreads();
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 4) k_sweep_tailc(TailArgs t, int *bar)
+{
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    const SweepArgs &a = t.a;
+    const int nthr = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int ph = 0; ph < t.nph; ++ph) {
+        const int b0 = t.cbeg[ph], b1 = t.cend[ph], cells = b1 - b0;
+        double *Wout = t.wout[ph] ? a.Wout : nullptr;
+        int L = 2;
+        while (L < 16 && cells * L * 2 <= nthr) L *= 2;
+        const int per = nthr / L;
+        const int rounds = (cells + per - 1) / per;
+        for (int r = 0; r < rounds; ++r) {
+            const int i = b0 + r * per + gtid / L, sub = gtid % L;
+            const bool valid = i < b1;
+            double acc[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+            if (valid) {
+                const int2 sd = __ldg(a.sinfo + i);
+                const int e1 = sd.x + sd.y;
+                for (int e = sd.x + sub; e < e1; e += L) {
+                    const int j = __ldg(a.sJe + e);
+                    double sr[4];
+                    ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                    const double *rj = a.rec + (size_t)j * RC::STRIDE;
+                    double w[NV], dw[NV];
+                    if constexpr (D == 3) {
+                        double c0[4], c1[4], c2[4];
+                        ld4cg(rj, c0);
+                        ld4cg(rj + 4, c1);
+                        ld4cg(rj + 8, c2);
+                        w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
+                        dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                    } else {
+                        ld4cg(rj, w);
+                        ld4cg(rj + 4, dw);
+                    }
+                    flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                }
+            }
+            for (int o = L / 2; o > 0; o >>= 1) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+            }
+            if (valid && sub == 0) {
+                double *ri = a.rec + (size_t)i * RC::STRIDE;
+                const size_t o = (size_t)i * NV;
+                double rr[NV], c1[4], c2[4];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) rr[q] = __ldcs(a.rhs + o + q);
+                ld4cg(ri + 4, c1);
+                ld4cg(ri + 8, c2);
+                if constexpr (D == 3) {
+                    const double invD = c2[2], ha = c2[3];
+                    double d[NV];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) d[q] = -(rr[q] + ha * acc[q]) * invD;
+                    const double w1[4] = {c1[0], d[0], d[1], d[2]};
+                    st4(ri + 4, w1);
+                    c2[0] = d[3];
+                    c2[1] = d[4];
+                    st4(ri + 8, c2);
+                    if (Wout) {
+                        double c0[4];
+                        ld4cg(ri, c0);
+                        Wout[o + 0] = c0[0] + d[0];
+                        Wout[o + 1] = c0[1] + d[1];
+                        Wout[o + 2] = c0[2] + d[2];
+                        Wout[o + 3] = c0[3] + d[3];
+                        Wout[o + 4] = c1[0] + d[4];
+                    }
+                } else {
+                    const double invD = c2[0], ha = c2[1];
+                    double d[4];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) d[q] = -(rr[q] + ha * acc[q]) * invD;
+                    st4(ri + 4, d);
+                    if (Wout) {
+                        double c0[4];
+                        ld4cg(ri, c0);
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) Wout[o + q] = c0[q] + d[q];
+                    }
+                }
+            }
+        }
+        if (ph + 1 < t.nph) grid_barrier(bar);
+    }
+}
+
 __device__ __forceinline__ void ld4(const double *p, double *v)
 {
     asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
