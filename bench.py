@@ -229,7 +229,7 @@ def main():
         torch.distributed.broadcast_object_list(uid, src=0)
         t_setup = time.perf_counter()
         s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, part=part, nranks=ws, rank=rank,
-                       nccl_id=uid[0], setup_device=1)
+                       nccl_id=uid[0], setup_device=0 if args.profile_only else 1)
         t_setup = time.perf_counter() - t_setup
         parallelism = (f"mesh partitioned over {ws} GPUs (RCB), "
                        + ("fused P2P halo (CUDA IPC)" if os.environ.get("GMG_P2P", "0") == "1"
@@ -237,7 +237,8 @@ def main():
     else:
         m, W, Winf = workload(args.config)
         t_setup = time.perf_counter()
-        s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, setup_device=1)
+        # (--profile-only: host setup, so that an ncu launch list starts with the V-cycle kernels)
+        s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, setup_device=0 if args.profile_only else 1)
         t_setup = time.perf_counter() - t_setup
         parallelism = f"{ws} independent replicas" if ws > 1 else "single GPU"
     s.set_state(W, Winf)
