@@ -255,6 +255,13 @@ gmg_status gmg_p2p_layout(gmg_ctx *ctx, int64_t *out);
 gmg_status gmg_get_p2p_targets(gmg_ctx *ctx, int level, int dom, int64_t *n_targets, int32_t *off,
                                int32_t *peer_slot, int32_t *ghost_local);
 gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base_off, const int64_t *layouts);
+/* Test only: one smoothing step (as gmg_smooth) of ALL local domains
+ * (local_domains >= 2, GMG_P2P=1) in ONE cooperative launch with one block
+ * group per domain, so that the fused-P2P-halo protocol (wait for the peers'
+ * phase counts, sweep + peer stores, publish) runs with the domains truly
+ * concurrent -- the single-GPU stand-in for ranks that wait on one another.
+ * dW_out as gmg_smooth (nullable). */
+gmg_status gmg_p2p_emulate_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out);
 
 const char *gmg_last_error(gmg_ctx *ctx); /* valid until the next call on ctx */
 void gmg_destroy(gmg_ctx *ctx);

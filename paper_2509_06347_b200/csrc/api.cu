@@ -877,6 +877,8 @@ void carve(gmg_ctx *ctx, Bump &b)
     ctx->d_hist = b.take<double>((size_t)ctx->hist_cap * nv);
     ctx->d_flag = b.take<int>(4);
     ctx->d_bar = b.take<int>(2);
+    ctx->d_emu = b.take<char>(sizeof(EmuDom) * kEmuMaxDom);
+    ctx->d_emu_bar = b.take<int>(2 * kEmuMaxDom);
     ctx->d_sumsq = b.take<double>((size_t)std::max<size_t>(1, ctx->dom.size()) * nv);
 }
 
@@ -1499,6 +1501,92 @@ gmg_status gmg_set_level_inputs(gmg_ctx *ctx, int level, const double *Rt, const
     }
     if (alpha) { st = put_natural(ctx, level, alpha, 1, [](DevLevel &L) { return L.alpha; }, false); if (st) return st; }
     CK(cudaStreamSynchronize(ctx->stream));
+    return GMG_OK;
+}
+
+// test only: one smoothing step of every local domain in ONE cooperative
+// launch, one block group per domain, running the fused-P2P-halo protocol
+// concurrently (kernels.cuh k_p2p_emulate)
+gmg_status gmg_p2p_emulate_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (level < 0 || level >= (int)ctx->lv.size() || n_sweeps < 1) { ctx->err = "bad level / n_sweeps"; return GMG_EINVAL; }
+    const int P = (int)ctx->dom.size();
+    if (!ctx->p2p || !ctx->p2p_ready || ctx->opt.nranks != 1 || P < 2 || P > kEmuMaxDom ||
+        ctx->lv[level].ncolor > kEmuMaxCol) {
+        ctx->err = "P2P emulation needs GMG_P2P=1, 2..16 local domains, <= 24 colors";
+        return GMG_ESTATE;
+    }
+    Launcher Lc{ctx, ctx->stream};
+    const int gf = G_PREPARE | G_SIGMA | G_COPY_W | G_ZERO_DW;
+    for (size_t d = 0; d < ctx->dom.size(); ++d) {
+        if (ctx->opt.dim == 2) {
+            enqueue_face<2>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false, false, true);
+            enqueue_gather<2>(Lc, ctx->dom[d], (int)d, level, gf, nullptr);
+        } else {
+            enqueue_face<3>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false, false, true);
+            enqueue_gather<3>(Lc, ctx->dom[d], (int)d, level, gf, nullptr);
+        }
+    }
+    if (ctx->opt.dim == 2) enqueue_ghost_wlin<2>(Lc, level);
+    else enqueue_ghost_wlin<3>(Lc, level);
+    // phases: a synchronisation phase, Algorithm 2 (repeated phases dropped), a synchronisation phase
+    const int nc = ctx->lv[level].ncolor;
+    EmuArgs e{};
+    std::vector<int> seq{255};
+    for (int sw = 0; sw < n_sweeps; ++sw)
+        for (int half = 0; half < 2; ++half)
+            for (int cc = 0; cc < nc; ++cc) {
+                const int c = half == 0 ? cc : nc - 1 - cc;
+                if (!(ctx->skip_repeat && seq.size() > 1 && seq.back() == c)) seq.push_back(c);
+            }
+    seq.push_back(255);
+    if ((int)seq.size() > kFlowMaxPh) { ctx->err = "too many phases"; return GMG_EINVAL; }
+    e.ndom = P;
+    e.nph = (int)seq.size();
+    for (size_t k = 0; k < seq.size(); ++k) e.ph[k] = (unsigned short)seq[k];
+    std::vector<EmuDom> ed(P);
+    for (int d = 0; d < P; ++d) {
+        DevLevel &L = ctx->dom[d].dv[level];
+        const DomLevel &H = ctx->dom[d].lv[level];
+        ed[d].a = SweepArgs{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, L.Rt, nullptr, 0, 0};
+        ed[d].p = P2PArgs{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_rec, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
+        for (int c = 0; c <= nc; ++c) ed[d].blk[c] = (int)H.blk[c];
+        ed[d].n_own = (int)H.n_own;
+        ed[d].rank = ctx->dom[d].rank;
+        ed[d].bar = ctx->d_emu_bar + 2 * d;
+    }
+    CK(cudaMemsetAsync(ctx->d_emu_bar, 0, sizeof(int) * 2 * kEmuMaxDom, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_emu, ed.data(), sizeof(EmuDom) * P, cudaMemcpyHostToDevice, ctx->stream));
+    e.dom = (const EmuDom *)ctx->d_emu;
+    int per_sm = 0, nsm = 0;
+    if (ctx->opt.dim == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p2p_emulate<2>, 256, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p2p_emulate<3>, 256, 0);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
+    e.per_group = std::max(1, per_sm * nsm / P);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(e.per_group * P);
+    cfg.blockDim = dim3(256);
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (ctx->opt.dim == 2) CK(cudaLaunchKernelEx(&cfg, k_p2p_emulate<2>, e));
+    else CK(cudaLaunchKernelEx(&cfg, k_p2p_emulate<3>, e));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (Domain &dm : ctx->dom) {
+        int c2 = 0;
+        CK(cudaMemcpy(&c2, dm.dv[0].p2p_ctl + 2, sizeof(int), cudaMemcpyDeviceToHost));
+        if (c2) { ctx->err = "P2P emulation: peer phase wait timed out"; return GMG_ECUDA; }
+    }
+    const int nv = ctx->opt.dim + 2;
+    const int RD = ctx->opt.dim == 3 ? Rec<3>::DW : Rec<2>::DW;
+    if (dW_out) return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.rec; }, nv, dW_out, kRecStride, RD);
     return GMG_OK;
 }
 

@@ -187,6 +187,8 @@ struct gmg_ctx {
     int tailc_grid = 0;               // resident CTAs of k_sweep_tailc
     int tailc_cells = 0;              // largest phase fused (0: one wave at 2 lanes per cell)
     int *d_bar = nullptr;             // grid barrier (count, generation) of k_sweep_tailc
+    char *d_emu = nullptr;            // test only: EmuDom[16] of k_p2p_emulate
+    int *d_emu_bar = nullptr;         // test only: group barriers of k_p2p_emulate
     int flow = 0;                     // dependency-driven persistent sweep (single domain), GMG_FLOW
     int flow_chunk = 512;             // cells per chunk, GMG_FLOW_CHUNK
     int p2p = 0;                      // fused P2P halo instead of pack / transport / unpack per color (GMG_P2P)

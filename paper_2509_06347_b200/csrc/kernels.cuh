@@ -1181,6 +1181,161 @@ __global__ void __launch_bounds__(256, 4) k_sweep_tailc(TailArgs t, int *bar)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Concurrency test of the fused P2P halo protocol on ONE GPU (test only,
+// gmg_p2p_emulate_smooth): the guide-sanctioned way to run mutually waiting
+// ranks on one device -- ONE cooperative launch, one group of blocks per
+// domain ("rank"), all groups resident and running at the same time.  Each
+// group runs its domain's smoothing step phase by phase with exactly the
+// protocol of k_sweep_p2p: wait until every peer's phase count reached its
+// own (acquire), sweep the color block storing boundary increments into the
+// peers' ghost records, then publish the new count (release); a group-wide
+// barrier stands in for the kernel boundaries of the production launches.
+// ---------------------------------------------------------------------------
+constexpr int kEmuMaxDom = 16, kEmuMaxCol = 24;
+struct EmuDom {
+    SweepArgs a;
+    P2PArgs p;
+    int blk[kEmuMaxCol + 1];
+    int n_own, rank;
+    int *bar;                      // [2] group barrier (count, generation)
+};
+struct EmuArgs {
+    int ndom, nph, per_group;
+    const EmuDom *dom;
+    unsigned short ph[kFlowMaxPh];  // color | last << 8, 255 = empty synchronisation phase
+};
+
+__device__ __forceinline__ void group_barrier(int *bar, int nblocks)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int g = ld_acquire(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1) == nblocks - 1) {
+            bar[0] = 0;
+            st_release(bar + 1, g + 1);
+        } else {
+            while (ld_acquire(bar + 1) == g) __nanosleep(32);
+        }
+    }
+    __syncthreads();
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 4) k_p2p_emulate(EmuArgs e)
+{
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    const int grp = blockIdx.x / e.per_group, gb = blockIdx.x % e.per_group;
+    if (grp >= e.ndom) return;
+    const EmuDom &dm = e.dom[grp];
+    const SweepArgs &a = dm.a;
+    const P2PArgs &p = dm.p;
+    const int nthr = e.per_group * blockDim.x, gtid = gb * blockDim.x + threadIdx.x;
+    __shared__ int s_bad;
+    for (int k = 0; k < e.nph; ++k) {
+        // wait: every peer completed as many phases as this rank
+        if (threadIdx.x == 0) {
+            s_bad = 0;
+            const int target = *(volatile int *)p.ctl;
+            for (int t = 0; t < p.np && !s_bad; ++t)
+                for (int spin = 0; ld_acquire(p.flags + p.wait_rank[t]) < target; ++spin) {
+                    if (spin > (1 << 24)) { atomicExch(p.ctl + 2, 1); s_bad = 1; break; }
+                    __nanosleep(64);
+                }
+        }
+        __syncthreads();
+        if (s_bad) return;
+        const int code = e.ph[k];
+        const int c = code & 255;
+        if (c != 255) {
+            double *Wout = (code >> 8 & 1) ? a.Wout : nullptr;
+            const int b0 = dm.blk[c], b1 = dm.blk[c + 1];
+            const int L = 2, per = nthr / L;
+            const int rounds = (b1 - b0 + per - 1) / per;
+            for (int r = 0; r < rounds; ++r) {
+                const int i = b0 + r * per + gtid / L, sub = gtid % L;
+                const bool valid = i < b1;
+                double acc[NV];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+                if (valid) {
+                    const int2 sd = __ldg(a.sinfo + i);
+                    for (int e2 = sd.x + sub; e2 < sd.x + sd.y; e2 += L) {
+                        const int j = __ldg(a.sJe + e2);
+                        double sr[4];
+                        ld4cs(a.sRe + (size_t)e2 * kSlotRec, sr);
+                        const double *rj = a.rec + (size_t)j * RC::STRIDE;
+                        double w[NV], dw[NV];
+                        if constexpr (D == 3) {
+                            double c0[4], c1[4], c2[4];
+                            ld4cg(rj, c0);
+                            ld4cg(rj + 4, c1);
+                            ld4cg(rj + 8, c2);
+                            w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
+                            dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                        } else {
+                            ld4cg(rj, w);
+                            ld4cg(rj + 4, dw);
+                        }
+                        flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 1);
+                if (valid && sub == 0) {
+                    double *ri = a.rec + (size_t)i * RC::STRIDE;
+                    const size_t o = (size_t)i * NV;
+                    double rr[NV], c1[4], c2[4];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) rr[q] = __ldcs(a.rhs + o + q);
+                    ld4cg(ri + 4, c1);
+                    ld4cg(ri + 8, c2);
+                    double d[NV];
+                    if constexpr (D == 3) {
+                        const double invD = c2[2], ha = c2[3];
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) d[q] = -(rr[q] + ha * acc[q]) * invD;
+                        const double w1[4] = {c1[0], d[0], d[1], d[2]};
+                        st4(ri + 4, w1);
+                        c2[0] = d[3];
+                        c2[1] = d[4];
+                        st4(ri + 8, c2);
+                        if (Wout) {
+                            double c0[4];
+                            ld4cg(ri, c0);
+                            for (int q = 0; q < 4; ++q) Wout[o + q] = c0[q] + d[q];
+                            Wout[o + 4] = c1[0] + d[4];
+                        }
+                    } else {
+                        const double invD = c2[0], ha = c2[1];
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) d[q] = -(rr[q] + ha * acc[q]) * invD;
+                        st4(ri + 4, d);
+                        if (Wout) {
+                            double c0[4];
+                            ld4cg(ri, c0);
+                            for (int q = 0; q < NV; ++q) Wout[o + q] = c0[q] + d[q];
+                        }
+                    }
+                    p2p_store<D, true>(p, i, d);
+                }
+            }
+        }
+        // the kernel boundary of the production launches: the group's stores, then the release
+        __threadfence();
+        group_barrier(dm.bar, e.per_group);
+        if (gb == 0 && threadIdx.x == 0) {
+            const int ph = p.ctl[0] + 1;
+            p.ctl[0] = ph;
+            __threadfence();
+            for (int t = 0; t < p.np; ++t) st_release(p.sig[t], ph);
+        }
+        group_barrier(dm.bar, e.per_group);   // ctl[0] visible to the group before the next wait
+    }
+}
+
 __device__ __forceinline__ void ld4(const double *p, double *v)
 {
     asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"

@@ -30,7 +30,7 @@ ABI_SYMBOLS = ["gmg_default_options", "gmg_create", "gmg_load_mesh", "gmg_set_co
                "gmg_set_workspace", "gmg_set_state", "gmg_set_level_state", "gmg_get_state", "gmg_set_alpha",
                "gmg_residual", "gmg_set_level_inputs", "gmg_smooth", "gmg_vcycle", "gmg_profile_vcycle",
                "gmg_time_smooth", "gmg_vcycle_launches", "gmg_partition_rcb", "gmg_get_halo", "gmg_p2p_layout",
-               "gmg_p2p_import", "gmg_get_p2p_targets", "gmg_last_error", "gmg_destroy"]
+               "gmg_p2p_import", "gmg_get_p2p_targets", "gmg_p2p_emulate_smooth", "gmg_last_error", "gmg_destroy"]
 
 
 class GmgError(RuntimeError):
@@ -87,6 +87,7 @@ def lib():
             "gmg_p2p_layout": (I, [P, P]),
             "gmg_p2p_import": (I, [P, P, P, P]),
             "gmg_get_p2p_targets": (I, [P, I, I, P, P, P, P]),
+            "gmg_p2p_emulate_smooth": (I, [P, I, I, P]),
             "gmg_last_error": (C.c_char_p, [P]),
             "gmg_destroy": (None, [P]),
         }
@@ -299,6 +300,13 @@ def gmg_get_p2p_targets(ctx, level, dom=0):
     g = np.zeros(nt.value, np.int32)
     _check(ctx, lib().gmg_get_p2p_targets(ctx, level, dom, None, _ptr(off), _ptr(k), _ptr(g)))
     return off, k, g
+
+
+def gmg_p2p_emulate_smooth(ctx, level, n_sweeps, nv, n):
+    """Test only: all local domains' smoothing step in one cooperative launch (see include/gmg.h)."""
+    dW = np.zeros((nv, n))
+    _check(ctx, lib().gmg_p2p_emulate_smooth(ctx, level, n_sweeps, _ptr(dW)))
+    return dW
 
 
 def gmg_last_error(ctx):

@@ -148,3 +148,24 @@ def test_partitioned_variants_parity(G, orc, mode, kw, monkeypatch):
     assert rel(s.get_state(0), Wo) <= TOL
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
     s.close()
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("level", [0, 1])
+def test_p2p_protocol_under_concurrency(G, monkeypatch, P, level):
+    """The fused-P2P-halo protocol with the domains running at the SAME time:
+    one cooperative launch, one block group per domain, each waiting on its
+    peers' phase counts (the single-GPU stand-in for ranks that wait on one
+    another).  Same increments as the sequential launches (up to the
+    summation order of the lanes per cell)."""
+    monkeypatch.setenv("GMG_P2P", "1")
+    m, Winf, W = _case("sphere")
+    part = G.gmg_partition_rcb(m.ctr, P)
+    s = G.Solver(m, n_levels=3, part=part, local_domains=P)
+    s.set_state(W, Winf)
+    s.vcycle(1)
+    ref = s.smooth(level, 4)
+    emu = G.gmg_p2p_emulate_smooth(s.ctx, level, 4, s.nv, s.n_cells(level))
+    assert np.all(np.isfinite(emu))
+    assert rel(emu, ref) <= 1e-12
+    s.close()
