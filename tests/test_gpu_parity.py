@@ -296,3 +296,17 @@ def test_zero_term_skip_is_roundoff_exact(G, orc, name, monkeypatch):
     for x, y in zip(a[2], b[2]):
         assert rel(x, y) <= 1e-13
     assert rel(a[3], b[3]) <= 1e-12
+
+
+@pytest.mark.slow
+def test_config2_long_history(G, orc):
+    """BASELINE configs[1] (NACA0012, impulsive start) over 200 V-cycles: the
+    residual history stays on the oracle's to 1e-10 of r0 per component and
+    the final state to 1e-10 (no drift from reassociation over a long run)."""
+    m = configs.config(2)
+    fs = configs.FREESTREAM[2]
+    Winf = state.winf(*fs)
+    W = state.uniform(m, *fs)
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 200)
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+    assert rel(Wg, Wo) <= TOL
