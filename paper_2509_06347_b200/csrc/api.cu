@@ -16,6 +16,7 @@
 
 #include "gmg_internal.h"
 #include "kernels.cuh"
+#include "kernels_tried.cuh"
 
 using namespace gmg;
 
