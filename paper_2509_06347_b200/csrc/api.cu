@@ -366,6 +366,12 @@ void launch_sweep(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, const 
     const int minb = ctx->minb, sweep_var = ctx->sweep_var;
     const bool pdl = ctx->pdl != 0;
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
+    if (ctx->sweep_bs == 128 && sweep_var == 3 && minb == 4) {   // default; the variants run at 256
+        int nb = (int)((nthreads + 127) / 128);
+        if (ctx->sweep_grid_cap > 0) nb = std::min(nb, 2 * ctx->sweep_grid_cap);
+        launch_with_window(k_sweep128<D, LPC>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl);
+        return;
+    }
     int nb = nblk(nthreads);
     if (ctx->sweep_grid_cap > 0) nb = std::min(nb, ctx->sweep_grid_cap);
     const dim3 g(nb), b(256);
@@ -1357,6 +1363,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         int waves = 1, nsm = 0, per_sm = 0;
         if (const char *e = std::getenv("GMG_SWEEP_WAVES")) waves = std::atoi(e);
         if (const char *e = std::getenv("GMG_SWEEPV")) ctx->sweep_var = std::atoi(e);
+        if (const char *e = std::getenv("GMG_SWEEP_BS")) ctx->sweep_bs = std::atoi(e);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
         if (ctx->opt.dim == 3)
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, 4, 3>, 256, 0);

@@ -731,6 +731,13 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
     sweep_body<D, LPC, VAR, false>(a, P2PArgs{});
 }
 
+// the default sweep launch: 128-thread blocks, 8 per SM (GMG_SWEEP_BS=256 -> k_sweep)
+template <int D, int LPC>
+__global__ void __launch_bounds__(128, 8) k_sweep128(SweepArgs a)
+{
+    sweep_body<D, LPC, 3, false>(a, P2PArgs{});
+}
+
 __device__ __forceinline__ int ld_acquire_sys(const int *p)
 {
     int v;
