@@ -22,14 +22,16 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gmg_oracle.c")
+_SRC3 = os.path.join(_HERE, "cgks3.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC),
+                                                                          os.path.getmtime(_SRC3)):
         subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-o", _LIB, _SRC, "-lm"])
+                               "-shared", "-o", _LIB, _SRC, _SRC3, "-lm"])
     return _LIB
 
 

@@ -370,6 +370,12 @@ static void ghost_state(int dim, int kind, const double *Wi, const double *Winf,
     }
 }
 
+/* exported for cgks3.c (NEXT-1): the same ghost states */
+void orc_ghost(int dim, int kind, const double *Wi, const double *Winf, const double *n, double *Wg)
+{
+    ghost_state(dim, kind, Wi, Winf, n, Wg);
+}
+
 /* ===================================================================== */
 /* O4. First-order KFVS flux (coarse operator named at P:637; free-       */
 /* transport of two Maxwellians) per unit area along unit n:   */

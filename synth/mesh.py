@@ -48,6 +48,11 @@ class Mesh:
     patch_kind: np.ndarray   # [n_patches] int32
     name: str = ""
     meta: dict = field(default_factory=dict)
+    # high-order geometry (NEXT-1, third-order CGKS fine operator):
+    m2: np.ndarray = None    # [d(d+1)/2][n] central second moments (1/|Omega|) int (x-x_c)_a (x-x_c)_b dV,
+                             #   components xx, xy, (xz,) yy, (yz, zz)  -- upper triangle, row major
+    gp: np.ndarray = None    # [d][G][nf] face Gauss points (G = 2 in 2D, 4 in 3D; triangles pad slot 3)
+    gw: np.ndarray = None    # [G][nf] Gauss weights, sum_k gw[k][f] = 1 (padding weight 0)
 
     @property
     def n_cells(self) -> int:
@@ -62,8 +67,9 @@ class Mesh:
         return int(np.count_nonzero(self.right >= 0))
 
     def contiguous(self) -> "Mesh":
-        for k in ("vol", "ctr", "avec", "fctr"):
-            setattr(self, k, np.ascontiguousarray(getattr(self, k), dtype=np.float64))
+        for k in ("vol", "ctr", "avec", "fctr", "m2", "gp", "gw"):
+            if getattr(self, k) is not None:
+                setattr(self, k, np.ascontiguousarray(getattr(self, k), dtype=np.float64))
         self.left = np.ascontiguousarray(self.left, dtype=np.int64)
         self.right = np.ascontiguousarray(self.right, dtype=np.int64)
         self.ngauss = np.ascontiguousarray(self.ngauss, dtype=np.int8)
@@ -80,6 +86,75 @@ def _cross(a, b):
 def _tet_vol_ctr(a, b, c, d):
     v = np.abs(np.einsum("ij,ij->i", b - a, _cross(c - a, d - a))) / 6.0
     return v, (a + b + c + d) / 4.0
+
+
+def _simplex_m2(P, scale):
+    """sum over a simplex of int x_a x_b for vertices P (list of [k][d], already
+    shifted to the cell centroid): scale * (sum_i p_ia p_ib + (sum_i p_ia)(sum_i p_ib)),
+    scale = |T|/12 (triangle) or |T|/20 (tetrahedron).  Returns [k][d][d]."""
+    S = sum(P)
+    out = np.einsum("ka,kb->kab", S, S)
+    for p in P:
+        out += np.einsum("ka,kb->kab", p, p)
+    return out * scale[:, None, None]
+
+
+def _cell_m2(dim, nodes, cell_type, conn, ctr, vol):
+    """central second moments (1/|Omega|) int (x-x_c)(x-x_c)^T dV, exact for the
+    straight-sided cells (fan triangulation / tetrahedral split of the cell)."""
+    n = cell_type.shape[0]
+    M = np.zeros((n, dim, dim))
+    for t in np.unique(cell_type):
+        idx = np.nonzero(cell_type == t)[0]
+        c = conn[idx]
+        X = [nodes[c[:, i]] - ctr[idx] for i in range(_NNODES[int(t)])]
+        if t in (TRI2, QUAD2):
+            tris = [(0, 1, 2)] if t == TRI2 else [(0, 1, 2), (0, 2, 3)]
+            for (a, b, cc) in tris:
+                e1, e2 = X[b] - X[a], X[cc] - X[a]
+                ar = 0.5 * np.abs(e1[:, 0] * e2[:, 1] - e1[:, 1] * e2[:, 0])
+                M[idx] += _simplex_m2([X[a], X[b], X[cc]], ar / 12.0)
+        else:
+            tets = [(0, 1, 2, 3)] if t == TET else [(0, 1, 2, 5), (0, 1, 5, 4), (0, 4, 5, 3)]
+            for (a, b, cc, d) in tets:
+                v = np.abs(np.einsum("ij,ij->i", X[b] - X[a], _cross(X[cc] - X[a], X[d] - X[a]))) / 6.0
+                M[idx] += _simplex_m2([X[a], X[b], X[cc], X[d]], v / 20.0)
+    M /= vol[:, None, None]
+    iu = np.triu_indices(dim)
+    return np.ascontiguousarray(M[:, iu[0], iu[1]].T)
+
+
+def _face_gauss(dim, nodes, fnodes):
+    """Gauss points of every face (PAPER.md:164-176: 3 per triangle, 4 per quad;
+    2 per 2D segment) and weights normalised to sum 1 over the face."""
+    nf = fnodes.shape[0]
+    if dim == 2:
+        a, b = nodes[fnodes[:, 0]], nodes[fnodes[:, 1]]
+        h = (b - a) / (2.0 * np.sqrt(3.0))
+        m = 0.5 * (a + b)
+        gp = np.stack([m - h, m + h], axis=0)                      # [G][nf][d]
+        gw = np.full((2, nf), 0.5)
+    else:
+        gp = np.zeros((4, nf, 3))
+        gw = np.zeros((4, nf))
+        tri = fnodes[:, 3] < 0
+        a, b, c = (nodes[fnodes[tri, i]] for i in range(3))
+        for k, (l0, l1, l2) in enumerate([(2 / 3, 1 / 6, 1 / 6), (1 / 6, 2 / 3, 1 / 6), (1 / 6, 1 / 6, 2 / 3)]):
+            gp[k, tri] = l0 * a + l1 * b + l2 * c
+            gw[k, tri] = 1.0 / 3.0
+        gp[3, tri] = (a + b + c) / 3.0
+        q = ~tri
+        a, b, c, d = (nodes[fnodes[q, i]] for i in range(4))
+        g = 1.0 / np.sqrt(3.0)
+        for k, (xi, eta) in enumerate([(-g, -g), (g, -g), (g, g), (-g, g)]):
+            N = [(1 - xi) * (1 - eta) / 4, (1 + xi) * (1 - eta) / 4, (1 + xi) * (1 + eta) / 4, (1 - xi) * (1 + eta) / 4]
+            gp[k, q] = N[0] * a + N[1] * b + N[2] * c + N[3] * d
+            dxi = (-(1 - eta) * a + (1 - eta) * b + (1 + eta) * c - (1 + eta) * d) / 4
+            deta = (-(1 - xi) * a - (1 + xi) * b + (1 + xi) * c + (1 - xi) * d) / 4
+            J = _cross(dxi, deta)
+            gw[k, q] = np.sqrt((J * J).sum(1))
+        gw[:, q] /= gw[:, q].sum(0)[None, :]
+    return np.ascontiguousarray(np.transpose(gp, (2, 0, 1))), gw
 
 
 def build_mesh(dim, nodes, cell_type, conn, patch_of, patch_kind, name="", meta=None) -> Mesh:
@@ -206,9 +281,11 @@ def build_mesh(dim, nodes, cell_type, conn, patch_of, patch_kind, name="", meta=
         right = right.copy()
         right[bnd] = -(pidx + 1)
 
+    gp, gw = _face_gauss(dim, nodes, fnodes)
     m = Mesh(dim=dim, vol=vol, ctr=np.ascontiguousarray(ctr.T), left=left, right=right,
              avec=np.ascontiguousarray(avec.T), fctr=np.ascontiguousarray(fctr.T), ngauss=ngauss,
-             patch_kind=np.asarray(patch_kind, dtype=np.int32), name=name, meta=dict(meta or {}))
+             patch_kind=np.asarray(patch_kind, dtype=np.int32), name=name, meta=dict(meta or {}),
+             m2=_cell_m2(dim, nodes, cell_type, conn, ctr, vol), gp=gp, gw=gw)
     m.meta.setdefault("n_nodes", int(nodes.shape[0]))
     m.meta.setdefault("cell_type_counts", {int(t): int(np.count_nonzero(cell_type == t)) for t in np.unique(cell_type)})
     return m.contiguous()
