@@ -99,6 +99,17 @@ typedef struct {
                                Algorithm 3 (agglomeration) on `device`.
                                The results are identical to the host setup (0, default):
                                same colors, renumbering and parent maps, bit for bit.         */
+    int fine_operator;      /* fine-level residual of the V-cycle:
+                               0 = first-order KFVS (O4, default); 1 = third-order compact GKS
+                               (§2.3-§3; readings C1-C14 of DESIGN.md §12):
+                               p2/p1 WENO + DF reconstruction from the cell averages and the
+                               cell-averaged slopes, BGK flux at the face Gauss points, direct
+                               slope evolution.  Needs gmg_load_ho_geometry, a single domain
+                               (nranks = local_domains = 1), fine_smoother = 0, df_mode = 0.  */
+    double ho_c1, ho_c2;    /* C9 collision time tau = c1 Dt + c2 Dt |pl - pr| / (pl + pr);
+                               defaults 0.05, 1.0                                              */
+    double ho_gam0;         /* C5 linear weight of the large (p2) stencil; default 0.95        */
+    double ho_eps;          /* C5 WENO-Z epsilon; default 1e-14                                */
 } gmg_options;
 
 /* Fill *o with the defaults above (dim = 3, single rank, device 0, stream 0). */
@@ -198,7 +209,7 @@ gmg_status gmg_vcycle(gmg_ctx *ctx, int n_cycles, double *res_hist);
  * (GMG_K_* below).  bytes_out[k] = algorithmic bytes moved by class k over
  * the run.  Arrays of length GMG_K_COUNT. */
 enum { GMG_K_FACE = 0, GMG_K_GATHER = 1, GMG_K_SWEEP = 2, GMG_K_RESTRICT = 3, GMG_K_PROLONG = 4,
-       GMG_K_NORM = 5, GMG_K_COUNT = 6 };
+       GMG_K_NORM = 5, GMG_K_HO_RECON = 6, GMG_K_HO_FLUX = 7, GMG_K_COUNT = 8 };
 gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_t *count_out, double *bytes_out);
 
 /* Sweep-only instrumentation: time one smoothing step's sweeps on `level`
@@ -255,6 +266,40 @@ gmg_status gmg_p2p_layout(gmg_ctx *ctx, int64_t *out);
 gmg_status gmg_get_p2p_targets(gmg_ctx *ctx, int level, int dom, int64_t *n_targets, int32_t *off,
                                int32_t *peer_slot, int32_t *ghost_local);
 gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base_off, const int64_t *layouts);
+/* ---------------------------------------------------------------------------
+ * NEXT-1: third-order compact GKS fine operator (fine_operator = 1,
+ * DESIGN.md §12).  Single domain only (GMG_EINVAL otherwise).
+ * ------------------------------------------------------------------------- */
+
+/* High-order fine-level geometry (host, natural order; after gmg_load_mesh,
+ * before gmg_workspace_bytes): m2[nq][n] central second moments
+ * (1/|Omega|) int (x - x_c)_a (x - x_c)_b dV, components a <= b row major
+ * (2D xx, xy, yy; 3D xx, xy, xz, yy, yz, zz) -- the p2 moments of P:318-322;
+ * gp[dim][G][nf] face Gauss points and gw[G][nf] weights summing to 1 per
+ * face (3 per triangle, 4 per quad, 2 per 2D segment; G = 4 in
+ * 3D, 2 in 2D; unused slots weight 0).  Copied; the caller keeps ownership.
+ * GMG_EINVAL on a bad G / NULL pointer, GMG_ESTATE before gmg_load_mesh. */
+gmg_status gmg_load_ho_geometry(gmg_ctx *ctx, const double *m2, int G, const double *gp, const double *gw);
+
+/* Cell-averaged slopes G[nv][dim][n] (component q, direction e at (q*dim+e)*n
+ * + i) and the carried DF alpha[n] (host/device, natural order); NULL = the
+ * initial values of reading C1 (G = 0, alpha = 1).  gmg_set_state does not
+ * touch them. */
+gmg_status gmg_set_ho_state(gmg_ctx *ctx, const double *G, const double *alpha);
+gmg_status gmg_get_ho_state(gmg_ctx *ctx, double *G_out, double *alpha_out);
+
+/* One evaluation of the operator at the current (W, G, alpha), no state
+ * change (readings C2-C13): R_out[nv][n] time-averaged flux sum (C11),
+ * G_out[nv][dim][n] the evolved slopes times DF (C13), alpha_out[n] (C7),
+ * sigma_out[n] (C8); any may be NULL.  Natural order, host/device. */
+gmg_status gmg_ho_residual(gmg_ctx *ctx, double *R_out, double *G_out, double *alpha_out, double *sigma_out);
+
+/* The reconstruction alone (C2-C6): poly_out[nv*nc][n] with nc = 1 + dim + nq,
+ * per component (c0, lin[dim], quad[nq]) of p(x) = c0 + lin . y + sum_k quad_k
+ * y_a y_b, y = x - x_cell (natural order); flags_out[n] bit 0 = p2 used,
+ * bit 1 = positivity fallback (C6b).  Either may be NULL. */
+gmg_status gmg_ho_recon(gmg_ctx *ctx, double *poly_out, int32_t *flags_out);
+
 /* Test only: one smoothing step (as gmg_smooth) of ALL local domains
  * (local_domains >= 2, GMG_P2P=1) in ONE cooperative launch with one block
  * group per domain, so that the fused-P2P-halo protocol (wait for the peers'

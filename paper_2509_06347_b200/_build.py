@@ -41,20 +41,27 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     bdir = os.path.join(HERE, "build")
     os.makedirs(bdir, exist_ok=True)
     inc = ["-I", os.path.join(CUDA, "include"), "-I", os.path.join(HERE, "..", "include")]
-    o_setup = os.path.join(bdir, "setup.o")
-    _run(["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-Wall", "-c",
-          os.path.join(CSRC, "setup.cpp"), "-o", o_setup] + inc)
-    o_api = os.path.join(bdir, "api.o")
+    gxx = ["g++", "-O2", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-Wall", "-c"]
     flags = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                        "--expt-relaxed-constexpr"]
     if verbose_ptxas:
         flags += ["-Xptxas", "-v"]
-    _run([NVCC] + flags + ["-c", os.path.join(CSRC, "api.cu"), "-o", o_api] + inc)
-    # device-side setup: no FMA contraction anywhere (bit-identical decisions to the host setup)
-    o_sdev = os.path.join(bdir, "setup_dev.o")
-    _run([NVCC] + flags + ["--fmad=false", "-c", os.path.join(CSRC, "setup_dev.cu"), "-o", o_sdev] + inc)
+    objs, jobs = [], []
+    nv = [NVCC] + flags + ["-c"]
+    for src, cmd in (("setup.cpp", gxx), ("ho_setup.cpp", gxx), ("api.cu", nv),
+                     ("ho.cu", nv),
+                     # device-side setup: no FMA contraction anywhere (bit-identical decisions to the host setup)
+                     ("setup_dev.cu", nv + ["--fmad=false"])):
+        o = os.path.join(bdir, os.path.splitext(src)[0] + ".o")
+        full = cmd + [os.path.join(CSRC, src), "-o", o] + inc
+        print(" ".join(full), file=sys.stderr)
+        jobs.append((full, subprocess.Popen(full)))
+        objs.append(o)
+    for full, pr in jobs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, full)
     tmp = OUT + ".tmp"
-    _run([NVCC] + GENCODE + ["-shared", "-o", tmp, o_setup, o_api, o_sdev, "-cudart", "static", "-lgomp"])
+    _run([NVCC] + GENCODE + ["-shared", "-o", tmp] + objs + ["-cudart", "static", "-lgomp"])
     os.replace(tmp, OUT)
     return OUT
 

@@ -18,6 +18,12 @@
 #include "kernels.cuh"
 #include "kernels_tried.cuh"
 
+namespace gmg {
+// ho.cu (NEXT-1): which = 0 k_ho_sr, 1 k_ho_recon, 2 k_ho_flux, 3 k_ho_gather(mode)
+void ho_launch(int which, const DevLevel &L, const HoDev &H, const Phys &ph, const BCs &bc, const gmg_options &o,
+               int mode, double *Rout, double *aout, cudaStream_t s);
+}
+
 using namespace gmg;
 
 #define CK(x)                                                                         \
@@ -684,6 +690,36 @@ void enqueue_restrict(Launcher &Lc, Domain &dm, int l)
     Lc.post(GMG_K_RESTRICT, dm.lbytes[l].restrict_);
 }
 
+// NEXT-1: one evaluation of the third-order CGKS operator on the fine level
+// (ho.cu): S r, reconstruction, Gauss-point BGK fluxes, gather(mode)
+void enqueue_ho_eval(Launcher &Lc, int mode, double *Rout = nullptr, double *aout = nullptr, bool recon_only = false)
+{
+    gmg_ctx *ctx = Lc.ctx;
+    Domain &dm = ctx->dom[0];
+    DevLevel &L = dm.dv[0];
+    const HoHost &H = *ctx->ho;
+    const Phys ph = phys(ctx);
+    const BCs bc = bcs(ctx);
+    Lc.pre(GMG_K_HO_RECON);
+    ho_launch(0, L, H.dev, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
+    Lc.post(GMG_K_HO_RECON, H.bytes_sr);
+    Lc.pre(GMG_K_HO_RECON);
+    ho_launch(1, L, H.dev, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
+    Lc.post(GMG_K_HO_RECON, H.bytes_recon);
+    if (recon_only) return;
+    Lc.pre(GMG_K_HO_FLUX);
+    ho_launch(2, L, H.dev, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
+    Lc.post(GMG_K_HO_FLUX, H.bytes_flux);
+    Lc.pre(GMG_K_GATHER);
+    ho_launch(3, L, H.dev, ph, bc, ctx->opt, mode, Rout, aout, Lc.s);
+    Lc.post(GMG_K_GATHER, H.bytes_gather);
+    if (mode & HO_NORM) {
+        Lc.pre(GMG_K_NORM);
+        klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(256), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq);
+        Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
+    }
+}
+
 // O8 -- one V-cycle, all on the device
 template <int D>
 void enqueue_vcycle(Launcher &Lc)
@@ -692,6 +728,14 @@ void enqueue_vcycle(Launcher &Lc)
     const int nl = (int)ctx->lv.size();
     const bool df0 = ctx->opt.df_mode == 0 || ctx->opt.df_mode == 3;   // DF helper alpha (prolongation)
     auto &doms = ctx->dom;
+    if (ctx->opt.fine_operator == 1) {
+        // NEXT-1, reading C14: CGKS3 evaluation at (W, G, alpha) -> history, Eq.(smo), slopes, DF;
+        // a second evaluation at the updated state -> restricted residual and DF
+        enqueue_ho_eval(Lc, HO_NORM | HO_UPDATE);
+        enqueue_norm_hist(Lc);
+        if (nl == 1) return;
+        enqueue_ho_eval(Lc, HO_RT);
+    } else {
     // 1-2. fine residual at the cycle start (history entry) + fine pre-smoothing
     enqueue_exchange<D>(Lc, 0, EX_W, -1);
     for (Domain &dm : doms)
@@ -717,6 +761,7 @@ void enqueue_vcycle(Launcher &Lc)
     for (size_t d = 0; d < doms.size(); ++d) {
         enqueue_face<D>(Lc, doms[d], 0, doms[d].dv[0].W, true, false, df0);
         enqueue_gather<D>(Lc, doms[d], (int)d, 0, G_FLUX | G_WRITE_RT | (df0 ? G_ALPHA : 0), nullptr);
+    }
     }
     // 4. coarse levels
     for (int l = 1; l < nl; ++l) {
@@ -750,6 +795,11 @@ template <int D>
 void enqueue_final_norm(Launcher &Lc)
 {
     gmg_ctx *ctx = Lc.ctx;
+    if (ctx->opt.fine_operator == 1) {
+        enqueue_ho_eval(Lc, HO_NORM);
+        enqueue_norm_hist(Lc);
+        return;
+    }
     enqueue_exchange<D>(Lc, 0, EX_W, -1);
     for (size_t d = 0; d < ctx->dom.size(); ++d) {
         enqueue_face<D>(Lc, ctx->dom[d], 0, ctx->dom[d].dv[0].W, true, false);
@@ -887,6 +937,32 @@ void carve(gmg_ctx *ctx, Bump &b)
     ctx->d_emu = b.take<char>(sizeof(EmuDom) * kEmuMaxDom);
     ctx->d_emu_bar = b.take<int>(2 * kEmuMaxDom);
     ctx->d_sumsq = b.take<double>((size_t)std::max<size_t>(1, ctx->dom.size()) * nv);
+    if (ctx->ho && ctx->ho->prepared) {                       // NEXT-1 (fine level, single domain)
+        HoHost &H = *ctx->ho;
+        HoDev &V = H.dev;
+        const DomLevel &D0 = ctx->dom[0].lv[0];
+        const int64_t n = D0.n_own, nf = D0.nf;
+        V.G = H.G;
+        V.nq = d * (d + 1) / 2;
+        V.nk = d + V.nq;
+        V.nc = 1 + V.nk;
+        V.ctr = b.take<double>((size_t)n * d);
+        V.m2 = b.take<double>((size_t)n * V.nq);
+        V.gp = b.take<double>((size_t)nf * H.G * d);
+        V.gw = b.take<double>((size_t)nf * H.G);
+        V.hfoff = b.take<int>(n + 1);
+        V.hface = b.take<int>(H.hface.size());
+        V.poff = b.take<int>(n + 1);
+        V.P = b.take<double>(H.P.size());
+        V.G_ = b.take<double>((size_t)n * nv * d);
+        V.alpha = b.take<double>(n);
+        V.poly = b.take<double>((size_t)n * nv * V.nc);
+        V.flags = b.take<int>(n);
+        V.sr = b.take<double>(nf);
+        V.dt = b.take<double>(n);
+        V.frec = b.take<double>((size_t)nf * 12);
+        V.Gout = b.take<double>((size_t)n * nv * d);
+    }
 }
 
 void compute_bytes(gmg_ctx *ctx)
@@ -984,6 +1060,11 @@ void gmg_default_options(gmg_options *o)
     o->local_domains = 1;
     o->setup_device = 0;
     o->beta = 0.5;
+    o->fine_operator = 0;
+    o->ho_c1 = 0.05;
+    o->ho_c2 = 1.0;
+    o->ho_gam0 = 0.95;
+    o->ho_eps = 1e-14;
 }
 
 gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
@@ -993,6 +1074,10 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     if ((opt->dim != 2 && opt->dim != 3) || !(opt->gamma > 1.0) || !(opt->cfl_imp > 0) || !(opt->cfl_exp > 0) ||
         opt->n_sweeps < 1 || opt->n_levels < 1 || opt->n_levels > 3 || opt->pre_smooth != 1 || opt->post_smooth != 0 ||
         !(opt->r_factor >= 1.0) || opt->fine_smoother < 0 || opt->fine_smoother > 1 || opt->df_mode < 0 ||
+        opt->fine_operator < 0 || opt->fine_operator > 1 ||
+        (opt->fine_operator == 1 && (opt->fine_smoother != 0 || opt->df_mode != 0 || !(opt->ho_c1 > 0.0) ||
+                                     !(opt->ho_c2 >= 0.0) || !(opt->ho_gam0 > 0.0 && opt->ho_gam0 <= 1.0) ||
+                                     !(opt->ho_eps > 0.0))) ||
         opt->df_mode > 3 || (opt->df_mode == 3 && !(opt->beta >= 0.0 && opt->beta <= 1.0)) || opt->nranks < 1 ||
         opt->rank < 0 || opt->rank >= opt->nranks || opt->local_domains < 1 ||
         opt->local_domains > 64 || (opt->nranks > 1 && (opt->local_domains != 1 || !opt->nccl_id)) ||
@@ -1224,6 +1309,7 @@ gmg_status gmg_get_level_geometry(gmg_ctx *ctx, int level, double *vol, double *
 size_t gmg_workspace_bytes(gmg_ctx *ctx)
 {
     if (!ctx || !ctx->built) return 0;
+    if (ctx->ho && ho_prepare(ctx) != GMG_OK) return 0;
     Bump b{nullptr};
     carve(ctx, b);
     return b.off + 256;
@@ -1234,6 +1320,11 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
     if (!ctx) return GMG_EINVAL;
     if (!ctx->built) { ctx->err = "hierarchy not built"; return GMG_ESTATE; }
     if (!dptr || ((uintptr_t)dptr & 15)) { ctx->err = "workspace must be a 16-byte aligned device pointer"; return GMG_EINVAL; }
+    if (ctx->ho) {
+        const gmg_status hs = ho_prepare(ctx);
+        if (hs) return hs;
+    }
+    if (ctx->opt.fine_operator == 1 && !ctx->ho) { ctx->err = "fine_operator 1 needs gmg_load_ho_geometry"; return GMG_ESTATE; }
     const size_t need = gmg_workspace_bytes(ctx);
     if (bytes < need) { ctx->err = "workspace too small: need " + std::to_string(need); return GMG_ENOMEM; }
     CK(cudaSetDevice(ctx->opt.device));
@@ -1409,6 +1500,25 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             return GMG_ENCCL;
         }
         ctx->nccl_comm = comm;
+    }
+    if (ctx->ho) {
+        HoHost &H = *ctx->ho;
+        HoDev &V = H.dev;
+        const int64_t n = ctx->dom[0].lv[0].n_own;
+        const int nvd = (ctx->opt.dim + 2) * ctx->opt.dim;
+        CK(cudaMemcpyAsync((void *)V.ctr, H.ctr.data(), H.ctr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync((void *)V.m2, H.m2l.data(), H.m2l.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync((void *)V.gp, H.gpl.data(), H.gpl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync((void *)V.gw, H.gwl.data(), H.gwl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync((void *)V.hfoff, H.hfoff.data(), H.hfoff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync((void *)V.hface, H.hface.data(), H.hface.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync((void *)V.poff, H.poff.data(), H.poff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        if (!H.P.empty())
+            CK(cudaMemcpyAsync((void *)V.P, H.P.data(), H.P.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+        k_fill<<<nblk(n * nvd), 256, 0, ctx->stream>>>((int)(n * nvd), V.G_, 0.0);   // reading C1
+        k_fill<<<nblk(n), 256, 0, ctx->stream>>>((int)n, V.alpha, 1.0);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     if (ctx->graph) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
     ctx->ws_ready = true;
@@ -1908,6 +2018,105 @@ gmg_status gmg_get_halo(gmg_ctx *ctx, int level, int dom, int64_t *n_owned, int6
 
 const char *gmg_last_error(gmg_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+// ---------------------------------------------------------------- NEXT-1
+gmg_status gmg_load_ho_geometry(gmg_ctx *ctx, const double *m2, int G, const double *gp, const double *gw)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->mesh_loaded) { ctx->err = "gmg_load_ho_geometry before gmg_load_mesh"; return GMG_ESTATE; }
+    if (ctx->ws_ready) { ctx->err = "gmg_load_ho_geometry after gmg_set_workspace"; return GMG_ESTATE; }
+    const int d = ctx->opt.dim;
+    if (!m2 || !gp || !gw || G != (d == 3 ? 4 : 2)) { ctx->err = "ho geometry: null pointer or G != 4 (3D) / 2 (2D)"; return GMG_EINVAL; }
+    if (ctx->opt.nranks != 1 || ctx->opt.local_domains > 1) { ctx->err = "ho geometry: single domain only"; return GMG_EINVAL; }
+    const HostLevel &L0 = ctx->lv[0];
+    const int64_t n = L0.n, nf = L0.nf;
+    const int nq = d * (d + 1) / 2;
+    delete ctx->ho;
+    ctx->ho = new HoHost;
+    ctx->ho->G = G;
+    ctx->ho->m2.assign(m2, m2 + (size_t)nq * n);
+    ctx->ho->gp.assign(gp, gp + (size_t)d * G * nf);
+    ctx->ho->gw.assign(gw, gw + (size_t)G * nf);
+    return GMG_OK;
+}
+
+static gmg_status ho_ready(gmg_ctx *ctx, bool need_state)
+{
+    gmg_status st = check_ready(ctx, need_state);
+    if (st) return st;
+    if (!ctx->ho || !ctx->ho->prepared) { ctx->err = "no high-order geometry (gmg_load_ho_geometry)"; return GMG_ESTATE; }
+    return GMG_OK;
+}
+
+gmg_status gmg_set_ho_state(gmg_ctx *ctx, const double *G, const double *alpha)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = ho_ready(ctx, false);
+    if (st) return st;
+    HoDev &V = ctx->ho->dev;
+    const int d = ctx->opt.dim, nvd = (d + 2) * d;
+    const int n = ctx->dom[0].dv[0].n;
+    if (G) { st = put_natural(ctx, 0, G, nvd, [&](DevLevel &) { return V.G_; }, false); if (st) return st; }
+    else k_fill<<<nblk((int64_t)n * nvd), 256, 0, ctx->stream>>>(n * nvd, V.G_, 0.0);
+    if (alpha) { st = put_natural(ctx, 0, alpha, 1, [&](DevLevel &) { return V.alpha; }, false); if (st) return st; }
+    else k_fill<<<nblk(n), 256, 0, ctx->stream>>>(n, V.alpha, 1.0);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GMG_OK;
+}
+
+gmg_status gmg_get_ho_state(gmg_ctx *ctx, double *G_out, double *alpha_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = ho_ready(ctx, false);
+    if (st) return st;
+    HoDev &V = ctx->ho->dev;
+    const int d = ctx->opt.dim;
+    if (G_out) { st = get_natural(ctx, 0, [&](DevLevel &) { return (const double *)V.G_; }, (d + 2) * d, G_out); if (st) return st; }
+    if (alpha_out) { st = get_natural(ctx, 0, [&](DevLevel &) { return (const double *)V.alpha; }, 1, alpha_out); if (st) return st; }
+    return GMG_OK;
+}
+
+gmg_status gmg_ho_residual(gmg_ctx *ctx, double *R_out, double *G_out, double *alpha_out, double *sigma_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = ho_ready(ctx, true);
+    if (st) return st;
+    Launcher Lc{ctx, ctx->stream};
+    DevLevel &L = ctx->dom[0].dv[0];
+    HoDev &V = ctx->ho->dev;
+    enqueue_ho_eval(Lc, HO_OUT, L.Rt, L.tmp);
+    CK(cudaGetLastError());
+    const int d = ctx->opt.dim, nv = d + 2;
+    if (R_out) { st = get_natural(ctx, 0, [](DevLevel &L_) { return (const double *)L_.Rt; }, nv, R_out); if (st) return st; }
+    if (G_out) { st = get_natural(ctx, 0, [&](DevLevel &) { return (const double *)V.Gout; }, nv * d, G_out); if (st) return st; }
+    if (alpha_out) { st = get_natural(ctx, 0, [](DevLevel &L_) { return (const double *)L_.tmp; }, 1, alpha_out); if (st) return st; }
+    if (sigma_out) { st = get_natural(ctx, 0, [](DevLevel &L_) { return (const double *)L_.sigma; }, 1, sigma_out); if (st) return st; }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GMG_OK;
+}
+
+gmg_status gmg_ho_recon(gmg_ctx *ctx, double *poly_out, int32_t *flags_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = ho_ready(ctx, true);
+    if (st) return st;
+    Launcher Lc{ctx, ctx->stream};
+    HoDev &V = ctx->ho->dev;
+    enqueue_ho_eval(Lc, 0, nullptr, nullptr, true);
+    CK(cudaGetLastError());
+    const int d = ctx->opt.dim, nv = d + 2;
+    if (poly_out) { st = get_natural(ctx, 0, [&](DevLevel &) { return (const double *)V.poly; }, nv * V.nc, poly_out); if (st) return st; }
+    if (flags_out) {
+        const DomLevel &D0 = ctx->dom[0].lv[0];
+        std::vector<int> fl(D0.n_own);
+        CK(cudaMemcpyAsync(fl.data(), V.flags, fl.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (int64_t i = 0; i < D0.n_own; ++i) flags_out[D0.l2n[i]] = fl[i];
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GMG_OK;
+}
+
 void gmg_destroy(gmg_ctx *ctx)
 {
     if (!ctx) return;
@@ -1917,6 +2126,7 @@ void gmg_destroy(gmg_ctx *ctx)
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy((ncclComm_t)ctx->nccl_comm);
     for (void *p : ctx->p2p_opened) cudaIpcCloseMemHandle(p);
+    delete ctx->ho;
     delete ctx;
 }
 

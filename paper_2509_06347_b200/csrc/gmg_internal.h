@@ -141,6 +141,47 @@ struct LevelBytes {
     std::vector<double> sweep_out; // per color, extra bytes when the launch also writes W = W0 + dW
 };
 
+// NEXT-1: third-order compact GKS fine operator.  Fine
+// level, single domain.  Device arrays live in the workspace (carve).
+struct HoDev {
+    int G = 0, nk = 0, nc = 0, nq = 0;   // Gauss slots per face, p2 unknowns, poly coefficients, m2 components
+    const double *ctr = nullptr;         // [n][D] centroids (local order)
+    const double *m2 = nullptr;          // [n][nq] central second moments
+    const double *gp = nullptr;          // [nf][G][D] Gauss points (local faces)
+    const double *gw = nullptr;          // [nf][G] weights (0 = padding)
+    const int *hfoff = nullptr;          // [n+1] cell -> faces
+    const int *hface = nullptr;          // signed local faces: +(f+1) cell is left, -(f+1) right; ascending natural id
+    const int *poff = nullptr;           // [n+1] offset (doubles) of the cell's p2 operator; empty = p1 only
+    const double *P = nullptr;           // per interior neighbour m: (D+1) columns of nk: d a / d(Q_m - Q_i), d a / d(Q_e)_m
+    double *G_ = nullptr;                // [n][nv][D] cell-averaged slopes (carried)
+    double *alpha = nullptr;             // [n] DF carried between evaluations (p1 factor, C4/C14)
+    double *poly = nullptr;              // [n][nv][nc] final polynomials (c0, lin[D], quad[nq]) about the centroid
+    int *flags = nullptr;                // [n] bit 0 p2 used, bit 1 positivity fallback
+    double *sr = nullptr;                // [nf] S r_f (first-order spectral radius, A5)
+    double *dt = nullptr;                // [n] Dt_i = CFL_exp V_i / Sigma_i (C8)
+    double *frec = nullptr;              // [nf][12] S sum_k w F_k / Dt_f [nv] | sum_k w W_k(Dt_f) [nv] | prod alpha_fk
+    double *Gout = nullptr;              // [n][nv][D] slopes of a non-updating evaluation
+};
+// modes of the NEXT-1 gather (ho.cu k_ho_gather)
+enum : int {
+    HO_NORM = 1,     // per-block partial sums of R_q^2 (history)
+    HO_UPDATE = 2,   // W -= CFL_exp R / Sigma (C12), G = new slopes, alpha carried = alpha
+    HO_RT = 4,       // Rt = R, level alpha = alpha (restriction inputs), alpha carried = alpha
+    HO_OUT = 8,      // R -> Rout (AoS), new slopes -> Gout, alpha -> alpha_out (ABI)
+};
+struct HoHost {
+    int G = 0;
+    double bytes_sr = 0, bytes_recon = 0, bytes_flux = 0, bytes_gather = 0;   // algorithmic bytes per launch
+    int64_t n_gauss_pts = 0;             // Gauss points of the local faces (flux work units)
+    std::vector<double> m2, gp, gw;      // natural order as loaded: [nq][N], [D][G][NF], [G][NF]
+    bool prepared = false;
+    // local (domain 0, level 0)
+    std::vector<double> ctr, m2l, gpl, gwl, P;
+    std::vector<int> hfoff, hface, poff;
+    int64_t n_p2 = 0;                    // cells with a p2 operator
+    HoDev dev;
+};
+
 struct Domain {
     int rank = 0;
     std::vector<DomLevel> lv;
@@ -209,6 +250,7 @@ struct gmg_ctx {
                                       // sweep (-1 = auto: NCCL ranks only; local domains measured 4-7% slower with it)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    gmg::HoHost *ho = nullptr;        // NEXT-1 geometry + setup (gmg_load_ho_geometry)
 };
 
 namespace gmg {
@@ -232,4 +274,6 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
 void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, DomLevel &Dc);
 void build_p2p_targets(DomLevel &D, int me, int ncolor, const std::vector<const DomLevel *> &peer_dom);
 void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *part);
+// ho_setup.cpp (NEXT-1): local geometry, cell -> face lists and the per-cell p2 operators
+gmg_status ho_prepare(gmg_ctx *ctx);
 }  // namespace gmg

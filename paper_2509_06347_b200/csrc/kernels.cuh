@@ -11,137 +11,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#include "gmg_internal.h"
+#include "device_common.cuh"
 
 namespace gmg {
-
-// per-cell sweep record layout (doubles)
-template <int D> struct Rec;
-// 3D: [W0..W3 | W4 dW0 dW1 dW2 | dW3 dW4 1/D a/2]: the own-cell epilogue reads
-// only the last 32-B chunk (1/D, alpha/2) and rewrites dW without reading the rest
-template <> struct Rec<3> { static constexpr int W = 0, DW = 5, INVD = 10, HA = 11, STRIDE = 12; };
-template <> struct Rec<2> { static constexpr int W = 0, DW = 4, INVD = 8, HA = 9, STRIDE = 12; };
-// (both 96 B: 32-byte aligned, so a neighbour record is three 256-bit loads)
-// per-slot record: A_0..A_{D-1}, S r at [D]
-constexpr int kSlotRec = 4;
-
-struct Phys {
-    double gamma, gm1, K, omega;
-};
-struct BCs {
-    double winf[5];
-    int kind[16];
-};
-
-enum : int {
-    G_FLUX = 1,       // accumulate R = sum sigma S F and alpha = prod alpha_f^M from the face buffers
-    G_NORM = 2,       // per-block partial sums of R_q^2
-    G_EXPLICIT = 4,   // W -= (cfl_exp / Sigma) R            (Eq.(smo), reading A9)
-    G_WRITE_RT = 8,   // Rt = R (+ F if G_ADD_F)
-    G_ADD_F = 16,
-    G_SET_F = 32,     // F = Rs - R
-    G_ALPHA = 64,     // alpha = prod alpha_f^{M_f}          (O5)
-    G_PREPARE = 128,  // 1/D, alpha/2 into the record, S r into the slot records (O6)
-    G_SIGMA = 256,    // store Sigma
-    G_ZERO_DW = 512,  // record dW = 0 (start of a smoothing step, O7 step 1)
-    G_COPY_W = 1024,  // record W_lin = W (fine-level smoothing)
-    G_BETA = 2048,    // prepare with the fixed relaxation factor beta instead of alpha (df_mode 3)
-};
-
-struct GArgs {
-    int flags;
-    double cfl_imp, cfl_exp;
-    double *Wexp;
-    double *partial;
-    double beta;
-};
-
-// Programmatic dependent launch (sm_90+): every V-cycle kernel may be
-// launched while its predecessor drains; it waits here until the predecessor
-// grid has completed and its writes are visible, and immediately lets its
-// own successor be scheduled.  No-ops when launched without the attribute.
-__device__ __forceinline__ void pdl_enter()
-{
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-template <int NV>
-__device__ __forceinline__ void ld_vec(const double *__restrict__ q, double *w)
-{
-#pragma unroll
-    for (int k = 0; k < NV; ++k) w[k] = __ldg(q + k);
-}
-
-// 256-bit global accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256); p 32-byte aligned
-__device__ __forceinline__ void ld4nc(const double *p, double *v)
-{
-    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
-}
-__device__ __forceinline__ void ld4cs(const double *p, double *v)
-{
-    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
-}
-__device__ __forceinline__ void st4(double *p, const double *v)
-{
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
-                 : "memory");
-}
-
-template <int D>
-__device__ __forceinline__ double pressure(const double *w, double gm1)
-{
-    double m2 = 0.0;
-#pragma unroll
-    for (int k = 0; k < D; ++k) m2 += w[1 + k] * w[1 + k];
-    return gm1 * (w[D + 1] - 0.5 * m2 / w[0]);
-}
-
-// ghost state of a boundary face (O4, reading A25); n = unit outward normal
-template <int D>
-__device__ __forceinline__ void ghost(int kind, const double *wi, const BCs &bc, const double *n, double *wg)
-{
-    if (kind == GMG_FARFIELD) {
-#pragma unroll
-        for (int q = 0; q < D + 2; ++q) wg[q] = bc.winf[q];
-        return;
-    }
-#pragma unroll
-    for (int q = 0; q < D + 2; ++q) wg[q] = wi[q];
-    if (kind == GMG_SLIP) {
-        double mn = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) mn += wi[1 + k] * n[k];
-#pragma unroll
-        for (int k = 0; k < D; ++k) wg[1 + k] = wi[1 + k] - 2.0 * mn * n[k];
-    } else if (kind == GMG_NOSLIP) {
-#pragma unroll
-        for (int k = 0; k < D; ++k) wg[1 + k] = -wi[1 + k];
-    }
-}
-
-// primitive view of one face side, shared by the KFVS flux, the DF helper
-// and nothing else recomputes it (one 1/rho, one 1/p, one rsqrt per side)
-template <int D>
-struct Side {
-    double rho, ir, u[D], U, u2, p, ip;
-};
-template <int D>
-__device__ __forceinline__ Side<D> side_of(const double *w, const double *n, double gm1)
-{
-    Side<D> s;
-    s.rho = w[0];
-    s.ir = 1.0 / s.rho;
-    s.U = 0.0;
-    s.u2 = 0.0;
-#pragma unroll
-    for (int k = 0; k < D; ++k) { s.u[k] = w[1 + k] * s.ir; s.U += s.u[k] * n[k]; s.u2 += s.u[k] * s.u[k]; }
-    s.p = gm1 * (w[D + 1] - 0.5 * s.rho * s.u2);
-    s.ip = 1.0 / s.p;
-    return s;
-}
 
 // one half-range side of the first-order KFVS flux (O4), accumulated into F:
 // sgn = +1 -> u.n > 0 half of the left state, sgn = -1 -> u.n < 0 half of the

@@ -21,11 +21,12 @@ LIBPATH = os.path.join(_HERE, "libgmg.so")
 GMG_OK, GMG_EINVAL, GMG_ETOPO, GMG_ECOLOR, GMG_ESTALL, GMG_ENOMEM, GMG_ECUDA, GMG_ENCCL, GMG_ENONFINITE, GMG_ESTATE = range(10)
 STATUS = ["GMG_OK", "GMG_EINVAL", "GMG_ETOPO", "GMG_ECOLOR", "GMG_ESTALL", "GMG_ENOMEM", "GMG_ECUDA", "GMG_ENCCL",
           "GMG_ENONFINITE", "GMG_ESTATE"]
-K_FACE, K_GATHER, K_SWEEP, K_RESTRICT, K_PROLONG, K_NORM, K_COUNT = range(7)
-K_NAMES = ["face", "gather", "sweep", "restrict", "prolong", "norm"]
+K_FACE, K_GATHER, K_SWEEP, K_RESTRICT, K_PROLONG, K_NORM, K_HO_RECON, K_HO_FLUX, K_COUNT = range(9)
+K_NAMES = ["face", "gather", "sweep", "restrict", "prolong", "norm", "ho_recon", "ho_flux"]
 
 # every symbol include/gmg.h declares
-ABI_SYMBOLS = ["gmg_default_options", "gmg_create", "gmg_load_mesh", "gmg_set_coloring", "gmg_build_hierarchy",
+ABI_SYMBOLS = ["gmg_load_ho_geometry", "gmg_set_ho_state", "gmg_get_ho_state", "gmg_ho_residual", "gmg_ho_recon",
+               "gmg_default_options", "gmg_create", "gmg_load_mesh", "gmg_set_coloring", "gmg_build_hierarchy",
                "gmg_get_level_info", "gmg_get_maps", "gmg_get_level_geometry", "gmg_workspace_bytes",
                "gmg_set_workspace", "gmg_set_state", "gmg_set_level_state", "gmg_get_state", "gmg_set_alpha",
                "gmg_residual", "gmg_set_level_inputs", "gmg_smooth", "gmg_vcycle", "gmg_profile_vcycle",
@@ -45,7 +46,8 @@ class Options(C.Structure):
                 ("skew_limit", C.c_double), ("r_factor", C.c_double), ("fine_smoother", C.c_int),
                 ("df_mode", C.c_int), ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p),
                 ("device", C.c_int), ("stream", C.c_void_p), ("beta", C.c_double), ("local_domains", C.c_int),
-                ("setup_device", C.c_int)]
+                ("setup_device", C.c_int), ("fine_operator", C.c_int), ("ho_c1", C.c_double), ("ho_c2", C.c_double),
+                ("ho_gam0", C.c_double), ("ho_eps", C.c_double)]
 
 
 _lib = None
@@ -88,6 +90,11 @@ def lib():
             "gmg_p2p_import": (I, [P, P, P, P]),
             "gmg_get_p2p_targets": (I, [P, I, I, P, P, P, P]),
             "gmg_p2p_emulate_smooth": (I, [P, I, I, P]),
+            "gmg_load_ho_geometry": (I, [P, P, I, P, P]),
+            "gmg_set_ho_state": (I, [P, P, P]),
+            "gmg_get_ho_state": (I, [P, P, P]),
+            "gmg_ho_residual": (I, [P, P, P, P, P]),
+            "gmg_ho_recon": (I, [P, P, P]),
             "gmg_last_error": (C.c_char_p, [P]),
             "gmg_destroy": (None, [P]),
         }
@@ -309,6 +316,29 @@ def gmg_p2p_emulate_smooth(ctx, level, n_sweeps, nv, n):
     return dW
 
 
+def gmg_load_ho_geometry(ctx, mesh):
+    m2, gp, gw = _f64(mesh.m2), _f64(mesh.gp), _f64(mesh.gw)
+    _check(ctx, lib().gmg_load_ho_geometry(ctx, _ptr(m2), int(gw.shape[0]), _ptr(gp), _ptr(gw)))
+
+
+def gmg_set_ho_state(ctx, G=None, alpha=None):
+    G = None if G is None else _f64(G)
+    alpha = None if alpha is None else _f64(alpha)
+    _check(ctx, lib().gmg_set_ho_state(ctx, _ptr(G), _ptr(alpha)))
+
+
+def gmg_get_ho_state(ctx, G_out=None, alpha_out=None):
+    _check(ctx, lib().gmg_get_ho_state(ctx, _ptr(G_out), _ptr(alpha_out)))
+
+
+def gmg_ho_residual(ctx, R_out=None, G_out=None, alpha_out=None, sigma_out=None):
+    _check(ctx, lib().gmg_ho_residual(ctx, _ptr(R_out), _ptr(G_out), _ptr(alpha_out), _ptr(sigma_out)))
+
+
+def gmg_ho_recon(ctx, poly_out=None, flags_out=None):
+    _check(ctx, lib().gmg_ho_recon(ctx, _ptr(poly_out), _ptr(flags_out)))
+
+
 def gmg_last_error(ctx):
     m = lib().gmg_last_error(ctx)
     return m.decode() if m else ""
@@ -328,7 +358,8 @@ class Solver:
     patch_kind, dim).  kw: gmg_options fields (cfl_imp, n_sweeps, ...).
     """
 
-    def __init__(self, mesh, n_levels=3, device=0, color0=None, build_only=False, part=None, nccl_id=None, **kw):
+    def __init__(self, mesh, n_levels=3, device=0, color0=None, build_only=False, part=None, nccl_id=None,
+                 ho_geometry=False, **kw):
         self.dim = int(mesh.dim)
         self.nv = self.dim + 2
         self.opt = gmg_default_options(dim=self.dim, n_levels=n_levels, device=device, **kw)
@@ -346,6 +377,8 @@ class Solver:
             self.opt.stream = torch.cuda.current_stream(self.device).cuda_stream
         self.ctx = gmg_create(self.opt)
         gmg_load_mesh(self.ctx, mesh, part)
+        if self.opt.fine_operator == 1 or ho_geometry:
+            gmg_load_ho_geometry(self.ctx, mesh)
         if color0 is not None:
             gmg_set_coloring(self.ctx, 0, color0)
         self.n_levels, self.build_status = gmg_build_hierarchy(self.ctx, n_levels)
@@ -423,6 +456,30 @@ class Solver:
 
     def vcycle_launches(self):
         return gmg_vcycle_launches(self.ctx)
+
+    # NEXT-1 (fine_operator = 1 or ho_geometry = True)
+    def set_ho_state(self, G=None, alpha=None):
+        gmg_set_ho_state(self.ctx, G, alpha)
+
+    def get_ho_state(self):
+        n = self.n_cells(0)
+        G, a = np.zeros((self.nv, self.dim, n)), np.zeros(n)
+        gmg_get_ho_state(self.ctx, G, a)
+        return G, a
+
+    def ho_residual(self):
+        n = self.n_cells(0)
+        R, G, a, s = np.zeros((self.nv, n)), np.zeros((self.nv, self.dim, n)), np.zeros(n), np.zeros(n)
+        gmg_ho_residual(self.ctx, R, G, a, s)
+        return R, G, a, s
+
+    def ho_recon(self):
+        n = self.n_cells(0)
+        nc = 1 + self.dim + self.dim * (self.dim + 1) // 2
+        poly = np.zeros((self.nv * nc, n))
+        fl = np.zeros(n, dtype=np.int32)
+        gmg_ho_recon(self.ctx, poly, fl)
+        return np.ascontiguousarray(poly.T.reshape(n, self.nv, nc)), fl
 
     def halo(self, level=0, dom=0):
         return gmg_get_halo(self.ctx, level, dom)

@@ -1,0 +1,149 @@
+"""GPU parity of the NEXT-1 third-order compact GKS fine operator (ho.cu,
+fine_operator = 1) against the oracle (oracle/cgks3.c), through the C ABI:
+the reconstruction (polynomials, p2 / fallback flags bit-exact), one
+evaluation (R, evolved slopes, DF, Sigma) and whole V-cycles (state,
+slopes, DF, residual history).  Tolerance: the north-star 1e-10 relative L2
+for FP64 states and histories."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import cgks3
+from synth import configs, state
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+def _cases():
+    F, S, N, E = configs.FARFIELD, configs.SLIP, configs.NOSLIP, configs.EXTRAP
+    return {
+        "tri2d": (configs.tri_square(12, 12, seed=3), (1.0, (0.5, 0.2), 0.8)),
+        "quad2d": (configs.quad_grid(10, 8, patch_kinds=(F, S, E, N)), (1.0, (0.4, -0.1), 0.7)),
+        "box3d_prism": (configs.box3d(6, 5, 4, 2, seed=1), (1.0, (0.6, 0.2, -0.1), 0.7)),
+        "box3d_tet": (configs.box3d(5, 5, 5, 0, seed=2, patch_kinds=(F, S, E, F)), (1.0, (0.3, -0.4, 0.2), 0.9)),
+    }
+
+
+def _state(m, fs, seed, eps=0.08):
+    W = state.perturbed(m, *fs, eps=eps, seed=seed)
+    rng = np.random.default_rng(seed + 100)
+    d, n = m.dim, m.n_cells
+    G = 0.3 * rng.standard_normal((d + 2, d, n))
+    alpha = 0.5 + 0.5 * rng.random(n)
+    return W, state.winf(*fs), G, alpha
+
+
+def _solver(m, **kw):
+    from paper_2509_06347_b200 import Solver
+    return Solver(m, fine_operator=1, **kw)
+
+
+@pytest.mark.parametrize("name", list(_cases()))
+def test_recon_matches_oracle(name):
+    m, fs = _cases()[name]
+    W, Winf, G, alpha = _state(m, fs, 1)
+    s = _solver(m, n_levels=1)
+    s.set_state(W, Winf)
+    s.set_ho_state(G, alpha)
+    poly, fl = s.ho_recon()
+    s.close()
+    po, flo, nfall = cgks3.recon(cgks3.Mesh3(m), W, G, alpha, Winf)
+    assert np.array_equal(fl, flo)
+    assert (flo & 1).sum() > 0
+    assert _rel(poly, po) <= TOL, _rel(poly, po)
+
+
+@pytest.mark.parametrize("name", list(_cases()))
+def test_one_evaluation_matches_oracle(name):
+    m, fs = _cases()[name]
+    W, Winf, G, alpha = _state(m, fs, 2)
+    s = _solver(m, n_levels=1)
+    s.set_state(W, Winf)
+    s.set_ho_state(G, alpha)
+    R, Gn, a, S = s.ho_residual()
+    G2, a2 = s.get_ho_state()
+    s.close()
+    Ro, Gno, ao, So, _, _ = cgks3.residual(cgks3.Mesh3(m), W, G, alpha, Winf)
+    assert _rel(S, So) <= 1e-13
+    assert _rel(R, Ro) <= TOL, _rel(R, Ro)
+    assert _rel(Gn, Gno) <= TOL, _rel(Gn, Gno)
+    assert _rel(a, ao) <= TOL, _rel(a, ao)
+    assert np.array_equal(G2, G) and np.array_equal(a2, alpha)      # no state change
+
+
+@pytest.mark.parametrize("name", list(_cases()))
+def test_vcycles_match_oracle(name):
+    m, fs = _cases()[name]
+    W, Winf, _, _ = _state(m, fs, 3)
+    nc = 4
+    s = _solver(m, n_levels=3)
+    s.set_state(W, Winf)
+    hist = s.vcycle(nc)
+    Wg = s.get_state(0)
+    Gg, ag = s.get_ho_state()
+    s.close()
+    H = oracle.build_hierarchy(m, 3, 0.5)
+    hs = {}
+    Wo, ho = oracle.vcycle(H, W, Winf, oracle.Options(fine_operator=1), nc, mesh=m, ho_state=hs)
+    assert _rel(Wg, Wo) <= TOL, _rel(Wg, Wo)
+    assert _rel(Gg, hs["G"]) <= TOL, _rel(Gg, hs["G"])
+    assert _rel(ag, hs["alpha"]) <= TOL
+    herr = np.max(np.abs(hist - ho) / ho[0][None, :])
+    assert herr <= TOL, herr
+
+
+def test_vcycles_continue_from_carried_state():
+    """slopes and DF persist across gmg_vcycle calls exactly as in one call."""
+    m, fs = _cases()["box3d_prism"]
+    W, Winf, _, _ = _state(m, fs, 4)
+    s = _solver(m, n_levels=3)
+    s.set_state(W, Winf)
+    s.vcycle(2)
+    h2 = s.vcycle(2)
+    W4 = s.get_state(0)
+    s.set_state(W, Winf)
+    s.set_ho_state()
+    s.vcycle(4)
+    assert np.array_equal(s.get_state(0), W4)
+    s.close()
+    assert np.all(np.isfinite(h2))
+
+
+def test_free_stream_preserved_on_device():
+    F = configs.FARFIELD
+    m = configs.box3d(6, 5, 4, 2, seed=5, patch_kinds=(F,))
+    fs = (1.0, (0.6, 0.2, -0.1), 0.7)
+    s = _solver(m, n_levels=3)
+    s.set_state(state.uniform(m, *fs), state.winf(*fs))
+    hist = s.vcycle(3)
+    W = s.get_state(0)
+    G, a = s.get_ho_state()
+    s.close()
+    assert np.max(np.abs(W - state.uniform(m, *fs))) < 1e-13
+    assert np.max(np.abs(G)) < 1e-12 and np.allclose(a, 1.0)
+    assert np.max(hist) < 1e-12
+
+
+@pytest.mark.slow
+def test_config2_sized_vcycle_matches_oracle():
+    """a larger 2D case in the launch configuration of a real run (tens of
+    thousands of Gauss points, many resident waves)."""
+    m = configs.naca_ogrid(ni=96, n_quad=24, n_tri=8)
+    fs = (1.0, (0.5, 0.0), 1.0 / 1.4)
+    W = state.uniform(m, *fs)
+    Winf = state.winf(*fs)
+    s = _solver(m, n_levels=3)
+    s.set_state(W, Winf)
+    hist = s.vcycle(2)
+    Wg = s.get_state(0)
+    s.close()
+    H = oracle.build_hierarchy(m, 3, 0.5)
+    Wo, ho = oracle.vcycle(H, W, Winf, oracle.Options(fine_operator=1), 2, mesh=m, ho_state={})
+    assert _rel(Wg, Wo) <= TOL
+    assert np.max(np.abs(hist - ho) / ho[0][None, :]) <= TOL
