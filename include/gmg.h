@@ -296,8 +296,9 @@ gmg_status gmg_ho_residual(gmg_ctx *ctx, double *R_out, double *G_out, double *a
 
 /* The reconstruction alone (C2-C6): poly_out[nv*nc][n] with nc = 1 + dim + nq,
  * per component (c0, lin[dim], quad[nq]) of p(x) = c0 + lin . y + sum_k quad_k
- * y_a y_b, y = x - x_cell (natural order); flags_out[n] bit 0 = p2 used,
- * bit 1 = positivity fallback (C6b).  Either may be NULL. */
+ * y_a y_b, y = x - x_cell (natural order); flags_out[n] bit 0 = p2 used
+ * (positivity, C6b, is applied per Gauss point in the flux).  Either may be
+ * NULL. */
 gmg_status gmg_ho_recon(gmg_ctx *ctx, double *poly_out, int32_t *flags_out);
 
 /* Test only: one smoothing step (as gmg_smooth) of ALL local domains

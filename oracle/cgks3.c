@@ -570,18 +570,29 @@ int orc3_p2(const orc3_mesh *M, const int64_t *nb, int nnb, int64_t i, const dou
     return ok;
 }
 
+/* C6b: a Gauss-point state is admissible if rho > 0 and p > 0; otherwise
+ * that side at that point takes the cell average with zero gradient */
+static int c3_admissible(int d, double gamma, const double *w)
+{
+    double m2s = 0.0;
+    for (int e = 0; e < d; ++e) m2s += w[1 + e] * w[1 + e];
+    double pr = (gamma - 1.0) * (w[d + 1] - 0.5 * m2s / w[0]);
+    return w[0] > 0.0 && pr > 0.0;
+}
+
 /* ===================================================================== */
 /* The fine operator (readings C1-C13):                                    */
 /* in: W [nv][n], G [nv][d][n] (cell-averaged slopes), alpha_in [n]        */
 /* out: R [nv][n] time-averaged flux sum (A4), Gnew [nv][d][n] the evolved */
 /* slopes times DF, alpha [n] DF, Sigma [n] */
-/* (first-order, A5/A6), flags [n] (bit 0: p2 used, bit 1: positivity      */
-/* fallback).  Returns the number of fallback cells.                        */
+/* (first-order, A5/A6), flags [n] (bit 0: p2 used; bit 1 unused)          */
+/* unused).  Returns the number of Gauss-point sides that fell back (C6b). */
 /* ===================================================================== */
 /* C2-C6: the final (WENO-combined, positivity-checked) polynomial of every
  * cell and component: poly [n][nv][1 + d + nq] = (c0, lin[d], quad[nq]) of
  * p(x) = c0 + lin . y + sum_k quad_k y_a y_b, y = x - x_cell.
- * flags [n]: bit 0 p2 used, bit 1 positivity fallback.  Returns fallbacks. */
+ * flags [n]: bit 0 p2 used.  Returns 0 (positivity is handled per Gauss
+ * point in orc3_residual, reading C6b). */
 int64_t orc3_recon(const orc3_mesh *M, const orc3_opt *o, const double *W, const double *G, const double *alpha_in,
                    const double *Winf, double *poly, int32_t *flags)
 {
@@ -669,29 +680,6 @@ int64_t orc3_recon(const orc3_mesh *M, const orc3_opt *o, const double *W, const
             }
         }
         if (flags) flags[i] = used2;
-        /* C6b: positivity at every Gauss point of the cell, else constant */
-        int bad = 0;
-        for (int64_t s = off[i]; s < off[i + 1] && !bad; ++s) {
-            int64_t f = fidx[s];
-            for (int k = 0; k < M->G; ++k) {
-                if (M->gw[(int64_t)k * nf + f] == 0.0) continue;
-                double y[3], w[5];
-                for (int e = 0; e < d; ++e) y[e] = M->gp[((int64_t)e * M->G + k) * nf + f] - M->ctr[(int64_t)e * n + i];
-                for (int q = 0; q < nv; ++q) w[q] = cp_eval(d, &P[i * nv + q], y);
-                double m2s = 0.0;
-                for (int e = 0; e < d; ++e) m2s += w[1 + e] * w[1 + e];
-                double pr = (o->gamma - 1.0) * (w[nv - 1] - 0.5 * m2s / w[0]);
-                if (!(w[0] > 0.0) || !(pr > 0.0)) { bad = 1; break; }
-            }
-        }
-        if (bad) {
-            ++nfall;
-            if (flags) flags[i] |= 2;
-            for (int q = 0; q < nv; ++q) {
-                memset(&P[i * nv + q], 0, sizeof(cpoly));
-                P[i * nv + q].c0 = W[(int64_t)q * n + i];
-            }
-        }
     }
 
     int nc = 1 + d + nq;
@@ -769,6 +757,11 @@ int64_t orc3_residual(const orc3_mesh *M, const orc3_opt *o, const double *W, co
                 cp_grad(d, &P[l * nv + q], yl, gr);
                 for (int e = 0; e < d; ++e) dWL[e * nv + q] = gr[e];
             }
+            if (!c3_admissible(d, o->gamma, WL)) {          /* C6b: this side, this point */
+                ++nfall;
+                for (int q = 0; q < nv; ++q) WL[q] = W[(int64_t)q * n + l];
+                for (int e = 0; e < d * nv; ++e) dWL[e] = 0.0;
+            }
             if (r >= 0) {
                 for (int e = 0; e < d; ++e) yr[e] = x[e] - M->ctr[(int64_t)e * n + r];
                 for (int q = 0; q < nv; ++q) {
@@ -776,6 +769,11 @@ int64_t orc3_residual(const orc3_mesh *M, const orc3_opt *o, const double *W, co
                     WR[q] = cp_eval(d, &P[r * nv + q], yr);
                     cp_grad(d, &P[r * nv + q], yr, gr);
                     for (int e = 0; e < d; ++e) dWR[e * nv + q] = gr[e];
+                }
+                if (!c3_admissible(d, o->gamma, WR)) {
+                    ++nfall;
+                    for (int q = 0; q < nv; ++q) WR[q] = W[(int64_t)q * n + r];
+                    for (int e = 0; e < d * nv; ++e) dWR[e] = 0.0;
                 }
             } else {                                       /* C6: ghost value, ghost gradient */
                 int kind = M->patch_kind[-r - 1];

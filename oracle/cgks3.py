@@ -122,7 +122,7 @@ def residual(M: Mesh3, W, G, alpha, Winf, opt: Opt3 = None):
 
 def recon(M: Mesh3, W, G, alpha, Winf, opt: Opt3 = None):
     """Final per-cell polynomials poly [n][nv][1+d+nq] (c0, lin, quad about the
-    centroid), flags [n] (bit 0 p2 used, bit 1 positivity fallback), fallbacks."""
+    centroid), flags [n] (bit 0 p2 used), 0 (positivity is per Gauss point, C6b)."""
     opt = opt or Opt3()
     d, n = M.dim, M.n
     nv, nc = d + 2, 1 + d + d * (d + 1) // 2

@@ -156,7 +156,7 @@ struct HoDev {
     double *G_ = nullptr;                // [n][nv][D] cell-averaged slopes (carried)
     double *alpha = nullptr;             // [n] DF carried between evaluations (p1 factor, C4/C14)
     double *poly = nullptr;              // [n][nv][nc] final polynomials (c0, lin[D], quad[nq]) about the centroid
-    int *flags = nullptr;                // [n] bit 0 p2 used, bit 1 positivity fallback
+    int *flags = nullptr;                // [n] bit 0 p2 used
     double *sr = nullptr;                // [nf] S r_f (first-order spectral radius, A5)
     double *dt = nullptr;                // [n] Dt_i = CFL_exp V_i / Sigma_i (C8)
     double *frec = nullptr;              // [nf][12] S sum_k w F_k / Dt_f [nv] | sum_k w W_k(Dt_f) [nv] | prod alpha_fk

@@ -4,10 +4,10 @@
 //
 //   k_ho_sr     per face   S r_f (first-order spectral radius of the cell averages, A5)
 //   k_ho_recon  per cell   Sigma_i, Dt_i, p1 (Green-Gauss x DF), p2 (stored KKT operator x
-//                          neighbour averages and slopes), WENO-Z weights, positivity check
+//                          neighbour averages and slopes), WENO-Z weights
 //                          -> one polynomial per cell and component
 //   k_ho_flux   per face   at every Gauss point: both sides' polynomial values and gradients,
-//                          DF, collision time, the BGK flux (Eqs. (dis1), (dis2)) integrated over
+//                          positivity (C6b), DF, collision time, the BGK flux (Eqs. (dis1), (dis2)) integrated over
 //                          Dt_f and the Gauss-point state at Dt_f  -> one face record
 //   k_ho_gather per cell   R_i, the evolved slopes, DF; update / restriction outputs
 //
@@ -24,23 +24,24 @@ namespace gmg {
 constexpr int kHoRec = 12;
 
 // ------------------------------------------------------------------ moments
-// normalised Maxwellian: Mu (full), Mp (u1 > 0), Mm (u1 < 0), Mv, Mw, <xi^2>, <xi^4>
-template <int D>
+// normalised Maxwellian moments: Mu (u1, full range), Mh (u1 on the half
+// range R: 1 = u1 > 0, 2 = u1 < 0; unused for R = 0), Mv, Mw, <xi^2>, <xi^4>
+template <int D, int R>
 struct Maxw {
-    double rho, lam;
-    double Mu[7], Mp[7], Mm[7], Mv[6], Mw[6];
+    double rho;
+    double Mu[7], Mh[R == 0 ? 1 : 7], Mv[6], Mw[D == 3 ? 6 : 1];
     double x1, x2;
 };
 
-__device__ __forceinline__ void rec_mom(double U, double inv2l, double *M, int n)
+template <int N>
+__device__ __forceinline__ void rec_mom(double U, double inv2l, double *M)
 {
 #pragma unroll
-    for (int k = 2; k < 7; ++k)
-        if (k < n) M[k] = U * M[k - 1] + (double)(k - 1) * inv2l * M[k - 2];
+    for (int k = 2; k < N; ++k) M[k] = U * M[k - 1] + (double)(k - 1) * inv2l * M[k - 2];
 }
 
-template <int D>
-__device__ __forceinline__ void maxw(const double *w, double gm1, double K, Maxw<D> &g)
+template <int D, int R>
+__device__ __forceinline__ void maxw(const double *w, double gm1, double K, Maxw<D, R> &g)
 {
     g.rho = w[0];
     const double ir = 1.0 / w[0];
@@ -48,140 +49,146 @@ __device__ __forceinline__ void maxw(const double *w, double gm1, double K, Maxw
 #pragma unroll
     for (int k = 0; k < D; ++k) { U[k] = w[1 + k] * ir; u2 += U[k] * U[k]; }
     const double p = gm1 * (w[D + 1] - 0.5 * w[0] * u2);
-    const double lam = 0.5 * w[0] / p;
-    const double inv2l = p * ir;                       // 1/(2 lambda)
-    g.lam = lam;
-    const double sl = sqrt(lam);
-    const double e = exp(-lam * U[0] * U[0]) * (0.28209479177387814 / sl);   // e^{-l U^2} / (2 sqrt(pi l))
+    const double inv2l = p * ir;                       // 1/(2 lambda), lambda = rho / (2p)
     g.Mu[0] = 1.0; g.Mu[1] = U[0];
-    g.Mp[0] = 0.5 * erfc(-sl * U[0]); g.Mp[1] = U[0] * g.Mp[0] + e;
-    g.Mm[0] = 0.5 * erfc(sl * U[0]);  g.Mm[1] = U[0] * g.Mm[0] - e;
-    rec_mom(U[0], inv2l, g.Mu, 7);
-    rec_mom(U[0], inv2l, g.Mp, 7);
-    rec_mom(U[0], inv2l, g.Mm, 7);
+    rec_mom<7>(U[0], inv2l, g.Mu);
+    if constexpr (R != 0) {
+        const double lam = 0.5 * w[0] / p;
+        const double sl = sqrt(lam);
+        const double e = exp(-lam * U[0] * U[0]) * (0.28209479177387814 / sl);   // e^{-l U^2} / (2 sqrt(pi l))
+        if constexpr (R == 1) { g.Mh[0] = 0.5 * erfc(-sl * U[0]); g.Mh[1] = U[0] * g.Mh[0] + e; }
+        else { g.Mh[0] = 0.5 * erfc(sl * U[0]); g.Mh[1] = U[0] * g.Mh[0] - e; }
+        rec_mom<7>(U[0], inv2l, g.Mh);
+    }
     g.Mv[0] = 1.0; g.Mv[1] = U[1];
-    rec_mom(U[1], inv2l, g.Mv, 6);
-    if constexpr (D == 3) { g.Mw[0] = 1.0; g.Mw[1] = U[2]; rec_mom(U[2], inv2l, g.Mw, 6); }
+    rec_mom<6>(U[1], inv2l, g.Mv);
+    if constexpr (D == 3) { g.Mw[0] = 1.0; g.Mw[1] = U[2]; rec_mom<6>(U[2], inv2l, g.Mw); }
     g.x1 = K * inv2l;
     g.x2 = (K * K + 2.0 * K) * inv2l * inv2l;
 }
 
-// <u^a v^b w^c psi> with the u1 moments of range R (0 full, 1 >0, 2 <0)
-template <int D, int R>
-__device__ __forceinline__ const double *umom(const Maxw<D> &g) { return R == 0 ? g.Mu : (R == 1 ? g.Mp : g.Mm); }
-
-template <int D, int R, int a, int b, int c>
-__device__ __forceinline__ void psi_m(const Maxw<D> &g, double *o)
+// u1 moments: H = false full range, true the Maxwellian's half range
+template <int D, int R, bool H>
+__device__ __forceinline__ const double *umom(const Maxw<D, R> &g)
 {
-    const double *Mu = umom<D, R>(g);
-    const double wc = D == 3 ? g.Mw[c] : 1.0;
-    const double base = Mu[a] * g.Mv[b] * wc;
-    o[0] = base;
-    o[1] = Mu[a + 1] * g.Mv[b] * wc;
-    o[2] = Mu[a] * g.Mv[b + 1] * wc;
+    if constexpr (H && R != 0) return g.Mh;
+    else return g.Mu;
+}
+
+// <u^a v^b w^c psi>
+template <int D, int R, bool H, int a, int b, int c>
+__device__ __forceinline__ void psi_m(const Maxw<D, R> &g, double *o)
+{
+    const double *Mu = umom<D, R, H>(g);
     if constexpr (D == 3) {
+        const double wc = g.Mw[c];
+        const double base = Mu[a] * g.Mv[b] * wc;
+        o[0] = base;
+        o[1] = Mu[a + 1] * g.Mv[b] * wc;
+        o[2] = Mu[a] * g.Mv[b + 1] * wc;
         o[3] = Mu[a] * g.Mv[b] * g.Mw[c + 1];
-        o[D + 1] = 0.5 * (Mu[a + 2] * g.Mv[b] * wc + Mu[a] * g.Mv[b + 2] * wc + Mu[a] * g.Mv[b] * g.Mw[c + 2] + g.x1 * base);
+        o[4] = 0.5 * (Mu[a + 2] * g.Mv[b] * wc + Mu[a] * g.Mv[b + 2] * wc + Mu[a] * g.Mv[b] * g.Mw[c + 2] + g.x1 * base);
     } else {
-        o[D + 1] = 0.5 * (Mu[a + 2] * g.Mv[b] + Mu[a] * g.Mv[b + 2] + g.x1 * base);
+        const double base = Mu[a] * g.Mv[b];
+        o[0] = base;
+        o[1] = Mu[a + 1] * g.Mv[b];
+        o[2] = Mu[a] * g.Mv[b + 1];
+        o[3] = 0.5 * (Mu[a + 2] * g.Mv[b] + Mu[a] * g.Mv[b + 2] + g.x1 * base);
     }
 }
 // <xi^2 u^a v^b w^c psi>
-template <int D, int R, int a, int b, int c>
-__device__ __forceinline__ void psi_xi(const Maxw<D> &g, double *o)
+template <int D, int R, bool H, int a, int b, int c>
+__device__ __forceinline__ void psi_xi(const Maxw<D, R> &g, double *o)
 {
-    const double *Mu = umom<D, R>(g);
-    const double wc = D == 3 ? g.Mw[c] : 1.0;
-    const double base = Mu[a] * g.Mv[b] * wc;
-    o[0] = g.x1 * base;
-    o[1] = g.x1 * Mu[a + 1] * g.Mv[b] * wc;
-    o[2] = g.x1 * Mu[a] * g.Mv[b + 1] * wc;
+    const double *Mu = umom<D, R, H>(g);
     if constexpr (D == 3) {
+        const double wc = g.Mw[c];
+        const double base = Mu[a] * g.Mv[b] * wc;
+        o[0] = g.x1 * base;
+        o[1] = g.x1 * Mu[a + 1] * g.Mv[b] * wc;
+        o[2] = g.x1 * Mu[a] * g.Mv[b + 1] * wc;
         o[3] = g.x1 * Mu[a] * g.Mv[b] * g.Mw[c + 1];
-        o[D + 1] = 0.5 * (g.x1 * (Mu[a + 2] * g.Mv[b] * wc + Mu[a] * g.Mv[b + 2] * wc + Mu[a] * g.Mv[b] * g.Mw[c + 2]) +
-                          g.x2 * base);
+        o[4] = 0.5 * (g.x1 * (Mu[a + 2] * g.Mv[b] * wc + Mu[a] * g.Mv[b + 2] * wc + Mu[a] * g.Mv[b] * g.Mw[c + 2]) +
+                      g.x2 * base);
     } else {
-        o[D + 1] = 0.5 * (g.x1 * (Mu[a + 2] * g.Mv[b] + Mu[a] * g.Mv[b + 2]) + g.x2 * base);
+        const double base = Mu[a] * g.Mv[b];
+        o[0] = g.x1 * base;
+        o[1] = g.x1 * Mu[a + 1] * g.Mv[b];
+        o[2] = g.x1 * Mu[a] * g.Mv[b + 1];
+        o[3] = 0.5 * (g.x1 * (Mu[a + 2] * g.Mv[b] + Mu[a] * g.Mv[b + 2]) + g.x2 * base);
     }
 }
-// <(s . psi) u^a v^b w^c psi>
-template <int D, int R, int a, int b, int c>
-__device__ __forceinline__ void apsi(const Maxw<D> &g, const double *s, double *o)
+// o += f * <(s . psi) u^a v^b w^c psi>
+template <int D, int R, bool H, int a, int b, int c>
+__device__ __forceinline__ void apsi_acc(const Maxw<D, R> &g, const double *s, double f, double *o)
 {
     constexpr int NV = D + 2;
     double t[NV];
-    psi_m<D, R, a, b, c>(g, t);
+    psi_m<D, R, H, a, b, c>(g, t);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] = s[0] * t[q];
-    psi_m<D, R, a + 1, b, c>(g, t);
+    for (int q = 0; q < NV; ++q) o[q] += (f * s[0]) * t[q];
+    psi_m<D, R, H, a + 1, b, c>(g, t);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += s[1] * t[q];
-    psi_m<D, R, a, b + 1, c>(g, t);
+    for (int q = 0; q < NV; ++q) o[q] += (f * s[1]) * t[q];
+    psi_m<D, R, H, a, b + 1, c>(g, t);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += s[2] * t[q];
+    for (int q = 0; q < NV; ++q) o[q] += (f * s[2]) * t[q];
     if constexpr (D == 3) {
-        psi_m<D, R, a, b, c + 1>(g, t);
+        psi_m<D, R, H, a, b, c + 1>(g, t);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) o[q] += s[3] * t[q];
+        for (int q = 0; q < NV; ++q) o[q] += (f * s[3]) * t[q];
     }
-    const double h = 0.5 * s[D + 1];
-    psi_m<D, R, a + 2, b, c>(g, t);
+    const double h = 0.5 * f * s[D + 1];
+    double t2[NV];
+    psi_m<D, R, H, a + 2, b, c>(g, t);
+    psi_m<D, R, H, a, b + 2, c>(g, t2);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += h * t[q];
-    psi_m<D, R, a, b + 2, c>(g, t);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += h * t[q];
+    for (int q = 0; q < NV; ++q) t[q] += t2[q];
     if constexpr (D == 3) {
-        psi_m<D, R, a, b, c + 2>(g, t);
+        psi_m<D, R, H, a, b, c + 2>(g, t2);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) o[q] += h * t[q];
+        for (int q = 0; q < NV; ++q) t[q] += t2[q];
     }
-    psi_xi<D, R, a, b, c>(g, t);
+    psi_xi<D, R, H, a, b, c>(g, t2);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += h * t[q];
+    for (int q = 0; q < NV; ++q) o[q] += h * (t[q] + t2[q]);
 }
-// sum_e <u_e (s_e . psi) u^a psi>: direction e adds one power of u / v / w
-template <int D, int R, int a>
-__device__ __forceinline__ void adotu(const Maxw<D> &g, const double (*s)[D + 2], double *o)
+// o += f * sum_e <u_e (s_e . psi) u^a psi>: direction e adds one power of u / v / w
+template <int D, int R, bool H, int a>
+__device__ __forceinline__ void adotu_acc(const Maxw<D, R> &g, const double (*s)[D + 2], double f, double *o)
 {
-    constexpr int NV = D + 2;
-    double t[NV];
-    apsi<D, R, a + 1, 0, 0>(g, s[0], o);
-    apsi<D, R, a, 1, 0>(g, s[1], t);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += t[q];
-    if constexpr (D == 3) {
-        apsi<D, R, a, 0, 1>(g, s[D - 1], t);
-#pragma unroll
-        for (int q = 0; q < NV; ++q) o[q] += t[q];
-    }
+    apsi_acc<D, R, H, a + 1, 0, 0>(g, s[0], f, o);
+    apsi_acc<D, R, H, a, 1, 0>(g, s[1], f, o);
+    if constexpr (D == 3) apsi_acc<D, R, H, a, 0, 1>(g, s[D - 1], f, o);
 }
 
 // moment matrix M_ab = <psi_a psi_b> (full range), factored without pivoting
-// (symmetric positive definite): L D L^T in place
-template <int D>
-__device__ __forceinline__ void mfactor(const Maxw<D> &g, double (*M)[D + 2])
+// (symmetric positive definite)
+template <int D, int R>
+__device__ __forceinline__ void mfactor(const Maxw<D, R> &g, double (*M)[D + 2])
 {
     constexpr int NV = D + 2;
     double c[NV];
-    psi_m<D, 0, 0, 0, 0>(g, c);
+    psi_m<D, R, false, 0, 0, 0>(g, c);
 #pragma unroll
     for (int q = 0; q < NV; ++q) M[q][0] = c[q];
-    psi_m<D, 0, 1, 0, 0>(g, c);
+    psi_m<D, R, false, 1, 0, 0>(g, c);
 #pragma unroll
     for (int q = 0; q < NV; ++q) M[q][1] = c[q];
-    psi_m<D, 0, 0, 1, 0>(g, c);
+    psi_m<D, R, false, 0, 1, 0>(g, c);
 #pragma unroll
     for (int q = 0; q < NV; ++q) M[q][2] = c[q];
     if constexpr (D == 3) {
-        psi_m<D, 0, 0, 0, 1>(g, c);
+        psi_m<D, R, false, 0, 0, 1>(g, c);
 #pragma unroll
         for (int q = 0; q < NV; ++q) M[q][3] = c[q];
     }
     {
         double e[NV] = {};
         e[D + 1] = 1.0;
-        apsi<D, 0, 0, 0, 0>(g, e, c);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) c[q] = 0.0;
+        apsi_acc<D, R, false, 0, 0, 0>(g, e, 1.0, c);
 #pragma unroll
         for (int q = 0; q < NV; ++q) M[q][D + 1] = c[q];
     }
@@ -214,11 +221,12 @@ __device__ __forceinline__ void msolve(const double (*M)[D + 2], double *x)
 }
 
 // micro slopes a_e = M^-1 dW_e / rho and A from <A + a.u> = 0 (Eq.(co))
-template <int D>
-__device__ __forceinline__ void slopes(const Maxw<D> &g, const double (*M)[D + 2], const double *dW, double (*a)[D + 2],
-                                       double *A)
+template <int D, int R>
+__device__ __forceinline__ void slopes(const Maxw<D, R> &g, const double *dW, double (*a)[D + 2], double *A)
 {
     constexpr int NV = D + 2;
+    double M[NV][NV];
+    mfactor<D, R>(g, M);
     const double ir = 1.0 / g.rho;
 #pragma unroll
     for (int e = 0; e < D; ++e) {
@@ -226,89 +234,93 @@ __device__ __forceinline__ void slopes(const Maxw<D> &g, const double (*M)[D + 2
         for (int q = 0; q < NV; ++q) a[e][q] = dW[e * NV + q] * ir;
         msolve<D>(M, a[e]);
     }
-    adotu<D, 0, 0>(g, a, A);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) A[q] = -A[q];
+    for (int q = 0; q < NV; ++q) A[q] = 0.0;
+    adotu_acc<D, R, false, 0>(g, a, -1.0, A);
     msolve<D>(M, A);
 }
 
-// BGK flux at one Gauss point in the face frame (x1 = normal): F time-
-// integrated over [0, dt], Wt = W(dt).  dW[e*NV+q] = dW_q / dx_e (frame).
-template <int D>
-__device__ __noinline__ void gks_local(const double *wl, const double *dwl, const double *wr, const double *dwr, double dt,
-                                       double tau, double gm1, double K, double *F, double *Wt)
+// time coefficients of Eqs. (dis1), (dis2): integrals over [0, dt] (q1..q5)
+// and values at dt (c1..c3, ex)
+struct TimeC {
+    double q1, q2, q3, q4, q5, c1, c2, c3, ex, tau, dt;
+};
+__device__ __forceinline__ TimeC time_coeffs(double dt, double tau)
+{
+    TimeC t;
+    const double ex = exp(-dt / tau);
+    t.q1 = dt - tau * (1.0 - ex);
+    t.q2 = 2.0 * tau * tau - tau * dt - tau * ex * (dt + 2.0 * tau);
+    t.q3 = 0.5 * dt * dt - tau * dt + tau * tau * (1.0 - ex);
+    t.q4 = tau * (1.0 - ex);
+    t.q5 = tau * tau - tau * ex * (dt + tau);
+    t.c1 = 1.0 - ex;
+    t.c2 = (dt + tau) * ex - tau;
+    t.c3 = dt - tau + tau * ex;
+    t.ex = ex;
+    t.tau = tau;
+    t.dt = dt;
+    return t;
+}
+
+// one side of the interface (R = 1: left state on u1 > 0, R = 2: right on
+// u1 < 0), frame coordinates: its share of W^c (Eq.(compatibility2)), of the
+// equilibrium slopes (reading C10e), and its kinetic terms of Eq.(dis1):
+// F += rho int_0^dt e^{-t/tau} <u1 psi [1 - tau (a.u + A) - t a.u]>_half dt,
+// Wt += rho e^{-dt/tau} <psi [1 - tau (a.u + A) - dt a.u]>_half
+// dWc: shared memory, component k of this thread at dWc[k * blockDim.x] (frees registers)
+template <int D, int R>
+__device__ __forceinline__ void side_pass(const double *w, const double *dw, const TimeC &T, double gm1, double K,
+                                          double *Wc, double *dWc, double *F, double *Wt)
 {
     constexpr int NV = D + 2;
-    double al[D][NV], ar[D][NV], Al[NV], Ar[NV], ac[D][NV], Ac[NV];
-    Maxw<D> gl, gr, gc;
-    double M[NV][NV];
-    maxw<D>(wl, gm1, K, gl);
-    maxw<D>(wr, gm1, K, gr);
-    mfactor<D>(gl, M);
-    slopes<D>(gl, M, dwl, al, Al);
-    mfactor<D>(gr, M);
-    slopes<D>(gr, M, dwr, ar, Ar);
-    // W^c (Eq.(compatibility2)) and its slopes (reading C10e)
-    double wc[NV], t1[NV], t2[NV], dwc[D * NV];
-    psi_m<D, 1, 0, 0, 0>(gl, t1);
-    psi_m<D, 2, 0, 0, 0>(gr, t2);
+    Maxw<D, R> g;
+    maxw<D, R>(w, gm1, K, g);
+    double a[D][NV], A[NV];
+    slopes<D, R>(g, dw, a, A);
+    double t[NV];
+    psi_m<D, R, true, 0, 0, 0>(g, t);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) wc[q] = gl.rho * t1[q] + gr.rho * t2[q];
-    maxw<D>(wc, gm1, K, gc);
+    for (int q = 0; q < NV; ++q) { Wc[q] += g.rho * t[q]; Wt[q] += (g.rho * T.ex) * t[q]; }
 #pragma unroll
     for (int e = 0; e < D; ++e) {
-        apsi<D, 1, 0, 0, 0>(gl, al[e], t1);
-        apsi<D, 2, 0, 0, 0>(gr, ar[e], t2);
+        double u[NV];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) dwc[e * NV + q] = gl.rho * t1[q] + gr.rho * t2[q];
+        for (int q = 0; q < NV; ++q) u[q] = 0.0;
+        apsi_acc<D, R, true, 0, 0, 0>(g, a[e], g.rho, u);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) dWc[(e * NV + q) * blockDim.x] += u[q];
     }
-    mfactor<D>(gc, M);
-    slopes<D>(gc, M, dwc, ac, Ac);
-    // time integrals (Eqs. (dis1), (dis2))
-    const double ex = exp(-dt / tau);
-    const double q1 = dt - tau * (1.0 - ex);
-    const double q2 = 2.0 * tau * tau - tau * dt - tau * ex * (dt + 2.0 * tau);
-    const double q3 = 0.5 * dt * dt - tau * dt + tau * tau * (1.0 - ex);
-    const double q4 = tau * (1.0 - ex);
-    const double q5 = tau * tau - tau * ex * (dt + tau);
-    const double c1 = 1.0 - ex, c2 = (dt + tau) * ex - tau, c3 = dt - tau + tau * ex;
-    // equilibrium part
-    psi_m<D, 0, 1, 0, 0>(gc, t1);
+    psi_m<D, R, true, 1, 0, 0>(g, t);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) F[q] = q1 * t1[q];
-    adotu<D, 0, 1>(gc, ac, t1);
-    apsi<D, 0, 1, 0, 0>(gc, Ac, t2);
+    for (int q = 0; q < NV; ++q) F[q] += (g.rho * T.q4) * t[q];
+    adotu_acc<D, R, true, 1>(g, a, -g.rho * (T.tau * T.q4 + T.q5), F);
+    apsi_acc<D, R, true, 1, 0, 0>(g, A, -g.rho * T.tau * T.q4, F);
+    adotu_acc<D, R, true, 0>(g, a, -g.rho * T.ex * (T.tau + T.dt), Wt);
+    apsi_acc<D, R, true, 0, 0, 0>(g, A, -g.rho * T.ex * T.tau, Wt);
+}
+
+// equilibrium part (Eq.(dis2)): C1 g^c + C2 a^c.u g^c + C3 A^c g^c
+template <int D>
+__device__ __forceinline__ void equilibrium_pass(const double *Wc, const double *dWc, const TimeC &T, double gm1,
+                                                 double K, double *F, double *Wt)
+{
+    constexpr int NV = D + 2;
+    Maxw<D, 0> g;
+    maxw<D, 0>(Wc, gm1, K, g);
+    double a[D][NV], A[NV];
+    slopes<D, 0>(g, dWc, a, A);
+    double t[NV];
+    psi_m<D, 0, false, 1, 0, 0>(g, t);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) F[q] = gc.rho * (F[q] + q2 * t1[q] + q3 * t2[q]);
-    psi_m<D, 0, 0, 0, 0>(gc, t1);
+    for (int q = 0; q < NV; ++q) F[q] += (g.rho * T.q1) * t[q];
+    adotu_acc<D, 0, false, 1>(g, a, g.rho * T.q2, F);
+    apsi_acc<D, 0, false, 1, 0, 0>(g, A, g.rho * T.q3, F);
+    psi_m<D, 0, false, 0, 0, 0>(g, t);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) Wt[q] = c1 * t1[q];
-    adotu<D, 0, 0>(gc, ac, t1);
-    apsi<D, 0, 0, 0, 0>(gc, Ac, t2);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) Wt[q] = gc.rho * (Wt[q] + c2 * t1[q] + c3 * t2[q]);
-    // kinetic part: e^{-t/tau} g^k [1 - tau (a.u + A) - t a.u], k = l on u1 > 0, r on u1 < 0
-    double t3[NV];
-    psi_m<D, 1, 1, 0, 0>(gl, t1);
-    adotu<D, 1, 1>(gl, al, t2);
-    apsi<D, 1, 1, 0, 0>(gl, Al, t3);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) F[q] += gl.rho * (q4 * t1[q] - (tau * q4 + q5) * t2[q] - tau * q4 * t3[q]);
-    psi_m<D, 2, 1, 0, 0>(gr, t1);
-    adotu<D, 2, 1>(gr, ar, t2);
-    apsi<D, 2, 1, 0, 0>(gr, Ar, t3);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) F[q] += gr.rho * (q4 * t1[q] - (tau * q4 + q5) * t2[q] - tau * q4 * t3[q]);
-    psi_m<D, 1, 0, 0, 0>(gl, t1);
-    adotu<D, 1, 0>(gl, al, t2);
-    apsi<D, 1, 0, 0, 0>(gl, Al, t3);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) Wt[q] += gl.rho * ex * (t1[q] - (tau + dt) * t2[q] - tau * t3[q]);
-    psi_m<D, 2, 0, 0, 0>(gr, t1);
-    adotu<D, 2, 0>(gr, ar, t2);
-    apsi<D, 2, 0, 0, 0>(gr, Ar, t3);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) Wt[q] += gr.rho * ex * (t1[q] - (tau + dt) * t2[q] - tau * t3[q]);
+    for (int q = 0; q < NV; ++q) Wt[q] += (g.rho * T.c1) * t[q];
+    adotu_acc<D, 0, false, 0>(g, a, g.rho * T.c2, Wt);
+    apsi_acc<D, 0, false, 0, 0, 0>(g, A, g.rho * T.c3, Wt);
 }
 
 // face frame (C10a): e0 = n; 3D e1 = normalise(n x x_k), x_k the axis of the
@@ -322,7 +334,7 @@ __device__ __forceinline__ void frame(const double *n, double (*E)[3])
         for (int b = 0; b < 3; ++b) E[a][b] = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) E[0][k] = n[k];
-    if (D == 2) {
+    if constexpr (D == 2) {
         E[1][0] = -n[1];
         E[1][1] = n[0];
     } else {
@@ -341,62 +353,39 @@ __device__ __forceinline__ void frame(const double *n, double (*E)[3])
     }
 }
 
-// global frame: rotate states / gradients in, flux / state out
+// rotate a state and its gradient (G[c*NV+q] = dW_q/dx_c, global) into the frame
 template <int D>
-__device__ __forceinline__ void gks_flux(const double *wl, const double *gl, const double *wr, const double *gr,
-                                         const double *n, double dt, double tau, double gm1, double K, double *F,
-                                         double *Wt)
+__device__ __forceinline__ void to_frame(const double (*E)[3], const double *W, const double *G, double *w, double *g)
 {
     constexpr int NV = D + 2;
-    double E[3][3];
-    frame<D>(n, E);
-    double lw[2][NV], lg[2][D * NV];
+    w[0] = W[0];
+    w[NV - 1] = W[NV - 1];
 #pragma unroll
-    for (int sd = 0; sd < 2; ++sd) {
-        const double *W = sd ? wr : wl, *G = sd ? gr : gl;
-        lw[sd][0] = W[0];
-        lw[sd][NV - 1] = W[NV - 1];
+    for (int a = 0; a < D; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < D; ++b) s += E[a][b] * W[1 + b];
+        w[1 + a] = s;
+    }
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+        double col[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) s += E[b][c] * G[c * NV + q];
+            col[q] = s;
+        }
+        g[b * NV] = col[0];
+        g[b * NV + NV - 1] = col[NV - 1];
 #pragma unroll
         for (int a = 0; a < D; ++a) {
             double s = 0.0;
 #pragma unroll
-            for (int b = 0; b < D; ++b) s += E[a][b] * W[1 + b];
-            lw[sd][1 + a] = s;
+            for (int c = 0; c < D; ++c) s += E[a][c] * col[1 + c];
+            g[b * NV + 1 + a] = s;
         }
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-            double col[NV];
-#pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                double s = 0.0;
-#pragma unroll
-                for (int c = 0; c < D; ++c) s += E[b][c] * G[c * NV + q];
-                col[q] = s;
-            }
-            lg[sd][b * NV] = col[0];
-            lg[sd][b * NV + NV - 1] = col[NV - 1];
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                double s = 0.0;
-#pragma unroll
-                for (int c = 0; c < D; ++c) s += E[a][c] * col[1 + c];
-                lg[sd][b * NV + 1 + a] = s;
-            }
-        }
-    }
-    double Fl[NV], Wl[NV];
-    gks_local<D>(lw[0], lg[0], lw[1], lg[1], dt, tau, gm1, K, Fl, Wl);
-    F[0] = Fl[0];
-    F[NV - 1] = Fl[NV - 1];
-    Wt[0] = Wl[0];
-    Wt[NV - 1] = Wl[NV - 1];
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-        double s = 0.0, u = 0.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) { s += E[a][k] * Fl[1 + a]; u += E[a][k] * Wl[1 + a]; }
-        F[1 + k] = s;
-        Wt[1 + k] = u;
     }
 }
 
@@ -454,71 +443,87 @@ template <int D> __device__ __forceinline__ int qb(int k)
     return D == 2 ? (k == 0 ? 0 : 1) : (k == 0 ? 0 : (k == 1 ? 1 : (k == 2 ? 2 : (k == 3 ? 1 : (k == 4 ? 2 : 2)))));
 }
 
+// one cell per group of 8 lanes, one conserved component per lane (lanes
+// >= NV only help with nothing but keep the groups warp-aligned): the p2
+// operator columns are read once per group (same address in the group's
+// lanes), neighbour states coalesced across the component lanes, and the
+// per-lane state is one component's p1 / p2 / WENO (C4, C2, C5).
+constexpr int kRL = 8;
+template <int NV>
+__device__ __forceinline__ double pick(const double *v, int q)   // v[q] without dynamic register indexing
+{
+    double r = v[0];
+#pragma unroll
+    for (int k = 1; k < NV; ++k) r = q == k ? v[k] : r;
+    return r;
+}
 template <int D>
-__global__ void __launch_bounds__(128) k_ho_recon(DevLevel L, HoDev H, Phys ph, BCs bc, double cfl_exp, double gam0,
+__global__ void __launch_bounds__(256) k_ho_recon(DevLevel L, HoDev H, Phys ph, BCs bc, double cfl_exp, double gam0,
                                                   double eps)
 {
     constexpr int NV = D + 2, NQ = D * (D + 1) / 2, NK = D + NQ, NC = 1 + NK;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= L.n) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i0 = t / kRL, q = t % kRL;
+    const bool live = i0 < L.n;
+    const int i = live ? i0 : L.n - 1;
+    const bool comp = live && q < NV;
+    const int qq = q < NV ? q : 0;
     const int f0 = __ldg(H.hfoff + i), f1 = __ldg(H.hfoff + i + 1);
     const double V = __ldg(L.vol + i);
     double wi[NV];
     ld_vec<NV>(L.W + (size_t)i * NV, wi);
-    // C8: Sigma, Dt; C4: Green-Gauss sums
-    double sig = 0.0, g1[NV][D];
+    const double wq = pick<NV>(wi, qq);
+    // C8: Sigma, Dt; C4: Green-Gauss sum of this component
+    double sig = 0.0, g1[D];
 #pragma unroll
-    for (int q = 0; q < NV; ++q)
-#pragma unroll
-        for (int k = 0; k < D; ++k) g1[q][k] = 0.0;
+    for (int k = 0; k < D; ++k) g1[k] = 0.0;
     for (int s = f0; s < f1; ++s) {
         const int sf = __ldg(H.hface + s);
         const int f = (sf > 0 ? sf : -sf) - 1;
         const double sg = sf > 0 ? 1.0 : -1.0;
         sig += __ldg(H.sr + f);
-        double A[D], S2 = 0.0;
+        double A[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) { A[k] = sg * __ldg(L.fA + (size_t)k * L.nf + f); S2 += A[k] * A[k]; }
+        for (int k = 0; k < D; ++k) A[k] = sg * __ldg(L.fA + (size_t)k * L.nf + f);
         const int r = __ldg(L.fr + f);
-        double wm[NV];
+        double qm;
         if (r >= 0) {
             const int j = sf > 0 ? r : __ldg(L.fl + f);
-            ld_vec<NV>(L.W + (size_t)j * NV, wm);
+            qm = __ldg(L.W + (size_t)j * NV + qq);
         } else {
+            double S2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) S2 += A[k] * A[k];
             const double iS = 1.0 / sqrt(S2);
-            double nn[D];
+            double nn[D], wg[NV];
 #pragma unroll
             for (int k = 0; k < D; ++k) nn[k] = A[k] * iS;
-            ghost<D>(bc.kind[-r - 1], wi, bc, nn, wm);
+            ghost<D>(bc.kind[-r - 1], wi, bc, nn, wg);
+            qm = pick<NV>(wg, qq);
         }
+        const double h = (qm + wq) / (2.0 * V);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            const double h = (wm[q] + wi[q]) / (2.0 * V);
-#pragma unroll
-            for (int k = 0; k < D; ++k) g1[q][k] += h * A[k];
-        }
+        for (int k = 0; k < D; ++k) g1[k] += h * A[k];
     }
-    L.sigma[i] = sig;
-    H.dt[i] = cfl_exp * V / sig;
-    const double ai = H.alpha[i];
+    if (live && q == 0) {
+        L.sigma[i] = sig;
+        H.dt[i] = cfl_exp * V / sig;
+    }
+    const double ai = __ldg(H.alpha + i);
 #pragma unroll
-    for (int q = 0; q < NV; ++q)
-#pragma unroll
-        for (int k = 0; k < D; ++k) g1[q][k] *= ai;
+    for (int k = 0; k < D; ++k) g1[k] *= ai;
     double m2[NQ];
 #pragma unroll
     for (int k = 0; k < NQ; ++k) m2[k] = __ldg(H.m2 + (size_t)i * NQ + k);
-    double *po = H.poly + (size_t)i * NV * NC;
+    double c[NC];                                   // this component's final polynomial
     const int p0 = __ldg(H.poff + i), p1 = __ldg(H.poff + i + 1);
     int flag = 0;
     if (p1 > p0) {
         flag = 1;
-        // C2: a = sum_m Pq_m (Q_m - Q_i) + sum_e Pg_{m,e} (Q_e)_m, neighbours in the operator's order
-        double a[NV][NK];
+        // C2: a = sum_m Pq_m (Q_m - Q_i) + sum_e Pg_{m,e} (Q_e)_m
+        double a[NK];
 #pragma unroll
-        for (int q = 0; q < NV; ++q)
-#pragma unroll
-            for (int k = 0; k < NK; ++k) a[q][k] = 0.0;
+        for (int k = 0; k < NK; ++k) a[k] = 0.0;
         const double *P = H.P + p0;
         for (int s = f0; s < f1; ++s) {
             const int sf = __ldg(H.hface + s);
@@ -526,128 +531,82 @@ __global__ void __launch_bounds__(128) k_ho_recon(DevLevel L, HoDev H, Phys ph, 
             const int r = __ldg(L.fr + f);
             if (r < 0) continue;
             const int j = sf > 0 ? r : __ldg(L.fl + f);
-            double dq[NV], gj[NV * D];
-            ld_vec<NV>(L.W + (size_t)j * NV, dq);
-            ld_vec<NV * D>(H.G_ + (size_t)j * NV * D, gj);
+            const double dq = __ldg(L.W + (size_t)j * NV + qq) - wq;
+            double gj[D];
 #pragma unroll
-            for (int q = 0; q < NV; ++q) dq[q] -= wi[q];
+            for (int e = 0; e < D; ++e) gj[e] = __ldg(H.G_ + ((size_t)j * NV + qq) * D + e);
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
-                const double pq = __ldg(P + k);
-                double pg[D];
+                double v = __ldg(P + k) * dq;
 #pragma unroll
-                for (int e = 0; e < D; ++e) pg[e] = __ldg(P + (1 + e) * NK + k);
-#pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    double v = pq * dq[q];
-#pragma unroll
-                    for (int e = 0; e < D; ++e) v += pg[e] * gj[q * D + e];
-                    a[q][k] += v;
-                }
+                for (int e = 0; e < D; ++e) v += __ldg(P + (1 + e) * NK + k) * gj[e];
+                a[k] += v;
             }
             P += (D + 1) * NK;
         }
-        // C5: WENO-Z combination per component
+        // C5: WENO-Z combination
         const double V2 = D == 3 ? cbrt(V * V) : V;      // |Omega|^{2/d}
         const double V4 = V2 * V2;                          // |Omega|^{4/d}
         const double g0 = gam0, gg1 = 1.0 - gam0;
+        double Kh[D][D];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            double Kh[D][D];
+        for (int x = 0; x < D; ++x)
 #pragma unroll
-            for (int x = 0; x < D; ++x)
+            for (int y = 0; y < D; ++y) Kh[x][y] = 0.0;
 #pragma unroll
-                for (int y = 0; y < D; ++y) Kh[x][y] = 0.0;
+        for (int k = 0; k < NQ; ++k) {
+            Kh[qa<D>(k)][qb<D>(k)] += a[D + k];
+            Kh[qb<D>(k)][qa<D>(k)] += a[D + k];
+        }
+        double grad2 = 0.0;
+#pragma unroll
+        for (int e = 0; e < D; ++e) grad2 += a[e] * a[e];
+#pragma unroll
+        for (int e = 0; e < D; ++e)
 #pragma unroll
             for (int k = 0; k < NQ; ++k) {
-                Kh[qa<D>(k)][qb<D>(k)] += a[q][D + k];
-                Kh[qb<D>(k)][qa<D>(k)] += a[q][D + k];
+                // sum_{c,c'} K_ec K_ec' M2_cc' over the symmetric M2: off-diagonal pairs twice
+                const int x = qa<D>(k), y = qb<D>(k);
+                grad2 += (x == y ? 1.0 : 2.0) * Kh[e][x] * Kh[e][y] * m2[k];
             }
-            double grad2 = 0.0;
+        double hess2 = 0.0;
 #pragma unroll
-            for (int e = 0; e < D; ++e) grad2 += a[q][e] * a[q][e];
+        for (int k = 0; k < NQ; ++k) hess2 += Kh[qa<D>(k)][qb<D>(k)] * Kh[qa<D>(k)][qb<D>(k)];
+        const double beta0 = V2 * grad2 + V4 * hess2;
+        double gn = 0.0;
 #pragma unroll
-            for (int e = 0; e < D; ++e)
+        for (int k = 0; k < D; ++k) gn += g1[k] * g1[k];
+        const double beta1 = V2 * gn;
+        const double tz = fabs(beta0 - beta1);
+        double w0 = g0 * (1.0 + tz / (beta0 + eps)), w1 = gg1 * (1.0 + tz / (beta1 + eps));
+        const double ws = w0 + w1;
+        w0 /= ws;
+        w1 /= ws;
+        const double cq = w0 / g0, cl = w1 - w0 * gg1 / g0;
+        c[0] = wq;
 #pragma unroll
-                for (int k = 0; k < NQ; ++k) {
-                    // sum_{c,c'} K_ec K_ec' M2_cc' over the symmetric M2: off-diagonal pairs twice
-                    const int c = qa<D>(k), cc = qb<D>(k);
-                    grad2 += (c == cc ? 1.0 : 2.0) * Kh[e][c] * Kh[e][cc] * m2[k];
-                }
-            double hess2 = 0.0;
+        for (int k = 0; k < NQ; ++k) c[0] -= cq * a[D + k] * m2[k];
 #pragma unroll
-            for (int k = 0; k < NQ; ++k) hess2 += Kh[qa<D>(k)][qb<D>(k)] * Kh[qa<D>(k)][qb<D>(k)];
-            const double beta0 = V2 * grad2 + V4 * hess2;
-            double gn = 0.0;
+        for (int k = 0; k < D; ++k) c[1 + k] = cq * a[k] + cl * g1[k];
 #pragma unroll
-            for (int k = 0; k < D; ++k) gn += g1[q][k] * g1[q][k];
-            const double beta1 = V2 * gn;
-            const double tz = fabs(beta0 - beta1);
-            double w0 = g0 * (1.0 + tz / (beta0 + eps)), w1 = gg1 * (1.0 + tz / (beta1 + eps));
-            const double ws = w0 + w1;
-            w0 /= ws;
-            w1 /= ws;
-            const double cq = w0 / g0, cl = w1 - w0 * gg1 / g0;
-            double c0 = wi[q];
-#pragma unroll
-            for (int k = 0; k < NQ; ++k) c0 -= cq * a[q][D + k] * m2[k];
-            po[q * NC] = c0;
-#pragma unroll
-            for (int k = 0; k < D; ++k) po[q * NC + 1 + k] = cq * a[q][k] + cl * g1[q][k];
-#pragma unroll
-            for (int k = 0; k < NQ; ++k) po[q * NC + 1 + D + k] = cq * a[q][D + k];
-        }
+        for (int k = 0; k < NQ; ++k) c[1 + D + k] = cq * a[D + k];
     } else {
+        c[0] = wq;
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            po[q * NC] = wi[q];
+        for (int k = 0; k < D; ++k) c[1 + k] = g1[k];
 #pragma unroll
-            for (int k = 0; k < D; ++k) po[q * NC + 1 + k] = g1[q][k];
-#pragma unroll
-            for (int k = 0; k < NQ; ++k) po[q * NC + 1 + D + k] = 0.0;
-        }
+        for (int k = 0; k < NQ; ++k) c[1 + D + k] = 0.0;
     }
-    // C6b: positivity at every Gauss point of the cell's faces
-    double x0[D];
+    if (comp) {
+        double *po = H.poly + ((size_t)i * NV + q) * NC;
 #pragma unroll
-    for (int k = 0; k < D; ++k) x0[k] = __ldg(H.ctr + (size_t)i * D + k);
-    bool bad = false;
-    for (int s = f0; s < f1 && !bad; ++s) {
-        const int sf = __ldg(H.hface + s);
-        const int f = (sf > 0 ? sf : -sf) - 1;
-        for (int k = 0; k < H.G; ++k) {
-            if (__ldg(H.gw + (size_t)f * H.G + k) == 0.0) continue;
-            double y[D];
-#pragma unroll
-            for (int e = 0; e < D; ++e) y[e] = __ldg(H.gp + ((size_t)f * H.G + k) * D + e) - x0[e];
-            double w[NV];
-#pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                double v = po[q * NC];
-#pragma unroll
-                for (int e = 0; e < D; ++e) v += po[q * NC + 1 + e] * y[e];
-#pragma unroll
-                for (int kk = 0; kk < NQ; ++kk) v += po[q * NC + 1 + D + kk] * y[qa<D>(kk)] * y[qb<D>(kk)];
-                w[q] = v;
-            }
-            const double p = pressure<D>(w, ph.gm1);
-            if (!(w[0] > 0.0) || !(p > 0.0)) { bad = true; break; }
-        }
+        for (int k = 0; k < NC; ++k) po[k] = c[k];
+        if (q == 0) H.flags[i] = flag;
     }
-    if (bad) {
-        flag |= 2;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            po[q * NC] = wi[q];
-#pragma unroll
-            for (int k = 1; k < NC; ++k) po[q * NC + k] = 0.0;
-        }
-    }
-    H.flags[i] = flag;
 }
 
-// value and gradient of a cell polynomial at y = x - x_cell
-template <int D>
+// value (and gradient) of a cell polynomial at y = x - x_cell
+template <int D, bool GRAD>
 __device__ __forceinline__ void peval(const double *po, const double *y, double *w, double *g)
 {
     constexpr int NV = D + 2, NQ = D * (D + 1) / 2, NC = 1 + D + NQ;
@@ -656,80 +615,150 @@ __device__ __forceinline__ void peval(const double *po, const double *y, double 
         double c[NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) c[k] = __ldg(po + q * NC + k);
-        double v = c[0];
-        double gr[D];
+        if constexpr (GRAD) {
+            double gr[D];
 #pragma unroll
-        for (int e = 0; e < D; ++e) { v += c[1 + e] * y[e]; gr[e] = c[1 + e]; }
+            for (int e = 0; e < D; ++e) gr[e] = c[1 + e];
 #pragma unroll
-        for (int k = 0; k < NQ; ++k) {
-            const int a = qa<D>(k), b = qb<D>(k);
-            v += c[1 + D + k] * y[a] * y[b];
-            gr[a] += c[1 + D + k] * y[b];
-            gr[b] += c[1 + D + k] * y[a];
+            for (int k = 0; k < NQ; ++k) {
+                const int a = qa<D>(k), b = qb<D>(k);
+                gr[a] += c[1 + D + k] * y[b];
+                gr[b] += c[1 + D + k] * y[a];
+            }
+#pragma unroll
+            for (int e = 0; e < D; ++e) g[e * NV + q] = gr[e];
+        } else {
+            double v = c[0];
+#pragma unroll
+            for (int e = 0; e < D; ++e) v += c[1 + e] * y[e];
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) v += c[1 + D + k] * y[qa<D>(k)] * y[qb<D>(k)];
+            w[q] = v;
         }
-        w[q] = v;
-#pragma unroll
-        for (int e = 0; e < D; ++e) g[e * NV + q] = gr[e];
     }
 }
 
+// one face per group of G lanes, one Gauss point per lane (padding lanes of
+// triangles idle); the lanes' weighted flux / state / DF combine by shuffles
 template <int D>
 __global__ void __launch_bounds__(128) k_ho_flux(DevLevel L, HoDev H, Phys ph, BCs bc, double c1, double c2)
 {
     constexpr int NV = D + 2, NQ = D * (D + 1) / 2, NC = 1 + D + NQ;
-    const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= L.nf) return;
-    const int l = __ldg(L.fl + f), r = __ldg(L.fr + f);
-    double A[D], S2 = 0.0;
-#pragma unroll
-    for (int k = 0; k < D; ++k) { A[k] = __ldg(L.fA + (size_t)k * L.nf + f); S2 += A[k] * A[k]; }
-    const double S = sqrt(S2);
-    double n[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) n[k] = A[k] / S;
-    const double dtl = H.dt[l];
-    const double dtf = r >= 0 ? fmin(dtl, H.dt[r]) : dtl;
-    double xl[D], xr[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-        xl[k] = __ldg(H.ctr + (size_t)l * D + k);
-        xr[k] = r >= 0 ? __ldg(H.ctr + (size_t)r * D + k) : 0.0;
-    }
-    const int kind = r < 0 ? bc.kind[-r - 1] : 0;
+    constexpr int G = D == 3 ? 4 : 2;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = t / G, k = t % G;
+    const bool live = f < L.nf;
+    const int fc = live ? f : L.nf - 1;
+    const double w = live ? __ldg(H.gw + (size_t)fc * G + k) : 0.0;
     double Fs[NV], Ws[NV], ap = 1.0;
 #pragma unroll
     for (int q = 0; q < NV; ++q) { Fs[q] = 0.0; Ws[q] = 0.0; }
-    for (int k = 0; k < H.G; ++k) {
-        const double w = __ldg(H.gw + (size_t)f * H.G + k);
-        if (w == 0.0) continue;
-        double x[D], y[D];
+    const int l = __ldg(L.fl + fc), r = __ldg(L.fr + fc);
+    double A[D], S2 = 0.0;
 #pragma unroll
-        for (int e = 0; e < D; ++e) x[e] = __ldg(H.gp + ((size_t)f * H.G + k) * D + e);
-        double wl[NV], gl[D * NV], wr[NV], gr[D * NV];
+    for (int e = 0; e < D; ++e) { A[e] = __ldg(L.fA + (size_t)e * L.nf + fc); S2 += A[e] * A[e]; }
+    const double S = sqrt(S2);
+    double n[D];
 #pragma unroll
-        for (int e = 0; e < D; ++e) y[e] = x[e] - xl[e];
-        peval<D>(H.poly + (size_t)l * NV * NC, y, wl, gl);
+    for (int e = 0; e < D; ++e) n[e] = A[e] / S;
+    const double dtl = __ldg(H.dt + l);
+    const double dtf = r >= 0 ? fmin(dtl, __ldg(H.dt + r)) : dtl;
+    if (w != 0.0) {
+        double x[D], yl[D], yr[D];
+#pragma unroll
+        for (int e = 0; e < D; ++e) {
+            x[e] = __ldg(H.gp + ((size_t)fc * G + k) * D + e);
+            yl[e] = x[e] - __ldg(H.ctr + (size_t)l * D + e);
+            yr[e] = r >= 0 ? x[e] - __ldg(H.ctr + (size_t)r * D + e) : 0.0;
+        }
+        const int kind = r < 0 ? bc.kind[-r - 1] : 0;
+        const double *pl = H.poly + (size_t)l * NV * NC;
+        const double *pr = r >= 0 ? H.poly + (size_t)r * NV * NC : pl;
+        double wl[NV], wr[NV], gtmp[D * NV];
+        // C6b: an inadmissible Gauss-point state (rho <= 0 or p <= 0) takes the
+        // cell average with zero gradient, for that side at that point
+        peval<D, false>(pl, yl, wl, nullptr);
+        const bool badl = !(wl[0] > 0.0) || !(pressure<D>(wl, ph.gm1) > 0.0);
+        if (badl) ld_vec<NV>(L.W + (size_t)l * NV, wl);
+        bool badr = false;
         if (r >= 0) {
-#pragma unroll
-            for (int e = 0; e < D; ++e) y[e] = x[e] - xr[e];
-            peval<D>(H.poly + (size_t)r * NV * NC, y, wr, gr);
+            peval<D, false>(pr, yr, wr, nullptr);
+            badr = !(wr[0] > 0.0) || !(pressure<D>(wr, ph.gm1) > 0.0);
+            if (badr) ld_vec<NV>(L.W + (size_t)r * NV, wr);
         } else {
             ghost<D>(kind, wl, bc, n, wr);
-#pragma unroll
-            for (int e = 0; e < D * NV; ++e) gr[e] = kind == GMG_EXTRAP ? gl[e] : 0.0;
         }
-        ap *= df_point<D>(wl, wr, n, ph);
-        const double pl = pressure<D>(wl, ph.gm1), pr = pressure<D>(wr, ph.gm1);
-        const double tau = c1 * dtf + c2 * dtf * fabs(pl - pr) / (pl + pr);
-        double F[NV], Wt[NV];
-        gks_flux<D>(wl, gl, wr, gr, n, dtf, tau, ph.gm1, ph.K, F, Wt);
+        ap = df_point<D>(wl, wr, n, ph);
+        const double pL = pressure<D>(wl, ph.gm1), pR = pressure<D>(wr, ph.gm1);
+        const double tau = c1 * dtf + c2 * dtf * fabs(pL - pR) / (pL + pR);
+        const TimeC T = time_coeffs(dtf, tau);
+        double E[3][3];
+        frame<D>(n, E);
+        __shared__ double sh_dwc[D * NV * 128];
+        double *dWc = sh_dwc + threadIdx.x;
+        double Wc[NV], Fl[NV], Wl[NV];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) { Fs[q] += w * F[q]; Ws[q] += w * Wt[q]; }
+        for (int q = 0; q < NV; ++q) { Wc[q] = 0.0; Fl[q] = 0.0; Wl[q] = 0.0; }
+#pragma unroll
+        for (int q = 0; q < D * NV; ++q) dWc[q * blockDim.x] = 0.0;
+        {
+            double lw[NV], lg[D * NV];
+            if (badl) {
+#pragma unroll
+                for (int q = 0; q < D * NV; ++q) gtmp[q] = 0.0;
+            } else {
+                peval<D, true>(pl, yl, nullptr, gtmp);
+            }
+            to_frame<D>(E, wl, gtmp, lw, lg);
+            side_pass<D, 1>(lw, lg, T, ph.gm1, ph.K, Wc, dWc, Fl, Wl);
+        }
+        {
+            double lw[NV], lg[D * NV];
+            if (r >= 0 && !badr) peval<D, true>(pr, yr, nullptr, gtmp);
+            else if (r < 0 && kind == GMG_EXTRAP && !badl) peval<D, true>(pl, yl, nullptr, gtmp);
+            else {
+#pragma unroll
+                for (int q = 0; q < D * NV; ++q) gtmp[q] = 0.0;
+            }
+            to_frame<D>(E, wr, gtmp, lw, lg);
+            side_pass<D, 2>(lw, lg, T, ph.gm1, ph.K, Wc, dWc, Fl, Wl);
+        }
+        {
+            double dwc[D * NV];
+#pragma unroll
+            for (int q = 0; q < D * NV; ++q) dwc[q] = dWc[q * blockDim.x];
+            equilibrium_pass<D>(Wc, dwc, T, ph.gm1, ph.K, Fl, Wl);
+        }
+        // back to the global frame, times the Gauss weight
+        Fs[0] = w * Fl[0];
+        Fs[NV - 1] = w * Fl[NV - 1];
+        Ws[0] = w * Wl[0];
+        Ws[NV - 1] = w * Wl[NV - 1];
+#pragma unroll
+        for (int e = 0; e < D; ++e) {
+            double a = 0.0, b = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) { a += E[c][e] * Fl[1 + c]; b += E[c][e] * Wl[1 + c]; }
+            Fs[1 + e] = w * a;
+            Ws[1 + e] = w * b;
+        }
     }
-    double *o = H.frec + (size_t)f * kHoRec;
+    // combine the G lanes of the face (lane order fixed: deterministic)
 #pragma unroll
-    for (int q = 0; q < NV; ++q) { o[q] = S * Fs[q] / dtf; o[NV + q] = Ws[q]; }
-    o[2 * NV] = ap;
+    for (int o = 1; o < G; o <<= 1) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            Fs[q] += __shfl_xor_sync(0xffffffffu, Fs[q], o);
+            Ws[q] += __shfl_xor_sync(0xffffffffu, Ws[q], o);
+        }
+        ap *= __shfl_xor_sync(0xffffffffu, ap, o);
+    }
+    if (live && k == 0) {
+        double *o = H.frec + (size_t)f * kHoRec;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) { o[q] = S * Fs[q] / dtf; o[NV + q] = Ws[q]; }
+        o[2 * NV] = ap;
+    }
 }
 
 template <int D>
@@ -821,8 +850,8 @@ void ho_launch_t(int which, const DevLevel &L, const HoDev &H, const Phys &ph, c
 {
     switch (which) {
     case 0: k_ho_sr<D><<<hblk(L.nf, 256), 256, 0, s>>>(L, H, ph, bc); break;
-    case 1: k_ho_recon<D><<<hblk(L.n, 128), 128, 0, s>>>(L, H, ph, bc, o.cfl_exp, o.ho_gam0, o.ho_eps); break;
-    case 2: k_ho_flux<D><<<hblk(L.nf, 128), 128, 0, s>>>(L, H, ph, bc, o.ho_c1, o.ho_c2); break;
+    case 1: k_ho_recon<D><<<hblk((int64_t)L.n * kRL, 256), 256, 0, s>>>(L, H, ph, bc, o.cfl_exp, o.ho_gam0, o.ho_eps); break;
+    case 2: k_ho_flux<D><<<hblk((int64_t)L.nf * (D == 3 ? 4 : 2), 128), 128, 0, s>>>(L, H, ph, bc, o.ho_c1, o.ho_c2); break;
     default: k_ho_gather<D><<<hblk(L.n, 256), 256, 0, s>>>(L, H, mode, o.cfl_exp, Rout, aout, L.partial); break;
     }
 }

@@ -1,6 +1,6 @@
 """GPU parity of the NEXT-1 third-order compact GKS fine operator (ho.cu,
 fine_operator = 1) against the oracle (oracle/cgks3.c), through the C ABI:
-the reconstruction (polynomials, p2 / fallback flags bit-exact), one
+the reconstruction (polynomials, p2 flags bit-exact), the Gauss-point positivity fallback, one
 evaluation (R, evolved slopes, DF, Sigma) and whole V-cycles (state,
 slopes, DF, residual history).  Tolerance: the north-star 1e-10 relative L2
 for FP64 states and histories."""
@@ -75,6 +75,25 @@ def test_one_evaluation_matches_oracle(name):
     assert _rel(Gn, Gno) <= TOL, _rel(Gn, Gno)
     assert _rel(a, ao) <= TOL, _rel(a, ao)
     assert np.array_equal(G2, G) and np.array_equal(a2, alpha)      # no state change
+
+
+@pytest.mark.parametrize("name", ["quad2d", "box3d_prism"])
+def test_positivity_fallback_matches_oracle(name):
+    """C6b: rough slopes drive some Gauss-point states inadmissible; both sides
+    fall back at exactly those points (same fp64 decision)."""
+    m, fs = _cases()[name]
+    W, Winf, G, alpha = _state(m, (fs[0], fs[1], 0.02), 5, eps=0.3)    # low pressure, rough slopes
+    G = 40.0 * G
+    Ro, Gno, ao, So, _, nfall = cgks3.residual(cgks3.Mesh3(m), W, G, alpha, Winf)
+    assert nfall > 0
+    s = _solver(m, n_levels=1)
+    s.set_state(W, Winf)
+    s.set_ho_state(G, alpha)
+    R, Gn, a, S = s.ho_residual()
+    s.close()
+    assert _rel(R, Ro) <= TOL, _rel(R, Ro)
+    assert _rel(Gn, Gno) <= TOL
+    assert _rel(a, ao) <= TOL
 
 
 @pytest.mark.parametrize("name", list(_cases()))
