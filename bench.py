@@ -95,6 +95,77 @@ def workload(config):
     return m, W, state.winf(*fs)
 
 
+def fp64_peak_tflops(dev):
+    """measured FP64 reference: torch float64 matmul (cuBLAS DGEMM) 8192^3, best of 3"""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    best = None
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def next1_block(m, W, Winf, args, dev):
+    """NEXT-1: the same V-cycle with the third-order compact GKS
+    fine operator on the same mesh and state; the Gauss-point BGK flux kernel is
+    FP64-ALU bound: roofline against the measured DGEMM FP64 rate, flops per
+    Gauss point from the ncu FP64 instruction counts (profiles/r01/ho_ncu.json)."""
+    import numpy as np
+    import torch
+    from paper_2509_06347_b200 import gmg
+    t0 = time.perf_counter()
+    s = gmg.Solver(m, n_levels=3, device=dev.index or 0, n_sweeps=args.n_sweeps, fine_operator=1, setup_device=1)
+    t_setup = time.perf_counter() - t0
+    s.set_state(W, Winf)
+    for _ in range(2):
+        s.vcycle(1)
+    s.set_state(W, Winf)
+    s.set_ho_state()
+    k = 10
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream(dev)
+    e0.record(st)
+    gmg.gmg_vcycle(s.ctx, k, None)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    s.set_state(W, Winf)
+    s.set_ho_state()
+    pms, pcnt, pby = s.profile_vcycle(3)
+    s.close()
+    gp = int(np.count_nonzero(m.gw))
+    kf = gmg.K_HO_FLUX
+    flux_ms = float(pms[kf]) / max(int(pcnt[kf]), 1)
+    flops_gp = None
+    fp = os.path.join(ROOT, "profiles", "r01", "ho_ncu.json")
+    if os.path.exists(fp):
+        flops_gp = json.load(open(fp)).get("flux_fp64_flops_per_gauss_point")
+    peak = fp64_peak_tflops(dev)
+    ach = flops_gp * gp / (flux_ms * 1e-3) / 1e12 if flops_gp else None
+    tot = float(pms.sum())
+    return {"workload": f"config{args.config}, fine_operator=1 (third-order CGKS fine operator, DESIGN.md §12)",
+            "ms_per_vcycle": ms, "fine_cell_vcycles_per_s": m.n_cells * 1e3 / ms, "setup_s": round(t_setup, 3),
+            "gauss_points": gp,
+            "kernels": {gmg.K_NAMES[q]: {"ms_per_cycle": float(pms[q]) / 3, "share": float(pms[q]) / tot}
+                        for q in range(gmg.K_COUNT) if pcnt[q] > 0},
+            "roofline": {"bound": "alu", "kernel": "k_ho_flux<3> (Gauss-point BGK flux)", "achieved": ach,
+                         "peak": peak, "unit": "TFLOP/s (FP64)", "frac": ach / peak if ach else None,
+                         "avg_launch_ms": flux_ms, "flops_per_gauss_point": flops_gp,
+                         "peak_source": "measured: torch float64 matmul 8192^3 (cuBLAS DGEMM), best of 3",
+                         "flops_def": "ncu FP64 thread instructions of one launch (2 dfma + dmul + dadd) / Gauss points"}}
+
+
 def sweep_updates_per_cycle(sizes, n_sweeps, fine_smoother):
     lv = range(0 if fine_smoother else 1, len(sizes))
     return sum(sizes[l][0] for l in lv) * 2 * n_sweeps
@@ -199,6 +270,7 @@ def main():
     ap.add_argument("--n-sweeps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/cpu)")
+    ap.add_argument("--no-next1", action="store_true", help="skip the NEXT-1 (third-order CGKS fine operator) line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
     args.steps_ref = max(1, min(args.steps, 5))
@@ -333,6 +405,9 @@ def main():
            "d2h_bytes_per_step": int(W.nbytes + (nv * 2 * 8)),
            "ms_per_step": e2e_s * 1e3, "timer": "host wall clock around synchronous ABI calls"}
 
+    next1 = None
+    if ws == 1 and not args.no_next1 and args.config == 4:
+        next1 = next1_block(m, W, Winf, args, dev)
     if rank != 0:
         return 0
     cpu = None
@@ -369,6 +444,7 @@ def main():
         "kernels": kernels, "sweep_only": sweep_only,
         "gpu_launches": int(launches_per_cycle * args.steps + 2),
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+        "next1_cgks3": next1,
     }
     print(json.dumps(line), flush=True)
     return 0

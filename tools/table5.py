@@ -1,7 +1,8 @@
 """Time-to-solution of the GPU multigrid vs the GPU explicit iteration on the
 same mesh -- the structure of the paper's Table 5 ("GPU
 explicit" vs "GPU multigrid" wall times), with this build's first-order KFVS
-operator on every level (the paper's CGKS fine operator is NEXT-1).
+operator on every level, or (--operator cgks3, NEXT-4) the third-order
+compact GKS fine operator of NEXT-1 on the fine level of both arms.
 
 Both arms: impulsive free-stream start, CUDA-graph-replayed iterations on one
 B200, wall time (device synchronised) until the fine residual (density
@@ -21,10 +22,10 @@ from paper_2509_06347_b200 import gmg  # noqa: E402
 from synth import configs, state  # noqa: E402
 
 
-def solve(m, W, Winf, n_levels, cap, chunk, levels):
+def solve(m, W, Winf, n_levels, cap, chunk, levels, fine_operator=0):
     """iterate to `cap` (or until the deepest level is reached); iterations and
     wall time (constant per iteration, graph replays) to each residual level"""
-    s = gmg.Solver(m, n_levels=n_levels)
+    s = gmg.Solver(m, n_levels=n_levels, fine_operator=fine_operator)
     s.set_state(W, Winf)
     s.vcycle(1)                      # graph capture + warm-up, not timed
     s.set_state(W, Winf)
@@ -52,19 +53,31 @@ def solve(m, W, Winf, n_levels, cap, chunk, levels):
 
 
 def main():
-    out = {}
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--operator", default="first", choices=["first", "cgks3"])
+    args = ap.parse_args()
+    fo = 1 if args.operator == "cgks3" else 0
+    out = {"fine_operator": args.operator}
     cases = [
         # name, mesh config, free stream, initial state, target, caps
         ("config2_naca_M0.5", 2, configs.FREESTREAM[2], "uniform", 1e-3, 2000, 400000),
         ("config4_sphere_M0.5", 4, (1.0, (0.5, 0.0, 0.0), 1.0 / 1.4), "uniform", 1e-3, 2000, 100000),
         ("config3_cylinder_M0.5", 3, (1.0, (0.5, 0.0), 1.0 / 1.4), "uniform", 1e-3, 2000, 200000),
     ]
+    if fo:
+        # NEXT-4 with the third-order CGKS fine operator (NEXT-1): "GPU explicit" is the 1-level
+        # iteration of the same operator, as the paper's Table 5 compares
+        cases = [
+            ("config2_naca_M0.5", 2, configs.FREESTREAM[2], "uniform", 1e-3, 2000, 100000),
+            ("config3_cylinder_M0.5", 3, (1.0, (0.5, 0.0), 1.0 / 1.4), "uniform", 1e-3, 1000, 40000),
+        ]
     levels = (1e-1, 1e-2, 1e-3)
     for name, k, fs, init, target, cap_gmg, cap_exp in cases:
         m = configs.config(k)
         W, Winf = state.uniform(m, *fs), state.winf(*fs)
-        g = solve(m, W, Winf, 3, cap_gmg, 50, levels)
-        e = solve(m, W, Winf, 1, cap_exp, 2000, levels)
+        g = solve(m, W, Winf, 3, cap_gmg, 50, levels, fo)
+        e = solve(m, W, Winf, 1, cap_exp, 2000, levels, fo)
         sp = {}
         for lv in levels:
             a, b = g[f"to_{lv:g}"], e[f"to_{lv:g}"]
@@ -75,7 +88,7 @@ def main():
                      "explicit_over_multigrid": sp}
         print(json.dumps({name: {"cells": out[name]["cells"], "speedups": sp}}), flush=True)
     os.makedirs("gpurun_out", exist_ok=True)
-    json.dump(out, open("gpurun_out/table5.json", "w"), indent=1)
+    json.dump(out, open("gpurun_out/table5%s.json" % ("_cgks3" if fo else ""), "w"), indent=1)
 
 
 if __name__ == "__main__":
