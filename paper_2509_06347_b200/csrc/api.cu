@@ -952,6 +952,7 @@ void carve(gmg_ctx *ctx, Bump &b)
         V.gw = b.take<double>((size_t)nf * H.G);
         V.hfoff = b.take<int>(n + 1);
         V.hface = b.take<int>(H.hface.size());
+        V.hrec = b.take<double>(H.hrec.size());
         V.poff = b.take<int>(n + 1);
         V.P = b.take<double>(H.P.size());
         V.G_ = b.take<double>((size_t)n * nv * d);
@@ -1512,6 +1513,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         CK(cudaMemcpyAsync((void *)V.gw, H.gwl.data(), H.gwl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync((void *)V.hfoff, H.hfoff.data(), H.hfoff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync((void *)V.hface, H.hface.data(), H.hface.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync((void *)V.hrec, H.hrec.data(), H.hrec.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync((void *)V.poff, H.poff.data(), H.poff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
         if (!H.P.empty())
             CK(cudaMemcpyAsync((void *)V.P, H.P.data(), H.P.size() * 8, cudaMemcpyHostToDevice, ctx->stream));

@@ -151,8 +151,11 @@ struct HoDev {
     const double *gw = nullptr;          // [nf][G] weights (0 = padding)
     const int *hfoff = nullptr;          // [n+1] cell -> faces
     const int *hface = nullptr;          // signed local faces: +(f+1) cell is left, -(f+1) right; ascending natural id
+    const double *hrec = nullptr;        // [slots][4] per (cell, face) slot: A outward (D doubles) | (neighbour or
+                                         //   -(patch+1), local face) as two int32 in the last double
     const int *poff = nullptr;           // [n+1] offset (doubles) of the cell's p2 operator; empty = p1 only
-    const double *P = nullptr;           // per interior neighbour m: (D+1) columns of nk: d a / d(Q_m - Q_i), d a / d(Q_e)_m
+    const double *P = nullptr;           // per interior neighbour m: (D+1) columns of nk: d a / d(Q_m - Q_i), d a / d(Q_e)_m,
+                                         // padded to a multiple of 4 doubles (32-byte aligned blocks)
     double *G_ = nullptr;                // [n][nv][D] cell-averaged slopes (carried)
     double *alpha = nullptr;             // [n] DF carried between evaluations (p1 factor, C4/C14)
     double *poly = nullptr;              // [n][nv][nc] final polynomials (c0, lin[D], quad[nq]) about the centroid
@@ -178,6 +181,7 @@ struct HoHost {
     // local (domain 0, level 0)
     std::vector<double> ctr, m2l, gpl, gwl, P;
     std::vector<int> hfoff, hface, poff;
+    std::vector<double> hrec;
     int64_t n_p2 = 0;                    // cells with a p2 operator
     HoDev dev;
 };

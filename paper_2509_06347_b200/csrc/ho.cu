@@ -443,12 +443,10 @@ template <int D> __device__ __forceinline__ int qb(int k)
     return D == 2 ? (k == 0 ? 0 : 1) : (k == 0 ? 0 : (k == 1 ? 1 : (k == 2 ? 2 : (k == 3 ? 1 : (k == 4 ? 2 : 2)))));
 }
 
-// one cell per group of 8 lanes, one conserved component per lane (lanes
-// >= NV only help with nothing but keep the groups warp-aligned): the p2
+// one cell per group of NV lanes, one conserved component per lane: the p2
 // operator columns are read once per group (same address in the group's
 // lanes), neighbour states coalesced across the component lanes, and the
 // per-lane state is one component's p1 / p2 / WENO (C4, C2, C5).
-constexpr int kRL = 8;
 template <int NV>
 __device__ __forceinline__ double pick(const double *v, int q)   // v[q] without dynamic register indexing
 {
@@ -458,12 +456,12 @@ __device__ __forceinline__ double pick(const double *v, int q)   // v[q] without
     return r;
 }
 template <int D>
-__global__ void __launch_bounds__(256) k_ho_recon(DevLevel L, HoDev H, Phys ph, BCs bc, double cfl_exp, double gam0,
+__global__ void __launch_bounds__(256, 4) k_ho_recon(DevLevel L, HoDev H, Phys ph, BCs bc, double cfl_exp, double gam0,
                                                   double eps)
 {
     constexpr int NV = D + 2, NQ = D * (D + 1) / 2, NK = D + NQ, NC = 1 + NK;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int i0 = t / kRL, q = t % kRL;
+    const int i0 = t / NV, q = t % NV;                // NV lanes per cell (no shuffles: any alignment)
     const bool live = i0 < L.n;
     const int i = live ? i0 : L.n - 1;
     const bool comp = live && q < NV;
@@ -473,23 +471,46 @@ __global__ void __launch_bounds__(256) k_ho_recon(DevLevel L, HoDev H, Phys ph, 
     double wi[NV];
     ld_vec<NV>(L.W + (size_t)i * NV, wi);
     const double wq = pick<NV>(wi, qq);
-    // C8: Sigma, Dt; C4: Green-Gauss sum of this component
-    double sig = 0.0, g1[D];
+    const int p0 = __ldg(H.poff + i), p1 = __ldg(H.poff + i + 1);
+    const bool has2 = p1 > p0;
+    // one pass over the cell's face slots (record: A outward | neighbour, face):
+    // C8 Sigma, C4 Green-Gauss sum of this component, C2 p2 = sum_m Pq_m (Q_m - Q_i) + sum_e Pg_{m,e} (Q_e)_m
+    double sig = 0.0, g1[D], a[NK];
 #pragma unroll
     for (int k = 0; k < D; ++k) g1[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < NK; ++k) a[k] = 0.0;
+    const double *P = H.P + p0;
     for (int s = f0; s < f1; ++s) {
-        const int sf = __ldg(H.hface + s);
-        const int f = (sf > 0 ? sf : -sf) - 1;
-        const double sg = sf > 0 ? 1.0 : -1.0;
+        double rc[4];
+        ld4nc(H.hrec + (size_t)s * 4, rc);
+        const int2 jf = *reinterpret_cast<const int2 *>(&rc[3]);
+        const int j = jf.x, f = jf.y;
         sig += __ldg(H.sr + f);
         double A[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) A[k] = sg * __ldg(L.fA + (size_t)k * L.nf + f);
-        const int r = __ldg(L.fr + f);
+        for (int k = 0; k < D; ++k) A[k] = rc[k];
         double qm;
-        if (r >= 0) {
-            const int j = sf > 0 ? r : __ldg(L.fl + f);
+        if (j >= 0) {
             qm = __ldg(L.W + (size_t)j * NV + qq);
+            if (has2) {
+                const double dq = qm - wq;
+                double gj[D];
+#pragma unroll
+                for (int e = 0; e < D; ++e) gj[e] = __ldg(H.G_ + ((size_t)j * NV + qq) * D + e);
+                constexpr int PST = ((D + 1) * NK + 3) & ~3;
+                double pb[PST];
+#pragma unroll
+                for (int k = 0; k < PST; k += 4) ld4nc(P + k, pb + k);
+#pragma unroll
+                for (int k = 0; k < NK; ++k) {
+                    double v = pb[k] * dq;
+#pragma unroll
+                    for (int e = 0; e < D; ++e) v += pb[(1 + e) * NK + k] * gj[e];
+                    a[k] += v;
+                }
+                P += PST;
+            }
         } else {
             double S2 = 0.0;
 #pragma unroll
@@ -498,7 +519,7 @@ __global__ void __launch_bounds__(256) k_ho_recon(DevLevel L, HoDev H, Phys ph, 
             double nn[D], wg[NV];
 #pragma unroll
             for (int k = 0; k < D; ++k) nn[k] = A[k] * iS;
-            ghost<D>(bc.kind[-r - 1], wi, bc, nn, wg);
+            ghost<D>(bc.kind[-j - 1], wi, bc, nn, wg);
             qm = pick<NV>(wg, qq);
         }
         const double h = (qm + wq) / (2.0 * V);
@@ -516,34 +537,9 @@ __global__ void __launch_bounds__(256) k_ho_recon(DevLevel L, HoDev H, Phys ph, 
 #pragma unroll
     for (int k = 0; k < NQ; ++k) m2[k] = __ldg(H.m2 + (size_t)i * NQ + k);
     double c[NC];                                   // this component's final polynomial
-    const int p0 = __ldg(H.poff + i), p1 = __ldg(H.poff + i + 1);
     int flag = 0;
-    if (p1 > p0) {
+    if (has2) {
         flag = 1;
-        // C2: a = sum_m Pq_m (Q_m - Q_i) + sum_e Pg_{m,e} (Q_e)_m
-        double a[NK];
-#pragma unroll
-        for (int k = 0; k < NK; ++k) a[k] = 0.0;
-        const double *P = H.P + p0;
-        for (int s = f0; s < f1; ++s) {
-            const int sf = __ldg(H.hface + s);
-            const int f = (sf > 0 ? sf : -sf) - 1;
-            const int r = __ldg(L.fr + f);
-            if (r < 0) continue;
-            const int j = sf > 0 ? r : __ldg(L.fl + f);
-            const double dq = __ldg(L.W + (size_t)j * NV + qq) - wq;
-            double gj[D];
-#pragma unroll
-            for (int e = 0; e < D; ++e) gj[e] = __ldg(H.G_ + ((size_t)j * NV + qq) * D + e);
-#pragma unroll
-            for (int k = 0; k < NK; ++k) {
-                double v = __ldg(P + k) * dq;
-#pragma unroll
-                for (int e = 0; e < D; ++e) v += __ldg(P + (1 + e) * NK + k) * gj[e];
-                a[k] += v;
-            }
-            P += (D + 1) * NK;
-        }
         // C5: WENO-Z combination
         const double V2 = D == 3 ? cbrt(V * V) : V;      // |Omega|^{2/d}
         const double V4 = V2 * V2;                          // |Omega|^{4/d}
@@ -779,13 +775,15 @@ __global__ void __launch_bounds__(256) k_ho_gather(DevLevel L, HoDev H, int mode
         double al = 1.0;
         const int f0 = __ldg(H.hfoff + i), f1 = __ldg(H.hfoff + i + 1);
         for (int s = f0; s < f1; ++s) {
+            double rc[4];
+            ld4nc(H.hrec + (size_t)s * 4, rc);                       // A outward | neighbour, face
+            const int f = reinterpret_cast<const int2 *>(&rc[3])->y;
             const int sf = __ldg(H.hface + s);
-            const int f = (sf > 0 ? sf : -sf) - 1;
             const double sg = sf > 0 ? 1.0 : -1.0;
             const double *o = H.frec + (size_t)f * kHoRec;
             double A[D];
 #pragma unroll
-            for (int k = 0; k < D; ++k) A[k] = sg * __ldg(L.fA + (size_t)k * L.nf + f);
+            for (int k = 0; k < D; ++k) A[k] = rc[k];
 #pragma unroll
             for (int q = 0; q < NV; ++q) {
                 R[q] += sg * __ldg(o + q);
@@ -850,7 +848,7 @@ void ho_launch_t(int which, const DevLevel &L, const HoDev &H, const Phys &ph, c
 {
     switch (which) {
     case 0: k_ho_sr<D><<<hblk(L.nf, 256), 256, 0, s>>>(L, H, ph, bc); break;
-    case 1: k_ho_recon<D><<<hblk((int64_t)L.n * kRL, 256), 256, 0, s>>>(L, H, ph, bc, o.cfl_exp, o.ho_gam0, o.ho_eps); break;
+    case 1: k_ho_recon<D><<<hblk((int64_t)L.n * (D + 2), 256), 256, 0, s>>>(L, H, ph, bc, o.cfl_exp, o.ho_gam0, o.ho_eps); break;
     case 2: k_ho_flux<D><<<hblk((int64_t)L.nf * (D == 3 ? 4 : 2), 128), 128, 0, s>>>(L, H, ph, bc, o.ho_c1, o.ho_c2); break;
     default: k_ho_gather<D><<<hblk(L.n, 256), 256, 0, s>>>(L, H, mode, o.cfl_exp, Rout, aout, L.partial); break;
     }

@@ -103,12 +103,25 @@ gmg_status ho_prepare(gmg_ctx *ctx)
                 return D0.fnat[std::abs(a) - 1] < D0.fnat[std::abs(b) - 1];
             });
     }
+    // per-slot records: A outward from the cell, (neighbour | -(patch+1), local face)
+    H.hrec.assign((size_t)H.hfoff[n] * 4, 0.0);
+    for (int64_t i = 0; i < n; ++i)
+        for (int s = H.hfoff[i]; s < H.hfoff[i + 1]; ++s) {
+            const int f = std::abs(H.hface[s]) - 1;
+            const double sg = H.hface[s] > 0 ? 1.0 : -1.0;
+            const int64_t g = D0.fnat[f];
+            for (int e = 0; e < d; ++e) H.hrec[(size_t)s * 4 + e] = sg * G.avec[(size_t)e * NF + g];
+            int32_t jf[2] = {D0.fr[f] < 0 ? D0.fr[f] : (D0.fl[f] == i ? D0.fr[f] : D0.fl[f]), (int32_t)f};
+            std::memcpy(&H.hrec[(size_t)s * 4 + 3], jf, sizeof jf);
+        }
     // p2 operators (C2, C3: >= d + 1 interior neighbours)
     std::vector<int> nnb(n, 0);
     for (int64_t i = 0; i < n; ++i)
         for (int s = H.hfoff[i]; s < H.hfoff[i + 1]; ++s) nnb[i] += D0.fr[std::abs(H.hface[s]) - 1] >= 0;
+    // per neighbour (d + 1) columns of nk, padded to a multiple of 4 doubles (32-byte loads)
+    const int pst = ((d + 1) * nk + 3) & ~3;
     H.poff.assign(n + 1, 0);
-    for (int64_t i = 0; i < n; ++i) H.poff[i + 1] = H.poff[i] + (nnb[i] >= d + 1 ? nnb[i] * (d + 1) * nk : 0);
+    for (int64_t i = 0; i < n; ++i) H.poff[i + 1] = H.poff[i] + (nnb[i] >= d + 1 ? nnb[i] * pst : 0);
     H.P.assign((size_t)H.poff[n], 0.0);
     std::vector<char> ok(n, 1);
     auto m2at = [&](int64_t c, int a, int b) {
@@ -167,7 +180,7 @@ gmg_status ho_prepare(gmg_ctx *ctx)
             std::fill(rhs.begin(), rhs.end(), 0.0);
             rhs[nk + q] = 1.0;
             lu_solve(m, K, piv, rhs.data());
-            double *col = out + (size_t)q * (d + 1) * nk;
+            double *col = out + (size_t)q * pst;
             for (int k = 0; k < nk; ++k) col[k] = rhs[k];
             // columns of the neighbour's averaged slopes: 2 L^T e_(q,e)
             for (int e = 0; e < d; ++e) {
