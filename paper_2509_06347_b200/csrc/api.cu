@@ -929,7 +929,10 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.recvbuf = b.take<double>((size_t)L.n_recv * nv);
         }
     }
-    ctx->d_stage = b.take<double>((size_t)nv * nmax);
+    // natural-order staging: nv components; with the NEXT-1 geometry also the slopes (nv d) and the
+    // polynomials (nv (1 + d + d(d+1)/2)) of gmg_set/get_ho_state, gmg_ho_residual, gmg_ho_recon
+    const int stage_comp = ctx->ho ? nv * (1 + d + d * (d + 1) / 2) : nv;
+    ctx->d_stage = b.take<double>((size_t)stage_comp * nmax);
     ctx->hist_cap = 4096;
     ctx->d_hist = b.take<double>((size_t)ctx->hist_cap * nv);
     ctx->d_flag = b.take<int>(4);

@@ -166,3 +166,70 @@ def test_config2_sized_vcycle_matches_oracle():
     Wo, ho = oracle.vcycle(H, W, Winf, oracle.Options(fine_operator=1), 2, mesh=m, ho_state={})
     assert _rel(Wg, Wo) <= TOL
     assert np.max(np.abs(hist - ho) / ho[0][None, :]) <= TOL
+
+
+@pytest.fixture(scope="module")
+def config4():
+    return configs.config(4)
+
+
+@pytest.mark.slow
+def test_config4_full_size_p2_sampled_against_oracle(config4):
+    """bench-size launch (1 M cells): with gamma_0 = 1 the device polynomial is
+    p2 (C5), which the oracle computes cell by cell (orc3_p2 needs only the
+    cell's stencil) -- compared on 2 000 sampled cells."""
+    m = config4
+    fs = configs.FREESTREAM[4]
+    W = state.bow_shock(m, *fs)
+    rng = np.random.default_rng(11)
+    d, n = m.dim, m.n_cells
+    G = 0.05 * rng.standard_normal((d + 2, d, n))
+    s = _solver(m, n_levels=3, ho_gam0=1.0, setup_device=1)
+    s.set_state(W, state.winf(*fs))
+    s.set_ho_state(G, np.ones(n))
+    poly, fl = s.ho_recon()
+    s.close()
+    M = cgks3.Mesh3(m)
+    cells = rng.choice(n, 2000, replace=False)
+    inn = np.nonzero(m.right >= 0)[0]
+    owner = np.concatenate([m.left, m.right[inn]])
+    face = np.concatenate([np.arange(m.n_faces), inn])
+    order = np.lexsort((face, owner))
+    owner, face = owner[order], face[order]
+    start = np.searchsorted(owner, np.arange(n + 1))
+    checked = 0
+    for i in cells:
+        f = face[start[i]:start[i + 1]]                      # ascending face id (the oracle's order)
+        nb = [int(m.right[x] if m.left[x] == i else m.left[x]) for x in f if m.right[x] >= 0]
+        for q in range(d + 2):
+            a = cgks3.p2(M, int(i), nb, W[q], G[q])
+            if a is None:
+                assert not (fl[i] & 1)
+                continue
+            assert fl[i] & 1
+            scale = np.abs(a).max() + 1e-300
+            assert np.max(np.abs(poly[i, q, 1:] - a)) <= 1e-10 * max(scale, 1.0), (i, q)
+            c0 = W[q, i] - float(np.dot(a[d:], m.m2[:, i]))
+            assert abs(poly[i, q, 0] - c0) <= 1e-12 * max(abs(c0), 1.0)
+            checked += 1
+    assert checked > 5000
+
+
+@pytest.mark.slow
+def test_config4_full_size_free_stream(config4):
+    """bench-size launch: with every patch far field, a uniform free stream is
+    preserved exactly by the third-order V-cycle (R = 0, slopes 0, DF 1)."""
+    import copy
+    m = copy.copy(config4)
+    m.patch_kind = np.zeros_like(config4.patch_kind)
+    fs = configs.FREESTREAM[4]
+    W = state.uniform(m, *fs)
+    s = _solver(m, n_levels=3, setup_device=1)
+    s.set_state(W, state.winf(*fs))
+    hist = s.vcycle(2)
+    Wg = s.get_state(0)
+    G, a = s.get_ho_state()
+    s.close()
+    assert np.max(np.abs(Wg - W)) <= 1e-12 * np.max(np.abs(W))
+    assert np.max(np.abs(G)) <= 1e-8 and np.allclose(a, 1.0)
+    assert np.max(hist) <= 1e-9 * max(1.0, float(np.abs(W).max()))
