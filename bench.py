@@ -154,7 +154,24 @@ def next1_block(m, W, Winf, args, dev):
     peak = fp64_peak_tflops(dev)
     ach = flops_gp * gp / (flux_ms * 1e-3) / 1e12 if flops_gp else None
     tot = float(pms.sum())
+    cpu = None
+    if not args.no_cpu_baseline:
+        # the oracle (oracle/cgks3.c + vcycle.py, 1 thread, as it stands) on a bounded sample: one V-cycle of a
+        # tet/prism box mesh, same operator and options
+        import oracle
+        from synth import configs, state
+        mb = configs.box3d(14, 14, 10, 4, seed=1)
+        fsb = (1.0, (0.6, 0.2, -0.1), 0.7)
+        Wb, Wib = state.perturbed(mb, *fsb, eps=0.1, seed=2), state.winf(*fsb)
+        Hb = oracle.build_hierarchy(mb, 3, 0.5)
+        t0 = time.perf_counter()
+        oracle.vcycle(Hb, Wb, Wib, oracle.Options(fine_operator=1), 1, mesh=mb, ho_state={})
+        dt = time.perf_counter() - t0
+        cpu = {"value": mb.n_cells / dt, "unit": "fine-cell V-cycles/s", "cores": 1, "kind": "oracle",
+               "sample": f"1 V-cycle (third-order fine operator) of a {mb.n_cells}-cell tet/prism box mesh "
+                         f"({dt:.1f} s), plain C oracle, 1 thread"}
     return {"workload": f"config{args.config}, fine_operator=1 (third-order CGKS fine operator, DESIGN.md §12)",
+            "cpu_baseline": cpu,
             "ms_per_vcycle": ms, "fine_cell_vcycles_per_s": m.n_cells * 1e3 / ms, "setup_s": round(t_setup, 3),
             "gauss_points": gp,
             "kernels": {gmg.K_NAMES[q]: {"ms_per_cycle": float(pms[q]) / 3, "share": float(pms[q]) / tot}

@@ -690,33 +690,106 @@ void enqueue_restrict(Launcher &Lc, Domain &dm, int l)
     Lc.post(GMG_K_RESTRICT, dm.lbytes[l].restrict_);
 }
 
-// NEXT-1: one evaluation of the third-order CGKS operator on the fine level
-// (ho.cu): S r, reconstruction, Gauss-point BGK fluxes, gather(mode)
-void enqueue_ho_eval(Launcher &Lc, int mode, double *Rout = nullptr, double *aout = nullptr, bool recon_only = false)
+// NEXT-1 halo (partitioned runs): owned -> ghost copies of a level-0 per-cell
+// array of ncomp doubles (slopes, polynomials, Dt), all colors at once
+void enqueue_exchange_ho(Launcher &Lc, double *HoDev::*arr, int ncomp)
 {
     gmg_ctx *ctx = Lc.ctx;
-    Domain &dm = ctx->dom[0];
-    DevLevel &L = dm.dv[0];
-    const HoHost &H = *ctx->ho;
+    if (ctx->nparts <= 1) return;
+    for (Domain &dm : ctx->dom) {
+        const DomLevel &H = dm.lv[0];
+        DevLevel &L = dm.dv[0];
+        const int64_t s1 = H.send_off.back();
+        if (s1 > 0) {
+            Lc.pre(GMG_K_NORM);
+            klaunch(ctx, k_pack, dim3(nblk(s1)), dim3(256), Lc.s, (int)s1, L.send_idx, (const double *)(L.ho.*arr), ncomp, 0,
+                    ncomp, dm.ho.sendbuf);
+            Lc.post(GMG_K_NORM, (double)s1 * ncomp * 16);
+        }
+    }
+    if (ctx->opt.nranks > 1) {
+        Domain &dm = ctx->dom[0];
+        const DomLevel &H = dm.lv[0];
+        const int np = (int)H.peers.size(), ng = (int)H.send_off.size() - 1;
+        nccl().GroupStart();
+        for (int g = 0; g < ng; ++g) {
+            const int peer = H.peers[g % np];
+            const int64_t sc = H.send_off[g + 1] - H.send_off[g], rc = H.recv_off[g + 1] - H.recv_off[g];
+            if (sc) nccl().Send(dm.ho.sendbuf + H.send_off[g] * ncomp, sc * ncomp, ncclDouble, peer, (ncclComm_t)ctx->nccl_comm, Lc.s);
+            if (rc) nccl().Recv(dm.ho.recvbuf + H.recv_off[g] * ncomp, rc * ncomp, ncclDouble, peer, (ncclComm_t)ctx->nccl_comm, Lc.s);
+        }
+        nccl().GroupEnd();
+    } else {
+        for (Domain &dm : ctx->dom) {
+            const DomLevel &H = dm.lv[0];
+            const int np = (int)H.peers.size(), ng = (int)H.send_off.size() - 1;
+            for (int g = 0; g < ng; ++g) {
+                const int64_t sc = H.send_off[g + 1] - H.send_off[g];
+                if (!sc) continue;
+                Domain &dp = ctx->dom[H.peers[g % np]];
+                const DomLevel &Hp = dp.lv[0];
+                const int npp = (int)Hp.peers.size();
+                const int kk = (int)(std::lower_bound(Hp.peers.begin(), Hp.peers.end(), dm.rank) - Hp.peers.begin());
+                const int gp = (g / np) * npp + kk;
+                cudaMemcpyAsync(dp.ho.recvbuf + Hp.recv_off[gp] * ncomp, dm.ho.sendbuf + H.send_off[g] * ncomp,
+                                sizeof(double) * sc * ncomp, cudaMemcpyDeviceToDevice, Lc.s);
+            }
+        }
+    }
+    for (Domain &dm : ctx->dom) {
+        const DomLevel &H = dm.lv[0];
+        DevLevel &L = dm.dv[0];
+        const int64_t r1 = H.recv_off.back();
+        if (r1 > 0) {
+            Lc.pre(GMG_K_NORM);
+            klaunch(ctx, k_unpack, dim3(nblk(r1)), dim3(256), Lc.s, (int)r1, L.recv_idx, (const double *)dm.ho.recvbuf,
+                    L.ho.*arr, ncomp, 0, ncomp, 0, 0);
+            Lc.post(GMG_K_NORM, (double)r1 * ncomp * 16);
+        }
+    }
+    ctx->exchanges++;
+}
+
+// NEXT-1: one evaluation of the third-order CGKS operator on the fine level
+// (ho.cu): S r, reconstruction, Gauss-point BGK fluxes, gather(mode).  Every
+// domain; on partitioned runs the ghosts' W, slopes, then polynomials and Dt
+// come by halo exchange.  Rout / aout: per-domain outputs (ABI), or null.
+template <int D>
+void enqueue_ho_eval(Launcher &Lc, int mode, double *DevLevel::*Rout = nullptr, double *DevLevel::*aout = nullptr,
+                     bool recon_only = false)
+{
+    gmg_ctx *ctx = Lc.ctx;
     const Phys ph = phys(ctx);
     const BCs bc = bcs(ctx);
-    Lc.pre(GMG_K_HO_RECON);
-    ho_launch(0, L, H.dev, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
-    Lc.post(GMG_K_HO_RECON, H.bytes_sr);
-    Lc.pre(GMG_K_HO_RECON);
-    ho_launch(1, L, H.dev, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
-    Lc.post(GMG_K_HO_RECON, H.bytes_recon);
+    constexpr int NV = D + 2, NC = 1 + D + D * (D + 1) / 2;
+    enqueue_exchange<D>(Lc, 0, EX_W, -1);
+    enqueue_exchange_ho(Lc, &HoDev::G_, NV * D);
+    for (Domain &dm : ctx->dom) {
+        DevLevel &L = dm.dv[0];
+        Lc.pre(GMG_K_HO_RECON);
+        ho_launch(0, L, L.ho, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
+        Lc.post(GMG_K_HO_RECON, dm.ho.bytes_sr);
+        Lc.pre(GMG_K_HO_RECON);
+        ho_launch(1, L, L.ho, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
+        Lc.post(GMG_K_HO_RECON, dm.ho.bytes_recon);
+    }
     if (recon_only) return;
-    Lc.pre(GMG_K_HO_FLUX);
-    ho_launch(2, L, H.dev, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
-    Lc.post(GMG_K_HO_FLUX, H.bytes_flux);
-    Lc.pre(GMG_K_GATHER);
-    ho_launch(3, L, H.dev, ph, bc, ctx->opt, mode, Rout, aout, Lc.s);
-    Lc.post(GMG_K_GATHER, H.bytes_gather);
-    if (mode & HO_NORM) {
-        Lc.pre(GMG_K_NORM);
-        klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(256), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq);
-        Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
+    enqueue_exchange_ho(Lc, &HoDev::poly, NV * NC);
+    enqueue_exchange_ho(Lc, &HoDev::dt, 1);
+    for (size_t di = 0; di < ctx->dom.size(); ++di) {
+        Domain &dm = ctx->dom[di];
+        DevLevel &L = dm.dv[0];
+        Lc.pre(GMG_K_HO_FLUX);
+        ho_launch(2, L, L.ho, ph, bc, ctx->opt, 0, nullptr, nullptr, Lc.s);
+        Lc.post(GMG_K_HO_FLUX, dm.ho.bytes_flux);
+        Lc.pre(GMG_K_GATHER);
+        ho_launch(3, L, L.ho, ph, bc, ctx->opt, mode, Rout ? L.*Rout : nullptr, aout ? L.*aout : nullptr, Lc.s);
+        Lc.post(GMG_K_GATHER, dm.ho.bytes_gather);
+        if (mode & HO_NORM) {
+            Lc.pre(GMG_K_NORM);
+            klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(256), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + di * L.nv);
+            Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
+        }
     }
 }
 
@@ -731,10 +804,10 @@ void enqueue_vcycle(Launcher &Lc)
     if (ctx->opt.fine_operator == 1) {
         // NEXT-1, reading C14: CGKS3 evaluation at (W, G, alpha) -> history, Eq.(smo), slopes, DF;
         // a second evaluation at the updated state -> restricted residual and DF
-        enqueue_ho_eval(Lc, HO_NORM | HO_UPDATE);
+        enqueue_ho_eval<D>(Lc, HO_NORM | HO_UPDATE);
         enqueue_norm_hist(Lc);
         if (nl == 1) return;
-        enqueue_ho_eval(Lc, HO_RT);
+        enqueue_ho_eval<D>(Lc, HO_RT);
     } else {
     // 1-2. fine residual at the cycle start (history entry) + fine pre-smoothing
     enqueue_exchange<D>(Lc, 0, EX_W, -1);
@@ -796,7 +869,7 @@ void enqueue_final_norm(Launcher &Lc)
 {
     gmg_ctx *ctx = Lc.ctx;
     if (ctx->opt.fine_operator == 1) {
-        enqueue_ho_eval(Lc, HO_NORM);
+        enqueue_ho_eval<D>(Lc, HO_NORM);
         enqueue_norm_hist(Lc);
         return;
     }
@@ -940,32 +1013,37 @@ void carve(gmg_ctx *ctx, Bump &b)
     ctx->d_emu = b.take<char>(sizeof(EmuDom) * kEmuMaxDom);
     ctx->d_emu_bar = b.take<int>(2 * kEmuMaxDom);
     ctx->d_sumsq = b.take<double>((size_t)std::max<size_t>(1, ctx->dom.size()) * nv);
-    if (ctx->ho && ctx->ho->prepared) {                       // NEXT-1 (fine level, single domain)
-        HoHost &H = *ctx->ho;
-        HoDev &V = H.dev;
-        const DomLevel &D0 = ctx->dom[0].lv[0];
-        const int64_t n = D0.n_own, nf = D0.nf;
-        V.G = H.G;
-        V.nq = d * (d + 1) / 2;
-        V.nk = d + V.nq;
-        V.nc = 1 + V.nk;
-        V.ctr = b.take<double>((size_t)n * d);
-        V.m2 = b.take<double>((size_t)n * V.nq);
-        V.gp = b.take<double>((size_t)nf * H.G * d);
-        V.gw = b.take<double>((size_t)nf * H.G);
-        V.hfoff = b.take<int>(n + 1);
-        V.hface = b.take<int>(H.hface.size());
-        V.hrec = b.take<double>(H.hrec.size());
-        V.poff = b.take<int>(n + 1);
-        V.P = b.take<double>(H.P.size());
-        V.G_ = b.take<double>((size_t)n * nv * d);
-        V.alpha = b.take<double>(n);
-        V.poly = b.take<double>((size_t)n * nv * V.nc);
-        V.flags = b.take<int>(n);
-        V.sr = b.take<double>(nf);
-        V.dt = b.take<double>(n);
-        V.frec = b.take<double>((size_t)nf * 12);
-        V.Gout = b.take<double>((size_t)n * nv * d);
+    if (ctx->ho && ctx->ho->prepared) {                       // NEXT-1 (fine level)
+        const HoHost &HH = *ctx->ho;
+        for (Domain &dm : ctx->dom) {
+            const HoLocal &H = dm.ho;
+            HoDev &V = dm.dv[0].ho;
+            const DomLevel &D0 = dm.lv[0];
+            const int64_t n = D0.n_own, nl = D0.n_loc, nf = D0.nf;
+            V.G = HH.G;
+            V.nq = d * (d + 1) / 2;
+            V.nk = d + V.nq;
+            V.nc = 1 + V.nk;
+            V.ctr = b.take<double>((size_t)nl * d);
+            V.m2 = b.take<double>((size_t)nl * V.nq);
+            V.gp = b.take<double>((size_t)nf * HH.G * d);
+            V.gw = b.take<double>((size_t)nf * HH.G);
+            V.hfoff = b.take<int>(n + 1);
+            V.hface = b.take<int>(H.hface.size());
+            V.hrec = b.take<double>(H.hrec.size());
+            V.poff = b.take<int>(n + 1);
+            V.P = b.take<double>(H.P.size());
+            V.G_ = b.take<double>((size_t)nl * nv * d);
+            V.alpha = b.take<double>(n);
+            V.poly = b.take<double>((size_t)nl * nv * V.nc);
+            V.flags = b.take<int>(n);
+            V.sr = b.take<double>(nf);
+            V.dt = b.take<double>(nl);
+            V.frec = b.take<double>((size_t)nf * 12);
+            V.Gout = b.take<double>((size_t)n * nv * d);
+            dm.ho.sendbuf = b.take<double>(D0.send_idx.size() * (size_t)nv * V.nc);
+            dm.ho.recvbuf = b.take<double>(D0.recv_idx.size() * (size_t)nv * V.nc);
+        }
     }
 }
 
@@ -1506,22 +1584,24 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         ctx->nccl_comm = comm;
     }
     if (ctx->ho) {
-        HoHost &H = *ctx->ho;
-        HoDev &V = H.dev;
-        const int64_t n = ctx->dom[0].lv[0].n_own;
         const int nvd = (ctx->opt.dim + 2) * ctx->opt.dim;
-        CK(cudaMemcpyAsync((void *)V.ctr, H.ctr.data(), H.ctr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync((void *)V.m2, H.m2l.data(), H.m2l.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync((void *)V.gp, H.gpl.data(), H.gpl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync((void *)V.gw, H.gwl.data(), H.gwl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync((void *)V.hfoff, H.hfoff.data(), H.hfoff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync((void *)V.hface, H.hface.data(), H.hface.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync((void *)V.hrec, H.hrec.data(), H.hrec.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync((void *)V.poff, H.poff.data(), H.poff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-        if (!H.P.empty())
-            CK(cudaMemcpyAsync((void *)V.P, H.P.data(), H.P.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-        k_fill<<<nblk(n * nvd), 256, 0, ctx->stream>>>((int)(n * nvd), V.G_, 0.0);   // reading C1
-        k_fill<<<nblk(n), 256, 0, ctx->stream>>>((int)n, V.alpha, 1.0);
+        for (Domain &dm : ctx->dom) {
+            const HoLocal &H = dm.ho;
+            HoDev &V = dm.dv[0].ho;
+            const int64_t nl = dm.lv[0].n_loc, n = dm.lv[0].n_own;
+            CK(cudaMemcpyAsync((void *)V.ctr, H.ctr.data(), H.ctr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync((void *)V.m2, H.m2l.data(), H.m2l.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync((void *)V.gp, H.gpl.data(), H.gpl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync((void *)V.gw, H.gwl.data(), H.gwl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync((void *)V.hfoff, H.hfoff.data(), H.hfoff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync((void *)V.hface, H.hface.data(), H.hface.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync((void *)V.hrec, H.hrec.data(), H.hrec.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync((void *)V.poff, H.poff.data(), H.poff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+            if (!H.P.empty())
+                CK(cudaMemcpyAsync((void *)V.P, H.P.data(), H.P.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            k_fill<<<nblk(nl * nvd), 256, 0, ctx->stream>>>((int)(nl * nvd), V.G_, 0.0);   // reading C1
+            k_fill<<<nblk(n), 256, 0, ctx->stream>>>((int)n, V.alpha, 1.0);
+        }
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(ctx->stream));
     }
@@ -2031,7 +2111,6 @@ gmg_status gmg_load_ho_geometry(gmg_ctx *ctx, const double *m2, int G, const dou
     if (ctx->ws_ready) { ctx->err = "gmg_load_ho_geometry after gmg_set_workspace"; return GMG_ESTATE; }
     const int d = ctx->opt.dim;
     if (!m2 || !gp || !gw || G != (d == 3 ? 4 : 2)) { ctx->err = "ho geometry: null pointer or G != 4 (3D) / 2 (2D)"; return GMG_EINVAL; }
-    if (ctx->opt.nranks != 1 || ctx->opt.local_domains > 1) { ctx->err = "ho geometry: single domain only"; return GMG_EINVAL; }
     const HostLevel &L0 = ctx->lv[0];
     const int64_t n = L0.n, nf = L0.nf;
     const int nq = d * (d + 1) / 2;
@@ -2057,13 +2136,14 @@ gmg_status gmg_set_ho_state(gmg_ctx *ctx, const double *G, const double *alpha)
     if (!ctx) return GMG_EINVAL;
     gmg_status st = ho_ready(ctx, false);
     if (st) return st;
-    HoDev &V = ctx->ho->dev;
     const int d = ctx->opt.dim, nvd = (d + 2) * d;
-    const int n = ctx->dom[0].dv[0].n;
-    if (G) { st = put_natural(ctx, 0, G, nvd, [&](DevLevel &) { return V.G_; }, false); if (st) return st; }
-    else k_fill<<<nblk((int64_t)n * nvd), 256, 0, ctx->stream>>>(n * nvd, V.G_, 0.0);
-    if (alpha) { st = put_natural(ctx, 0, alpha, 1, [&](DevLevel &) { return V.alpha; }, false); if (st) return st; }
-    else k_fill<<<nblk(n), 256, 0, ctx->stream>>>(n, V.alpha, 1.0);
+    if (G) { st = put_natural(ctx, 0, G, nvd, [](DevLevel &L) { return L.ho.G_; }, true); if (st) return st; }
+    else
+        for (Domain &dm : ctx->dom)
+            k_fill<<<nblk((int64_t)dm.dv[0].n_loc * nvd), 256, 0, ctx->stream>>>(dm.dv[0].n_loc * nvd, dm.dv[0].ho.G_, 0.0);
+    if (alpha) { st = put_natural(ctx, 0, alpha, 1, [](DevLevel &L) { return L.ho.alpha; }, false); if (st) return st; }
+    else
+        for (Domain &dm : ctx->dom) k_fill<<<nblk(dm.dv[0].n), 256, 0, ctx->stream>>>(dm.dv[0].n, dm.dv[0].ho.alpha, 1.0);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     return GMG_OK;
@@ -2074,10 +2154,9 @@ gmg_status gmg_get_ho_state(gmg_ctx *ctx, double *G_out, double *alpha_out)
     if (!ctx) return GMG_EINVAL;
     gmg_status st = ho_ready(ctx, false);
     if (st) return st;
-    HoDev &V = ctx->ho->dev;
     const int d = ctx->opt.dim;
-    if (G_out) { st = get_natural(ctx, 0, [&](DevLevel &) { return (const double *)V.G_; }, (d + 2) * d, G_out); if (st) return st; }
-    if (alpha_out) { st = get_natural(ctx, 0, [&](DevLevel &) { return (const double *)V.alpha; }, 1, alpha_out); if (st) return st; }
+    if (G_out) { st = get_natural(ctx, 0, [](DevLevel &L) { return (const double *)L.ho.G_; }, (d + 2) * d, G_out); if (st) return st; }
+    if (alpha_out) { st = get_natural(ctx, 0, [](DevLevel &L) { return (const double *)L.ho.alpha; }, 1, alpha_out); if (st) return st; }
     return GMG_OK;
 }
 
@@ -2087,13 +2166,12 @@ gmg_status gmg_ho_residual(gmg_ctx *ctx, double *R_out, double *G_out, double *a
     gmg_status st = ho_ready(ctx, true);
     if (st) return st;
     Launcher Lc{ctx, ctx->stream};
-    DevLevel &L = ctx->dom[0].dv[0];
-    HoDev &V = ctx->ho->dev;
-    enqueue_ho_eval(Lc, HO_OUT, L.Rt, L.tmp);
+    if (ctx->opt.dim == 2) enqueue_ho_eval<2>(Lc, HO_OUT, &DevLevel::Rt, &DevLevel::tmp);
+    else enqueue_ho_eval<3>(Lc, HO_OUT, &DevLevel::Rt, &DevLevel::tmp);
     CK(cudaGetLastError());
     const int d = ctx->opt.dim, nv = d + 2;
     if (R_out) { st = get_natural(ctx, 0, [](DevLevel &L_) { return (const double *)L_.Rt; }, nv, R_out); if (st) return st; }
-    if (G_out) { st = get_natural(ctx, 0, [&](DevLevel &) { return (const double *)V.Gout; }, nv * d, G_out); if (st) return st; }
+    if (G_out) { st = get_natural(ctx, 0, [](DevLevel &L_) { return (const double *)L_.ho.Gout; }, nv * d, G_out); if (st) return st; }
     if (alpha_out) { st = get_natural(ctx, 0, [](DevLevel &L_) { return (const double *)L_.tmp; }, 1, alpha_out); if (st) return st; }
     if (sigma_out) { st = get_natural(ctx, 0, [](DevLevel &L_) { return (const double *)L_.sigma; }, 1, sigma_out); if (st) return st; }
     CK(cudaStreamSynchronize(ctx->stream));
@@ -2106,17 +2184,19 @@ gmg_status gmg_ho_recon(gmg_ctx *ctx, double *poly_out, int32_t *flags_out)
     gmg_status st = ho_ready(ctx, true);
     if (st) return st;
     Launcher Lc{ctx, ctx->stream};
-    HoDev &V = ctx->ho->dev;
-    enqueue_ho_eval(Lc, 0, nullptr, nullptr, true);
+    if (ctx->opt.dim == 2) enqueue_ho_eval<2>(Lc, 0, nullptr, nullptr, true);
+    else enqueue_ho_eval<3>(Lc, 0, nullptr, nullptr, true);
     CK(cudaGetLastError());
-    const int d = ctx->opt.dim, nv = d + 2;
-    if (poly_out) { st = get_natural(ctx, 0, [&](DevLevel &) { return (const double *)V.poly; }, nv * V.nc, poly_out); if (st) return st; }
+    const int d = ctx->opt.dim, nv = d + 2, nc = 1 + d + d * (d + 1) / 2;
+    if (poly_out) { st = get_natural(ctx, 0, [](DevLevel &L) { return (const double *)L.ho.poly; }, nv * nc, poly_out); if (st) return st; }
     if (flags_out) {
-        const DomLevel &D0 = ctx->dom[0].lv[0];
-        std::vector<int> fl(D0.n_own);
-        CK(cudaMemcpyAsync(fl.data(), V.flags, fl.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        for (int64_t i = 0; i < D0.n_own; ++i) flags_out[D0.l2n[i]] = fl[i];
+        for (Domain &dm : ctx->dom) {
+            const DomLevel &D0 = dm.lv[0];
+            std::vector<int> fl(D0.n_own);
+            CK(cudaMemcpyAsync(fl.data(), dm.dv[0].ho.flags, fl.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            for (int64_t i = 0; i < D0.n_own; ++i) flags_out[D0.l2n[i]] = fl[i];
+        }
     }
     CK(cudaStreamSynchronize(ctx->stream));
     return GMG_OK;

@@ -80,6 +80,31 @@ struct DomLevel {
     std::vector<int32_t> p2p_off, p2p_k, p2p_g;
 };
 
+// NEXT-1: third-order compact GKS fine operator, fine level.
+// Device arrays live in the workspace (carve); [n] = owned cells, [nl] = owned + ghosts.
+struct HoDev {
+    int G = 0, nk = 0, nc = 0, nq = 0;   // Gauss slots per face, p2 unknowns, poly coefficients, m2 components
+    const double *ctr = nullptr;         // [nl][D] centroids (local order)
+    const double *m2 = nullptr;          // [nl][nq] central second moments
+    const double *gp = nullptr;          // [nf][G][D] Gauss points (local faces)
+    const double *gw = nullptr;          // [nf][G] weights (0 = padding)
+    const int *hfoff = nullptr;          // [n+1] cell -> faces
+    const int *hface = nullptr;          // signed local faces: +(f+1) cell is left, -(f+1) right; ascending natural id
+    const double *hrec = nullptr;        // [slots][4] per (cell, face) slot: A outward (D doubles) | (neighbour or
+                                         //   -(patch+1), local face) as two int32 in the last double
+    const int *poff = nullptr;           // [n+1] offset (doubles) of the cell's p2 operator; empty = p1 only
+    const double *P = nullptr;           // per interior neighbour m: (D+1) columns of nk: d a / d(Q_m - Q_i), d a / d(Q_e)_m,
+                                         // padded to a multiple of 4 doubles (32-byte aligned blocks)
+    double *G_ = nullptr;                // [nl][nv][D] cell-averaged slopes (carried; ghosts by halo)
+    double *alpha = nullptr;             // [n] DF carried between evaluations (p1 factor, C4/C14)
+    double *poly = nullptr;              // [nl][nv][nc] final polynomials (c0, lin[D], quad[nq]) about the centroid
+    int *flags = nullptr;                // [n] bit 0 p2 used
+    double *sr = nullptr;                // [nf] S r_f (first-order spectral radius, A5)
+    double *dt = nullptr;                // [nl] Dt_i = CFL_exp V_i / Sigma_i (C8)
+    double *frec = nullptr;              // [nf][12] S sum_k w F_k / Dt_f [nv] | sum_k w W_k(Dt_f) [nv] | prod alpha_fk
+    double *Gout = nullptr;              // [n][nv][D] slopes of a non-updating evaluation
+};
+
 struct DevLevel {
     int dim, nv, ncolor;
     int n, n_loc, nf;            // owned cells, owned + ghost cells, local faces
@@ -123,6 +148,7 @@ struct DevLevel {
     int n_send, n_recv;
     const int *send_idx, *recv_idx;
     double *sendbuf, *recvbuf;   // [n_send][nv], [n_recv][nv]
+    HoDev ho;                    // NEXT-1 (level 0 only)
 };
 
 struct Profile {
@@ -141,30 +167,6 @@ struct LevelBytes {
     std::vector<double> sweep_out; // per color, extra bytes when the launch also writes W = W0 + dW
 };
 
-// NEXT-1: third-order compact GKS fine operator.  Fine
-// level, single domain.  Device arrays live in the workspace (carve).
-struct HoDev {
-    int G = 0, nk = 0, nc = 0, nq = 0;   // Gauss slots per face, p2 unknowns, poly coefficients, m2 components
-    const double *ctr = nullptr;         // [n][D] centroids (local order)
-    const double *m2 = nullptr;          // [n][nq] central second moments
-    const double *gp = nullptr;          // [nf][G][D] Gauss points (local faces)
-    const double *gw = nullptr;          // [nf][G] weights (0 = padding)
-    const int *hfoff = nullptr;          // [n+1] cell -> faces
-    const int *hface = nullptr;          // signed local faces: +(f+1) cell is left, -(f+1) right; ascending natural id
-    const double *hrec = nullptr;        // [slots][4] per (cell, face) slot: A outward (D doubles) | (neighbour or
-                                         //   -(patch+1), local face) as two int32 in the last double
-    const int *poff = nullptr;           // [n+1] offset (doubles) of the cell's p2 operator; empty = p1 only
-    const double *P = nullptr;           // per interior neighbour m: (D+1) columns of nk: d a / d(Q_m - Q_i), d a / d(Q_e)_m,
-                                         // padded to a multiple of 4 doubles (32-byte aligned blocks)
-    double *G_ = nullptr;                // [n][nv][D] cell-averaged slopes (carried)
-    double *alpha = nullptr;             // [n] DF carried between evaluations (p1 factor, C4/C14)
-    double *poly = nullptr;              // [n][nv][nc] final polynomials (c0, lin[D], quad[nq]) about the centroid
-    int *flags = nullptr;                // [n] bit 0 p2 used
-    double *sr = nullptr;                // [nf] S r_f (first-order spectral radius, A5)
-    double *dt = nullptr;                // [n] Dt_i = CFL_exp V_i / Sigma_i (C8)
-    double *frec = nullptr;              // [nf][12] S sum_k w F_k / Dt_f [nv] | sum_k w W_k(Dt_f) [nv] | prod alpha_fk
-    double *Gout = nullptr;              // [n][nv][D] slopes of a non-updating evaluation
-};
 // modes of the NEXT-1 gather (ho.cu k_ho_gather)
 enum : int {
     HO_NORM = 1,     // per-block partial sums of R_q^2 (history)
@@ -172,22 +174,25 @@ enum : int {
     HO_RT = 4,       // Rt = R, level alpha = alpha (restriction inputs), alpha carried = alpha
     HO_OUT = 8,      // R -> Rout (AoS), new slopes -> Gout, alpha -> alpha_out (ABI)
 };
+// NEXT-1 geometry as loaded (natural order) -- ctx->ho
 struct HoHost {
     int G = 0;
-    double bytes_sr = 0, bytes_recon = 0, bytes_flux = 0, bytes_gather = 0;   // algorithmic bytes per launch
-    int64_t n_gauss_pts = 0;             // Gauss points of the local faces (flux work units)
-    std::vector<double> m2, gp, gw;      // natural order as loaded: [nq][N], [D][G][NF], [G][NF]
+    std::vector<double> m2, gp, gw;      // [nq][N], [D][G][NF], [G][NF]
     bool prepared = false;
-    // local (domain 0, level 0)
-    std::vector<double> ctr, m2l, gpl, gwl, P;
-    std::vector<int> hfoff, hface, poff;
-    std::vector<double> hrec;
+};
+// NEXT-1 per domain, level 0, local order (ho_setup.cpp)
+struct HoLocal {
+    std::vector<double> ctr, m2l, gpl, gwl, P, hrec;   // ctr / m2l over owned + ghost cells
+    std::vector<int> hfoff, hface, poff;               // owned cells
     int64_t n_p2 = 0;                    // cells with a p2 operator
-    HoDev dev;
+    int64_t n_gauss_pts = 0;             // Gauss points of the local faces (flux work units)
+    double bytes_sr = 0, bytes_recon = 0, bytes_flux = 0, bytes_gather = 0;   // algorithmic bytes per launch
+    double *sendbuf = nullptr, *recvbuf = nullptr;     // halo of slopes / polynomials / Dt (partitioned)
 };
 
 struct Domain {
     int rank = 0;
+    HoLocal ho;                  // NEXT-1 (level 0)
     std::vector<DomLevel> lv;
     std::vector<DevLevel> dv;
     std::vector<LevelBytes> lbytes;

@@ -54,49 +54,45 @@ void lu_solve(int m, const std::vector<double> &A, const std::vector<int> &piv, 
 
 }  // namespace
 
-gmg_status ho_prepare(gmg_ctx *ctx)
+// one domain: local geometry over owned + ghost cells, face slots of the
+// owned cells, their p2 operators
+static gmg_status ho_prepare_domain(gmg_ctx *ctx, const HoHost &HH, Domain &dm)
 {
-    HoHost &H = *ctx->ho;
-    if (H.prepared) return GMG_OK;
-    if (ctx->dom.size() != 1 || ctx->opt.nranks != 1) {
-        ctx->err = "fine_operator 1 (third-order CGKS) runs on a single domain";
-        return GMG_EINVAL;
-    }
+    HoLocal &H = dm.ho;
     const HostLevel &G = ctx->lv[0];
-    const DomLevel &D0 = ctx->dom[0].lv[0];
-    const int d = G.dim, nq = d * (d + 1) / 2, nk = d + nq, Gs = H.G;
-    const int64_t n = D0.n_own, nf = D0.nf, N = G.n, NF = G.nf;
-    if (D0.n_loc != n) { ctx->err = "fine_operator 1: unexpected ghost cells"; return GMG_EINVAL; }
-    // local geometry (AoS)
-    H.ctr.assign((size_t)n * d, 0.0);
-    H.m2l.assign((size_t)n * nq, 0.0);
-    for (int64_t i = 0; i < n; ++i) {
+    const DomLevel &D0 = dm.lv[0];
+    const int d = G.dim, nq = d * (d + 1) / 2, nk = d + nq, Gs = HH.G;
+    const int64_t n = D0.n_own, nl = D0.n_loc, nf = D0.nf, N = G.n, NF = G.nf;
+    // local geometry (AoS), owned + ghosts
+    H.ctr.assign((size_t)nl * d, 0.0);
+    H.m2l.assign((size_t)nl * nq, 0.0);
+    for (int64_t i = 0; i < nl; ++i) {
         const int64_t g = D0.l2n[i];
         for (int e = 0; e < d; ++e) H.ctr[i * d + e] = G.ctr[(size_t)e * N + g];
-        for (int k = 0; k < nq; ++k) H.m2l[i * nq + k] = H.m2[(size_t)k * N + g];
+        for (int k = 0; k < nq; ++k) H.m2l[i * nq + k] = HH.m2[(size_t)k * N + g];
     }
     H.gpl.assign((size_t)nf * Gs * d, 0.0);
     H.gwl.assign((size_t)nf * Gs, 0.0);
     for (int64_t f = 0; f < nf; ++f) {
         const int64_t g = D0.fnat[f];
         for (int k = 0; k < Gs; ++k) {
-            H.gwl[f * Gs + k] = H.gw[(size_t)k * NF + g];
-            for (int e = 0; e < d; ++e) H.gpl[(f * Gs + k) * d + e] = H.gp[((size_t)e * Gs + k) * NF + g];
+            H.gwl[f * Gs + k] = HH.gw[(size_t)k * NF + g];
+            for (int e = 0; e < d; ++e) H.gpl[(f * Gs + k) * d + e] = HH.gp[((size_t)e * Gs + k) * NF + g];
         }
     }
-    // cell -> faces, ascending natural face id (the oracle's order)
+    // owned cell -> faces, ascending natural face id (the oracle's order)
     H.hfoff.assign(n + 1, 0);
     for (int64_t f = 0; f < nf; ++f) {
-        H.hfoff[D0.fl[f] + 1]++;
-        if (D0.fr[f] >= 0) H.hfoff[D0.fr[f] + 1]++;
+        if (D0.fl[f] < n) H.hfoff[D0.fl[f] + 1]++;
+        if (D0.fr[f] >= 0 && D0.fr[f] < n) H.hfoff[D0.fr[f] + 1]++;
     }
     for (int64_t i = 0; i < n; ++i) H.hfoff[i + 1] += H.hfoff[i];
     H.hface.assign(H.hfoff[n], 0);
     {
         std::vector<int> fill(H.hfoff.begin(), H.hfoff.end() - 1);
         for (int64_t f = 0; f < nf; ++f) {
-            H.hface[fill[D0.fl[f]]++] = (int)(f + 1);
-            if (D0.fr[f] >= 0) H.hface[fill[D0.fr[f]]++] = -(int)(f + 1);
+            if (D0.fl[f] < n) H.hface[fill[D0.fl[f]]++] = (int)(f + 1);
+            if (D0.fr[f] >= 0 && D0.fr[f] < n) H.hface[fill[D0.fr[f]]++] = -(int)(f + 1);
         }
         for (int64_t i = 0; i < n; ++i)
             std::sort(H.hface.begin() + H.hfoff[i], H.hface.begin() + H.hfoff[i + 1], [&](int a, int b) {
@@ -137,8 +133,8 @@ gmg_status ho_prepare(gmg_ctx *ctx)
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t i = 0; i < n; ++i) {
         if (H.poff[i + 1] == H.poff[i]) continue;
-        const int nb = nnb[i], m = nk + nb, nl = d * nb;
-        std::vector<double> Cm((size_t)nb * nk, 0.0), L((size_t)nl * nk, 0.0);
+        const int nb = nnb[i], m = nk + nb, nlsq = d * nb;
+        std::vector<double> Cm((size_t)nb * nk, 0.0), L((size_t)nlsq * nk, 0.0);
         int r = 0;
         for (int s = H.hfoff[i]; s < H.hfoff[i + 1]; ++s) {
             const int f = std::abs(H.hface[s]) - 1;
@@ -162,9 +158,9 @@ gmg_status ho_prepare(gmg_ctx *ctx)
         std::vector<double> K((size_t)m * m, 0.0);
         for (int x = 0; x < nk; ++x) {
             for (int y = 0; y < nk; ++y) {
-                double s = 0.0;
-                for (int q = 0; q < nl; ++q) s += L[(size_t)q * nk + x] * L[(size_t)q * nk + y];
-                K[x * m + y] = 2.0 * s;
+                double sum = 0.0;
+                for (int q = 0; q < nlsq; ++q) sum += L[(size_t)q * nk + x] * L[(size_t)q * nk + y];
+                K[x * m + y] = 2.0 * sum;
             }
             for (int q = 0; q < nb; ++q) {
                 K[x * m + nk + q] = Cm[q * nk + x];
@@ -192,7 +188,6 @@ gmg_status ho_prepare(gmg_ctx *ctx)
         }
     }
     // a singular system (not expected with >= d + 1 neighbours) -> p1 only
-    int64_t moved = 0;
     std::vector<int> poff2(n + 1, 0);
     for (int64_t i = 0; i < n; ++i) poff2[i + 1] = poff2[i] + ((H.poff[i + 1] > H.poff[i] && ok[i]) ? H.poff[i + 1] - H.poff[i] : 0);
     if (poff2[n] != H.poff[n]) {
@@ -201,9 +196,7 @@ gmg_status ho_prepare(gmg_ctx *ctx)
             if (poff2[i + 1] > poff2[i]) std::memcpy(&P2[poff2[i]], &H.P[H.poff[i]], sizeof(double) * (poff2[i + 1] - poff2[i]));
         H.P.swap(P2);
         H.poff.swap(poff2);
-        moved = 1;
     }
-    (void)moved;
     H.n_p2 = 0;
     for (int64_t i = 0; i < n; ++i) H.n_p2 += H.poff[i + 1] > H.poff[i];
     // algorithmic bytes per launch: each datum moved once
@@ -215,12 +208,22 @@ gmg_status ho_prepare(gmg_ctx *ctx)
     }
     H.n_gauss_pts = gpts;
     H.bytes_sr = (double)nf * (d * 8 + 8 + 8) + (double)(nint + nf) * nv * 8;
-    H.bytes_recon = (double)n * (nv * 8 + 8 + 8 + nq * 8 + d * 8 + 4 * 2 + nv * nc * 8 + 8 + 8 + 4) +
-                    (double)nslots * (4 + d * 8 + 8 + 8 * Gs * (d + 1)) + (double)nint * 2 * (nv * 8 + nv * d * 8) +
-                    (double)H.P.size() * 8;
+    H.bytes_recon = (double)n * (nv * 8 + 8 + 8 + nq * 8 + 4 * 2 + nv * nc * 8 + 8 + 8) +
+                    (double)nslots * (32 + 8) + (double)nint * 2 * (nv * 8 + nv * d * 8) + (double)H.P.size() * 8;
     H.bytes_flux = (double)nf * (8 + d * 8 + Gs * (d + 1) * 8 + 12 * 8) + (double)(nint + nf) * (nv * nc * 8 + d * 8 + 8);
-    H.bytes_gather = (double)nslots * (4 + d * 8 + (2 * nv + 1) * 8) + (double)n * (8 + 8 + 4 * 2 + nv * 8 * 2 + nv * d * 8 + 8);
-    H.prepared = true;
+    H.bytes_gather = (double)nslots * (4 + 32 + (2 * nv + 1) * 8) + (double)n * (8 + 8 + 4 * 2 + nv * 8 * 2 + nv * d * 8 + 8);
+    return GMG_OK;
+}
+
+gmg_status ho_prepare(gmg_ctx *ctx)
+{
+    HoHost &HH = *ctx->ho;
+    if (HH.prepared) return GMG_OK;
+    for (Domain &dm : ctx->dom) {
+        const gmg_status st = ho_prepare_domain(ctx, HH, dm);
+        if (st) return st;
+    }
+    HH.prepared = true;
     return GMG_OK;
 }
 

@@ -233,3 +233,49 @@ def test_config4_full_size_free_stream(config4):
     assert np.max(np.abs(Wg - W)) <= 1e-12 * np.max(np.abs(W))
     assert np.max(np.abs(G)) <= 1e-8 and np.allclose(a, 1.0)
     assert np.max(hist) <= 1e-9 * max(1.0, float(np.abs(W).max()))
+
+
+@pytest.mark.parametrize("name", ["tri2d", "box3d_prism", "box3d_tet"])
+@pytest.mark.parametrize("P", [2, 3])
+def test_partitioned_vcycles_match_oracle(name, P, monkeypatch):
+    """the third-order fine operator on P sub-domains (gmg_options.local_domains,
+    the partitioned path's layouts, halo plans and exchange points; ghosts'
+    W, slopes, polynomials and Dt by halo) against the oracle on the same
+    partition-constrained hierarchy."""
+    from paper_2509_06347_b200 import gmg
+    monkeypatch.setenv("GMG_P2P", "0")
+    m, fs = _cases()[name]
+    W, Winf, _, _ = _state(m, fs, 6)
+    part = gmg.gmg_partition_rcb(m.ctr, P)
+    s = _solver(m, n_levels=3, part=part, local_domains=P)
+    s.set_state(W, Winf)
+    hist = s.vcycle(3)
+    Wg = s.get_state(0)
+    Gg, ag = s.get_ho_state()
+    s.close()
+    H = oracle.build_hierarchy(m, 3, 0.5, part=part)
+    hs = {}
+    Wo, ho = oracle.vcycle(H, W, Winf, oracle.Options(fine_operator=1), 3, mesh=m, ho_state=hs)
+    assert _rel(Wg, Wo) <= TOL, _rel(Wg, Wo)
+    assert _rel(Gg, hs["G"]) <= TOL
+    assert _rel(ag, hs["alpha"]) <= TOL
+    assert np.max(np.abs(hist - ho) / ho[0][None, :]) <= TOL
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_partitioned_one_evaluation_matches_oracle(P):
+    from paper_2509_06347_b200 import gmg
+    m, fs = _cases()["box3d_prism"]
+    W, Winf, G, alpha = _state(m, fs, 7)
+    part = gmg.gmg_partition_rcb(m.ctr, P)
+    s = _solver(m, n_levels=1, part=part, local_domains=P)
+    s.set_state(W, Winf)
+    s.set_ho_state(G, alpha)
+    R, Gn, a, S = s.ho_residual()
+    poly, fl = s.ho_recon()
+    s.close()
+    Ro, Gno, ao, So, _, _ = cgks3.residual(cgks3.Mesh3(m), W, G, alpha, Winf)
+    po, flo, _ = cgks3.recon(cgks3.Mesh3(m), W, G, alpha, Winf)
+    assert np.array_equal(fl, flo)
+    assert _rel(poly, po) <= TOL
+    assert _rel(R, Ro) <= TOL and _rel(Gn, Gno) <= TOL and _rel(a, ao) <= TOL
