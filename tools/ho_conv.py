@@ -1,0 +1,39 @@
+"""NEXT-1 convergence probe: residual history of the third-order-operator
+V-cycle on config 2 (NACA0012, M 0.5, impulsive start) for a few settings of
+the readings the paper defers (C5 WENO epsilon / linear weights, C9 collision
+time).  One JSON line per setting: the density residual / r0 every 100 cycles."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2509_06347_b200 import gmg  # noqa: E402
+from synth import configs, state  # noqa: E402
+
+
+def main():
+    k = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
+    m = configs.config(k)
+    fs = configs.FREESTREAM[k] if k == 2 else (1.0, (0.5, 0.0), 1.0 / 1.4)
+    W, Winf = state.uniform(m, *fs), state.winf(*fs)
+    for kw in [dict(), dict(ho_eps=1e-6), dict(ho_gam0=1.0), dict(ho_c1=0.01), dict(ho_c1=0.2), dict(fine_operator=0)]:
+        kw2 = dict(kw)
+        fo = kw2.pop("fine_operator", 1)
+        s = gmg.Solver(m, n_levels=3, fine_operator=fo, **kw2)
+        s.set_state(W, Winf)
+        try:
+            h = s.vcycle(n)
+        except gmg.GmgError as e:
+            print(json.dumps({"config": k, "setting": kw, "error": str(e)[:80]}), flush=True)
+            s.close()
+            continue
+        r = h[:, 0] / h[0, 0]
+        print(json.dumps({"config": k, "setting": kw, "rho_res_every100": [float("%.3g" % x) for x in r[::100]],
+                          "min": float(r.min())}), flush=True)
+        s.close()
+
+
+if __name__ == "__main__":
+    main()
