@@ -75,123 +75,74 @@ __device__ __forceinline__ const double *umom(const Maxw<D, R> &g)
     else return g.Mu;
 }
 
-// <u^a v^b w^c psi>
+// T^{abc}_{qj} = <psi_q psi_j u^a v^b w^c>: the symmetric moment matrix of a
+// monomial weight, built once from products of 1D moments and then applied
+// to several micro-slope vectors (every contraction of Eqs. (dis1), (dis2),
+// (co) is o += f T^{abc} s).  H: u1 moments over the Maxwellian's half range.
 template <int D, int R, bool H, int a, int b, int c>
-__device__ __forceinline__ void psi_m(const Maxw<D, R> &g, double *o)
+__device__ __forceinline__ void tmat(const Maxw<D, R> &g, double (*T)[D + 2])
 {
     const double *Mu = umom<D, R, H>(g);
+    const double x1 = g.x1, x2 = g.x2;
     if constexpr (D == 3) {
-        const double wc = g.Mw[c];
-        const double base = Mu[a] * g.Mv[b] * wc;
-        o[0] = base;
-        o[1] = Mu[a + 1] * g.Mv[b] * wc;
-        o[2] = Mu[a] * g.Mv[b + 1] * wc;
-        o[3] = Mu[a] * g.Mv[b] * g.Mw[c + 1];
-        o[4] = 0.5 * (Mu[a + 2] * g.Mv[b] * wc + Mu[a] * g.Mv[b + 2] * wc + Mu[a] * g.Mv[b] * g.Mw[c + 2] + g.x1 * base);
+        auto P = [&](int i, int j, int k) { return Mu[i] * g.Mv[j] * g.Mw[k]; };
+        auto E = [&](int i, int j, int k) { return 0.5 * (P(i + 2, j, k) + P(i, j + 2, k) + P(i, j, k + 2) + x1 * P(i, j, k)); };
+        T[0][0] = P(a, b, c);
+        T[0][1] = P(a + 1, b, c);
+        T[0][2] = P(a, b + 1, c);
+        T[0][3] = P(a, b, c + 1);
+        T[0][4] = E(a, b, c);
+        T[1][1] = P(a + 2, b, c);
+        T[1][2] = P(a + 1, b + 1, c);
+        T[1][3] = P(a + 1, b, c + 1);
+        T[1][4] = E(a + 1, b, c);
+        T[2][2] = P(a, b + 2, c);
+        T[2][3] = P(a, b + 1, c + 1);
+        T[2][4] = E(a, b + 1, c);
+        T[3][3] = P(a, b, c + 2);
+        T[3][4] = E(a, b, c + 1);
+        const double s2 = P(a + 2, b, c) + P(a, b + 2, c) + P(a, b, c + 2);
+        T[4][4] = 0.25 * (P(a + 4, b, c) + P(a, b + 4, c) + P(a, b, c + 4) +
+                          2.0 * (P(a + 2, b + 2, c) + P(a + 2, b, c + 2) + P(a, b + 2, c + 2)) + 2.0 * x1 * s2 +
+                          x2 * P(a, b, c));
     } else {
-        const double base = Mu[a] * g.Mv[b];
-        o[0] = base;
-        o[1] = Mu[a + 1] * g.Mv[b];
-        o[2] = Mu[a] * g.Mv[b + 1];
-        o[3] = 0.5 * (Mu[a + 2] * g.Mv[b] + Mu[a] * g.Mv[b + 2] + g.x1 * base);
+        auto P = [&](int i, int j) { return Mu[i] * g.Mv[j]; };
+        auto E = [&](int i, int j) { return 0.5 * (P(i + 2, j) + P(i, j + 2) + x1 * P(i, j)); };
+        T[0][0] = P(a, b);
+        T[0][1] = P(a + 1, b);
+        T[0][2] = P(a, b + 1);
+        T[0][3] = E(a, b);
+        T[1][1] = P(a + 2, b);
+        T[1][2] = P(a + 1, b + 1);
+        T[1][3] = E(a + 1, b);
+        T[2][2] = P(a, b + 2);
+        T[2][3] = E(a, b + 1);
+        T[3][3] = 0.25 * (P(a + 4, b) + P(a, b + 4) + 2.0 * P(a + 2, b + 2) + 2.0 * x1 * (P(a + 2, b) + P(a, b + 2)) +
+                          x2 * P(a, b));
     }
+#pragma unroll
+    for (int q = 1; q < D + 2; ++q)
+#pragma unroll
+        for (int j = 0; j < q; ++j) T[q][j] = T[j][q];
 }
-// <xi^2 u^a v^b w^c psi>
-template <int D, int R, bool H, int a, int b, int c>
-__device__ __forceinline__ void psi_xi(const Maxw<D, R> &g, double *o)
+// o += f T s
+template <int D>
+__device__ __forceinline__ void tmv(const double (*T)[D + 2], const double *s, double f, double *o)
 {
-    const double *Mu = umom<D, R, H>(g);
-    if constexpr (D == 3) {
-        const double wc = g.Mw[c];
-        const double base = Mu[a] * g.Mv[b] * wc;
-        o[0] = g.x1 * base;
-        o[1] = g.x1 * Mu[a + 1] * g.Mv[b] * wc;
-        o[2] = g.x1 * Mu[a] * g.Mv[b + 1] * wc;
-        o[3] = g.x1 * Mu[a] * g.Mv[b] * g.Mw[c + 1];
-        o[4] = 0.5 * (g.x1 * (Mu[a + 2] * g.Mv[b] * wc + Mu[a] * g.Mv[b + 2] * wc + Mu[a] * g.Mv[b] * g.Mw[c + 2]) +
-                      g.x2 * base);
-    } else {
-        const double base = Mu[a] * g.Mv[b];
-        o[0] = g.x1 * base;
-        o[1] = g.x1 * Mu[a + 1] * g.Mv[b];
-        o[2] = g.x1 * Mu[a] * g.Mv[b + 1];
-        o[3] = 0.5 * (g.x1 * (Mu[a + 2] * g.Mv[b] + Mu[a] * g.Mv[b + 2]) + g.x2 * base);
+#pragma unroll
+    for (int q = 0; q < D + 2; ++q) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < D + 2; ++j) v += T[q][j] * s[j];
+        o[q] += f * v;
     }
-}
-// o += f * <(s . psi) u^a v^b w^c psi>
-template <int D, int R, bool H, int a, int b, int c>
-__device__ __forceinline__ void apsi_acc(const Maxw<D, R> &g, const double *s, double f, double *o)
-{
-    constexpr int NV = D + 2;
-    double t[NV];
-    psi_m<D, R, H, a, b, c>(g, t);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += (f * s[0]) * t[q];
-    psi_m<D, R, H, a + 1, b, c>(g, t);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += (f * s[1]) * t[q];
-    psi_m<D, R, H, a, b + 1, c>(g, t);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += (f * s[2]) * t[q];
-    if constexpr (D == 3) {
-        psi_m<D, R, H, a, b, c + 1>(g, t);
-#pragma unroll
-        for (int q = 0; q < NV; ++q) o[q] += (f * s[3]) * t[q];
-    }
-    const double h = 0.5 * f * s[D + 1];
-    double t2[NV];
-    psi_m<D, R, H, a + 2, b, c>(g, t);
-    psi_m<D, R, H, a, b + 2, c>(g, t2);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) t[q] += t2[q];
-    if constexpr (D == 3) {
-        psi_m<D, R, H, a, b, c + 2>(g, t2);
-#pragma unroll
-        for (int q = 0; q < NV; ++q) t[q] += t2[q];
-    }
-    psi_xi<D, R, H, a, b, c>(g, t2);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) o[q] += h * (t[q] + t2[q]);
-}
-// o += f * sum_e <u_e (s_e . psi) u^a psi>: direction e adds one power of u / v / w
-template <int D, int R, bool H, int a>
-__device__ __forceinline__ void adotu_acc(const Maxw<D, R> &g, const double (*s)[D + 2], double f, double *o)
-{
-    apsi_acc<D, R, H, a + 1, 0, 0>(g, s[0], f, o);
-    apsi_acc<D, R, H, a, 1, 0>(g, s[1], f, o);
-    if constexpr (D == 3) apsi_acc<D, R, H, a, 0, 1>(g, s[D - 1], f, o);
 }
 
-// moment matrix M_ab = <psi_a psi_b> (full range), factored without pivoting
-// (symmetric positive definite)
-template <int D, int R>
-__device__ __forceinline__ void mfactor(const Maxw<D, R> &g, double (*M)[D + 2])
+// in-place factorisation of the SPD moment matrix (no pivoting) and solve
+template <int D>
+__device__ __forceinline__ void mfactor(double (*M)[D + 2])
 {
     constexpr int NV = D + 2;
-    double c[NV];
-    psi_m<D, R, false, 0, 0, 0>(g, c);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) M[q][0] = c[q];
-    psi_m<D, R, false, 1, 0, 0>(g, c);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) M[q][1] = c[q];
-    psi_m<D, R, false, 0, 1, 0>(g, c);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) M[q][2] = c[q];
-    if constexpr (D == 3) {
-        psi_m<D, R, false, 0, 0, 1>(g, c);
-#pragma unroll
-        for (int q = 0; q < NV; ++q) M[q][3] = c[q];
-    }
-    {
-        double e[NV] = {};
-        e[D + 1] = 1.0;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) c[q] = 0.0;
-        apsi_acc<D, R, false, 0, 0, 0>(g, e, 1.0, c);
-#pragma unroll
-        for (int q = 0; q < NV; ++q) M[q][D + 1] = c[q];
-    }
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
         const double piv = 1.0 / M[k][k];
@@ -220,13 +171,15 @@ __device__ __forceinline__ void msolve(const double (*M)[D + 2], double *x)
     }
 }
 
-// micro slopes a_e = M^-1 dW_e / rho and A from <A + a.u> = 0 (Eq.(co))
+// micro slopes a_e = M^-1 dW_e / rho (M = T^{000}, full range) and A from
+// <A + a.u> = 0, i.e. M A = -sum_e T^{e_e} a_e (Eq.(co))
 template <int D, int R>
 __device__ __forceinline__ void slopes(const Maxw<D, R> &g, const double *dW, double (*a)[D + 2], double *A)
 {
     constexpr int NV = D + 2;
-    double M[NV][NV];
-    mfactor<D, R>(g, M);
+    double M[NV][NV], T[NV][NV];
+    tmat<D, R, false, 0, 0, 0>(g, M);
+    mfactor<D>(M);
     const double ir = 1.0 / g.rho;
 #pragma unroll
     for (int e = 0; e < D; ++e) {
@@ -236,7 +189,14 @@ __device__ __forceinline__ void slopes(const Maxw<D, R> &g, const double *dW, do
     }
 #pragma unroll
     for (int q = 0; q < NV; ++q) A[q] = 0.0;
-    adotu_acc<D, R, false, 0>(g, a, -1.0, A);
+    tmat<D, R, false, 1, 0, 0>(g, T);
+    tmv<D>(T, a[0], -1.0, A);
+    tmat<D, R, false, 0, 1, 0>(g, T);
+    tmv<D>(T, a[1], -1.0, A);
+    if constexpr (D == 3) {
+        tmat<D, R, false, 0, 0, 1>(g, T);
+        tmv<D>(T, a[2], -1.0, A);
+    }
     msolve<D>(M, A);
 }
 
@@ -276,28 +236,46 @@ __device__ __forceinline__ void side_pass(const double *w, const double *dw, con
     constexpr int NV = D + 2;
     Maxw<D, R> g;
     maxw<D, R>(w, gm1, K, g);
-    double a[D][NV], A[NV];
+    double a[D][NV], A[NV], M[NV][NV];
     slopes<D, R>(g, dw, a, A);
-    double t[NV];
-    psi_m<D, R, true, 0, 0, 0>(g, t);
+    const double rho = g.rho, fw = -rho * T.ex * (T.tau + T.dt);
+    // weight 1 (half range): <psi>, dW^c_e, -tau <A psi>
+    tmat<D, R, true, 0, 0, 0>(g, M);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) { Wc[q] += g.rho * t[q]; Wt[q] += (g.rho * T.ex) * t[q]; }
+    for (int q = 0; q < NV; ++q) { Wc[q] += rho * M[q][0]; Wt[q] += (rho * T.ex) * M[q][0]; }
 #pragma unroll
     for (int e = 0; e < D; ++e) {
         double u[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) u[q] = 0.0;
-        apsi_acc<D, R, true, 0, 0, 0>(g, a[e], g.rho, u);
+        tmv<D>(M, a[e], rho, u);
 #pragma unroll
         for (int q = 0; q < NV; ++q) dWc[(e * NV + q) * blockDim.x] += u[q];
     }
-    psi_m<D, R, true, 1, 0, 0>(g, t);
+    tmv<D>(M, A, -rho * T.ex * T.tau, Wt);
+    // weight u1: <u1 psi> (flux), a_0 (state), A (flux)
+    tmat<D, R, true, 1, 0, 0>(g, M);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) F[q] += (g.rho * T.q4) * t[q];
-    adotu_acc<D, R, true, 1>(g, a, -g.rho * (T.tau * T.q4 + T.q5), F);
-    apsi_acc<D, R, true, 1, 0, 0>(g, A, -g.rho * T.tau * T.q4, F);
-    adotu_acc<D, R, true, 0>(g, a, -g.rho * T.ex * (T.tau + T.dt), Wt);
-    apsi_acc<D, R, true, 0, 0, 0>(g, A, -g.rho * T.ex * T.tau, Wt);
+    for (int q = 0; q < NV; ++q) F[q] += (rho * T.q4) * M[q][0];
+    tmv<D>(M, a[0], fw, Wt);
+    tmv<D>(M, A, -rho * T.tau * T.q4, F);
+    // weights u2, u3: a_1, a_2 (state)
+    tmat<D, R, true, 0, 1, 0>(g, M);
+    tmv<D>(M, a[1], fw, Wt);
+    if constexpr (D == 3) {
+        tmat<D, R, true, 0, 0, 1>(g, M);
+        tmv<D>(M, a[2], fw, Wt);
+    }
+    // weights u1 u_e: a_e (flux)
+    const double ff = -rho * (T.tau * T.q4 + T.q5);
+    tmat<D, R, true, 2, 0, 0>(g, M);
+    tmv<D>(M, a[0], ff, F);
+    tmat<D, R, true, 1, 1, 0>(g, M);
+    tmv<D>(M, a[1], ff, F);
+    if constexpr (D == 3) {
+        tmat<D, R, true, 1, 0, 1>(g, M);
+        tmv<D>(M, a[2], ff, F);
+    }
 }
 
 // equilibrium part (Eq.(dis2)): C1 g^c + C2 a^c.u g^c + C3 A^c g^c
@@ -308,19 +286,32 @@ __device__ __forceinline__ void equilibrium_pass(const double *Wc, const double 
     constexpr int NV = D + 2;
     Maxw<D, 0> g;
     maxw<D, 0>(Wc, gm1, K, g);
-    double a[D][NV], A[NV];
+    double a[D][NV], A[NV], M[NV][NV];
     slopes<D, 0>(g, dWc, a, A);
-    double t[NV];
-    psi_m<D, 0, false, 1, 0, 0>(g, t);
+    const double rho = g.rho;
+    tmat<D, 0, false, 0, 0, 0>(g, M);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) F[q] += (g.rho * T.q1) * t[q];
-    adotu_acc<D, 0, false, 1>(g, a, g.rho * T.q2, F);
-    apsi_acc<D, 0, false, 1, 0, 0>(g, A, g.rho * T.q3, F);
-    psi_m<D, 0, false, 0, 0, 0>(g, t);
+    for (int q = 0; q < NV; ++q) Wt[q] += (rho * T.c1) * M[q][0];
+    tmv<D>(M, A, rho * T.c3, Wt);
+    tmat<D, 0, false, 1, 0, 0>(g, M);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) Wt[q] += (g.rho * T.c1) * t[q];
-    adotu_acc<D, 0, false, 0>(g, a, g.rho * T.c2, Wt);
-    apsi_acc<D, 0, false, 0, 0, 0>(g, A, g.rho * T.c3, Wt);
+    for (int q = 0; q < NV; ++q) F[q] += (rho * T.q1) * M[q][0];
+    tmv<D>(M, A, rho * T.q3, F);
+    tmv<D>(M, a[0], rho * T.c2, Wt);
+    tmat<D, 0, false, 0, 1, 0>(g, M);
+    tmv<D>(M, a[1], rho * T.c2, Wt);
+    if constexpr (D == 3) {
+        tmat<D, 0, false, 0, 0, 1>(g, M);
+        tmv<D>(M, a[2], rho * T.c2, Wt);
+    }
+    tmat<D, 0, false, 2, 0, 0>(g, M);
+    tmv<D>(M, a[0], rho * T.q2, F);
+    tmat<D, 0, false, 1, 1, 0>(g, M);
+    tmv<D>(M, a[1], rho * T.q2, F);
+    if constexpr (D == 3) {
+        tmat<D, 0, false, 1, 0, 1>(g, M);
+        tmv<D>(M, a[2], rho * T.q2, F);
+    }
 }
 
 // face frame (C10a): e0 = n; 3D e1 = normalise(n x x_k), x_k the axis of the
