@@ -185,6 +185,15 @@ def _worker(rank, world, port, name, q):
             n_own = {r: len(allp[r]["owned"]) for r in range(world)}
             ok &= _check_targets(mine["owned"], off, k, g, mine["peers"], ghost_of, n_own)
         s.close()
+        # NEXT-1 host setup on this rank's domain (owned + ghost geometry, slots, p2 operators): the
+        # workspace sizing runs it; it must succeed on every rank and add to the first-order workspace
+        s0 = gmg.Solver(m, n_levels=3, build_only=True, part=part, nranks=world, rank=rank, nccl_id=bytes(128))
+        s1 = gmg.Solver(m, n_levels=3, build_only=True, part=part, nranks=world, rank=rank, nccl_id=bytes(128),
+                        fine_operator=1)
+        b0, b1 = gmg.gmg_workspace_bytes(s0.ctx), gmg.gmg_workspace_bytes(s1.ctx)
+        ok &= b0 > 0 and b1 > b0
+        s0.close()
+        s1.close()
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
