@@ -1,7 +1,9 @@
 """NEXT-1 convergence probe: residual history of the third-order-operator
 V-cycle on config 2 (NACA0012, M 0.5, impulsive start) for a few settings of
 the readings the paper defers (C5 WENO epsilon / linear weights, C9 collision
-time).  One JSON line per setting: the density residual / r0 every 100 cycles."""
+time).  One JSON line per setting: the density residual / r0 every 100 cycles.
+
+    python tools/ho_conv.py [config] [cycles] [p1|cfl]"""
 import json
 import os
 import sys
@@ -18,7 +20,14 @@ def main():
     m = configs.config(k)
     fs = configs.FREESTREAM[k] if k == 2 else (1.0, (0.5, 0.0), 1.0 / 1.4)
     W, Winf = state.uniform(m, *fs), state.winf(*fs)
-    for kw in [dict(), dict(ho_eps=1e-6), dict(ho_gam0=1.0), dict(ho_c1=0.01), dict(ho_c1=0.2), dict(fine_operator=0)]:
+    sets = [dict(), dict(ho_eps=1e-6), dict(ho_gam0=1.0), dict(ho_c1=0.01), dict(ho_c1=0.2), dict(fine_operator=0)]
+    mode = sys.argv[3] if len(sys.argv) > 3 else ""
+    if mode == "p1":       # Green-Gauss only (gamma_0 -> 0) and intermediate linear weights
+        sets = [dict(ho_gam0=1e-12), dict(ho_gam0=0.5), dict(ho_gam0=0.8)]
+    elif mode == "cfl":    # explicit CFL of the fine pre-smoother
+        sets = [dict(cfl_exp=0.2), dict(cfl_exp=0.1), dict(cfl_exp=0.2, ho_gam0=1.0), dict(cfl_exp=0.1, ho_gam0=1.0),
+                dict(cfl_exp=0.2, ho_eps=1e-6)]
+    for kw in sets:
         kw2 = dict(kw)
         fo = kw2.pop("fine_operator", 1)
         s = gmg.Solver(m, n_levels=3, fine_operator=fo, **kw2)
