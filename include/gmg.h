@@ -218,6 +218,26 @@ gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_
 gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, double *ms, double *cell_updates,
                            double *bytes);
 
+/* Pipelined host I/O (single rank): the same operations as gmg_set_state /
+ * gmg_vcycle / gmg_get_state, enqueued without host synchronisation so that
+ * the host<->device copies of consecutive calls overlap the V-cycles of the
+ * others.  Copies run on two library-owned copy streams (one per direction)
+ * through two device staging buffers per direction; the compute stream
+ * orders everything else.
+ *   gmg_set_state_async: W[nv][n] natural order; the host buffer (pinned for
+ *     real overlap) must stay valid and unmodified until gmg_sync.
+ *   gmg_vcycle_async: n_cycles V-cycles + the residual norm (history kept on
+ *     the device; no host read).
+ *   gmg_get_state_async: W_out[nv][n] natural order, written by gmg_sync.
+ *   gmg_sync: waits for everything enqueued; GMG_ENONFINITE if any cycle
+ *     since the last sync produced a non-finite residual.
+ * Results are bit-identical to the synchronous calls in the same order.
+ * GMG_EINVAL for nranks > 1 (the synchronous calls serve ranks). */
+gmg_status gmg_set_state_async(gmg_ctx *ctx, const double *W, const double *W_inf);
+gmg_status gmg_vcycle_async(gmg_ctx *ctx, int n_cycles);
+gmg_status gmg_get_state_async(gmg_ctx *ctx, double *W_out);
+gmg_status gmg_sync(gmg_ctx *ctx);
+
 /* Number of kernels one V-cycle launches (graph nodes). */
 int64_t gmg_vcycle_launches(gmg_ctx *ctx);
 

@@ -1006,6 +1006,10 @@ void carve(gmg_ctx *ctx, Bump &b)
     // polynomials (nv (1 + d + d(d+1)/2)) of gmg_set/get_ho_state, gmg_ho_residual, gmg_ho_recon
     const int stage_comp = ctx->ho ? nv * (1 + d + d * (d + 1) / 2) : nv;
     ctx->d_stage = b.take<double>((size_t)stage_comp * nmax);
+    for (int k = 0; k < 2; ++k) {               // pipelined host I/O staging (fine level, natural order)
+        ctx->stage_in[k] = b.take<double>((size_t)nv * ctx->lv[0].n);
+        ctx->stage_out[k] = b.take<double>((size_t)nv * ctx->lv[0].n);
+    }
     ctx->hist_cap = 4096;
     ctx->d_hist = b.take<double>((size_t)ctx->hist_cap * nv);
     ctx->d_flag = b.take<int>(4);
@@ -1516,6 +1520,18 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             }
         ctx->p2p_ready = true;
     }
+    if (!ctx->copy) {                      // copy stream + events of the pipelined host I/O
+        CK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaEventCreateWithFlags(&ctx->ev_in_ready[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_in_free[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_out_ready[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_out_free[k], cudaEventDisableTiming));
+            CK(cudaEventRecord(ctx->ev_in_free[k], ctx->stream));
+            CK(cudaEventRecord(ctx->ev_out_free[k], ctx->copy_out));
+        }
+    }
     if (ctx->nparts > 1 && !ctx->side) {   // side stream + events of the exchange overlap
         CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
@@ -1895,6 +1911,105 @@ gmg_status gmg_vcycle(gmg_ctx *ctx, int n_cycles, double *res_hist)
     return finish_history(ctx, n_cycles, res_hist);
 }
 
+// ---------------------------------------------------------------- pipelined host I/O
+static gmg_status async_ready(gmg_ctx *ctx, bool need_state)
+{
+    gmg_status st = check_ready(ctx, need_state);
+    if (st) return st;
+    if (ctx->opt.nranks > 1) { ctx->err = "pipelined host I/O is single-rank"; return GMG_EINVAL; }
+    if (!ctx->async_flag_reset) {
+        CK(cudaMemsetAsync(ctx->d_flag, 0, 3 * sizeof(int), ctx->stream));
+        ctx->async_flag_reset = true;
+    }
+    return GMG_OK;
+}
+
+gmg_status gmg_set_state_async(gmg_ctx *ctx, const double *W, const double *W_inf)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = async_ready(ctx, false);
+    if (st) return st;
+    if (!W || !W_inf) { ctx->err = "null state"; return GMG_EINVAL; }
+    const int nv = ctx->opt.dim + 2;
+    bool same = true;
+    for (int q = 0; q < nv; ++q) {
+        same = same && std::memcmp(&ctx->winf[q], &W_inf[q], sizeof(double)) == 0;
+        ctx->winf[q] = W_inf[q];
+    }
+    if (ctx->graph && !same) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+    const int k = ctx->in_slot;
+    const int64_t N = ctx->lv[0].n;
+    // copy stream: wait until the compute stream has consumed this slot, then H2D
+    CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_in_free[k], 0));
+    CK(cudaMemcpyAsync(ctx->stage_in[k], W, sizeof(double) * nv * N, cudaMemcpyDefault, ctx->copy));
+    CK(cudaEventRecord(ctx->ev_in_ready[k], ctx->copy));
+    // compute stream: scatter into every domain's local state (owned + ghosts)
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in_ready[k], 0));
+    for (Domain &dm : ctx->dom) {
+        DevLevel &L = dm.dv[0];
+        k_to_internal<<<nblk(L.n_loc), 256, 0, ctx->stream>>>(L.n_loc, (int)N, nv, L.perm, ctx->stage_in[k], L.W, nv, 0);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev_in_free[k], ctx->stream));
+    ctx->in_slot ^= 1;
+    ctx->state_set = true;
+    return GMG_OK;
+}
+
+gmg_status gmg_vcycle_async(gmg_ctx *ctx, int n_cycles)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = async_ready(ctx, true);
+    if (st) return st;
+    if (n_cycles < 0) { ctx->err = "n_cycles out of range"; return GMG_EINVAL; }
+    if (!ctx->graph) { st = build_graph(ctx); if (st) return st; }
+    for (int k = 0; k < n_cycles; ++k) CK(cudaGraphLaunch(ctx->graph, ctx->stream));
+    Launcher Lc{ctx, ctx->stream};
+    if (ctx->opt.dim == 2) enqueue_final_norm<2>(Lc);
+    else enqueue_final_norm<3>(Lc);
+    CK(cudaGetLastError());
+    return GMG_OK;
+}
+
+gmg_status gmg_get_state_async(gmg_ctx *ctx, double *W_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = async_ready(ctx, false);
+    if (st) return st;
+    if (!W_out) { ctx->err = "null output"; return GMG_EINVAL; }
+    const int nv = ctx->opt.dim + 2;
+    const int k = ctx->out_slot;
+    const int64_t N = ctx->lv[0].n;
+    // compute stream: wait until the previous D2H of this slot has drained, gather to natural order
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_out_free[k], 0));
+    for (Domain &dm : ctx->dom) {
+        DevLevel &L = dm.dv[0];
+        k_to_natural<<<nblk(L.n), 256, 0, ctx->stream>>>(L.n, (int)N, nv, L.perm, L.W, ctx->stage_out[k], nv, 0);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev_out_ready[k], ctx->stream));
+    // result copy stream (its own FIFO, so the next input copy never queues behind it): D2H once gathered
+    CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_out_ready[k], 0));
+    CK(cudaMemcpyAsync(W_out, ctx->stage_out[k], sizeof(double) * nv * N, cudaMemcpyDefault, ctx->copy_out));
+    CK(cudaEventRecord(ctx->ev_out_free[k], ctx->copy_out));
+    ctx->out_slot ^= 1;
+    return GMG_OK;
+}
+
+gmg_status gmg_sync(gmg_ctx *ctx)
+{
+    if (!ctx) return GMG_EINVAL;
+    if (!ctx->ws_ready) { ctx->err = "workspace not set"; return GMG_ESTATE; }
+    int flags[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(flags, ctx->d_flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->copy));
+    CK(cudaStreamSynchronize(ctx->copy_out));
+    ctx->async_flag_reset = false;
+    if (flags[1]) { ctx->err = "non-finite residual (level 0)"; return GMG_ENONFINITE; }
+    return GMG_OK;
+}
+
 gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_t *count_out, double *bytes_out)
 {
     if (!ctx) return GMG_EINVAL;
@@ -2209,6 +2324,18 @@ void gmg_destroy(gmg_ctx *ctx)
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->copy) {
+        cudaStreamSynchronize(ctx->copy);
+        cudaStreamSynchronize(ctx->copy_out);
+        cudaStreamDestroy(ctx->copy);
+        cudaStreamDestroy(ctx->copy_out);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(ctx->ev_in_ready[k]);
+            cudaEventDestroy(ctx->ev_in_free[k]);
+            cudaEventDestroy(ctx->ev_out_ready[k]);
+            cudaEventDestroy(ctx->ev_out_free[k]);
+        }
+    }
     if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy((ncclComm_t)ctx->nccl_comm);
     for (void *p : ctx->p2p_opened) cudaIpcCloseMemHandle(p);
     delete ctx->ho;

@@ -260,6 +260,12 @@ struct gmg_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     gmg::HoHost *ho = nullptr;        // NEXT-1 geometry + setup (gmg_load_ho_geometry)
+    // pipelined host I/O (gmg_*_async): copy stream, double-buffered staging, events
+    cudaStream_t copy = nullptr, copy_out = nullptr;   // host->device / device->host copy streams
+    double *stage_in[2] = {nullptr, nullptr}, *stage_out[2] = {nullptr, nullptr};   // [nv][N0] natural order
+    cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
+    int in_slot = 0, out_slot = 0;
+    bool async_flag_reset = false;    // d_flag cleared for the current async epoch
 };
 
 namespace gmg {
