@@ -238,6 +238,13 @@ gmg_status gmg_vcycle_async(gmg_ctx *ctx, int n_cycles);
 gmg_status gmg_get_state_async(gmg_ctx *ctx, double *W_out);
 gmg_status gmg_sync(gmg_ctx *ctx);
 
+/* Rank-local variants (any nranks, one domain per rank): W_owned[nv][n_own]
+ * holds only this rank's owned fine cells, column p = owned cell p in the
+ * order gmg_get_halo(level 0) lists them ("owned"); ghosts are refreshed by
+ * the V-cycle's own halo exchange.  Same buffer-lifetime rules as above. */
+gmg_status gmg_set_state_owned_async(gmg_ctx *ctx, const double *W_owned, const double *W_inf);
+gmg_status gmg_get_state_owned_async(gmg_ctx *ctx, double *W_owned_out);
+
 /* Number of kernels one V-cycle launches (graph nodes). */
 int64_t gmg_vcycle_launches(gmg_ctx *ctx);
 

@@ -1912,11 +1912,12 @@ gmg_status gmg_vcycle(gmg_ctx *ctx, int n_cycles, double *res_hist)
 }
 
 // ---------------------------------------------------------------- pipelined host I/O
-static gmg_status async_ready(gmg_ctx *ctx, bool need_state)
+static gmg_status async_ready(gmg_ctx *ctx, bool need_state, bool natural = true)
 {
     gmg_status st = check_ready(ctx, need_state);
     if (st) return st;
-    if (ctx->opt.nranks > 1) { ctx->err = "pipelined host I/O is single-rank"; return GMG_EINVAL; }
+    if (natural && ctx->opt.nranks > 1) { ctx->err = "natural-order pipelined host I/O is single-rank (use *_owned_async)"; return GMG_EINVAL; }
+    if (!natural && ctx->dom.size() != 1) { ctx->err = "owned-layout host I/O needs one domain per process"; return GMG_EINVAL; }
     if (!ctx->async_flag_reset) {
         CK(cudaMemsetAsync(ctx->d_flag, 0, 3 * sizeof(int), ctx->stream));
         ctx->async_flag_reset = true;
@@ -1959,7 +1960,7 @@ gmg_status gmg_set_state_async(gmg_ctx *ctx, const double *W, const double *W_in
 gmg_status gmg_vcycle_async(gmg_ctx *ctx, int n_cycles)
 {
     if (!ctx) return GMG_EINVAL;
-    gmg_status st = async_ready(ctx, true);
+    gmg_status st = async_ready(ctx, true, ctx->opt.nranks == 1);
     if (st) return st;
     if (n_cycles < 0) { ctx->err = "n_cycles out of range"; return GMG_EINVAL; }
     if (!ctx->graph) { st = build_graph(ctx); if (st) return st; }
@@ -1991,6 +1992,58 @@ gmg_status gmg_get_state_async(gmg_ctx *ctx, double *W_out)
     // result copy stream (its own FIFO, so the next input copy never queues behind it): D2H once gathered
     CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_out_ready[k], 0));
     CK(cudaMemcpyAsync(W_out, ctx->stage_out[k], sizeof(double) * nv * N, cudaMemcpyDefault, ctx->copy_out));
+    CK(cudaEventRecord(ctx->ev_out_free[k], ctx->copy_out));
+    ctx->out_slot ^= 1;
+    return GMG_OK;
+}
+
+static bool winf_update(gmg_ctx *ctx, const double *W_inf)
+{
+    const int nv = ctx->opt.dim + 2;
+    bool same = true;
+    for (int q = 0; q < nv; ++q) {
+        same = same && std::memcmp(&ctx->winf[q], &W_inf[q], sizeof(double)) == 0;
+        ctx->winf[q] = W_inf[q];
+    }
+    if (ctx->graph && !same) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
+    return same;
+}
+
+gmg_status gmg_set_state_owned_async(gmg_ctx *ctx, const double *W_owned, const double *W_inf)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = async_ready(ctx, false, false);
+    if (st) return st;
+    if (!W_owned || !W_inf) { ctx->err = "null state"; return GMG_EINVAL; }
+    winf_update(ctx, W_inf);
+    const int nv = ctx->opt.dim + 2, k = ctx->in_slot;
+    DevLevel &L = ctx->dom[0].dv[0];
+    CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_in_free[k], 0));
+    CK(cudaMemcpyAsync(ctx->stage_in[k], W_owned, sizeof(double) * nv * L.n, cudaMemcpyDefault, ctx->copy));
+    CK(cudaEventRecord(ctx->ev_in_ready[k], ctx->copy));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in_ready[k], 0));
+    k_soa_to_aos<<<nblk(L.n), 256, 0, ctx->stream>>>(L.n, nv, ctx->stage_in[k], L.W);   // ghosts: V-cycle halo
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev_in_free[k], ctx->stream));
+    ctx->in_slot ^= 1;
+    ctx->state_set = true;
+    return GMG_OK;
+}
+
+gmg_status gmg_get_state_owned_async(gmg_ctx *ctx, double *W_owned_out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = async_ready(ctx, false, false);
+    if (st) return st;
+    if (!W_owned_out) { ctx->err = "null output"; return GMG_EINVAL; }
+    const int nv = ctx->opt.dim + 2, k = ctx->out_slot;
+    DevLevel &L = ctx->dom[0].dv[0];
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_out_free[k], 0));
+    k_aos_to_soa<<<nblk(L.n), 256, 0, ctx->stream>>>(L.n, nv, L.W, ctx->stage_out[k]);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev_out_ready[k], ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_out_ready[k], 0));
+    CK(cudaMemcpyAsync(W_owned_out, ctx->stage_out[k], sizeof(double) * nv * L.n, cudaMemcpyDefault, ctx->copy_out));
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->copy_out));
     ctx->out_slot ^= 1;
     return GMG_OK;

@@ -743,6 +743,19 @@ __global__ void k_to_natural(int n, int N, int ncomp, const int *__restrict__ pe
     const int nat = perm[i];
     for (int q = 0; q < ncomp; ++q) dst[(size_t)q * N + nat] = src[(size_t)i * stride + offset + q];
 }
+// owned-compact [ncomp][n] (SoA, local owned order) <-> AoS [n][ncomp]
+__global__ void k_soa_to_aos(int n, int ncomp, const double *__restrict__ src, double *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int q = 0; q < ncomp; ++q) dst[(size_t)i * ncomp + q] = src[(size_t)q * n + i];
+}
+__global__ void k_aos_to_soa(int n, int ncomp, const double *__restrict__ src, double *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int q = 0; q < ncomp; ++q) dst[(size_t)q * n + i] = src[(size_t)i * ncomp + q];
+}
 __global__ void k_fill(int n, double *p, double v)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;

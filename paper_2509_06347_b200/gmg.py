@@ -25,7 +25,7 @@ K_FACE, K_GATHER, K_SWEEP, K_RESTRICT, K_PROLONG, K_NORM, K_HO_RECON, K_HO_FLUX,
 K_NAMES = ["face", "gather", "sweep", "restrict", "prolong", "norm", "ho_recon", "ho_flux"]
 
 # every symbol include/gmg.h declares
-ABI_SYMBOLS = ["gmg_set_state_async", "gmg_vcycle_async", "gmg_get_state_async", "gmg_sync",
+ABI_SYMBOLS = ["gmg_set_state_owned_async", "gmg_get_state_owned_async", "gmg_set_state_async", "gmg_vcycle_async", "gmg_get_state_async", "gmg_sync",
                "gmg_load_ho_geometry", "gmg_set_ho_state", "gmg_get_ho_state", "gmg_ho_residual", "gmg_ho_recon",
                "gmg_default_options", "gmg_create", "gmg_load_mesh", "gmg_set_coloring", "gmg_build_hierarchy",
                "gmg_get_level_info", "gmg_get_maps", "gmg_get_level_geometry", "gmg_workspace_bytes",
@@ -91,6 +91,8 @@ def lib():
             "gmg_p2p_import": (I, [P, P, P, P]),
             "gmg_get_p2p_targets": (I, [P, I, I, P, P, P, P]),
             "gmg_p2p_emulate_smooth": (I, [P, I, I, P]),
+            "gmg_set_state_owned_async": (I, [P, P, P]),
+            "gmg_get_state_owned_async": (I, [P, P]),
             "gmg_set_state_async": (I, [P, P, P]),
             "gmg_vcycle_async": (I, [P, I]),
             "gmg_get_state_async": (I, [P, P]),
@@ -325,6 +327,16 @@ def gmg_set_state_async(ctx, W, W_inf):
     """W: pinned host tensor / device tensor / array that stays alive until gmg_sync"""
     Wi = _f64(W_inf)
     _check(ctx, lib().gmg_set_state_async(ctx, _ptr(W), _ptr(Wi)))
+
+
+def gmg_set_state_owned_async(ctx, W_owned, W_inf):
+    """W_owned[nv][n_own]: this rank's owned cells in gmg_get_halo(level 0) "owned" order"""
+    Wi = _f64(W_inf)
+    _check(ctx, lib().gmg_set_state_owned_async(ctx, _ptr(W_owned), _ptr(Wi)))
+
+
+def gmg_get_state_owned_async(ctx, W_owned_out):
+    _check(ctx, lib().gmg_get_state_owned_async(ctx, _ptr(W_owned_out)))
 
 
 def gmg_vcycle_async(ctx, n_cycles):
