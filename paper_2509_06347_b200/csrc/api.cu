@@ -339,7 +339,7 @@ void enqueue_ghost_w(Launcher &Lc, int l)
 
 template <class K>
 void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArgs &a, const void *win, size_t win_bytes,
-                        bool pdl)
+                        bool pdl, float hit = 1.0f)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = g;
@@ -351,7 +351,7 @@ void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArg
         at[na].id = cudaLaunchAttributeAccessPolicyWindow;
         at[na].val.accessPolicyWindow.base_ptr = const_cast<void *>(win);
         at[na].val.accessPolicyWindow.num_bytes = win_bytes;
-        at[na].val.accessPolicyWindow.hitRatio = 1.0f;
+        at[na].val.accessPolicyWindow.hitRatio = hit;
         at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         ++na;
@@ -371,11 +371,13 @@ void launch_sweep(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, const 
 {
     const int minb = ctx->minb, sweep_var = ctx->sweep_var;
     const bool pdl = ctx->pdl != 0;
+    // a window larger than the set-aside persists that fraction of its lines (GMG_L2FULL)
+    const float hit = (ctx->l2_window && win_bytes > ctx->l2_window) ? (float)((double)ctx->l2_window / (double)win_bytes) : 1.0f;
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
     if (ctx->sweep_bs == 128 && sweep_var == 3 && minb == 4) {   // default; the variants run at 256
         int nb = (int)((nthreads + 127) / 128);
         if (ctx->sweep_grid_cap > 0) nb = std::min(nb, 2 * ctx->sweep_grid_cap);
-        launch_with_window(k_sweep128<D, LPC>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl);
+        launch_with_window(k_sweep128<D, LPC>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
         return;
     }
     int nb = nblk(nthreads);
@@ -457,7 +459,8 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
         return;
     }
     const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
-    const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * kRecStride * sizeof(double)) : 0;
+    const size_t rec_bytes = (size_t)L.n_loc * kRecStride * sizeof(double);
+    const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_full ? ctx->l2_maxw : ctx->l2_window, rec_bytes) : 0;
     // small color blocks are latency bound (one partial wave, each lane walks
     // its slots one dependent gather after the other): spread the slots over
     // more lanes while the whole block still fits in one resident wave
@@ -1553,6 +1556,8 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             const size_t setaside = std::min<size_t>((size_t)maxp, want);
             CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside));
             ctx->l2_window = std::min<size_t>((size_t)maxw, setaside);
+            ctx->l2_maxw = (size_t)maxw;
+            if (const char *f = std::getenv("GMG_L2FULL")) ctx->l2_full = std::atoi(f);
         }
     }
     {   // sweep grid: whole resident waves only (grid-stride kernel), GMG_SWEEP_WAVES (0 = uncapped)

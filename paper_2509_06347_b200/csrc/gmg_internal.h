@@ -250,6 +250,8 @@ struct gmg_ctx {
     int flow_grid = 0;                // resident CTAs of k_sweep_flow (set with the workspace)
     int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
+    size_t l2_maxw = 0;               // device max access-policy window bytes
+    int l2_full = 0;                  // window over all records with hitRatio = set-aside / bytes (GMG_L2FULL)
     int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (no measured gain)
     int wsweep = 0;                   // warp-staged sweep: warps per block (0 = register-gather sweep)
     int spsweep = 0;                  // slot-parallel sweep (thread per slot + block segmented reduction)
