@@ -1179,7 +1179,9 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     ctx->nparts = std::max(opt->nranks, opt->local_domains);
     if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
     if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
-    if (const char *e = std::getenv("GMG_PDL")) ctx->pdl = std::atoi(e);   // programmatic dependent launch
+    // programmatic dependent launch between the V-cycle kernels (every kernel launched with the attribute
+    // waits in pdl_enter() before touching its predecessor's outputs): measured neutral, off by default
+    if (const char *e = std::getenv("GMG_PDL")) ctx->pdl = std::atoi(e);
     if (const char *e = std::getenv("GMG_WSWEEP")) ctx->wsweep = std::atoi(e);   // warp-staged sweep
     if (const char *e = std::getenv("GMG_SPSWEEP")) ctx->spsweep = std::atoi(e); // slot-parallel sweep
     if (const char *e = std::getenv("GMG_TAIL")) ctx->tail_cells = std::atoi(e);  // tiny-color fusion threshold

@@ -607,6 +607,7 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 template <int D, int LPC>
 __global__ void __launch_bounds__(128, 8) k_sweep128(SweepArgs a)
 {
+    pdl_enter();
     sweep_body<D, LPC, 3, false>(a, P2PArgs{});
 }
 
