@@ -55,6 +55,8 @@ struct GArgs {
 // launched while its predecessor drains; it waits here until the predecessor
 // grid has completed and its writes are visible, and immediately lets its
 // own successor be scheduled.  No-ops when launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_enter()
 {
     asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -252,7 +252,7 @@ struct gmg_ctx {
     size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
     size_t l2_maxw = 0;               // device max access-policy window bytes
     int l2_full = 0;                  // window over all records with hitRatio = set-aside / bytes (GMG_L2FULL)
-    int pdl = 0;                      // programmatic dependent launch between V-cycle kernels (GMG_PDL; measured neutral)
+    int pdl = 1;                      // programmatic dependent launch between V-cycle kernels (GMG_PDL, default on)
     int wsweep = 0;                   // warp-staged sweep: warps per block (0 = register-gather sweep)
     int spsweep = 0;                  // slot-parallel sweep (thread per slot + block segmented reduction)
     int tail_cells = 0;               // fuse runs of consecutive color phases with <= this many cells (0 = off; neutral)

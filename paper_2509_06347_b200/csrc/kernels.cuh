@@ -557,7 +557,24 @@ __device__ __forceinline__ void sweep_body(const SweepArgs &a, const P2PArgs &p)
             }
         }
         const int e0 = sd.x, e1 = sd.x + sd.y;
-        if constexpr ((VAR & 2) != 0) {
+        if constexpr ((VAR & 8) != 0) {
+            // PDL prologue: the slot indices are static during a smoothing step, so the cell's slot range
+            // and first neighbour index are loaded before griddepcontrol.wait -- they overlap the previous
+            // phase's tail; slot records and neighbour records (previous phases' increments) after it
+            int e = e0 + sub;
+            int j = e < e1 ? __ldg(a.sJe + e) : 0;
+            if (r == 0) pdl_wait();
+            for (; e < e1; e += LPC) {
+                const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
+                if (j >= a.zlo && j < a.zhi) { j = jn; continue; }
+                double sr[4];
+                ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                double w[NV], dw[NV];
+                ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
+                flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                j = jn;
+            }
+        } else if constexpr ((VAR & 2) != 0) {
             int e = e0 + sub;
             int j = e < e1 ? __ldg(a.sJe + e) : 0;
             for (; e < e1; e += LPC) {
@@ -594,6 +611,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs &a, const P2PArgs &p)
         else sweep_finish<D>(a, i, acc);
     }
     }
+    if constexpr ((VAR & 8) != 0) pdl_wait();   // threads without a cell: nothing may run past the predecessor
 }
 
 template <int D, int LPC, int MINB, int VAR = 3>
@@ -607,8 +625,8 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 template <int D, int LPC>
 __global__ void __launch_bounds__(128, 8) k_sweep128(SweepArgs a)
 {
-    pdl_enter();
-    sweep_body<D, LPC, 3, false>(a, P2PArgs{});
+    pdl_launch_dependents();                       // the next phase may start its static prologue now
+    sweep_body<D, LPC, 3 | 8, false>(a, P2PArgs{});
 }
 
 __device__ __forceinline__ int ld_acquire_sys(const int *p)
