@@ -60,14 +60,16 @@ template <int D> struct FR { static constexpr int SR = D + 2, AM = D + 3; };
 template <int D, bool FLUX, int STRIDE, bool DF, bool PREP>
 __global__ void __launch_bounds__(256, DF ? 3 : 4) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
 {
-    pdl_enter();
+    pdl_launch_dependents();
     constexpr int NV = D + 2;
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= L.nf) return;
+    if (f >= L.nf) { pdl_wait(); return; }
+    // static face data before the PDL wait (overlaps the predecessor's tail), states after it
     const int l = __ldg(L.fl + f), r = __ldg(L.fr + f);
     double A[D], S2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) { A[k] = __ldg(L.fA + (size_t)k * L.nf + f); S2 += A[k] * A[k]; }
+    pdl_wait();
     const double iS = rsqrt(S2), S = S2 * iS;
     double n[D];
 #pragma unroll
@@ -144,16 +146,19 @@ __global__ void __launch_bounds__(256, DF ? 3 : 4) k_face(DevLevel L, const doub
 template <int D>
 __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 {
-    pdl_enter();
+    pdl_launch_dependents();
     constexpr int NV = D + 2;
     using RC = Rec<D>;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double R[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) R[q] = 0.0;
+    // static slot data before the PDL wait (overlaps the predecessor's tail), face records after it
+    int4 gi = make_int4(0, 0, 0, 0);
+    if (i < L.n) gi = __ldg(L.ginfo + i);
+    pdl_wait();
     if (i < L.n) {
         // (gather base, all slots | interior slots << 16, sweep slot 0, sweep stride): one 16-byte load
-        const int4 gi = __ldg(L.ginfo + i);
         const int gb = gi.x, nt = gi.y & 0xffff;
         double sig = 0.0, al = 1.0;
         for (int s = 0; s < nt; ++s) {
