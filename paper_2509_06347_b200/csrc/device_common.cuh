@@ -12,9 +12,11 @@ namespace gmg {
 
 // per-cell sweep record layout (doubles)
 template <int D> struct Rec;
-// 3D: [W0..W3 | W4 dW0 dW1 dW2 | dW3 dW4 1/D a/2]: the own-cell epilogue reads
-// only the last 32-B chunk (1/D, alpha/2) and rewrites dW without reading the rest
-template <> struct Rec<3> { static constexpr int W = 0, DW = 5, INVD = 10, HA = 11, STRIDE = 12; };
+// 3D: [W0..W3 | W4 1/D a/2 dW0 | dW1 dW2 dW3 dW4]: the own-cell epilogue reads
+// one 32-B chunk (the 1/D and alpha/2 it needs, with W4 and dW0) and writes the
+// new dW as two whole chunks -- 32 B read + 64 B written per update, no partial
+// sectors (the previous [W0..W3 | W4 dW0..dW2 | dW3 dW4 1/D a/2] read 64 B)
+template <> struct Rec<3> { static constexpr int W = 0, INVD = 5, HA = 6, DW = 7, STRIDE = 12; };
 template <> struct Rec<2> { static constexpr int W = 0, DW = 4, INVD = 8, HA = 9, STRIDE = 12; };
 // (both 96 B: 32-byte aligned, so a neighbour record is three 256-bit loads)
 // per-slot record: A_0..A_{D-1}, S r at [D]

@@ -384,7 +384,7 @@ __device__ __forceinline__ void ld_neighbour(const double *rj, double *w, double
         ld4nc(rj + 4, c1);
         ld4nc(rj + 8, c2);
         w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-        dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+        dw[0] = c1[3]; dw[1] = c2[0]; dw[2] = c2[1]; dw[3] = c2[2]; dw[4] = c2[3];
     } else {
         ld4nc(rj, w);
         ld4nc(rj + 4, dw);
@@ -404,26 +404,23 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, int i, const do
 #pragma unroll
     for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
     if constexpr (D == 3) {
-        double c2[4];
-        ld4nc(ri + 8, c2);                          // dW3, dW4, 1/D, alpha/2
-        const double invD = c2[2], ha = c2[3];
+        double c1[4];
+        ld4nc(ri + 4, c1);                          // W4, 1/D, alpha/2, dW0
+        const double invD = c1[1], ha = c1[2];
         double d[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-        ri[5] = d[0];                               // dW0 (W4 at ri[4] untouched)
-        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(ri + 6), "d"(d[1]), "d"(d[2]) : "memory");
-        c2[0] = d[3];
-        c2[1] = d[4];
+        ri[RC::DW] = d[0];                          // dW0 alone: a partial-sector write
+        const double c2[4] = {d[1], d[2], d[3], d[4]};
         st4(ri + 8, c2);
         if (a.Wout) {
             double c0[4];
             ld4nc(ri, c0);
-            const double w4 = __ldg(ri + 4);
             a.Wout[o + 0] = c0[0] + d[0];
             a.Wout[o + 1] = c0[1] + d[1];
             a.Wout[o + 2] = c0[2] + d[2];
             a.Wout[o + 3] = c0[3] + d[3];
-            a.Wout[o + 4] = w4 + d[4];
+            a.Wout[o + 4] = c1[0] + d[4];
         }
     } else {
         double c2[4];
@@ -443,7 +440,7 @@ __device__ __forceinline__ void sweep_finish(const SweepArgs &a, int i, const do
 }
 
 // sweep variants (template bits, GMG_SWEEPV; default 3, measured DESIGN.md §6):
-//  1 = dW0..2 written as the whole 32-B chunk (W4 | dW0..2), no partial sector
+//  1 = dW0 written inside the whole 32-B chunk (W4 1/D alpha/2 | dW0), no partial sector
 //  2 = neighbour index of the next slot loaded one iteration ahead
 //  4 = own record tail + rhs prefetched to L1 before the slot loop
 // Fused halo (GMG_P2P): the sweep that computes a boundary cell's increment
@@ -488,18 +485,17 @@ __device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, con
     double r[NV], c1[4], c2[4];
 #pragma unroll
     for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
-    if constexpr (D == 3) ld4nc(ri + 4, c1);
-    ld4nc(ri + 8, c2);
+    if constexpr (D == 3) ld4nc(ri + 4, c1);       // W4, 1/D, alpha/2, dW0
+    else ld4nc(ri + 8, c2);                         // 1/D, alpha/2, -, -
     if constexpr (D == 3) {
-        const double invD = c2[2], ha = c2[3];
+        const double invD = c1[1], ha = c1[2];
         double d[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-        double w1[4] = {c1[0], d[0], d[1], d[2]};
+        const double w1[4] = {c1[0], c1[1], c1[2], d[0]};
         st4(ri + 4, w1);
-        c2[0] = d[3];
-        c2[1] = d[4];
-        st4(ri + 8, c2);
+        const double w2[4] = {d[1], d[2], d[3], d[4]};
+        st4(ri + 8, w2);
         p2p_store<D, P2P>(p, i, d);
         if (a.Wout) {
             double c0[4];

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256, 4) k_sweep_flow(SweepArgs a, FlowArgs f)
                                 ld4cg(rj + 4, c1);
                                 ld4cg(rj + 8, c2);
                                 w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-                                dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                                dw[0] = c1[3]; dw[1] = c2[0]; dw[2] = c2[1]; dw[3] = c2[2]; dw[4] = c2[3];
                             } else {
                                 ld4cg(rj, w);
                                 ld4cg(rj + 4, dw);
@@ -123,15 +123,14 @@ __global__ void __launch_bounds__(256, 4) k_sweep_flow(SweepArgs a, FlowArgs f)
                         ld4cg(ri + 4, c1);
                         ld4cg(ri + 8, c2);
                         if constexpr (D == 3) {
-                            const double invD = c2[2], ha = c2[3];
+                            const double invD = c1[1], ha = c1[2];
                             double d[NV];
 #pragma unroll
                             for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-                            const double w1[4] = {c1[0], d[0], d[1], d[2]};
+                            const double w1[4] = {c1[0], c1[1], c1[2], d[0]};
                             st4(ri + 4, w1);
-                            c2[0] = d[3];
-                            c2[1] = d[4];
-                            st4(ri + 8, c2);
+                            const double w2[4] = {d[1], d[2], d[3], d[4]};
+                            st4(ri + 8, w2);
                             if (Wout) {
                                 double c0[4];
                                 ld4cg(ri, c0);
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(256, 4) k_sweep_flow_w(SweepArgs a, FlowArgs f
                                 ld4cg(rj + 4, c1);
                                 ld4cg(rj + 8, c2);
                                 w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-                                dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                                dw[0] = c1[3]; dw[1] = c2[0]; dw[2] = c2[1]; dw[3] = c2[2]; dw[4] = c2[3];
                             } else {
                                 ld4cg(rj, w);
                                 ld4cg(rj + 4, dw);
@@ -241,15 +240,14 @@ __global__ void __launch_bounds__(256, 4) k_sweep_flow_w(SweepArgs a, FlowArgs f
                         ld4cg(ri + 4, c1);
                         ld4cg(ri + 8, c2);
                         if constexpr (D == 3) {
-                            const double invD = c2[2], ha = c2[3];
+                            const double invD = c1[1], ha = c1[2];
                             double d[NV];
 #pragma unroll
                             for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-                            const double w1[4] = {c1[0], d[0], d[1], d[2]};
+                            const double w1[4] = {c1[0], c1[1], c1[2], d[0]};
                             st4(ri + 4, w1);
-                            c2[0] = d[3];
-                            c2[1] = d[4];
-                            st4(ri + 8, c2);
+                            const double w2[4] = {d[1], d[2], d[3], d[4]};
+                            st4(ri + 8, w2);
                             if (Wout) {
                                 double c0[4];
                                 ld4cg(ri, c0);
@@ -354,7 +352,7 @@ __global__ void __launch_bounds__(256, 4) k_sweep_tailc(TailArgs t, int *bar)
                         ld4cg(rj + 4, c1);
                         ld4cg(rj + 8, c2);
                         w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-                        dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                        dw[0] = c1[3]; dw[1] = c2[0]; dw[2] = c2[1]; dw[3] = c2[2]; dw[4] = c2[3];
                     } else {
                         ld4cg(rj, w);
                         ld4cg(rj + 4, dw);
@@ -375,15 +373,14 @@ __global__ void __launch_bounds__(256, 4) k_sweep_tailc(TailArgs t, int *bar)
                 ld4cg(ri + 4, c1);
                 ld4cg(ri + 8, c2);
                 if constexpr (D == 3) {
-                    const double invD = c2[2], ha = c2[3];
+                    const double invD = c1[1], ha = c1[2];
                     double d[NV];
 #pragma unroll
                     for (int q = 0; q < NV; ++q) d[q] = -(rr[q] + ha * acc[q]) * invD;
-                    const double w1[4] = {c1[0], d[0], d[1], d[2]};
+                    const double w1[4] = {c1[0], c1[1], c1[2], d[0]};
                     st4(ri + 4, w1);
-                    c2[0] = d[3];
-                    c2[1] = d[4];
-                    st4(ri + 8, c2);
+                    const double w2[4] = {d[1], d[2], d[3], d[4]};
+                    st4(ri + 8, w2);
                     if (Wout) {
                         double c0[4];
                         ld4cg(ri, c0);
@@ -505,7 +502,7 @@ __global__ void __launch_bounds__(256, 4) k_p2p_emulate(EmuArgs e)
                             ld4cg(rj + 4, c1);
                             ld4cg(rj + 8, c2);
                             w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-                            dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                            dw[0] = c1[3]; dw[1] = c2[0]; dw[2] = c2[1]; dw[3] = c2[2]; dw[4] = c2[3];
                         } else {
                             ld4cg(rj, w);
                             ld4cg(rj + 4, dw);
@@ -525,14 +522,13 @@ __global__ void __launch_bounds__(256, 4) k_p2p_emulate(EmuArgs e)
                     ld4cg(ri + 8, c2);
                     double d[NV];
                     if constexpr (D == 3) {
-                        const double invD = c2[2], ha = c2[3];
+                        const double invD = c1[1], ha = c1[2];
 #pragma unroll
                         for (int q = 0; q < NV; ++q) d[q] = -(rr[q] + ha * acc[q]) * invD;
-                        const double w1[4] = {c1[0], d[0], d[1], d[2]};
+                        const double w1[4] = {c1[0], c1[1], c1[2], d[0]};
                         st4(ri + 4, w1);
-                        c2[0] = d[3];
-                        c2[1] = d[4];
-                        st4(ri + 8, c2);
+                        const double w2[4] = {d[1], d[2], d[3], d[4]};
+                        st4(ri + 8, w2);
                         if (Wout) {
                             double c0[4];
                             ld4cg(ri, c0);
@@ -607,7 +603,7 @@ __global__ void __launch_bounds__(kTailT) k_sweep_tail(TailArgs t)
                         ld4(rj + 4, c1);
                         ld4(rj + 8, c2);
                         w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-                        dw[0] = c1[1]; dw[1] = c1[2]; dw[2] = c1[3]; dw[3] = c2[0]; dw[4] = c2[1];
+                        dw[0] = c1[3]; dw[1] = c2[0]; dw[2] = c2[1]; dw[3] = c2[2]; dw[4] = c2[3];
                     } else {
                         ld4(rj, w);
                         ld4(rj + 4, dw);
@@ -777,7 +773,7 @@ __device__ __forceinline__ void pipe_issue(const SweepArgs &a, int c0, int c1, i
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(a.rhs + (size_t)c0 * NV + t) : "memory");
     }
     for (int t = lane; t < nc * 2; t += 32)
-        cp_async16(ownS + 2 * t, a.rec + (size_t)(c0 + t / 2) * RC::STRIDE + 8 + 2 * (t & 1));
+        cp_async16(ownS + 2 * t, a.rec + (size_t)(c0 + t / 2) * RC::STRIDE + RC::INVD - RC::INVD % 4 + 2 * (t & 1));
 }
 
 template <int D>
@@ -855,8 +851,8 @@ __global__ void __launch_bounds__(kPW * 32) k_sweep_pipe(SweepArgs a, PipeLayout
 #pragma unroll
                 for (int q = 0; q < NV; ++q) acc[q] += part[s * 5 + q];
             }
-            const double *own = ownS + lane * 4;     // 3D: dW3, dW4, 1/D, a/2   2D: 1/D, a/2, -, -
-            const double invD = own[D == 3 ? 2 : 0], ha = own[D == 3 ? 3 : 1];
+            const double *own = ownS + lane * 4;     // the 32-B chunk holding 1/D and alpha/2
+            const double invD = own[RC::INVD % 4], ha = own[RC::HA % 4];
             double d[NV];
 #pragma unroll
             for (int q = 0; q < NV; ++q) d[q] = -(rhsS[lane * NV + q] + ha * acc[q]) * invD;
