@@ -8,9 +8,12 @@ The arithmetic lives in gmg_oracle.c (plain C, fp64, natural order,
 -O2 -ffp-contract=off); this package only builds/loads it and orchestrates the
 V-cycle (oracle/vcycle.py) in the order of SURVEY.md §8(c) O8.
 
-Parity-unpinned functions: residual histories over many V-cycles (the
-paper's convergence curves are images without data); they
-are pinned only through their constituent steps.
+Residual histories over many V-cycles have no printed values to pin against
+(the paper's convergence curves are images without data):
+they are pinned through their constituent steps and by invariants only -- the
+free-stream fixed point and frame equivariance (a 90-degree rotation or a
+reflection of mesh and velocities reproduces the 40-cycle 2D and 25-cycle 3D
+histories with the momentum norms permuted, tests/test_oracle_pins.py).
 """
 from __future__ import annotations
 
