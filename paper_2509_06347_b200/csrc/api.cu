@@ -374,10 +374,11 @@ void launch_sweep(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, const 
     // a window larger than the set-aside persists that fraction of its lines (GMG_L2FULL)
     const float hit = (ctx->l2_window && win_bytes > ctx->l2_window) ? (float)((double)ctx->l2_window / (double)win_bytes) : 1.0f;
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
-    if (ctx->sweep_bs == 128 && sweep_var == 3 && minb == 4) {   // default; the variants run at 256
+    if (ctx->sweep_bs == 128 && (sweep_var == 3 || sweep_var == 19) && minb == 4) {   // default; the variants run at 256
         int nb = (int)((nthreads + 127) / 128);
         if (ctx->sweep_grid_cap > 0) nb = std::min(nb, 2 * ctx->sweep_grid_cap);
-        launch_with_window(k_sweep128<D, LPC>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
+        if (sweep_var == 19) launch_with_window(k_sweep128<D, LPC, 3 | 8 | 16>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
+        else launch_with_window(k_sweep128<D, LPC>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
         return;
     }
     int nb = nblk(nthreads);

@@ -615,6 +615,67 @@ __device__ __forceinline__ void sweep_body(const SweepArgs &a, const P2PArgs &p)
     if constexpr ((VAR & 8) != 0) pdl_wait();   // threads without a cell: nothing may run past the predecessor
 }
 
+// (VAR bit 16) the same sweep software-pipelined across grid-stride rounds: a
+// launch sized to one resident wave runs each thread over several cells, one
+// after the other, and every cell is a chain of dependent round trips
+// ((first slot, degree) -> neighbour index -> records -> epilogue).  The next
+// round's (first slot, degree) is loaded when a round starts and its first
+// neighbour index before the round's epilogue, so a later round starts with
+// its record loads; round 0's indices are loaded before griddepcontrol.wait.
+template <int D, int LPC>
+__device__ __forceinline__ void sweep_body_pipe(const SweepArgs &a)
+{
+    constexpr int NV = D + 2;
+    using RC = Rec<D>;
+    const int stride = gridDim.x * blockDim.x;            // a multiple of LPC: sub is fixed per thread
+    const int g0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const int sub = g0 % LPC;
+    const int cstep = stride / LPC;
+    int i = a.cbeg + g0 / LPC;
+    int2 sd = make_int2(0, 0);
+    int jf = 0;
+    if (i < a.cend) {
+        sd = __ldg(a.sinfo + i);
+        jf = sub < sd.y ? __ldg(a.sJe + sd.x + sub) : 0;
+    }
+    pdl_wait();
+    const int total = (a.cend - a.cbeg) * LPC;
+    const int rounds = (total + stride - 1) / stride;
+    for (int r = 0; r < rounds; ++r, i += cstep) {
+        const bool valid = i < a.cend;
+        const int in = i + cstep;
+        int2 sdn = make_int2(0, 0);
+        if (in < a.cend) sdn = __ldg(a.sinfo + in);
+        double acc[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+        if (valid) {
+            const int e1 = sd.x + sd.y;
+            int j = jf;
+            for (int e = sd.x + sub; e < e1; e += LPC) {
+                const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
+                if (j >= a.zlo && j < a.zhi) { j = jn; continue; }
+                double sr[4];
+                ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                double w[NV], dw[NV];
+                ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
+                flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                j = jn;
+            }
+        }
+        jf = (in < a.cend && sub < sdn.y) ? __ldg(a.sJe + sdn.x + sub) : 0;
+        sd = sdn;
+        if (LPC > 1) {
+#pragma unroll
+            for (int o = LPC / 2; o > 0; o >>= 1) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+            }
+        }
+        if (valid && sub == 0) sweep_finish_full<D, false>(a, i, acc);
+    }
+}
+
 template <int D, int LPC, int MINB, int VAR = 3>
 __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 {
@@ -623,11 +684,12 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 }
 
 // the default sweep launch: 128-thread blocks, 8 per SM (GMG_SWEEP_BS=256 -> k_sweep)
-template <int D, int LPC>
+template <int D, int LPC, int VAR = 3 | 8>
 __global__ void __launch_bounds__(128, 8) k_sweep128(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
-    sweep_body<D, LPC, 3 | 8, false>(a, P2PArgs{});
+    if constexpr ((VAR & 16) != 0) sweep_body_pipe<D, LPC>(a);
+    else sweep_body<D, LPC, VAR, false>(a, P2PArgs{});
 }
 
 __device__ __forceinline__ int ld_acquire_sys(const int *p)
