@@ -213,7 +213,9 @@ enum { GMG_K_FACE = 0, GMG_K_GATHER = 1, GMG_K_SWEEP = 2, GMG_K_RESTRICT = 3, GM
 gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_t *count_out, double *bytes_out);
 
 /* Sweep-only instrumentation: time one smoothing step's sweeps on `level`
- * (graph-replayed `reps` times); *ms = total device ms, *cell_updates =
+ * (graph-replayed `reps` times) -- the same launches as the V-cycle's step,
+ * including the W = W_lin + dW write of the last backward half-sweep, so the
+ * level's W is overwritten; *ms = total device ms, *cell_updates =
  * N_l * 2 * n_sweeps * reps, *bytes = algorithmic bytes. */
 gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, double *ms, double *cell_updates,
                            double *bytes);

@@ -2140,11 +2140,13 @@ gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, doub
     for (double &b : ctx->kbytes) b = 0;
     cudaGraph_t g;
     cudaGraphExec_t ge;
+    // the launches of the V-cycle's smoothing step on this level, unchanged: the last backward half-sweep
+    // also writes W = W_lin + dW (the level's W is an output of the step, rewritten by every V-cycle)
     auto rhs = [](DevLevel &L) { return (const double *)L.Rt; };
-    auto nowout = [](DevLevel &) { return (double *)nullptr; };
+    auto wout = [](DevLevel &L) { return L.W; };
     CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    if (ctx->opt.dim == 2) enqueue_sweeps<2>(Lc, level, n_sweeps, rhs, nowout);
-    else enqueue_sweeps<3>(Lc, level, n_sweeps, rhs, nowout);
+    if (ctx->opt.dim == 2) enqueue_sweeps<2>(Lc, level, n_sweeps, rhs, wout);
+    else enqueue_sweeps<3>(Lc, level, n_sweeps, rhs, wout);
     CK(cudaStreamEndCapture(cs, &g));
     CK(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
