@@ -157,6 +157,17 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     int4 gi = make_int4(0, 0, 0, 0);
     if (i < L.n) gi = __ldg(L.ginfo + i);
     pdl_wait();
+    // the cell's one per-cell input of the epilogue (W for G_COPY_W, Rs for G_SET_F, F for G_ADD_F, the
+    // explicit state for G_EXPLICIT) is loaded before the slot loop: its latency hides under the gathers,
+    // and the epilogue's stores no longer wait on loads the compiler cannot hoist above them (aliasing)
+    const int pk = (a.flags & G_COPY_W) ? G_COPY_W : (a.flags & G_SET_F) ? G_SET_F
+                 : ((a.flags & G_WRITE_RT) && (a.flags & G_ADD_F)) ? G_ADD_F : (a.flags & G_EXPLICIT) ? G_EXPLICIT : 0;
+    double pre[NV];
+    if (i < L.n && pk) {
+        const double *src = pk == G_COPY_W ? L.W : pk == G_SET_F ? L.Rs : pk == G_ADD_F ? L.F : a.Wexp;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) pre[q] = src[(size_t)i * NV + q];
+    }
     if (i < L.n) {
         // (gather base, all slots | interior slots << 16, sweep slot 0, sweep stride): one 16-byte load
         const int gb = gi.x, nt = gi.y & 0xffff;
@@ -196,16 +207,26 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         const size_t o = (size_t)i * NV;
         if (a.flags & G_COPY_W) {
 #pragma unroll
-            for (int q = 0; q < NV; ++q) rc[RC::W + q] = L.W[o + q];
+            for (int q = 0; q < NV; ++q) rc[RC::W + q] = pre[q];
         }
         if (a.flags & G_SET_F) {
+            if (pk == G_SET_F) {
 #pragma unroll
-            for (int q = 0; q < NV; ++q) L.F[o + q] = L.Rs[o + q] - R[q];
+                for (int q = 0; q < NV; ++q) L.F[o + q] = pre[q] - R[q];
+            } else {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) L.F[o + q] = L.Rs[o + q] - R[q];
+            }
         }
         if (a.flags & G_WRITE_RT) {
             if (a.flags & G_ADD_F) {
+                if (pk == G_ADD_F) {
 #pragma unroll
-                for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q] + L.F[o + q];
+                    for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q] + pre[q];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q] + L.F[o + q];
+                }
             } else {
 #pragma unroll
                 for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q];
@@ -213,8 +234,13 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         }
         if (a.flags & G_EXPLICIT) {
             const double c = a.cfl_exp / sig;
+            if (pk == G_EXPLICIT) {
 #pragma unroll
-            for (int q = 0; q < NV; ++q) a.Wexp[o + q] = a.Wexp[o + q] - c * R[q];
+                for (int q = 0; q < NV; ++q) a.Wexp[o + q] = pre[q] - c * R[q];
+            } else {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) a.Wexp[o + q] = a.Wexp[o + q] - c * R[q];
+            }
         }
     }
     if (a.flags & G_NORM) {
