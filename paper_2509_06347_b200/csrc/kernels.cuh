@@ -710,8 +710,8 @@ __global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
 }
 
 // the default sweep launch: 128-thread blocks, 8 per SM (GMG_SWEEP_BS=256 -> k_sweep)
-template <int D, int LPC, int VAR = 3 | 8>
-__global__ void __launch_bounds__(128, 8) k_sweep128(SweepArgs a)
+template <int D, int LPC, int VAR = 3 | 8, int MINB = 8>
+__global__ void __launch_bounds__(128, MINB) k_sweep128(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
     if constexpr ((VAR & 16) != 0) sweep_body_pipe<D, LPC>(a);
