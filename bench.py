@@ -87,9 +87,9 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def workload(config):
+def workload(config, p_equiv=1):
     from synth import configs, state
-    m = configs.config(config)
+    m = configs.config(config, p_equiv) if config == 5 else configs.config(config)
     fs = configs.FREESTREAM[config]
     W = state.bow_shock(m, *fs)
     return m, W, state.winf(*fs)
@@ -285,6 +285,8 @@ def main():
     ap.add_argument("--impl", default="gmg", choices=["gmg", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n-sweeps", type=int, default=6)
+    ap.add_argument("--p-equiv", type=int, default=1,
+                    help="--config 5 on one GPU at the mesh size of P GPUs (P = 8: the whole ~8 M-cell config 5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/cpu)")
     ap.add_argument("--no-next1", action="store_true", help="skip the NEXT-1 (third-order CGKS fine operator) line")
@@ -324,7 +326,7 @@ def main():
                        + ("fused P2P halo (CUDA IPC)" if os.environ.get("GMG_P2P", "0") == "1"
                           else "NCCL halo exchange per color, overlapped with the interior sweep"))
     else:
-        m, W, Winf = workload(args.config)
+        m, W, Winf = workload(args.config, args.p_equiv)
         t_setup = time.perf_counter()
         # (--profile-only: host setup, so that an ncu launch list starts with the V-cycle kernels)
         s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, setup_device=0 if args.profile_only else 1)
@@ -378,7 +380,8 @@ def main():
     achieved = (pbytes[sw] / (pms[sw] * 1e-3)) / 1e9 if pms[sw] > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_sweep_traffic.json")
-    if os.path.exists(tp):
+    # the ncu capture is of config 4 on one GPU: other workloads report traffic = null
+    if os.path.exists(tp) and args.config == 4 and ws == 1:
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
         except Exception:
