@@ -471,7 +471,7 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
     // small color blocks are latency bound (one partial wave, each lane walks
     // its slots one dependent gather after the other): spread the slots over
     // more lanes while the whole block still fits in one resident wave
-    int lpc = ctx->lpc;
+    int lpc = (l < 8 && ctx->lpc_level[l] > 0) ? ctx->lpc_level[l] : ctx->lpc;
     if (ctx->adapt_lpc && ctx->sweep_grid_cap > 0) {
         const int64_t wave = (int64_t)ctx->sweep_grid_cap * 256, cells = a.cend - a.cbeg;
         while (lpc < 16 && cells * lpc * 2 <= wave) lpc *= 2;
@@ -1185,6 +1185,14 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
     ctx->stream = (cudaStream_t)opt->stream;
     ctx->nparts = std::max(opt->nranks, opt->local_domains);
     if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
+    if (const char *e = std::getenv("GMG_LPC_LEVELS")) {                     // per level: "2,2,4"
+        int k = 0;
+        for (const char *p = e; *p && k < 8; ++k) {
+            ctx->lpc_level[k] = std::atoi(p);
+            while (*p && *p != ',') ++p;
+            if (*p == ',') ++p;
+        }
+    }
     if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
     // programmatic dependent launch between the V-cycle kernels: every kernel launched with the attribute
     // waits (griddepcontrol.wait) before touching its predecessor's outputs; the sweep phases load their

@@ -231,6 +231,7 @@ struct gmg_ctx {
     int sweep_var = 3;                // k_sweep variant bits (kernels.cuh), GMG_SWEEPV
     int sweep_bs = 128;               // sweep block size: 128 x 8 per SM (0.4 % faster than 256 x 4), GMG_SWEEP_BS
     int lpc = 2;                      // sweep lanes per cell (1, 2, 4) of the large color blocks
+    int lpc_level[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // per-level override of lpc (GMG_LPC_LEVELS=a,b,c; 0 = lpc)
     int adapt_lpc = 1;                // blocks that fit one wave at 2x lanes get up to 16 lanes per cell
     int skip_repeat = 1;              // drop the repeated same-color phase at every sweep turn (exact)
     int skip_zero = 1;                // first forward half-sweep: skip later-color neighbours (dW = +0, exact)
