@@ -366,3 +366,29 @@ def test_owned_layout_host_io_equals_synchronous():
     s.close()
     for k in range(len(Ws)):
         assert np.array_equal(outs[k].numpy(), ref[k][:, own]), k
+
+
+@pytest.mark.parametrize("var, val", [("GMG_SWEEPV", "19"), ("GMG_MINB", "9")], ids=["pipelined_rounds", "minb9"])
+def test_sweep_launch_variants_bit_exact(G, var, val, monkeypatch):
+    """Launch-shape variants of the sweep kept for the record (rounds
+    software-pipelined, 9 blocks per SM) keep every cell's arithmetic -- the same
+    lanes per cell, slot order per lane and shuffle tree -- so they reproduce the
+    default bits.  The mesh (sphere shell, ~360 k cells) is large enough that the
+    big color blocks take several grid-stride rounds of the one-wave launch."""
+    m = configs.sphere_shell(24)
+    fs = configs.FREESTREAM[4]
+    W, Winf = state.bow_shock(m, *fs), state.winf(*fs)
+    out = []
+    for v in (None, val):
+        if v is None:
+            monkeypatch.delenv(var, raising=False)
+        else:
+            monkeypatch.setenv(var, v)
+        s = G.Solver(m, n_levels=3)
+        s.set_state(W, Winf)
+        h = s.vcycle(2)
+        out.append((h, s.get_state(0), s.get_state(1)))
+        s.close()
+    (h0, W0, C0), (h1, W1, C1) = out
+    assert np.array_equal(h0, h1) and np.array_equal(W0, W1) and np.array_equal(C0, C1)
+    assert np.all(np.isfinite(W0))
