@@ -380,10 +380,11 @@ void launch_sweep(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, const 
         launch_with_window(k_sweep128<D, LPC, 3 | 8, 9>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
         return;
     }
-    if (ctx->sweep_bs == 128 && (sweep_var == 3 || sweep_var == 19) && minb == 4) {   // default; the variants run at 256
+    if (ctx->sweep_bs == 128 && (sweep_var == 3 || sweep_var == 19 || sweep_var == 35) && minb == 4) {   // default; the variants run at 256
         int nb = (int)((nthreads + 127) / 128);
         if (ctx->sweep_grid_cap > 0) nb = std::min(nb, 2 * ctx->sweep_grid_cap);
         if (sweep_var == 19) launch_with_window(k_sweep128<D, LPC, 3 | 8 | 16>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
+        else if (sweep_var == 35) launch_with_window(k_sweep128<D, LPC, 3 | 8 | 32>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
         else launch_with_window(k_sweep128<D, LPC>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
         return;
     }

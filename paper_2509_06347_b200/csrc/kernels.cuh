@@ -501,7 +501,7 @@ __device__ __forceinline__ void p2p_store(const P2PArgs &p, int i, const double 
     }
 }
 
-template <int D, bool P2P = false>
+template <int D, bool P2P = false, bool CS = true>
 __device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, const double *acc,
                                                   const P2PArgs &p = P2PArgs{})
 {
@@ -510,7 +510,7 @@ __device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, con
     const size_t o = (size_t)i * NV;
     double r[NV], c1[4], c2[4];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
+    for (int q = 0; q < NV; ++q) r[q] = CS ? __ldcs(a.rhs + o + q) : __ldg(a.rhs + o + q);
     if constexpr (D == 3) ld4nc(ri + 4, c1);       // W4, 1/D, alpha/2, dW0
     else ld4nc(ri + 8, c2);                         // 1/D, alpha/2, -, -
     if constexpr (D == 3) {
@@ -595,7 +595,8 @@ __device__ __forceinline__ void sweep_body(const SweepArgs &a, const P2PArgs &p)
                 const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
                 if (j >= a.zlo && j < a.zhi) { j = jn; continue; }
                 double sr[4];
-                ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                if constexpr ((VAR & 32) != 0) ld4nc(a.sRe + (size_t)e * kSlotRec, sr);   // L2-resident
+                else ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
                 double w[NV], dw[NV];
                 ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
                 flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
@@ -634,7 +635,7 @@ __device__ __forceinline__ void sweep_body(const SweepArgs &a, const P2PArgs &p)
         }
     }
     if (valid && sub == 0) {
-        if constexpr ((VAR & 1) != 0 || P2P) sweep_finish_full<D, P2P>(a, i, acc, p);
+        if constexpr ((VAR & 1) != 0 || P2P) sweep_finish_full<D, P2P, (VAR & 32) == 0>(a, i, acc, p);
         else sweep_finish<D>(a, i, acc);
     }
     }
