@@ -374,6 +374,12 @@ void launch_sweep(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, const 
     // a window larger than the set-aside persists that fraction of its lines (GMG_L2FULL)
     const float hit = (ctx->l2_window && win_bytes > ctx->l2_window) ? (float)((double)ctx->l2_window / (double)win_bytes) : 1.0f;
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
+    if (ctx->sweep_bs == 64 && sweep_var == 3 && minb == 4) {   // GMG_SWEEP_BS=64: 16 blocks of 64 per SM
+        int nb = (int)((nthreads + 63) / 64);
+        if (ctx->sweep_grid_cap > 0) nb = std::min(nb, 4 * ctx->sweep_grid_cap);
+        launch_with_window(k_sweep64<D, LPC>, dim3(nb), dim3(64), s, a, win, win_bytes, pdl, hit);
+        return;
+    }
     if (ctx->sweep_bs == 128 && sweep_var == 3 && minb == 9) {   // GMG_MINB=9: 9 blocks of 128 per SM (56 registers)
         int nb = (int)((nthreads + 127) / 128);
         if (ctx->sweep_grid_cap > 0) nb = std::min(nb, (9 * ctx->sweep_grid_cap) / 4);

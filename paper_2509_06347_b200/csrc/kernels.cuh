@@ -719,6 +719,15 @@ __global__ void __launch_bounds__(128, MINB) k_sweep128(SweepArgs a)
     else sweep_body<D, LPC, VAR, false>(a, P2PArgs{});
 }
 
+// 64-thread blocks, 16 per SM (GMG_SWEEP_BS=64): finer-grained block
+// scheduling for the partial last round of a grid-stride color launch
+template <int D, int LPC>
+__global__ void __launch_bounds__(64, 16) k_sweep64(SweepArgs a)
+{
+    pdl_launch_dependents();
+    sweep_body<D, LPC, 3 | 8, false>(a, P2PArgs{});
+}
+
 __device__ __forceinline__ int ld_acquire_sys(const int *p)
 {
     int v;

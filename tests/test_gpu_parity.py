@@ -368,7 +368,8 @@ def test_owned_layout_host_io_equals_synchronous():
         assert np.array_equal(outs[k].numpy(), ref[k][:, own]), k
 
 
-@pytest.mark.parametrize("var, val", [("GMG_SWEEPV", "19"), ("GMG_MINB", "9")], ids=["pipelined_rounds", "minb9"])
+@pytest.mark.parametrize("var, val", [("GMG_SWEEPV", "19"), ("GMG_MINB", "9"), ("GMG_SWEEP_BS", "64")],
+                         ids=["pipelined_rounds", "minb9", "bs64"])
 def test_sweep_launch_variants_bit_exact(G, var, val, monkeypatch):
     """Launch-shape variants of the sweep kept for the record (rounds
     software-pipelined, 9 blocks per SM) keep every cell's arithmetic -- the same
