@@ -1,0 +1,123 @@
+"""Mutation check of the oracle's pins (CPU only).
+
+Each mutant is a plausible mistake in one step of the oracle -- a dropped
+term, a wrong sign or index, a wrong reading -- applied to a COPY of oracle/
+in a temporary directory (text replacement in gmg_oracle.c or vcycle.py,
+rebuilt with the same gcc flags).  The named pin is then run against the
+mutant in a fresh interpreter and must FAIL; the same pin passes on the real
+oracle (it is part of the suite).  DESIGN.md §3 lists, per oracle function,
+the pin that fixes it; this file is the evidence that those pins bite.
+"""
+import os
+import shutil
+import subprocess
+import sys
+import textwrap
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+C, PY = "gmg_oracle.c", "vcycle.py"
+P1, P2 = "test_oracle_pins", "test_oracle_pins_fas"
+
+# (id, file, old, new, pin module, pin function, params)
+MUTANTS = [
+    # FAS forcing (readings A8, A11)
+    ("F_sign_flipped", PY, "F = Rs - Rc", "F = Rc - Rs", P2, "test_fas_steady_state_consistency", {}),
+    ("F_dropped_on_level2", PY, "Rt_prev = Rl + F", "Rt_prev = Rl", P2, "test_fas_steady_state_consistency", {}),
+    ("coarse_rhs_R_of_W0", PY, "dW = smooth(L[l], W0c, Rs, relax(ac)", "dW = smooth(L[l], W0c, Rc, relax(ac)",
+     P2, "test_fas_steady_state_consistency", {}),
+    # DF helper (A16, A17)
+    ("df_exponent_dropped", C, "for (int g = 0; g < L->ngauss[f]; ++g) afM *= af;", "afM = af;",
+     P2, "test_df_cell_product_mixed_gauss_points", {}),
+    ("df_min_not_product", C, "if (alpha) alpha[l] *= afM;", "if (alpha) alpha[l] = fmin(alpha[l], afM);",
+     P2, "test_df_cell_product_mixed_gauss_points", {}),
+    ("df_Mat_not_squared", C, "dMt2 += t * t;", "dMt2 += fabs(t);", P2, "test_df_tangential_mach_term", {}),
+    ("df_Mat_magnitudes", C, "double t = (ul[k] - Ul * n[k]) / al - (ur[k] - Ur * n[k]) / ar;",
+     "double t = fabs(ul[k] - Ul * n[k]) / al - fabs(ur[k] - Ur * n[k]) / ar;", P2, "test_df_tangential_mach_term",
+     {}),
+    ("df_Man_dropped", C, "double D = fabs(pl - pr) / pl + fabs(pl - pr) / pr + dMn * dMn + dMt2;",
+     "double D = fabs(pl - pr) / pl + fabs(pl - pr) / pr + dMt2;", P1, "test_df_examples", {}),
+    # spectral radius / Sigma (A5, A6)
+    ("sigma_interior_only", C, "if (Sigma) Sigma[l] += S * rr;", "if (Sigma && r >= 0) Sigma[l] += S * rr;",
+     P2, "test_sigma_single_boundary_cell_hand_computed", {}),
+    ("r_of_left_state_only", C, "Wb[q] = 0.5 * (WL[q] + WR[q]);", "Wb[q] = WL[q];",
+     P2, "test_sigma_single_boundary_cell_hand_computed", {}),
+    ("slip_ghost_half_reflection", C, "Wg[1 + k] = Wi[1 + k] - 2.0 * mn * n[k];", "Wg[1 + k] = Wi[1 + k] - mn * n[k];",
+     P2, "test_sigma_single_boundary_cell_hand_computed", {}),
+    # MC-SGS sweep (A1, A7)
+    ("sweep_r_sign", C, "sum[q] += S * (T1[q] - T0[q] - rf[f] * dWj[q]);",
+     "sum[q] += S * (T1[q] - T0[q] + rf[f] * dWj[q]);", P2, "test_linear_flux_sweep_is_symmetric_gauss_seidel",
+     {"mk": "tri"}),
+    ("sweep_half_dropped", C, "-(Rt[q * n + i] + 0.5 * alpha[i] * sum[q]) / D[i]",
+     "-(Rt[q * n + i] + alpha[i] * sum[q]) / D[i]", P2, "test_linear_flux_sweep_is_symmetric_gauss_seidel",
+     {"mk": "box"}),
+    ("sweep_backward_runs_forward", C, "int c = half == 0 ? cc + 1 : ncolor - cc;", "int c = cc + 1;",
+     P2, "test_linear_flux_sweep_is_symmetric_gauss_seidel", {"mk": "tri"}),
+    ("sweep_normal_not_flipped", C, "nn[k] = sigma * A[k] / S;", "nn[k] = A[k] / S;",
+     P2, "test_linear_flux_sweep_is_symmetric_gauss_seidel", {"mk": "tri"}),
+    ("diag_cfl_swapped", C, "(1.0 - alpha[i]) * (Sigma[i] / cfl_exp)", "(1.0 - alpha[i]) * (Sigma[i] / cfl_imp)",
+     P1, "test_hybrid_diagonal_examples", {}),
+    # residual / KFVS (O4)
+    ("residual_right_sign", C, "for (int q = 0; q < nv; ++q) R[q * n + r] -= S * F[q];",
+     "for (int q = 0; q < nv; ++q) R[q * n + r] += S * F[q];", P1, "test_freestream_residual_zero", {"mk": 1}),
+    ("kfvs_recurrence_coeff", C, "double m3 = U * m2 + (2.0 / (2.0 * lambda)) * m1;",
+     "double m3 = U * m2 + (1.0 / (2.0 * lambda)) * m1;", P1, "test_kfvs_equal_states_give_euler_flux",
+     {"dim": 3}),
+    # explicit step, restriction, prolongation (A9, A13, A15)
+    ("explicit_V_over_dt", C, "W[q * n + i] - (cfl_exp / Sigma[i]) * R[q * n + i]",
+     "W[q * n + i] - (Sigma[i] / cfl_exp) * R[q * n + i]", P2, "test_explicit_step_worked_example", {}),
+    ("restrict_alpha_max", C, "if (af[i] < ac[c]) ac[c] = af[i];", "if (af[i] > ac[c]) ac[c] = af[i];",
+     P1, "test_restrict_worked_example", {}),
+    ("prolong_sign", C, "Wf[q * nfine + i] + alpha_f[i] * (Wc[q * nc + c] - W0c[q * nc + c])",
+     "Wf[q * nfine + i] - alpha_f[i] * (Wc[q * nc + c] - W0c[q * nc + c])", P1,
+     "test_restrict_conservation_and_prolong_limits", {}),
+    # setup (Algorithms 1 and 3)
+    ("hash_product_dropped", C, "return (23u * (l + r) + l * r) % nf_interior;",
+     "return (23u * (l + r)) % nf_interior;", P1, "test_face_hash_worked_examples", {}),
+    ("color_start_2", C, "color[next_start] = 1;                               /* color(v0) = 1 */",
+     "color[next_start] = 2;", P1, "test_coloring_valid_and_matches_brute_force", {"mk": 1}),
+]
+_RUNNER = textwrap.dedent("""
+    import sys
+    tmp, root, module, name, params = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4], eval(sys.argv[5])
+    sys.path.insert(0, tmp)
+    sys.path.insert(1, root)
+    import oracle
+    assert oracle.__file__.startswith(tmp), oracle.__file__
+    oracle.lib()
+    import importlib
+    mod = importlib.import_module("tests." + module)
+    fn = getattr(mod, name)
+    kw = dict(params)
+    if "steady" in fn.__code__.co_varnames[:fn.__code__.co_argcount]:
+        kw["steady"] = mod._steady_naca(oracle)
+    try:
+        fn(oracle, **kw)
+    except AssertionError:
+        sys.exit(3)          # the pin fails on the mutant: killed
+    sys.exit(0)              # survived
+""")
+
+
+def _mutant_dir(tmp_path, fname, old, new):
+    d = tmp_path / "oracle"
+    d.mkdir()
+    src = os.path.join(ROOT, "oracle")
+    for f in os.listdir(src):
+        if f.endswith((".c", ".py")):
+            shutil.copy(os.path.join(src, f), d / f)
+    text = (d / fname).read_text()
+    # every occurrence (F appears in both the KFVS and the CGKS3 V-cycle orchestration)
+    assert text.count(old) >= 1, f"mutation site absent: {old!r}"
+    (d / fname).write_text(text.replace(old, new))
+    return str(tmp_path)
+
+
+@pytest.mark.parametrize("mid,fname,old,new,module,name,params", MUTANTS, ids=[m[0] for m in MUTANTS])
+def test_pin_kills_mutant(tmp_path, mid, fname, old, new, module, name, params):
+    tmp = _mutant_dir(tmp_path, fname, old, new)
+    r = subprocess.run([sys.executable, "-c", _RUNNER, tmp, ROOT, module, name, repr(params)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 3, f"mutant {mid} survived {module}.{name} (rc {r.returncode})\n{r.stdout}\n{r.stderr}"
