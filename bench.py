@@ -7,16 +7,22 @@ prepare + 6 MC-LU-SGS sweeps on each coarse level, DF prolongation, residual
 norm) on BASELINE configs[3]: the 3D ~1M-cell tet/prism sphere shell
 (synthetic, seeded), FP64.
 
-value  = MC-LU-SGS cell-updates per V-cycle / device time per V-cycle
-         (one cell-update = one cell's dW solved once),
-         summed over all ranks.
-e2e    = the same metric through the C ABI with pinned HOST buffers: per step
-         gmg_set_state (H2D) + gmg_vcycle + gmg_get_state (D2H).
-roofline: the sweep kernel (dominant), algorithmic bytes / its
-         CUDA-event time inside the profiled V-cycles, vs MEASURED_PEAKS hbm.
-cpu_baseline: the oracle (plain C, 1 thread) on one V-cycle of the same mesh.
+value  = MC-LU-SGS cell-updates EXECUTED per V-cycle / device time per
+         V-cycle (one cell-update = one cell's increment solved once, SURVEY
+         §8(d); the repeated phases dropped by skip_repeat are not counted --
+         Algorithm 2's nominal count is reported beside it), summed over ranks.
+e2e    = the same metric through the C ABI with pinned HOST buffers, as a
+         dependent time loop: step k+1's input is step k's result read back to
+         the host (gmg_set_state H2D + gmg_vcycle + gmg_get_state D2H); the
+         pipelined throughput of independent inputs is reported beside it.
+roofline: the sweep kernel (dominant), algorithmic bytes (SURVEY §8(d),
+         DESIGN.md §8) / its in-step launch time, vs MEASURED_PEAKS hbm.
+cpu_baseline: the oracle's timing build (oracle/: -O3 -march=native, OpenMP
+         within a color, built on the box) on one V-cycle of the same mesh,
+         all host cores, with the single-thread figure beside it.
 
---impl reference runs the oracle as the reference arm (rank 0 only).
+--impl reference runs the oracle's timing build (all host cores) as the
+reference arm (rank 0 only).
 """
 from __future__ import annotations
 
@@ -184,40 +190,49 @@ def next1_block(m, W, Winf, args, dev):
 
 
 def sweep_updates_per_cycle(sizes, n_sweeps, fine_smoother):
+    """Algorithm 2's nominal count: N_l * 2 * n_sweeps per smoothed level."""
     lv = range(0 if fine_smoother else 1, len(sizes))
     return sum(sizes[l][0] for l in lv) * 2 * n_sweeps
 
 
-def sweep_cells_executed_per_cycle(solver, n_sweeps, fine_smoother):
-    """cell visits the library actually runs: the same-color phase at every
-    sweep turn (c_N then c_N, c_1 then c_1) is idempotent and skipped (exact,
-    DESIGN.md §6); the metric counts Algorithm 2's nominal N * 2 * n_sweeps
-    updates, whose result is delivered bit for bit
-    (tests/test_gpu_parity.py::test_repeated_phase_skip_is_bit_exact)"""
-    import numpy as np
-    tot = 0
-    for l in range(0 if fine_smoother else 1, solver.n_levels):
-        cnt = np.bincount(solver.maps(l)[0])[1:]
-        if len(cnt) == 1:
-            tot += int(cnt[0])
-        else:
-            tot += int(cnt.sum()) * 2 * n_sweeps - n_sweeps * int(cnt[-1]) - (n_sweeps - 1) * int(cnt[0])
-    return tot
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
-def cpu_baseline(m, W, Winf, n_sweeps, n_cycles=1):
-    """The oracle, as it stands (single thread), on n_cycles V-cycles of the
-    same mesh.  Hierarchy build is setup, not timed."""
+def cpu_oracle_rate(H, W, Winf, n_sweeps, threads, n_cycles=1):
+    """The oracle's timing build (oracle.use_timing_build: -O3 -march=native,
+    OpenMP parallel-for within a color, built on this host) with `threads`
+    OpenMP threads: executed-equivalent sweep cell-updates per second over
+    n_cycles V-cycles (hierarchy build not timed).  The oracle runs every
+    phase of Algorithm 2, so its count is the nominal one."""
     import oracle
-    H = oracle.build_hierarchy(m, 3, 0.5)
+    oracle.use_timing_build(threads)
     opt = oracle.Options(n_sweeps=n_sweeps)
     t0 = time.perf_counter()
     oracle.vcycle(H, W, Winf, opt, n_cycles)
     dt = time.perf_counter() - t0
     cu = sum(e["level"].n for e in H[1:]) * 2 * n_sweeps * n_cycles
-    return {"value": cu / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n_cycles} V-cycle(s) of the same {m.n_cells}-cell mesh ({dt:.1f} s), "
-                      f"plain C oracle, 1 thread, host {os.cpu_count()} cores"}
+    return cu / dt, dt
+
+
+def cpu_baseline(m, W, Winf, n_sweeps):
+    """all host cores (the headline) and one thread, one V-cycle each"""
+    import oracle
+    H = oracle.build_hierarchy(m, 3, 0.5)
+    cores = os.cpu_count() or 1
+    v_all, t_all = cpu_oracle_rate(H, W, Winf, n_sweeps, cores)
+    v_one, t_one = cpu_oracle_rate(H, W, Winf, n_sweeps, 1)
+    oracle.use_parity_build()
+    return {"value": v_all, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"1 V-cycle of the same {m.n_cells}-cell mesh ({t_all:.2f} s), oracle timing build "
+                      f"(-O3 -march=native, OpenMP within a color), {cores} threads on {_cpu_model()}",
+            "single_thread": {"value": v_one, "cores": 1, "sample": f"1 V-cycle ({t_one:.2f} s), 1 thread"}}
 
 
 def dist_init(args):
@@ -251,6 +266,8 @@ def run_reference(args, ws, rank):
         m, W, Winf = workload(args.config)
     import oracle
     H = oracle.build_hierarchy(m, 3, 0.5, part=part)
+    cores = os.cpu_count() or 1
+    oracle.use_timing_build(cores)
     opt = oracle.Options(n_sweeps=args.n_sweeps)
     cu = sum(e["level"].n for e in H[1:]) * 2 * args.n_sweeps
     Wc = W
@@ -269,9 +286,9 @@ def run_reference(args, ws, rank):
             "data": "synthetic", "config": {"workload": f"config{args.config}: 3D sphere shell {m.n_cells} cells "
                                                       "(tet+prism), 3-level V-cycle, 6 MC-LU-SGS sweeps",
                                             "n_cells": m.n_cells},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{len(times)} V-cycles of config{args.config}{sample}, plain C oracle, "
-                                       "1 thread"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{len(times)} V-cycles of config{args.config}{sample}, oracle timing build "
+                                       f"(-O3 -march=native, OpenMP within a color), {cores} threads on {_cpu_model()}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -290,6 +307,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/cpu)")
     ap.add_argument("--no-next1", action="store_true", help="skip the NEXT-1 (third-order CGKS fine operator) line")
+    ap.add_argument("--p2p", type=int, default=0, help="N > 1: fused P2P halo over CUDA IPC instead of NCCL")
+    ap.add_argument("--l2-persist-mb", type=int, default=0, help="persisting-L2 set-aside for the W' records")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
     args.steps_ref = max(1, min(args.steps, 5))
@@ -320,23 +339,33 @@ def main():
         torch.distributed.broadcast_object_list(uid, src=0)
         t_setup = time.perf_counter()
         s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, part=part, nranks=ws, rank=rank,
-                       nccl_id=uid[0], setup_device=0 if args.profile_only else 1)
+                       nccl_id=uid[0], setup_device=0 if args.profile_only else 1, p2p=args.p2p,
+                       l2_persist_mb=args.l2_persist_mb)
         t_setup = time.perf_counter() - t_setup
         parallelism = (f"mesh partitioned over {ws} GPUs (RCB), "
-                       + ("fused P2P halo (CUDA IPC)" if os.environ.get("GMG_P2P", "0") == "1"
+                       + ("fused P2P halo (CUDA IPC)" if args.p2p
                           else "NCCL halo exchange per color, overlapped with the interior sweep"))
     else:
         m, W, Winf = workload(args.config, args.p_equiv)
         t_setup = time.perf_counter()
         # (--profile-only: host setup, so that an ncu launch list starts with the V-cycle kernels)
-        s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, setup_device=0 if args.profile_only else 1)
+        s = gmg.Solver(m, n_levels=3, device=local, n_sweeps=args.n_sweeps, setup_device=0 if args.profile_only else 1,
+                       l2_persist_mb=args.l2_persist_mb)
         t_setup = time.perf_counter() - t_setup
         parallelism = f"{ws} independent replicas" if ws > 1 else "single GPU"
     s.set_state(W, Winf)
     stream = torch.cuda.current_stream(dev)
     nv = s.nv
-    # global sweep cell-updates per V-cycle (all ranks' owned cells when partitioned)
-    cu_cycle = sweep_updates_per_cycle(s.sizes, args.n_sweeps, 0) * (ws if replicas else 1)
+    # global sweep cell-updates per V-cycle (all ranks' owned cells when partitioned): executed (the value) and
+    # Algorithm 2's nominal count (the repeated phase at each sweep turn is not run, gmg_options.skip_repeat)
+    nominal_cycle = sweep_updates_per_cycle(s.sizes, args.n_sweeps, 0) * (ws if replicas else 1)
+    cu_cycle = s.vcycle_visits()
+    if ws > 1 and not replicas:
+        t = torch.tensor([float(cu_cycle)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t)
+        cu_cycle = int(t.item())
+    elif replicas:
+        cu_cycle *= ws
 
     # warm-up (builds + replays the CUDA graph)
     for _ in range(args.warmup):
@@ -419,65 +448,53 @@ def main():
         timing_def = "isolated: CUDA events around each sweep launch of a V-cycle"
 
     # ---------------- e2e through the C ABI with pinned host buffers ----------
-    Wh = torch.from_numpy(W).pin_memory()
-    Wo = torch.empty_like(Wh).pin_memory()
+    # a dependent time loop driven from the host: step k+1's input IS step k's result, read back to pinned
+    # host memory (gmg_get_state synchronizes), then uploaded again (gmg_set_state)
     winf = np.ascontiguousarray(Winf)
-    for _ in range(2):
-        gmg.gmg_set_state(s.ctx, Wh, winf)
-        gmg.gmg_vcycle(s.ctx, 1, None)
-        gmg.gmg_get_state(s.ctx, 0, Wo)
-    e_steps = max(3, min(args.steps, 10))
+    e_steps = max(3, min(args.steps, 20))
+    if ws > 1 and not replicas:
+        own = s.halo(0, 0)["owned"]
+        bufs = [torch.from_numpy(np.ascontiguousarray(W[:, own])).pin_memory()]
+        bufs.append(torch.empty_like(bufs[0]).pin_memory())
+
+        def e2e_step(k):
+            gmg.gmg_set_state_owned_async(s.ctx, bufs[k % 2], winf)
+            gmg.gmg_vcycle_async(s.ctx, 1)
+            gmg.gmg_get_state_owned_async(s.ctx, bufs[(k + 1) % 2])
+            gmg.gmg_sync(s.ctx)
+        bscope = "per rank (owned cells)"
+    else:
+        bufs = [torch.from_numpy(W).pin_memory()]
+        bufs.append(torch.empty_like(bufs[0]).pin_memory())
+
+        def e2e_step(k):
+            gmg.gmg_set_state(s.ctx, bufs[k % 2], winf)
+            gmg.gmg_vcycle(s.ctx, 1, None)
+            gmg.gmg_get_state(s.ctx, 0, bufs[(k + 1) % 2])
+        bscope = "whole mesh"
+    for k in range(2):
+        e2e_step(k)
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(e_steps):
-        gmg.gmg_set_state(s.ctx, Wh, winf)
-        gmg.gmg_vcycle(s.ctx, 1, None)
-        gmg.gmg_get_state(s.ctx, 0, Wo)
+    for k in range(e_steps):
+        e2e_step(k)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e_steps
     if ws > 1:
         t = torch.tensor([e2e_s], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": cu_cycle / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(W.nbytes),
-           "d2h_bytes_per_step": int(W.nbytes + (nv * 2 * 8)),
-           "ms_per_step": e2e_s * 1e3, "timer": "host wall clock around synchronous ABI calls"}
-    if ws > 1 and not replicas:
-        # ranks: each rank copies only its owned cells' input and result (gmg_*_owned_async), pipelined
-        own = s.halo(0, 0)["owned"]
-        Wo_in = torch.from_numpy(np.ascontiguousarray(W[:, own])).pin_memory()
-        outs = [torch.empty_like(Wo_in).pin_memory() for _ in range(2)]
-        for k in range(2):
-            gmg.gmg_set_state_owned_async(s.ctx, Wo_in, winf)
-            gmg.gmg_vcycle_async(s.ctx, 1)
-            gmg.gmg_get_state_owned_async(s.ctx, outs[k % 2])
-        gmg.gmg_sync(s.ctx)
-        p_steps = max(10, min(args.steps, 50))
-        torch.distributed.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for k in range(p_steps):
-            gmg.gmg_set_state_owned_async(s.ctx, Wo_in, winf)
-            gmg.gmg_vcycle_async(s.ctx, 1)
-            gmg.gmg_get_state_owned_async(s.ctx, outs[k % 2])
-        gmg.gmg_sync(s.ctx)
-        pe_s = (time.perf_counter() - t0) / p_steps
-        t = torch.tensor([pe_s], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        pe_s = float(t.item())
-        e2e_sync = dict(e2e)
-        e2e = {"value": cu_cycle / pe_s, "unit": UNIT, "h2d_bytes_per_step": int(Wo_in.numel() * 8),
-               "d2h_bytes_per_step": int(Wo_in.numel() * 8), "bytes_scope": "per rank (owned cells)",
-               "ms_per_step": pe_s * 1e3, "steps": p_steps,
-               "timer": "host wall clock (max over ranks) over K steps of gmg_set_state_owned_async + "
-                        "gmg_vcycle_async + gmg_get_state_owned_async and one gmg_sync",
-               "synchronous": e2e_sync}
+    io_bytes = int(bufs[0].numel() * 8)
+    e2e = {"value": cu_cycle / e2e_s, "unit": UNIT, "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
+           "bytes_scope": bscope, "ms_per_step": e2e_s * 1e3, "steps": e_steps,
+           "timer": "host wall clock (max over ranks) over K dependent steps: set state from pinned host memory, "
+                    "one V-cycle, read the resulting state back to pinned host memory, which is the next input"}
     if ws == 1:
-        # pipelined through the public async ABI: every step still copies its input host->device and its
-        # result device->host, but step k+1's input copy and step k-1's result copy overlap step k's
-        # V-cycle (copy stream, double-buffered staging); one gmg_sync closes the timed region
+        # beside it: the pipelined throughput of INDEPENDENT inputs through the async ABI (copy streams,
+        # double-buffered staging): step k+1's input copy and step k-1's result copy overlap step k
+        Wh = bufs[0]
         outs = [torch.empty_like(Wh).pin_memory() for _ in range(2)]
         for k in range(2):
             gmg.gmg_set_state_async(s.ctx, Wh, winf)
@@ -493,12 +510,10 @@ def main():
             gmg.gmg_get_state_async(s.ctx, outs[k % 2])
         gmg.gmg_sync(s.ctx)
         pe_s = (time.perf_counter() - t0) / p_steps
-        e2e_sync = dict(e2e)
-        e2e = {"value": cu_cycle / pe_s, "unit": UNIT, "h2d_bytes_per_step": int(W.nbytes),
-               "d2h_bytes_per_step": int(W.nbytes), "ms_per_step": pe_s * 1e3, "steps": p_steps,
-               "timer": "host wall clock over K steps of gmg_set_state_async + gmg_vcycle_async + "
-                        "gmg_get_state_async (pinned host buffers) and one gmg_sync",
-               "synchronous": e2e_sync}
+        e2e["independent_inputs_pipelined"] = {
+            "value": cu_cycle / pe_s, "ms_per_step": pe_s * 1e3, "steps": p_steps,
+            "timer": "host wall clock over K steps of gmg_set_state_async + gmg_vcycle_async + gmg_get_state_async "
+                     "(pinned host buffers, the same input every step) and one gmg_sync"}
 
     next1 = None
     if ws == 1 and not args.no_next1 and args.config == 4:
@@ -507,7 +522,7 @@ def main():
         return 0
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        cpu = cpu_baseline(m, W, Winf, args.n_sweeps, 1)
+        cpu = cpu_baseline(m, W, Winf, args.n_sweeps)
     ws_bytes = int(s.ws.numel())
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -516,20 +531,22 @@ def main():
         "config": {"workload": f"config{args.config}: 3D sphere shell, {m.n_cells} cells "
                                f"({m.meta['cell_type_counts']}), 3-level V-cycle, {args.n_sweeps} MC-LU-SGS sweeps",
                    "levels": [{"cells": int(n), "colors": int(c), "faces": int(f)} for (n, c, f) in s.sizes],
-                   "sweep_cell_updates_per_vcycle": int(cu_cycle),
-                   "sweep_cell_visits_executed_per_vcycle": int(sweep_cells_executed_per_cycle(s, args.n_sweeps, 0))
-                   * (ws if replicas else 1),
+                   "sweep_cell_updates_executed_per_vcycle": int(cu_cycle),
+                   "sweep_cell_updates_nominal_per_vcycle": int(nominal_cycle),
+                   "value_def": "executed sweep cell-updates (the repeated phase at each sweep turn is not run, "
+                                "gmg_options.skip_repeat) / device time per V-cycle",
                    "l2": f"inputs larger than L2: workspace {ws_bytes / 1e9:.2f} GB >> 126 MB",
                    "parallelism": parallelism,
                    "setup_s": round(t_setup, 3),
                    "setup": "hierarchy with device-side Algorithms 1 and 3 (bit-identical to the host setup), "
                             "not timed",
                    "n_gpus_partitions": 1 if replicas else ws},
+        "nominal_value": nominal_cycle / (ms_step * 1e-3),
         "vcycles_per_s": 1e3 / ms_step * (ws if replicas else 1),
         "fine_cell_vcycles_per_s": m.n_cells * 1e3 / ms_step * (ws if replicas else 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_sweep128<3, LPC> (per-color MC-LU-SGS sweep)",
+                     "kernel": "k_sweep<3, LPC, FF> (per-color MC-LU-SGS sweep, W' formulation)",
                      "avg_launch_ms": sweep_ms_avg, "peak_source": peak_src, "timing": timing_def,
                      "isolated": {"avg_launch_ms": sweep_ms_isolated, "achieved": achieved_isolated,
                                   "frac": (achieved_isolated / peak) if achieved_isolated else None},
@@ -537,8 +554,10 @@ def main():
                      # the in-step DRAM bytes) / live launch time
                      "traffic_GBs": (traffic / (sweep_ms_avg * 1e-3) / 1e9) if traffic and sweep_ms_avg else None,
                      "traffic_frac": (traffic / (sweep_ms_avg * 1e-3) / 1e9 / peak) if traffic and sweep_ms_avg else None,
-                     "bytes_def": "algorithmic: own Rt, 1/D, alpha/2, dW write + neighbour-unique W, dW + "
-                                  "face data once per face + 4 B/slot (DESIGN.md)"},
+                     "bytes_def": "algorithmic, SURVEY §8(d): per cell-update own Rt, 1/D, alpha/2, dW write + "
+                                  "neighbour-unique W, dW + face data once per face + 4 B/slot; first forward "
+                                  "half-sweep: only the slots (and the share of the neighbour term) of earlier-"
+                                  "color neighbours, whose increments are nonzero (DESIGN.md §8)"},
         "kernels": kernels, "sweep_only": sweep_only,
         "gpu_launches": int(launches_per_cycle * args.steps + 2),
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,

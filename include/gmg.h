@@ -110,6 +110,29 @@ typedef struct {
                                defaults 0.05, 1.0                                              */
     double ho_gam0;         /* C5 linear weight of the large (p2) stencil; default 0.95        */
     double ho_eps;          /* C5 WENO-Z epsilon; default 1e-14                                */
+    /* execution choices (no effect on the results beyond rounding) */
+    int skip_repeat;        /* 1 (default): the color phase that directly repeats the previous
+                               one at every sweep turn of Algorithm 2 (c_N forward then c_N
+                               backward, c_1 backward then c_1 forward) is not run -- it reads
+                               only other-colored neighbours, none of which changed, so it
+                               recomputes identical values (exact); 0 runs every phase.        */
+    int p2p;                /* partitioned runs: 1 = fused halo, the sweep epilogue stores a
+                               boundary cell's new state into the peers' ghost records over
+                               peer memory (CUDA IPC between ranks, gmg_p2p_layout/_import);
+                               0 (default) = pack / NCCL send-recv (device copies between local
+                               domains) / unpack after every color.                           */
+    int overlap;            /* partitioned runs: 1 = sweep a color's boundary cells, exchange
+                               them on a side stream while its interior cells are swept; 0 =
+                               sweep, then exchange; -1 (default) = 1 for NCCL ranks, 0 for
+                               local domains.                                                 */
+    int l2_persist_mb;      /* > 0: set aside this many MB of L2 as persisting and attach an
+                               access-policy window over the gathered W' records to the sweep
+                               launches (the previous device limit is restored and the
+                               persisting lines reset by gmg_destroy); 0 (default) = off.      */
+    int sweep_lanes;        /* lanes per cell of the sweep kernel for the large color blocks:
+                               1, 2 (default; 0 = default) or 4                                */
+    int pdl;                /* 1 (default): programmatic dependent launch between the kernels
+                               of a V-cycle; 0 = plain stream order                            */
 } gmg_options;
 
 /* Fill *o with the defaults above (dim = 3, single rank, device 0, stream 0). */
@@ -173,6 +196,20 @@ gmg_status gmg_set_level_state(gmg_ctx *ctx, int level, const double *W);
  * a V-cycle this is W0 + dW before prolongation. */
 gmg_status gmg_get_state(gmg_ctx *ctx, int level, double *W_out);
 
+/* Tests / inspection: one per-cell field of a level after the last call that
+ * produced it, natural order, out[ncomp][n_level] (host/device):
+ *   GMG_FIELD_W     the level's state W (nv comps; coarse: W0 + dW after a V-cycle)
+ *   GMG_FIELD_W0    the linearisation state of the level's last smoothing step
+ *                   (coarse: the restricted W0 of P:643-647)            (nv)
+ *   GMG_FIELD_DW    the increment dW of the last smoothing step         (nv)
+ *   GMG_FIELD_RS    the restricted residual Res*             (nv)
+ *   GMG_FIELD_F     the forcing F = Res* - R(W0)            (nv)
+ *   GMG_FIELD_RT    the level's last right-hand side / residual buffer  (nv)
+ *   GMG_FIELD_ALPHA the level's DF alpha (coarse: min over children)    (1) */
+enum { GMG_FIELD_W = 0, GMG_FIELD_W0 = 1, GMG_FIELD_DW = 2, GMG_FIELD_RS = 3, GMG_FIELD_F = 4, GMG_FIELD_RT = 5,
+       GMG_FIELD_ALPHA = 6 };
+gmg_status gmg_get_level_field(gmg_ctx *ctx, int level, int field, double *out);
+
 /* df_mode 1: fine-level DF alpha[n] (natural order, host/device). */
 gmg_status gmg_set_alpha(gmg_ctx *ctx, const double *alpha);
 
@@ -209,7 +246,8 @@ gmg_status gmg_vcycle(gmg_ctx *ctx, int n_cycles, double *res_hist);
  * (GMG_K_* below).  bytes_out[k] = algorithmic bytes moved by class k over
  * the run.  Arrays of length GMG_K_COUNT. */
 enum { GMG_K_FACE = 0, GMG_K_GATHER = 1, GMG_K_SWEEP = 2, GMG_K_RESTRICT = 3, GMG_K_PROLONG = 4,
-       GMG_K_NORM = 5, GMG_K_HO_RECON = 6, GMG_K_HO_FLUX = 7, GMG_K_COUNT = 8 };
+       GMG_K_NORM = 5, GMG_K_HO_RECON = 6, GMG_K_HO_FLUX = 7, GMG_K_HALO = 8, GMG_K_COUNT = 9 };
+/* (GMG_K_HALO: halo pack / unpack and ghost-record kernels of partitioned runs) */
 gmg_status gmg_profile_vcycle(gmg_ctx *ctx, int n_cycles, double *ms_out, int64_t *count_out, double *bytes_out);
 
 /* Sweep-only instrumentation: time one smoothing step's sweeps on `level`
@@ -249,6 +287,9 @@ gmg_status gmg_get_state_owned_async(gmg_ctx *ctx, double *W_owned_out);
 
 /* Number of kernels one V-cycle launches (graph nodes). */
 int64_t gmg_vcycle_launches(gmg_ctx *ctx);
+/* Sweep cell-updates (one cell's increment solved once) EXECUTED per V-cycle
+ * (the repeated phases dropped by skip_repeat are not counted). */
+int64_t gmg_vcycle_visits(gmg_ctx *ctx);
 
 /* a5: recursive coordinate bisection of the cell centroids (host, natural
  * order; centroid[dim][n]) into nparts partitions -> part_out[n] in

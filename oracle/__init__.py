@@ -31,11 +31,57 @@ _lib = None
 
 
 def build(force: bool = False) -> str:
+    """The parity build: -O2 -ffp-contract=off, sequential (the OpenMP pragmas are ignored)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC),
                                                                           os.path.getmtime(_SRC3)):
         subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
                                "-shared", "-o", _LIB, _SRC, _SRC3, "-lm"])
     return _LIB
+
+
+def build_timing() -> str:
+    """The timing build (bench.py's CPU baseline only): the same sources with
+    -O3 -march=native -fopenmp -ffp-contract=off, compiled on THIS host (the
+    -march=native code is host specific) into the temp directory, keyed by the
+    sources and the CPU model.  Same results bit for bit as the parity build
+    (tests/test_oracle_timing.py)."""
+    import hashlib
+    import tempfile
+    h = hashlib.sha1()
+    for f in (_SRC, _SRC3):
+        h.update(open(f, "rb").read())
+    try:
+        h.update(open("/proc/cpuinfo", "rb").read().split(b"\n\n")[0])
+    except OSError:
+        pass
+    out = os.path.join(tempfile.gettempdir(), f"liboracle_timing_{h.hexdigest()[:16]}.so")
+    if not os.path.exists(out):
+        tmp = out + f".{os.getpid()}"
+        subprocess.check_call(["gcc", "-O3", "-march=native", "-fopenmp", "-std=gnu11", "-ffp-contract=off",
+                               "-fno-fast-math", "-fPIC", "-shared", "-o", tmp, _SRC, _SRC3, "-lm"])
+        os.replace(tmp, out)
+    return out
+
+
+_parity_lib = None
+
+
+def use_timing_build(threads: int):
+    """Route the wrappers below to the timing build with `threads` OpenMP threads."""
+    global _lib, _parity_lib
+    if _parity_lib is None:
+        _parity_lib = lib()
+    L = C.CDLL(build_timing())
+    _declare(L)
+    L.omp_set_num_threads.argtypes = [C.c_int]
+    L.omp_set_num_threads(int(threads))
+    _lib = L
+
+
+def use_parity_build():
+    global _lib
+    if _parity_lib is not None:
+        _lib = _parity_lib
 
 
 class OrcLevel(C.Structure):
@@ -52,8 +98,14 @@ class OrcLevelOut(C.Structure):
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
-        L = _lib
+        L = C.CDLL(build())
+        _declare(L)
+        _lib = L
+    return _lib
+
+
+def _declare(L):
+    if True:
         P = C.c_void_p
         L.orc_color.restype = C.c_int
         L.orc_color.argtypes = [C.c_int64, C.c_int64, P, P, P]
@@ -85,7 +137,6 @@ def lib():
         L.orc_restrict.argtypes = [C.c_int64, C.c_int64, C.c_int, P, P, P, P, P, P, P, P, P]
         L.orc_prolong.restype = None
         L.orc_prolong.argtypes = [C.c_int64, C.c_int64, C.c_int, P, P, P, P, P]
-    return _lib
 
 
 def _p(a):

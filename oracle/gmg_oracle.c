@@ -13,6 +13,13 @@
  * floating-point decisions of the agglomeration (skewness test) are exactly
  * the expressions written below.
  *
+ * Timing build (bench.py cpu_baseline / --impl reference only): the same
+ * source with -O3 -march=native -fopenmp -ffp-contract=off.  The OpenMP
+ * pragmas below parallelise only loops whose iterations are independent
+ * (cells of ONE color in the sweep, per-face flux evaluations, per-cell
+ * updates); every sum keeps its sequential order, so the timing build
+ * returns the same bits as the parity build (tests/test_oracle_timing.py).
+ *
  * Citations: "P:n" = /root/reference/PAPER.md line n; "S:n" = SPEC.md line
  * n; "O#" / "A#" = the SURVEY.md §8(c) oracle step / reading adopted (also
  * listed in DESIGN.md "Readings").
@@ -473,13 +480,17 @@ void orc_residual(const orc_level *L, double gamma, double omega, const double *
                   double *R, double *alpha, double *Sigma, double *rf)
 {
     int dim = L->dim, nv = dim + 2;
-    int64_t n = L->n;
-    for (int q = 0; q < nv; ++q) for (int64_t i = 0; i < n; ++i) R[q * n + i] = 0.0;
-    for (int64_t i = 0; i < n; ++i) { if (alpha) alpha[i] = 1.0; if (Sigma) Sigma[i] = 0.0; }
-    for (int64_t f = 0; f < L->nf; ++f) {
+    int64_t n = L->n, nf = L->nf;
+    /* per face: S, S F (flux, KFVS), r, alpha_f^{M_f} -- independent evaluations */
+    double *fS = malloc(sizeof(double) * (size_t)(nf + 1));
+    double *fF = malloc(sizeof(double) * (size_t)(nv * nf + 1));
+    double *fr = malloc(sizeof(double) * (size_t)(nf + 1));
+    double *fa = malloc(sizeof(double) * (size_t)(nf + 1));
+#pragma omp parallel for schedule(static)
+    for (int64_t f = 0; f < nf; ++f) {
         int64_t l = L->left[f], r = L->right[f];
         double A[3] = {0, 0, 0}, nn[3] = {0, 0, 0};
-        for (int k = 0; k < dim; ++k) A[k] = L->avec[k * L->nf + f];
+        for (int k = 0; k < dim; ++k) A[k] = L->avec[k * nf + f];
         double S = 0.0;
         for (int k = 0; k < dim; ++k) S += A[k] * A[k];
         S = sqrt(S);
@@ -489,20 +500,31 @@ void orc_residual(const orc_level *L, double gamma, double omega, const double *
         if (r >= 0) for (int q = 0; q < nv; ++q) WR[q] = W[q * n + r];
         else ghost_state(dim, L->patch_kind[-r - 1], WL, Winf, nn, WR);
         orc_kfvs_flux(dim, gamma, WL, WR, nn, F);
-        double rr = orc_spectral_radius(dim, gamma, omega, WL, WR, nn);
         double af = orc_df_face(dim, gamma, WL, WR, nn);
         double afM = 1.0;
         for (int g = 0; g < L->ngauss[f]; ++g) afM *= af;
+        fS[f] = S;
+        for (int q = 0; q < nv; ++q) fF[q * nf + f] = F[q];
+        fr[f] = orc_spectral_radius(dim, gamma, omega, WL, WR, nn);
+        fa[f] = afM;
+    }
+    /* assembly in face order: R_i = sum_f sigma_if S_f F_f, Sigma_i = sum_f S_f r_f, alpha_i = prod_f alpha_f^M_f */
+    for (int q = 0; q < nv; ++q) for (int64_t i = 0; i < n; ++i) R[q * n + i] = 0.0;
+    for (int64_t i = 0; i < n; ++i) { if (alpha) alpha[i] = 1.0; if (Sigma) Sigma[i] = 0.0; }
+    for (int64_t f = 0; f < nf; ++f) {
+        int64_t l = L->left[f], r = L->right[f];
+        double S = fS[f], rr = fr[f], afM = fa[f];
         if (rf) rf[f] = rr;
-        for (int q = 0; q < nv; ++q) R[q * n + l] += S * F[q];
+        for (int q = 0; q < nv; ++q) R[q * n + l] += S * fF[q * nf + f];
         if (Sigma) Sigma[l] += S * rr;
         if (alpha) alpha[l] *= afM;
         if (r >= 0) {
-            for (int q = 0; q < nv; ++q) R[q * n + r] -= S * F[q];
+            for (int q = 0; q < nv; ++q) R[q * n + r] -= S * fF[q * nf + f];
             if (Sigma) Sigma[r] += S * rr;
             if (alpha) alpha[r] *= afM;
         }
     }
+    free(fS); free(fF); free(fr); free(fa);
 }
 
 /* O6. DF-hybrid diagonal (Eq.(gpu-forward-relaxation) P:538 with readings */
@@ -512,6 +534,7 @@ void orc_residual(const orc_level *L, double gamma, double omega, const double *
 /* Pins: S:453 -> 11; alpha = 0 -> V/Dt_exp; alpha = 1 -> V/Dt + Sigma/2.  */
 void orc_diag(int64_t n, const double *Sigma, const double *alpha, double cfl_imp, double cfl_exp, double *D)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i)
         D[i] = alpha[i] * (Sigma[i] / cfl_imp + 0.5 * Sigma[i]) + (1.0 - alpha[i]) * (Sigma[i] / cfl_exp);
 }
@@ -544,6 +567,8 @@ void orc_smooth(const orc_level *L, double gamma, const double *W, const double 
         for (int half = 0; half < 2; ++half) {
             for (int cc = 0; cc < ncolor; ++cc) {
                 int c = half == 0 ? cc + 1 : ncolor - cc;      /* forward 1..Nc, backward Nc..1 */
+                /* cells of one color never neighbour each other: independent updates */
+#pragma omp parallel for schedule(dynamic, 256)
                 for (int64_t i = 0; i < n; ++i) {
                     if (color[i] != c) continue;
                     double sum[5] = {0, 0, 0, 0, 0};
@@ -582,6 +607,7 @@ void orc_smooth(const orc_level *L, double gamma, const double *W, const double 
 /* Dt_exp = CFL_exp V / Sigma.                                             */
 void orc_explicit_update(int64_t n, int nv, double cfl_exp, const double *Sigma, const double *R, double *W)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i)
         for (int q = 0; q < nv; ++q) W[q * n + i] = W[q * n + i] - (cfl_exp / Sigma[i]) * R[q * n + i];
 }
@@ -620,6 +646,7 @@ void orc_restrict(int64_t nfine, int64_t nc, int nv, const int64_t *parent, cons
 void orc_prolong(int64_t nfine, int64_t nc, int nv, const int64_t *parent, const double *alpha_f,
                  const double *Wc, const double *W0c, double *Wf)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < nfine; ++i) {
         int64_t c = parent[i];
         for (int q = 0; q < nv; ++q)

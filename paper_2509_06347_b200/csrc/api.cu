@@ -16,7 +16,7 @@
 
 #include "gmg_internal.h"
 #include "kernels.cuh"
-#include "kernels_tried.cuh"
+#include "p2p_emulate.cuh"
 
 namespace gmg {
 // ho.cu (NEXT-1): which = 0 k_ho_sr, 1 k_ho_recon, 2 k_ho_flux, 3 k_ho_gather(mode)
@@ -141,7 +141,7 @@ void klaunch(gmg_ctx *ctx, void (*k)(KP...), dim3 g, dim3 b, cudaStream_t s, A..
     cfg.blockDim = b;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
-    if (ctx->pdl) {
+    if (ctx->opt.pdl) {
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
@@ -150,17 +150,16 @@ void klaunch(gmg_ctx *ctx, void (*k)(KP...), dim3 g, dim3 b, cudaStream_t s, A..
     cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-constexpr int kRecStride = 12;   // Rec<2>::STRIDE == Rec<3>::STRIDE
-
 // prep: the launch also writes the sweep slot records (A outward | S r) of
-// both cells of every interior face (whole 32-byte records)
+// both cells of every interior face (whole 32-byte records).  from_rec: W is
+// a W_lin array (stride Wp<D>::STRIDE), else a state array (stride nv)
 template <int D>
 void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, bool from_rec, bool df = false,
                   bool prep = false)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
-    constexpr int RS = Rec<D>::STRIDE, NV = D + 2;
+    constexpr int RS = Wp<D>::STRIDE, NV = D + 2;
     Lc.pre(GMG_K_FACE);
     const dim3 g(nblk(L.nf)), b(256);
     const Phys ph = phys(ctx);
@@ -216,10 +215,10 @@ void enqueue_norm_hist(Launcher &Lc)
 }
 
 // --------------------------------------------------------------------------
-// halo exchange (a13).  kind: increments of one color, record W_lin (+ dW
-// = 0) of all colors, or the state W of all colors.
+// halo exchange (a13).  kind: the W' of one color (after its sweep phase),
+// W_lin of all colors (the ghosts' W' set to it), or the state W of all colors.
 // --------------------------------------------------------------------------
-enum { EX_DW = 0, EX_WLIN = 1, EX_W = 2 };
+enum { EX_WP = 0, EX_WLIN = 1, EX_W = 2 };
 
 template <int D>
 void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
@@ -227,12 +226,10 @@ void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
     gmg_ctx *ctx = Lc.ctx;
     if (ctx->nparts <= 1) return;
     constexpr int NV = D + 2;
-    using RC = Rec<D>;
     const int ncolor = ctx->lv[l].ncolor;
-    int stride = RC::STRIDE, offset = RC::DW, zero_at = 0, nzero = 0;
-    if (kind == EX_WLIN) { offset = RC::W; zero_at = RC::DW; nzero = NV; }
-    if (kind == EX_W) { stride = NV; offset = 0; }
-    auto src_of = [&](DevLevel &L) { return kind == EX_W ? L.W : L.rec; };
+    const int stride = kind == EX_W ? NV : Wp<D>::STRIDE, offset = 0;
+    auto src_of = [&](DevLevel &L) { return kind == EX_W ? L.W : kind == EX_WLIN ? L.wlin : L.wp; };
+    auto dst2_of = [&](DevLevel &L) { return kind == EX_WLIN ? L.wp : (double *)nullptr; };
     auto grange = [&](const DomLevel &H, int &g0, int &g1) {
         const int np = (int)H.peers.size();
         g0 = color >= 0 ? color * np : 0;
@@ -246,10 +243,10 @@ void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
         grange(H, g0, g1);
         const int64_t s0 = H.send_off[g0], s1 = H.send_off[g1];
         if (s1 > s0) {
-            Lc.pre(GMG_K_NORM);
+            Lc.pre(GMG_K_HALO);
             klaunch(Lc.ctx, k_pack, dim3(nblk(s1 - s0)), dim3(256), Lc.s, (int)(s1 - s0), L.send_idx + s0, src_of(L), stride, offset, NV,
                                                    L.sendbuf + s0 * NV);
-            Lc.post(GMG_K_NORM, (double)(s1 - s0) * NV * 16);
+            Lc.post(GMG_K_HALO, (double)(s1 - s0) * NV * 16);
         }
     }
     // transport
@@ -295,10 +292,10 @@ void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
         grange(H, g0, g1);
         const int64_t r0 = H.recv_off[g0], r1 = H.recv_off[g1];
         if (r1 > r0) {
-            Lc.pre(GMG_K_NORM);
+            Lc.pre(GMG_K_HALO);
             klaunch(Lc.ctx, k_unpack, dim3(nblk(r1 - r0)), dim3(256), Lc.s, (int)(r1 - r0), L.recv_idx + r0, L.recvbuf + r0 * NV,
-                                                     src_of(L), stride, offset, NV, zero_at, nzero);
-            Lc.post(GMG_K_NORM, (double)(r1 - r0) * NV * 16);
+                                                     src_of(L), stride, offset, NV, dst2_of(L));
+            Lc.post(GMG_K_HALO, (double)(r1 - r0) * NV * (kind == EX_WLIN ? 24 : 16));
         }
     }
     ctx->exchanges++;
@@ -310,9 +307,9 @@ void enqueue_ghost_wlin(Launcher &Lc, int l)
     for (Domain &dm : Lc.ctx->dom) {
         DevLevel &L = dm.dv[l];
         if (L.n_loc > L.n) {
-            Lc.pre(GMG_K_NORM);
-            klaunch(Lc.ctx, k_ghost_wlin<D>, dim3(nblk(L.n_loc - L.n)), dim3(256), Lc.s, L.n, L.n_loc, L.W, L.rec);
-            Lc.post(GMG_K_NORM, 0.0);
+            Lc.pre(GMG_K_HALO);
+            klaunch(Lc.ctx, k_ghost_wlin<D>, dim3(nblk(L.n_loc - L.n)), dim3(256), Lc.s, L.n, L.n_loc, L.W, L.wlin, L.wp);
+            Lc.post(GMG_K_HALO, (double)(L.n_loc - L.n) * (D + 2) * 24);
         }
     }
 }
@@ -323,9 +320,9 @@ void enqueue_ghost_w(Launcher &Lc, int l)
     for (Domain &dm : Lc.ctx->dom) {
         DevLevel &L = dm.dv[l];
         if (L.n_loc > L.n) {
-            Lc.pre(GMG_K_NORM);
-            klaunch(Lc.ctx, k_ghost_w<D>, dim3(nblk(L.n_loc - L.n)), dim3(256), Lc.s, L.n, L.n_loc, L.rec, L.W);
-            Lc.post(GMG_K_NORM, 0.0);
+            Lc.pre(GMG_K_HALO);
+            klaunch(Lc.ctx, k_ghost_w<D>, dim3(nblk(L.n_loc - L.n)), dim3(256), Lc.s, L.n, L.n_loc, L.wp, L.W);
+            Lc.post(GMG_K_HALO, (double)(L.n_loc - L.n) * (D + 2) * 16);
         }
     }
 }
@@ -333,13 +330,11 @@ void enqueue_ghost_w(Launcher &Lc, int l)
 // --------------------------------------------------------------------------
 // sweeps
 // --------------------------------------------------------------------------
-// optional L2 access-policy window over the level's cell records (the
-// gathered data), attached per launch so that graph capture keeps it
-// sweep grid cap = resident waves x SMs x blocks/SM (set in gmg_set_workspace; 0 = one thread per cell)
-
+// optional persisting-L2 access-policy window over the level's W' records
+// (the gathered data), attached per launch so that graph capture keeps it
 template <class K>
 void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArgs &a, const void *win, size_t win_bytes,
-                        bool pdl, float hit = 1.0f)
+                        bool pdl)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = g;
@@ -351,7 +346,7 @@ void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArg
         at[na].id = cudaLaunchAttributeAccessPolicyWindow;
         at[na].val.accessPolicyWindow.base_ptr = const_cast<void *>(win);
         at[na].val.accessPolicyWindow.num_bytes = win_bytes;
-        at[na].val.accessPolicyWindow.hitRatio = hit;
+        at[na].val.accessPolicyWindow.hitRatio = 1.0f;
         at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         ++na;
@@ -366,131 +361,90 @@ void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArg
     cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
-template <int D, int LPC>
-void launch_sweep(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, const void *win, size_t win_bytes)
+// lanes per cell of a color block: the configured lanes for large blocks; a
+// block that still fits one resident wave at twice the lanes gets them (up to
+// 16) -- small trailing colors are latency chains of ceil(deg/LPC) gathers
+int sweep_lpc(const gmg_ctx *ctx, int64_t cells)
 {
-    const int minb = ctx->minb, sweep_var = ctx->sweep_var;
-    const bool pdl = ctx->pdl != 0;
-    // a window larger than the set-aside persists that fraction of its lines (GMG_L2FULL)
-    const float hit = (ctx->l2_window && win_bytes > ctx->l2_window) ? (float)((double)ctx->l2_window / (double)win_bytes) : 1.0f;
+    int lpc = ctx->lpc;
+    if (ctx->adapt_lpc && ctx->sweep_grid_cap > 0) {
+        const int64_t wave = (int64_t)ctx->sweep_grid_cap * 128;
+        while (lpc < 16 && cells * lpc * 2 <= wave) lpc *= 2;
+    }
+    return lpc;
+}
+
+template <int D, int LPC, bool FF>
+void launch_sweep_lpc(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, const void *win, size_t win_bytes)
+{
     const int64_t nthreads = (int64_t)(a.cend - a.cbeg) * LPC;
-    if (ctx->sweep_bs == 64 && sweep_var == 3 && minb == 4) {   // GMG_SWEEP_BS=64: 16 blocks of 64 per SM
-        int nb = (int)((nthreads + 63) / 64);
-        if (ctx->sweep_grid_cap > 0) nb = std::min(nb, 4 * ctx->sweep_grid_cap);
-        launch_with_window(k_sweep64<D, LPC>, dim3(nb), dim3(64), s, a, win, win_bytes, pdl, hit);
-        return;
+    int nb = (int)((nthreads + 127) / 128);
+    const int cap = FF ? ctx->sweep_grid_cap_ff : ctx->sweep_grid_cap;
+    if (cap > 0) nb = std::min(nb, cap);
+    launch_with_window(k_sweep<D, LPC, FF>, dim3(std::max(nb, 1)), dim3(128), s, a, win, win_bytes, ctx->opt.pdl != 0);
+}
+
+template <int D, bool FF>
+void launch_sweep(const gmg_ctx *ctx, const SweepArgs &a, int lpc, cudaStream_t s, const void *win, size_t win_bytes)
+{
+    switch (lpc) {
+        case 1: launch_sweep_lpc<D, 1, FF>(ctx, a, s, win, win_bytes); break;
+        case 4: launch_sweep_lpc<D, 4, FF>(ctx, a, s, win, win_bytes); break;
+        case 8: launch_sweep_lpc<D, 8, FF>(ctx, a, s, win, win_bytes); break;
+        case 16: launch_sweep_lpc<D, 16, FF>(ctx, a, s, win, win_bytes); break;
+        default: launch_sweep_lpc<D, 2, FF>(ctx, a, s, win, win_bytes); break;
     }
-    if (ctx->sweep_bs == 128 && sweep_var == 3 && minb == 9) {   // GMG_MINB=9: 9 blocks of 128 per SM (56 registers)
-        int nb = (int)((nthreads + 127) / 128);
-        if (ctx->sweep_grid_cap > 0) nb = std::min(nb, (9 * ctx->sweep_grid_cap) / 4);
-        launch_with_window(k_sweep128<D, LPC, 3 | 8, 9>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
-        return;
-    }
-    if (ctx->sweep_bs == 128 && (sweep_var == 3 || sweep_var == 19 || sweep_var == 35) && minb == 4) {   // default; the variants run at 256
-        int nb = (int)((nthreads + 127) / 128);
-        if (ctx->sweep_grid_cap > 0) nb = std::min(nb, 2 * ctx->sweep_grid_cap);
-        if (sweep_var == 19) launch_with_window(k_sweep128<D, LPC, 3 | 8 | 16>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
-        else if (sweep_var == 35) launch_with_window(k_sweep128<D, LPC, 3 | 8 | 32>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
-        else launch_with_window(k_sweep128<D, LPC>, dim3(nb), dim3(128), s, a, win, win_bytes, pdl, hit);
-        return;
-    }
-    int nb = nblk(nthreads);
-    if (ctx->sweep_grid_cap > 0) nb = std::min(nb, ctx->sweep_grid_cap);
-    const dim3 g(nb), b(256);
-    // variants kept for the record; 3 is the default
-    if (sweep_var == 0) { launch_with_window(k_sweep<D, LPC, 4, 0>, g, b, s, a, win, win_bytes, pdl); return; }
-    if (sweep_var == 1) { launch_with_window(k_sweep<D, LPC, 4, 1>, g, b, s, a, win, win_bytes, pdl); return; }
-    if (sweep_var == 2) { launch_with_window(k_sweep<D, LPC, 4, 2>, g, b, s, a, win, win_bytes, pdl); return; }
-    if (sweep_var == 7) { launch_with_window(k_sweep<D, LPC, 4, 7>, g, b, s, a, win, win_bytes, pdl); return; }
-    switch (minb) {
-        case 6: launch_with_window(k_sweep<D, LPC, 6>, g, b, s, a, win, win_bytes, pdl); break;
-        case 8: launch_with_window(k_sweep<D, LPC, 8>, g, b, s, a, win, win_bytes, pdl); break;
-        default: launch_with_window(k_sweep<D, LPC, 4>, g, b, s, a, win, win_bytes, pdl); break;
-    }
+}
+
+SweepArgs sweep_args(const gmg_ctx *ctx, DevLevel &L, const DomLevel &H, int c, int b0, int b1, const double *rhs,
+                     double *Wout)
+{
+    SweepArgs a;
+    a.cbeg = b0;
+    a.cend = b1;
+    a.lo = c >= 0 ? (int)H.blk[c] : 0;
+    a.n_own = (int)H.n_own;
+    a.gm1 = ctx->opt.gamma - 1.0;
+    a.sinfo = L.sinfo;
+    a.sJe = L.sJe;
+    a.sRe = L.sRe;
+    a.wp = L.wp;
+    a.xr = L.xr;
+    a.wlin = L.wlin;
+    a.rhs = rhs;
+    a.dc = L.dc;
+    a.Wout = Wout;
+    return a;
 }
 
 // one color block of one domain (Eq.(gpu-forward-relaxation) / (gpu-backward-relaxation))
 // part: 0 = whole block, 1 = its boundary cells (ghost neighbours), 2 = its interior cells
-// first_fwd: a phase of the first forward half-sweep of a smoothing step --
-// owned neighbours of later colors still hold dW = +0 (zeroed before the
-// step), so their terms are exactly +0 and the kernel skips them
+// ff: a phase of the first forward half-sweep of a smoothing step (k_sweep<.., FF>)
 template <int D>
-void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout, int part = 0,
-                         bool first_fwd = false)
+void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout, int part, bool ff)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
     const DomLevel &H = dm.lv[l];
     int b0 = (int)H.blk[c], b1 = (int)H.blk[c + 1];
-    const int zlo = (first_fwd && ctx->skip_zero) ? (int)H.blk[c + 1] : 0;
-    const int zhi = (first_fwd && ctx->skip_zero) ? (int)H.n_own : 0;
+    double frac = 1.0;
     if (part) {
         const int mid = b0 + (int)H.nbnd[c];
-        const double frac = b1 > b0 ? (double)(part == 1 ? mid - b0 : b1 - mid) / (b1 - b0) : 0.0;
+        frac = b1 > b0 ? (double)(part == 1 ? mid - b0 : b1 - mid) / (b1 - b0) : 0.0;
         if (part == 1) b1 = mid;
         else b0 = mid;
-        SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs, Wout, zlo, zhi};
-        if (b1 <= b0) return;
-        Lc.pre(GMG_K_SWEEP);
-        switch (ctx->lpc) {
-            case 1: launch_sweep<D, 1>(ctx, a, Lc.s, nullptr, 0); break;
-            case 4: launch_sweep<D, 4>(ctx, a, Lc.s, nullptr, 0); break;
-            default: launch_sweep<D, 2>(ctx, a, Lc.s, nullptr, 0); break;
-        }
-        Lc.post(GMG_K_SWEEP, frac * (dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0)));
-        return;
     }
-    SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs, Wout, zlo, zhi};
-    if (a.cend <= a.cbeg) return;
+    if (b1 <= b0) return;
+    const SweepArgs a = sweep_args(ctx, L, H, c, b0, b1, rhs, Wout);
+    const void *win = ctx->l2_window ? (const void *)L.wp : nullptr;
+    const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * Wp<D>::STRIDE * 8) : 0;
+    const int lpc = part ? ctx->lpc : sweep_lpc(ctx, b1 - b0);
     Lc.pre(GMG_K_SWEEP);
-    if (ctx->pipe) {
-        PipeLayout pl{dm.lbytes[l].max_pipe};
-        const size_t smem = (size_t)kPW * pl.warp() * sizeof(double);
-        const int nb = (a.cend - a.cbeg + kPB - 1) / kPB;
-        int per_sm = 0, nsm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_pipe<D>, kPW * 32, smem);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
-        const int grid = std::max(1, std::min((nb + kPW - 1) / kPW, nsm * std::max(per_sm, 1)));
-        k_sweep_pipe<D><<<grid, kPW * 32, smem, Lc.s>>>(a, pl);
-        Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
-        return;
-    }
-    if (ctx->spsweep) {
-        const int64_t g0 = H.sp_off[c], ng = H.sp_off[c + 1] - g0 - 1;
-        klaunch(ctx, k_sweep_sp<D>, dim3((unsigned)ng), dim3(kSpT), Lc.s, a, L.spcell + g0);
-        Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
-        return;
-    }
-    if (ctx->wsweep) {
-        const int W = ctx->wsweep, ms = dm.lbytes[l].max_ws;
-        const size_t smem = (size_t)W * ms * (kRecS + kSlotRec) * sizeof(double);
-        const int groups = (a.cend - a.cbeg + 31) / 32;
-        const dim3 g((groups + W - 1) / W), b(W * 32);
-        if (W == 1) k_sweep_ws<D, 1><<<g, b, smem, Lc.s>>>(a, ms);
-        else if (W == 4) k_sweep_ws<D, 4><<<g, b, smem, Lc.s>>>(a, ms);
-        else k_sweep_ws<D, 2><<<g, b, smem, Lc.s>>>(a, ms);
-        Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
-        return;
-    }
-    const void *win = ctx->l2_window ? (const void *)L.rec : nullptr;
-    const size_t rec_bytes = (size_t)L.n_loc * kRecStride * sizeof(double);
-    const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_full ? ctx->l2_maxw : ctx->l2_window, rec_bytes) : 0;
-    // small color blocks are latency bound (one partial wave, each lane walks
-    // its slots one dependent gather after the other): spread the slots over
-    // more lanes while the whole block still fits in one resident wave
-    int lpc = (l < 8 && ctx->lpc_level[l] > 0) ? ctx->lpc_level[l] : ctx->lpc;
-    if (ctx->adapt_lpc && ctx->sweep_grid_cap > 0) {
-        const int64_t wave = (int64_t)ctx->sweep_grid_cap * 256, cells = a.cend - a.cbeg;
-        while (lpc < 16 && cells * lpc * 2 <= wave) lpc *= 2;
-    }
-    switch (lpc) {
-        case 1: launch_sweep<D, 1>(ctx, a, Lc.s, win, wb); break;
-        case 4: launch_sweep<D, 4>(ctx, a, Lc.s, win, wb); break;
-        case 8: launch_sweep<D, 8>(ctx, a, Lc.s, win, wb); break;
-        case 16: launch_sweep<D, 16>(ctx, a, Lc.s, win, wb); break;
-        default: launch_sweep<D, 2>(ctx, a, Lc.s, win, wb); break;
-    }
-    Lc.post(GMG_K_SWEEP, dm.lbytes[l].sweep[c] + (Wout ? dm.lbytes[l].sweep_out[c] : 0.0));
+    if (ff) launch_sweep<D, true>(ctx, a, lpc, Lc.s, win, wb);
+    else launch_sweep<D, false>(ctx, a, lpc, Lc.s, win, wb);
+    Lc.post(GMG_K_SWEEP, frac * ((ff ? dm.lbytes[l].sweep_ff[c] : dm.lbytes[l].sweep[c]) +
+                                 (Wout ? dm.lbytes[l].sweep_out[c] : 0.0)));
+    ctx->visits += (int64_t)(b1 - b0);
 }
 
 // one color phase with the fused P2P halo on every domain (an empty phase,
@@ -504,196 +458,94 @@ void enqueue_p2p_phase(Launcher &Lc, int l, int c, bool last, bool ff, std::func
         DevLevel &L = dm.dv[l];
         const DomLevel &H = dm.lv[l];
         const int b0 = c < 0 ? 0 : (int)H.blk[c], b1 = c < 0 ? 0 : (int)H.blk[c + 1];
-        const bool z = c >= 0 && ff && ctx->skip_zero;
-        SweepArgs a{b0, b1, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs(L),
-                    last ? wout(L) : nullptr, z ? (int)H.blk[c + 1] : 0, z ? (int)H.n_own : 0};
-        P2PArgs p{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_rec, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
-        int lpc = ctx->lpc;
-        const int64_t cells = b1 - b0;
-        if (ctx->adapt_lpc && ctx->sweep_grid_cap > 0)
-            while (lpc < 16 && cells * lpc * 2 <= (int64_t)ctx->sweep_grid_cap * 256) lpc *= 2;
-        int nb = nblk(cells * lpc);
-        if (ctx->sweep_grid_cap > 0) nb = std::min(nb, ctx->sweep_grid_cap);
+        const SweepArgs a = sweep_args(ctx, L, H, c, b0, b1, rhs(L), last ? wout(L) : nullptr);
+        P2PArgs p{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_wp, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
+        const int lpc = sweep_lpc(ctx, b1 - b0);
+        int nb = nblk((int64_t)(b1 - b0) * lpc);
+        if (ctx->sweep_grid_cap > 0) nb = std::min(nb, ctx->sweep_grid_cap / 2);
         const dim3 g(std::max(nb, 1)), b(256);
         Lc.pre(GMG_K_SWEEP);
+#define GMG_P2P_LAUNCH(LP)                                                          \
+    (ff ? k_sweep_p2p<D, LP, true><<<g, b, 0, Lc.s>>>(a, p)                         \
+        : k_sweep_p2p<D, LP, false><<<g, b, 0, Lc.s>>>(a, p))
         switch (lpc) {
-            case 1: k_sweep_p2p<D, 1><<<g, b, 0, Lc.s>>>(a, p); break;
-            case 4: k_sweep_p2p<D, 4><<<g, b, 0, Lc.s>>>(a, p); break;
-            case 8: k_sweep_p2p<D, 8><<<g, b, 0, Lc.s>>>(a, p); break;
-            case 16: k_sweep_p2p<D, 16><<<g, b, 0, Lc.s>>>(a, p); break;
-            default: k_sweep_p2p<D, 2><<<g, b, 0, Lc.s>>>(a, p); break;
+            case 1: GMG_P2P_LAUNCH(1); break;
+            case 4: GMG_P2P_LAUNCH(4); break;
+            case 8: GMG_P2P_LAUNCH(8); break;
+            case 16: GMG_P2P_LAUNCH(16); break;
+            default: GMG_P2P_LAUNCH(2); break;
         }
-        Lc.post(GMG_K_SWEEP, c < 0 ? 0.0 : dm.lbytes[l].sweep[c] + (last ? dm.lbytes[l].sweep_out[c] : 0.0));
+#undef GMG_P2P_LAUNCH
+        Lc.post(GMG_K_SWEEP, c < 0 ? 0.0 : (ff ? dm.lbytes[l].sweep_ff[c] : dm.lbytes[l].sweep[c]) +
+                                              (last ? dm.lbytes[l].sweep_out[c] : 0.0));
+        ctx->visits += (int64_t)(b1 - b0);
     }
 }
 
-// n_sweeps x (forward colors 1..Nc, backward Nc..1), Algorithm 2;
-// after every color its increments go to the ranks/domains that ghost them.
-// The record's W_lin is the linearisation state; the last backward pass also
-// writes W = W_lin + dW (rhs/Wout select the domain's arrays).
+// Algorithm 2's phase list of one smoothing step: n_sweeps x
+// (forward colors 1..Nc, backward Nc..1).  With skip_repeat a color phase
+// that directly follows a phase of the SAME color (the turn of every forward
+// -> backward and backward -> forward pass: c_N then c_N, c_1 then c_1) is
+// dropped: a cell's update reads only other-colored neighbours, none of which
+// changed in between, and never its own state -- so it would recompute
+// identical values (its W write, if any, moves to the kept phase).  Exact,
+// not an approximation: the oracle runs every phase.
+struct Phase { int c; bool last; bool ff; };
+std::vector<Phase> phase_list(const gmg_ctx *ctx, int l, int n_sweeps)
+{
+    const int nc = ctx->lv[l].ncolor;
+    std::vector<Phase> seq;
+    for (int s = 0; s < n_sweeps; ++s)
+        for (int half = 0; half < 2; ++half)
+            for (int cc = 0; cc < nc; ++cc) {
+                const Phase ph{half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1, s == 0 && half == 0};
+                if (ctx->opt.skip_repeat && !seq.empty() && seq.back().c == ph.c) seq.back().last |= ph.last;
+                else seq.push_back(ph);
+            }
+    return seq;
+}
+
+// one smoothing step's sweeps; after every color its W' goes to the
+// ranks/domains that ghost it.  rhs/wout select the domain's arrays: the first
+// forward half-sweep reads rhs (with W_lin and 1/D, c) and the last backward
+// half-sweep writes W = W' into wout.
 template <int D>
 void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const double *(DevLevel &)> rhs,
                     std::function<double *(DevLevel &)> wout)
 {
     gmg_ctx *ctx = Lc.ctx;
-    const int nc = ctx->lv[l].ncolor;
-    struct Ph { int c; bool last; bool ff; };
-    std::vector<Ph> seq;
-    // Algorithm 2's phase list.  A color phase that directly follows a phase
-    // of the SAME color (the turn of every forward -> backward and backward ->
-    // forward pass: c_N then c_N, c_1 then c_1) is idempotent: a cell's update
-    // reads only other-colored neighbours, none of which changed in between,
-    // and never its own dW -- so it recomputes bit-identical values and is
-    // dropped (its W = W_lin + dW write, if any, moves to the kept phase).
-    // Exact, not an approximation: the oracle runs every phase.
-    for (int s = 0; s < n_sweeps; ++s)
-        for (int half = 0; half < 2; ++half)
-            for (int cc = 0; cc < nc; ++cc) {
-                const Ph ph{half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1, s == 0 && half == 0};
-                if (ctx->skip_repeat && !seq.empty() && seq.back().c == ph.c) seq.back().last |= ph.last;
-                else seq.push_back(ph);
-            }
-    // fused P2P halo: increments go to the ghosts from the sweep epilogue; a
-    // synchronisation phase before (the ghosts' local zeroing is done) and
-    // after (the peers' last increments have landed) the step
-    if (ctx->p2p && ctx->p2p_ready && ctx->nparts > 1) {
+    const std::vector<Phase> seq = phase_list(ctx, l, n_sweeps);
+    // fused P2P halo: states go to the ghosts from the sweep epilogue; a
+    // synchronisation phase before (the ghosts' local initialisation is done)
+    // and after (the peers' last states have landed) the step
+    if (ctx->opt.p2p && ctx->p2p_ready && ctx->nparts > 1) {
         enqueue_p2p_phase<D>(Lc, l, -1, false, false, rhs, wout);
-        for (const Ph &ph : seq) enqueue_p2p_phase<D>(Lc, l, ph.c, ph.last, ph.ff, rhs, wout);
+        for (const Phase &ph : seq) enqueue_p2p_phase<D>(Lc, l, ph.c, ph.last, ph.ff, rhs, wout);
         enqueue_p2p_phase<D>(Lc, l, -1, false, false, rhs, wout);
         return;
     }
-    // dependency-driven persistent sweep: one launch for the whole smoothing step
-    if (ctx->flow && ctx->flow_grid > 0 && ctx->nparts == 1 && ctx->dom.size() == 1 && ctx->dom[0].dv[l].nchunk > 0 &&
-        (int)seq.size() <= kFlowMaxPh && !ctx->pipe && !ctx->spsweep && !ctx->wsweep) {
-        Domain &dm = ctx->dom[0];
-        DevLevel &L = dm.dv[l];
-        FlowArgs f{};
-        f.nph = (int)seq.size();
-        f.K = L.nchunk;
-        f.n_own = L.n;
-        f.seg = L.seg;
-        f.cnoff = L.cnoff;
-        f.cnidx = L.cnidx;
-        f.prog = L.prog;
-        f.err = ctx->d_flag + 2;
-        double bytes = 0;
-        for (size_t k = 0; k < seq.size(); ++k) {
-            f.ph[k] = (unsigned short)(seq[k].c | (seq[k].last ? 1 << 8 : 0) | (seq[k].ff && ctx->skip_zero ? 1 << 9 : 0));
-            bytes += dm.lbytes[l].sweep[seq[k].c] + (seq[k].last ? dm.lbytes[l].sweep_out[seq[k].c] : 0.0);
-        }
-        SweepArgs a{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs(L), wout(L), 0, 0};
-        cudaMemsetAsync(L.prog, 0, sizeof(int) * L.nchunk, Lc.s);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(std::min(ctx->flow_grid, L.nchunk));
-        cfg.blockDim = dim3(256);
-        cfg.stream = Lc.s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeCooperative;
-        at[0].val.cooperative = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        if (ctx->flow == 2) cfg.gridDim = dim3(std::min(ctx->flow_grid, (L.nchunk + 7) / 8));
-        Lc.pre(GMG_K_SWEEP);
-        if (ctx->flow == 2) cudaLaunchKernelEx(&cfg, k_sweep_flow_w<D>, a, f);
-        else cudaLaunchKernelEx(&cfg, k_sweep_flow<D>, a, f);
-        Lc.post(GMG_K_SWEEP, bytes);
-        return;
-    }
-    const bool fuse = ctx->tail_cells > 0 && ctx->nparts == 1 && ctx->dom.size() == 1;
-    const bool tailc = ctx->tailc && !fuse && ctx->tailc_grid > 0 && ctx->nparts == 1 && ctx->dom.size() == 1 &&
-                       ctx->sweep_grid_cap > 0 && !ctx->pipe && !ctx->spsweep && !ctx->wsweep;
-    const bool overlap = (ctx->overlap < 0 ? ctx->opt.nranks > 1 : ctx->overlap != 0) && ctx->nparts > 1 && ctx->side && !ctx->pipe && !ctx->spsweep && !ctx->wsweep;
-    for (size_t k = 0; k < seq.size();) {
-        if (fuse) {
-            // a run of >= 2 consecutive tiny color phases -> one single-CTA launch
-            Domain &dm = ctx->dom[0];
-            const DomLevel &H = dm.lv[l];
-            auto tiny = [&](size_t t) {
-                return t < seq.size() && H.blk[seq[t].c + 1] - H.blk[seq[t].c] <= ctx->tail_cells;
-            };
-            size_t r = k;
-            while (tiny(r) && r - k < (size_t)kTailMaxPh) ++r;
-            if (r - k >= 2) {
-                DevLevel &L = dm.dv[l];
-                TailArgs t{};
-                t.nph = (int)(r - k);
-                for (size_t p = k; p < r; ++p) {
-                    t.cbeg[p - k] = (int)H.blk[seq[p].c];
-                    t.cend[p - k] = (int)H.blk[seq[p].c + 1];
-                    t.wout[p - k] = seq[p].last ? 1 : 0;
-                }
-                t.a = SweepArgs{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs(L), wout(L)};
-                double bytes = 0;
-                for (size_t p = k; p < r; ++p)
-                    bytes += dm.lbytes[l].sweep[seq[p].c] + (seq[p].last ? dm.lbytes[l].sweep_out[seq[p].c] : 0.0);
-                Lc.pre(GMG_K_SWEEP);
-                klaunch(ctx, k_sweep_tail<D>, dim3(1), dim3(kTailT), Lc.s, t);
-                Lc.post(GMG_K_SWEEP, bytes);
-                k = r;
-                continue;
-            }
-        }
-        if (tailc) {
-            // a run of >= 2 consecutive small phases (each fits one resident wave at 2 lanes per
-            // cell) -> one cooperative launch, grid barriers between the phases
-            Domain &dm = ctx->dom[0];
-            const DomLevel &H = dm.lv[l];
-            const int64_t small = ctx->tailc_cells > 0 ? ctx->tailc_cells : (int64_t)ctx->sweep_grid_cap * 256 / 2;
-            auto is_small = [&](size_t t) { return t < seq.size() && H.blk[seq[t].c + 1] - H.blk[seq[t].c] <= small; };
-            size_t r = k;
-            int64_t mx = 0;
-            while (is_small(r) && r - k < (size_t)kTailMaxPh) { mx = std::max<int64_t>(mx, H.blk[seq[r].c + 1] - H.blk[seq[r].c]); ++r; }
-            if (r - k >= 2) {
-                DevLevel &L = dm.dv[l];
-                TailArgs t{};
-                t.nph = (int)(r - k);
-                double bytes = 0;
-                for (size_t p = k; p < r; ++p) {
-                    t.cbeg[p - k] = (int)H.blk[seq[p].c];
-                    t.cend[p - k] = (int)H.blk[seq[p].c + 1];
-                    t.wout[p - k] = seq[p].last ? 1 : 0;
-                    bytes += dm.lbytes[l].sweep[seq[p].c] + (seq[p].last ? dm.lbytes[l].sweep_out[seq[p].c] : 0.0);
-                }
-                t.a = SweepArgs{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, rhs(L), wout(L)};
-                const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->tailc_grid, (mx * 16 + 255) / 256));
-                cudaLaunchConfig_t cfg = {};
-                cfg.gridDim = dim3(grid);
-                cfg.blockDim = dim3(256);
-                cfg.stream = Lc.s;
-                cudaLaunchAttribute at[1];
-                at[0].id = cudaLaunchAttributeCooperative;
-                at[0].val.cooperative = 1;
-                cfg.attrs = at;
-                cfg.numAttrs = 1;
-                int *bar = ctx->d_bar;
-                Lc.pre(GMG_K_SWEEP);
-                cudaLaunchKernelEx(&cfg, k_sweep_tailc<D>, t, bar);
-                Lc.post(GMG_K_SWEEP, bytes);
-                k = r;
-                continue;
-            }
-        }
-        const int c = seq[k].c;
+    const bool overlap = (ctx->opt.overlap < 0 ? ctx->opt.nranks > 1 : ctx->opt.overlap != 0) && ctx->nparts > 1 && ctx->side;
+    for (const Phase &ph : seq) {
+        const int c = ph.c;
         if (overlap) {
-            // boundary cells of color c first; their increments travel on the
-            // side stream while the interior cells of c (no ghost neighbours)
-            // are swept; the next color waits for the ghosts (fork / join)
+            // boundary cells of color c first; their states travel on the side
+            // stream while the interior cells of c (no ghost neighbours) are
+            // swept; the next color waits for the ghosts (fork / join)
             for (Domain &dm : ctx->dom)
-                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 1, seq[k].ff);
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), ph.last ? wout(dm.dv[l]) : nullptr, 1, ph.ff);
             cudaEventRecord(ctx->ev_fork, Lc.s);
             cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
             Launcher Ls{ctx, ctx->side};
-            enqueue_exchange<D>(Ls, l, EX_DW, c);
+            enqueue_exchange<D>(Ls, l, EX_WP, c);
             cudaEventRecord(ctx->ev_join, ctx->side);
             for (Domain &dm : ctx->dom)
-                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 2, seq[k].ff);
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), ph.last ? wout(dm.dv[l]) : nullptr, 2, ph.ff);
             cudaStreamWaitEvent(Lc.s, ctx->ev_join, 0);
         } else {
             for (Domain &dm : ctx->dom)
-                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), seq[k].last ? wout(dm.dv[l]) : nullptr, 0, seq[k].ff);
-            enqueue_exchange<D>(Lc, l, EX_DW, c);
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), ph.last ? wout(dm.dv[l]) : nullptr, 0, ph.ff);
+            enqueue_exchange<D>(Lc, l, EX_WP, c);
         }
-        ++k;
     }
 }
 
@@ -718,10 +570,10 @@ void enqueue_exchange_ho(Launcher &Lc, double *HoDev::*arr, int ncomp)
         DevLevel &L = dm.dv[0];
         const int64_t s1 = H.send_off.back();
         if (s1 > 0) {
-            Lc.pre(GMG_K_NORM);
+            Lc.pre(GMG_K_HALO);
             klaunch(ctx, k_pack, dim3(nblk(s1)), dim3(256), Lc.s, (int)s1, L.send_idx, (const double *)(L.ho.*arr), ncomp, 0,
                     ncomp, dm.ho.sendbuf);
-            Lc.post(GMG_K_NORM, (double)s1 * ncomp * 16);
+            Lc.post(GMG_K_HALO, (double)s1 * ncomp * 16);
         }
     }
     if (ctx->opt.nranks > 1) {
@@ -758,10 +610,10 @@ void enqueue_exchange_ho(Launcher &Lc, double *HoDev::*arr, int ncomp)
         DevLevel &L = dm.dv[0];
         const int64_t r1 = H.recv_off.back();
         if (r1 > 0) {
-            Lc.pre(GMG_K_NORM);
+            Lc.pre(GMG_K_HALO);
             klaunch(ctx, k_unpack, dim3(nblk(r1)), dim3(256), Lc.s, (int)r1, L.recv_idx, (const double *)dm.ho.recvbuf,
-                    L.ho.*arr, ncomp, 0, ncomp, 0, 0);
-            Lc.post(GMG_K_NORM, (double)r1 * ncomp * 16);
+                    L.ho.*arr, ncomp, 0, ncomp, (double *)nullptr);
+            Lc.post(GMG_K_HALO, (double)r1 * ncomp * 16);
         }
     }
     ctx->exchanges++;
@@ -838,7 +690,7 @@ void enqueue_vcycle(Launcher &Lc)
     } else {
         for (size_t d = 0; d < doms.size(); ++d)
             enqueue_gather<D>(Lc, doms[d], (int)d, 0,
-                              G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | G_ZERO_DW | G_COPY_W | (df0 ? G_ALPHA : 0),
+                              G_FLUX | G_NORM | G_WRITE_RT | G_PREPARE | G_COPY_W | (df0 ? G_ALPHA : 0),
                               nullptr);
         enqueue_norm_hist(Lc);
         enqueue_ghost_wlin<D>(Lc, 0);
@@ -859,7 +711,7 @@ void enqueue_vcycle(Launcher &Lc)
         for (Domain &dm : doms) enqueue_restrict<D>(Lc, dm, l);                // W0, Res*, alpha, dW = 0
         enqueue_exchange<D>(Lc, l, EX_WLIN, -1);                                // ghosts' W0, dW = 0
         for (size_t d = 0; d < doms.size(); ++d) {
-            enqueue_face<D>(Lc, doms[d], l, doms[d].dv[l].rec, !last, true, false, true);   // R(W0) only if F is needed later
+            enqueue_face<D>(Lc, doms[d], l, doms[d].dv[l].wlin, !last, true, false, true);   // R(W0) only if F is needed later
             enqueue_gather<D>(Lc, doms[d], (int)d, l, (last ? 0 : (G_FLUX | G_SET_F)) | G_PREPARE, nullptr);
         }
         enqueue_sweeps<D>(Lc, l, ctx->opt.n_sweeps, [](DevLevel &L) { return (const double *)L.Rs; },
@@ -943,6 +795,23 @@ gmg_status get_natural(gmg_ctx *ctx, int l, std::function<const double *(DevLeve
     return GMG_OK;
 }
 
+// every domain's owned dW = W' - W_lin -> natural SoA (gmg_smooth)
+gmg_status get_dw_natural(gmg_ctx *ctx, int l, double *dst)
+{
+    const int64_t N = ctx->lv[l].n;
+    const int ncomp = ctx->opt.dim + 2, ws = ctx->opt.dim == 3 ? Wp<3>::STRIDE : Wp<2>::STRIDE;
+    if (ctx->opt.nranks > 1)
+        CK(cudaMemcpyAsync(ctx->d_stage, dst, sizeof(double) * ncomp * N, cudaMemcpyDefault, ctx->stream));
+    for (Domain &dm : ctx->dom) {
+        DevLevel &L = dm.dv[l];
+        k_diff_to_natural<<<nblk(L.n), 256, 0, ctx->stream>>>(L.n, (int)N, ncomp, L.perm, L.wp, L.wlin, ws, ctx->d_stage);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(dst, ctx->d_stage, sizeof(double) * ncomp * N, cudaMemcpyDefault, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GMG_OK;
+}
+
 // ----------------------------------------------------------------- workspace
 struct Bump {
     char *base;
@@ -981,29 +850,25 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.Frec = b.take<double>((size_t)kFaceRec * nf);
             L.vol = b.take<double>(n);
             L.W = b.take<double>((size_t)nv * nloc); L.Rt = b.take<double>((size_t)nv * n);
-            L.rec = b.take<double>((size_t)kRecStride * nloc);
+            L.wlin = b.take<double>((size_t)Wp<3>::STRIDE * nloc);   // >= Wp<2>::STRIDE
+            L.wp = b.take<double>((size_t)Wp<3>::STRIDE * nloc);
+            L.xr = b.take<double>((size_t)kXr * n);
+            L.dc = b.take<double>((size_t)2 * n);
             L.tmp = b.take<double>(n);
             L.Rs = b.take<double>((size_t)nv * n); L.F = b.take<double>((size_t)nv * n);
             L.alpha = b.take<double>(n); L.sigma = b.take<double>(n);
             L.deg_int = b.take<uint8_t>(n); L.deg_all = b.take<uint8_t>(n);
             L.gbase = b.take<int>(n);
             L.gface = b.take<int>(H.ng_entries);
-            L.ecell = b.take<int>(n); L.estride = b.take<int>(n);
-            L.spcell = b.take<int>(H.sp_cell.size());
             L.sinfo = b.take<int2>(n);
             L.fslot = b.take<int2>(nf);
             L.npeer = (int)H.peers.size();
             L.p2p_off = b.take<int>(H.p2p_off.size());
             L.p2p_k = b.take<int>(H.p2p_k.size());
             L.p2p_g = b.take<int>(H.p2p_g.size());
-            L.peer_rec = b.take<double *>(H.peers.size());
+            L.peer_wp = b.take<double *>(H.peers.size());
             L.p2p_sig = b.take<int *>(H.peers.size());
             L.p2p_wait = b.take<int>(H.peers.size());
-            L.nchunk = H.nchunk;
-            L.seg = b.take<int>(H.seg.size());
-            L.cnoff = b.take<int>(H.cnoff.size());
-            L.cnidx = b.take<int>(H.cnidx.size());
-            L.prog = b.take<int>(H.nchunk);
             L.ginfo = b.take<int4>(n);
             L.sJe = b.take<int>(H.sJe.size());
             L.sRe = b.take<double>(H.sRe.size());
@@ -1030,7 +895,6 @@ void carve(gmg_ctx *ctx, Bump &b)
     ctx->hist_cap = 4096;
     ctx->d_hist = b.take<double>((size_t)ctx->hist_cap * nv);
     ctx->d_flag = b.take<int>(4);
-    ctx->d_bar = b.take<int>(2);
     ctx->d_emu = b.take<char>(sizeof(EmuDom) * kEmuMaxDom);
     ctx->d_emu_bar = b.take<int>(2 * kEmuMaxDom);
     ctx->d_sumsq = b.take<double>((size_t)std::max<size_t>(1, ctx->dom.size()) * nv);
@@ -1094,38 +958,35 @@ void compute_bytes(gmg_ctx *ctx)
             for (int64_t i = 0; i < H.n_own; ++i) slots += H.deg_all[i];
             B.gather = slots * (4 + nv * 8 + 16) + (double)H.n_own * (10 + 2 * nv * 8);
             // sweep (compulsory): own Rt, 1/D, alpha/2, dW write; neighbour-unique W, dW;
-            // face data (A, S r) once per face + 4 B per slot
+            // face data (A, S r) once per face + 4 B per slot.  First forward half-sweep: only the
+            // neighbours of earlier colors (and ghosts of earlier colors) carry an increment, so only
+            // their slots and their share of the neighbour term are charged
             B.sweep.assign(ncolor, 0.0);
+            B.sweep_ff.assign(ncolor, 0.0);
             B.sweep_out.assign(ncolor, 0.0);
+            B.visits.assign(ncolor, 0);
+            const std::vector<int32_t> &gcol = ctx->lv[l].color;
             for (int c = 0; c < ncolor; ++c) {
-                double s = 0;
-                for (int64_t i = H.blk[c]; i < H.blk[c + 1]; ++i)
+                double s = 0, sf = 0;
+                for (int64_t i = H.blk[c]; i < H.blk[c + 1]; ++i) {
                     s += (2 * nv * 8 + 16) + 2 * nv * 8 + H.deg_int[i] * ((d + 1) * 8 / 2.0 + 4);
+                    int lower = 0;
+                    for (int32_t e = H.soffc[i]; e < H.soffc[i + 1]; ++e) {
+                        const int32_t j = H.sJe[e];
+                        lower += j < H.n_own ? (j < H.blk[c]) : (gcol[H.l2n[j]] - 1 < c);
+                    }
+                    sf += (2 * nv * 8 + 16) + (H.deg_int[i] ? 2 * nv * 8 * (double)lower / H.deg_int[i] : 0.0) +
+                          lower * ((d + 1) * 8 / 2.0 + 4);
+                }
                 B.sweep[c] = s;
+                B.sweep_ff[c] = sf;
                 B.sweep_out[c] = (double)(H.blk[c + 1] - H.blk[c]) * 2 * nv * 8;
+                B.visits[c] = H.blk[c + 1] - H.blk[c];
             }
             B.restrict_ = l > 0 ? (double)dm.lv[l - 1].n_own * (2 * nv * 8 + 16) + (double)H.n_own * (3 * nv * 8 + 16) : 0;
-            B.prolong = (double)H.n_own * (2 * nv * 8 + 8 + 4) + (nl > 1 ? (double)dm.lv[1].n_own * (nv * 8 + 12) : 0) +
-                        (nl > 2 ? (double)dm.lv[2].n_own * nv * 8 : 0);
+            B.prolong = (double)H.n_own * (2 * nv * 8 + 8 + 4) + (nl > 1 ? (double)dm.lv[1].n_own * (2 * nv * 8 + 12) : 0) +
+                        (nl > 2 ? (double)dm.lv[2].n_own * 2 * nv * 8 : 0);
             B.update = (double)H.n_own * 3 * nv * 8;
-            int mws = 1;
-            for (int c = 0; c < ncolor; ++c)
-                for (int64_t i0 = H.blk[c]; i0 < H.blk[c + 1]; i0 += kChunk) {
-                    const int64_t i1 = std::min<int64_t>(i0 + kChunk, H.blk[c + 1]);
-                    int s = 0;
-                    for (int64_t i = i0; i < i1; ++i) s += H.deg_int[i];
-                    mws = std::max(mws, s);
-                }
-            B.max_ws = mws;
-            int mp = 1;
-            for (int c = 0; c < ncolor; ++c)
-                for (int64_t i0 = H.blk[c]; i0 < H.blk[c + 1]; i0 += kPB) {
-                    const int64_t i1 = std::min<int64_t>(i0 + kPB, H.blk[c + 1]);
-                    int s = 0;
-                    for (int64_t i = i0; i < i1; ++i) s += H.deg_int[i];
-                    mp = std::max(mp, s);
-                }
-            B.max_pipe = std::min(mp, 128);   // batch slots live in 4 registers per lane
         }
     }
 }
@@ -1168,6 +1029,12 @@ void gmg_default_options(gmg_options *o)
     o->ho_c2 = 1.0;
     o->ho_gam0 = 0.95;
     o->ho_eps = 1e-14;
+    o->skip_repeat = 1;
+    o->p2p = 0;
+    o->overlap = -1;
+    o->l2_persist_mb = 0;
+    o->sweep_lanes = 2;
+    o->pdl = 1;
 }
 
 gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
@@ -1184,44 +1051,17 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
         opt->df_mode > 3 || (opt->df_mode == 3 && !(opt->beta >= 0.0 && opt->beta <= 1.0)) || opt->nranks < 1 ||
         opt->rank < 0 || opt->rank >= opt->nranks || opt->local_domains < 1 ||
         opt->local_domains > 64 || (opt->nranks > 1 && (opt->local_domains != 1 || !opt->nccl_id)) ||
-        opt->setup_device < 0 || opt->setup_device > 1)
+        opt->setup_device < 0 || opt->setup_device > 1 || opt->skip_repeat < 0 || opt->skip_repeat > 1 ||
+        opt->p2p < 0 || opt->p2p > 1 || opt->overlap < -1 || opt->overlap > 1 || opt->l2_persist_mb < 0 ||
+        !(opt->sweep_lanes == 0 || opt->sweep_lanes == 1 || opt->sweep_lanes == 2 || opt->sweep_lanes == 4) ||
+        opt->pdl < 0 || opt->pdl > 1)
         return GMG_EINVAL;
     gmg_ctx *ctx = new (std::nothrow) gmg_ctx();
     if (!ctx) return GMG_ENOMEM;
     ctx->opt = *opt;
     ctx->stream = (cudaStream_t)opt->stream;
     ctx->nparts = std::max(opt->nranks, opt->local_domains);
-    if (const char *e = std::getenv("GMG_LPC")) ctx->lpc = std::atoi(e);   // lanes per cell in the sweep
-    if (const char *e = std::getenv("GMG_LPC_LEVELS")) {                     // per level: "2,2,4"
-        int k = 0;
-        for (const char *p = e; *p && k < 8; ++k) {
-            ctx->lpc_level[k] = std::atoi(p);
-            while (*p && *p != ',') ++p;
-            if (*p == ',') ++p;
-        }
-    }
-    if (const char *e = std::getenv("GMG_MINB")) ctx->minb = std::atoi(e); // min resident blocks (occupancy)
-    // programmatic dependent launch between the V-cycle kernels: every kernel launched with the attribute
-    // waits (griddepcontrol.wait) before touching its predecessor's outputs; the sweep phases load their
-    // static slot indices before that wait, overlapping the previous phase's tail (v16: -3.5 % per
-    // V-cycle).  GMG_PDL=0 disables
-    ctx->pdl = 1;
-    if (const char *e = std::getenv("GMG_PDL")) ctx->pdl = std::atoi(e);
-    if (const char *e = std::getenv("GMG_WSWEEP")) ctx->wsweep = std::atoi(e);   // warp-staged sweep
-    if (const char *e = std::getenv("GMG_SPSWEEP")) ctx->spsweep = std::atoi(e); // slot-parallel sweep
-    if (const char *e = std::getenv("GMG_TAIL")) ctx->tail_cells = std::atoi(e);  // tiny-color fusion threshold
-    if (const char *e = std::getenv("GMG_PIPE")) ctx->pipe = std::atoi(e);        // pipelined warp sweep
-    if (const char *e = std::getenv("GMG_OVERLAP")) ctx->overlap = std::atoi(e);  // boundary-first exchange overlap
-    if (const char *e = std::getenv("GMG_ALPC")) ctx->adapt_lpc = std::atoi(e);   // wider lanes for small colors
-    if (const char *e = std::getenv("GMG_SKIP_REPEAT")) ctx->skip_repeat = std::atoi(e);   // drop idempotent phases
-    if (const char *e = std::getenv("GMG_SKIP_ZERO")) ctx->skip_zero = std::atoi(e);       // skip +0 neighbour terms
-    if (const char *e = std::getenv("GMG_FLOW")) ctx->flow = std::atoi(e);                 // dependency-driven sweep
-    if (const char *e = std::getenv("GMG_P2P")) ctx->p2p = std::atoi(e);                   // fused P2P halo
-    if (const char *e = std::getenv("GMG_TAILC")) ctx->tailc = std::atoi(e);               // cooperative small-phase runs
-    if (const char *e = std::getenv("GMG_TAILC_CELLS")) ctx->tailc_cells = std::atoi(e);
-    if (const char *e = std::getenv("GMG_CHUNK_ORDER")) ctx->chunk_order = std::atoi(e);   // (color, chunk, id) order
-    if (const char *e = std::getenv("GMG_ORDER_CHUNK")) ctx->order_chunk = std::max(8, std::atoi(e));
-    if (const char *e = std::getenv("GMG_FLOW_CHUNK")) ctx->flow_chunk = std::max(32, std::atoi(e));
+    ctx->lpc = opt->sweep_lanes ? opt->sweep_lanes : 2;
     *out = ctx;
     return GMG_OK;
 }
@@ -1334,9 +1174,7 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
             dm.rank = ctx->opt.nranks > 1 ? ctx->opt.rank : k;
             dm.lv.resize(ctx->lv.size());
             for (size_t l = 0; l < ctx->lv.size(); ++l) {
-                build_domain_level(ctx->lv[l], dm.rank, dm.lv[l],
-                                   ctx->nparts != 1 ? 0 : ctx->flow ? ctx->flow_chunk : ctx->chunk_order ? ctx->order_chunk : 0,
-                                   ctx->flow != 0);
+                build_domain_level(ctx->lv[l], dm.rank, dm.lv[l], ctx->nparts == 1);
                 lap("domain_level", (int)l);
             }
             for (size_t l = 0; l + 1 < ctx->lv.size(); ++l)
@@ -1347,7 +1185,7 @@ gmg_status gmg_build_hierarchy(gmg_ctx *ctx, int n_levels, int *n_levels_built)
                              (long long)sst.color_levels, (long long)sst.color_rounds, (long long)sst.match_rounds);
             ctx->dom.push_back(std::move(dm));
         }
-        if (ctx->p2p && ctx->nparts > 1) {   // fused P2P halo targets
+        if (ctx->opt.p2p && ctx->nparts > 1) {   // fused P2P halo targets
             for (Domain &dm : ctx->dom)
                 for (size_t l = 0; l < ctx->lv.size(); ++l) {
                     DomLevel &D = dm.lv[l];
@@ -1483,33 +1321,24 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.deg_all, H.deg_all.data(), H.deg_all.size()));
             CK(up_raw(L.gbase, H.gbase.data(), H.gbase.size() * sizeof(int)));
             CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
-            CK(up_raw(L.ecell, H.ell_cell.data(), H.ell_cell.size() * sizeof(int)));
-            CK(up_raw(L.spcell, H.sp_cell.data(), H.sp_cell.size() * sizeof(int)));
             CK(up_raw(L.fslot, H.fslot.data(), H.fslot.size() * sizeof(int)));
             CK(up_raw(L.p2p_off, H.p2p_off.data(), H.p2p_off.size() * sizeof(int)));
             CK(up_raw(L.p2p_k, H.p2p_k.data(), H.p2p_k.size() * sizeof(int)));
             CK(up_raw(L.p2p_g, H.p2p_g.data(), H.p2p_g.size() * sizeof(int)));
             CK(up_raw(L.p2p_wait, H.peers.data(), H.peers.size() * sizeof(int)));
-            if (H.nchunk) {
-                std::vector<int> sg(H.seg.begin(), H.seg.end());
-                CK(up_i(L.seg, std::move(sg)));
-                CK(up_raw(L.cnoff, H.cnoff.data(), H.cnoff.size() * sizeof(int)));
-                CK(up_raw(L.cnidx, H.cnidx.data(), H.cnidx.size() * sizeof(int)));
-            }
             {
                 std::vector<int> si(2 * H.n_own);
-                for (int64_t i = 0; i < H.n_own; ++i) { si[2 * i] = H.ell_cell[i]; si[2 * i + 1] = H.deg_int[i]; }
+                for (int64_t i = 0; i < H.n_own; ++i) { si[2 * i] = H.soffc[i]; si[2 * i + 1] = H.deg_int[i]; }
                 CK(up_i((const int *)L.sinfo, std::move(si)));
                 std::vector<int> gi(4 * H.n_own);
                 for (int64_t i = 0; i < H.n_own; ++i) {
                     gi[4 * i] = H.gbase[i];
                     gi[4 * i + 1] = (int)H.deg_all[i] | ((int)H.deg_int[i] << 16);
-                    gi[4 * i + 2] = H.ell_cell[i];
-                    gi[4 * i + 3] = H.ell_stride[i];
+                    gi[4 * i + 2] = H.soffc[i];
+                    gi[4 * i + 3] = 0;
                 }
                 CK(up_i((const int *)L.ginfo, std::move(gi)));
             }
-            CK(up_raw(L.estride, H.ell_stride.data(), H.ell_stride.size() * sizeof(int)));
             CK(up_raw(L.sJe, H.sJe.data(), H.sJe.size() * sizeof(int)));
             CK(up_raw(L.sRe, H.sRe.data(), H.sRe.size() * sizeof(double)));
             std::vector<int> perm(H.n_loc);
@@ -1521,17 +1350,19 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.recv_idx, H.recv_idx.data(), H.recv_idx.size() * sizeof(int)));
             // alpha = 1 until set (df_mode 2 keeps it)
             k_fill<<<nblk(H.n_own), 256, 0, ctx->stream>>>((int)H.n_own, L.alpha, 1.0);
-            CK(cudaMemsetAsync(L.rec, 0, sizeof(double) * kRecStride * H.n_loc, ctx->stream));
+            CK(cudaMemsetAsync(L.wlin, 0, sizeof(double) * Wp<3>::STRIDE * H.n_loc, ctx->stream));
+            CK(cudaMemsetAsync(L.wp, 0, sizeof(double) * Wp<3>::STRIDE * H.n_loc, ctx->stream));
+            CK(cudaMemsetAsync(L.xr, 0, sizeof(double) * kXr * H.n_own, ctx->stream));
+            CK(cudaMemsetAsync(L.dc, 0, sizeof(double) * 2 * H.n_own, ctx->stream));
         }
     }
     CK(cudaMemsetAsync(ctx->d_flag, 0, 4 * sizeof(int), ctx->stream));
-    CK(cudaMemsetAsync(ctx->d_bar, 0, 2 * sizeof(int), ctx->stream));
     for (Domain &dm : ctx->dom) {   // P2P phase counts / control
         CK(cudaMemsetAsync(dm.dv[0].p2p_flags, 0, sizeof(int) * std::max(ctx->nparts, 1), ctx->stream));
         CK(cudaMemsetAsync(dm.dv[0].p2p_ctl, 0, sizeof(int) * 4, ctx->stream));
     }
     ctx->p2p_ready = false;
-    if (ctx->p2p && ctx->nparts > 1 && ctx->opt.nranks == 1) {   // local domains: peers are in this process
+    if (ctx->opt.p2p && ctx->nparts > 1 && ctx->opt.nranks == 1) {   // local domains: peers are in this process
         CK(cudaStreamSynchronize(ctx->stream));
         for (Domain &dm : ctx->dom)
             for (int l = 0; l < nl; ++l) {
@@ -1540,11 +1371,11 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
                 std::vector<int *> sg(H.peers.size());
                 for (size_t k = 0; k < H.peers.size(); ++k) {
                     DevLevel &Q = ctx->dom[H.peers[k]].dv[l];
-                    pr[k] = Q.rec;
+                    pr[k] = Q.wp;
                     sg[k] = Q.p2p_flags + dm.rank;
                 }
                 if (!pr.empty()) {
-                    CK(cudaMemcpy(dm.dv[l].peer_rec, pr.data(), pr.size() * sizeof(double *), cudaMemcpyHostToDevice));
+                    CK(cudaMemcpy(dm.dv[l].peer_wp, pr.data(), pr.size() * sizeof(double *), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(dm.dv[l].p2p_sig, sg.data(), sg.size() * sizeof(int *), cudaMemcpyHostToDevice));
                 }
             }
@@ -1569,62 +1400,31 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
-    {   // persisting-L2 window over the gathered cell records, attached to the sweep launches only, with a
-        // 40 MB set-aside (GMG_L2PERSIST: 0 = off, 1 = the largest set-aside, > 1 = that many MB).  Measured
-        // (DESIGN §6): 40 MB -3 % per V-cycle; the largest set-aside speeds the sweeps but starves the rest
-        const char *e = std::getenv("GMG_L2PERSIST");
-        if (!e) e = "40";
-        if (std::atoi(e) > 0) {
-            int maxp = 0, maxw = 0;
-            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->opt.device);
-            cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, ctx->opt.device);
-            // GMG_L2PERSIST=1: the largest set-aside; > 1: that many MB
-            const size_t want = std::atoi(e) > 1 ? (size_t)std::atoi(e) << 20 : (size_t)maxp;
-            const size_t setaside = std::min<size_t>((size_t)maxp, want);
-            CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside));
-            ctx->l2_window = std::min<size_t>((size_t)maxw, setaside);
-            ctx->l2_maxw = (size_t)maxw;
-            if (const char *f = std::getenv("GMG_L2FULL")) ctx->l2_full = std::atoi(f);
-        }
+    if (ctx->opt.l2_persist_mb > 0 && !ctx->l2_changed) {
+        // persisting-L2 window over the gathered W' records, attached to the sweep launches only (opt-in,
+        // gmg_options.l2_persist_mb).  The limit is device-wide: the previous value is restored and the
+        // persisting lines are reset by gmg_destroy
+        int maxp = 0, maxw = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->opt.device);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, ctx->opt.device);
+        const size_t setaside = std::min<size_t>((size_t)maxp, (size_t)ctx->opt.l2_persist_mb << 20);
+        CK(cudaDeviceGetLimit(&ctx->l2_prev_limit, cudaLimitPersistingL2CacheSize));
+        CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside));
+        ctx->l2_changed = true;
+        ctx->l2_window = std::min<size_t>((size_t)maxw, setaside);
     }
-    {   // sweep grid: whole resident waves only (grid-stride kernel), GMG_SWEEP_WAVES (0 = uncapped)
-        int waves = 1, nsm = 0, per_sm = 0;
-        if (const char *e = std::getenv("GMG_SWEEP_WAVES")) waves = std::atoi(e);
-        if (const char *e = std::getenv("GMG_SWEEPV")) ctx->sweep_var = std::atoi(e);
-        if (const char *e = std::getenv("GMG_SWEEP_BS")) ctx->sweep_bs = std::atoi(e);
+    {   // sweep grid: exactly one resident wave (grid-stride kernel, DESIGN.md §6 v5)
+        int nsm = 0, per_sm = 0, per_ff = 0;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
-        if (ctx->opt.dim == 3)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, 4, 3>, 256, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, 4, 3>, 256, 0);
-        ctx->sweep_grid_cap = waves > 0 ? waves * nsm * std::max(per_sm, 1) : 0;
-        int per_flow = 0;
-        if (ctx->opt.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_flow, k_sweep_flow<3>, 256, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_flow, k_sweep_flow<2>, 256, 0);
-        ctx->flow_grid = per_flow * nsm;
-        int per_tail = 0;
-        if (ctx->opt.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_tail, k_sweep_tailc<3>, 256, 0);
-        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_tail, k_sweep_tailc<2>, 256, 0);
-        ctx->tailc_grid = per_tail * nsm;
-    }
-    {   // dynamic shared memory of the warp-staged sweep (may exceed the 48 KB default)
-        int mx = 1;
-        for (Domain &dm : ctx->dom)
-            for (auto &B : dm.lbytes) mx = std::max(mx, B.max_ws);
-        const int per_warp = mx * (kRecS + kSlotRec) * (int)sizeof(double);
-        CK(cudaFuncSetAttribute(k_sweep_ws<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(per_warp, 227 * 1024)));
-        CK(cudaFuncSetAttribute(k_sweep_ws<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(2 * per_warp, 227 * 1024)));
-        CK(cudaFuncSetAttribute(k_sweep_ws<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(4 * per_warp, 227 * 1024)));
-        CK(cudaFuncSetAttribute(k_sweep_ws<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(per_warp, 227 * 1024)));
-        CK(cudaFuncSetAttribute(k_sweep_ws<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(2 * per_warp, 227 * 1024)));
-        CK(cudaFuncSetAttribute(k_sweep_ws<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(4 * per_warp, 227 * 1024)));
-        if (ctx->wsweep && ctx->wsweep * per_warp > 227 * 1024) ctx->wsweep = 1;
-        int mp = 1;
-        for (Domain &dm : ctx->dom)
-            for (auto &B : dm.lbytes) mp = std::max(mp, B.max_pipe);
-        const int pipe_bytes = std::min(kPW * PipeLayout{mp}.warp() * (int)sizeof(double), 227 * 1024);
-        CK(cudaFuncSetAttribute(k_sweep_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe_bytes));
-        CK(cudaFuncSetAttribute(k_sweep_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe_bytes));
+        if (ctx->opt.dim == 3) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, false>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff, k_sweep<3, 2, true>, 128, 0);
+        } else {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, false>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff, k_sweep<2, 2, true>, 128, 0);
+        }
+        ctx->sweep_grid_cap = nsm * std::max(per_sm, 1);
+        ctx->sweep_grid_cap_ff = nsm * std::max(per_ff, 1);
     }
     if (ctx->opt.nranks > 1 && !ctx->nccl_comm) {
         if (!nccl().load(ctx->err)) return GMG_ENCCL;
@@ -1772,13 +1572,13 @@ gmg_status gmg_p2p_emulate_smooth(gmg_ctx *ctx, int level, int n_sweeps, double 
     if (st) return st;
     if (level < 0 || level >= (int)ctx->lv.size() || n_sweeps < 1) { ctx->err = "bad level / n_sweeps"; return GMG_EINVAL; }
     const int P = (int)ctx->dom.size();
-    if (!ctx->p2p || !ctx->p2p_ready || ctx->opt.nranks != 1 || P < 2 || P > kEmuMaxDom ||
+    if (!ctx->opt.p2p || !ctx->p2p_ready || ctx->opt.nranks != 1 || P < 2 || P > kEmuMaxDom ||
         ctx->lv[level].ncolor > kEmuMaxCol) {
-        ctx->err = "P2P emulation needs GMG_P2P=1, 2..16 local domains, <= 24 colors";
+        ctx->err = "P2P emulation needs p2p = 1, 2..16 local domains, <= 24 colors";
         return GMG_ESTATE;
     }
     Launcher Lc{ctx, ctx->stream};
-    const int gf = G_PREPARE | G_SIGMA | G_COPY_W | G_ZERO_DW;
+    const int gf = G_PREPARE | G_SIGMA | G_COPY_W;
     for (size_t d = 0; d < ctx->dom.size(); ++d) {
         if (ctx->opt.dim == 2) {
             enqueue_face<2>(Lc, ctx->dom[d], level, ctx->dom[d].dv[level].W, false, false, false, true);
@@ -1794,14 +1594,9 @@ gmg_status gmg_p2p_emulate_smooth(gmg_ctx *ctx, int level, int n_sweeps, double 
     const int nc = ctx->lv[level].ncolor;
     EmuArgs e{};
     std::vector<int> seq{255};
-    for (int sw = 0; sw < n_sweeps; ++sw)
-        for (int half = 0; half < 2; ++half)
-            for (int cc = 0; cc < nc; ++cc) {
-                const int c = half == 0 ? cc : nc - 1 - cc;
-                if (!(ctx->skip_repeat && seq.size() > 1 && seq.back() == c)) seq.push_back(c);
-            }
+    for (const Phase &ph : phase_list(ctx, level, n_sweeps)) seq.push_back(ph.c | (ph.ff ? 1 << 9 : 0));
     seq.push_back(255);
-    if ((int)seq.size() > kFlowMaxPh) { ctx->err = "too many phases"; return GMG_EINVAL; }
+    if ((int)seq.size() > kEmuMaxPh) { ctx->err = "too many phases"; return GMG_EINVAL; }
     e.ndom = P;
     e.nph = (int)seq.size();
     for (size_t k = 0; k < seq.size(); ++k) e.ph[k] = (unsigned short)seq[k];
@@ -1809,10 +1604,9 @@ gmg_status gmg_p2p_emulate_smooth(gmg_ctx *ctx, int level, int n_sweeps, double 
     for (int d = 0; d < P; ++d) {
         DevLevel &L = ctx->dom[d].dv[level];
         const DomLevel &H = ctx->dom[d].lv[level];
-        ed[d].a = SweepArgs{0, 0, ctx->opt.gamma - 1.0, L.rec, L.ecell, L.deg_int, L.sinfo, L.sJe, L.sRe, L.Rt, nullptr, 0, 0};
-        ed[d].p = P2PArgs{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_rec, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
+        ed[d].a = sweep_args(ctx, L, H, -1, 0, 0, L.Rt, nullptr);
+        ed[d].p = P2PArgs{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_wp, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
         for (int c = 0; c <= nc; ++c) ed[d].blk[c] = (int)H.blk[c];
-        ed[d].n_own = (int)H.n_own;
         ed[d].rank = ctx->dom[d].rank;
         ed[d].bar = ctx->d_emu_bar + 2 * d;
     }
@@ -1842,9 +1636,7 @@ gmg_status gmg_p2p_emulate_smooth(gmg_ctx *ctx, int level, int n_sweeps, double 
         CK(cudaMemcpy(&c2, dm.dv[0].p2p_ctl + 2, sizeof(int), cudaMemcpyDeviceToHost));
         if (c2) { ctx->err = "P2P emulation: peer phase wait timed out"; return GMG_ECUDA; }
     }
-    const int nv = ctx->opt.dim + 2;
-    const int RD = ctx->opt.dim == 3 ? Rec<3>::DW : Rec<2>::DW;
-    if (dW_out) return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.rec; }, nv, dW_out, kRecStride, RD);
+    if (dW_out) return get_dw_natural(ctx, level, dW_out);
     return GMG_OK;
 }
 
@@ -1855,7 +1647,7 @@ gmg_status gmg_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out)
     if (st) return st;
     if (level < 0 || level >= (int)ctx->lv.size() || n_sweeps < 1) { ctx->err = "bad level / n_sweeps"; return GMG_EINVAL; }
     Launcher Lc{ctx, ctx->stream};
-    const int gf = G_PREPARE | G_SIGMA | G_COPY_W | G_ZERO_DW;
+    const int gf = G_PREPARE | G_SIGMA | G_COPY_W;
     auto rhs = [](DevLevel &L) { return (const double *)L.Rt; };
     auto nowout = [](DevLevel &) { return (double *)nullptr; };
     if (ctx->opt.dim == 2) {
@@ -1874,16 +1666,16 @@ gmg_status gmg_smooth(gmg_ctx *ctx, int level, int n_sweeps, double *dW_out)
         enqueue_sweeps<3>(Lc, level, n_sweeps, rhs, nowout);
     }
     CK(cudaGetLastError());
-    {
-        int fe = 0;
-        CK(cudaMemcpyAsync(&fe, ctx->d_flag + 2, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        if (fe) { ctx->err = "dependency-driven sweep: progress wait timed out"; return GMG_ECUDA; }
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->opt.p2p) {
+        for (Domain &dm : ctx->dom) {
+            int c2 = 0;
+            CK(cudaMemcpy(&c2, dm.dv[0].p2p_ctl + 2, sizeof(int), cudaMemcpyDeviceToHost));
+            if (c2) { ctx->err = "P2P halo: peer phase wait timed out"; return GMG_ECUDA; }
+        }
     }
-    const int nv = ctx->opt.dim + 2;
-    const int RD = ctx->opt.dim == 3 ? Rec<3>::DW : Rec<2>::DW;
     if (dW_out) {
-        st = get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.rec; }, nv, dW_out, kRecStride, RD);
+        st = get_dw_natural(ctx, level, dW_out);
         if (st) return st;
     }
     return GMG_OK;
@@ -1897,6 +1689,7 @@ static gmg_status build_graph(gmg_ctx *ctx)
     Launcher Lc{ctx, cs};
     ctx->launches = 0;
     ctx->exchanges = 0;
+    ctx->visits = 0;
     for (double &b : ctx->kbytes) b = 0;
     cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
@@ -1910,7 +1703,35 @@ static gmg_status build_graph(gmg_ctx *ctx)
     cudaGraphDestroy(g);
     if (e != cudaSuccess) { ctx->err = std::string("graph instantiate: ") + cudaGetErrorString(e); return GMG_ECUDA; }
     ctx->graph_launches = ctx->launches;
+    ctx->graph_visits = ctx->visits;
     return GMG_OK;
+}
+
+// GMG_ENONFINITE: the history went non-finite; name the first level (fine first) and the first
+// natural cell whose state or fine residual holds a NaN / Inf
+static gmg_status report_nonfinite(gmg_ctx *ctx)
+{
+    const int nv = ctx->opt.dim + 2;
+    ctx->err = "non-finite residual history";
+    for (int l = 0; l < (int)ctx->lv.size(); ++l) {
+        for (int which = 0; which < 2; ++which) {
+            if (which == 1 && l > 0) break;
+            std::vector<double> h((size_t)nv * ctx->lv[l].n, 0.0);
+            const gmg_status st = which == 0 ? get_natural(ctx, l, [](DevLevel &L) { return (const double *)L.W; }, nv, h.data())
+                                             : get_natural(ctx, l, [](DevLevel &L) { return (const double *)L.Rt; }, nv, h.data());
+            if (st) return st;
+            const int64_t N = ctx->lv[l].n;
+            for (int64_t i = 0; i < N; ++i)
+                for (int q = 0; q < nv; ++q)
+                    if (!std::isfinite(h[(size_t)q * N + i])) {
+                        ctx->err = std::string("non-finite ") + (which == 0 ? "state" : "fine residual") + " at level " +
+                                   std::to_string(l) + ", cell " + std::to_string(i) + " (natural id), component " +
+                                   std::to_string(q);
+                        return GMG_ENONFINITE;
+                    }
+        }
+    }
+    return GMG_ENONFINITE;
 }
 
 static gmg_status finish_history(gmg_ctx *ctx, int n_cycles, double *res_hist)
@@ -1922,15 +1743,14 @@ static gmg_status finish_history(gmg_ctx *ctx, int n_cycles, double *res_hist)
         CK(cudaMemcpyAsync(res_hist, ctx->d_hist, sizeof(double) * nv * std::min(n_cycles + 1, ctx->hist_cap),
                            cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (flags[2]) { ctx->err = "dependency-driven sweep: progress wait timed out"; return GMG_ECUDA; }
-    if (ctx->p2p) {
+    if (ctx->opt.p2p) {
         for (Domain &dm : ctx->dom) {
             int c2 = 0;
             CK(cudaMemcpy(&c2, dm.dv[0].p2p_ctl + 2, sizeof(int), cudaMemcpyDeviceToHost));
             if (c2) { ctx->err = "P2P halo: peer phase wait timed out"; return GMG_ECUDA; }
         }
     }
-    if (flags[1]) { ctx->err = "non-finite residual (level 0)"; return GMG_ENONFINITE; }
+    if (flags[1]) return report_nonfinite(ctx);
     return GMG_OK;
 }
 
@@ -2098,7 +1918,7 @@ gmg_status gmg_sync(gmg_ctx *ctx)
     CK(cudaStreamSynchronize(ctx->copy));
     CK(cudaStreamSynchronize(ctx->copy_out));
     ctx->async_flag_reset = false;
-    if (flags[1]) { ctx->err = "non-finite residual (level 0)"; return GMG_ENONFINITE; }
+    if (flags[1]) return report_nonfinite(ctx);
     return GMG_OK;
 }
 
@@ -2201,6 +2021,34 @@ int64_t gmg_vcycle_launches(gmg_ctx *ctx)
     return ctx->graph_launches;
 }
 
+int64_t gmg_vcycle_visits(gmg_ctx *ctx)
+{
+    if (!ctx) return -1;
+    if (!ctx->graph && check_ready(ctx) == GMG_OK) build_graph(ctx);
+    return ctx->graph_visits;
+}
+
+gmg_status gmg_get_level_field(gmg_ctx *ctx, int level, int field, double *out)
+{
+    if (!ctx) return GMG_EINVAL;
+    gmg_status st = check_ready(ctx, false);
+    if (st) return st;
+    if (level < 0 || level >= (int)ctx->lv.size() || !out || field < GMG_FIELD_W || field > GMG_FIELD_ALPHA) {
+        ctx->err = "bad level / field / null";
+        return GMG_EINVAL;
+    }
+    const int nv = ctx->opt.dim + 2, ws = ctx->opt.dim == 3 ? Wp<3>::STRIDE : Wp<2>::STRIDE;
+    switch (field) {
+        case GMG_FIELD_W: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.W; }, nv, out);
+        case GMG_FIELD_W0: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.wlin; }, nv, out, ws);
+        case GMG_FIELD_DW: return get_dw_natural(ctx, level, out);
+        case GMG_FIELD_RS: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.Rs; }, nv, out);
+        case GMG_FIELD_F: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.F; }, nv, out);
+        case GMG_FIELD_RT: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.Rt; }, nv, out);
+        default: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.alpha; }, 1, out);
+    }
+}
+
 gmg_status gmg_partition_rcb(int64_t n_cells, int dim, const double *centroid, int nparts, int32_t *part_out)
 {
     if (n_cells < 1 || (dim != 2 && dim != 3) || !centroid || nparts < 1 || !part_out) return GMG_EINVAL;
@@ -2214,7 +2062,7 @@ gmg_status gmg_p2p_layout(gmg_ctx *ctx, int64_t *out)
     if (!ctx->ws_ready && !ctx->ws) { ctx->err = "workspace not set"; return GMG_ESTATE; }
     const int nl = (int)ctx->lv.size();
     const Domain &dm = ctx->dom[0];
-    for (int l = 0; l < nl; ++l) out[l] = (int64_t)((const char *)dm.dv[l].rec - (const char *)ctx->ws);
+    for (int l = 0; l < nl; ++l) out[l] = (int64_t)((const char *)dm.dv[l].wp - (const char *)ctx->ws);
     out[nl] = (int64_t)((const char *)dm.dv[0].p2p_flags - (const char *)ctx->ws);
     return GMG_OK;
 }
@@ -2229,7 +2077,7 @@ gmg_status gmg_get_p2p_targets(gmg_ctx *ctx, int level, int dom, int64_t *n_targ
         return GMG_EINVAL;
     }
     const DomLevel &H = ctx->dom[dom].lv[level];
-    if (!ctx->p2p || ctx->nparts < 2 || H.p2p_off.empty()) { ctx->err = "no P2P targets (GMG_P2P=1, > 1 partition)"; return GMG_ESTATE; }
+    if (!ctx->opt.p2p || ctx->nparts < 2 || H.p2p_off.empty()) { ctx->err = "no P2P targets (p2p = 1, > 1 partition)"; return GMG_ESTATE; }
     if (n_targets) *n_targets = (int64_t)H.p2p_k.size();
     if (off && peer_slot && ghost_local) {
         std::copy(H.p2p_off.begin(), H.p2p_off.end(), off);
@@ -2243,7 +2091,7 @@ gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base
 {
     if (!ctx || !handles || !base_off || !layouts) return GMG_EINVAL;
     if (!ctx->ws) { ctx->err = "workspace not set"; return GMG_ESTATE; }
-    if (ctx->opt.nranks < 2 || !ctx->p2p) { ctx->err = "P2P import needs nranks > 1 and GMG_P2P=1"; return GMG_ESTATE; }
+    if (ctx->opt.nranks < 2 || !ctx->opt.p2p) { ctx->err = "P2P import needs nranks > 1 and p2p = 1"; return GMG_ESTATE; }
     CK(cudaSetDevice(ctx->opt.device));
     const int nl = (int)ctx->lv.size(), me = ctx->opt.rank;
     Domain &dm = ctx->dom[0];
@@ -2273,7 +2121,7 @@ gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base
             sg[k] = (int *)(base[q] + lay[nl]) + me;
         }
         if (!pr.empty()) {
-            CK(cudaMemcpy(dm.dv[l].peer_rec, pr.data(), pr.size() * sizeof(double *), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dm.dv[l].peer_wp, pr.data(), pr.size() * sizeof(double *), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(dm.dv[l].p2p_sig, sg.data(), sg.size() * sizeof(int *), cudaMemcpyHostToDevice));
         }
     }
@@ -2431,6 +2279,11 @@ void gmg_destroy(gmg_ctx *ctx)
         }
     }
     if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy((ncclComm_t)ctx->nccl_comm);
+    if (ctx->l2_changed) {   // the persisting-L2 set-aside is device-wide: give it back
+        if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->l2_prev_limit);
+    }
     for (void *p : ctx->p2p_opened) cudaIpcCloseMemHandle(p);
     delete ctx->ho;
     delete ctx;

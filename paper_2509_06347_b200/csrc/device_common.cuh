@@ -10,15 +10,18 @@
 
 namespace gmg {
 
-// per-cell sweep record layout (doubles)
-template <int D> struct Rec;
-// 3D: [W0..W3 | W4 1/D a/2 dW0 | dW1 dW2 dW3 dW4]: the own-cell epilogue reads
-// one 32-B chunk (the 1/D and alpha/2 it needs, with W4 and dW0) and writes the
-// new dW as two whole chunks -- 32 B read + 64 B written per update, no partial
-// sectors (the previous [W0..W3 | W4 dW0..dW2 | dW3 dW4 1/D a/2] read 64 B)
-template <> struct Rec<3> { static constexpr int W = 0, INVD = 5, HA = 6, DW = 7, STRIDE = 12; };
-template <> struct Rec<2> { static constexpr int W = 0, DW = 4, INVD = 8, HA = 9, STRIDE = 12; };
-// (both 96 B: 32-byte aligned, so a neighbour record is three 256-bit loads)
+// Sweep state layout (doubles).  The smoother works on W' = W_lin + dW (the
+// linearisation state plus the current increment), DESIGN.md §6 "W'
+// formulation":
+//  * Wp<D>::STRIDE -- per-cell record of W' (and of W_lin, same layout): 3D
+//    [W0..W3 | W4 0 0 0], 2D [W0..W3]; 32-byte aligned, so a neighbour gather
+//    is two (3D) or one (2D) 256-bit loads touching exactly that many sectors.
+//  * kXr -- own-cell record [X_0..X_{nv-1}, c (, pad)], X = W_lin - Rt/D + c P,
+//    c = alpha/(2D), written by the first forward half-sweep of a smoothing step.
+template <int D> struct Wp;
+template <> struct Wp<3> { static constexpr int STRIDE = 8; };
+template <> struct Wp<2> { static constexpr int STRIDE = 4; };
+constexpr int kXr = 6;
 // per-slot record: A_0..A_{D-1}, S r at [D]
 constexpr int kSlotRec = 4;
 
@@ -38,10 +41,9 @@ enum : int {
     G_ADD_F = 16,
     G_SET_F = 32,     // F = Rs - R
     G_ALPHA = 64,     // alpha = prod alpha_f^{M_f}          (O5)
-    G_PREPARE = 128,  // 1/D, alpha/2 into the record, S r into the slot records (O6)
+    G_PREPARE = 128,  // dc = (1/D, alpha/(2D)) of the hybrid diagonal (O6)
     G_SIGMA = 256,    // store Sigma
-    G_ZERO_DW = 512,  // record dW = 0 (start of a smoothing step, O7 step 1)
-    G_COPY_W = 1024,  // record W_lin = W (fine-level smoothing)
+    G_COPY_W = 1024,  // W_lin = W (fine-level smoothing)
     G_BETA = 2048,    // prepare with the fixed relaxation factor beta instead of alpha (df_mode 3)
 };
 
@@ -83,12 +85,42 @@ __device__ __forceinline__ void ld4cs(const double *p, double *v)
     asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
                  : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
 }
+__device__ __forceinline__ void ld4cg(const double *p, double *v)
+{
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p) : "memory");
+}
+// 128-bit accesses (p 16-byte aligned)
+__device__ __forceinline__ void ld2nc(const double *p, double *v)
+{
+    asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
+}
+__device__ __forceinline__ void ld2cg(const double *p, double *v)
+{
+    asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st2(double *p, const double *v)
+{
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v[0]), "d"(v[1]) : "memory");
+}
 __device__ __forceinline__ void st4(double *p, const double *v)
 {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
                  : "memory");
 }
 
+// one state into a Wp<D> record (whole 32-byte chunks, zero padding)
+template <int D>
+__device__ __forceinline__ void st_state(double *r, const double *w)
+{
+    if constexpr (D == 3) {
+        const double c0[4] = {w[0], w[1], w[2], w[3]}, c1[4] = {w[4], 0.0, 0.0, 0.0};
+        st4(r, c0);
+        st4(r + 4, c1);
+    } else {
+        st4(r, w);
+    }
+}
 template <int D>
 __device__ __forceinline__ double pressure(const double *w, double gm1)
 {

@@ -49,10 +49,6 @@ struct DomLevel {
     std::vector<int64_t> l2n;              // [n_loc] local -> natural
     std::vector<int64_t> blk;              // [ncolor+1] color blocks over owned cells
     std::vector<int64_t> nbnd;             // [ncolor] boundary cells (ghost neighbour) at the start of each block
-    // dependency-driven sweep (single domain): spatial chunks, (color, chunk) segments, chunk adjacency
-    int nchunk = 0;
-    std::vector<int64_t> seg;              // [ncolor][nchunk+1] first local cell of (color c, chunk x)
-    std::vector<int32_t> cnoff, cnidx;     // chunk -> neighbouring chunks (CSR, ascending, no self)
     std::vector<int64_t> fnat;             // [nf] natural ids of the local faces (ascending)
     std::vector<int32_t> fl, fr;           // [nf] local left / right, fr < 0: -(patch+1)
     std::vector<double> vol;               // [n_own]
@@ -65,10 +61,7 @@ struct DomLevel {
     std::vector<int32_t> soffc;            // [n_own+1]
     std::vector<int32_t> sJe;              // [ns] local neighbour (owned or ghost)
     std::vector<double> sRe;               // [ns][4] (A outward | S r)
-    std::vector<int32_t> ell_cell, ell_stride;   // [n_own] entry of slot 0, stride between slots
     std::vector<int32_t> fslot;            // [nf][2] sweep entry of the face in its left / right cell's slots (-1: none)
-    std::vector<int32_t> sp_cell;          // slot-parallel sweep: group cell boundaries, per color
-    std::vector<int64_t> sp_off;           // [ncolor+1] first boundary of each color in sp_cell
     // multigrid links (local indices)
     std::vector<int32_t> child;            // [2][n_own] coarse levels: fine children, -1 = none
     std::vector<int32_t> parent;           // [n_own] levels with a coarser one: coarse parent
@@ -118,28 +111,26 @@ struct DevLevel {
     double *W;                   // [n_loc][nv] state
     double *Rt, *Rs, *F;         // [n][nv] RHS / restricted residual / forcing
     double *alpha, *sigma, *tmp; // [n]
-    double *rec;                 // [n_loc][12] sweep record: W_lin | 1/D | dW | alpha/2 (kernels.cuh Rec<D>)
+    // smoother state (W' formulation; strides Wp<D>::STRIDE, kXr)
+    double *wlin;                // [n_loc][Wp] linearisation state W_lin (coarse: the restricted W0)
+    double *wp;                  // [n_loc][Wp] W' = W_lin + dW of the current half-sweep
+    double *xr;                  // [n][kXr] X = W_lin - Rt/D + c P, c = alpha/(2D) (own-cell record)
+    double *dc;                  // [n][2] 1/D, alpha/(2D) of the hybrid diagonal (gather G_PREPARE)
     const uint8_t *deg_int, *deg_all;    // [n]
     const int *gbase;            // [n]
     const int *gface;
-    const int *ecell, *estride;  // [n] ELL entry of slot 0, stride between slots (cells of the color)
-    const int *spcell;           // slot-parallel sweep group boundaries
     const int2 *sinfo;           // [n] (first sweep slot, interior slots) packed for one 8-byte load
     const int2 *fslot;           // [nf] sweep entries of the face (left cell, right cell), -1 = none
-    const int4 *ginfo;           // [n] (gbase, deg_all | deg_int << 16, ecell, estride) for the gather
+    const int4 *ginfo;           // [n] (gbase, deg_all | deg_int << 16, first sweep slot, 0) for the gather
     const int *sJe;              // [ne] neighbour, -1 = padding
     double *sRe;                 // [ne][4] A outward + S r
     const int *perm;             // [n_loc] local -> natural
     const int *child;            // [2][n]
     const int *parent;           // [n]
     double *partial;             // [nblocks][nv] norm partials
-    // dependency-driven sweep
-    int nchunk;
-    const int *seg, *cnoff, *cnidx;   // [ncolor][nchunk+1], [nchunk+1], chunk neighbours
-    int *prog;                        // [nchunk] phases completed (zeroed before every smoothing step)
-    // fused P2P halo (GMG_P2P)
+    // fused P2P halo (gmg_options.p2p)
     const int *p2p_off, *p2p_k, *p2p_g;
-    double **peer_rec;                // [npeer] peers' record arrays (this level)
+    double **peer_wp;                 // [npeer] peers' W' arrays (this level)
     int **p2p_sig;                    // [npeer] &peer.flags[my rank]
     int *p2p_wait;                    // [npeer] peer ranks
     int *p2p_flags, *p2p_ctl;         // per domain: [nparts] published phase counts, [4] control
@@ -161,10 +152,11 @@ struct Profile {
 // algorithmic bytes bookkeeping
 struct LevelBytes {
     double face_flux = 0, face_prep = 0, face_slots = 0, gather = 0, restrict_ = 0, prolong = 0, update = 0;
-    int max_ws = 1;                // warp-staged sweep: max slots of any 32-cell group
-    int max_pipe = 1;              // pipelined sweep: max slots of any 8-cell batch
-    std::vector<double> sweep;     // per color
+    std::vector<double> sweep;     // per color, SURVEY §8(d) compulsory bytes of one half-sweep phase
+    std::vector<double> sweep_ff;  // per color, the same for the first forward half-sweep (only the lower-color
+                                   // neighbours carry an increment: their slots and records are charged)
     std::vector<double> sweep_out; // per color, extra bytes when the launch also writes W = W0 + dW
+    std::vector<int64_t> visits;   // per color: owned cells (one cell-update each)
 };
 
 // modes of the NEXT-1 gather (ho.cu k_ho_gather)
@@ -222,44 +214,24 @@ struct gmg_ctx {
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph = nullptr;  // one V-cycle
     int64_t graph_launches = 0;
+    int64_t graph_visits = 0;         // sweep cell-updates executed per captured V-cycle
     void *nccl_comm = nullptr;        // ncclComm_t (multi-rank)
     gmg::Profile prof;
     double kbytes[GMG_K_COUNT] = {0}; // algorithmic bytes accumulated by the recorded sequence
     int64_t launches = 0;             // kernels launched by the last recorded sequence
     int64_t exchanges = 0;            // halo exchanges in the last recorded sequence
-    int sweep_grid_cap = 0;           // sweep grid = resident waves x SMs x blocks/SM (set with the workspace)
-    int sweep_var = 3;                // k_sweep variant bits (kernels.cuh), GMG_SWEEPV
-    int sweep_bs = 128;               // sweep block size: 128 x 8 per SM (0.4 % faster than 256 x 4), GMG_SWEEP_BS
-    int lpc = 2;                      // sweep lanes per cell (1, 2, 4) of the large color blocks
-    int lpc_level[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // per-level override of lpc (GMG_LPC_LEVELS=a,b,c; 0 = lpc)
+    int sweep_grid_cap = 0;           // sweep grid = one resident wave: SMs x blocks/SM (set with the workspace)
+    int sweep_grid_cap_ff = 0;        // the same for the first-forward variant (more registers)
+    int64_t visits = 0;               // cell-updates executed by the last recorded sequence
+    int lpc = 2;                      // sweep lanes per cell of the large color blocks (gmg_options.sweep_lanes)
     int adapt_lpc = 1;                // blocks that fit one wave at 2x lanes get up to 16 lanes per cell
-    int skip_repeat = 1;              // drop the repeated same-color phase at every sweep turn (exact)
-    int skip_zero = 1;                // first forward half-sweep: skip later-color neighbours (dW = +0, exact)
-    int tailc = 0;                    // runs of small color phases in one cooperative launch (GMG_TAILC; measured slower)
-    int tailc_grid = 0;               // resident CTAs of k_sweep_tailc
-    int tailc_cells = 0;              // largest phase fused (0: one wave at 2 lanes per cell)
-    int *d_bar = nullptr;             // grid barrier (count, generation) of k_sweep_tailc
-    char *d_emu = nullptr;            // test only: EmuDom[16] of k_p2p_emulate
-    int *d_emu_bar = nullptr;         // test only: group barriers of k_p2p_emulate
-    int flow = 0;                     // dependency-driven persistent sweep (single domain), GMG_FLOW
-    int flow_chunk = 512;             // cells per chunk, GMG_FLOW_CHUNK
-    int p2p = 0;                      // fused P2P halo instead of pack / transport / unpack per color (GMG_P2P)
     bool p2p_ready = false;           // peer pointers known (local domains: at workspace; ranks: after import)
     std::vector<void *> p2p_opened;   // IPC mappings of the peers' workspaces (ranks)
-    int chunk_order = 1;              // order cells inside color blocks by spatial RCB chunk (GMG_CHUNK_ORDER)
-    int order_chunk = 128;            // cells per ordering chunk without GMG_FLOW (GMG_ORDER_CHUNK)
-    int flow_grid = 0;                // resident CTAs of k_sweep_flow (set with the workspace)
-    int minb = 4;                     // sweep __launch_bounds__ min blocks per SM (4, 6, 8)
-    size_t l2_window = 0;             // persisting-L2 window over records (0 = off; experiment)
-    size_t l2_maxw = 0;               // device max access-policy window bytes
-    int l2_full = 0;                  // window over all records with hitRatio = set-aside / bytes (GMG_L2FULL)
-    int pdl = 1;                      // programmatic dependent launch between V-cycle kernels (GMG_PDL, default on)
-    int wsweep = 0;                   // warp-staged sweep: warps per block (0 = register-gather sweep)
-    int spsweep = 0;                  // slot-parallel sweep (thread per slot + block segmented reduction)
-    int tail_cells = 0;               // fuse runs of consecutive color phases with <= this many cells (0 = off; neutral)
-    int pipe = 0;                     // pipelined persistent warp sweep (2-stage cp.async ring)
-    int overlap = -1;                 // partitioned runs: sweep boundary cells, exchange on `side` while interior cells
-                                      // sweep (-1 = auto: NCCL ranks only; local domains measured 4-7% slower with it)
+    char *d_emu = nullptr;            // test only: EmuDom[16] of k_p2p_emulate
+    int *d_emu_bar = nullptr;         // test only: group barriers of k_p2p_emulate
+    size_t l2_window = 0;             // persisting-L2 window over the W' records (gmg_options.l2_persist_mb)
+    size_t l2_prev_limit = 0;         // the device's persisting-L2 limit before this context changed it
+    bool l2_changed = false;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     gmg::HoHost *ho = nullptr;        // NEXT-1 geometry + setup (gmg_load_ho_geometry)
@@ -288,7 +260,7 @@ bool validate_coloring(const HostLevel &L, const std::vector<int32_t> &col);
 int64_t agglomerate(const HostLevel &L, double theta, std::vector<int64_t> &parent, int64_t &nc);
 void build_coarse(const HostLevel &fine, HostLevel &coarse);
 void renumber(HostLevel &L);
-void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells = 0, bool flow = false);
+void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton = false);
 void link_domain_levels(const HostLevel &Gf, const HostLevel &Gc, DomLevel &Df, DomLevel &Dc);
 void build_p2p_targets(DomLevel &D, int me, int ncolor, const std::vector<const DomLevel *> &peer_dom);
 void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *part);

@@ -3,11 +3,10 @@
 //
 // Every kernel is HBM/latency bound gather-streaming work; see DESIGN.md
 // "Kernels and rooflines".  Cell arrays are AoS [n][nv] in color-contiguous
-// internal order.  The sweep reads a per-cell 32-byte aligned record
-// Rec<D> = (W_lin | dW | 1/D | alpha/2), 96 bytes, with three 256-bit loads
-// per neighbour, and per-slot 32-byte records (A outward | S r).  The sweep
-// variants that were measured and lost, and the test-only P2P concurrency
-// emulation, live in kernels_tried.cuh.
+// internal order.  The sweep gathers one 32-byte aligned state record W'
+// (Wp<D>, two 256-bit loads in 3D) per neighbour and per-slot 32-byte records
+// (A outward | S r); the own cell reads its (X, c) record (W' formulation,
+// DESIGN.md §6).  The test-only P2P concurrency emulation is p2p_emulate.cuh.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -47,7 +46,7 @@ __device__ __forceinline__ void kfvs_side(const Side<D> &s, const double *n, dou
 // ---------------------------------------------------------------------------
 // Face kernel (a6 + a10 per face): r_f = omega (|u.n| + a) of the average
 // state; with FLUX also S F_f (KFVS) and alpha_f^{M_f} (DF helper).  The
-// state is read with a stride (NV for W, Rec<D>::STRIDE for the record).
+// state is read with a stride (NV for W, Wp<D>::STRIDE for W_lin).
 // Output: one 64-byte record per face, Frec = (S F[nv] | S r | alpha^M | 0..),
 // written with two 256-bit stores.
 // ---------------------------------------------------------------------------
@@ -148,7 +147,6 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 {
     pdl_launch_dependents();
     constexpr int NV = D + 2;
-    using RC = Rec<D>;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     double R[NV];
 #pragma unroll
@@ -192,23 +190,16 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         }
         if (a.flags & G_ALPHA) L.alpha[i] = al;
         if (a.flags & G_SIGMA) L.sigma[i] = sig;
-        double *rc = L.rec + (size_t)i * RC::STRIDE;
         if (a.flags & G_PREPARE) {
             const double ai = (a.flags & G_BETA) ? a.beta : ((a.flags & G_ALPHA) ? al : L.alpha[i]);
-            // D = alpha (V/Dt_imp + Sigma/2) + (1 - alpha) V/Dt_exp (O6, A2, A3)
+            // D = alpha (V/Dt_imp + Sigma/2) + (1 - alpha) V/Dt_exp (O6, A2, A3); c = alpha / (2 D)
             const double Dg = ai * (sig / a.cfl_imp + 0.5 * sig) + (1.0 - ai) * (sig / a.cfl_exp);
-            rc[RC::INVD] = 1.0 / Dg;
-            rc[RC::HA] = 0.5 * ai;
-        }
-        if (a.flags & G_ZERO_DW) {
-#pragma unroll
-            for (int q = 0; q < NV; ++q) rc[RC::DW + q] = 0.0;
+            const double iD = 1.0 / Dg;
+            const double dc[2] = {iD, 0.5 * ai * iD};
+            st2(L.dc + 2 * (size_t)i, dc);
         }
         const size_t o = (size_t)i * NV;
-        if (a.flags & G_COPY_W) {
-#pragma unroll
-            for (int q = 0; q < NV; ++q) rc[RC::W + q] = pre[q];
-        }
+        if (a.flags & G_COPY_W) st_state<D>(L.wlin + (size_t)i * Wp<D>::STRIDE, pre);
         if (a.flags & G_SET_F) {
             if (pk == G_SET_F) {
 #pragma unroll
@@ -301,7 +292,8 @@ __global__ void k_norm_hist(const double *__restrict__ sumsq, int ndom, int nv, 
 // ---------------------------------------------------------------------------
 // Halo exchange helpers (a13): pack owned cells' values, unpack into ghosts.
 // Element k of a buffer holds ncomp doubles of cell idx[k]; src/dst are cell
-// arrays with the given stride/offset (record dW, record W_lin, or W).
+// arrays with the given stride/offset (W', W_lin or W).  dst2 (nullable)
+// receives a second copy with the same layout (ghost W' = W_lin).
 // ---------------------------------------------------------------------------
 __global__ void k_pack(int count, const int *__restrict__ idx, const double *__restrict__ src, int stride,
                        int offset, int ncomp, double *__restrict__ buf)
@@ -313,175 +305,129 @@ __global__ void k_pack(int count, const int *__restrict__ idx, const double *__r
     for (int q = 0; q < ncomp; ++q) buf[(size_t)k * ncomp + q] = s[q];
 }
 __global__ void k_unpack(int count, const int *__restrict__ idx, const double *__restrict__ buf, double *dst,
-                         int stride, int offset, int ncomp, int zero_at, int nzero)
+                         int stride, int offset, int ncomp, double *dst2)
 {
     pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= count) return;
-    double *d = dst + (size_t)idx[k] * stride;
-    for (int q = 0; q < ncomp; ++q) d[offset + q] = buf[(size_t)k * ncomp + q];
-    for (int q = 0; q < nzero; ++q) d[zero_at + q] = 0.0;
-}
-
-// ghost records from the (current) ghost state: W_lin = W, dW = 0
-template <int D>
-__global__ void k_ghost_wlin(int n, int n_loc, const double *__restrict__ W, double *rec)
-{
-    pdl_enter();
-    using RC = Rec<D>;
-    const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n_loc) return;
-#pragma unroll
-    for (int q = 0; q < D + 2; ++q) {
-        rec[(size_t)g * RC::STRIDE + RC::W + q] = W[(size_t)g * (D + 2) + q];
-        rec[(size_t)g * RC::STRIDE + RC::DW + q] = 0.0;
+    const size_t o = (size_t)idx[k] * stride + offset;
+    for (int q = 0; q < ncomp; ++q) {
+        const double v = buf[(size_t)k * ncomp + q];
+        dst[o + q] = v;
+        if (dst2) dst2[o + q] = v;
     }
 }
-// ghost states after a smoothing step: W = W_lin + dW (both already exchanged)
+
+// Wp<D> record -> state (two / one 256-bit loads); CG: L2-coherent (records
+// written by other blocks of the same launch), else the non-coherent path
+template <int D, bool CG = false>
+__device__ __forceinline__ void ld_state(const double *r, double *w)
+{
+    if constexpr (D == 3) {
+        double c0[4], c1[4];
+        if constexpr (CG) { ld4cg(r, c0); ld4cg(r + 4, c1); }
+        else { ld4nc(r, c0); ld4nc(r + 4, c1); }
+        w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
+    } else {
+        if constexpr (CG) ld4cg(r, w);
+        else ld4nc(r, w);
+    }
+}
+
+// ghost records from the (current) ghost state: W_lin = W' = W
 template <int D>
-__global__ void k_ghost_w(int n, int n_loc, const double *__restrict__ rec, double *W)
+__global__ void k_ghost_wlin(int n, int n_loc, const double *__restrict__ W, double *wlin, double *wp)
 {
     pdl_enter();
-    using RC = Rec<D>;
+    constexpr int WS = Wp<D>::STRIDE;
+    const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n_loc) return;
+    double w[D + 2];
+#pragma unroll
+    for (int q = 0; q < D + 2; ++q) w[q] = W[(size_t)g * (D + 2) + q];
+    st_state<D>(wlin + (size_t)g * WS, w);
+    st_state<D>(wp + (size_t)g * WS, w);
+}
+// ghost states after a smoothing step: W = W' (already exchanged)
+template <int D>
+__global__ void k_ghost_w(int n, int n_loc, const double *__restrict__ wp, double *W)
+{
+    pdl_enter();
     const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_loc) return;
 #pragma unroll
-    for (int q = 0; q < D + 2; ++q)
-        W[(size_t)g * (D + 2) + q] = rec[(size_t)g * RC::STRIDE + RC::W + q] + rec[(size_t)g * RC::STRIDE + RC::DW + q];
+    for (int q = 0; q < D + 2; ++q) W[(size_t)g * (D + 2) + q] = wp[(size_t)g * Wp<D>::STRIDE + q];
 }
 
 // ---------------------------------------------------------------------------
-// MC-LU-SGS sweep over one color block (a11 / a12), reading all neighbours'
-// current increments (reading A7):
-//   dW_i = -( Rt_i + alpha_i/2 sum_j [T(W_j+dW_j; A) - T(W_j; A) - S r dW_j] ) / D_i
-// with A = sigma S n (the Euler flux is linear in its normal, S T(W;n) = T(W;A)).
+// MC-LU-SGS sweep over one color block (a11 / a12): Eq.(gpu-forward-
+// relaxation) / Eq.(gpu-backward-relaxation) P:536-551 with reading A7
+// (every half-sweep reads all neighbours' current increments),
+//   dW_i = -( Rt_i + alpha_i/2 sum_j [T(W_j+dW_j; A) - T(W_j; A) - S r dW_j] ) / D_i,
+// A = sigma S n outward from i (the Euler flux is linear in its normal,
+// S T(W; n) = T(W; A)), evaluated in the W' formulation (DESIGN.md §6,
+// reading B4).  With W'_j = W_j + dW_j the W-only part
+// P_i = sum_j [T(W_j; A) - S r W_j] is fixed during a smoothing step, so
+//   W'_i = X_i - c_i sum_j [T(W'_j; A) - S r W'_j],
+//   X_i  = W_i - Rt_i / D_i + c_i P_i,   c_i = alpha_i / (2 D_i):
+// a neighbour contributes ONE flux evaluation of ONE state (two 256-bit loads
+// in 3D, one in 2D) instead of two evaluations of (W, dW).  The first forward
+// half-sweep of a step (FF) evaluates P_i on the way -- every neighbour's
+// W_lin -- and stores X_i; its later-color owned neighbours still hold
+// W' = W_lin, so only the lower-color (and ghost) neighbours contribute a
+// difference [T(W') - S r W'] - [T(W) - S r W], read from W' and W_lin.
+// Same-color cells never neighbour each other, so a color launch reads no
+// state it writes (non-coherent loads are safe).
 // LPC lanes per cell: each lane gathers its slots' neighbours (one dependent
-// index->record round trip), partial sums are combined with warp shuffles.
-// Same-color cells never neighbour each other, so the in-place dW update is
-// race free and neighbours' dW may be read through the non-coherent path.
+// index -> record round trip), partial sums are combined with warp shuffles.
 // ---------------------------------------------------------------------------
+// t = T(w; A) - Sr w  (3D: 1 division, 27 FMA-class operations)
 template <int D>
-__device__ __forceinline__ void flux_diff(const double *w, const double *dw, const double *A, double gm1,
-                                          double Sr, double *acc)
+__device__ __forceinline__ void flux_rw(const double *w, const double *A, double Sr, double gm1, double *t)
 {
-    const double r0 = w[0], r1 = w[0] + dw[0];
-    const double i0 = 1.0 / r0, i1 = 1.0 / r1;
-    double mA0 = 0.0, mA1 = 0.0, m20 = 0.0, m21 = 0.0;
+    const double ir = 1.0 / w[0];
+    double mA = 0.0, m2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        const double a0 = w[1 + k], a1 = w[1 + k] + dw[1 + k];
-        mA0 += a0 * A[k];
-        mA1 += a1 * A[k];
-        m20 += a0 * a0;
-        m21 += a1 * a1;
+        mA += w[1 + k] * A[k];
+        m2 += w[1 + k] * w[1 + k];
     }
-    const double E0 = w[D + 1], E1 = w[D + 1] + dw[D + 1];
-    const double p0 = gm1 * (E0 - 0.5 * m20 * i0), p1 = gm1 * (E1 - 0.5 * m21 * i1);
-    const double U0 = mA0 * i0, U1 = mA1 * i1;
-    acc[0] += (mA1 - mA0) - Sr * dw[0];
+    const double p = gm1 * (w[D + 1] - 0.5 * m2 * ir);
+    const double U = mA * ir;
+    t[0] = mA - Sr * w[0];
 #pragma unroll
-    for (int k = 0; k < D; ++k)
-        acc[1 + k] += ((w[1 + k] + dw[1 + k]) * U1 + p1 * A[k]) - (w[1 + k] * U0 + p0 * A[k]) - Sr * dw[1 + k];
-    acc[D + 1] += (E1 + p1) * U1 - (E0 + p0) * U0 - Sr * dw[D + 1];
+    for (int k = 0; k < D; ++k) t[1 + k] = (w[1 + k] * U + p * A[k]) - Sr * w[1 + k];
+    t[D + 1] = (w[D + 1] + p) * U - Sr * w[D + 1];
 }
 
 struct SweepArgs {
-    int cbeg, cend;            // color block [cbeg, cend) of owned cells
+    int cbeg, cend;            // cells [cbeg, cend) of one color block (or its boundary / interior part)
+    int lo, n_own;             // FF: owned neighbours j < lo are of earlier colors; j >= n_own are ghosts
     double gm1;
-    double *rec;               // [n_loc][Rec::STRIDE]
-    const int *ecell;          // [n] first slot entry of each cell
-    const uint8_t *deg;        // [n] interior slots of each cell
-    const int2 *sinfo;         // [n] (first slot entry, interior slots) packed
+    const int2 *sinfo;         // [n] (first slot entry, interior slots)
     const int *sJe;            // [ns] neighbour
     const double *sRe;         // [ns][4] (A outward | S r)
-    const double *rhs;         // [n][nv]
-    double *Wout;              // [n][nv] or null: W = W_lin + dW (last backward half-sweep)
-    int zlo, zhi;              // neighbours j in [zlo, zhi) still hold dW = +0 exactly (first
-                               // forward half-sweep, later colors): their term is +0, skipped
+    double *wp;                // [n_loc][Wp] W'
+    double *xr;                // [n][kXr] (X, c)
+    const double *wlin;        // [n_loc][Wp] W_lin        (FF)
+    const double *rhs;         // [n][nv] right-hand side Rt (FF)
+    const double *dc;          // [n][2] (1/D, c)          (FF)
+    double *Wout;              // [n][nv] or null: W = W' (last backward half-sweep)
 };
 
-// neighbour record -> (W_lin, dW)
-template <int D>
-__device__ __forceinline__ void ld_neighbour(const double *rj, double *w, double *dw)
-{
-    if constexpr (D == 3) {
-        double c0[4], c1[4], c2[4];
-        ld4nc(rj, c0);
-        ld4nc(rj + 4, c1);
-        ld4nc(rj + 8, c2);
-        w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-        dw[0] = c1[3]; dw[1] = c2[0]; dw[2] = c2[1]; dw[3] = c2[2]; dw[4] = c2[3];
-    } else {
-        ld4nc(rj, w);
-        ld4nc(rj + 4, dw);
-    }
-}
-
-// own-cell epilogue: dW_i = -(rhs_i + alpha_i/2 acc) / D_i into the record,
-// and W = W_lin + dW on the last backward half-sweep
-template <int D>
-__device__ __forceinline__ void sweep_finish(const SweepArgs &a, int i, const double *acc)
-{
-    constexpr int NV = D + 2;
-    using RC = Rec<D>;
-    double *ri = a.rec + (size_t)i * RC::STRIDE;
-    const size_t o = (size_t)i * NV;
-    double r[NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) r[q] = __ldcs(a.rhs + o + q);
-    if constexpr (D == 3) {
-        double c1[4];
-        ld4nc(ri + 4, c1);                          // W4, 1/D, alpha/2, dW0
-        const double invD = c1[1], ha = c1[2];
-        double d[NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-        ri[RC::DW] = d[0];                          // dW0 alone: a partial-sector write
-        const double c2[4] = {d[1], d[2], d[3], d[4]};
-        st4(ri + 8, c2);
-        if (a.Wout) {
-            double c0[4];
-            ld4nc(ri, c0);
-            a.Wout[o + 0] = c0[0] + d[0];
-            a.Wout[o + 1] = c0[1] + d[1];
-            a.Wout[o + 2] = c0[2] + d[2];
-            a.Wout[o + 3] = c0[3] + d[3];
-            a.Wout[o + 4] = c1[0] + d[4];
-        }
-    } else {
-        double c2[4];
-        ld4nc(ri + 8, c2);                          // 1/D, alpha/2, -, -
-        const double invD = c2[0], ha = c2[1];
-        double d[4];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-        st4(ri + 4, d);
-        if (a.Wout) {
-            double c0[4];
-            ld4nc(ri, c0);
-#pragma unroll
-            for (int q = 0; q < NV; ++q) a.Wout[o + q] = c0[q] + d[q];
-        }
-    }
-}
-
-// sweep variants (template bits, GMG_SWEEPV; default 3, measured DESIGN.md §6):
-//  1 = dW0 written inside the whole 32-B chunk (W4 1/D alpha/2 | dW0), no partial sector
-//  2 = neighbour index of the next slot loaded one iteration ahead
-//  4 = own record tail + rhs prefetched to L1 before the slot loop
-// Fused halo (GMG_P2P): the sweep that computes a boundary cell's increment
+// Fused halo (gmg_options.p2p): the sweep that computes a boundary cell's W'
 // also stores it straight into the ghost record of every rank (domain) that
 // ghosts the cell, over peer memory (NVLink P2P between GPUs; plain device
 // memory between the domains of one process).  Ordering between phases:
 // every rank counts its completed color phases (ctl[0]); the last block of a
-// sweep launch fences the increments system-wide and publishes the new count
+// sweep launch fences the stores system-wide and publishes the new count
 // into each peer's flags[my rank] (st.release.sys); the next launch waits
 // until every peer's count has reached its own (ld.acquire.sys) -- so a peer
-// never reads a ghost before its phase's increments landed, and never
-// overwrites one that is still being read (each side waits for the other).
+// never reads a ghost before its phase's values landed, and never overwrites
+// one that is still being read (each side waits for the other).
 struct P2PArgs {
     const int *off, *k, *g;      // per owned cell: remote targets (peer slot, ghost local index), CSR
-    double *const *peer_rec;     // [peer slot] the peer's record array on this level
+    double *const *peer_wp;      // [peer slot] the peer's W' array on this level
     int np;                      // peers on this level (0: count phases only)
     const int *wait_rank;        // [np] their ranks
     int *const *sig;             // [np] &peer.flags[my rank]
@@ -489,243 +435,136 @@ struct P2PArgs {
     int *ctl;                    // [0] phases completed, [1] blocks done, [2] wait timeout
 };
 
-template <int D, bool P2P = false>
-__device__ __forceinline__ void p2p_store(const P2PArgs &p, int i, const double *d)
+template <int D, bool P2P>
+__device__ __forceinline__ void p2p_store(const P2PArgs &p, int i, const double *w)
 {
     if constexpr (P2P) {
         for (int m = p.off[i]; m < p.off[i + 1]; ++m) {
-            double *r = p.peer_rec[p.k[m]] + (size_t)p.g[m] * Rec<D>::STRIDE + Rec<D>::DW;
+            double *r = p.peer_wp[p.k[m]] + (size_t)p.g[m] * Wp<D>::STRIDE;
 #pragma unroll
-            for (int q = 0; q < D + 2; ++q) r[q] = d[q];
+            for (int q = 0; q < D + 2; ++q) r[q] = w[q];
         }
     }
 }
 
-template <int D, bool P2P = false, bool CS = true>
-__device__ __forceinline__ void sweep_finish_full(const SweepArgs &a, int i, const double *acc,
-                                                  const P2PArgs &p = P2PArgs{})
+template <bool CG>
+__device__ __forceinline__ void ld2x(const double *p, double *v)
 {
-    constexpr int NV = D + 2;
-    double *ri = a.rec + (size_t)i * Rec<D>::STRIDE;
-    const size_t o = (size_t)i * NV;
-    double r[NV], c1[4], c2[4];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) r[q] = CS ? __ldcs(a.rhs + o + q) : __ldg(a.rhs + o + q);
-    if constexpr (D == 3) ld4nc(ri + 4, c1);       // W4, 1/D, alpha/2, dW0
-    else ld4nc(ri + 8, c2);                         // 1/D, alpha/2, -, -
-    if constexpr (D == 3) {
-        const double invD = c1[1], ha = c1[2];
-        double d[NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-        const double w1[4] = {c1[0], c1[1], c1[2], d[0]};
-        st4(ri + 4, w1);
-        const double w2[4] = {d[1], d[2], d[3], d[4]};
-        st4(ri + 8, w2);
-        p2p_store<D, P2P>(p, i, d);
-        if (a.Wout) {
-            double c0[4];
-            ld4nc(ri, c0);
-            a.Wout[o + 0] = c0[0] + d[0];
-            a.Wout[o + 1] = c0[1] + d[1];
-            a.Wout[o + 2] = c0[2] + d[2];
-            a.Wout[o + 3] = c0[3] + d[3];
-            a.Wout[o + 4] = c1[0] + d[4];
-        }
-    } else {
-        const double invD = c2[0], ha = c2[1];
-        double d[4];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) d[q] = -(r[q] + ha * acc[q]) * invD;
-        st4(ri + 4, d);
-        p2p_store<D, P2P>(p, i, d);
-        if (a.Wout) {
-            double c0[4];
-            ld4nc(ri, c0);
-#pragma unroll
-            for (int q = 0; q < NV; ++q) a.Wout[o + q] = c0[q] + d[q];
-        }
-    }
+    if constexpr (CG) ld2cg(p, v);
+    else ld2nc(p, v);
 }
 
-template <int D, int LPC, int VAR, bool P2P>
-__device__ __forceinline__ void sweep_body(const SweepArgs &a, const P2PArgs &p)
+// the cells [cbeg, cend) x LPC lanes, grid-stride from thread gt0 with nthr
+// threads (a launch sized to exactly one resident wave has no partial last
+// wave); PDL: the slot range and first neighbour index (static during a
+// smoothing step) are loaded before griddepcontrol.wait, so they overlap the
+// previous phase's tail, and the records after it
+template <int D, int LPC, bool FF, bool CG, bool P2P>
+__device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p, int gt0, int nthr, bool pdl)
 {
-    constexpr int NV = D + 2;
-    using RC = Rec<D>;
-    // grid-stride over the color's cells: a launch sized to exactly the
-    // resident waves has no partial last wave (the block count of a color is
-    // rarely a multiple of SMs x resident blocks)
+    constexpr int NV = D + 2, WS = Wp<D>::STRIDE;
     const int total = (a.cend - a.cbeg) * LPC;
-    const int stride = gridDim.x * blockDim.x;
-    const int rounds = (total + stride - 1) / stride;
+    const int rounds = (total + nthr - 1) / nthr;
     for (int r = 0; r < rounds; ++r) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x + r * stride;
-    const int i = a.cbeg + g / LPC;
-    const int sub = g % LPC;
-    const bool valid = i < a.cend;
-    double acc[NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-    if (valid) {
-        // per-cell contiguous slots (CSR): [ecell[i], ecell[i] + deg[i]); the
-        // two index loads are independent.  (Measured against ELL and
-        // chunked-ELL layouts: CSR wins on the coarse levels, where the degree
-        // spread is wide -- DESIGN.md §6.)
-        // (first slot, degree) in ONE 8-byte load: separate loads were
-        // serialised by the compiler (degree test before the offset load)
-        const int2 sd = __ldg(a.sinfo + i);
-        if constexpr ((VAR & 4) != 0) {
-            if (sub == 0) {   // own record tail + rhs towards L1 while the gathers run
-                const double *ri = a.rec + (size_t)i * RC::STRIDE;
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(ri + 4));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rhs + (size_t)i * NV));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rhs + (size_t)i * NV + NV - 1));
-            }
-        }
-        const int e0 = sd.x, e1 = sd.x + sd.y;
-        if constexpr ((VAR & 8) != 0) {
-            // PDL prologue: the slot indices are static during a smoothing step, so the cell's slot range
-            // and first neighbour index are loaded before griddepcontrol.wait -- they overlap the previous
-            // phase's tail; slot records and neighbour records (previous phases' increments) after it
-            int e = e0 + sub;
-            int j = e < e1 ? __ldg(a.sJe + e) : 0;
-            if (r == 0) pdl_wait();
-            for (; e < e1; e += LPC) {
-                const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
-                if (j >= a.zlo && j < a.zhi) { j = jn; continue; }
-                double sr[4];
-                if constexpr ((VAR & 32) != 0) ld4nc(a.sRe + (size_t)e * kSlotRec, sr);   // L2-resident
-                else ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
-                double w[NV], dw[NV];
-                ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
-                flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
-                j = jn;
-            }
-        } else if constexpr ((VAR & 2) != 0) {
-            int e = e0 + sub;
-            int j = e < e1 ? __ldg(a.sJe + e) : 0;
-            for (; e < e1; e += LPC) {
-                const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
-                if (j >= a.zlo && j < a.zhi) { j = jn; continue; }
-                double sr[4];
-                ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
-                double w[NV], dw[NV];
-                ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
-                flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
-                j = jn;
-            }
-        } else {
-            for (int e = e0 + sub; e < e1; e += LPC) {
-                const int j = __ldg(a.sJe + e);
-                if (j >= a.zlo && j < a.zhi) continue;
-                double sr[4];
-                ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
-                double w[NV], dw[NV];
-                ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
-                flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
-            }
-        }
-    }
-    if (LPC > 1) {
-#pragma unroll
-        for (int o = LPC / 2; o > 0; o >>= 1) {
-#pragma unroll
-            for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-        }
-    }
-    if (valid && sub == 0) {
-        if constexpr ((VAR & 1) != 0 || P2P) sweep_finish_full<D, P2P, (VAR & 32) == 0>(a, i, acc, p);
-        else sweep_finish<D>(a, i, acc);
-    }
-    }
-    if constexpr ((VAR & 8) != 0) pdl_wait();   // threads without a cell: nothing may run past the predecessor
-}
-
-// (VAR bit 16) the same sweep software-pipelined across grid-stride rounds: a
-// launch sized to one resident wave runs each thread over several cells, one
-// after the other, and every cell is a chain of dependent round trips
-// ((first slot, degree) -> neighbour index -> records -> epilogue).  The next
-// round's (first slot, degree) is loaded when a round starts and its first
-// neighbour index before the round's epilogue, so a later round starts with
-// its record loads; round 0's indices are loaded before griddepcontrol.wait.
-template <int D, int LPC>
-__device__ __forceinline__ void sweep_body_pipe(const SweepArgs &a)
-{
-    constexpr int NV = D + 2;
-    using RC = Rec<D>;
-    const int stride = gridDim.x * blockDim.x;            // a multiple of LPC: sub is fixed per thread
-    const int g0 = blockIdx.x * blockDim.x + threadIdx.x;
-    const int sub = g0 % LPC;
-    const int cstep = stride / LPC;
-    int i = a.cbeg + g0 / LPC;
-    int2 sd = make_int2(0, 0);
-    int jf = 0;
-    if (i < a.cend) {
-        sd = __ldg(a.sinfo + i);
-        jf = sub < sd.y ? __ldg(a.sJe + sd.x + sub) : 0;
-    }
-    pdl_wait();
-    const int total = (a.cend - a.cbeg) * LPC;
-    const int rounds = (total + stride - 1) / stride;
-    for (int r = 0; r < rounds; ++r, i += cstep) {
+        const int g = gt0 + r * nthr;
+        const int i = a.cbeg + g / LPC;
+        const int sub = g % LPC;
         const bool valid = i < a.cend;
-        const int in = i + cstep;
-        int2 sdn = make_int2(0, 0);
-        if (in < a.cend) sdn = __ldg(a.sinfo + in);
-        double acc[NV];
+        double acc[NV], accP[NV];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+        for (int q = 0; q < NV; ++q) { acc[q] = 0.0; accP[q] = 0.0; }
         if (valid) {
+            const int2 sd = __ldg(a.sinfo + i);     // (first slot, degree) in one 8-byte load
             const int e1 = sd.x + sd.y;
-            int j = jf;
-            for (int e = sd.x + sub; e < e1; e += LPC) {
+            int e = sd.x + sub;
+            int j = e < e1 ? __ldg(a.sJe + e) : 0;
+            if (pdl && r == 0) pdl_wait();
+            for (; e < e1; e += LPC) {
                 const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
-                if (j >= a.zlo && j < a.zhi) { j = jn; continue; }
                 double sr[4];
                 ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
-                double w[NV], dw[NV];
-                ld_neighbour<D>(a.rec + (size_t)j * RC::STRIDE, w, dw);
-                flux_diff<D>(w, dw, sr, a.gm1, sr[D], acc);
+                if constexpr (FF) {
+                    double wl[NV], t0[NV];
+                    ld_state<D, CG>(a.wlin + (size_t)j * WS, wl);
+                    flux_rw<D>(wl, sr, sr[D], a.gm1, t0);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) accP[q] += t0[q];
+                    if (j < a.lo || j >= a.n_own) {   // earlier color (updated in this half-sweep) or ghost
+                        double w1[NV], t1[NV];
+                        ld_state<D, CG>(a.wp + (size_t)j * WS, w1);
+                        flux_rw<D>(w1, sr, sr[D], a.gm1, t1);
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) acc[q] += t1[q] - t0[q];
+                    }
+                } else {
+                    double w1[NV], t1[NV];
+                    ld_state<D, CG>(a.wp + (size_t)j * WS, w1);
+                    flux_rw<D>(w1, sr, sr[D], a.gm1, t1);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) acc[q] += t1[q];
+                }
                 j = jn;
             }
         }
-        jf = (in < a.cend && sub < sdn.y) ? __ldg(a.sJe + sdn.x + sub) : 0;
-        sd = sdn;
         if (LPC > 1) {
 #pragma unroll
             for (int o = LPC / 2; o > 0; o >>= 1) {
 #pragma unroll
-                for (int q = 0; q < NV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                for (int q = 0; q < NV; ++q) {
+                    acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                    if constexpr (FF) accP[q] += __shfl_xor_sync(0xffffffffu, accP[q], o);
+                }
             }
         }
-        if (valid && sub == 0) sweep_finish_full<D, false>(a, i, acc);
+        if (valid && sub == 0) {
+            double wn[NV], x[kXr];
+            if constexpr (FF) {
+                double wl[NV], rr[NV], dd[2];
+                ld_state<D, CG>(a.wlin + (size_t)i * WS, wl);
+#pragma unroll
+                for (int q = 0; q < NV; ++q) rr[q] = CG ? __ldcg(a.rhs + (size_t)i * NV + q) : __ldcs(a.rhs + (size_t)i * NV + q);
+                ld2x<CG>(a.dc + 2 * (size_t)i, dd);
+                const double invD = dd[0], c = dd[1];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    const double b = wl[q] - rr[q] * invD;   // W - Rt/D
+                    x[q] = b + c * accP[q];                  // X = W - Rt/D + c P
+                    wn[q] = b - c * acc[q];                  // W' = W - Rt/D - c sum_lower (...)
+                }
+                x[NV] = c;
+                if constexpr (NV + 1 < kXr) x[NV + 1] = 0.0;
+                double *xo = a.xr + (size_t)i * kXr;
+                st2(xo, x);
+                st2(xo + 2, x + 2);
+                st2(xo + 4, x + 4);
+            } else {
+                const double *xi = a.xr + (size_t)i * kXr;
+                ld2x<CG>(xi, x);
+                ld2x<CG>(xi + 2, x + 2);
+                ld2x<CG>(xi + 4, x + 4);
+                const double c = x[NV];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) wn[q] = x[q] - c * acc[q];
+            }
+            st_state<D>(a.wp + (size_t)i * WS, wn);
+            p2p_store<D, P2P>(p, i, wn);
+            if (a.Wout) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) a.Wout[(size_t)i * NV + q] = wn[q];
+            }
+        }
     }
+    if (pdl) pdl_wait();   // threads without a cell: nothing may run past the predecessor
 }
 
-template <int D, int LPC, int MINB, int VAR = 3>
-__global__ void __launch_bounds__(256, MINB) k_sweep(SweepArgs a)
-{
-    pdl_enter();
-    sweep_body<D, LPC, VAR, false>(a, P2PArgs{});
-}
-
-// the default sweep launch: 128-thread blocks, 8 per SM (GMG_SWEEP_BS=256 -> k_sweep)
-template <int D, int LPC, int VAR = 3 | 8, int MINB = 8>
-__global__ void __launch_bounds__(128, MINB) k_sweep128(SweepArgs a)
+// the sweep launch: 128-thread blocks, 8 per SM (FF, with its second set of
+// accumulators: 6 per SM), grid = one resident wave
+template <int D, int LPC, bool FF>
+__global__ void __launch_bounds__(128, FF ? 6 : 8) k_sweep(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
-    if constexpr ((VAR & 16) != 0) sweep_body_pipe<D, LPC>(a);
-    else sweep_body<D, LPC, VAR, false>(a, P2PArgs{});
-}
-
-// 64-thread blocks, 16 per SM (GMG_SWEEP_BS=64): finer-grained block
-// scheduling for the partial last round of a grid-stride color launch
-template <int D, int LPC>
-__global__ void __launch_bounds__(64, 16) k_sweep64(SweepArgs a)
-{
-    pdl_launch_dependents();
-    sweep_body<D, LPC, 3 | 8, false>(a, P2PArgs{});
+    sweep_cells<D, LPC, FF, false, false>(a, P2PArgs{}, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x,
+                                          true);
 }
 
 __device__ __forceinline__ int ld_acquire_sys(const int *p)
@@ -741,8 +580,8 @@ __device__ __forceinline__ void st_release_sys(int *p, int v)
 
 // the sweep with the fused halo (see P2PArgs).  Launched for every phase on
 // every rank, also with no cells, so that all phase counts advance together.
-template <int D, int LPC>
-__global__ void __launch_bounds__(256, 4) k_sweep_p2p(SweepArgs a, P2PArgs p)
+template <int D, int LPC, bool FF>
+__global__ void __launch_bounds__(256, FF ? 3 : 4) k_sweep_p2p(SweepArgs a, P2PArgs p)
 {
     __shared__ int s_bad;
     if (threadIdx.x == 0) {
@@ -756,7 +595,8 @@ __global__ void __launch_bounds__(256, 4) k_sweep_p2p(SweepArgs a, P2PArgs p)
         }
     }
     __syncthreads();
-    if (!s_bad) sweep_body<D, LPC, 3, true>(a, p);
+    if (!s_bad)
+        sweep_cells<D, LPC, FF, false, true>(a, p, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, false);
     // publish: every block orders its peer stores before its arrival on the
     // done counter (gpu scope); the last block to arrive -- which has observed
     // all arrivals -- fences at system scope and releases the new phase count
@@ -774,15 +614,14 @@ __global__ void __launch_bounds__(256, 4) k_sweep_p2p(SweepArgs a, P2PArgs p)
     }
 }
 
-// restriction to a coarse level (a8, A15) into the coarse record's
-// W_lin, plus dW = 0 for its sweeps
+// restriction to a coarse level (a8, A15): W0 into the coarse
+// W_lin record, Res*, alpha = min over the children
 template <int D>
 __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const double *__restrict__ Wf,
                                                   const double *__restrict__ Rf)
 {
     pdl_enter();
     constexpr int NV = D + 2;
-    using RC = Rec<D>;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C.n) return;
     const int k0 = C.child[c], k1 = C.child[C.n + c];
@@ -798,52 +637,38 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
         a = fmin(a, Fn.alpha[k1]);
     }
     const double vc = C.vol[c];
-    double *rc = C.rec + (size_t)c * RC::STRIDE;
     const size_t o = (size_t)c * NV;
 #pragma unroll
     for (int q = 0; q < NV; ++q) { w[q] = w[q] / vc; C.Rs[o + q] = r[q]; }
-    // whole 32-byte chunks (no partial-sector writes): W_lin, dW = 0; the 3D
-    // record's 1/D and alpha/2 slots are zeroed too -- the next prepare sets them
-    if constexpr (D == 3) {
-        const double c0[4] = {w[0], w[1], w[2], w[3]}, c1[4] = {w[4], 0.0, 0.0, 0.0}, c2[4] = {0.0, 0.0, 0.0, 0.0};
-        st4(rc, c0);
-        st4(rc + 4, c1);
-        st4(rc + 8, c2);
-    } else {
-        const double c1[4] = {0.0, 0.0, 0.0, 0.0};
-        st4(rc, w);
-        st4(rc + 4, c1);
-    }
+    st_state<D>(C.wlin + (size_t)c * Wp<D>::STRIDE, w);
     C.alpha[c] = a;
 }
 
 // DF-limited prolongation, both levels fused (a15, A13, A14):
-//   W_0 += alpha_0 (dW_1 + alpha_1 dW_2[parent_1])[parent_0]
+//   W_0 += alpha_0 ((W_1 - W0_1) + alpha_1 (W_2 - W0_2)[parent_1])[parent_0]
 template <int D>
 __global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLevel C2, int nl)
 {
     pdl_enter();
-    constexpr int NV = D + 2;
-    using RC = Rec<D>;
+    constexpr int NV = D + 2, WS = Wp<D>::STRIDE;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= F0.n) return;
     const int p = F0.parent[i];
     double corr[NV];
-    const double *r1 = C1.rec + (size_t)p * RC::STRIDE + RC::DW;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) corr[q] = r1[q];
+    for (int q = 0; q < NV; ++q) corr[q] = C1.W[(size_t)p * NV + q] - C1.wlin[(size_t)p * WS + q];
     if (nl >= 3) {
         const int pp = C1.parent[p];
         const double a1 = C1.alpha[p];
-        const double *r2 = C2.rec + (size_t)pp * RC::STRIDE + RC::DW;
 #pragma unroll
-        for (int q = 0; q < NV; ++q) corr[q] += a1 * r2[q];
+        for (int q = 0; q < NV; ++q) corr[q] += a1 * (C2.W[(size_t)pp * NV + q] - C2.wlin[(size_t)pp * WS + q]);
     }
     const double a0 = F0.alpha[i];
 #pragma unroll
     for (int q = 0; q < NV; ++q) F0.W[(size_t)i * NV + q] += a0 * corr[q];
 }
 
+// ---------------------------------------------------------------------------
 // natural SoA [ncomp][N]  <->  local AoS (stride, offset), n local cells
 __global__ void k_to_internal(int n, int N, int ncomp, const int *__restrict__ perm, const double *__restrict__ src,
                               double *__restrict__ dst, int stride, int offset)
@@ -860,6 +685,15 @@ __global__ void k_to_natural(int n, int N, int ncomp, const int *__restrict__ pe
     if (i >= n) return;
     const int nat = perm[i];
     for (int q = 0; q < ncomp; ++q) dst[(size_t)q * N + nat] = src[(size_t)i * stride + offset + q];
+}
+// dW = W' - W_lin of n owned cells -> natural SoA [ncomp][N] (gmg_smooth)
+__global__ void k_diff_to_natural(int n, int N, int ncomp, const int *__restrict__ perm, const double *__restrict__ a,
+                                  const double *__restrict__ b, int stride, double *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int nat = perm[i];
+    for (int q = 0; q < ncomp; ++q) dst[(size_t)q * N + nat] = a[(size_t)i * stride + q] - b[(size_t)i * stride + q];
 }
 // owned-compact [ncomp][n] (SoA, local owned order) <-> AoS [n][ncomp]
 __global__ void k_soa_to_aos(int n, int ncomp, const double *__restrict__ src, double *__restrict__ dst)

@@ -394,10 +394,10 @@ void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *p
 
 // Domain of `rank` on a global level: owned cells in color
 // blocks (boundary cells -- a face neighbour on another rank -- first), inside
-// a block by the Morton key of the centroid when chunk_cells > 0 (natural id
-// otherwise; RCB chunks for the dependency-driven sweep), then one layer of
-// ghosts in (owner, color, natural id) order; local faces = faces touching an
-// owned cell, ordered by their first local cell; layouts over owned cells:
+// a block by the Morton key of the centroid when `morton` (natural id
+// otherwise), then one layer of ghosts in (owner, color, natural id) order;
+// local faces = faces touching an owned cell, ordered by their first local
+// cell; layouts over owned cells:
 //  * gather slots (residual/prepare, thread per cell): SELL-32 -- per color,
 //    chunks of 32 consecutive cells, entries [slot][lane], chunk padded to its
 //    max degree.  Slots: interior faces (ascending id) then boundary faces.
@@ -407,7 +407,7 @@ void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *p
 //    with A = sigma S n oriented outward from the cell.
 //  * halo plan grouped (color, peer), natural id ascending within a group, so
 //    a sender's group equals the receiver's group element by element.
-void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cells, bool flow)
+void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton)
 {
     const int d = G.dim;
     const int64_t N = G.n;
@@ -439,13 +439,10 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
         auto mid = std::stable_partition(b0, b1, [&](int64_t nat) { return bnd[nat] != 0; });
         D.nbnd[c] = (int64_t)(mid - b0);
     }
-    // single domain: spatial chunks of ~chunk_cells cells (RCB of the
-    // centroids); inside each color block the cells are ordered (chunk,
-    // natural id) -- neighbours of consecutive cells are then close in memory
-    // (better L2 reuse of the gathered records, DESIGN.md §6 v13) -- and for
-    // the dependency-driven sweep (color c, chunk x) is a contiguous segment
-    D.nchunk = 0;
-    if (chunk_cells > 0 && !flow) {
+    // single domain: inside each color block the cells are ordered by the
+    // Morton (Z-order) key of their centroid -- neighbours of consecutive cells
+    // are then close in memory (L2 reuse of the gathered records, DESIGN.md §6 v13)
+    if (morton) {
         // Morton (Z-order) key of the centroid: the same spatial grouping as
         // fine RCB chunks at a fraction of the setup cost
         double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
@@ -477,47 +474,6 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
         for (int c = 0; c < G.ncolor; ++c) {
             std::sort(D.l2n.begin() + D.blk[c], D.l2n.begin() + D.blk[c] + D.nbnd[c], cmp);
             std::sort(D.l2n.begin() + D.blk[c] + D.nbnd[c], D.l2n.begin() + D.blk[c + 1], cmp);
-        }
-    }
-    if (chunk_cells > 0 && N == D.n_own && flow) {
-        const int K = (int)std::max<int64_t>(1, (N + chunk_cells - 1) / chunk_cells);
-        std::vector<int32_t> ch(N, 0);
-        partition_rcb(N, d, G.ctr.data(), K, ch.data());
-        {   // stable counting sort of every color block by chunk
-            std::vector<int64_t> cnt(K + 1), out;
-            for (int c = 0; c < G.ncolor; ++c) {
-                std::fill(cnt.begin(), cnt.end(), 0);
-                for (int64_t i = D.blk[c]; i < D.blk[c + 1]; ++i) cnt[ch[D.l2n[i]] + 1]++;
-                std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
-                out.resize(D.blk[c + 1] - D.blk[c]);
-                for (int64_t i = D.blk[c]; i < D.blk[c + 1]; ++i) out[cnt[ch[D.l2n[i]]]++] = D.l2n[i];
-                std::copy(out.begin(), out.end(), D.l2n.begin() + D.blk[c]);
-            }
-        }
-        D.nchunk = K;
-        D.seg.assign((size_t)G.ncolor * (K + 1), 0);
-        for (int c = 0; c < G.ncolor; ++c) {
-            int64_t *sg = D.seg.data() + (size_t)c * (K + 1);
-            std::vector<int64_t> cnt(K + 1, 0);
-            for (int64_t i = D.blk[c]; i < D.blk[c + 1]; ++i) cnt[ch[D.l2n[i]] + 1]++;
-            sg[0] = D.blk[c];
-            for (int x = 0; x < K; ++x) sg[x + 1] = sg[x] + cnt[x + 1];
-        }
-        std::vector<std::vector<int32_t>> adj(K);
-        for (int64_t f = 0; f < G.nf; ++f) {
-            const int64_t l = G.left[f], r = G.right[f];
-            if (r < 0 || ch[l] == ch[r]) continue;
-            adj[ch[l]].push_back(ch[r]);
-            adj[ch[r]].push_back(ch[l]);
-        }
-        D.cnoff.assign(K + 1, 0);
-        D.cnidx.clear();
-        for (int x = 0; x < K; ++x) {
-            auto &a = adj[x];
-            std::sort(a.begin(), a.end());
-            a.erase(std::unique(a.begin(), a.end()), a.end());
-            D.cnidx.insert(D.cnidx.end(), a.begin(), a.end());
-            D.cnoff[x + 1] = (int32_t)D.cnidx.size();
         }
     }
     for (int64_t i = 0; i < D.n_own; ++i) n2l[D.l2n[i]] = (int32_t)i;
@@ -654,27 +610,6 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, int chunk_cel
             }
         }
     }
-    // device sweep slots: CSR (entry of slot s of cell i
-    // = ell_cell[i] + s * ell_stride[i]; the indirection lets the layout be
-    // swapped for ELL variants, which measured slower on the coarse levels)
-    D.ell_cell.assign(D.soffc.begin(), D.soffc.end() - 1);
-    D.ell_stride.assign(D.n_own, 1);
-    // slot-parallel sweep groups: per color, runs of whole cells whose slots fit in 256 lanes
-    D.sp_off.assign(G.ncolor + 1, 0);
-    D.sp_cell.clear();
-    for (int c = 0; c < G.ncolor; ++c) {
-        D.sp_off[c] = (int64_t)D.sp_cell.size();
-        int64_t i = D.blk[c];
-        D.sp_cell.push_back((int32_t)i);
-        while (i < D.blk[c + 1]) {
-            int slots = 0, cells = 0;
-            while (i < D.blk[c + 1] && cells < 256 && slots + D.deg_int[i] <= 256) { slots += D.deg_int[i]; ++i; ++cells; }
-            if (cells == 0) throw std::runtime_error("cell with more than 256 interior faces");
-            D.sp_cell.push_back((int32_t)i);
-        }
-    }
-    D.sp_off[G.ncolor] = (int64_t)D.sp_cell.size();
-
     // halo plan
     for (int64_t g = D.n_own; g < D.n_loc; ++g) D.peers.push_back(G.part_of(D.l2n[g]));
     std::sort(D.peers.begin(), D.peers.end());

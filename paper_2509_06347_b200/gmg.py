@@ -21,7 +21,10 @@ LIBPATH = os.path.join(_HERE, "libgmg.so")
 GMG_OK, GMG_EINVAL, GMG_ETOPO, GMG_ECOLOR, GMG_ESTALL, GMG_ENOMEM, GMG_ECUDA, GMG_ENCCL, GMG_ENONFINITE, GMG_ESTATE = range(10)
 STATUS = ["GMG_OK", "GMG_EINVAL", "GMG_ETOPO", "GMG_ECOLOR", "GMG_ESTALL", "GMG_ENOMEM", "GMG_ECUDA", "GMG_ENCCL",
           "GMG_ENONFINITE", "GMG_ESTATE"]
-K_FACE, K_GATHER, K_SWEEP, K_RESTRICT, K_PROLONG, K_NORM, K_HO_RECON, K_HO_FLUX, K_COUNT = range(9)
+K_FACE, K_GATHER, K_SWEEP, K_RESTRICT, K_PROLONG, K_NORM, K_HO_RECON, K_HO_FLUX, K_HALO, K_COUNT = range(10)
+K_NAMES = ["face", "gather", "sweep", "restrict", "prolong", "norm", "ho_recon", "ho_flux", "halo"]
+# gmg_get_level_field fields (include/gmg.h)
+FIELD_W, FIELD_W0, FIELD_DW, FIELD_RS, FIELD_F, FIELD_RT, FIELD_ALPHA = range(7)
 K_NAMES = ["face", "gather", "sweep", "restrict", "prolong", "norm", "ho_recon", "ho_flux"]
 
 # every symbol include/gmg.h declares
@@ -31,7 +34,7 @@ ABI_SYMBOLS = ["gmg_set_state_owned_async", "gmg_get_state_owned_async", "gmg_se
                "gmg_get_level_info", "gmg_get_maps", "gmg_get_level_geometry", "gmg_workspace_bytes",
                "gmg_set_workspace", "gmg_set_state", "gmg_set_level_state", "gmg_get_state", "gmg_set_alpha",
                "gmg_residual", "gmg_set_level_inputs", "gmg_smooth", "gmg_vcycle", "gmg_profile_vcycle",
-               "gmg_time_smooth", "gmg_vcycle_launches", "gmg_partition_rcb", "gmg_get_halo", "gmg_p2p_layout",
+               "gmg_time_smooth", "gmg_vcycle_launches", "gmg_vcycle_visits", "gmg_get_level_field", "gmg_partition_rcb", "gmg_get_halo", "gmg_p2p_layout",
                "gmg_p2p_import", "gmg_get_p2p_targets", "gmg_p2p_emulate_smooth", "gmg_last_error", "gmg_destroy"]
 
 
@@ -48,7 +51,8 @@ class Options(C.Structure):
                 ("df_mode", C.c_int), ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p),
                 ("device", C.c_int), ("stream", C.c_void_p), ("beta", C.c_double), ("local_domains", C.c_int),
                 ("setup_device", C.c_int), ("fine_operator", C.c_int), ("ho_c1", C.c_double), ("ho_c2", C.c_double),
-                ("ho_gam0", C.c_double), ("ho_eps", C.c_double)]
+                ("ho_gam0", C.c_double), ("ho_eps", C.c_double), ("skip_repeat", C.c_int), ("p2p", C.c_int),
+                ("overlap", C.c_int), ("l2_persist_mb", C.c_int), ("sweep_lanes", C.c_int), ("pdl", C.c_int)]
 
 
 _lib = None
@@ -85,6 +89,8 @@ def lib():
             "gmg_profile_vcycle": (I, [P, I, P, P, P]),
             "gmg_time_smooth": (I, [P, I, I, I, P, P, P]),
             "gmg_vcycle_launches": (I64, [P]),
+            "gmg_vcycle_visits": (I64, [P]),
+            "gmg_get_level_field": (I, [P, I, I, P]),
             "gmg_partition_rcb": (I, [I64, I, P, I, P]),
             "gmg_get_halo": (I, [P, I, I, P, P, P, P, P, P, P, P, P, P, P, P]),
             "gmg_p2p_layout": (I, [P, P]),
@@ -113,11 +119,22 @@ def lib():
     return _lib
 
 
-def _ptr(a):
+def _ptr(a, count=None):
+    """Raw pointer of a float64-or-index buffer.  With `count` (the doubles the
+    call reads or writes) the buffer must be float64, contiguous and at least
+    that large: a mismatched buffer would otherwise be read or written out of
+    bounds by the library."""
     if a is None:
         return None
     if hasattr(a, "data_ptr"):
+        if count is not None:
+            import torch
+            if a.dtype != torch.float64 or not a.is_contiguous() or a.numel() < count:
+                raise ValueError(f"need a contiguous float64 tensor of >= {count} elements, got {a.dtype} "
+                                 f"{tuple(a.shape)} contiguous={a.is_contiguous()}")
         return a.data_ptr()
+    if count is not None and (a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"] or a.size < count):
+        raise ValueError(f"need a C-contiguous float64 array of >= {count} elements, got {a.dtype} {a.shape}")
     return a.ctypes.data
 
 
@@ -143,11 +160,19 @@ def _check(ctx, st, allow=()):
     return st
 
 
+_NV = {}   # context handle -> nv (for the buffer-size checks of the wrappers)
+
+
+def _nv(ctx):
+    return _NV.get(ctx.value if hasattr(ctx, "value") else ctx, 1)
+
+
 def gmg_create(opt: Options):
     h = C.c_void_p()
     st = lib().gmg_create(C.byref(opt), C.byref(h))
     if st != GMG_OK:
         raise GmgError(st, "gmg_create: invalid options")
+    _NV[h.value] = opt.dim + 2
     return h
 
 
@@ -208,16 +233,24 @@ def gmg_set_workspace(ctx, dptr, nbytes):
 def gmg_set_state(ctx, W, W_inf):
     Wk = W if hasattr(W, "data_ptr") else _f64(W)
     wi = _f64(W_inf)
-    return _check(ctx, lib().gmg_set_state(ctx, _ptr(Wk), _ptr(wi)))
+    n, _, _ = gmg_get_level_info(ctx, 0)
+    return _check(ctx, lib().gmg_set_state(ctx, _ptr(Wk, _nv(ctx) * n), _ptr(wi, _nv(ctx))))
 
 
 def gmg_set_level_state(ctx, level, W):
     Wk = W if hasattr(W, "data_ptr") else _f64(W)
-    return _check(ctx, lib().gmg_set_level_state(ctx, level, _ptr(Wk)))
+    n, _, _ = gmg_get_level_info(ctx, level)
+    return _check(ctx, lib().gmg_set_level_state(ctx, level, _ptr(Wk, _nv(ctx) * n)))
 
 
 def gmg_get_state(ctx, level, out):
-    return _check(ctx, lib().gmg_get_state(ctx, level, _ptr(out)))
+    n, _, _ = gmg_get_level_info(ctx, level)
+    return _check(ctx, lib().gmg_get_state(ctx, level, _ptr(out, _nv(ctx) * n)))
+
+
+def gmg_get_level_field(ctx, level, field, out):
+    n, _, _ = gmg_get_level_info(ctx, level)
+    return _check(ctx, lib().gmg_get_level_field(ctx, level, field, _ptr(out, (1 if field == FIELD_ALPHA else _nv(ctx)) * n)))
 
 
 def gmg_set_alpha(ctx, alpha):
@@ -259,6 +292,10 @@ def gmg_time_smooth(ctx, level, n_sweeps, reps):
 
 def gmg_vcycle_launches(ctx):
     return int(lib().gmg_vcycle_launches(ctx))
+
+
+def gmg_vcycle_visits(ctx):
+    return int(lib().gmg_vcycle_visits(ctx))
 
 
 def gmg_partition_rcb(ctr, nparts):
@@ -326,7 +363,8 @@ def gmg_p2p_emulate_smooth(ctx, level, n_sweeps, nv, n):
 def gmg_set_state_async(ctx, W, W_inf):
     """W: pinned host tensor / device tensor / array that stays alive until gmg_sync"""
     Wi = _f64(W_inf)
-    _check(ctx, lib().gmg_set_state_async(ctx, _ptr(W), _ptr(Wi)))
+    n, _, _ = gmg_get_level_info(ctx, 0)
+    _check(ctx, lib().gmg_set_state_async(ctx, _ptr(W, _nv(ctx) * n), _ptr(Wi, _nv(ctx))))
 
 
 def gmg_set_state_owned_async(ctx, W_owned, W_inf):
@@ -344,7 +382,8 @@ def gmg_vcycle_async(ctx, n_cycles):
 
 
 def gmg_get_state_async(ctx, W_out):
-    _check(ctx, lib().gmg_get_state_async(ctx, _ptr(W_out)))
+    n, _, _ = gmg_get_level_info(ctx, 0)
+    _check(ctx, lib().gmg_get_state_async(ctx, _ptr(W_out, _nv(ctx) * n)))
 
 
 def gmg_sync(ctx):
@@ -380,6 +419,7 @@ def gmg_last_error(ctx):
 
 
 def gmg_destroy(ctx):
+    _NV.pop(ctx.value if hasattr(ctx, "value") else ctx, None)
     lib().gmg_destroy(ctx)
 
 
@@ -423,7 +463,7 @@ class Solver:
             nb = gmg_workspace_bytes(self.ctx)
             self.ws = self._torch.empty(nb, dtype=self._torch.uint8, device=self.device)
             gmg_set_workspace(self.ctx, self.ws.data_ptr(), nb)
-            if self.opt.nranks > 1 and os.environ.get("GMG_P2P", "0") == "1":
+            if self.opt.nranks > 1 and self.opt.p2p == 1:
                 self._p2p_exchange()
 
     def _p2p_exchange(self):
@@ -491,6 +531,14 @@ class Solver:
 
     def vcycle_launches(self):
         return gmg_vcycle_launches(self.ctx)
+
+    def vcycle_visits(self):
+        return gmg_vcycle_visits(self.ctx)
+
+    def level_field(self, level, field):
+        out = np.zeros((1 if field == FIELD_ALPHA else self.nv, self.n_cells(level)))
+        gmg_get_level_field(self.ctx, level, field, out)
+        return out[0] if field == FIELD_ALPHA else out
 
     # NEXT-1 (fine_operator = 1 or ho_geometry = True)
     def set_ho_state(self, G=None, alpha=None):

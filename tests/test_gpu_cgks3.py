@@ -243,7 +243,6 @@ def test_partitioned_vcycles_match_oracle(name, P, monkeypatch):
     W, slopes, polynomials and Dt by halo) against the oracle on the same
     partition-constrained hierarchy."""
     from paper_2509_06347_b200 import gmg
-    monkeypatch.setenv("GMG_P2P", "0")
     m, fs = _cases()[name]
     W, Winf, _, _ = _state(m, fs, 6)
     part = gmg.gmg_partition_rcb(m.ctr, P)

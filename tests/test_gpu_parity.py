@@ -1,21 +1,17 @@
 """GPU parity: libgmg's CUDA path (through the C ABI) vs the CPU oracle on
 the same seeded inputs.  Tolerances: maps bit-exact
-(tests/test_abi_host.py); FP64 increments, states and residuals relative L2
-<= 1e-10 (BASELINE.json north_star); residual histories normalised-absolute
-|r_gpu(k) - r_orc(k)| <= 1e-10 r_orc(0).
+(tests/test_abi_host.py); FP64 increments, states, forcing and residuals
+element by element, max_i |gpu_i - ref_i| <= 1e-10 max_i |ref_i| per component
+(tests/parity.py; BASELINE.json north_star); residual histories
+normalised-absolute |r_gpu(k) - r_orc(k)| <= 1e-10 r_orc(0).
 """
 import numpy as np
 import pytest
 
 from synth import configs, state
+from tests.parity import TOL, check_levels, elem, rel
 
 pytestmark = pytest.mark.gpu
-TOL = 1e-10
-
-
-def rel(a, b):
-    nb = np.linalg.norm(b)
-    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
 @pytest.fixture(scope="module")
@@ -65,9 +61,9 @@ def test_residual_parity(G, orc, name):
     s.set_state(W, Winf)
     R, a, sig = s.residual(0)
     Ro, ao, so, _ = orc.residual(orc.Level.from_mesh(m), W, Winf)
-    assert rel(R, Ro) <= 1e-12
-    assert rel(a, ao) <= 1e-12
-    assert rel(sig, so) <= 1e-13
+    assert elem(R, Ro) <= 1e-12
+    assert elem(a, ao, np.ones_like(ao)) <= 1e-12
+    assert elem(sig, so) <= 1e-13
     s.close()
 
 
@@ -85,7 +81,7 @@ def test_fine_smooth_parity(G, orc, name, n_sweeps):
     col, nc = orc.color(lv)
     D = orc.diag(S, alpha, 10.0, 0.5)
     dWo = orc.smooth(lv, W, R, alpha, D, rf, col, nc, n_sweeps)
-    assert rel(dW, dWo) <= TOL
+    assert elem(dW, dWo) <= TOL
     s.close()
 
 
@@ -109,11 +105,13 @@ def test_coarse_smooth_parity(G, orc, name):
         dW = s.smooth(l, 6)
         D = orc.diag(S, alpha, 10.0, 0.5)
         dWo = orc.smooth(lv, Wl, R, alpha, D, rf, H[l]["color"], H[l]["ncolor"], 6)
-        assert rel(dW, dWo) <= TOL, f"level {l}"
+        assert elem(dW, dWo) <= TOL, f"level {l}"
     s.close()
 
 
-def _vcycle_pair(G, orc, m, Winf, W, n_cycles, **kw):
+def _vcycle_pair(G, orc, m, Winf, W, n_cycles, levels=True, **kw):
+    """n_cycles V-cycles on both sides; with `levels` the coarse levels of the
+    last cycle are compared element by element (tests/parity.check_levels)."""
     opt = orc.Options(**{k: v for k, v in kw.items() if k in orc.Options.__dataclass_fields__})
     fields = [f[0] for f in G.Options._fields_]
     s = G.Solver(m, n_levels=opt.n_levels, **{k: v for k, v in kw.items() if k in fields and k != "n_levels"})
@@ -124,7 +122,10 @@ def _vcycle_pair(G, orc, m, Winf, W, n_cycles, **kw):
     hist = s.vcycle(n_cycles)
     Wg = s.get_state(0)
     H = orc.build_hierarchy(m, opt.n_levels, opt.skew_limit)
-    Wo, ho = orc.vcycle(H, W, Winf, opt, n_cycles, user_alpha=ua)
+    trace = []
+    Wo, ho = orc.vcycle(H, W, Winf, opt, n_cycles, user_alpha=ua, trace=trace)
+    if levels and len(H) > 1:
+        check_levels(G, s, trace[-(len(H) - 1):], len(H))
     s.close()
     return Wg, hist, Wo, ho
 
@@ -133,7 +134,7 @@ def _vcycle_pair(G, orc, m, Winf, W, n_cycles, **kw):
 def test_vcycle_parity_short(G, orc, name):
     m, Winf, W = _case(name)
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3)
-    assert rel(Wg, Wo) <= TOL
+    assert elem(Wg, Wo) <= TOL
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
 
 
@@ -142,13 +143,13 @@ def test_vcycle_parity_100_cycles_config1(G, orc):
     m, Winf, W = _case("config1")
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 100)
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
-    assert rel(Wg, Wo) <= TOL
+    assert elem(Wg, Wo) <= TOL
 
 
 def test_vcycle_parity_fine_mclusgs(G, orc):
     m, Winf, W = _case("box")
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, fine_smoother=1)
-    assert rel(Wg, Wo) <= TOL
+    assert elem(Wg, Wo) <= TOL
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
 
 
@@ -157,20 +158,20 @@ def test_vcycle_parity_df_modes(G, orc, df_mode):
     m, Winf, W = _case("config1")
     ua = np.random.default_rng(3).uniform(0, 1, m.n_cells) if df_mode == 1 else None
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, df_mode=df_mode, _alpha=ua, beta=0.7)
-    assert rel(Wg, Wo) <= TOL
+    assert elem(Wg, Wo) <= TOL
 
 
 def test_vcycle_parity_fixed_beta_3d(G, orc):
     m, Winf, W = _case("sphere_small")
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, df_mode=3, beta=0.3)
-    assert rel(Wg, Wo) <= TOL
+    assert elem(Wg, Wo) <= TOL
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
 
 
 def test_vcycle_two_levels(G, orc):
     m, Winf, W = _case("config1")
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 2, n_levels=2)
-    assert rel(Wg, Wo) <= TOL
+    assert elem(Wg, Wo) <= TOL
 
 
 def test_freestream_fixed_point_gpu(G):
@@ -205,6 +206,7 @@ def test_nonfinite_detected(G):
     with pytest.raises(G.GmgError) as e:
         s.vcycle(1)
     assert e.value.status == G.GMG_ENONFINITE
+    assert "level" in str(e.value) and "cell" in str(e.value)    # level and cell named
     s.close()
 
 
@@ -231,71 +233,98 @@ def test_configs_2_3_full_size_vcycles(G, orc, k):
     fs = configs.FREESTREAM[k]
     W = state.bow_shock(m, *fs) if k == 3 else state.perturbed(m, *fs, eps=0.05, seed=2)
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, state.winf(*fs), W, 5)
-    assert rel(Wg, Wo) <= TOL
+    assert elem(Wg, Wo) <= TOL
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
 
 
 @pytest.mark.slow
-def test_config4_full_size_vcycle(G, orc):
-    """BASELINE configs[3] (the bench workload) at full size: maps bit-exact
-    and one V-cycle (the bench's launch configuration) vs the oracle."""
+def test_config4_full_size_vcycles(G, orc):
+    """BASELINE configs[3] (the bench workload, 1 M cells) at full size, in the
+    bench's launch configuration: 10 V-cycles, history, final state and the
+    last cycle's coarse levels element by element vs the oracle."""
     m = configs.config(4)
     fs = configs.FREESTREAM[4]
     W = state.bow_shock(m, *fs)
     Winf = state.winf(*fs)
-    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 1)
-    assert rel(Wg, Wo) <= TOL
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 10)
+    assert elem(Wg, Wo) <= TOL
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
 
 
-def _skip_runs(G, name, monkeypatch, var, values, fixed):
+@pytest.mark.parametrize("name", ["config1", "sphere_small", "cyl_small"])
+def test_repeated_phase_skip_is_exact(G, name):
+    """The same-color phase at each sweep turn (c_N then c_N, c_1 then c_1) is
+    dropped by default (gmg_options.skip_repeat).  A cell's update never reads
+    its own state and its other-colored neighbours do not change in between,
+    so the repeated phase recomputes the same values: bit for bit at the
+    backward -> forward turns; at the first forward -> backward turn the
+    repeated phase evaluates the same sum in the W' form X - c sum T(W')
+    instead of the first-forward form W - Rt/D - c sum [T(W') - T(W)]
+    (DESIGN.md §6), equal up to rounding.  Running every phase of Algorithm 2
+    must therefore agree to rounding (and execute more cell-updates)."""
     m, Winf, W = _case(name)
     out = {}
-    for k, v in fixed.items():
-        monkeypatch.setenv(k, v)
-    for v in values:
-        monkeypatch.setenv(var, v)
-        s = G.Solver(m, n_levels=3)
+    for v in (0, 1):
+        s = G.Solver(m, n_levels=3, skip_repeat=v)
         s.set_state(W, Winf)
         h = s.vcycle(3)
         Wv = s.get_state(0)
         coarse = [s.get_state(l) for l in (1, 2)]
         s.set_level_state(1, coarse[0])
         dW = s.smooth(1, 4)
-        out[v] = (h, Wv, coarse, dW)
+        out[v] = (h, Wv, coarse, dW, s.vcycle_visits())
         s.close()
-    return out
-
-
-@pytest.mark.parametrize("name", ["config1", "sphere_small", "cyl_small"])
-def test_repeated_phase_skip_is_bit_exact(G, name, monkeypatch):
-    """The same-color phase at each sweep turn (c_N then c_N, c_1 then c_1) is
-    dropped by default; running every phase of Algorithm 2 must give the SAME
-    bits (a cell's update never reads its own dW, and its other-colored
-    neighbours do not change in between: the kernel would recompute the
-    identical arithmetic on identical inputs)."""
-    out = _skip_runs(G, name, monkeypatch, "GMG_SKIP_REPEAT", ("0", "1"), {"GMG_SKIP_ZERO": "1"})
-    a, b = out["0"], out["1"]
-    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-    for x, y in zip(a[2], b[2]):
-        assert np.array_equal(x, y)
-    assert np.array_equal(a[3], b[3])
-
-
-@pytest.mark.parametrize("name", ["config1", "sphere_small", "cyl_small"])
-def test_zero_term_skip_is_roundoff_exact(G, orc, name, monkeypatch):
-    """First forward half-sweep: later-colored neighbours still hold dW = +0,
-    so their terms T(W+0) - T(W) - r 0 are exactly 0 in exact arithmetic (and
-    in the oracle, which has no FMA contraction).  Skipping them changes the
-    device result only by the FMA-contraction roundoff of those would-be-zero
-    differences."""
-    out = _skip_runs(G, name, monkeypatch, "GMG_SKIP_ZERO", ("0", "1"), {"GMG_SKIP_REPEAT": "1"})
-    a, b = out["0"], out["1"]
-    assert rel(a[1], b[1]) <= 1e-13
+    a, b = out[0], out[1]
     assert np.all(np.abs(a[0] - b[0]) <= 1e-13 * a[0][0][None, :])
+    assert elem(a[1], b[1]) <= 1e-13
     for x, y in zip(a[2], b[2]):
-        assert rel(x, y) <= 1e-13
-    assert rel(a[3], b[3]) <= 1e-12
+        assert elem(x, y) <= 1e-13
+    assert elem(a[3], b[3]) <= 1e-12
+    assert b[4] < a[4]                 # fewer cell-updates executed
+
+
+@pytest.mark.parametrize("lanes", [1, 4])
+def test_sweep_lanes_parity(G, orc, lanes):
+    """1 and 4 lanes per cell (another summation order of a cell's slots)."""
+    m, Winf, W = _case("sphere_small")
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 3, sweep_lanes=lanes)
+    assert elem(Wg, Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+
+
+@pytest.mark.parametrize("name", ["cyl_small", "sphere_small"])
+def test_per_cycle_correction_elementwise(G, orc, name):
+    """The correction one V-cycle applies to the fine state, W_out - W_in, from
+    the SAME input on both sides (the oracle's state of cycle k), element by
+    element for 8 consecutive cycles of a bow-shock case (DF alpha spanning
+    (0, 1], DF-limited prolongation)."""
+    m, Winf, W = _case(name)
+    H = orc.build_hierarchy(m, 3, 0.5)
+    s = G.Solver(m, n_levels=3)
+    Wk = W
+    for k in range(8):
+        s.set_state(Wk, Winf)
+        s.vcycle(1)
+        Wg = s.get_state(0)
+        Wn, _ = orc.vcycle(H, Wk, Winf, orc.Options(), 1)
+        assert elem(Wg - Wk, Wn - Wk) <= TOL, k
+        Wk = Wn
+    s.close()
+
+
+@pytest.mark.slow
+def test_config3_100_cycles(G, orc):
+    """BASELINE configs[2] (Mach-8 cylinder, 100k cells, bow shock, DF-adaptive
+    relaxation with alpha spanning (0, 1], DF-limited prolongation across the
+    shock) over 100 V-cycles: residual history per component within
+    1e-10 of r0, final state and the last cycle's coarse levels element by
+    element."""
+    m = configs.config(3)
+    fs = configs.FREESTREAM[3]
+    W = state.bow_shock(m, *fs)
+    Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, state.winf(*fs), W, 100)
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+    assert elem(Wg, Wo) <= TOL
 
 
 @pytest.mark.slow
@@ -309,7 +338,7 @@ def test_config2_long_history(G, orc):
     W = state.uniform(m, *fs)
     Wg, hist, Wo, ho = _vcycle_pair(G, orc, m, Winf, W, 200)
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
-    assert rel(Wg, Wo) <= TOL
+    assert elem(Wg, Wo) <= TOL
 
 
 def test_pipelined_host_io_equals_synchronous():
@@ -366,30 +395,3 @@ def test_owned_layout_host_io_equals_synchronous():
     s.close()
     for k in range(len(Ws)):
         assert np.array_equal(outs[k].numpy(), ref[k][:, own]), k
-
-
-@pytest.mark.parametrize("var, val", [("GMG_SWEEPV", "19"), ("GMG_MINB", "9"), ("GMG_SWEEP_BS", "64")],
-                         ids=["pipelined_rounds", "minb9", "bs64"])
-def test_sweep_launch_variants_bit_exact(G, var, val, monkeypatch):
-    """Launch-shape variants of the sweep kept for the record (rounds
-    software-pipelined, 9 blocks per SM) keep every cell's arithmetic -- the same
-    lanes per cell, slot order per lane and shuffle tree -- so they reproduce the
-    default bits.  The mesh (sphere shell, ~360 k cells) is large enough that the
-    big color blocks take several grid-stride rounds of the one-wave launch."""
-    m = configs.sphere_shell(24)
-    fs = configs.FREESTREAM[4]
-    W, Winf = state.bow_shock(m, *fs), state.winf(*fs)
-    out = []
-    for v in (None, val):
-        if v is None:
-            monkeypatch.delenv(var, raising=False)
-        else:
-            monkeypatch.setenv(var, v)
-        s = G.Solver(m, n_levels=3)
-        s.set_state(W, Winf)
-        h = s.vcycle(2)
-        out.append((h, s.get_state(0), s.get_state(1)))
-        s.close()
-    (h0, W0, C0), (h1, W1, C1) = out
-    assert np.array_equal(h0, h1) and np.array_equal(W0, W1) and np.array_equal(C0, C1)
-    assert np.all(np.isfinite(W0))

@@ -85,13 +85,45 @@ def test_device_setup_partitioned(G, P):
         assert np.array_equal(c0, c1) and np.array_equal(p0, p1) and np.array_equal(q0, q1)
 
 
-def test_device_setup_full_size(G):
-    """config 4 (998,400 cells), the benchmark's mesh"""
+def _oracle_maps(orc, m, part=None):
+    """the oracle's hierarchy (O1-O3): per level (color, perm, parent, geometry)"""
+    H = orc.build_hierarchy(m, 3, 0.5, part=part)
+    out = []
+    for k, e in enumerate(H):
+        lv = e["level"]
+        par = e["parent"] if e["parent"] is not None else np.full(lv.n, -1, np.int64)
+        geo = dict(vol=lv.vol, ctr=lv.ctr, left=lv.left, right=lv.right, avec=lv.avec, fctr=lv.fctr,
+                   ngauss=lv.ngauss)
+        out.append((e["color"], orc.perm_from_color(e["color"]), par, geo))
+    return out
+
+
+@pytest.mark.slow
+def test_device_setup_full_size_vs_oracle(G, orc):
+    """config 4 (998,400 cells, the benchmark's mesh): the DEVICE-built
+    hierarchy (Algorithms 1 and 3 on the GPU) against the ORACLE's, bit for
+    bit -- colors, renumbering, parent maps and the coarse geometry."""
     m = configs.config(4)
-    h = _hier(G, m, 0)
     d = _hier(G, m, 1)
-    for (c0, p0, q0, _), (c1, p1, q1, _) in zip(h, d):
-        assert np.array_equal(c0, c1) and np.array_equal(p0, p1) and np.array_equal(q0, q1)
+    o = _oracle_maps(orc, m)
+    assert len(d) == len(o)
+    for l, ((c1, p1, q1, g1), (c0, p0, q0, g0)) in enumerate(zip(d, o)):
+        assert np.array_equal(c1, c0), l
+        assert np.array_equal(p1, p0), l
+        assert np.array_equal(q1, q0), l
+        for k in g0:
+            assert np.array_equal(np.asarray(g1[k]).ravel(), np.asarray(g0[k]).ravel()), (l, k)
+
+
+@pytest.mark.parametrize("name", ["sphere", "disconnected"])
+def test_device_setup_vs_oracle(G, orc, name):
+    m = MESHES[name]()
+    d = _hier(G, m, 1)
+    o = _oracle_maps(orc, m)
+    for (c1, p1, q1, g1), (c0, p0, q0, g0) in zip(d, o):
+        assert np.array_equal(c1, c0) and np.array_equal(p1, p0) and np.array_equal(q1, q0)
+        for k in g0:
+            assert np.array_equal(np.asarray(g1[k]).ravel(), np.asarray(g0[k]).ravel()), k
 
 
 def test_device_built_hierarchy_runs_identically(G):

@@ -60,8 +60,9 @@ MUTANTS = [
     ("diag_cfl_swapped", C, "(1.0 - alpha[i]) * (Sigma[i] / cfl_exp)", "(1.0 - alpha[i]) * (Sigma[i] / cfl_imp)",
      P1, "test_hybrid_diagonal_examples", {}),
     # residual / KFVS (O4)
-    ("residual_right_sign", C, "for (int q = 0; q < nv; ++q) R[q * n + r] -= S * F[q];",
-     "for (int q = 0; q < nv; ++q) R[q * n + r] += S * F[q];", P1, "test_freestream_residual_zero", {"mk": 1}),
+    ("residual_right_sign", C, "for (int q = 0; q < nv; ++q) R[q * n + r] -= S * fF[q * nf + f];",
+     "for (int q = 0; q < nv; ++q) R[q * n + r] += S * fF[q * nf + f];", P1, "test_freestream_residual_zero",
+     {"mk": 1}),
     ("kfvs_recurrence_coeff", C, "double m3 = U * m2 + (2.0 / (2.0 * lambda)) * m1;",
      "double m3 = U * m2 + (1.0 / (2.0 * lambda)) * m1;", P1, "test_kfvs_equal_states_give_euler_flux",
      {"dim": 3}),

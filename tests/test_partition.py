@@ -131,10 +131,9 @@ def test_p2p_targets_local_domains(G, name, P, monkeypatch):
     """Fused P2P halo addressing (host side): each owned boundary cell's
     targets are exactly the peers' ghost copies of that cell, and every ghost
     of every domain is targeted by its owner exactly once."""
-    monkeypatch.setenv("GMG_P2P", "1")
     m = MESHES[name]()
     part = G.gmg_partition_rcb(m.ctr, P)
-    s = G.Solver(m, n_levels=3, build_only=True, part=part, local_domains=P)
+    s = G.Solver(m, n_levels=3, build_only=True, part=part, local_domains=P, p2p=1)
     for l in range(s.n_levels):
         plans = _plans(s, P, l)
         ghost_of = {r: p["ghost"] for r, p in enumerate(plans)}
@@ -154,13 +153,12 @@ def _worker(rank, world, port, name, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ["GMG_P2P"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2509_06347_b200 import gmg
         m = MESHES[name]()
         part = gmg.gmg_partition_rcb(m.ctr, world)
-        s = gmg.Solver(m, n_levels=3, build_only=True, part=part, nranks=world, rank=rank, nccl_id=bytes(128))
+        s = gmg.Solver(m, n_levels=3, build_only=True, part=part, nranks=world, rank=rank, nccl_id=bytes(128), p2p=1)
         ok = True
         for l in range(s.n_levels):
             mine = s.halo(l, 0)
