@@ -25,7 +25,6 @@ K_FACE, K_GATHER, K_SWEEP, K_RESTRICT, K_PROLONG, K_NORM, K_HO_RECON, K_HO_FLUX,
 K_NAMES = ["face", "gather", "sweep", "restrict", "prolong", "norm", "ho_recon", "ho_flux", "halo"]
 # gmg_get_level_field fields (include/gmg.h)
 FIELD_W, FIELD_W0, FIELD_DW, FIELD_RS, FIELD_F, FIELD_RT, FIELD_ALPHA = range(7)
-K_NAMES = ["face", "gather", "sweep", "restrict", "prolong", "norm", "ho_recon", "ho_flux"]
 
 # every symbol include/gmg.h declares
 ABI_SYMBOLS = ["gmg_set_state_owned_async", "gmg_get_state_owned_async", "gmg_set_state_async", "gmg_vcycle_async", "gmg_get_state_async", "gmg_sync",

@@ -24,14 +24,21 @@ def elem(a, b, scale=None):
     return float(np.max(np.abs(a - b).max(axis=1) / s))
 
 
-def check_levels(G, s, entries, n_levels, tol=TOL):
+def check_levels(G, s, entries, n_levels, tol=TOL, first=None):
     """Coarse levels of the last V-cycle (oracle trace entries) against the
     library's level fields, element by element: restricted state W0
     (P:643-647), restricted residual Res* (P:648-652), DF alpha (min over the
     children, A15), forcing F = Res* - R(W0) (absolute error scale
     of its operands, Res*), the smoothing increment dW and the coarse state
-    W0 + dW.  Returns the worst ratio per field."""
+    W0 + dW.  Returns the worst ratio per field.
+
+    first: the FIRST cycle's trace entries of a long run.  Then every field is
+    measured against max(|ref|, |first-cycle ref|) per component -- the
+    normalised-absolute reading SURVEY §8(c) fixes for histories (|r_gpu(k) -
+    r_orc(k)| <= 1e-10 r(0)): once a run has converged, Res*, F and dW are
+    rounding-level quantities and their relative error says nothing."""
     worst = {}
+    f0 = {t["level"]: t for t in first} if first else {}
     for t in entries:
         l = t["level"]
         got = {
@@ -44,6 +51,11 @@ def check_levels(G, s, entries, n_levels, tol=TOL):
         if l < n_levels - 1:
             got["F"] = (s.level_field(l, G.FIELD_F), t["F"], t["Rs"])
         for k, (a, b, sc) in got.items():
+            if l in f0 and k != "alpha":
+                t0 = f0[l]
+                b0 = {"W0": t0["W0"], "Rs": t0["Rs"], "dW": t0["dW"], "W": t0["W0"] + t0["dW"], "F": t0["Rs"]}[k]
+                base = np.abs(np.atleast_2d(b if sc is None else sc))
+                sc = np.maximum(base.max(axis=1, keepdims=True), np.abs(np.atleast_2d(b0)).max(axis=1, keepdims=True))
             e = elem(a, b, sc)
             worst[f"L{l}.{k}"] = e
             assert e <= tol, f"level {l} {k}: {e:.3e}"

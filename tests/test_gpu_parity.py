@@ -125,7 +125,8 @@ def _vcycle_pair(G, orc, m, Winf, W, n_cycles, levels=True, **kw):
     trace = []
     Wo, ho = orc.vcycle(H, W, Winf, opt, n_cycles, user_alpha=ua, trace=trace)
     if levels and len(H) > 1:
-        check_levels(G, s, trace[-(len(H) - 1):], len(H))
+        nc = len(H) - 1
+        check_levels(G, s, trace[-nc:], len(H), first=trace[:nc] if n_cycles >= 50 else None)
     s.close()
     return Wg, hist, Wo, ho
 
