@@ -265,7 +265,11 @@ gmg_status gmg_time_smooth(gmg_ctx *ctx, int level, int n_sweeps, int reps, doub
  * through two device staging buffers per direction; the compute stream
  * orders everything else.
  *   gmg_set_state_async: W[nv][n] natural order; the host buffer (pinned for
- *     real overlap) must stay valid and unmodified until gmg_sync.
+ *     real overlap) must stay valid and unmodified until gmg_sync, and must be
+ *     fully written by the host when the call is made (the call does not wait
+ *     for GPU work that might still be filling a host buffer).  A DEVICE
+ *     pointer is read after all work already enqueued on gmg_options.stream
+ *     (the copy waits for it), so a tensor produced on that stream is safe.
  *   gmg_vcycle_async: n_cycles V-cycles + the residual norm (history kept on
  *     the device; no host read).
  *   gmg_get_state_async: W_out[nv][n] natural order, written by gmg_sync.

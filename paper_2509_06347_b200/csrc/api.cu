@@ -1384,6 +1384,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
     if (!ctx->copy) {                      // copy stream + events of the pipelined host I/O
         CK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_call, cudaEventDisableTiming));
         for (int k = 0; k < 2; ++k) {
             CK(cudaEventCreateWithFlags(&ctx->ev_in_ready[k], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ctx->ev_in_free[k], cudaEventDisableTiming));
@@ -1784,6 +1785,18 @@ static gmg_status async_ready(gmg_ctx *ctx, bool need_state, bool natural = true
     return GMG_OK;
 }
 
+// a device pointer passed to the async host-I/O calls may be produced by work on the compute stream: order
+// the copy stream after it (host buffers need no GPU ordering; waiting for them would serialise the pipeline)
+static cudaError_t order_device_source(gmg_ctx *ctx, const void *p)
+{
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return cudaSuccess; }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return cudaSuccess;
+    cudaError_t e = cudaEventRecord(ctx->ev_call, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->copy, ctx->ev_call, 0);
+    return e;
+}
+
 gmg_status gmg_set_state_async(gmg_ctx *ctx, const double *W, const double *W_inf)
 {
     if (!ctx) return GMG_EINVAL;
@@ -1799,8 +1812,10 @@ gmg_status gmg_set_state_async(gmg_ctx *ctx, const double *W, const double *W_in
     if (ctx->graph && !same) { cudaGraphExecDestroy(ctx->graph); ctx->graph = nullptr; }
     const int k = ctx->in_slot;
     const int64_t N = ctx->lv[0].n;
-    // copy stream: wait until the compute stream has consumed this slot, then H2D
+    // copy stream: wait until the compute stream has consumed this slot, then H2D; a device source is
+    // ordered after everything already enqueued on the compute stream (it may be produced there)
     CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_in_free[k], 0));
+    CK(order_device_source(ctx, W));
     CK(cudaMemcpyAsync(ctx->stage_in[k], W, sizeof(double) * nv * N, cudaMemcpyDefault, ctx->copy));
     CK(cudaEventRecord(ctx->ev_in_ready[k], ctx->copy));
     // compute stream: scatter into every domain's local state (owned + ghosts)
@@ -1878,6 +1893,7 @@ gmg_status gmg_set_state_owned_async(gmg_ctx *ctx, const double *W_owned, const 
     const int nv = ctx->opt.dim + 2, k = ctx->in_slot;
     DevLevel &L = ctx->dom[0].dv[0];
     CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_in_free[k], 0));
+    CK(order_device_source(ctx, W_owned));
     CK(cudaMemcpyAsync(ctx->stage_in[k], W_owned, sizeof(double) * nv * L.n, cudaMemcpyDefault, ctx->copy));
     CK(cudaEventRecord(ctx->ev_in_ready[k], ctx->copy));
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in_ready[k], 0));
@@ -2271,6 +2287,7 @@ void gmg_destroy(gmg_ctx *ctx)
         cudaStreamSynchronize(ctx->copy_out);
         cudaStreamDestroy(ctx->copy);
         cudaStreamDestroy(ctx->copy_out);
+        if (ctx->ev_call) cudaEventDestroy(ctx->ev_call);
         for (int k = 0; k < 2; ++k) {
             cudaEventDestroy(ctx->ev_in_ready[k]);
             cudaEventDestroy(ctx->ev_in_free[k]);

@@ -239,6 +239,7 @@ struct gmg_ctx {
     cudaStream_t copy = nullptr, copy_out = nullptr;   // host->device / device->host copy streams
     double *stage_in[2] = {nullptr, nullptr}, *stage_out[2] = {nullptr, nullptr};   // [nv][N0] natural order
     cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
+    cudaEvent_t ev_call = nullptr;    // compute-stream position when an async call reads a device source
     int in_slot = 0, out_slot = 0;
     bool async_flag_reset = false;    // d_flag cleared for the current async epoch
 };

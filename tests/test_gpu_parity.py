@@ -396,3 +396,36 @@ def test_owned_layout_host_io_equals_synchronous():
     s.close()
     for k in range(len(Ws)):
         assert np.array_equal(outs[k].numpy(), ref[k][:, own]), k
+
+
+def test_async_device_source_is_ordered_after_the_stream():
+    """gmg_set_state_async with a DEVICE tensor produced on the compute stream
+    (ADVICE r1): the library's copy stream must wait for that producer.  A long
+    matmul is queued first, then the new state is written into the tensor on
+    the same stream; the async V-cycle must see the new state (bit-identical
+    to the synchronous calls on it), not the old one."""
+    import torch
+    from paper_2509_06347_b200 import gmg
+    m = configs.box3d(6, 5, 4, 2, seed=3)
+    fs = (1.0, (0.6, 0.2, -0.1), 0.7)
+    Winf = state.winf(*fs)
+    W1 = np.ascontiguousarray(state.perturbed(m, *fs, eps=0.1, seed=21))
+    W2 = np.ascontiguousarray(state.perturbed(m, *fs, eps=0.1, seed=22))
+    s = gmg.Solver(m, n_levels=3)
+    s.set_state(W2, Winf)
+    s.vcycle(1)
+    ref = s.get_state(0)
+    Wd = torch.from_numpy(W1).cuda()
+    W2d = torch.from_numpy(W2).cuda()
+    out = torch.empty_like(torch.from_numpy(W1)).pin_memory()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.float64)
+    torch.cuda.synchronize()
+    for _ in range(4):
+        a = a @ a / 4096.0                      # keeps the stream busy for a while
+    Wd.copy_(W2d)                               # the producer, on the compute stream
+    gmg.gmg_set_state_async(s.ctx, Wd, Winf)
+    gmg.gmg_vcycle_async(s.ctx, 1)
+    gmg.gmg_get_state_async(s.ctx, out)
+    gmg.gmg_sync(s.ctx)
+    s.close()
+    assert np.array_equal(out.numpy(), ref)
