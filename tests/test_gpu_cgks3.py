@@ -278,3 +278,28 @@ def test_partitioned_one_evaluation_matches_oracle(P):
     assert np.array_equal(fl, flo)
     assert _rel(poly, po) <= TOL
     assert _rel(R, Ro) <= TOL and _rel(Gn, Gno) <= TOL and _rel(a, ao) <= TOL
+
+
+@pytest.mark.parametrize("name", ["tri2d", "box3d_prism"])
+def test_explicit_cgks3_iteration_matches_oracle(name):
+    """NEXT-4's explicit arm (the "GPU explicit" row of Table 5):
+    the one-level cycle with the third-order operator IS one explicit CGKS3
+    iteration (Eq.(smo), readings C12/C14, no coarse correction).  40
+    iterations on the device vs the oracle: state, slopes, DF and residual
+    history, element by element."""
+    from tests.parity import elem
+    m, fs = _cases()[name]
+    W, Winf, _, _ = _state(m, fs, 7)
+    s = _solver(m, n_levels=1)
+    s.set_state(W, Winf)
+    hist = s.vcycle(40)
+    Wg = s.get_state(0)
+    Gg, ag = s.get_ho_state()
+    s.close()
+    H = oracle.build_hierarchy(m, 1, 0.5)
+    hs = {}
+    Wo, ho = oracle.vcycle(H, W, Winf, oracle.Options(fine_operator=1, n_levels=1), 40, mesh=m, ho_state=hs)
+    assert elem(Wg, Wo) <= TOL
+    assert elem(Gg.reshape(-1, m.n_cells), hs["G"].reshape(-1, m.n_cells)) <= TOL
+    assert elem(ag, hs["alpha"], np.ones_like(ag)) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])

@@ -34,7 +34,10 @@ part = gmg.gmg_partition_rcb(m.ctr, world)
 s = gmg.Solver(m, n_levels=3, part=part, nranks=world, rank=rank, nccl_id=bytes(128))
 W, Winf = state.bow_shock(m, *fs), state.winf(*fs)
 s.set_state(W, Winf)
-s.vcycle(1)
+try:
+    s.vcycle(1)     # the shim moves no data: ghosts stay unset and the state goes non-finite; only the
+except gmg.GmgError as e:   # recorded protocol matters here
+    assert e.status == gmg.GMG_ENONFINITE, e
 print(json.dumps({"rank": rank, "launches": s.vcycle_launches(), "cells": int(m.n_cells)}))
 s.close()
 dist.barrier()
