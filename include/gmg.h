@@ -133,6 +133,10 @@ typedef struct {
                                1, 2 (default; 0 = default) or 4                                */
     int pdl;                /* 1 (default): programmatic dependent launch between the kernels
                                of a V-cycle; 0 = plain stream order                            */
+    int ho_p2min;           /* fine_operator 1, readings C3 / C3b: a cell uses
+                               the p2 reconstruction only with at least this many interior
+                               von Neumann neighbours; 0 (default) = d + 1 (C3); d + 2 keeps the
+                               simplices (triangles / tets) on p1 (C3b)                       */
 } gmg_options;
 
 /* Fill *o with the defaults above (dim = 3, single rank, device 0, stream 0). */

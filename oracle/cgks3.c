@@ -59,6 +59,7 @@ typedef struct {
     double c1, c2;               /* C9: tau = c1 dt + c2 dt |pl-pr|/(pl+pr) */
     double gam0;                 /* C5: linear weight of the large stencil (gamma_1 = 1 - gam0) */
     double eps;                  /* C5: WENO-Z epsilon */
+    int p2min;                   /* C3: p2 needs >= p2min interior neighbours (0: d + 1; C3b: d + 2) */
 } orc3_opt;
 
 /* ===================================================================== */
@@ -637,7 +638,8 @@ int64_t orc3_recon(const orc3_mesh *M, const orc3_opt *o, const double *W, const
             cpoly *pp = &P[i * nv + q];
             memset(pp, 0, sizeof *pp);
             double a[9];
-            int has2 = orc3_p2(M, nb, nnb, i, Qb, G + (int64_t)q * d * n, a);
+            /* C3 / C3b: the compact stencil must hold at least p2min interior neighbours */
+            int has2 = nnb >= (o->p2min > 0 ? o->p2min : d + 1) ? orc3_p2(M, nb, nnb, i, Qb, G + (int64_t)q * d * n, a) : 0;
             if (!has2) {                                   /* C3: p1 only */
                 pp->c0 = Qb[i];
                 for (int k = 0; k < d; ++k) pp->lin[k] = g1v[k];

@@ -21,7 +21,7 @@ class Orc3Mesh(C.Structure):
 
 class Orc3Opt(C.Structure):
     _fields_ = [("gamma", C.c_double), ("cfl_exp", C.c_double), ("c1", C.c_double), ("c2", C.c_double),
-                ("gam0", C.c_double), ("eps", C.c_double)]
+                ("gam0", C.c_double), ("eps", C.c_double), ("p2min", C.c_int)]
 
 
 @dataclass
@@ -33,9 +33,10 @@ class Opt3:
     c2: float = 1.0
     gam0: float = 0.95
     eps: float = 1e-14
+    p2min: int = 0             # C3: p2 needs >= p2min interior neighbours (0: d + 1); C3b: d + 2
 
     def c(self):
-        return Orc3Opt(self.gamma, self.cfl_exp, self.c1, self.c2, self.gam0, self.eps)
+        return Orc3Opt(self.gamma, self.cfl_exp, self.c1, self.c2, self.gam0, self.eps, self.p2min)
 
 
 def _lib3():

@@ -34,6 +34,7 @@ class Options:
     c1: float = 0.05            # C9 collision time tau = c1 dt + c2 dt |pl-pr|/(pl+pr)
     c2: float = 1.0
     gam0: float = 0.95          # C5 linear weight of the large stencil
+    p2min: int = 0              # C3 / C3b: interior neighbours p2 needs (0: d + 1)
 
 
 def perm_from_color(col):
@@ -155,7 +156,7 @@ def _vcycle_cgks3(levels, W0, Winf, opt: Options, n_cycles, mesh, ho_state):
     if opt.fine_smoother != 0 or opt.df_mode != 0:
         raise ValueError("the CGKS3 fine operator runs with the explicit fine smoother and DF mode 0")
     g, om = opt.gamma, opt.r_factor
-    o3 = cgks3.Opt3(gamma=g, cfl_exp=opt.cfl_exp, c1=opt.c1, c2=opt.c2, gam0=opt.gam0)
+    o3 = cgks3.Opt3(gamma=g, cfl_exp=opt.cfl_exp, c1=opt.c1, c2=opt.c2, gam0=opt.gam0, p2min=opt.p2min)
     M3 = cgks3.Mesh3(mesh)
     L = [e["level"] for e in levels]
     nl = len(L)

@@ -1035,6 +1035,7 @@ void gmg_default_options(gmg_options *o)
     o->l2_persist_mb = 0;
     o->sweep_lanes = 2;
     o->pdl = 1;
+    o->ho_p2min = 0;
 }
 
 gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
@@ -1054,7 +1055,7 @@ gmg_status gmg_create(const gmg_options *opt, gmg_ctx **out)
         opt->setup_device < 0 || opt->setup_device > 1 || opt->skip_repeat < 0 || opt->skip_repeat > 1 ||
         opt->p2p < 0 || opt->p2p > 1 || opt->overlap < -1 || opt->overlap > 1 || opt->l2_persist_mb < 0 ||
         !(opt->sweep_lanes == 0 || opt->sweep_lanes == 1 || opt->sweep_lanes == 2 || opt->sweep_lanes == 4) ||
-        opt->pdl < 0 || opt->pdl > 1)
+        opt->pdl < 0 || opt->pdl > 1 || opt->ho_p2min < 0)
         return GMG_EINVAL;
     gmg_ctx *ctx = new (std::nothrow) gmg_ctx();
     if (!ctx) return GMG_ENOMEM;

@@ -117,7 +117,8 @@ static gmg_status ho_prepare_domain(gmg_ctx *ctx, const HoHost &HH, Domain &dm)
     // per neighbour (d + 1) columns of nk, padded to a multiple of 4 doubles (32-byte loads)
     const int pst = ((d + 1) * nk + 3) & ~3;
     H.poff.assign(n + 1, 0);
-    for (int64_t i = 0; i < n; ++i) H.poff[i + 1] = H.poff[i] + (nnb[i] >= d + 1 ? nnb[i] * pst : 0);
+    const int p2min = ctx->opt.ho_p2min > 0 ? ctx->opt.ho_p2min : d + 1;   // C3 / C3b
+    for (int64_t i = 0; i < n; ++i) H.poff[i + 1] = H.poff[i] + (nnb[i] >= p2min ? nnb[i] * pst : 0);
     H.P.assign((size_t)H.poff[n], 0.0);
     std::vector<char> ok(n, 1);
     auto m2at = [&](int64_t c, int a, int b) {

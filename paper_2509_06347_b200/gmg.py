@@ -51,7 +51,8 @@ class Options(C.Structure):
                 ("device", C.c_int), ("stream", C.c_void_p), ("beta", C.c_double), ("local_domains", C.c_int),
                 ("setup_device", C.c_int), ("fine_operator", C.c_int), ("ho_c1", C.c_double), ("ho_c2", C.c_double),
                 ("ho_gam0", C.c_double), ("ho_eps", C.c_double), ("skip_repeat", C.c_int), ("p2p", C.c_int),
-                ("overlap", C.c_int), ("l2_persist_mb", C.c_int), ("sweep_lanes", C.c_int), ("pdl", C.c_int)]
+                ("overlap", C.c_int), ("l2_persist_mb", C.c_int), ("sweep_lanes", C.c_int), ("pdl", C.c_int),
+                ("ho_p2min", C.c_int)]
 
 
 _lib = None

@@ -303,3 +303,32 @@ def test_explicit_cgks3_iteration_matches_oracle(name):
     assert elem(Gg.reshape(-1, m.n_cells), hs["G"].reshape(-1, m.n_cells)) <= TOL
     assert elem(ag, hs["alpha"], np.ones_like(ag)) <= TOL
     assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])
+
+
+def test_p2min_reading_c3b_matches_oracle():
+    """Reading C3b (gmg_options.ho_p2min = d + 2: simplices keep p1):
+    on a hybrid quad / triangle O-grid the p2 flags (quads only) are bit-exact
+    and 4 V-cycles match the oracle run with the same reading."""
+    from tests.parity import elem
+    m = configs.naca_ogrid(ni=48, n_quad=8, n_tri=4)
+    fs = configs.FREESTREAM[2]
+    W, Winf = state.perturbed(m, *fs, eps=0.05, seed=5), state.winf(*fs)
+    s = _solver(m, n_levels=3, ho_p2min=4)
+    s.set_state(W, Winf)
+    poly, fl = s.ho_recon()
+    hist = s.vcycle(4)
+    Wg = s.get_state(0)
+    s.close()
+    _, flo, _ = cgks3.recon(cgks3.Mesh3(m), W, np.zeros((4, 2, m.n_cells)), np.ones(m.n_cells), Winf,
+                            cgks3.Opt3(p2min=4))
+    assert np.array_equal(fl & 1, flo & 1)
+    nint = np.zeros(m.n_cells, int)
+    for f in range(m.n_faces):
+        if m.right[f] >= 0:
+            nint[m.left[f]] += 1
+            nint[m.right[f]] += 1
+    assert np.all((flo & 1) <= (nint >= 4))           # no cell with fewer than 4 interior neighbours uses p2
+    H = oracle.build_hierarchy(m, 3, 0.5)
+    Wo, ho = oracle.vcycle(H, W, Winf, oracle.Options(fine_operator=1, p2min=4), 4, mesh=m, ho_state={})
+    assert elem(Wg, Wo) <= TOL
+    assert np.all(np.abs(hist - ho) <= TOL * ho[0][None, :])

@@ -405,3 +405,26 @@ def test_residual_discrete_conservation(k):
     G = np.zeros((d + 2, d, n))
     R, Gn, a, S, fl, nf = cgks3.residual(M, W, G, np.ones(n), Winf)
     assert np.max(np.abs(R.sum(axis=1))) < 1e-12 * np.max(np.abs(R)), R.sum(axis=1)
+
+
+def test_p2min_reading_c3b(orc):
+    """Reading C3b: with p2min = d + 2 a cell uses p2 only with at
+    least d + 2 interior neighbours -- on a triangulated square no cell does (3
+    faces each), on a quad grid the interior cells still do; where p2 is off
+    the polynomial is the p1 (Green-Gauss x DF) one, identical to the default
+    run's p1 cells."""
+    from oracle import cgks3
+    for m, expect_p2 in ((configs.tri_square(6, 6, seed=2), False), (configs.quad_grid(6, 6), True)):
+        W = state.perturbed(m, 1.0, [0.5, 0.1], 0.7, eps=0.05, seed=1)
+        Winf = state.winf(1.0, [0.5, 0.1], 0.7)
+        G0 = np.zeros((4, 2, m.n_cells))
+        a0 = np.ones(m.n_cells)
+        M = cgks3.Mesh3(m)
+        p_def, f_def, _ = cgks3.recon(M, W, G0, a0, Winf)
+        p_b, f_b, _ = cgks3.recon(M, W, G0, a0, Winf, cgks3.Opt3(p2min=4))
+        assert bool((f_b & 1).any()) == expect_p2
+        assert bool((f_def & 1).any())
+        same = (f_b & 1) == (f_def & 1)
+        assert np.array_equal(p_b[same], p_def[same])
+        gone = (f_def & 1) & ~(f_b & 1)
+        assert np.all(p_b[gone.astype(bool)][:, :, 3:] == 0.0)     # no quadratic terms where p2 is off
