@@ -308,7 +308,7 @@ def main():
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/cpu)")
     ap.add_argument("--no-next1", action="store_true", help="skip the NEXT-1 (third-order CGKS fine operator) line")
     ap.add_argument("--p2p", type=int, default=0, help="N > 1: fused P2P halo over CUDA IPC instead of NCCL")
-    ap.add_argument("--l2-persist-mb", type=int, default=0, help="persisting-L2 set-aside for the W' records")
+X
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
     args.steps_ref = max(1, min(args.steps, 5))

@@ -560,7 +560,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
 // the sweep launch: 128-thread blocks, 8 per SM (FF, with its second set of
 // accumulators: 6 per SM), grid = one resident wave
 template <int D, int LPC, bool FF>
-__global__ void __launch_bounds__(128, FF ? 6 : 8) k_sweep(SweepArgs a)
+__global__ void __launch_bounds__(128, FF ? 7 : 8) k_sweep(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
     sweep_cells<D, LPC, FF, false, false>(a, P2PArgs{}, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x,

@@ -13,12 +13,12 @@ from synth import configs, state  # noqa: E402
 m = configs.config(4)
 fs = configs.FREESTREAM[4]
 W, Winf = state.bow_shock(m, *fs), state.winf(*fs)
-s = gmg.Solver(m, n_levels=3, setup_device=1, sweep_lanes=int(os.environ.get("LANES", "2")))
+s = gmg.Solver(m, n_levels=3, setup_device=1, sweep_lanes=int(os.environ.get("LANES", "0")),
+               l2_persist_mb=int(os.environ.get("L2MB", "0")))
 s.set_state(W, Winf)
 for _ in range(3):
     s.vcycle(1)
-out = {"var": os.environ.get("GMG_DEV_VAR", "0"), "grid": os.environ.get("GMG_DEV_GRID", "0"),
-       "lanes": os.environ.get("LANES", "2")}
+out = {"lanes": os.environ.get("LANES", "0"), "l2mb": os.environ.get("L2MB", "0")}
 for l in (1, 2):
     ms, cu, by = s.time_smooth(l, 6, 10)
     out[f"L{l}_ms"] = ms / 10
