@@ -308,7 +308,10 @@ def main():
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/cpu)")
     ap.add_argument("--no-next1", action="store_true", help="skip the NEXT-1 (third-order CGKS fine operator) line")
     ap.add_argument("--p2p", type=int, default=0, help="N > 1: fused P2P halo over CUDA IPC instead of NCCL")
-X
+    ap.add_argument("--l2-persist-mb", type=int, default=40,
+                    help="persisting-L2 set-aside (MB) for the gathered W' records (gmg_options.l2_persist_mb; "
+                         "0 / 24 / 32 / 40 / 48 MB -> 2.694 / 2.626 / 2.628 / 2.625 / 2.637 ms per V-cycle, "
+                         "profiles/r02/l2_persist.jsonl); restored when the solver is destroyed")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
     args.steps_ref = max(1, min(args.steps, 5))
@@ -540,6 +543,7 @@ X
                    "setup_s": round(t_setup, 3),
                    "setup": "hierarchy with device-side Algorithms 1 and 3 (bit-identical to the host setup), "
                             "not timed",
+                   "l2_persist_mb": args.l2_persist_mb,
                    "n_gpus_partitions": 1 if replicas else ws},
         "nominal_value": nominal_cycle / (ms_step * 1e-3),
         "vcycles_per_s": 1e3 / ms_step * (ws if replicas else 1),
