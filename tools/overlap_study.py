@@ -1,5 +1,5 @@
 """Dev tool: V-cycle time of the partitioned path on one GPU (local domains),
-exchange overlap on/off (GMG_OVERLAP), and the agreement of the two."""
+exchange overlap on/off (gmg_options.overlap), and the agreement of the two."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -15,9 +15,8 @@ out = {"config": k, "n_cells": int(m.vol.size)}
 for P in (1, 2, 4):
     part = gmg.gmg_partition_rcb(m.ctr, P) if P > 1 else None
     ref = None
-    for ov in (0, 1):  # GMG_OVERLAP (default: off for local domains, on for NCCL ranks)
-        os.environ["GMG_OVERLAP"] = str(ov)
-        s = gmg.Solver(m, n_levels=3, part=part, local_domains=P) if P > 1 else gmg.Solver(m, n_levels=3)
+    for ov in (0, 1):  # gmg_options.overlap (default -1: off for local domains, on for NCCL ranks)
+        s = gmg.Solver(m, n_levels=3, part=part, local_domains=P, overlap=ov) if P > 1 else gmg.Solver(m, n_levels=3)
         s.set_state(W, state.winf(*fs))
         h = s.vcycle(3)
         Wn = s.get_state()
