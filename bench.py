@@ -308,10 +308,10 @@ def main():
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/cpu)")
     ap.add_argument("--no-next1", action="store_true", help="skip the NEXT-1 (third-order CGKS fine operator) line")
     ap.add_argument("--p2p", type=int, default=0, help="N > 1: fused P2P halo over CUDA IPC instead of NCCL")
-    ap.add_argument("--l2-persist-mb", type=int, default=40,
-                    help="persisting-L2 set-aside (MB) for the gathered W' records (gmg_options.l2_persist_mb; "
-                         "0 / 24 / 32 / 40 / 48 MB -> 2.694 / 2.626 / 2.628 / 2.625 / 2.637 ms per V-cycle, "
-                         "profiles/r02/l2_persist.jsonl); restored when the solver is destroyed")
+    ap.add_argument("--l2-persist-mb", type=int, default=0,
+                    help="persisting-L2 set-aside (MB) for the gathered W' states (gmg_options.l2_persist_mb, "
+                         "restored when the solver is destroyed); with the split state layout (v24) 40 MB speeds "
+                         "the sweeps but not the V-cycle (2.351 vs 2.355 ms), so it is off by default")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile_only else args.warmup
     args.steps_ref = max(1, min(args.steps, 5))

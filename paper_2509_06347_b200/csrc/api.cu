@@ -152,14 +152,14 @@ void klaunch(gmg_ctx *ctx, void (*k)(KP...), dim3 g, dim3 b, cudaStream_t s, A..
 
 // prep: the launch also writes the sweep slot records (A outward | S r) of
 // both cells of every interior face (whole 32-byte records).  from_rec: W is
-// a W_lin array (stride Wp<D>::STRIDE), else a state array (stride nv)
+// a W_lin state array (Wp<D> layout), else a W array (stride nv)
 template <int D>
 void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, bool from_rec, bool df = false,
                   bool prep = false)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
-    constexpr int RS = Wp<D>::STRIDE, NV = D + 2;
+    constexpr int RS = 0, NV = D + 2;   // RS: the state-array layout (k_face STRIDE 0)
     Lc.pre(GMG_K_FACE);
     const dim3 g(nblk(L.nf)), b(256);
     const Phys ph = phys(ctx);
@@ -227,7 +227,8 @@ void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
     if (ctx->nparts <= 1) return;
     constexpr int NV = D + 2;
     const int ncolor = ctx->lv[l].ncolor;
-    const int stride = kind == EX_W ? NV : Wp<D>::STRIDE, offset = 0;
+    const int stride = kind == EX_W ? NV : 4, offset = 0;
+    auto split_of = [&](DevLevel &L) { return (kind != EX_W && D == 3) ? L.n_loc : 0; };
     auto src_of = [&](DevLevel &L) { return kind == EX_W ? L.W : kind == EX_WLIN ? L.wlin : L.wp; };
     auto dst2_of = [&](DevLevel &L) { return kind == EX_WLIN ? L.wp : (double *)nullptr; };
     auto grange = [&](const DomLevel &H, int &g0, int &g1) {
@@ -245,7 +246,7 @@ void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
         if (s1 > s0) {
             Lc.pre(GMG_K_HALO);
             klaunch(Lc.ctx, k_pack, dim3(nblk(s1 - s0)), dim3(256), Lc.s, (int)(s1 - s0), L.send_idx + s0, src_of(L), stride, offset, NV,
-                                                   L.sendbuf + s0 * NV);
+                                                   L.sendbuf + s0 * NV, split_of(L));
             Lc.post(GMG_K_HALO, (double)(s1 - s0) * NV * 16);
         }
     }
@@ -294,7 +295,7 @@ void enqueue_exchange(Launcher &Lc, int l, int kind, int color)
         if (r1 > r0) {
             Lc.pre(GMG_K_HALO);
             klaunch(Lc.ctx, k_unpack, dim3(nblk(r1 - r0)), dim3(256), Lc.s, (int)(r1 - r0), L.recv_idx + r0, L.recvbuf + r0 * NV,
-                                                     src_of(L), stride, offset, NV, dst2_of(L));
+                                                     src_of(L), stride, offset, NV, dst2_of(L), split_of(L));
             Lc.post(GMG_K_HALO, (double)(r1 - r0) * NV * (kind == EX_WLIN ? 24 : 16));
         }
     }
@@ -404,6 +405,7 @@ SweepArgs sweep_args(const gmg_ctx *ctx, DevLevel &L, const DomLevel &H, int c, 
     a.cend = b1;
     a.lo = c >= 0 ? (int)H.blk[c] : 0;
     a.n_own = (int)H.n_own;
+    a.n_loc = (int)H.n_loc;
     a.gm1 = ctx->opt.gamma - 1.0;
     a.sinfo = L.sinfo;
     a.sJe = L.sJe;
@@ -437,7 +439,7 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
     if (b1 <= b0) return;
     const SweepArgs a = sweep_args(ctx, L, H, c, b0, b1, rhs, Wout);
     const void *win = ctx->l2_window ? (const void *)L.wp : nullptr;
-    const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * Wp<D>::STRIDE * 8) : 0;
+    const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * (D + 2) * 8) : 0;
     const int lpc = part ? ctx->lpc : sweep_lpc(ctx, b1 - b0);
     Lc.pre(GMG_K_SWEEP);
     if (ff) launch_sweep<D, true>(ctx, a, lpc, Lc.s, win, wb);
@@ -459,7 +461,7 @@ void enqueue_p2p_phase(Launcher &Lc, int l, int c, bool last, bool ff, std::func
         const DomLevel &H = dm.lv[l];
         const int b0 = c < 0 ? 0 : (int)H.blk[c], b1 = c < 0 ? 0 : (int)H.blk[c + 1];
         const SweepArgs a = sweep_args(ctx, L, H, c, b0, b1, rhs(L), last ? wout(L) : nullptr);
-        P2PArgs p{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_wp, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
+        P2PArgs p{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_wp, L.peer_nloc, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
         const int lpc = sweep_lpc(ctx, b1 - b0);
         int nb = nblk((int64_t)(b1 - b0) * lpc);
         if (ctx->sweep_grid_cap > 0) nb = std::min(nb, ctx->sweep_grid_cap / 2);
@@ -572,7 +574,7 @@ void enqueue_exchange_ho(Launcher &Lc, double *HoDev::*arr, int ncomp)
         if (s1 > 0) {
             Lc.pre(GMG_K_HALO);
             klaunch(ctx, k_pack, dim3(nblk(s1)), dim3(256), Lc.s, (int)s1, L.send_idx, (const double *)(L.ho.*arr), ncomp, 0,
-                    ncomp, dm.ho.sendbuf);
+                    ncomp, dm.ho.sendbuf, 0);
             Lc.post(GMG_K_HALO, (double)s1 * ncomp * 16);
         }
     }
@@ -612,7 +614,7 @@ void enqueue_exchange_ho(Launcher &Lc, double *HoDev::*arr, int ncomp)
         if (r1 > 0) {
             Lc.pre(GMG_K_HALO);
             klaunch(ctx, k_unpack, dim3(nblk(r1)), dim3(256), Lc.s, (int)r1, L.recv_idx, (const double *)dm.ho.recvbuf,
-                    L.ho.*arr, ncomp, 0, ncomp, (double *)nullptr);
+                    L.ho.*arr, ncomp, 0, ncomp, (double *)nullptr, 0);
             Lc.post(GMG_K_HALO, (double)r1 * ncomp * 16);
         }
     }
@@ -795,16 +797,17 @@ gmg_status get_natural(gmg_ctx *ctx, int l, std::function<const double *(DevLeve
     return GMG_OK;
 }
 
-// every domain's owned dW = W' - W_lin -> natural SoA (gmg_smooth)
-gmg_status get_dw_natural(gmg_ctx *ctx, int l, double *dst)
+// every domain's owned dW = W' - W_lin (or W_lin itself) -> natural SoA (gmg_smooth, gmg_get_level_field)
+gmg_status get_dw_natural(gmg_ctx *ctx, int l, double *dst, bool wlin_only = false)
 {
     const int64_t N = ctx->lv[l].n;
-    const int ncomp = ctx->opt.dim + 2, ws = ctx->opt.dim == 3 ? Wp<3>::STRIDE : Wp<2>::STRIDE;
+    const int ncomp = ctx->opt.dim + 2;
     if (ctx->opt.nranks > 1)
         CK(cudaMemcpyAsync(ctx->d_stage, dst, sizeof(double) * ncomp * N, cudaMemcpyDefault, ctx->stream));
     for (Domain &dm : ctx->dom) {
         DevLevel &L = dm.dv[l];
-        k_diff_to_natural<<<nblk(L.n), 256, 0, ctx->stream>>>(L.n, (int)N, ncomp, L.perm, L.wp, L.wlin, ws, ctx->d_stage);
+        k_state_to_natural<<<nblk(L.n), 256, 0, ctx->stream>>>(L.n, (int)N, ncomp, L.perm, wlin_only ? L.wlin : L.wp,
+                                                               wlin_only ? nullptr : L.wlin, L.n_loc, ctx->d_stage);
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(dst, ctx->d_stage, sizeof(double) * ncomp * N, cudaMemcpyDefault, ctx->stream));
@@ -850,8 +853,8 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.Frec = b.take<double>((size_t)kFaceRec * nf);
             L.vol = b.take<double>(n);
             L.W = b.take<double>((size_t)nv * nloc); L.Rt = b.take<double>((size_t)nv * n);
-            L.wlin = b.take<double>((size_t)Wp<3>::STRIDE * nloc);   // >= Wp<2>::STRIDE
-            L.wp = b.take<double>((size_t)Wp<3>::STRIDE * nloc);
+            L.wlin = b.take<double>((size_t)nv * nloc);   // state arrays, Wp<D> layout
+            L.wp = b.take<double>((size_t)nv * nloc);
             L.xr = b.take<double>((size_t)kXr * n);
             L.dc = b.take<double>((size_t)2 * n);
             L.tmp = b.take<double>(n);
@@ -867,6 +870,7 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.p2p_k = b.take<int>(H.p2p_k.size());
             L.p2p_g = b.take<int>(H.p2p_g.size());
             L.peer_wp = b.take<double *>(H.peers.size());
+            L.peer_nloc = b.take<int>(H.peers.size());
             L.p2p_sig = b.take<int *>(H.peers.size());
             L.p2p_wait = b.take<int>(H.peers.size());
             L.ginfo = b.take<int4>(n);
@@ -1351,8 +1355,8 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.recv_idx, H.recv_idx.data(), H.recv_idx.size() * sizeof(int)));
             // alpha = 1 until set (df_mode 2 keeps it)
             k_fill<<<nblk(H.n_own), 256, 0, ctx->stream>>>((int)H.n_own, L.alpha, 1.0);
-            CK(cudaMemsetAsync(L.wlin, 0, sizeof(double) * Wp<3>::STRIDE * H.n_loc, ctx->stream));
-            CK(cudaMemsetAsync(L.wp, 0, sizeof(double) * Wp<3>::STRIDE * H.n_loc, ctx->stream));
+            CK(cudaMemsetAsync(L.wlin, 0, sizeof(double) * L.nv * H.n_loc, ctx->stream));
+            CK(cudaMemsetAsync(L.wp, 0, sizeof(double) * L.nv * H.n_loc, ctx->stream));
             CK(cudaMemsetAsync(L.xr, 0, sizeof(double) * kXr * H.n_own, ctx->stream));
             CK(cudaMemsetAsync(L.dc, 0, sizeof(double) * 2 * H.n_own, ctx->stream));
         }
@@ -1370,12 +1374,15 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
                 const DomLevel &H = dm.lv[l];
                 std::vector<double *> pr(H.peers.size());
                 std::vector<int *> sg(H.peers.size());
+                std::vector<int> pn(H.peers.size());
                 for (size_t k = 0; k < H.peers.size(); ++k) {
                     DevLevel &Q = ctx->dom[H.peers[k]].dv[l];
                     pr[k] = Q.wp;
                     sg[k] = Q.p2p_flags + dm.rank;
+                    pn[k] = Q.n_loc;
                 }
                 if (!pr.empty()) {
+                    CK(cudaMemcpy(dm.dv[l].peer_nloc, pn.data(), pn.size() * sizeof(int), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(dm.dv[l].peer_wp, pr.data(), pr.size() * sizeof(double *), cudaMemcpyHostToDevice));
                     CK(cudaMemcpy(dm.dv[l].p2p_sig, sg.data(), sg.size() * sizeof(int *), cudaMemcpyHostToDevice));
                 }
@@ -1607,7 +1614,7 @@ gmg_status gmg_p2p_emulate_smooth(gmg_ctx *ctx, int level, int n_sweeps, double 
         DevLevel &L = ctx->dom[d].dv[level];
         const DomLevel &H = ctx->dom[d].lv[level];
         ed[d].a = sweep_args(ctx, L, H, -1, 0, 0, L.Rt, nullptr);
-        ed[d].p = P2PArgs{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_wp, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
+        ed[d].p = P2PArgs{L.p2p_off, L.p2p_k, L.p2p_g, L.peer_wp, L.peer_nloc, L.npeer, L.p2p_wait, L.p2p_sig, L.p2p_flags, L.p2p_ctl};
         for (int c = 0; c <= nc; ++c) ed[d].blk[c] = (int)H.blk[c];
         ed[d].rank = ctx->dom[d].rank;
         ed[d].bar = ctx->d_emu_bar + 2 * d;
@@ -2054,10 +2061,10 @@ gmg_status gmg_get_level_field(gmg_ctx *ctx, int level, int field, double *out)
         ctx->err = "bad level / field / null";
         return GMG_EINVAL;
     }
-    const int nv = ctx->opt.dim + 2, ws = ctx->opt.dim == 3 ? Wp<3>::STRIDE : Wp<2>::STRIDE;
+    const int nv = ctx->opt.dim + 2;
     switch (field) {
         case GMG_FIELD_W: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.W; }, nv, out);
-        case GMG_FIELD_W0: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.wlin; }, nv, out, ws);
+        case GMG_FIELD_W0: return get_dw_natural(ctx, level, out, true);
         case GMG_FIELD_DW: return get_dw_natural(ctx, level, out);
         case GMG_FIELD_RS: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.Rs; }, nv, out);
         case GMG_FIELD_F: return get_natural(ctx, level, [](DevLevel &L) { return (const double *)L.F; }, nv, out);
@@ -2138,6 +2145,9 @@ gmg_status gmg_p2p_import(gmg_ctx *ctx, const void *handles, const int64_t *base
             sg[k] = (int *)(base[q] + lay[nl]) + me;
         }
         if (!pr.empty()) {
+            // the peers' state-array sizes (owned + ghost cells of their domain on this level), from the setup
+            CK(cudaMemcpy(dm.dv[l].peer_nloc, H.p2p_peer_nloc.data(), H.p2p_peer_nloc.size() * sizeof(int),
+                          cudaMemcpyHostToDevice));
             CK(cudaMemcpy(dm.dv[l].peer_wp, pr.data(), pr.size() * sizeof(double *), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(dm.dv[l].p2p_sig, sg.data(), sg.size() * sizeof(int *), cudaMemcpyHostToDevice));
         }

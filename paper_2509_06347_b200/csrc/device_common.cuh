@@ -12,15 +12,16 @@ namespace gmg {
 
 // Sweep state layout (doubles).  The smoother works on W' = W_lin + dW (the
 // linearisation state plus the current increment), DESIGN.md §6 "W'
-// formulation":
-//  * Wp<D>::STRIDE -- per-cell record of W' (and of W_lin, same layout): 3D
-//    [W0..W3 | W4 0 0 0], 2D [W0..W3]; 32-byte aligned, so a neighbour gather
-//    is two (3D) or one (2D) 256-bit loads touching exactly that many sectors.
+// formulation".  A state array (W' and W_lin) of n_loc cells holds nv * n_loc
+// doubles: 2D [n_loc][4] = (rho, m, rho E), one 32-byte sector per cell; 3D
+// split [n_loc][4] = (rho, m) followed by [n_loc] = rho E -- a neighbour
+// gather is one 256-bit load plus one 64-bit load (40 B, no padding; the
+// rho E words of neighbouring cells share sectors), round 2 v24.
 //  * kXr -- own-cell record [X_0..X_{nv-1}, c (, pad)], X = W_lin - Rt/D + c P,
 //    c = alpha/(2D), written by the first forward half-sweep of a smoothing step.
 template <int D> struct Wp;
-template <> struct Wp<3> { static constexpr int STRIDE = 8; };
-template <> struct Wp<2> { static constexpr int STRIDE = 4; };
+template <> struct Wp<3> { static constexpr bool SPLIT = true; };
+template <> struct Wp<2> { static constexpr bool SPLIT = false; };
 constexpr int kXr = 6;
 // per-slot record: A_0..A_{D-1}, S r at [D]
 constexpr int kSlotRec = 4;
@@ -109,18 +110,25 @@ __device__ __forceinline__ void st4(double *p, const double *v)
                  : "memory");
 }
 
-// one state into a Wp<D> record (whole 32-byte chunks, zero padding)
+// one state into cell i of a state array of nloc cells (layout above)
 template <int D>
-__device__ __forceinline__ void st_state(double *r, const double *w)
+__device__ __forceinline__ void st_state(double *base, size_t nloc, size_t i, const double *w)
 {
-    if constexpr (D == 3) {
-        const double c0[4] = {w[0], w[1], w[2], w[3]}, c1[4] = {w[4], 0.0, 0.0, 0.0};
-        st4(r, c0);
-        st4(r + 4, c1);
-    } else {
-        st4(r, w);
-    }
+    st4(base + 4 * i, w);
+    if constexpr (D == 3) base[4 * nloc + i] = w[4];
 }
+
+// cell i of a state array of nloc cells -> w[nv] (one 256-bit load, plus one
+// 64-bit load in 3D); CG: L2-coherent (states written by other blocks of the
+// same launch), else the non-coherent path
+template <int D, bool CG = false>
+__device__ __forceinline__ void ld_state(const double *base, size_t nloc, size_t i, double *w)
+{
+    if constexpr (CG) ld4cg(base + 4 * i, w);
+    else ld4nc(base + 4 * i, w);
+    if constexpr (D == 3) w[4] = CG ? __ldcg(base + 4 * nloc + i) : __ldg(base + 4 * nloc + i);
+}
+
 template <int D>
 __device__ __forceinline__ double pressure(const double *w, double gm1)
 {

@@ -71,6 +71,7 @@ struct DomLevel {
     std::vector<int64_t> send_off, recv_off;   // [ncolor*npeers + 1]
     // fused P2P halo: per owned cell, the ghost copies it must update (peer slot, peer-local ghost index)
     std::vector<int32_t> p2p_off, p2p_k, p2p_g;
+    std::vector<int32_t> p2p_peer_nloc;    // [npeers] the peers' owned + ghost cells on this level
 };
 
 // NEXT-1: third-order compact GKS fine operator, fine level.
@@ -112,8 +113,8 @@ struct DevLevel {
     double *Rt, *Rs, *F;         // [n][nv] RHS / restricted residual / forcing
     double *alpha, *sigma, *tmp; // [n]
     // smoother state (W' formulation; strides Wp<D>::STRIDE, kXr)
-    double *wlin;                // [n_loc][Wp] linearisation state W_lin (coarse: the restricted W0)
-    double *wp;                  // [n_loc][Wp] W' = W_lin + dW of the current half-sweep
+    double *wlin;                // state array (Wp<D> layout, n_loc cells): W_lin (coarse: the restricted W0)
+    double *wp;                  // state array: W' = W_lin + dW of the current half-sweep
     double *xr;                  // [n][kXr] X = W_lin - Rt/D + c P, c = alpha/(2D) (own-cell record)
     double *dc;                  // [n][2] 1/D, alpha/(2D) of the hybrid diagonal (gather G_PREPARE)
     const uint8_t *deg_int, *deg_all;    // [n]
@@ -131,6 +132,7 @@ struct DevLevel {
     // fused P2P halo (gmg_options.p2p)
     const int *p2p_off, *p2p_k, *p2p_g;
     double **peer_wp;                 // [npeer] peers' W' arrays (this level)
+    int *peer_nloc;                   // [npeer] their state-array sizes (owned + ghost cells)
     int **p2p_sig;                    // [npeer] &peer.flags[my rank]
     int *p2p_wait;                    // [npeer] peer ranks
     int *p2p_flags, *p2p_ctl;         // per domain: [nparts] published phase counts, [4] control

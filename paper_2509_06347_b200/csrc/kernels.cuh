@@ -4,7 +4,7 @@
 // Every kernel is HBM/latency bound gather-streaming work; see DESIGN.md
 // "Kernels and rooflines".  Cell arrays are AoS [n][nv] in color-contiguous
 // internal order.  The sweep gathers one 32-byte aligned state record W'
-// (Wp<D>, two 256-bit loads in 3D) per neighbour and per-slot 32-byte records
+// (Wp<D> layout: one 256-bit + one 64-bit load in 3D) per neighbour and per-slot 32-byte records
 // (A outward | S r); the own cell reads its (X, c) record (W' formulation,
 // DESIGN.md §6).  The test-only P2P concurrency emulation is p2p_emulate.cuh.
 #pragma once
@@ -46,7 +46,7 @@ __device__ __forceinline__ void kfvs_side(const Side<D> &s, const double *n, dou
 // ---------------------------------------------------------------------------
 // Face kernel (a6 + a10 per face): r_f = omega (|u.n| + a) of the average
 // state; with FLUX also S F_f (KFVS) and alpha_f^{M_f} (DF helper).  The
-// state is read with a stride (NV for W, Wp<D>::STRIDE for W_lin).
+// state is read with a stride (NV for W; STRIDE 0 = a W_lin state array, Wp<D> layout).
 // Output: one 64-byte record per face, Frec = (S F[nv] | S r | alpha^M | 0..),
 // written with two 256-bit stores.
 // ---------------------------------------------------------------------------
@@ -74,9 +74,14 @@ __global__ void __launch_bounds__(256, DF ? 3 : 4) k_face(DevLevel L, const doub
 #pragma unroll
     for (int k = 0; k < D; ++k) n[k] = A[k] * iS;
     double wl[NV], wr[NV];
-    ld_vec<NV>(Wsrc + (size_t)l * STRIDE, wl);
-    if (r >= 0) ld_vec<NV>(Wsrc + (size_t)r * STRIDE, wr);
-    else ghost<D>(bc.kind[-r - 1], wl, bc, n, wr);
+    if constexpr (STRIDE == 0) {   // a state array (Wp layout): W_lin
+        ld_state<D>(Wsrc, (size_t)L.n_loc, l, wl);
+        if (r >= 0) ld_state<D>(Wsrc, (size_t)L.n_loc, r, wr);
+    } else {
+        ld_vec<NV>(Wsrc + (size_t)l * STRIDE, wl);
+        if (r >= 0) ld_vec<NV>(Wsrc + (size_t)r * STRIDE, wr);
+    }
+    if (r < 0) ghost<D>(bc.kind[-r - 1], wl, bc, n, wr);
 
     double out[kFaceRec];
 #pragma unroll
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
             st2(L.dc + 2 * (size_t)i, dc);
         }
         const size_t o = (size_t)i * NV;
-        if (a.flags & G_COPY_W) st_state<D>(L.wlin + (size_t)i * Wp<D>::STRIDE, pre);
+        if (a.flags & G_COPY_W) st_state<D>(L.wlin, (size_t)L.n_loc, i, pre);
         if (a.flags & G_SET_F) {
             if (pk == G_SET_F) {
 #pragma unroll
@@ -295,58 +300,50 @@ __global__ void k_norm_hist(const double *__restrict__ sumsq, int ndom, int nv, 
 // arrays with the given stride/offset (W', W_lin or W).  dst2 (nullable)
 // receives a second copy with the same layout (ghost W' = W_lin).
 // ---------------------------------------------------------------------------
+// element q of cell c of an array: AoS (stride, offset) when split == 0, else
+// a 3D split state array of `split` cells ([split][4] then [split], Wp<3>)
+__device__ __forceinline__ size_t elem_at(size_t c, int q, int stride, int offset, int split)
+{
+    if (split) return q < 4 ? 4 * c + q : 4 * (size_t)split + c;
+    return c * stride + offset + q;
+}
 __global__ void k_pack(int count, const int *__restrict__ idx, const double *__restrict__ src, int stride,
-                       int offset, int ncomp, double *__restrict__ buf)
+                       int offset, int ncomp, double *__restrict__ buf, int split)
 {
     pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= count) return;
-    const double *s = src + (size_t)idx[k] * stride + offset;
-    for (int q = 0; q < ncomp; ++q) buf[(size_t)k * ncomp + q] = s[q];
+    const size_t c = (size_t)idx[k];
+    for (int q = 0; q < ncomp; ++q) buf[(size_t)k * ncomp + q] = src[elem_at(c, q, stride, offset, split)];
 }
 __global__ void k_unpack(int count, const int *__restrict__ idx, const double *__restrict__ buf, double *dst,
-                         int stride, int offset, int ncomp, double *dst2)
+                         int stride, int offset, int ncomp, double *dst2, int split)
 {
     pdl_enter();
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= count) return;
-    const size_t o = (size_t)idx[k] * stride + offset;
+    const size_t c = (size_t)idx[k];
     for (int q = 0; q < ncomp; ++q) {
         const double v = buf[(size_t)k * ncomp + q];
-        dst[o + q] = v;
-        if (dst2) dst2[o + q] = v;
+        const size_t o = elem_at(c, q, stride, offset, split);
+        dst[o] = v;
+        if (dst2) dst2[o] = v;
     }
 }
 
-// Wp<D> record -> state (two / one 256-bit loads); CG: L2-coherent (records
-// written by other blocks of the same launch), else the non-coherent path
-template <int D, bool CG = false>
-__device__ __forceinline__ void ld_state(const double *r, double *w)
-{
-    if constexpr (D == 3) {
-        double c0[4], c1[4];
-        if constexpr (CG) { ld4cg(r, c0); ld4cg(r + 4, c1); }
-        else { ld4nc(r, c0); ld4nc(r + 4, c1); }
-        w[0] = c0[0]; w[1] = c0[1]; w[2] = c0[2]; w[3] = c0[3]; w[4] = c1[0];
-    } else {
-        if constexpr (CG) ld4cg(r, w);
-        else ld4nc(r, w);
-    }
-}
 
 // ghost records from the (current) ghost state: W_lin = W' = W
 template <int D>
 __global__ void k_ghost_wlin(int n, int n_loc, const double *__restrict__ W, double *wlin, double *wp)
 {
     pdl_enter();
-    constexpr int WS = Wp<D>::STRIDE;
     const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_loc) return;
     double w[D + 2];
 #pragma unroll
     for (int q = 0; q < D + 2; ++q) w[q] = W[(size_t)g * (D + 2) + q];
-    st_state<D>(wlin + (size_t)g * WS, w);
-    st_state<D>(wp + (size_t)g * WS, w);
+    st_state<D>(wlin, n_loc, g, w);
+    st_state<D>(wp, n_loc, g, w);
 }
 // ghost states after a smoothing step: W = W' (already exchanged)
 template <int D>
@@ -355,8 +352,10 @@ __global__ void k_ghost_w(int n, int n_loc, const double *__restrict__ wp, doubl
     pdl_enter();
     const int g = n + blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= n_loc) return;
+    double w[D + 2];
+    ld_state<D>(wp, n_loc, g, w);
 #pragma unroll
-    for (int q = 0; q < D + 2; ++q) W[(size_t)g * (D + 2) + q] = wp[(size_t)g * Wp<D>::STRIDE + q];
+    for (int q = 0; q < D + 2; ++q) W[(size_t)g * (D + 2) + q] = w[q];
 }
 
 // ---------------------------------------------------------------------------
@@ -403,13 +402,14 @@ __device__ __forceinline__ void flux_rw(const double *w, const double *A, double
 struct SweepArgs {
     int cbeg, cend;            // cells [cbeg, cend) of one color block (or its boundary / interior part)
     int lo, n_own;             // FF: owned neighbours j < lo are of earlier colors; j >= n_own are ghosts
+    int n_loc;                 // cells of the state arrays (owned + ghosts)
     double gm1;
     const int2 *sinfo;         // [n] (first slot entry, interior slots)
     const int *sJe;            // [ns] neighbour
     const double *sRe;         // [ns][4] (A outward | S r)
-    double *wp;                // [n_loc][Wp] W'
+    double *wp;                // W' (state array of n_loc cells, Wp<D> layout)
     double *xr;                // [n][kXr] (X, c)
-    const double *wlin;        // [n_loc][Wp] W_lin        (FF)
+    const double *wlin;        // W_lin (same layout)     (FF)
     const double *rhs;         // [n][nv] right-hand side Rt (FF)
     const double *dc;          // [n][2] (1/D, c)          (FF)
     double *Wout;              // [n][nv] or null: W = W' (last backward half-sweep)
@@ -428,6 +428,7 @@ struct SweepArgs {
 struct P2PArgs {
     const int *off, *k, *g;      // per owned cell: remote targets (peer slot, ghost local index), CSR
     double *const *peer_wp;      // [peer slot] the peer's W' array on this level
+    const int *peer_nloc;        // [peer slot] the peer's cells (owned + ghosts) on this level
     int np;                      // peers on this level (0: count phases only)
     const int *wait_rank;        // [np] their ranks
     int *const *sig;             // [np] &peer.flags[my rank]
@@ -440,9 +441,11 @@ __device__ __forceinline__ void p2p_store(const P2PArgs &p, int i, const double 
 {
     if constexpr (P2P) {
         for (int m = p.off[i]; m < p.off[i + 1]; ++m) {
-            double *r = p.peer_wp[p.k[m]] + (size_t)p.g[m] * Wp<D>::STRIDE;
+            double *r = p.peer_wp[p.k[m]];
+            const size_t g = (size_t)p.g[m], nl = (size_t)p.peer_nloc[p.k[m]];
 #pragma unroll
-            for (int q = 0; q < D + 2; ++q) r[q] = w[q];
+            for (int q = 0; q < 4; ++q) r[4 * g + q] = w[q];
+            if constexpr (D == 3) r[4 * nl + g] = w[4];
         }
     }
 }
@@ -462,7 +465,8 @@ __device__ __forceinline__ void ld2x(const double *p, double *v)
 template <int D, int LPC, bool FF, bool CG, bool P2P>
 __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p, int gt0, int nthr, bool pdl)
 {
-    constexpr int NV = D + 2, WS = Wp<D>::STRIDE;
+    constexpr int NV = D + 2;
+    const size_t nl = (size_t)a.n_loc;
     const int total = (a.cend - a.cbeg) * LPC;
     const int rounds = (total + nthr - 1) / nthr;
     for (int r = 0; r < rounds; ++r) {
@@ -485,20 +489,20 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
                 ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
                 if constexpr (FF) {
                     double wl[NV], t0[NV];
-                    ld_state<D, CG>(a.wlin + (size_t)j * WS, wl);
+                    ld_state<D, CG>(a.wlin, nl, j, wl);
                     flux_rw<D>(wl, sr, sr[D], a.gm1, t0);
 #pragma unroll
                     for (int q = 0; q < NV; ++q) accP[q] += t0[q];
                     if (j < a.lo || j >= a.n_own) {   // earlier color (updated in this half-sweep) or ghost
                         double w1[NV], t1[NV];
-                        ld_state<D, CG>(a.wp + (size_t)j * WS, w1);
+                        ld_state<D, CG>(a.wp, nl, j, w1);
                         flux_rw<D>(w1, sr, sr[D], a.gm1, t1);
 #pragma unroll
                         for (int q = 0; q < NV; ++q) acc[q] += t1[q] - t0[q];
                     }
                 } else {
                     double w1[NV], t1[NV];
-                    ld_state<D, CG>(a.wp + (size_t)j * WS, w1);
+                    ld_state<D, CG>(a.wp, nl, j, w1);
                     flux_rw<D>(w1, sr, sr[D], a.gm1, t1);
 #pragma unroll
                     for (int q = 0; q < NV; ++q) acc[q] += t1[q];
@@ -520,7 +524,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
             double wn[NV], x[kXr];
             if constexpr (FF) {
                 double wl[NV], rr[NV], dd[2];
-                ld_state<D, CG>(a.wlin + (size_t)i * WS, wl);
+                ld_state<D, CG>(a.wlin, nl, i, wl);
 #pragma unroll
                 for (int q = 0; q < NV; ++q) rr[q] = CG ? __ldcg(a.rhs + (size_t)i * NV + q) : __ldcs(a.rhs + (size_t)i * NV + q);
                 ld2x<CG>(a.dc + 2 * (size_t)i, dd);
@@ -546,7 +550,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
 #pragma unroll
                 for (int q = 0; q < NV; ++q) wn[q] = x[q] - c * acc[q];
             }
-            st_state<D>(a.wp + (size_t)i * WS, wn);
+            st_state<D>(a.wp, nl, i, wn);
             p2p_store<D, P2P>(p, i, wn);
             if (a.Wout) {
 #pragma unroll
@@ -560,7 +564,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
 // the sweep launch: 128-thread blocks, 8 per SM (FF, with its second set of
 // accumulators: 6 per SM), grid = one resident wave
 template <int D, int LPC, bool FF>
-__global__ void __launch_bounds__(128, FF ? 7 : 8) k_sweep(SweepArgs a)
+__global__ void __launch_bounds__(128, FF ? 6 : 8) k_sweep(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
     sweep_cells<D, LPC, FF, false, false>(a, P2PArgs{}, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x,
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
     const size_t o = (size_t)c * NV;
 #pragma unroll
     for (int q = 0; q < NV; ++q) { w[q] = w[q] / vc; C.Rs[o + q] = r[q]; }
-    st_state<D>(C.wlin + (size_t)c * Wp<D>::STRIDE, w);
+    st_state<D>(C.wlin, (size_t)C.n_loc, c, w);
     C.alpha[c] = a;
 }
 
@@ -650,18 +654,20 @@ template <int D>
 __global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLevel C2, int nl)
 {
     pdl_enter();
-    constexpr int NV = D + 2, WS = Wp<D>::STRIDE;
+    constexpr int NV = D + 2;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= F0.n) return;
     const int p = F0.parent[i];
-    double corr[NV];
+    double corr[NV], w0[NV];
+    ld_state<D>(C1.wlin, (size_t)C1.n_loc, p, w0);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) corr[q] = C1.W[(size_t)p * NV + q] - C1.wlin[(size_t)p * WS + q];
+    for (int q = 0; q < NV; ++q) corr[q] = C1.W[(size_t)p * NV + q] - w0[q];
     if (nl >= 3) {
         const int pp = C1.parent[p];
         const double a1 = C1.alpha[p];
+        ld_state<D>(C2.wlin, (size_t)C2.n_loc, pp, w0);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) corr[q] += a1 * (C2.W[(size_t)pp * NV + q] - C2.wlin[(size_t)pp * WS + q]);
+        for (int q = 0; q < NV; ++q) corr[q] += a1 * (C2.W[(size_t)pp * NV + q] - w0[q]);
     }
     const double a0 = F0.alpha[i];
 #pragma unroll
@@ -686,14 +692,19 @@ __global__ void k_to_natural(int n, int N, int ncomp, const int *__restrict__ pe
     const int nat = perm[i];
     for (int q = 0; q < ncomp; ++q) dst[(size_t)q * N + nat] = src[(size_t)i * stride + offset + q];
 }
-// dW = W' - W_lin of n owned cells -> natural SoA [ncomp][N] (gmg_smooth)
-__global__ void k_diff_to_natural(int n, int N, int ncomp, const int *__restrict__ perm, const double *__restrict__ a,
-                                  const double *__restrict__ b, int stride, double *__restrict__ dst)
+// a state array (Wp layout, nloc cells) minus another (nullable) over n owned cells -> natural SoA [ncomp][N]
+// (W0 = W_lin, dW = W' - W_lin; gmg_get_level_field, gmg_smooth)
+__global__ void k_state_to_natural(int n, int N, int ncomp, const int *__restrict__ perm, const double *__restrict__ a,
+                                   const double *__restrict__ b, int nloc, double *__restrict__ dst)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int nat = perm[i];
-    for (int q = 0; q < ncomp; ++q) dst[(size_t)q * N + nat] = a[(size_t)i * stride + q] - b[(size_t)i * stride + q];
+    const int split = ncomp == 5 ? nloc : 0;
+    for (int q = 0; q < ncomp; ++q) {
+        const size_t o = elem_at((size_t)i, q, 4, 0, split);
+        dst[(size_t)q * N + nat] = b ? a[o] - b[o] : a[o];
+    }
 }
 // owned-compact [ncomp][n] (SoA, local owned order) <-> AoS [n][ncomp]
 __global__ void k_soa_to_aos(int n, int ncomp, const double *__restrict__ src, double *__restrict__ dst)

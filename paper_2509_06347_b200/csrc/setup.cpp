@@ -666,6 +666,8 @@ void build_p2p_targets(DomLevel &D, int me, int ncolor, const std::vector<const 
                 tg[D.send_idx[s0 + t]].push_back({(int32_t)k, Q.recv_idx[r0 + t]});
         }
     }
+    D.p2p_peer_nloc.assign(np, 0);
+    for (int k = 0; k < np; ++k) D.p2p_peer_nloc[k] = (int32_t)peer_dom[k]->n_loc;
     D.p2p_off.assign(D.n_own + 1, 0);
     D.p2p_k.clear();
     D.p2p_g.clear();
