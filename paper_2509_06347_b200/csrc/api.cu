@@ -197,7 +197,7 @@ void enqueue_gather(Launcher &Lc, Domain &dm, int di, int l, int flags, double *
     Lc.post(GMG_K_GATHER, dm.lbytes[l].gather);
     if (flags & G_NORM) {
         Lc.pre(GMG_K_NORM);
-        klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(256), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + (size_t)di * L.nv);
+        klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(1024), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + (size_t)di * L.nv);
         Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
     }
 }
@@ -658,7 +658,7 @@ void enqueue_ho_eval(Launcher &Lc, int mode, double *DevLevel::*Rout = nullptr, 
         Lc.post(GMG_K_GATHER, dm.ho.bytes_gather);
         if (mode & HO_NORM) {
             Lc.pre(GMG_K_NORM);
-            klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(256), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + di * L.nv);
+            klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(1024), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + di * L.nv);
             Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
         }
     }

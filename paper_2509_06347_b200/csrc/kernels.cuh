@@ -257,23 +257,30 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     }
 }
 
-// deterministic reduction of one domain's norm partials -> sumsq[q]
-__global__ void __launch_bounds__(256) k_norm_sum(const double *__restrict__ partial, int nblocks, int nv,
-                                                  double *sumsq)
+// deterministic reduction of one domain's norm partials -> sumsq[q]: 1024
+// threads, each sums a fixed strided subset of the blocks for all nv
+// components at once, then a fixed shuffle + shared-memory tree (the same
+// order on every run)
+__global__ void __launch_bounds__(1024) k_norm_sum(const double *__restrict__ partial, int nblocks, int nv,
+                                                   double *sumsq)
 {
     pdl_enter();
-    __shared__ double sh[256];
+    __shared__ double sh[32][5];
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < nblocks; b += 1024)
+        for (int q = 0; q < nv; ++q) v[q] += partial[(size_t)b * nv + q];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int q = 0; q < nv; ++q) {
-        double s = 0.0;
-        for (int b = threadIdx.x; b < nblocks; b += 256) s += partial[(size_t)b * nv + q];
-        sh[threadIdx.x] = s;
-        __syncthreads();
-        for (int w = 128; w > 0; w >>= 1) {
-            if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-            __syncthreads();
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], o);
+        if (lane == 0) sh[wid][q] = v[q];
+    }
+    __syncthreads();
+    if (wid == 0) {
+        for (int q = 0; q < nv; ++q) {
+            double t = sh[lane][q];
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+            if (lane == 0) sumsq[q] = t;
         }
-        if (threadIdx.x == 0) sumsq[q] = sh[0];
-        __syncthreads();
     }
 }
 
@@ -564,7 +571,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
 // the sweep launch: 128-thread blocks, 8 per SM (FF, with its second set of
 // accumulators: 6 per SM), grid = one resident wave
 template <int D, int LPC, bool FF>
-__global__ void __launch_bounds__(128, FF ? 6 : 8) k_sweep(SweepArgs a)
+__global__ void __launch_bounds__(128, FF ? 6 : 9) k_sweep(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
     sweep_cells<D, LPC, FF, false, false>(a, P2PArgs{}, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x,
