@@ -365,12 +365,16 @@ void launch_with_window(K kernel, dim3 g, dim3 b, cudaStream_t s, const SweepArg
 // lanes per cell of a color block: the configured lanes for large blocks; a
 // block that still fits one resident wave at twice the lanes gets them (up to
 // 16) -- small trailing colors are latency chains of ceil(deg/LPC) gathers
+#ifndef GMG_MAX_LPC
+#define GMG_MAX_LPC 16
+#endif
+constexpr int kMaxLpc = GMG_MAX_LPC;
 int sweep_lpc(const gmg_ctx *ctx, int64_t cells)
 {
     int lpc = ctx->lpc;
     if (ctx->adapt_lpc && ctx->sweep_grid_cap > 0) {
         const int64_t wave = (int64_t)ctx->sweep_grid_cap * 128;
-        while (lpc < 16 && cells * lpc * 2 <= wave) lpc *= 2;
+        while (lpc < kMaxLpc && cells * lpc * 2 <= wave) lpc *= 2;
     }
     return lpc;
 }

@@ -137,8 +137,10 @@ __global__ void __launch_bounds__(256, DF ? 3 : 4) k_face(DevLevel L, const doub
         }
     }
     double *o = L.Frec + (size_t)f * kFaceRec;
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o), "d"(out[0]), "d"(out[1]), "d"(out[2]), "d"(out[3])
-                 : "memory");
+    // without the flux only S r (in the second 32-B chunk) is read back: the first chunk is not written
+    if (FLUX)
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o), "d"(out[0]), "d"(out[1]), "d"(out[2]), "d"(out[3])
+                     : "memory");
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(o + 4), "d"(out[4]), "d"(out[5]), "d"(out[6]),
                  "d"(out[7])
                  : "memory");
