@@ -46,6 +46,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
                        "--expt-relaxed-constexpr"]
     if verbose_ptxas:
         flags += ["-Xptxas", "-v"]
+    flags += os.environ.get("GMG_NVCC_DEFS", "").split()   # development builds of kernel variants (-D...)
     objs, jobs = [], []
     nv = [NVCC] + flags + ["-c"]
     for src, cmd in (("setup.cpp", gxx), ("ho_setup.cpp", gxx), ("api.cu", nv),

@@ -81,6 +81,23 @@ __device__ __forceinline__ void ld4nc(const double *p, double *v)
     asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
                  : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
 }
+// L1 policy hints of the sweep: slot records and the own (X, c) record are
+// read once (no L1 allocation), the gathered neighbour records are the ones
+// worth keeping (evict last)
+__device__ __forceinline__ void ld4na(const double *p, double *v)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld4el(const double *p, double *v)
+{
+    asm volatile("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld2na(const double *p, double *v)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
+}
 __device__ __forceinline__ void ld4cs(const double *p, double *v)
 {
     asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
@@ -120,11 +137,12 @@ __device__ __forceinline__ void st_state(double *base, size_t nloc, size_t i, co
 
 // cell i of a state array of nloc cells -> w[nv] (one 256-bit load, plus one
 // 64-bit load in 3D); CG: L2-coherent (states written by other blocks of the
-// same launch), else the non-coherent path
-template <int D, bool CG = false>
+// same launch), else the non-coherent path (EL: L1 evict-last)
+template <int D, bool CG = false, bool EL = false>
 __device__ __forceinline__ void ld_state(const double *base, size_t nloc, size_t i, double *w)
 {
     if constexpr (CG) ld4cg(base + 4 * i, w);
+    else if constexpr (EL) ld4el(base + 4 * i, w);
     else ld4nc(base + 4 * i, w);
     if constexpr (D == 3) w[4] = CG ? __ldcg(base + 4 * nloc + i) : __ldg(base + 4 * nloc + i);
 }

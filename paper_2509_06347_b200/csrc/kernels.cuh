@@ -459,10 +459,11 @@ __device__ __forceinline__ void p2p_store(const P2PArgs &p, int i, const double 
     }
 }
 
-template <bool CG>
+template <bool CG, bool NA = false>
 __device__ __forceinline__ void ld2x(const double *p, double *v)
 {
     if constexpr (CG) ld2cg(p, v);
+    else if constexpr (NA) ld2na(p, v);
     else ld2nc(p, v);
 }
 
@@ -495,7 +496,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
             for (; e < e1; e += LPC) {
                 const int jn = e + LPC < e1 ? __ldg(a.sJe + e + LPC) : 0;
                 double sr[4];
-                ld4cs(a.sRe + (size_t)e * kSlotRec, sr);
+                ld4na(a.sRe + (size_t)e * kSlotRec, sr);   // read once: not allocated in L1
                 if constexpr (FF) {
                     double wl[NV], t0[NV];
                     ld_state<D, CG>(a.wlin, nl, j, wl);
@@ -511,7 +512,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
                     }
                 } else {
                     double w1[NV], t1[NV];
-                    ld_state<D, CG>(a.wp, nl, j, w1);
+                    ld_state<D, CG, true>(a.wp, nl, j, w1);
                     flux_rw<D>(w1, sr, sr[D], a.gm1, t1);
 #pragma unroll
                     for (int q = 0; q < NV; ++q) acc[q] += t1[q];
@@ -552,9 +553,9 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
                 st2(xo + 4, x + 4);
             } else {
                 const double *xi = a.xr + (size_t)i * kXr;
-                ld2x<CG>(xi, x);
-                ld2x<CG>(xi + 2, x + 2);
-                ld2x<CG>(xi + 4, x + 4);
+                ld2x<CG, true>(xi, x);
+                ld2x<CG, true>(xi + 2, x + 2);
+                ld2x<CG, true>(xi + 4, x + 4);
                 const double c = x[NV];
 #pragma unroll
                 for (int q = 0; q < NV; ++q) wn[q] = x[q] - c * acc[q];
