@@ -224,6 +224,7 @@ struct gmg_ctx {
     int64_t exchanges = 0;            // halo exchanges in the last recorded sequence
     int sweep_grid_cap = 0;           // sweep grid = one resident wave: SMs x blocks/SM (set with the workspace)
     int sweep_grid_cap_ff = 0;        // the same for the first-forward variant (more registers)
+    int sweep_grid_cap_ff1 = 0;       // ... and for the first-forward phase of the first color (no W' gathers)
     int64_t visits = 0;               // cell-updates executed by the last recorded sequence
     int lpc = 2;                      // sweep lanes per cell of the large color blocks (gmg_options.sweep_lanes)
     int adapt_lpc = 1;                // blocks that fit one wave at 2x lanes get up to 16 lanes per cell

@@ -472,7 +472,10 @@ __device__ __forceinline__ void ld2x(const double *p, double *v)
 // wave); PDL: the slot range and first neighbour index (static during a
 // smoothing step) are loaded before griddepcontrol.wait, so they overlap the
 // previous phase's tail, and the records after it
-template <int D, int LPC, bool FF, bool CG, bool P2P>
+// FF: 0 = a plain phase, 1 = a first-forward phase, 2 = the first-forward
+// phase of the first color with no ghosts (no earlier-color neighbour: no W'
+// gathers, W' = W - Rt/D)
+template <int D, int LPC, int FF, bool CG, bool P2P>
 __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p, int gt0, int nthr, bool pdl)
 {
     constexpr int NV = D + 2;
@@ -503,7 +506,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
                     flux_rw<D>(wl, sr, sr[D], a.gm1, t0);
 #pragma unroll
                     for (int q = 0; q < NV; ++q) accP[q] += t0[q];
-                    if (j < a.lo || j >= a.n_own) {   // earlier color (updated in this half-sweep) or ghost
+                    if (FF == 1 && (j < a.lo || j >= a.n_own)) {   // earlier color (updated in this half-sweep) or ghost
                         double w1[NV], t1[NV];
                         ld_state<D, CG>(a.wp, nl, j, w1);
                         flux_rw<D>(w1, sr, sr[D], a.gm1, t1);
@@ -571,10 +574,11 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
     if (pdl) pdl_wait();   // threads without a cell: nothing may run past the predecessor
 }
 
-// the sweep launch: 128-thread blocks, 8 per SM (FF, with its second set of
-// accumulators: 6 per SM), grid = one resident wave
-template <int D, int LPC, bool FF>
-__global__ void __launch_bounds__(128, FF ? 6 : 9) k_sweep(SweepArgs a)
+// the sweep launch: 128-thread blocks, 9 per SM (FF, with its second set of
+// accumulators: 6 per SM; the first color's FF, without W' gathers: 7),
+// grid = one resident wave
+template <int D, int LPC, int FF>
+__global__ void __launch_bounds__(128, FF == 2 ? 7 : FF ? 6 : 9) k_sweep(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
     sweep_cells<D, LPC, FF, false, false>(a, P2PArgs{}, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x,
