@@ -1348,11 +1348,12 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
                 for (int64_t i = 0; i < H.n_own; ++i) { si[2 * i] = H.soffc[i]; si[2 * i + 1] = H.deg_int[i]; }
                 CK(up_i((const int *)L.sinfo, std::move(si)));
                 std::vector<int> gi(4 * H.n_own);
-                for (int64_t i = 0; i < H.n_own; ++i) {
-                    gi[4 * i] = H.gbase[i];
-                    gi[4 * i + 1] = (int)H.deg_all[i] | ((int)H.deg_int[i] << 16);
-                    gi[4 * i + 2] = H.soffc[i];
-                    gi[4 * i + 3] = 0;
+                for (int64_t t = 0; t < H.n_own; ++t) {
+                    const int i = H.gord[t];
+                    gi[4 * t] = H.gbase[i];
+                    gi[4 * t + 1] = (int)H.deg_all[i] | ((int)H.deg_int[i] << 16);
+                    gi[4 * t + 2] = i;
+                    gi[4 * t + 3] = 0;
                 }
                 CK(up_i((const int *)L.ginfo, std::move(gi)));
             }

@@ -52,7 +52,8 @@ struct DomLevel {
     std::vector<int64_t> fnat;             // [nf] natural ids of the local faces (ascending)
     std::vector<int32_t> fl, fr;           // [nf] local left / right, fr < 0: -(patch+1)
     std::vector<double> vol;               // [n_own]
-    // gather slots (SELL-32 over owned cells: per color, chunks of 32 cells, entries [slot][lane])
+    // gather slots (SELL-32 over owned cells in the gather order: chunks of 32 cells, entries [slot][lane])
+    std::vector<int32_t> gord;             // [n_own] gather position -> owned cell (Morton across colors)
     int64_t nchunks = 0, ng_entries = 0, ns_entries = 0;
     std::vector<int32_t> goff, gbase;      // [nchunks], [n_own]
     std::vector<uint8_t> deg_int, deg_all; // [n_own]
@@ -122,7 +123,7 @@ struct DevLevel {
     const int *gface;
     const int2 *sinfo;           // [n] (first sweep slot, interior slots) packed for one 8-byte load
     const int2 *fslot;           // [nf] sweep entries of the face (left cell, right cell), -1 = none
-    const int4 *ginfo;           // [n] (gbase, deg_all | deg_int << 16, first sweep slot, 0) for the gather
+    const int4 *ginfo;           // [n] per gather position t: (gbase, deg_all | deg_int << 16, cell, 0)
     const int *sJe;              // [ne] neighbour, -1 = padding
     double *sRe;                 // [ne][4] A outward + S r
     const int *perm;             // [n_loc] local -> natural

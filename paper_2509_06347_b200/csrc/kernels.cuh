@@ -154,13 +154,14 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 {
     pdl_launch_dependents();
     constexpr int NV = D + 2;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;   // gather position (ginfo.z: the cell)
     double R[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) R[q] = 0.0;
     // static slot data before the PDL wait (overlaps the predecessor's tail), face records after it
     int4 gi = make_int4(0, 0, 0, 0);
-    if (i < L.n) gi = __ldg(L.ginfo + i);
+    if (t < L.n) gi = __ldg(L.ginfo + t);
+    const int i = gi.z;
     pdl_wait();
     // the cell's one per-cell input of the epilogue (W for G_COPY_W, Rs for G_SET_F, F for G_ADD_F, the
     // explicit state for G_EXPLICIT) is loaded before the slot loop: its latency hides under the gathers,
@@ -168,13 +169,13 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     const int pk = (a.flags & G_COPY_W) ? G_COPY_W : (a.flags & G_SET_F) ? G_SET_F
                  : ((a.flags & G_WRITE_RT) && (a.flags & G_ADD_F)) ? G_ADD_F : (a.flags & G_EXPLICIT) ? G_EXPLICIT : 0;
     double pre[NV];
-    if (i < L.n && pk) {
+    if (t < L.n && pk) {
         const double *src = pk == G_COPY_W ? L.W : pk == G_SET_F ? L.Rs : pk == G_ADD_F ? L.F : a.Wexp;
 #pragma unroll
         for (int q = 0; q < NV; ++q) pre[q] = src[(size_t)i * NV + q];
     }
-    if (i < L.n) {
-        // (gather base, all slots | interior slots << 16, sweep slot 0, sweep stride): one 16-byte load
+    if (t < L.n) {
+        // (gather base, all slots | interior slots << 16, cell, 0): one 16-byte load
         const int gb = gi.x, nt = gi.y & 0xffff;
         double sig = 0.0, al = 1.0;
         for (int s = 0; s < nt; ++s) {

@@ -398,9 +398,10 @@ void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *p
 // otherwise), then one layer of ghosts in (owner, color, natural id) order;
 // local faces = faces touching an owned cell, ordered by their first local
 // cell; layouts over owned cells:
-//  * gather slots (residual/prepare, thread per cell): SELL-32 -- per color,
-//    chunks of 32 consecutive cells, entries [slot][lane], chunk padded to its
-//    max degree.  Slots: interior faces (ascending id) then boundary faces.
+//  * gather slots (residual/prepare, thread per cell, cells in the gather
+//    order gord -- Morton across colors): SELL-32 -- chunks of 32 consecutive
+//    cells of that order, entries [slot][lane], chunk padded to its max
+//    degree.  Slots: interior faces (ascending id) then boundary faces.
 //  * sweep slots (lanes per cell): CSR -- cell i's interior slots are
 //    contiguous at [soffc[i], soffc[i+1]), same order as its gather slots;
 //    per slot the neighbour sJe and a 32-byte record (A_x, A_y, [A_z,] S r)
@@ -442,6 +443,7 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton)
     // single domain: inside each color block the cells are ordered by the
     // Morton (Z-order) key of their centroid -- neighbours of consecutive cells
     // are then close in memory (L2 reuse of the gathered records, DESIGN.md §6 v13)
+    std::vector<uint64_t> key;
     if (morton) {
         // Morton (Z-order) key of the centroid: the same spatial grouping as
         // fine RCB chunks at a fraction of the setup cost
@@ -458,7 +460,7 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton)
             for (int b = 0; b < bits; ++b) r |= ((v >> b) & 1ull) << (b * d);
             return r;
         };
-        std::vector<uint64_t> key(N);
+        key.assign(N, 0);
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < N; ++i) {
             uint64_t code = 0;
@@ -564,21 +566,31 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton)
             D.deg_all[i] = (uint8_t)(a1 - a0);
         }
     }
-    // SELL-32 gather chunks per color
+    // gather order (the residual / prepare kernels have no color dependency): the
+    // owned cells by Morton key across all colors, so the two cells of a face --
+    // which read its face record -- are visited close in time (the second read
+    // hits L2); without Morton keys the internal order
+    D.gord.resize(D.n_own);
+    for (int64_t i = 0; i < D.n_own; ++i) D.gord[i] = (int32_t)i;
+    if (!key.empty())
+        std::sort(D.gord.begin(), D.gord.end(), [&](int32_t a, int32_t b) {
+            const uint64_t ka = key[D.l2n[a]], kb = key[D.l2n[b]];
+            return ka < kb || (ka == kb && D.l2n[a] < D.l2n[b]);
+        });
+    // SELL-32 gather chunks: 32 consecutive cells of the gather order
     std::vector<int32_t> cchunk(D.n_own, 0), lane(D.n_own, 0);
     int64_t go = 0;
-    for (int c = 0; c < G.ncolor; ++c) {
-        for (int64_t i0 = D.blk[c]; i0 < D.blk[c + 1]; i0 += kChunk) {
-            const int64_t i1 = std::min<int64_t>(i0 + kChunk, D.blk[c + 1]);
-            int mg = 0;
-            for (int64_t i = i0; i < i1; ++i) {
-                mg = std::max<int>(mg, D.deg_all[i]);
-                cchunk[i] = (int32_t)D.goff.size();
-                lane[i] = (int32_t)(i - i0);
-            }
-            D.goff.push_back((int32_t)go);
-            go += (int64_t)mg * kChunk;
+    for (int64_t t0 = 0; t0 < D.n_own; t0 += kChunk) {
+        const int64_t t1 = std::min<int64_t>(t0 + kChunk, D.n_own);
+        int mg = 0;
+        for (int64_t t = t0; t < t1; ++t) {
+            const int32_t i = D.gord[t];
+            mg = std::max<int>(mg, D.deg_all[i]);
+            cchunk[i] = (int32_t)D.goff.size();
+            lane[i] = (int32_t)(t - t0);
         }
+        D.goff.push_back((int32_t)go);
+        go += (int64_t)mg * kChunk;
     }
     D.nchunks = (int64_t)D.goff.size();
     D.soffc.assign(D.n_own + 1, 0);
