@@ -479,6 +479,17 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton)
         }
     }
     for (int64_t i = 0; i < D.n_own; ++i) n2l[D.l2n[i]] = (int32_t)i;
+    // gather order (the residual / prepare kernels have no color dependency): the
+    // owned cells by Morton key across all colors, so the two cells of a face --
+    // which read its face record -- are visited close in time (the second read
+    // hits L2); without Morton keys the internal order
+    D.gord.resize(D.n_own);
+    for (int64_t i = 0; i < D.n_own; ++i) D.gord[i] = (int32_t)i;
+    if (!key.empty())
+        std::sort(D.gord.begin(), D.gord.end(), [&](int32_t a, int32_t b) {
+            const uint64_t ka = key[D.l2n[a]], kb = key[D.l2n[b]];
+            return ka < kb || (ka == kb && D.l2n[a] < D.l2n[b]);
+        });
     std::vector<int64_t> ghosts;
     for (int64_t f = 0; f < G.nf; ++f) {
         const int64_t l = G.left[f], r = G.right[f];
@@ -566,17 +577,6 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton)
             D.deg_all[i] = (uint8_t)(a1 - a0);
         }
     }
-    // gather order (the residual / prepare kernels have no color dependency): the
-    // owned cells by Morton key across all colors, so the two cells of a face --
-    // which read its face record -- are visited close in time (the second read
-    // hits L2); without Morton keys the internal order
-    D.gord.resize(D.n_own);
-    for (int64_t i = 0; i < D.n_own; ++i) D.gord[i] = (int32_t)i;
-    if (!key.empty())
-        std::sort(D.gord.begin(), D.gord.end(), [&](int32_t a, int32_t b) {
-            const uint64_t ka = key[D.l2n[a]], kb = key[D.l2n[b]];
-            return ka < kb || (ka == kb && D.l2n[a] < D.l2n[b]);
-        });
     // SELL-32 gather chunks: 32 consecutive cells of the gather order
     std::vector<int32_t> cchunk(D.n_own, 0), lane(D.n_own, 0);
     int64_t go = 0;
