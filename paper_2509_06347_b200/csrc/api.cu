@@ -873,7 +873,7 @@ void carve(gmg_ctx *ctx, Bump &b)
             L.Rs = b.take<double>((size_t)nv * n); L.F = b.take<double>((size_t)nv * n);
             L.alpha = b.take<double>(n); L.sigma = b.take<double>(n);
             L.deg_int = b.take<uint8_t>(n); L.deg_all = b.take<uint8_t>(n);
-            L.gbase = b.take<int>(n);
+            L.gord = b.take<int>(n);
             L.gface = b.take<int>(H.ng_entries);
             L.sinfo = b.take<int2>(n);
             L.fslot = b.take<int2>(nf);
@@ -1336,7 +1336,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(up_raw(L.vol, H.vol.data(), H.vol.size() * sizeof(double)));
             CK(up_raw(L.deg_int, H.deg_int.data(), H.deg_int.size()));
             CK(up_raw(L.deg_all, H.deg_all.data(), H.deg_all.size()));
-            CK(up_raw(L.gbase, H.gbase.data(), H.gbase.size() * sizeof(int)));
+            CK(up_raw(L.gord, H.gord.data(), H.gord.size() * sizeof(int)));
             CK(up_raw(L.gface, H.gface.data(), H.gface.size() * sizeof(int)));
             CK(up_raw(L.fslot, H.fslot.data(), H.fslot.size() * sizeof(int)));
             CK(up_raw(L.p2p_off, H.p2p_off.data(), H.p2p_off.size() * sizeof(int)));

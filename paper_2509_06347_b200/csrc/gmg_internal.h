@@ -119,7 +119,7 @@ struct DevLevel {
     double *xr;                  // [n][kXr] X = W_lin - Rt/D + c P, c = alpha/(2D) (own-cell record)
     double *dc;                  // [n][2] 1/D, alpha/(2D) of the hybrid diagonal (gather G_PREPARE)
     const uint8_t *deg_int, *deg_all;    // [n]
-    const int *gbase;            // [n]
+    const int *gord;             // [n] gather position -> owned cell (Morton across colors)
     const int *gface;
     const int2 *sinfo;           // [n] (first sweep slot, interior slots) packed for one 8-byte load
     const int2 *fslot;           // [nf] sweep entries of the face (left cell, right cell), -1 = none

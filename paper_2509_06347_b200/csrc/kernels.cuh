@@ -641,8 +641,10 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
 {
     pdl_enter();
     constexpr int NV = D + 2;
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C.n) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= C.n) return;
+    const int c = __ldg(C.gord + t);   // coarse cells in the Morton order across colors: the children's
+                                       // records are read as one ordered stream per fine color block
     const int k0 = C.child[c], k1 = C.child[C.n + c];
     const double V0 = Fn.vol[k0];
     double w[NV], r[NV];
@@ -670,8 +672,9 @@ __global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLe
 {
     pdl_enter();
     constexpr int NV = D + 2;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= F0.n) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= F0.n) return;
+    const int i = __ldg(F0.gord + t);   // fine cells in the Morton order across colors (see k_restrict)
     const int p = F0.parent[i];
     double corr[NV], w0[NV];
     ld_state<D>(C1.wlin, (size_t)C1.n_loc, p, w0);
