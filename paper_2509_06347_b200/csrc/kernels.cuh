@@ -57,7 +57,7 @@ template <int D> struct FR { static constexpr int SR = D + 2, AM = D + 3; };
 // cells -- whole 32-byte records, so no partial-sector update (the gather
 // used to patch S r into each slot)
 template <int D, bool FLUX, int STRIDE, bool DF, bool PREP>
-__global__ void __launch_bounds__(256, DF ? 3 : 4) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
+__global__ void __launch_bounds__(256, 4) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
 {
     pdl_launch_dependents();
     constexpr int NV = D + 2;
