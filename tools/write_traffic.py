@@ -28,7 +28,7 @@ def main(d, tag):
     cls = defaultdict(float)
     for k in cyc:
         cls[k[1].split("(")[0].split("<")[0].replace("void ", "")] += per[k]["gpu__time_duration.sum"]
-    out = {"kernel": "k_sweep<3, LPC, FF> (W' formulation: neighbour record W' 64 B, own (X, c) 48 B)",
+    out = {"kernel": "k_sweep<3, LPC, FF> (W' formulation: neighbour record W' 40 B: [n][4] (rho, m) + [n] rho E, own (X, c) 48 B)",
            "captured": f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, "
                        f"bench.py --profile-only (config 4), every sweep launch of one V-cycle, cold L2 per launch; "
                        f"tools/profile_r2.sh {tag}",
