@@ -127,6 +127,60 @@ __device__ __forceinline__ void st4(double *p, const double *v)
                  : "memory");
 }
 
+// Cell record i of an AoS array [n][NV] (base 256-B aligned).  NV = 4: one
+// 256-bit access.  NV = 5 (40 B): three accesses instead of five -- a 128-bit
+// pair starting at the first 16-B boundary of the record (element 0 for even
+// i, element 1 for odd i), a second pair after it and the remaining scalar;
+// every lane issues the same three instructions (no divergence on parity).
+// NC: the read-only path (the array is not written by the kernel).
+template <int NV, bool NC = false>
+__device__ __forceinline__ void ld_rec(const double *base, size_t i, double *w)
+{
+    const double *p = base + (size_t)NV * i;
+    if constexpr (NV == 4) {
+        if constexpr (NC) ld4nc(p, w);
+        else {
+            asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(w[0]), "=d"(w[1]), "=d"(w[2]), "=d"(w[3]) : "l"(p) : "memory");
+        }
+    } else {
+        static_assert(NV == 5, "records of 4 or 5 doubles");
+        const int o = (int)(i & 1);
+        double a[2], b[2], s;
+        if constexpr (NC) {
+            ld2nc(p + o, a);
+            ld2nc(p + o + 2, b);
+            s = __ldg(p + (o ? 0 : 4));
+        } else {
+            const double2 va = *reinterpret_cast<const double2 *>(p + o);
+            const double2 vb = *reinterpret_cast<const double2 *>(p + o + 2);
+            a[0] = va.x; a[1] = va.y; b[0] = vb.x; b[1] = vb.y;
+            s = p[o ? 0 : 4];
+        }
+        w[0] = o ? s : a[0];
+        w[1] = o ? a[0] : a[1];
+        w[2] = o ? a[1] : b[0];
+        w[3] = o ? b[0] : b[1];
+        w[4] = o ? b[1] : s;
+    }
+}
+template <int NV>
+__device__ __forceinline__ void st_rec(double *base, size_t i, const double *w)
+{
+    double *p = base + (size_t)NV * i;
+    if constexpr (NV == 4) {
+        st4(p, w);
+    } else {
+        static_assert(NV == 5, "records of 4 or 5 doubles");
+        const int o = (int)(i & 1);
+        const double a[2] = {o ? w[1] : w[0], o ? w[2] : w[1]};
+        const double b[2] = {o ? w[3] : w[2], o ? w[4] : w[3]};
+        st2(p + o, a);
+        st2(p + o + 2, b);
+        p[o ? 0 : 4] = o ? w[0] : w[4];
+    }
+}
+
 // one state into cell i of a state array of nloc cells (layout above)
 template <int D>
 __device__ __forceinline__ void st_state(double *base, size_t nloc, size_t i, const double *w)

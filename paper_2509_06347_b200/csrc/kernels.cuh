@@ -78,8 +78,9 @@ __global__ void __launch_bounds__(256, 4) k_face(DevLevel L, const double *__res
         ld_state<D>(Wsrc, (size_t)L.n_loc, l, wl);
         if (r >= 0) ld_state<D>(Wsrc, (size_t)L.n_loc, r, wr);
     } else {
-        ld_vec<NV>(Wsrc + (size_t)l * STRIDE, wl);
-        if (r >= 0) ld_vec<NV>(Wsrc + (size_t)r * STRIDE, wr);
+        static_assert(STRIDE == NV, "W arrays are [n][nv]");
+        ld_rec<NV, true>(Wsrc, l, wl);
+        if (r >= 0) ld_rec<NV, true>(Wsrc, r, wr);
     }
     if (r < 0) ghost<D>(bc.kind[-r - 1], wl, bc, n, wr);
 
@@ -171,8 +172,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     double pre[NV];
     if (t < L.n && pk) {
         const double *src = pk == G_COPY_W ? L.W : pk == G_SET_F ? L.Rs : pk == G_ADD_F ? L.F : a.Wexp;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) pre[q] = src[(size_t)i * NV + q];
+        ld_rec<NV>(src, i, pre);
     }
     if (t < L.n) {
         // (gather base, all slots | interior slots << 16, cell, 0): one 16-byte load
@@ -210,8 +210,10 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         if (a.flags & G_COPY_W) st_state<D>(L.wlin, (size_t)L.n_loc, i, pre);
         if (a.flags & G_SET_F) {
             if (pk == G_SET_F) {
+                double v[NV];
 #pragma unroll
-                for (int q = 0; q < NV; ++q) L.F[o + q] = pre[q] - R[q];
+                for (int q = 0; q < NV; ++q) v[q] = pre[q] - R[q];
+                st_rec<NV>(L.F, i, v);
             } else {
 #pragma unroll
                 for (int q = 0; q < NV; ++q) L.F[o + q] = L.Rs[o + q] - R[q];
@@ -220,22 +222,25 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         if (a.flags & G_WRITE_RT) {
             if (a.flags & G_ADD_F) {
                 if (pk == G_ADD_F) {
+                    double v[NV];
 #pragma unroll
-                    for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q] + pre[q];
+                    for (int q = 0; q < NV; ++q) v[q] = R[q] + pre[q];
+                    st_rec<NV>(L.Rt, i, v);
                 } else {
 #pragma unroll
                     for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q] + L.F[o + q];
                 }
             } else {
-#pragma unroll
-                for (int q = 0; q < NV; ++q) L.Rt[o + q] = R[q];
+                st_rec<NV>(L.Rt, i, R);
             }
         }
         if (a.flags & G_EXPLICIT) {
             const double c = a.cfl_exp / sig;
             if (pk == G_EXPLICIT) {
+                double v[NV];
 #pragma unroll
-                for (int q = 0; q < NV; ++q) a.Wexp[o + q] = pre[q] - c * R[q];
+                for (int q = 0; q < NV; ++q) v[q] = pre[q] - c * R[q];
+                st_rec<NV>(a.Wexp, i, v);
             } else {
 #pragma unroll
                 for (int q = 0; q < NV; ++q) a.Wexp[o + q] = a.Wexp[o + q] - c * R[q];
@@ -566,10 +571,7 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
             }
             st_state<D>(a.wp, nl, i, wn);
             p2p_store<D, P2P>(p, i, wn);
-            if (a.Wout) {
-#pragma unroll
-                for (int q = 0; q < NV; ++q) a.Wout[(size_t)i * NV + q] = wn[q];
-            }
+            if (a.Wout) st_rec<NV>(a.Wout, i, wn);
         }
     }
     if (pdl) pdl_wait();   // threads without a cell: nothing may run past the predecessor
@@ -647,20 +649,24 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
                                        // records are read as one ordered stream per fine color block
     const int k0 = C.child[c], k1 = C.child[C.n + c];
     const double V0 = Fn.vol[k0];
-    double w[NV], r[NV];
+    double w[NV], r[NV], wk[NV], rk[NV];
     double a = Fn.alpha[k0];
+    ld_rec<NV, true>(Wf, k0, wk);
+    ld_rec<NV, true>(Rf, k0, rk);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) { w[q] = V0 * Wf[(size_t)k0 * NV + q]; r[q] = Rf[(size_t)k0 * NV + q]; }
+    for (int q = 0; q < NV; ++q) { w[q] = V0 * wk[q]; r[q] = rk[q]; }
     if (k1 >= 0) {
         const double V1 = Fn.vol[k1];
+        ld_rec<NV, true>(Wf, k1, wk);
+        ld_rec<NV, true>(Rf, k1, rk);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) { w[q] = w[q] + V1 * Wf[(size_t)k1 * NV + q]; r[q] = r[q] + Rf[(size_t)k1 * NV + q]; }
+        for (int q = 0; q < NV; ++q) { w[q] = w[q] + V1 * wk[q]; r[q] = r[q] + rk[q]; }
         a = fmin(a, Fn.alpha[k1]);
     }
     const double vc = C.vol[c];
-    const size_t o = (size_t)c * NV;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) { w[q] = w[q] / vc; C.Rs[o + q] = r[q]; }
+    for (int q = 0; q < NV; ++q) w[q] = w[q] / vc;
+    st_rec<NV>(C.Rs, c, r);
     st_state<D>(C.wlin, (size_t)C.n_loc, c, w);
     C.alpha[c] = a;
 }
@@ -676,20 +682,25 @@ __global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLe
     if (t >= F0.n) return;
     const int i = __ldg(F0.gord + t);   // fine cells in the Morton order across colors (see k_restrict)
     const int p = F0.parent[i];
-    double corr[NV], w0[NV];
+    double corr[NV], w0[NV], wc[NV];
     ld_state<D>(C1.wlin, (size_t)C1.n_loc, p, w0);
+    ld_rec<NV, true>(C1.W, p, wc);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) corr[q] = C1.W[(size_t)p * NV + q] - w0[q];
+    for (int q = 0; q < NV; ++q) corr[q] = wc[q] - w0[q];
     if (nl >= 3) {
         const int pp = C1.parent[p];
         const double a1 = C1.alpha[p];
         ld_state<D>(C2.wlin, (size_t)C2.n_loc, pp, w0);
+        ld_rec<NV, true>(C2.W, pp, wc);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) corr[q] += a1 * (C2.W[(size_t)pp * NV + q] - w0[q]);
+        for (int q = 0; q < NV; ++q) corr[q] += a1 * (wc[q] - w0[q]);
     }
     const double a0 = F0.alpha[i];
+    double wf[NV];
+    ld_rec<NV>(F0.W, i, wf);
 #pragma unroll
-    for (int q = 0; q < NV; ++q) F0.W[(size_t)i * NV + q] += a0 * corr[q];
+    for (int q = 0; q < NV; ++q) wf[q] += a0 * corr[q];
+    st_rec<NV>(F0.W, i, wf);
 }
 
 // ---------------------------------------------------------------------------
