@@ -155,7 +155,7 @@ void klaunch(gmg_ctx *ctx, void (*k)(KP...), dim3 g, dim3 b, cudaStream_t s, A..
 // a W_lin state array (Wp<D> layout), else a W array (stride nv)
 template <int D>
 void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, bool from_rec, bool df = false,
-                  bool prep = false)
+                  bool prep = false, bool sr = true)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
@@ -165,21 +165,21 @@ void enqueue_face(Launcher &Lc, Domain &dm, int l, const double *W, bool flux, b
     const Phys ph = phys(ctx);
     const BCs bc = bcs(ctx);
     if (prep) {
-        if (flux && df && !from_rec) klaunch(ctx, k_face<D, true, NV, true, true>, g, b, Lc.s, L, W, ph, bc);
-        else if (flux && !df && from_rec) klaunch(ctx, k_face<D, true, RS, false, true>, g, b, Lc.s, L, W, ph, bc);
-        else if (flux && !df && !from_rec) klaunch(ctx, k_face<D, true, NV, false, true>, g, b, Lc.s, L, W, ph, bc);
-        else if (!flux && from_rec) klaunch(ctx, k_face<D, false, RS, false, true>, g, b, Lc.s, L, W, ph, bc);
-        else if (!flux && !from_rec) klaunch(ctx, k_face<D, false, NV, false, true>, g, b, Lc.s, L, W, ph, bc);
+        if (flux && df && !from_rec) klaunch(ctx, k_face<D, true, NV, true, true>, g, b, Lc.s, L, W, ph, bc, (int)sr);
+        else if (flux && !df && from_rec) klaunch(ctx, k_face<D, true, RS, false, true>, g, b, Lc.s, L, W, ph, bc, (int)sr);
+        else if (flux && !df && !from_rec) klaunch(ctx, k_face<D, true, NV, false, true>, g, b, Lc.s, L, W, ph, bc, (int)sr);
+        else if (!flux && from_rec) klaunch(ctx, k_face<D, false, RS, false, true>, g, b, Lc.s, L, W, ph, bc, (int)sr);
+        else if (!flux && !from_rec) klaunch(ctx, k_face<D, false, NV, false, true>, g, b, Lc.s, L, W, ph, bc, (int)sr);
         else { ctx->err = "enqueue_face: unsupported prep variant"; return; }
     } else if (flux && df) {
-        if (from_rec) klaunch(ctx, k_face<D, true, RS, true, false>, g, b, Lc.s, L, W, ph, bc);
-        else klaunch(ctx, k_face<D, true, NV, true, false>, g, b, Lc.s, L, W, ph, bc);
+        if (from_rec) klaunch(ctx, k_face<D, true, RS, true, false>, g, b, Lc.s, L, W, ph, bc, (int)sr);
+        else klaunch(ctx, k_face<D, true, NV, true, false>, g, b, Lc.s, L, W, ph, bc, (int)sr);
     } else if (flux) {
-        if (from_rec) klaunch(ctx, k_face<D, true, RS, false, false>, g, b, Lc.s, L, W, ph, bc);
-        else klaunch(ctx, k_face<D, true, NV, false, false>, g, b, Lc.s, L, W, ph, bc);
+        if (from_rec) klaunch(ctx, k_face<D, true, RS, false, false>, g, b, Lc.s, L, W, ph, bc, (int)sr);
+        else klaunch(ctx, k_face<D, true, NV, false, false>, g, b, Lc.s, L, W, ph, bc, (int)sr);
     } else {
-        if (from_rec) klaunch(ctx, k_face<D, false, RS, false, false>, g, b, Lc.s, L, W, ph, bc);
-        else klaunch(ctx, k_face<D, false, NV, false, false>, g, b, Lc.s, L, W, ph, bc);
+        if (from_rec) klaunch(ctx, k_face<D, false, RS, false, false>, g, b, Lc.s, L, W, ph, bc, (int)sr);
+        else klaunch(ctx, k_face<D, false, NV, false, false>, g, b, Lc.s, L, W, ph, bc, (int)sr);
     }
     Lc.post(GMG_K_FACE, (flux ? dm.lbytes[l].face_flux : dm.lbytes[l].face_prep) + (prep ? dm.lbytes[l].face_slots : 0.0));
 }
@@ -715,7 +715,7 @@ void enqueue_vcycle(Launcher &Lc)
     if (nl == 1) return;
     // 3. residual at the smoothed state (A10) -> restricted
     for (size_t d = 0; d < doms.size(); ++d) {
-        enqueue_face<D>(Lc, doms[d], 0, doms[d].dv[0].W, true, false, df0);
+        enqueue_face<D>(Lc, doms[d], 0, doms[d].dv[0].W, true, false, df0, false, false);
         enqueue_gather<D>(Lc, doms[d], (int)d, 0, G_FLUX | G_WRITE_RT | (df0 ? G_ALPHA : 0), nullptr);
     }
     }
@@ -733,7 +733,7 @@ void enqueue_vcycle(Launcher &Lc)
         if (!last) {
             enqueue_ghost_w<D>(Lc, l);
             for (size_t d = 0; d < doms.size(); ++d) {
-                enqueue_face<D>(Lc, doms[d], l, doms[d].dv[l].W, true, false);
+                enqueue_face<D>(Lc, doms[d], l, doms[d].dv[l].W, true, false, false, false, false);
                 enqueue_gather<D>(Lc, doms[d], (int)d, l, G_FLUX | G_WRITE_RT | G_ADD_F, nullptr);   // Rt = R(W) + F (A11)
             }
         }
@@ -758,7 +758,7 @@ void enqueue_final_norm(Launcher &Lc)
     }
     enqueue_exchange<D>(Lc, 0, EX_W, -1);
     for (size_t d = 0; d < ctx->dom.size(); ++d) {
-        enqueue_face<D>(Lc, ctx->dom[d], 0, ctx->dom[d].dv[0].W, true, false);
+        enqueue_face<D>(Lc, ctx->dom[d], 0, ctx->dom[d].dv[0].W, true, false, false, false, false);
         enqueue_gather<D>(Lc, ctx->dom[d], (int)d, 0, G_FLUX | G_NORM, nullptr);
     }
     enqueue_norm_hist(Lc);

@@ -57,7 +57,7 @@ template <int D> struct FR { static constexpr int SR = D + 2, AM = D + 3; };
 // cells -- whole 32-byte records, so no partial-sector update (the gather
 // used to patch S r into each slot)
 template <int D, bool FLUX, int STRIDE, bool DF, bool PREP>
-__global__ void __launch_bounds__(256, 4) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc)
+__global__ void __launch_bounds__(256, 4) k_face(DevLevel L, const double *__restrict__ Wsrc, Phys ph, BCs bc, int need_sr)
 {
     pdl_launch_dependents();
     constexpr int NV = D + 2;
@@ -87,8 +87,9 @@ __global__ void __launch_bounds__(256, 4) k_face(DevLevel L, const double *__res
     double out[kFaceRec];
 #pragma unroll
     for (int q = 0; q < kFaceRec; ++q) out[q] = 0.0;
-    // spectral radius of the conservative average (O6, reading A5)
-    {
+    // spectral radius of the conservative average (O6, reading A5); launches whose
+    // gather uses no Sigma (restricted residual, R + F, norms) skip it
+    if (PREP || need_sr) {
         double wb[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) wb[q] = 0.5 * (wl[q] + wr[q]);
