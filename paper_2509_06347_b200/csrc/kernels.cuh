@@ -579,10 +579,10 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
 }
 
 // the sweep launch: 128-thread blocks, 9 per SM (FF, with its second set of
-// accumulators: 6 per SM; the first color's FF, without W' gathers: 7),
-// grid = one resident wave
+// accumulators, and the first color's FF, without W' gathers: 7), grid = one
+// resident wave
 template <int D, int LPC, int FF>
-__global__ void __launch_bounds__(128, FF == 2 ? 7 : FF ? 6 : 9) k_sweep(SweepArgs a)
+__global__ void __launch_bounds__(128, FF ? 7 : 9) k_sweep(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
     sweep_cells<D, LPC, FF, false, false>(a, P2PArgs{}, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x,
