@@ -4,6 +4,6 @@ cd "$(dirname "$0")/../.."
 cp paper_2509_06347_b200/libgmg.so /tmp/libgmg_keep.so
 for v in "$@"; do
     cp tools/dev/so/libgmg_$v.so paper_2509_06347_b200/libgmg.so
-    LANES=0 python ${TIMER:-tools/sweep_variants.py} | sed "s/^/$v /"
+    LANES=0 python ${TIMER:-tools/sweep_variants.py} 2>&1 | tail -1 | sed "s/^/$v /"
 done
 cp /tmp/libgmg_keep.so paper_2509_06347_b200/libgmg.so
