@@ -368,7 +368,7 @@ def test_weno_weights_favour_the_smooth_sub_stencil():
 def _farfield_meshes():
     F = configs.FARFIELD
     return [configs.tri_square(6, 6, seed=1), configs.quad_grid(5, 5),
-            configs.box3d(3, 3, 2, 1, seed=1, patch_kinds=(F,)), configs.box3d(2, 3, 3, 0, seed=3, patch_kinds=(F,))]
+            configs.box3d(4, 4, 3, 1, seed=1, patch_kinds=(F,)), configs.box3d(2, 3, 3, 0, seed=3, patch_kinds=(F,))]
 
 
 @pytest.mark.parametrize("k", range(4))
