@@ -193,7 +193,15 @@ void enqueue_gather(Launcher &Lc, Domain &dm, int di, int l, int flags, double *
     if ((flags & G_PREPARE) && ctx->opt.df_mode == 3) flags |= G_BETA;   // fixed-beta relaxation
     GArgs a{flags, ctx->opt.cfl_imp, ctx->opt.cfl_exp, Wexp, L.partial, ctx->opt.beta};
     Lc.pre(GMG_K_GATHER);
-    klaunch(Lc.ctx, k_gather<D>, dim3(nblk(L.n)), dim3(256), Lc.s, L, a);
+    const dim3 g(nblk(L.n)), b(256);
+    switch (flags) {   // the V-cycle's combinations as compile-time flag sets
+        case G_FLUX | G_NORM | G_EXPLICIT: klaunch(Lc.ctx, k_gather<D, G_FLUX | G_NORM | G_EXPLICIT>, g, b, Lc.s, L, a); break;
+        case G_FLUX | G_WRITE_RT | G_ALPHA: klaunch(Lc.ctx, k_gather<D, G_FLUX | G_WRITE_RT | G_ALPHA>, g, b, Lc.s, L, a); break;
+        case G_FLUX | G_SET_F | G_PREPARE: klaunch(Lc.ctx, k_gather<D, G_FLUX | G_SET_F | G_PREPARE>, g, b, Lc.s, L, a); break;
+        case G_FLUX | G_WRITE_RT | G_ADD_F: klaunch(Lc.ctx, k_gather<D, G_FLUX | G_WRITE_RT | G_ADD_F>, g, b, Lc.s, L, a); break;
+        case G_PREPARE: klaunch(Lc.ctx, k_gather<D, G_PREPARE>, g, b, Lc.s, L, a); break;
+        default: klaunch(Lc.ctx, k_gather<D, -1>, g, b, Lc.s, L, a); break;
+    }
     Lc.post(GMG_K_GATHER, dm.lbytes[l].gather);
     if (flags & G_NORM) {
         Lc.pre(GMG_K_NORM);

@@ -151,9 +151,12 @@ __global__ void __launch_bounds__(256, 4) k_face(DevLevel L, const double *__res
 // ---------------------------------------------------------------------------
 // Cell gather (a6, a7, a9, a10, a16): per cell over its face slots.
 // ---------------------------------------------------------------------------
-template <int D>
+// FL >= 0: the flag set as a compile-time constant (the V-cycle's fixed
+// combinations: dead paths and their registers drop out); FL = -1: a.flags
+template <int D, int FL>
 __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 {
+    const int flags = FL >= 0 ? FL : a.flags;
     pdl_launch_dependents();
     constexpr int NV = D + 2;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;   // gather position (ginfo.z: the cell)
@@ -168,8 +171,8 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     // the cell's one per-cell input of the epilogue (W for G_COPY_W, Rs for G_SET_F, F for G_ADD_F, the
     // explicit state for G_EXPLICIT) is loaded before the slot loop: its latency hides under the gathers,
     // and the epilogue's stores no longer wait on loads the compiler cannot hoist above them (aliasing)
-    const int pk = (a.flags & G_COPY_W) ? G_COPY_W : (a.flags & G_SET_F) ? G_SET_F
-                 : ((a.flags & G_WRITE_RT) && (a.flags & G_ADD_F)) ? G_ADD_F : (a.flags & G_EXPLICIT) ? G_EXPLICIT : 0;
+    const int pk = (flags & G_COPY_W) ? G_COPY_W : (flags & G_SET_F) ? G_SET_F
+                 : ((flags & G_WRITE_RT) && (flags & G_ADD_F)) ? G_ADD_F : (flags & G_EXPLICIT) ? G_EXPLICIT : 0;
     double pre[NV];
     if (t < L.n && pk) {
         const double *src = pk == G_COPY_W ? L.W : pk == G_SET_F ? L.Rs : pk == G_ADD_F ? L.F : a.Wexp;
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
             ld4nc(fr + 4, c1);                 // 3D: SF4, Sr, alpha^M, 0   2D: Sr, alpha^M, 0, 0
             const double srf = c1[FR<D>::SR - 4];
             sig += srf;
-            if (a.flags & G_FLUX) {
+            if (flags & G_FLUX) {
                 double c0[4];
                 ld4nc(fr, c0);
                 const double sg = sf > 0 ? 1.0 : -1.0;
@@ -197,10 +200,10 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
                 al *= c1[FR<D>::AM - 4];
             }
         }
-        if (a.flags & G_ALPHA) L.alpha[i] = al;
-        if (a.flags & G_SIGMA) L.sigma[i] = sig;
-        if (a.flags & G_PREPARE) {
-            const double ai = (a.flags & G_BETA) ? a.beta : ((a.flags & G_ALPHA) ? al : L.alpha[i]);
+        if (flags & G_ALPHA) L.alpha[i] = al;
+        if (flags & G_SIGMA) L.sigma[i] = sig;
+        if (flags & G_PREPARE) {
+            const double ai = (flags & G_BETA) ? a.beta : ((flags & G_ALPHA) ? al : L.alpha[i]);
             // D = alpha (V/Dt_imp + Sigma/2) + (1 - alpha) V/Dt_exp (O6, A2, A3); c = alpha / (2 D)
             const double Dg = ai * (sig / a.cfl_imp + 0.5 * sig) + (1.0 - ai) * (sig / a.cfl_exp);
             const double iD = 1.0 / Dg;
@@ -208,8 +211,8 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
             st2(L.dc + 2 * (size_t)i, dc);
         }
         const size_t o = (size_t)i * NV;
-        if (a.flags & G_COPY_W) st_state<D>(L.wlin, (size_t)L.n_loc, i, pre);
-        if (a.flags & G_SET_F) {
+        if (flags & G_COPY_W) st_state<D>(L.wlin, (size_t)L.n_loc, i, pre);
+        if (flags & G_SET_F) {
             if (pk == G_SET_F) {
                 double v[NV];
 #pragma unroll
@@ -220,8 +223,8 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
                 for (int q = 0; q < NV; ++q) L.F[o + q] = L.Rs[o + q] - R[q];
             }
         }
-        if (a.flags & G_WRITE_RT) {
-            if (a.flags & G_ADD_F) {
+        if (flags & G_WRITE_RT) {
+            if (flags & G_ADD_F) {
                 if (pk == G_ADD_F) {
                     double v[NV];
 #pragma unroll
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
                 st_rec<NV>(L.Rt, i, R);
             }
         }
-        if (a.flags & G_EXPLICIT) {
+        if (flags & G_EXPLICIT) {
             const double c = a.cfl_exp / sig;
             if (pk == G_EXPLICIT) {
                 double v[NV];
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
             }
         }
     }
-    if (a.flags & G_NORM) {
+    if (flags & G_NORM) {
         __shared__ double sh[8][NV];
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
