@@ -395,14 +395,22 @@ void launch_sweep_lpc(const gmg_ctx *ctx, const SweepArgs &a, cudaStream_t s, co
     if (FF && a.lo == 0 && a.n_own == a.n_loc) {   // first color, no ghosts: no W' gathers
         const int cap = ctx->sweep_grid_cap_ff1;
         if (cap > 0) nb = std::min(nb, cap);
-        launch_with_window(k_sweep<D, LPC, 2>, dim3(std::max(nb, 1)), dim3(128), s, a, win, win_bytes,
-                           ctx->opt.pdl != 0);
+        if (a.Wout)
+            launch_with_window(k_sweep<D, LPC, 2, 1>, dim3(std::max(nb, 1)), dim3(128), s, a, win, win_bytes,
+                               ctx->opt.pdl != 0);
+        else
+            launch_with_window(k_sweep<D, LPC, 2, 0>, dim3(std::max(nb, 1)), dim3(128), s, a, win, win_bytes,
+                               ctx->opt.pdl != 0);
         return;
     }
     const int cap = FF ? ctx->sweep_grid_cap_ff : ctx->sweep_grid_cap;
     if (cap > 0) nb = std::min(nb, cap);
-    launch_with_window(k_sweep<D, LPC, FF ? 1 : 0>, dim3(std::max(nb, 1)), dim3(128), s, a, win, win_bytes,
-                       ctx->opt.pdl != 0);
+    if (a.Wout)   // the last backward phase also writes W
+        launch_with_window(k_sweep<D, LPC, FF ? 1 : 0, 1>, dim3(std::max(nb, 1)), dim3(128), s, a, win, win_bytes,
+                           ctx->opt.pdl != 0);
+    else
+        launch_with_window(k_sweep<D, LPC, FF ? 1 : 0, 0>, dim3(std::max(nb, 1)), dim3(128), s, a, win, win_bytes,
+                           ctx->opt.pdl != 0);
 }
 
 template <int D, bool FF>
@@ -1447,13 +1455,13 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
         int nsm = 0, per_sm = 0, per_ff = 0, per_ff1 = 0;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->opt.device);
         if (ctx->opt.dim == 3) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, 0>, 128, 0);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff, k_sweep<3, 2, 1>, 128, 0);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff1, k_sweep<3, 2, 2>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<3, 2, 0, 0>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff, k_sweep<3, 2, 1, 0>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff1, k_sweep<3, 2, 2, 0>, 128, 0);
         } else {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, 0>, 128, 0);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff, k_sweep<2, 2, 1>, 128, 0);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff1, k_sweep<2, 2, 2>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<2, 2, 0, 0>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff, k_sweep<2, 2, 1, 0>, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_ff1, k_sweep<2, 2, 2, 0>, 128, 0);
         }
         ctx->sweep_grid_cap = nsm * std::max(per_sm, 1);
         ctx->sweep_grid_cap_ff = nsm * std::max(per_ff, 1);

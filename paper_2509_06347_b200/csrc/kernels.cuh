@@ -485,7 +485,7 @@ __device__ __forceinline__ void ld2x(const double *p, double *v)
 // FF: 0 = a plain phase, 1 = a first-forward phase, 2 = the first-forward
 // phase of the first color with no ghosts (no earlier-color neighbour: no W'
 // gathers, W' = W - Rt/D)
-template <int D, int LPC, int FF, bool CG, bool P2P>
+template <int D, int LPC, int FF, bool CG, bool P2P, int WO = -1>
 __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p, int gt0, int nthr, bool pdl)
 {
     constexpr int NV = D + 2;
@@ -575,7 +575,8 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
             }
             st_state<D>(a.wp, nl, i, wn);
             p2p_store<D, P2P>(p, i, wn);
-            if (a.Wout) st_rec<NV>(a.Wout, i, wn);
+            // WO: the W write of the last backward phase known at compile time (1 / 0), -1: a.Wout decides
+            if (WO == 1 || (WO < 0 && a.Wout)) st_rec<NV>(a.Wout, i, wn);
         }
     }
     if (pdl) pdl_wait();   // threads without a cell: nothing may run past the predecessor
@@ -584,12 +585,12 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
 // the sweep launch: 128-thread blocks, 9 per SM (FF, with its second set of
 // accumulators, and the first color's FF, without W' gathers: 7), grid = one
 // resident wave
-template <int D, int LPC, int FF>
+template <int D, int LPC, int FF, int WO>
 __global__ void __launch_bounds__(128, FF ? 7 : 9) k_sweep(SweepArgs a)
 {
     pdl_launch_dependents();                       // the next phase may start its static prologue now
-    sweep_cells<D, LPC, FF, false, false>(a, P2PArgs{}, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x,
-                                          true);
+    sweep_cells<D, LPC, FF, false, false, WO>(a, P2PArgs{}, blockIdx.x * blockDim.x + threadIdx.x,
+                                              gridDim.x * blockDim.x, true);
 }
 
 __device__ __forceinline__ int ld_acquire_sys(const int *p)
