@@ -340,6 +340,31 @@ def test_green_gauss_exact_for_linear_on_uniform_grid():
         assert np.allclose(poly[i, 0, 3:], 0.0)
 
 
+@pytest.mark.parametrize("gam0", [0.95, 0.5])
+def test_weno_combination_consistent_for_linear_data(gam0):
+    """C5: p = w0 (p2 - g1 p1) / g0 + w1 p1 reproduces a field that
+    BOTH candidates represent exactly, whatever the nonlinear weights: linear
+    averages with consistent slopes on a uniform quad grid (p2 exact for
+    quadratics, Green-Gauss exact for linear data at interior cells) come back
+    exactly at every interior p2 cell for any linear weight gamma_0."""
+    m = configs.quad_grid(6, 6)
+    M = cgks3.Mesh3(m)
+    n = m.n_cells
+    b = np.array([0.3, -0.2])
+    W = np.zeros((4, n))
+    W[0] = 1.0 + m.ctr.T @ b
+    W[3] = 3.0
+    G = np.zeros((4, 2, n))
+    G[0] = b[:, None]
+    Winf = W[:, 0].copy()
+    poly, fl, _ = cgks3.recon(M, W, G, np.ones(n), Winf, cgks3.Opt3(gam0=gam0))
+    interior = [i for i in range(n) if len(_nbrs(m, i)) == 4 and (fl[i] & 1)]
+    assert interior
+    for i in interior:
+        assert np.allclose(poly[i, 0, 1:3], b, rtol=1e-12, atol=1e-13)
+        assert np.allclose(poly[i, 0, 3:], 0.0, atol=1e-13)
+
+
 def test_weno_weights_favour_the_smooth_sub_stencil():
     """C5: averages of a linear field (p1 smooth) with wildly wrong neighbour
     slopes (p2 rough): the large-stencil weight collapses, the final

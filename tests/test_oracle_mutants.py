@@ -18,8 +18,8 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-C, PY = "gmg_oracle.c", "vcycle.py"
-P1, P2 = "test_oracle_pins", "test_oracle_pins_fas"
+C, PY, C3 = "gmg_oracle.c", "vcycle.py", "cgks3.c"
+P1, P2, P3 = "test_oracle_pins", "test_oracle_pins_fas", "test_oracle_cgks3"
 
 # (id, file, old, new, pin module, pin function, params)
 MUTANTS = [
@@ -79,6 +79,23 @@ MUTANTS = [
      "return (23u * (l + r)) % nf_interior;", P1, "test_face_hash_worked_examples", {}),
     ("color_start_2", C, "color[next_start] = 1;                               /* color(v0) = 1 */",
      "color[next_start] = 2;", P1, "test_coloring_valid_and_matches_brute_force", {"mk": 1}),
+    # NEXT-1 oracle (cgks3.c, readings C1-C14)
+    ("gks_moment_recurrence", C3, "M[k + 2] = U * M[k + 1] + (double)(k + 1) / (2.0 * lambda) * M[k];",
+     "M[k + 2] = U * M[k + 1] + (double)(k) / (2.0 * lambda) * M[k];", P3,
+     "test_gks_local_matches_bruteforce_quadrature", {"dim": 3, "seed": 0}),
+    ("gks_half_range_sign", C3, "gauss_moments(U, lam, l0, U * l0 - e, g->Mu[2]);",
+     "gauss_moments(U, lam, l0, U * l0 + e, g->Mu[2]);", P3, "test_gks_local_matches_bruteforce_quadrature",
+     {"dim": 2, "seed": 1}),
+    ("gks_time_derivative_sign", C3, "for (int q = 0; q < dim + 2; ++q) b[q] = -b[q];", "", P3,
+     "test_gks_local_matches_bruteforce_quadrature", {"dim": 3, "seed": 1}),
+    ("gks_internal_dof", C3, "return dim == 3 ? (5.0 - 3.0 * gamma) / (gamma - 1.0)",
+     "return dim == 3 ? (3.0 - gamma) / (gamma - 1.0)", P3, "test_gks_free_stream_is_euler_flux", {"dim": 3}),
+    ("p2_constraint_offset_dropped", C3, "Cm[r * nk + d + k] = (m2_at(M, j, A, B) + dl[A] * dl[B]) - m2_at(M, i, A, B);",
+     "Cm[r * nk + d + k] = m2_at(M, j, A, B) - m2_at(M, i, A, B);", P3, "test_p2_exact_for_quadratic_fields", {"k": 0}),
+    ("weno_combination_uncorrected", C3, "double cq = w0 / g0, cl = w1 - w0 * g1 / g0;", "double cq = w0 / g0, cl = w1;",
+     P3, "test_weno_combination_consistent_for_linear_data", {"gam0": 0.95}),
+    ("cgks3_residual_right_sign", C3, "R[(int64_t)q * n + r] -= S * Fs[q] / dtf;",
+     "R[(int64_t)q * n + r] += S * Fs[q] / dtf;", P3, "test_residual_discrete_conservation", {"k": 2}),
 ]
 _RUNNER = textwrap.dedent("""
     import sys
@@ -92,10 +109,14 @@ _RUNNER = textwrap.dedent("""
     mod = importlib.import_module("tests." + module)
     fn = getattr(mod, name)
     kw = dict(params)
-    if "steady" in fn.__code__.co_varnames[:fn.__code__.co_argcount]:
+    names = fn.__code__.co_varnames[:fn.__code__.co_argcount]
+    if "steady" in names:
         kw["steady"] = mod._steady_naca(oracle)
     try:
-        fn(oracle, **kw)
+        if names and names[0] in ("orc", "oracle"):
+            fn(oracle, **kw)
+        else:                # the NEXT-1 pins import oracle.cgks3 themselves (the mutant copy: first on sys.path)
+            fn(**kw)
     except AssertionError:
         sys.exit(3)          # the pin fails on the mutant: killed
     sys.exit(0)              # survived
