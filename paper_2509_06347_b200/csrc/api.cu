@@ -957,6 +957,8 @@ void carve(gmg_ctx *ctx, Bump &b)
             V.sr = b.take<double>(nf);
             V.dt = b.take<double>(nl);
             V.frec = b.take<double>((size_t)nf * 12);
+            V.nlane = (int)(H.glane.size() / 2);
+            V.glane = b.take<int2>(V.nlane);
             V.Gout = b.take<double>((size_t)n * nv * d);
             dm.ho.sendbuf = b.take<double>(D0.send_idx.size() * (size_t)nv * V.nc);
             dm.ho.recvbuf = b.take<double>(D0.recv_idx.size() * (size_t)nv * V.nc);
@@ -1489,6 +1491,7 @@ gmg_status gmg_set_workspace(gmg_ctx *ctx, void *dptr, size_t bytes)
             CK(cudaMemcpyAsync((void *)V.m2, H.m2l.data(), H.m2l.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
             CK(cudaMemcpyAsync((void *)V.gp, H.gpl.data(), H.gpl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
             CK(cudaMemcpyAsync((void *)V.gw, H.gwl.data(), H.gwl.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+            CK(cudaMemcpyAsync((void *)V.glane, H.glane.data(), H.glane.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
             CK(cudaMemcpyAsync((void *)V.hfoff, H.hfoff.data(), H.hfoff.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
             CK(cudaMemcpyAsync((void *)V.hface, H.hface.data(), H.hface.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
             CK(cudaMemcpyAsync((void *)V.hrec, H.hrec.data(), H.hrec.size() * 8, cudaMemcpyHostToDevice, ctx->stream));

@@ -96,6 +96,8 @@ struct HoDev {
     int *flags = nullptr;                // [n] bit 0 p2 used
     double *sr = nullptr;                // [nf] S r_f (first-order spectral radius, A5)
     double *dt = nullptr;                // [nl] Dt_i = CFL_exp V_i / Sigma_i (C8)
+    const int2 *glane = nullptr;         // [nlane] packed Gauss-point lanes of the flux kernel (HoLocal::glane)
+    int nlane = 0;
     double *frec = nullptr;              // [nf][12] S sum_k w F_k / Dt_f [nv] | sum_k w W_k(Dt_f) [nv] | prod alpha_fk
     double *Gout = nullptr;              // [n][nv][D] slopes of a non-updating evaluation
 };
@@ -179,6 +181,7 @@ struct HoHost {
 struct HoLocal {
     std::vector<double> ctr, m2l, gpl, gwl, P, hrec;   // ctr / m2l over owned + ghost cells
     std::vector<int> hfoff, hface, poff;               // owned cells
+    std::vector<int32_t> glane;          // [nlane][2] flux lanes: (f G + k | -1, Gauss points of f on its first lane, else 0)
     int64_t n_p2 = 0;                    // cells with a p2 operator
     int64_t n_gauss_pts = 0;             // Gauss points of the local faces (flux work units)
     double bytes_sr = 0, bytes_recon = 0, bytes_flux = 0, bytes_gather = 0;   // algorithmic bytes per launch

@@ -625,16 +625,18 @@ __device__ __forceinline__ void peval(const double *po, const double *y, double 
     }
 }
 
-// one face per group of G lanes, one Gauss point per lane (padding lanes of
-// triangles idle); the lanes' weighted flux / state / DF combine by shuffles
+// one Gauss point per lane (H.glane: packed, no idle padding lanes for
+// triangles; a face's points on consecutive lanes of one warp); the face's
+// first lane adds the others' weighted flux / state / DF by shuffles
 template <int D>
 __global__ void __launch_bounds__(128) k_ho_flux(DevLevel L, HoDev H, Phys ph, BCs bc, double c1, double c2)
 {
     constexpr int NV = D + 2, NQ = D * (D + 1) / 2, NC = 1 + D + NQ;
     constexpr int G = D == 3 ? 4 : 2;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int f = t / G, k = t % G;
-    const bool live = f < L.nf;
+    const int2 gl = t < H.nlane ? __ldg(H.glane + t) : make_int2(-1, 0);
+    const bool live = gl.x >= 0;
+    const int f = live ? gl.x / G : 0, k = live ? gl.x % G : 0;
     const int fc = live ? f : L.nf - 1;
     const double w = live ? __ldg(H.gw + (size_t)fc * G + k) : 0.0;
     double Fs[NV], Ws[NV], ap = 1.0;
@@ -730,17 +732,21 @@ __global__ void __launch_bounds__(128) k_ho_flux(DevLevel L, HoDev H, Phys ph, B
             Ws[1 + e] = w * b;
         }
     }
-    // combine the G lanes of the face (lane order fixed: deterministic)
+    // the face's first lane adds its other points in lane order (deterministic); only first lanes
+    // change their values, and they read only their own face's lanes (j < its point count)
 #pragma unroll
-    for (int o = 1; o < G; o <<= 1) {
+    for (int j = 1; j < G; ++j) {
+        const bool take = j < gl.y;
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-            Fs[q] += __shfl_xor_sync(0xffffffffu, Fs[q], o);
-            Ws[q] += __shfl_xor_sync(0xffffffffu, Ws[q], o);
+            const double xf = __shfl_down_sync(0xffffffffu, Fs[q], j);
+            const double xw = __shfl_down_sync(0xffffffffu, Ws[q], j);
+            if (take) { Fs[q] += xf; Ws[q] += xw; }
         }
-        ap *= __shfl_xor_sync(0xffffffffu, ap, o);
+        const double xa = __shfl_down_sync(0xffffffffu, ap, j);
+        if (take) ap *= xa;
     }
-    if (live && k == 0) {
+    if (gl.y > 0) {
         double *o = H.frec + (size_t)f * kHoRec;
 #pragma unroll
         for (int q = 0; q < NV; ++q) { o[q] = S * Fs[q] / dtf; o[NV + q] = Ws[q]; }
@@ -840,7 +846,7 @@ void ho_launch_t(int which, const DevLevel &L, const HoDev &H, const Phys &ph, c
     switch (which) {
     case 0: k_ho_sr<D><<<hblk(L.nf, 256), 256, 0, s>>>(L, H, ph, bc); break;
     case 1: k_ho_recon<D><<<hblk((int64_t)L.n * (D + 2), 256), 256, 0, s>>>(L, H, ph, bc, o.cfl_exp, o.ho_gam0, o.ho_eps); break;
-    case 2: k_ho_flux<D><<<hblk((int64_t)L.nf * (D == 3 ? 4 : 2), 128), 128, 0, s>>>(L, H, ph, bc, o.ho_c1, o.ho_c2); break;
+    case 2: k_ho_flux<D><<<hblk((int64_t)H.nlane, 128), 128, 0, s>>>(L, H, ph, bc, o.ho_c1, o.ho_c2); break;
     default: k_ho_gather<D><<<hblk(L.n, 256), 256, 0, s>>>(L, H, mode, o.cfl_exp, Rout, aout, L.partial); break;
     }
 }

@@ -80,6 +80,24 @@ static gmg_status ho_prepare_domain(gmg_ctx *ctx, const HoHost &HH, Domain &dm)
             for (int e = 0; e < d; ++e) H.gpl[(f * Gs + k) * d + e] = HH.gp[((size_t)e * Gs + k) * NF + g];
         }
     }
+    // flux lanes: one lane per Gauss point (no idle padding lanes of triangles), a face's points on
+    // consecutive lanes of one warp (its first lane reduces them), faces in local order
+    H.glane.clear();
+    for (int64_t f = 0; f < nf; ++f) {
+        int c = 0;
+        for (int k = 0; k < Gs; ++k) c += H.gwl[f * Gs + k] != 0.0;
+        if (c == 0) continue;
+        const int64_t pos = (int64_t)H.glane.size() / 2;
+        if (pos % 32 + c > 32)
+            for (int64_t p = pos; p % 32 != 0; ++p) { H.glane.push_back(-1); H.glane.push_back(0); }
+        bool first = true;
+        for (int k = 0; k < Gs; ++k) {
+            if (H.gwl[f * Gs + k] == 0.0) continue;
+            H.glane.push_back((int32_t)(f * Gs + k));
+            H.glane.push_back(first ? c : 0);
+            first = false;
+        }
+    }
     // owned cell -> faces, ascending natural face id (the oracle's order)
     H.hfoff.assign(n + 1, 0);
     for (int64_t f = 0; f < nf; ++f) {
