@@ -40,8 +40,11 @@ __device__ __forceinline__ void rec_mom(double U, double inv2l, double *M)
     for (int k = 2; k < N; ++k) M[k] = U * M[k - 1] + (double)(k - 1) * inv2l * M[k - 2];
 }
 
+// R = 1, 2: the half range u1 > 0 / u1 < 0; sgn (+1 / -1) selects it at run time
+// when one copy of the code serves both sides (R = 1 with sgn = -1 is the R = 2 range)
 template <int D, int R>
-__device__ __forceinline__ void maxw(const double *w, double gm1, double K, Maxw<D, R> &g)
+__device__ __forceinline__ void maxw(const double *w, double gm1, double K, Maxw<D, R> &g,
+                                     double sgn = R == 2 ? -1.0 : 1.0)
 {
     g.rho = w[0];
     const double ir = 1.0 / w[0];
@@ -56,8 +59,8 @@ __device__ __forceinline__ void maxw(const double *w, double gm1, double K, Maxw
         const double lam = 0.5 * w[0] / p;
         const double sl = sqrt(lam);
         const double e = exp(-lam * U[0] * U[0]) * (0.28209479177387814 / sl);   // e^{-l U^2} / (2 sqrt(pi l))
-        if constexpr (R == 1) { g.Mh[0] = 0.5 * erfc(-sl * U[0]); g.Mh[1] = U[0] * g.Mh[0] + e; }
-        else { g.Mh[0] = 0.5 * erfc(sl * U[0]); g.Mh[1] = U[0] * g.Mh[0] - e; }
+        g.Mh[0] = 0.5 * erfc(-sgn * sl * U[0]);
+        g.Mh[1] = U[0] * g.Mh[0] + sgn * e;
         rec_mom<7>(U[0], inv2l, g.Mh);
     }
     g.Mv[0] = 1.0; g.Mv[1] = U[1];
@@ -231,11 +234,11 @@ __device__ __forceinline__ TimeC time_coeffs(double dt, double tau)
 // dWc: shared memory, component k of this thread at dWc[k * blockDim.x] (frees registers)
 template <int D, int R>
 __device__ __forceinline__ void side_pass(const double *w, const double *dw, const TimeC &T, double gm1, double K,
-                                          double *Wc, double *dWc, double *F, double *Wt)
+                                          double *Wc, double *dWc, double *F, double *Wt, double sgn = R == 2 ? -1.0 : 1.0)
 {
     constexpr int NV = D + 2;
     Maxw<D, R> g;
-    maxw<D, R>(w, gm1, K, g);
+    maxw<D, R>(w, gm1, K, g, sgn);
     double a[D][NV], A[NV], M[NV][NV];
     slopes<D, R>(g, dw, a, A);
     const double rho = g.rho, fw = -rho * T.ex * (T.tau + T.dt);
@@ -690,27 +693,24 @@ __global__ void __launch_bounds__(128) k_ho_flux(DevLevel L, HoDev H, Phys ph, B
         for (int q = 0; q < NV; ++q) { Wc[q] = 0.0; Fl[q] = 0.0; Wl[q] = 0.0; }
 #pragma unroll
         for (int q = 0; q < D * NV; ++q) dWc[q * blockDim.x] = 0.0;
-        {
+        // both sides through ONE copy of the side pass (a loop, not unrolled: half the code body of
+        // the kernel, fewer instruction-fetch stalls); the half range by its sign at run time
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
             double lw[NV], lg[D * NV];
-            if (badl) {
-#pragma unroll
-                for (int q = 0; q < D * NV; ++q) gtmp[q] = 0.0;
+            const bool useg = side == 0 ? !badl : ((r >= 0 && !badr) || (r < 0 && kind == GMG_EXTRAP && !badl));
+            if (useg) {
+                const bool lp = side == 0 || r < 0;
+                peval<D, true>(lp ? pl : pr, lp ? yl : yr, nullptr, gtmp);
             } else {
-                peval<D, true>(pl, yl, nullptr, gtmp);
-            }
-            to_frame<D>(E, wl, gtmp, lw, lg);
-            side_pass<D, 1>(lw, lg, T, ph.gm1, ph.K, Wc, dWc, Fl, Wl);
-        }
-        {
-            double lw[NV], lg[D * NV];
-            if (r >= 0 && !badr) peval<D, true>(pr, yr, nullptr, gtmp);
-            else if (r < 0 && kind == GMG_EXTRAP && !badl) peval<D, true>(pl, yl, nullptr, gtmp);
-            else {
 #pragma unroll
                 for (int q = 0; q < D * NV; ++q) gtmp[q] = 0.0;
             }
-            to_frame<D>(E, wr, gtmp, lw, lg);
-            side_pass<D, 2>(lw, lg, T, ph.gm1, ph.K, Wc, dWc, Fl, Wl);
+            double ws[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) ws[q] = side == 0 ? wl[q] : wr[q];
+            to_frame<D>(E, ws, gtmp, lw, lg);
+            side_pass<D, 1>(lw, lg, T, ph.gm1, ph.K, Wc, dWc, Fl, Wl, side == 0 ? 1.0 : -1.0);
         }
         {
             double dwc[D * NV];
