@@ -47,7 +47,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     if verbose_ptxas:
         flags += ["-Xptxas", "-v"]
     flags += os.environ.get("GMG_NVCC_DEFS", "").split()   # development builds of kernel variants (-D...)
-    gxx += os.environ.get("GMG_NVCC_DEFS", "").split()
+    gxx += [x for x in os.environ.get("GMG_NVCC_DEFS", "").split() if x.startswith("-D")]
     objs, jobs = [], []
     nv = [NVCC] + flags + ["-c"]
     for src, cmd in (("setup.cpp", gxx), ("ho_setup.cpp", gxx), ("api.cu", nv),

@@ -44,7 +44,7 @@ __device__ __forceinline__ void rec_mom(double U, double inv2l, double *M)
 // when one copy of the code serves both sides (R = 1 with sgn = -1 is the R = 2 range)
 template <int D, int R>
 __device__ __forceinline__ void maxw(const double *w, double gm1, double K, Maxw<D, R> &g,
-                                     double sgn = R == 2 ? -1.0 : 1.0)
+                                     double sgn = R == 2 ? -1.0 : 1.0, bool half = true)
 {
     g.rho = w[0];
     const double ir = 1.0 / w[0];
@@ -55,7 +55,7 @@ __device__ __forceinline__ void maxw(const double *w, double gm1, double K, Maxw
     const double inv2l = p * ir;                       // 1/(2 lambda), lambda = rho / (2p)
     g.Mu[0] = 1.0; g.Mu[1] = U[0];
     rec_mom<7>(U[0], inv2l, g.Mu);
-    if constexpr (R != 0) {
+    if (R != 0 && half) {
         const double lam = 0.5 * w[0] / p;
         const double sl = sqrt(lam);
         const double e = exp(-lam * U[0] * U[0]) * (0.28209479177387814 / sl);   // e^{-l U^2} / (2 sqrt(pi l))
@@ -226,94 +226,73 @@ __device__ __forceinline__ TimeC time_coeffs(double dt, double tau)
     return t;
 }
 
-// one side of the interface (R = 1: left state on u1 > 0, R = 2: right on
-// u1 < 0), frame coordinates: its share of W^c (Eq.(compatibility2)), of the
-// equilibrium slopes (reading C10e), and its kinetic terms of Eq.(dis1):
-// F += rho int_0^dt e^{-t/tau} <u1 psi [1 - tau (a.u + A) - t a.u]>_half dt,
-// Wt += rho e^{-dt/tau} <psi [1 - tau (a.u + A) - dt a.u]>_half
-// dWc: shared memory, component k of this thread at dWc[k * blockDim.x] (frees registers)
-template <int D, int R>
-__device__ __forceinline__ void side_pass(const double *w, const double *dw, const TimeC &T, double gm1, double K,
-                                          double *Wc, double *dWc, double *F, double *Wt, double sgn = R == 2 ? -1.0 : 1.0)
-{
-    constexpr int NV = D + 2;
-    Maxw<D, R> g;
-    maxw<D, R>(w, gm1, K, g, sgn);
-    double a[D][NV], A[NV], M[NV][NV];
-    slopes<D, R>(g, dw, a, A);
-    const double rho = g.rho, fw = -rho * T.ex * (T.tau + T.dt);
-    // weight 1 (half range): <psi>, dW^c_e, -tau <A psi>
-    tmat<D, R, true, 0, 0, 0>(g, M);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) { Wc[q] += rho * M[q][0]; Wt[q] += (rho * T.ex) * M[q][0]; }
-#pragma unroll
-    for (int e = 0; e < D; ++e) {
-        double u[NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) u[q] = 0.0;
-        tmv<D>(M, a[e], rho, u);
-#pragma unroll
-        for (int q = 0; q < NV; ++q) dWc[(e * NV + q) * blockDim.x] += u[q];
-    }
-    tmv<D>(M, A, -rho * T.ex * T.tau, Wt);
-    // weight u1: <u1 psi> (flux), a_0 (state), A (flux)
-    tmat<D, R, true, 1, 0, 0>(g, M);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) F[q] += (rho * T.q4) * M[q][0];
-    tmv<D>(M, a[0], fw, Wt);
-    tmv<D>(M, A, -rho * T.tau * T.q4, F);
-    // weights u2, u3: a_1, a_2 (state)
-    tmat<D, R, true, 0, 1, 0>(g, M);
-    tmv<D>(M, a[1], fw, Wt);
-    if constexpr (D == 3) {
-        tmat<D, R, true, 0, 0, 1>(g, M);
-        tmv<D>(M, a[2], fw, Wt);
-    }
-    // weights u1 u_e: a_e (flux)
-    const double ff = -rho * (T.tau * T.q4 + T.q5);
-    tmat<D, R, true, 2, 0, 0>(g, M);
-    tmv<D>(M, a[0], ff, F);
-    tmat<D, R, true, 1, 1, 0>(g, M);
-    tmv<D>(M, a[1], ff, F);
-    if constexpr (D == 3) {
-        tmat<D, R, true, 1, 0, 1>(g, M);
-        tmv<D>(M, a[2], ff, F);
-    }
-}
-
-// equilibrium part (Eq.(dis2)): C1 g^c + C2 a^c.u g^c + C3 A^c g^c
+// The three kinetic passes of a Gauss point through ONE code copy (round 2:
+// a smaller kernel body, fewer instruction-fetch stalls), frame coordinates.
+// mode 0 / 1 -- one side of the interface (left state on u1 > 0, right on
+// u1 < 0; the half range by its sign): its share of W^c (Eq.(compatibility2)),
+// of the equilibrium slopes (reading C10e; dWc in shared memory, component k
+// of this thread at dWc[k * blockDim.x]) and its kinetic terms of Eq.(dis1):
+//   F  += rho int_0^dt e^{-t/tau} <u1 psi [1 - tau (a.u + A) - t a.u]>_half dt,
+//   Wt += rho e^{-dt/tau} <psi [1 - tau (a.u + A) - dt a.u]>_half;
+// mode 2 -- the equilibrium part of Eq.(dis2), C1 g^c + C2 a^c.u g^c + C3 A^c g^c
+// (full range): the same contractions with the coefficients below.
 template <int D>
-__device__ __forceinline__ void equilibrium_pass(const double *Wc, const double *dWc, const TimeC &T, double gm1,
-                                                 double K, double *F, double *Wt)
+__device__ __forceinline__ void kin_pass(const double *w, const double *dw, const TimeC &T, double gm1, double K,
+                                         int mode, double *Wc, double *dWc, double *F, double *Wt)
 {
     constexpr int NV = D + 2;
-    Maxw<D, 0> g;
-    maxw<D, 0>(Wc, gm1, K, g);
+    const bool side = mode < 2;
+    Maxw<D, 1> g;
+    maxw<D, 1>(w, gm1, K, g, mode == 0 ? 1.0 : -1.0, side);
     double a[D][NV], A[NV], M[NV][NV];
-    slopes<D, 0>(g, dWc, a, A);
-    const double rho = g.rho;
-    tmat<D, 0, false, 0, 0, 0>(g, M);
+    slopes<D, 1>(g, dw, a, A);
+    if (!side) {   // the equilibrium's weights are full-range moments
 #pragma unroll
-    for (int q = 0; q < NV; ++q) Wt[q] += (rho * T.c1) * M[q][0];
-    tmv<D>(M, A, rho * T.c3, Wt);
-    tmat<D, 0, false, 1, 0, 0>(g, M);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) F[q] += (rho * T.q1) * M[q][0];
-    tmv<D>(M, A, rho * T.q3, F);
-    tmv<D>(M, a[0], rho * T.c2, Wt);
-    tmat<D, 0, false, 0, 1, 0>(g, M);
-    tmv<D>(M, a[1], rho * T.c2, Wt);
-    if constexpr (D == 3) {
-        tmat<D, 0, false, 0, 0, 1>(g, M);
-        tmv<D>(M, a[2], rho * T.c2, Wt);
+        for (int i = 0; i < 7; ++i) g.Mh[i] = g.Mu[i];
     }
-    tmat<D, 0, false, 2, 0, 0>(g, M);
-    tmv<D>(M, a[0], rho * T.q2, F);
-    tmat<D, 0, false, 1, 1, 0>(g, M);
-    tmv<D>(M, a[1], rho * T.q2, F);
+    const double rho = g.rho;
+    const double cW0 = side ? rho * T.ex : rho * T.c1;
+    const double cWA = side ? -rho * T.ex * T.tau : rho * T.c3;
+    const double cF0 = side ? rho * T.q4 : rho * T.q1;
+    const double cWa = side ? -rho * T.ex * (T.tau + T.dt) : rho * T.c2;
+    const double cFA = side ? -rho * T.tau * T.q4 : rho * T.q3;
+    const double cFa = side ? -rho * (T.tau * T.q4 + T.q5) : rho * T.q2;
+    tmat<D, 1, true, 0, 0, 0>(g, M);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        if (side) Wc[q] += rho * M[q][0];
+        Wt[q] += cW0 * M[q][0];
+    }
+    if (side) {
+#pragma unroll
+        for (int e = 0; e < D; ++e) {
+            double u[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) u[q] = 0.0;
+            tmv<D>(M, a[e], rho, u);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) dWc[(e * NV + q) * blockDim.x] += u[q];
+        }
+    }
+    tmv<D>(M, A, cWA, Wt);
+    tmat<D, 1, true, 1, 0, 0>(g, M);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) F[q] += cF0 * M[q][0];
+    tmv<D>(M, a[0], cWa, Wt);
+    tmv<D>(M, A, cFA, F);
+    tmat<D, 1, true, 0, 1, 0>(g, M);
+    tmv<D>(M, a[1], cWa, Wt);
     if constexpr (D == 3) {
-        tmat<D, 0, false, 1, 0, 1>(g, M);
-        tmv<D>(M, a[2], rho * T.q2, F);
+        tmat<D, 1, true, 0, 0, 1>(g, M);
+        tmv<D>(M, a[2], cWa, Wt);
+    }
+    tmat<D, 1, true, 2, 0, 0>(g, M);
+    tmv<D>(M, a[0], cFa, F);
+    tmat<D, 1, true, 1, 1, 0>(g, M);
+    tmv<D>(M, a[1], cFa, F);
+    if constexpr (D == 3) {
+        tmat<D, 1, true, 1, 0, 1>(g, M);
+        tmv<D>(M, a[2], cFa, F);
     }
 }
 
@@ -695,28 +674,30 @@ __global__ void __launch_bounds__(128) k_ho_flux(DevLevel L, HoDev H, Phys ph, B
         for (int q = 0; q < D * NV; ++q) dWc[q * blockDim.x] = 0.0;
         // both sides through ONE copy of the side pass (a loop, not unrolled: half the code body of
         // the kernel, fewer instruction-fetch stalls); the half range by its sign at run time
+        // all three kinetic passes through one code copy (pass 2: the equilibrium on the summed W^c, slopes)
 #pragma unroll 1
-        for (int side = 0; side < 2; ++side) {
+        for (int pass = 0; pass < 3; ++pass) {
             double lw[NV], lg[D * NV];
-            const bool useg = side == 0 ? !badl : ((r >= 0 && !badr) || (r < 0 && kind == GMG_EXTRAP && !badl));
-            if (useg) {
-                const bool lp = side == 0 || r < 0;
-                peval<D, true>(lp ? pl : pr, lp ? yl : yr, nullptr, gtmp);
+            if (pass < 2) {
+                const bool useg = pass == 0 ? !badl : ((r >= 0 && !badr) || (r < 0 && kind == GMG_EXTRAP && !badl));
+                if (useg) {
+                    const bool lp = pass == 0 || r < 0;
+                    peval<D, true>(lp ? pl : pr, lp ? yl : yr, nullptr, gtmp);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < D * NV; ++q) gtmp[q] = 0.0;
+                }
+                double ws[NV];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) ws[q] = pass == 0 ? wl[q] : wr[q];
+                to_frame<D>(E, ws, gtmp, lw, lg);
             } else {
 #pragma unroll
-                for (int q = 0; q < D * NV; ++q) gtmp[q] = 0.0;
+                for (int q = 0; q < NV; ++q) lw[q] = Wc[q];
+#pragma unroll
+                for (int q = 0; q < D * NV; ++q) lg[q] = dWc[q * blockDim.x];
             }
-            double ws[NV];
-#pragma unroll
-            for (int q = 0; q < NV; ++q) ws[q] = side == 0 ? wl[q] : wr[q];
-            to_frame<D>(E, ws, gtmp, lw, lg);
-            side_pass<D, 1>(lw, lg, T, ph.gm1, ph.K, Wc, dWc, Fl, Wl, side == 0 ? 1.0 : -1.0);
-        }
-        {
-            double dwc[D * NV];
-#pragma unroll
-            for (int q = 0; q < D * NV; ++q) dwc[q] = dWc[q * blockDim.x];
-            equilibrium_pass<D>(Wc, dwc, T, ph.gm1, ph.K, Fl, Wl);
+            kin_pass<D>(lw, lg, T, ph.gm1, ph.K, pass, Wc, dWc, Fl, Wl);
         }
         // back to the global frame, times the Gauss weight
         Fs[0] = w * Fl[0];
