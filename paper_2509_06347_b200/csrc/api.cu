@@ -444,6 +444,7 @@ SweepArgs sweep_args(const gmg_ctx *ctx, DevLevel &L, const DomLevel &H, int c, 
     a.rhs = rhs;
     a.dc = L.dc;
     a.Wout = Wout;
+    a.rev = 0;
     return a;
 }
 
@@ -451,7 +452,8 @@ SweepArgs sweep_args(const gmg_ctx *ctx, DevLevel &L, const DomLevel &H, int c, 
 // part: 0 = whole block, 1 = its boundary cells (ghost neighbours), 2 = its interior cells
 // ff: a phase of the first forward half-sweep of a smoothing step (k_sweep<.., FF>)
 template <int D>
-void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout, int part, bool ff)
+void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *rhs, double *Wout, int part, bool ff,
+                         bool rev = false)
 {
     gmg_ctx *ctx = Lc.ctx;
     DevLevel &L = dm.dv[l];
@@ -465,7 +467,9 @@ void enqueue_sweep_color(Launcher &Lc, Domain &dm, int l, int c, const double *r
         else b0 = mid;
     }
     if (b1 <= b0) return;
-    const SweepArgs a = sweep_args(ctx, L, H, c, b0, b1, rhs, Wout);
+    SweepArgs a = sweep_args(ctx, L, H, c, b0, b1, rhs, Wout);
+    a.rev = rev ? 1 : 0;   // backward half-sweeps from the block's end: the cells swept last in the
+                           // previous visit of this color come first, while their records are still in L2
     const void *win = ctx->l2_window ? (const void *)L.wp : nullptr;
     const size_t wb = ctx->l2_window ? std::min<size_t>(ctx->l2_window, (size_t)L.n_loc * (D + 2) * 8) : 0;
     const int lpc = part ? ctx->lpc : sweep_lpc(ctx, b1 - b0);
@@ -520,7 +524,7 @@ void enqueue_p2p_phase(Launcher &Lc, int l, int c, bool last, bool ff, std::func
 // changed in between, and never its own state -- so it would recompute
 // identical values (its W write, if any, moves to the kept phase).  Exact,
 // not an approximation: the oracle runs every phase.
-struct Phase { int c; bool last; bool ff; };
+struct Phase { int c; bool last; bool ff; bool rev; };
 std::vector<Phase> phase_list(const gmg_ctx *ctx, int l, int n_sweeps)
 {
     const int nc = ctx->lv[l].ncolor;
@@ -528,7 +532,8 @@ std::vector<Phase> phase_list(const gmg_ctx *ctx, int l, int n_sweeps)
     for (int s = 0; s < n_sweeps; ++s)
         for (int half = 0; half < 2; ++half)
             for (int cc = 0; cc < nc; ++cc) {
-                const Phase ph{half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1, s == 0 && half == 0};
+                const Phase ph{half == 0 ? cc : nc - 1 - cc, (s == n_sweeps - 1) && half == 1, s == 0 && half == 0,
+                               half == 1};
                 if (ctx->opt.skip_repeat && !seq.empty() && seq.back().c == ph.c) seq.back().last |= ph.last;
                 else seq.push_back(ph);
             }
@@ -573,7 +578,8 @@ void enqueue_sweeps(Launcher &Lc, int l, int n_sweeps, std::function<const doubl
             cudaStreamWaitEvent(Lc.s, ctx->ev_join, 0);
         } else {
             for (Domain &dm : ctx->dom)
-                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), ph.last ? wout(dm.dv[l]) : nullptr, 0, ph.ff);
+                enqueue_sweep_color<D>(Lc, dm, l, c, rhs(dm.dv[l]), ph.last ? wout(dm.dv[l]) : nullptr, 0, ph.ff,
+                                       ph.rev);
             enqueue_exchange<D>(Lc, l, EX_WP, c);
         }
     }

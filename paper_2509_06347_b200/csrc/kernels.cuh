@@ -432,6 +432,7 @@ struct SweepArgs {
     const double *rhs;         // [n][nv] right-hand side Rt (FF)
     const double *dc;          // [n][2] (1/D, c)          (FF)
     double *Wout;              // [n][nv] or null: W = W' (last backward half-sweep)
+    int rev;                   // 1: visit the cells from the end of the block (order only)
 };
 
 // Fused halo (gmg_options.p2p): the sweep that computes a boundary cell's W'
@@ -494,9 +495,10 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
     const int rounds = (total + nthr - 1) / nthr;
     for (int r = 0; r < rounds; ++r) {
         const int g = gt0 + r * nthr;
-        const int i = a.cbeg + g / LPC;
         const int sub = g % LPC;
-        const bool valid = i < a.cend;
+        const bool valid = g / LPC < a.cend - a.cbeg;
+        // rev: the block from its end (backward half-sweeps; cells of one color are independent)
+        const int i = a.rev ? a.cend - 1 - g / LPC : a.cbeg + g / LPC;
         double acc[NV], accP[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) { acc[q] = 0.0; accP[q] = 0.0; }
