@@ -480,7 +480,7 @@ __device__ __forceinline__ void ld2x(const double *p, double *v)
 
 // the cells [cbeg, cend) x LPC lanes, grid-stride from thread gt0 with nthr
 // threads (a launch sized to exactly one resident wave has no partial last
-// wave); PDL: the slot range and first neighbour index (static during a
+// wave), ascending or (a.rev, backward half-sweeps) descending; PDL: the slot range and first neighbour index (static during a
 // smoothing step) are loaded before griddepcontrol.wait, so they overlap the
 // previous phase's tail, and the records after it
 // FF: 0 = a plain phase, 1 = a first-forward phase, 2 = the first-forward
