@@ -187,12 +187,13 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
             const int f = (sf > 0 ? sf : -sf) - 1;
             const double *fr = L.Frec + (size_t)f * kFaceRec;
             double c1[4];
-            ld4nc(fr + 4, c1);                 // 3D: SF4, Sr, alpha^M, 0   2D: Sr, alpha^M, 0, 0
+            ld4na(fr + 4, c1);   // 3D: SF4, Sr, alpha^M, 0   2D: Sr, alpha^M, 0, 0 (no L1 allocation: the other
+                                 // cell of the face reads the record much later, from L2)
             const double srf = c1[FR<D>::SR - 4];
             sig += srf;
             if (flags & G_FLUX) {
                 double c0[4];
-                ld4nc(fr, c0);
+                ld4na(fr, c0);
                 const double sg = sf > 0 ? 1.0 : -1.0;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) R[q] += sg * c0[q];
