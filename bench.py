@@ -186,7 +186,11 @@ def next1_block(m, W, Winf, args, dev):
                          "peak": peak, "unit": "TFLOP/s (FP64)", "frac": ach / peak if ach else None,
                          "avg_launch_ms": flux_ms, "flops_per_gauss_point": flops_gp,
                          "peak_source": "measured: torch float64 matmul 8192^3 (cuBLAS DGEMM), best of 3",
-                         "flops_def": "ncu FP64 thread instructions of one launch (2 dfma + dmul + dadd) / Gauss points"}}
+                         "flops_def": "ncu FP64 thread instructions of one launch (2 dfma + dmul + dadd) / Gauss points, "
+                                      "round-1 kernel (profiles/r01/ho_ncu.json, 6 870 per Gauss point); the "
+                                      "round-2 kernel executes 7 413 (profiles/r02/ho_ncu_executed_v33.json) for "
+                                      "the same operator -- the lower count is used, so redundant instructions "
+                                      "do not raise the figure"}}
 
 
 def sweep_updates_per_cycle(sizes, n_sweeps, fine_smoother):

@@ -1,5 +1,6 @@
 """Summarise an ncu --csv metrics capture of the NEXT-1 kernels (k_ho_*) into
-profiles/r01/ho_ncu.json: per kernel time, DRAM bytes, FP64 thread
+profiles/r02/ho_ncu.json (round 1: profiles/r01/; the round-2 capture is kept as
+profiles/r02/ho_ncu_executed_v33.json): per kernel time, DRAM bytes, FP64 thread
 instructions and flops (2 dfma + dmul + dadd); for k_ho_flux the FP64 flops
 per Gauss point that bench.py's next1 roofline uses.
 
@@ -42,8 +43,8 @@ def main(path, gauss_points):
                                 "registers": m.get(METRICS[8])}
         if "k_ho_flux" in name:
             out["flux_fp64_flops_per_gauss_point"] = fl / gauss_points
-    os.makedirs("profiles/r01", exist_ok=True)
-    json.dump(out, open("profiles/r01/ho_ncu.json", "w"), indent=1)
+    os.makedirs("profiles/r02", exist_ok=True)
+    json.dump(out, open("profiles/r02/ho_ncu.json", "w"), indent=1)
     print(json.dumps(out))
 
 
