@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(256, 4) k_ho_recon(DevLevel L, HoDev H, Phys p
     const double *P = H.P + p0;
     for (int s = f0; s < f1; ++s) {
         double rc[4];
-        ld4nc(H.hrec + (size_t)s * 4, rc);
+        ld4na(H.hrec + (size_t)s * 4, rc);   // per-slot records, read once per launch: no L1 allocation
         const int2 jf = *reinterpret_cast<const int2 *>(&rc[3]);
         const int j = jf.x, f = jf.y;
         sig += __ldg(H.sr + f);
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(256, 4) k_ho_recon(DevLevel L, HoDev H, Phys p
                 constexpr int PST = ((D + 1) * NK + 3) & ~3;
                 double pb[PST];
 #pragma unroll
-                for (int k = 0; k < PST; k += 4) ld4nc(P + k, pb + k);
+                for (int k = 0; k < PST; k += 4) ld4na(P + k, pb + k);   // streamed once: no L1 allocation
 #pragma unroll
                 for (int k = 0; k < NK; ++k) {
                     double v = pb[k] * dq;
@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(256) k_ho_gather(DevLevel L, HoDev H, int mode
         const int f0 = __ldg(H.hfoff + i), f1 = __ldg(H.hfoff + i + 1);
         for (int s = f0; s < f1; ++s) {
             double rc[4];
-            ld4nc(H.hrec + (size_t)s * 4, rc);                       // A outward | neighbour, face
+            ld4na(H.hrec + (size_t)s * 4, rc);                       // A outward | neighbour, face
             const int f = reinterpret_cast<const int2 *>(&rc[3])->y;
             const int sf = __ldg(H.hface + s);
             const double sg = sf > 0 ? 1.0 : -1.0;
