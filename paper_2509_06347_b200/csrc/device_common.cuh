@@ -98,11 +98,6 @@ __device__ __forceinline__ void ld2na(const double *p, double *v)
 {
     asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
 }
-__device__ __forceinline__ void ld4cs(const double *p, double *v)
-{
-    asm volatile("ld.global.cs.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
-}
 __device__ __forceinline__ void ld4cg(const double *p, double *v)
 {
     asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
