@@ -1,12 +1,15 @@
 // kernels.cuh -- sm_100a device kernels of libgmg (FP64, no tensor cores:
 // the per-cell implicit "block" is a scalar times identity).
 //
-// Every kernel is HBM/latency bound gather-streaming work; see DESIGN.md
-// "Kernels and rooflines".  Cell arrays are AoS [n][nv] in color-contiguous
-// internal order.  The sweep gathers one 32-byte aligned state record W'
-// (Wp<D> layout: one 256-bit + one 64-bit load in 3D) per neighbour and per-slot 32-byte records
-// (A outward | S r); the own cell reads its (X, c) record (W' formulation,
-// DESIGN.md §6).  The test-only P2P concurrency emulation is p2p_emulate.cuh.
+// Every kernel is HBM/latency bound gather-streaming work (the face kernel
+// leans on the FP64 pipe as well); see DESIGN.md §6.  Cell arrays are AoS
+// [n][nv] in color-contiguous internal order (40-B records read and written
+// as two aligned 128-bit pairs + one scalar, ld_rec / st_rec).  The sweep
+// gathers one state W' per neighbour (Wp<D> layout: one 256-bit + one 64-bit
+// load in 3D) and per-slot 32-byte records (A outward | S r); the own cell
+// reads its (X, c) record (W' formulation).  The residual gather, restriction
+// and prolongation walk the cells in the Morton order across colors (gord /
+// ginfo).  The test-only P2P concurrency emulation is p2p_emulate.cuh.
 #pragma once
 #include <cuda_runtime.h>
 
