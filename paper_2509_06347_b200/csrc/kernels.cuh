@@ -517,14 +517,16 @@ __device__ __forceinline__ void sweep_cells(const SweepArgs &a, const P2PArgs &p
                 double sr[4];
                 ld4na(a.sRe + (size_t)e * kSlotRec, sr);   // read once: not allocated in L1
                 if constexpr (FF) {
-                    double wl[NV], t0[NV];
+                    // both states of an earlier-color neighbour requested before either flux (one round trip)
+                    const bool upd = FF == 1 && (j < a.lo || j >= a.n_own);
+                    double wl[NV], w1[NV], t0[NV];
                     ld_state<D, CG>(a.wlin, nl, j, wl);
+                    if (upd) ld_state<D, CG>(a.wp, nl, j, w1);
                     flux_rw<D>(wl, sr, sr[D], a.gm1, t0);
 #pragma unroll
                     for (int q = 0; q < NV; ++q) accP[q] += t0[q];
-                    if (FF == 1 && (j < a.lo || j >= a.n_own)) {   // earlier color (updated in this half-sweep) or ghost
-                        double w1[NV], t1[NV];
-                        ld_state<D, CG>(a.wp, nl, j, w1);
+                    if (upd) {
+                        double t1[NV];
                         flux_rw<D>(w1, sr, sr[D], a.gm1, t1);
 #pragma unroll
                         for (int q = 0; q < NV; ++q) acc[q] += t1[q] - t0[q];
