@@ -170,6 +170,8 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
     int4 gi = make_int4(0, 0, 0, 0);
     if (t < L.n) gi = __ldg(L.ginfo + t);
     const int i = gi.z;
+    // the first face id (static) before the wait as well; each next one a slot ahead (one round trip per slot)
+    int sfn = (t < L.n && (gi.y & 0xffff) > 0) ? __ldg(L.gface + gi.x) : 0;
     pdl_wait();
     // the cell's one per-cell input of the epilogue (W for G_COPY_W, Rs for G_SET_F, F for G_ADD_F, the
     // explicit state for G_EXPLICIT) is loaded before the slot loop: its latency hides under the gathers,
@@ -185,8 +187,11 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         // (gather base, all slots | interior slots << 16, cell, 0): one 16-byte load
         const int gb = gi.x, nt = gi.y & 0xffff;
         double sig = 0.0, al = 1.0;
+        // coarse prepare: the restricted alpha is needed after the loop -- requested now
+        const double a0 = ((flags & G_PREPARE) && !(flags & (G_BETA | G_ALPHA))) ? L.alpha[i] : 1.0;
         for (int s = 0; s < nt; ++s) {
-            const int sf = __ldg(L.gface + gb + kChunk * s);
+            const int sf = sfn;
+            if (s + 1 < nt) sfn = __ldg(L.gface + gb + kChunk * (s + 1));
             const int f = (sf > 0 ? sf : -sf) - 1;
             const double *fr = L.Frec + (size_t)f * kFaceRec;
             double c1[4];
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
         if (flags & G_ALPHA) L.alpha[i] = al;
         if (flags & G_SIGMA) L.sigma[i] = sig;
         if (flags & G_PREPARE) {
-            const double ai = (flags & G_BETA) ? a.beta : ((flags & G_ALPHA) ? al : L.alpha[i]);
+            const double ai = (flags & G_BETA) ? a.beta : ((flags & G_ALPHA) ? al : a0);
             // D = alpha (V/Dt_imp + Sigma/2) + (1 - alpha) V/Dt_exp (O6, A2, A3); c = alpha / (2 D)
             const double Dg = ai * (sig / a.cfl_imp + 0.5 * sig) + (1.0 - ai) * (sig / a.cfl_exp);
             const double iD = 1.0 / Dg;
