@@ -659,14 +659,18 @@ template <int D>
 __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const double *__restrict__ Wf,
                                                   const double *__restrict__ Rf)
 {
-    pdl_enter();
+    pdl_launch_dependents();
     constexpr int NV = D + 2;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= C.n) return;
+    if (t >= C.n) { pdl_wait(); return; }
+    // static hierarchy data before the PDL wait, the states after it
     const int c = __ldg(C.gord + t);   // coarse cells in the Morton order across colors: the children's
                                        // records are read as one ordered stream per fine color block
-    const int k0 = C.child[c], k1 = C.child[C.n + c];
-    const double V0 = Fn.vol[k0];
+    const int k0 = __ldg(C.child + c), k1 = __ldg(C.child + C.n + c);
+    const double V0 = __ldg(Fn.vol + k0);
+    const double V1 = k1 >= 0 ? __ldg(Fn.vol + k1) : 0.0;
+    const double vc = __ldg(C.vol + c);
+    pdl_wait();
     double w[NV], r[NV], wk[NV], rk[NV];
     double a = Fn.alpha[k0];
     ld_rec<NV, true>(Wf, k0, wk);
@@ -674,14 +678,12 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
 #pragma unroll
     for (int q = 0; q < NV; ++q) { w[q] = V0 * wk[q]; r[q] = rk[q]; }
     if (k1 >= 0) {
-        const double V1 = Fn.vol[k1];
         ld_rec<NV, true>(Wf, k1, wk);
         ld_rec<NV, true>(Rf, k1, rk);
 #pragma unroll
         for (int q = 0; q < NV; ++q) { w[q] = w[q] + V1 * wk[q]; r[q] = r[q] + rk[q]; }
         a = fmin(a, Fn.alpha[k1]);
     }
-    const double vc = C.vol[c];
 #pragma unroll
     for (int q = 0; q < NV; ++q) w[q] = w[q] / vc;
     st_rec<NV>(C.Rs, c, r);
@@ -694,19 +696,21 @@ __global__ void __launch_bounds__(256) k_restrict(DevLevel C, DevLevel Fn, const
 template <int D>
 __global__ void __launch_bounds__(256) k_prolong(DevLevel F0, DevLevel C1, DevLevel C2, int nl)
 {
-    pdl_enter();
+    pdl_launch_dependents();
     constexpr int NV = D + 2;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= F0.n) return;
+    if (t >= F0.n) { pdl_wait(); return; }
+    // static hierarchy data before the PDL wait, the states after it
     const int i = __ldg(F0.gord + t);   // fine cells in the Morton order across colors (see k_restrict)
-    const int p = F0.parent[i];
+    const int p = __ldg(F0.parent + i);
+    const int pp = nl >= 3 ? __ldg(C1.parent + p) : 0;
+    pdl_wait();
     double corr[NV], w0[NV], wc[NV];
     ld_state<D>(C1.wlin, (size_t)C1.n_loc, p, w0);
     ld_rec<NV, true>(C1.W, p, wc);
 #pragma unroll
     for (int q = 0; q < NV; ++q) corr[q] = wc[q] - w0[q];
     if (nl >= 3) {
-        const int pp = C1.parent[p];
         const double a1 = C1.alpha[p];
         ld_state<D>(C2.wlin, (size_t)C2.n_loc, pp, w0);
         ld_rec<NV, true>(C2.W, pp, wc);
