@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(256, 4) k_face(DevLevel L, const double *__res
     double A[D], S2 = 0.0;
 #pragma unroll
     for (int k = 0; k < D; ++k) { A[k] = __ldg(L.fA + (size_t)k * L.nf + f); S2 += A[k] * A[k]; }
+    const int M = DF ? (int)L.fM[f] : 0;                              // Gauss points of the face (DF exponent)
+    const int2 es = PREP ? __ldg(L.fslot + f) : make_int2(-1, -1);   // its sweep slots (prepare)
     pdl_wait();
     const double iS = rsqrt(S2), S = S2 * iS;
     double n[D];
@@ -125,12 +127,10 @@ __global__ void __launch_bounds__(256, 4) k_face(DevLevel L, const double *__res
         const double Dv = dp * sl.ip + dp * sr.ip + dMn * dMn + dMt2;
         const double af = 1.0 / (1.0 + Dv * Dv);
         double aM = 1.0;
-        const int M = L.fM[f];
         for (int g = 0; g < M; ++g) aM *= af;
         out[FR<D>::AM] = aM;
     }
     if (PREP) {
-        const int2 es = __ldg(L.fslot + f);
         const double sr = out[FR<D>::SR];
         if (es.x >= 0) {
             const double v[4] = {A[0], A[1], D == 3 ? A[D - 1] : sr, D == 3 ? sr : 0.0};
