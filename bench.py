@@ -567,7 +567,9 @@ def main():
                                   "half-sweep: only the slots (and the share of the neighbour term) of earlier-"
                                   "color neighbours, whose increments are nonzero (DESIGN.md §8)"},
         "kernels": kernels, "sweep_only": sweep_only,
-        "gpu_launches": int(launches_per_cycle * args.steps + 2),
+        # K graph replays of one V-cycle + the final residual norm (face, gather, norm reduction; with more
+        # than one rank the all-reduced sums take one more launch for the history entry)
+        "gpu_launches": int(launches_per_cycle * args.steps + (3 if ws == 1 else 4)),
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
         "next1_cgks3": next1,
     }

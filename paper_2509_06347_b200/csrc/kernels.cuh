@@ -282,8 +282,10 @@ __global__ void __launch_bounds__(256) k_gather(DevLevel L, GArgs a)
 // threads, each sums a fixed strided subset of the blocks for all nv
 // components at once, then a fixed shuffle + shared-memory tree (the same
 // order on every run)
+// fin (one domain, one rank: nothing to combine): also writes the history
+// entry -- sqrt of the same sums, the bits k_norm_hist would write
 __global__ void __launch_bounds__(1024) k_norm_sum(const double *__restrict__ partial, int nblocks, int nv,
-                                                   double *sumsq)
+                                                   double *sumsq, double *hist, int hist_cap, int *flags, int fin)
 {
     pdl_enter();
     __shared__ double sh[32][5];
@@ -297,11 +299,20 @@ __global__ void __launch_bounds__(1024) k_norm_sum(const double *__restrict__ pa
     }
     __syncthreads();
     if (wid == 0) {
+        const int idx = fin ? flags[0] : 0;
         for (int q = 0; q < nv; ++q) {
             double t = sh[lane][q];
             for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-            if (lane == 0) sumsq[q] = t;
+            if (lane == 0) {
+                sumsq[q] = t;
+                if (fin) {
+                    const double v = sqrt(t);
+                    if (idx < hist_cap) hist[(size_t)idx * nv + q] = v;
+                    if (!isfinite(v)) flags[1] = 1;
+                }
+            }
         }
+        if (fin && lane == 0) flags[0] = idx + 1;
     }
 }
 

@@ -6,6 +6,10 @@
 
 inline int nblk(int64_t n, int b = 256) { return (int)std::max<int64_t>(1, (n + b - 1) / b); }
 
+// one domain on one rank: the residual-norm sums need no combination, so the
+// reduction kernel writes the history entry itself (one launch less)
+inline bool norm_fused(const gmg_ctx *ctx) { return ctx->dom.size() == 1 && ctx->opt.nranks == 1; }
+
 Phys phys(const gmg_ctx *ctx)
 {
     Phys p;
@@ -172,7 +176,8 @@ void enqueue_gather(Launcher &Lc, Domain &dm, int di, int l, int flags, double *
     Lc.post(GMG_K_GATHER, dm.lbytes[l].gather);
     if (flags & G_NORM) {
         Lc.pre(GMG_K_NORM);
-        klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(1024), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + (size_t)di * L.nv);
+        klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(1024), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + (size_t)di * L.nv,
+                ctx->d_hist, ctx->hist_cap, ctx->d_flag, (int)norm_fused(ctx));
         Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
     }
 }
@@ -181,6 +186,7 @@ void enqueue_gather(Launcher &Lc, Domain &dm, int di, int l, int flags, double *
 void enqueue_norm_hist(Launcher &Lc)
 {
     gmg_ctx *ctx = Lc.ctx;
+    if (norm_fused(ctx)) return;   // k_norm_sum already wrote the history entry
     const int nv = ctx->opt.dim + 2;
     if (ctx->opt.nranks > 1)
         nccl().AllReduce(ctx->d_sumsq, ctx->d_sumsq, nv, ncclDouble, ncclSum, (ncclComm_t)ctx->nccl_comm, Lc.s);
@@ -659,7 +665,8 @@ void enqueue_ho_eval(Launcher &Lc, int mode, double *DevLevel::*Rout = nullptr, 
         Lc.post(GMG_K_GATHER, dm.ho.bytes_gather);
         if (mode & HO_NORM) {
             Lc.pre(GMG_K_NORM);
-            klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(1024), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + di * L.nv);
+            klaunch(Lc.ctx, k_norm_sum, dim3(1), dim3(1024), Lc.s, L.partial, nblk(L.n), L.nv, ctx->d_sumsq + di * L.nv,
+                    ctx->d_hist, ctx->hist_cap, ctx->d_flag, (int)norm_fused(ctx));
             Lc.post(GMG_K_NORM, (double)nblk(L.n) * L.nv * 8);
         }
     }
