@@ -22,9 +22,12 @@ def launches(path):
 
 def main(d):
     per = launches(f"{d}/launches.csv")
-    # one V-cycle = the launches between two k_norm_hist (history) launches
+    # one V-cycle = the launches between two history launches (k_norm_hist; on one rank and one domain the
+    # norm reduction k_norm_sum writes the history entry itself)
     keys = sorted(per)
     hist = [i for i, (_, n) in enumerate(keys) if n.startswith("k_norm_hist")]
+    if len(hist) < 3:   # fused history (one rank, one domain): the norm reductions delimit the cycles
+        hist = [i for i, (_, n) in enumerate(keys) if n.startswith("k_norm_sum")]
     a, b = (hist[-3] + 1, hist[-2] + 1) if len(hist) >= 3 else (0, len(keys))
     cyc = keys[a:b]
     cls = defaultdict(lambda: [0.0, 0, 0.0])

@@ -21,6 +21,8 @@ def main(d, tag):
             per[(int(r[ix["ID"]]), r[ix["Kernel Name"]])][r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", "") or 0)
     keys = sorted(per)
     hist = [i for i, (_, n) in enumerate(keys) if n.startswith("k_norm_hist")]
+    if len(hist) < 3:   # fused history (one rank, one domain): the norm reductions delimit the cycles
+        hist = [i for i, (_, n) in enumerate(keys) if n.startswith("k_norm_sum")]
     cyc = keys[hist[-3] + 1:hist[-2] + 1]
     sw = [per[k] for k in cyc if "k_sweep" in k[1]]
     by = [m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"] for m in sw]
