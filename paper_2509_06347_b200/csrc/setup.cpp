@@ -401,7 +401,7 @@ void partition_rcb(int64_t n, int dim, const double *ctr, int nparts, int32_t *p
 //  * gather slots (residual/prepare, thread per cell, cells in the gather
 //    order gord -- Morton across colors): SELL-32 -- chunks of 32 consecutive
 //    cells of that order, entries [slot][lane], chunk padded to its max
-//    degree.  Slots: interior faces (ascending id) then boundary faces.
+//    degree.  Slots: interior faces (by neighbour local index: lower colors first) then boundary faces.
 //  * sweep slots (lanes per cell): CSR -- cell i's interior slots are
 //    contiguous at [soffc[i], soffc[i+1]), same order as its gather slots;
 //    per slot the neighbour sJe and a 32-byte record (A_x, A_y, [A_z,] S r)
@@ -555,7 +555,7 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton)
             if (D.fr[k] >= 0 && D.fr[k] < D.n_own) iidx[pos[D.fr[k]]++] = k;
         }
     }
-    // slots of cell i = its incident faces, interior ones first (stable), in place in iidx
+    // slots of cell i = its incident faces, interior ones first (by neighbour), in place in iidx
     D.deg_int.assign(D.n_own, 0);
     D.deg_all.assign(D.n_own, 0);
     for (int64_t i = 0; i < D.n_own; ++i)
@@ -570,6 +570,13 @@ void build_domain_level(const HostLevel &G, int rank, DomLevel &D, bool morton)
             for (int64_t a = a0; a < a1; ++a)
                 if (D.fr[iidx[a]] >= 0) tmp.push_back(iidx[a]);
             const size_t ni = tmp.size();
+            // interior slots by neighbour (local index: color-major, so lower-color neighbours first --
+            // which keeps the two lanes of a cell on the same side of the first-forward
+            // "earlier color" branch more often, and a cell's neighbour loads in address order)
+            std::stable_sort(tmp.begin(), tmp.end(), [&](int64_t x, int64_t y) {
+                const int32_t jx = D.fl[x] == i ? D.fr[x] : D.fl[x], jy = D.fl[y] == i ? D.fr[y] : D.fl[y];
+                return jx < jy;
+            });
             for (int64_t a = a0; a < a1; ++a)
                 if (D.fr[iidx[a]] < 0) tmp.push_back(iidx[a]);
             std::copy(tmp.begin(), tmp.end(), iidx.begin() + a0);
